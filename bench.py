@@ -1,0 +1,383 @@
+"""Benchmark of the QTNH hot path on B200 (config 1 of BASELINE.json).
+
+Workload (BASELINE.json configs[1]): pairwise dense complex128 contraction of a
+rank-28 tensor A with a rank-14 tensor B, all index dims 2, 7 shared indices at
+seeded random positions of both operands (so both need a permutation), result
+rank 28 in the SPEC.md:408 order. One step = qtnh contract(A, B): the layout
+permutation of A and B (strided-copy kernels) + the complex128 GEMM on the FP64
+tensor cores (M = 2^21, N = 2^7, K = 2^7; 8MNK = 2.749e11 flop).
+
+Multi-GPU (torchrun, one process per GPU): A gets log2(N) extra leading open
+indices that are distributed (M-sharding); every rank holds a
+2^28 shard and the replicated B, so per-GPU work is fixed ("weak") and the step
+has no data-path collective.
+
+JSON line: value = whole-job FP64 TFLOP/s with operands resident in HBM; e2e =
+the same metric through the public API with host buffers (pinned H2D of A and B
+and D2H of the result inside the timed region); roofline for the dominant kernel
+(zgemm) against the FP64 DMMA peak measured live on this device; cpu_baseline =
+the unmodified reference (oracle/_ref: t2m -> SUMMA zgemm -> m2t, OpenBLAS) on a
+bounded rank-22 sample on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+RANK_A, RANK_B, K_SHARED, SEED = 28, 14, 7, 2025
+METRIC = "contraction FP64 TFLOP/s (complex128, rank-28 x rank-14, 7 shared indices)"
+UNIT = "TFLOP/s"
+
+
+def flops_for(rank_a: int) -> float:
+    m = 2 ** (rank_a - K_SHARED)
+    return 8.0 * m * 2 ** (RANK_B - K_SHARED) * 2**K_SHARED
+
+
+# ---- clocks sampling (B200_PROFILING.md) ------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---- reference / CPU arm ---------------------------------------------------------------------
+def cpu_reference_sample(budget_s: float = 15.0, rank_a: int = 22):
+    """The unmodified reference (oracle/_ref) on a bounded sample of the same
+    workload: a rank-22 A (same rank-14 B, 7 shared seeded positions), World(1),
+    OpenBLAS with all host threads. Returns (TFLOP/s, cores, sample description)."""
+    import numpy as np
+
+    import oracle
+    from paper_2505_06119_b200 import circuits
+
+    cores = os.cpu_count() or 1
+    R = oracle.ref() if oracle.ref_available() else None
+    a = circuits.counter_state(SEED, 2**rank_a)
+    b = circuits.counter_state(SEED + 1, 2**RANK_B)
+    ap, bp = circuits.contraction_positions(SEED, rank_a, RANK_B, K_SHARED)
+    if R is None:
+        P = oracle.port()
+        t0 = time.perf_counter()
+        P.contract([2] * rank_a, a, [2] * RANK_B, b, ap, bp)
+        dt = time.perf_counter() - t0
+        return flops_for(rank_a) / dt / 1e12, 1, f"C port brute force, rank-{rank_a} A, 1 call", "port"
+    R.set_threads(cores)
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        _, _, _, t = R.contract(1, [2] * rank_a, 0, (1, 1, 0), a, [2] * RANK_B, 0, (1, 1, 0), b, ap, bp, timing=True)
+        times.append(t[3] / 1e3)
+        if time.perf_counter() - t_start > budget_s or len(times) >= 20:
+            break
+    best = min(times)
+    return (flops_for(rank_a) / best / 1e12, cores,
+            f"reference t2m->pgemm->m2t, rank-{rank_a} A x rank-14 B, {len(times)} calls, best of",
+            "reference")
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps = []
+    value, cores, sample, kind = None, None, None, None
+    for _ in range(args.warmup):
+        cpu_reference_sample(budget_s=2.0)
+    for _ in range(args.steps):
+        value, cores, sample, kind = cpu_reference_sample(budget_s=2.0)
+        steps.append(value)
+    v = statistics.median(steps)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (seeded counter-based normals)",
+            "config": {"workload": "C1 sample: rank-22 A x rank-14 B, 7 shared indices (host cores)"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---- GPU arm -------------------------------------------------------------------------------------
+def run_gpu_arm(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_06119_b200 import circuits, kernel_launches, qtnh
+    from paper_2505_06119_b200.qtnh import DistParams, IndexTuple, Tensor, World, contract
+
+    world_size = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world_size > 1:
+        dist.init_process_group("gloo", init_method="env://")
+    s = (world_size - 1).bit_length() if world_size > 1 else 0
+    if world_size > 1 and 2**s != world_size:
+        raise SystemExit("--gpus must be a power of two")
+    rank_a_global = RANK_A + s
+    flops_rank = flops_for(RANK_A)
+
+    world = World.from_env() if world_size > 1 else World(1, [local])
+    stream = torch.cuda.Stream()
+    lib = qtnh.lib
+    result = {}
+
+    # seeded inputs: this rank's 2^28 shard of A and the full B (counter-based streams)
+    a_host = torch.empty(2**RANK_A, dtype=torch.complex128).pin_memory()
+    a_np = a_host.numpy()
+    lib.qtnh_counter_complex_normals(SEED, rank * 2**RANK_A, 2**RANK_A, a_np.ctypes.data, min(32, os.cpu_count() or 1))
+    b_host = torch.from_numpy(circuits.counter_state(SEED + 1, 2**RANK_B)).pin_memory()
+    c_host = torch.empty(2**RANK_A, dtype=torch.complex128).pin_memory()
+    ap_local, bp = circuits.contraction_positions(SEED, RANK_A, RANK_B, K_SHARED)
+    ap = [p + s for p in ap_local]  # the distributed leading indices are open
+
+    def barrier():
+        if world_size > 1:
+            dist.barrier()
+
+    def body(rk):
+        rk.set_stream(stream.cuda_stream)
+        with torch.cuda.stream(stream):
+            ta = Tensor.dense(rk, IndexTuple([2] * rank_a_global, s), DistParams(1, 1, 0), None)
+            tb = Tensor.dense(rk, IndexTuple([2] * RANK_B, 0), DistParams(world_size, 1, 0), None)
+            qtnh.check(lib.qtnh_tensor_upload_local(ta._h, C.c_void_p(a_host.data_ptr())))
+            qtnh.check(lib.qtnh_tensor_upload_local(tb._h, C.c_void_p(b_host.data_ptr())))
+            rk.synchronize()
+
+            def step():
+                c = contract(ta, tb, ap, bp)
+                return c
+
+            # warm-up
+            for _ in range(args.warmup):
+                step().free()
+            rk.synchronize()
+            torch.cuda.synchronize()
+            # ---- timed: resident operands -----------------------------------------------
+            barrier()
+            torch.cuda.synchronize()
+            k0 = kernel_launches()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with ClockSampler(local) as clk:
+                e0.record(stream)
+                for _ in range(args.steps):
+                    step().free()
+                e1.record(stream)
+                e1.synchronize()
+            torch.cuda.synchronize()
+            barrier()
+            launches = kernel_launches() - k0
+            ms = e0.elapsed_time(e1) / args.steps
+            result.update(ms=ms, launches=launches, clocks=clk.summary())
+
+            # ---- dominant kernel: zgemm alone on the permuted operands ---------------------------
+            M, N, K = 2 ** (RANK_A - K_SHARED), 2 ** (RANK_B - K_SHARED), 2**K_SHARED
+            ga = torch.empty((M, K), dtype=torch.complex128, device="cuda")
+            gb = torch.empty((K, N), dtype=torch.complex128, device="cuda")
+            gc = torch.empty((M, N), dtype=torch.complex128, device="cuda")
+            ga.copy_(torch.from_numpy(a_np[: M * K].reshape(M, K)))
+            gb.copy_(b_host.reshape(K, N))
+            for _ in range(3):
+                qtnh.check(lib.qtnh_zgemm_device(rk._h, M, N, K, C.c_void_p(ga.data_ptr()),
+                                                 C.c_void_p(gb.data_ptr()), C.c_void_p(gc.data_ptr())))
+            z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(5, args.steps)
+            z0.record(stream)
+            for _ in range(reps):
+                qtnh.check(lib.qtnh_zgemm_device(rk._h, M, N, K, C.c_void_p(ga.data_ptr()),
+                                                 C.c_void_p(gb.data_ptr()), C.c_void_p(gc.data_ptr())))
+            z1.record(stream)
+            z1.synchronize()
+            result["zgemm_ms"] = z0.elapsed_time(z1) / reps
+            # numerics spot check of the timed GEMM against a host product of one row block
+            rows = 64
+            want = a_np[: rows * K].reshape(rows, K) @ b_host.numpy().reshape(K, N)
+            got = gc[:rows].cpu().numpy()
+            result["zgemm_spot_rel_err"] = float(np.linalg.norm(got - want) / np.linalg.norm(want))
+            del ga, gb, gc
+            # permute kernel share (A layout permutation)
+            perm_a = [i for i in range(RANK_A) if i not in ap_local] + ap_local
+            out = torch.empty(2**RANK_A, dtype=torch.complex128, device="cuda")
+            src = C.c_void_p(ta.device_ptr())
+            from paper_2505_06119_b200._lib import i32_array, i64_array
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            qtnh.check(lib.qtnh_permute_device(rk._h, RANK_A, i64_array([2] * RANK_A), i32_array(perm_a), src,
+                                               C.c_void_p(out.data_ptr())))
+            p0.record(stream)
+            for _ in range(reps):
+                qtnh.check(lib.qtnh_permute_device(rk._h, RANK_A, i64_array([2] * RANK_A), i32_array(perm_a), src,
+                                                   C.c_void_p(out.data_ptr())))
+            p1.record(stream)
+            p1.synchronize()
+            result["permute_ms"] = p0.elapsed_time(p1) / reps
+            del out
+            peak = C.c_double(0.0)
+            qtnh.check(lib.qtnh_probe_fp64_peak(C.c_void_p(stream.cuda_stream), C.byref(peak)))
+            result["fp64_peak"] = peak.value
+
+            # ---- e2e through the public API with host buffers -----------------------------------------
+            def e2e_step():
+                qtnh.check(lib.qtnh_tensor_upload_local(ta._h, C.c_void_p(a_host.data_ptr())))
+                qtnh.check(lib.qtnh_tensor_upload_local(tb._h, C.c_void_p(b_host.data_ptr())))
+                c = contract(ta, tb, ap, bp)
+                qtnh.check(lib.qtnh_tensor_download_local_async(c._h, C.c_void_p(c_host.data_ptr())))
+                return c
+
+            e2e_step().free()
+            rk.synchronize()
+            barrier()
+            torch.cuda.synchronize()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e2e_steps = max(3, min(args.steps, 5))
+            f0.record(stream)
+            for _ in range(e2e_steps):
+                e2e_step().free()
+            f1.record(stream)
+            f1.synchronize()
+            barrier()
+            result["e2e_ms"] = f0.elapsed_time(f1) / e2e_steps
+            result["h2d"] = (2**RANK_A + 2**RANK_B) * 16
+            result["d2h"] = 2**RANK_A * 16
+            ta.free()
+            tb.free()
+
+    world.run(body)
+
+    # max over ranks
+    def rmax(x):
+        if world_size == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = rmax(result["ms"])
+    e2e_ms = rmax(result["e2e_ms"])
+    zg = rmax(result["zgemm_ms"])
+    total_flops = flops_rank * world_size
+    value = total_flops / (ms * 1e-3) / 1e12
+    achieved = flops_rank / (zg * 1e-3) / 1e12
+    peak = result["fp64_peak"]
+    cpu = None
+    if rank == 0 and world_size == 1 and not args.no_cpu_baseline:
+        try:
+            v, cores, sample, kind = cpu_reference_sample(budget_s=args.cpu_budget)
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+        except Exception as e:  # reported, never fatal for the GPU number
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "zgemm_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128 (f64)",
+            "data": "synthetic (seeded counter-based complex normals, common.hpp hash_counter + Box-Muller)",
+            "config": {"workload": "C1: A rank-%d (dims 2, %d distributed) x B rank-14, 7 shared indices at "
+                                   "seeded random positions; result rank-%d in open(A),open(B) order"
+                                   % (rank_a_global, s, rank_a_global),
+                       "global_batch": 1, "per_gpu_elements_A": 2**RANK_A,
+                       "parallelism": f"M-sharded over {world_size} GPU(s) (A's leading open indices)",
+                       "l2": "inputs (4 GiB A, 4 GiB result per GPU) exceed the 126 MB L2"},
+            "roofline": {"bound": "tensor", "kernel": "k_zgemm<64,128> (DMMA m8n8k4, 4M complex)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "peak_source": "DMMA-only microbenchmark run live on this device (MEASURED_PEAKS.json "
+                                        "has no FP64 entry)",
+                         "traffic": traffic, "zgemm_ms": zg, "permute_ms": result["permute_ms"],
+                         "zgemm_spot_rel_err": result["zgemm_spot_rel_err"]},
+            "cpu_baseline": cpu,
+            "e2e": {"value": total_flops / (e2e_ms * 1e-3) / 1e12, "unit": UNIT,
+                    "h2d_bytes_per_step": result["h2d"], "d2h_bytes_per_step": result["d2h"],
+                    "ms_per_step": e2e_ms},
+            "gpu_launches": result["launches"],
+            "clocks": result["clocks"],
+        }
+        print(json.dumps(line), flush=True)
+    if world_size > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    world.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,197 @@
+/*
+ * qtnh_b200.h -- C ABI of libqtnh_b200.so, the B200-native (sm_100a) hot path of
+ * the QTNH distributed tensor-network library (arXiv 2505.06119).
+ *
+ * The reference (/root/reference/proj/include/qtnh, header-only C++20) exposes the
+ * path as C++ functions, not an FFI; each entry point below replaces one of them
+ * and keeps its argument meaning, result layout and error class:
+ *
+ *   qtnh_world_create_local / qtnh_rank_bind  <- World(n) + World::run  runtime.hpp:245, :263-299
+ *   qtnh_world_create_nccl                    <- Backend::external_message_passing  runtime.hpp:248-251
+ *   qtnh_tensor_dense / _from_global          <- Tensor::dense / from_global  tensor.hpp:61, :83
+ *   qtnh_tensor_download_local / _global      <- Tensor::local_data / to_global_vector  tensor.hpp:177, :341
+ *   qtnh_permute                              <- ops::permute  ops.hpp:27-49
+ *   qtnh_rebcast                              <- ops::rebcast (dense)  ops.hpp:54, :104-109
+ *   qtnh_scatter_index / qtnh_gather_index    <- ops::scatter_index / gather_index  ops.hpp:118, :133
+ *   qtnh_slice_local_dims / _pad_local_dims   <- ops::slice_local_dims / pad_local_dims  ops.hpp:166, :201
+ *   qtnh_conj / qtnh_scale                    <- ops::conj / ops::scale  ops.hpp:147-161
+ *   qtnh_contract                             <- tensor_to_matrix -> pgemm -> matrix_to_tensor
+ *                                                linalg.hpp:208, :347, :273 with the SPEC.md:408 order
+ *   qtnh_gate_apply                           <- contract(state, gate) + permute back (same values,
+ *                                                index order kept, in place)
+ *   qtnh_svd                                  <- psvd + truncate_svd + absorb_singular_*  linalg.hpp:441-523
+ *
+ * Conventions
+ *   - Elements are complex128 stored as interleaved (re, im) doubles, row-major,
+ *     rightmost index fastest (indexing.hpp:106-134).
+ *   - perm[new_pos] = old_pos (ops.hpp:21-23).
+ *   - dist[3] = {stretch, cycles, offset} (indexing.hpp:84-101); NULL means {1,1,0}.
+ *   - Every tensor operation is collective over the union of the involved spans and
+ *     must be called by each member rank with equal arguments; ranks
+ *     outside every span return immediately with a metadata-only handle.
+ *   - Elements whose real and imaginary parts are both zero come out as (+0, +0),
+ *     exactly like the reference's zero-skipping remap (remap.hpp:69-70, :125-127).
+ *   - Every function returns a status: 0 on success, else one QTNH_E_* code.
+ *     qtnh_last_error() returns the thread-local message; qtnh_last_error_info()
+ *     the required rank count (QTNH_E_RESOURCE) or solver info (QTNH_E_NUMERICAL).
+ */
+#ifndef QTNH_B200_H_
+#define QTNH_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error classes, one per qtnh::Error subclass (common.hpp:31-74). */
+enum {
+  QTNH_OK = 0,
+  QTNH_E_INVALID_ARGUMENT = 1, /* InvalidArgument */
+  QTNH_E_RESOURCE = 2,         /* ResourceError(required_ranks) */
+  QTNH_E_PROTOCOL = 3,         /* ProtocolError */
+  QTNH_E_NUMERICAL = 4,        /* NumericalError(info) */
+  QTNH_E_PRECONDITION = 5,     /* PreconditionError */
+  QTNH_E_DEGENERATE = 6,       /* DegenerateStateError */
+  QTNH_E_ABORTED = 7,          /* AbortedError */
+  QTNH_E_RUNTIME = 8           /* Error: CUDA / NCCL / allocation failure */
+};
+
+typedef struct qtnh_world_s* qtnh_world_t;
+typedef struct qtnh_rank_s* qtnh_rank_t;
+typedef struct qtnh_tensor_s* qtnh_tensor_t;
+
+/* ---- errors / build info ------------------------------------------------- */
+int qtnh_last_error(char* buf, size_t len);
+int64_t qtnh_last_error_info(void);
+const char* qtnh_version(void);
+/* Number of this library's kernels launched so far by the calling process. */
+int64_t qtnh_kernel_launch_count(void);
+
+/* ---- worlds and ranks ---------------------------------------------------- */
+/* In-process world of n ranks; rank r runs on device devices[r] (NULL: all on
+ * device 0). Each rank is driven by its own host thread that calls
+ * qtnh_rank_bind(world, r, &rank) -- the B200 analogue of World::run. Exchanges
+ * are stream-ordered device (or NVLink peer) copies coordinated by a host
+ * rendezvous; no kernel ever waits on another rank. */
+int qtnh_world_create_local(int n_ranks, const int* devices, qtnh_world_t* out);
+/* One process per GPU (torchrun): this process is rank `rank` of `size` and owns
+ * `device`. uid is the 128-byte NCCL unique id produced by qtnh_nccl_unique_id on
+ * rank 0 and shared out of band. NCCL is loaded lazily (dlopen). */
+int qtnh_nccl_unique_id(void* uid128);
+int qtnh_world_create_nccl(int rank, int size, int device, const void* uid128, qtnh_world_t* out);
+int qtnh_world_destroy(qtnh_world_t w);
+int qtnh_world_size(qtnh_world_t w);
+/* Abort all pending and future collectives of the world (AbortedError on peers). */
+int qtnh_world_abort(qtnh_world_t w);
+
+int qtnh_rank_bind(qtnh_world_t w, int rank, qtnh_rank_t* out);
+int qtnh_rank_release(qtnh_rank_t r);
+int qtnh_rank_id(qtnh_rank_t r);
+/* Stream the rank launches on (cudaStream_t as void*); set NULL for the rank's own. */
+int qtnh_rank_set_stream(qtnh_rank_t r, void* stream);
+void* qtnh_rank_stream(qtnh_rank_t r);
+int qtnh_rank_synchronize(qtnh_rank_t r);
+int qtnh_barrier(qtnh_rank_t r);
+
+/* ---- tensors ------------------------------------------------------------- */
+/* Dense tensor; `local` holds local_size complex numbers of this rank's block
+ * (host memory, NULL = zeros). Ranks outside the span ignore `local`. */
+int qtnh_tensor_dense(qtnh_rank_t r, int n_idx, const int64_t* dims, int split,
+                      const int64_t* dist, const double* local, qtnh_tensor_t* out);
+/* Dense tensor from a replicated global host vector (tensor.hpp:83-94). */
+int qtnh_tensor_from_global(qtnh_rank_t r, int n_idx, const int64_t* dims, int split,
+                            const int64_t* dist, const double* global, qtnh_tensor_t* out);
+/* Dense tensor adopting this rank's block from device memory (copied, stream-ordered). */
+int qtnh_tensor_from_device(qtnh_rank_t r, int n_idx, const int64_t* dims, int split,
+                            const int64_t* dist, const void* dev_local, qtnh_tensor_t* out);
+int qtnh_tensor_retain(qtnh_tensor_t t);
+int qtnh_tensor_free(qtnh_tensor_t t);
+
+int qtnh_tensor_rank(qtnh_tensor_t t);                 /* number of indices */
+int qtnh_tensor_dims(qtnh_tensor_t t, int64_t* dims);  /* n_idx entries */
+int qtnh_tensor_split(qtnh_tensor_t t);
+int qtnh_tensor_dist(qtnh_tensor_t t, int64_t* dist3);
+int64_t qtnh_tensor_local_size(qtnh_tensor_t t);
+int64_t qtnh_tensor_span(qtnh_tensor_t t);
+int qtnh_tensor_in_span(qtnh_tensor_t t);
+int64_t qtnh_tensor_my_block(qtnh_tensor_t t);
+int qtnh_tensor_is_canonical(qtnh_tensor_t t);
+/* Device pointer of this rank's block (interleaved complex128), NULL outside the span. */
+void* qtnh_tensor_device_ptr(qtnh_tensor_t t);
+/* Copy this rank's block to host (local_size complex). Synchronises the rank stream. */
+int qtnh_tensor_download_local(qtnh_tensor_t t, double* host);
+/* Async variant into caller-provided (pinned) host memory; completes on the rank stream. */
+int qtnh_tensor_download_local_async(qtnh_tensor_t t, double* host);
+int qtnh_tensor_upload_local(qtnh_tensor_t t, const double* host);
+/* Span-collective gather of the full global vector into `host` (total_size complex)
+ * on every span rank (tensor.hpp:341-371). */
+int qtnh_tensor_to_global(qtnh_tensor_t t, double* host);
+
+/* ---- structural ops (ops.hpp) --------------------------------------------- */
+int qtnh_permute(qtnh_tensor_t t, const int* perm, int new_split, qtnh_tensor_t* out);
+int qtnh_rebcast(qtnh_tensor_t t, const int64_t* new_dist, qtnh_tensor_t* out);
+int qtnh_scatter_index(qtnh_tensor_t t, int pos, qtnh_tensor_t* out);
+int qtnh_gather_index(qtnh_tensor_t t, int pos, qtnh_tensor_t* out);
+int qtnh_slice_local_dims(qtnh_tensor_t t, const int64_t* new_local_dims, qtnh_tensor_t* out);
+int qtnh_pad_local_dims(qtnh_tensor_t t, const int64_t* new_local_dims, qtnh_tensor_t* out);
+int qtnh_conj(qtnh_tensor_t t, qtnh_tensor_t* out);
+int qtnh_scale(qtnh_tensor_t t, double re, double im, qtnh_tensor_t* out);
+
+/* ---- contraction ----------------------------------------------------------- */
+/* Contract a[a_pos[i]] with b[b_pos[i]] for i < n_pairs. Result indices: open
+ * indices of a, then open indices of b, each in operand order;
+ * DistParams of a; split = number of a's distributed indices left
+ * open. complex128 GEMM on the FP64 tensor cores (DMMA). */
+int qtnh_contract(qtnh_tensor_t a, qtnh_tensor_t b, int n_pairs, const int* a_pos,
+                  const int* b_pos, qtnh_tensor_t* out);
+
+/* In-place gate application on a state whose indices all have the same role as
+ * in contract(state, gate) followed by a permute that puts the gate outputs back
+ * at `targets`. gate: host row-major D x D complex matrix, D = prod dims[targets],
+ * row index = gate output (targets[0] most significant). `diagonal` != 0 means the
+ * matrix is diagonal and only its D diagonal entries are passed. Copy-on-write:
+ * if the state handle is shared, it is duplicated first. */
+int qtnh_gate_apply(qtnh_tensor_t state, int n_targets, const int* targets,
+                    const double* gate, int diagonal);
+
+/* ---- factorisation --------------------------------------------------------- */
+enum { QTNH_ABSORB_NONE = 0, QTNH_ABSORB_LEFT = 1, QTNH_ABSORB_RIGHT = 2, QTNH_ABSORB_SPLIT = 3 };
+/* Batched thin SVD of `batch` row-major m x n matrices stored back to back in
+ * device memory a (not modified), truncated/zero-padded to chi columns
+ * (linalg.hpp:476-505), singular values absorbed per `absorb` (linalg.hpp:508-523).
+ * Outputs (device, row-major): u [batch][m][chi], s [batch][chi] (doubles,
+ * descending), vh [batch][chi][n]. chi <= 0 means min(m, n). Runs on the rank's
+ * stream. NumericalError if Jacobi sweeps fail to converge. */
+int qtnh_svd_device(qtnh_rank_t r, int64_t batch, int64_t m, int64_t n, const void* a,
+                    int64_t chi, int absorb, void* u, void* s, void* vh);
+
+/* ---- seeded inputs (common.hpp:83-146) ------------------------------------- */
+/* hash_counter(seed, k0, k1, k2) of the reference (common.hpp:93-100). */
+uint64_t qtnh_hash_counter(uint64_t seed, uint64_t k0, uint64_t k1, uint64_t k2);
+/* `count` values of one sequential Rng(seed).next_complex_normal() stream (host,
+ * bit-identical to the reference). */
+void qtnh_rng_complex_normals(uint64_t seed, int64_t count, double* out);
+/* Counter-based complex normals for elements start..start+count-1 (host, glibc
+ * Box-Muller, bit-identical across shards and runs); `threads` host threads. */
+void qtnh_counter_complex_normals(uint64_t seed, int64_t start, int64_t count, double* out, int threads);
+/* Same stream generated on the device (CUDA log/sincos: ~1 ulp from glibc). */
+int qtnh_counter_complex_normals_device(void* stream, uint64_t seed, int64_t start, int64_t count, void* out);
+
+/* ---- raw kernels on device buffers (bench / integration) ------------------ */
+/* out = a(M x K) * b(K x N), row-major complex128 on the rank's stream. */
+int qtnh_zgemm_device(qtnh_rank_t r, int64_t m, int64_t n, int64_t k, const void* a,
+                      const void* b, void* c);
+/* Local strided permutation of a dense block: out (row-major over permuted dims)
+ * <- in (row-major over dims), perm[new] = old; zero canonicalisation applied. */
+int qtnh_permute_device(qtnh_rank_t r, int n_idx, const int64_t* dims, const int* perm,
+                        const void* in, void* out);
+
+/* FP64 tensor-pipe (DMMA) peak measured on the current device, TFLOP/s. */
+int qtnh_probe_fp64_peak(void* stream, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QTNH_B200_H_ */

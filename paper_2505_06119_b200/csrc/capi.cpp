@@ -1,0 +1,508 @@
+// extern "C" boundary of libqtnh_b200.so (declared in include/qtnh_b200.h).
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <string>
+
+#include "nccl_loader.h"
+#include "ops.h"
+#include "strided_copy.h"
+
+using namespace qtnhb;
+
+namespace {
+
+thread_local std::string t_err;
+thread_local int64_t t_info = 0;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return QTNH_OK;
+  } catch (const Status& s) {
+    t_err = s.what();
+    t_info = s.info;
+    return s.code;
+  } catch (const std::bad_alloc&) {
+    t_err = "host allocation failed";
+    t_info = 0;
+    return QTNH_E_RUNTIME;
+  } catch (const std::exception& e) {
+    t_err = e.what();
+    t_info = 0;
+    return QTNH_E_RUNTIME;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw_invalid(std::string("null ") + what);
+}
+
+RankCtx& ctx_of(qtnh_rank_t r) {
+  need(r, "rank");
+  r->ctx->activate();
+  return *r->ctx;
+}
+
+TP& impl_of(qtnh_tensor_t t) {
+  need(t, "tensor");
+  t->impl->rank->activate();
+  return t->impl;
+}
+
+qtnh_tensor_t wrap(TP p) {
+  auto* h = new qtnh_tensor_s;
+  h->impl = std::move(p);
+  return h;
+}
+
+Shape shape_from(int n, const int64_t* dims, int split) {
+  if (n < 0) throw_invalid("negative tensor rank");
+  if (n > 0) need(dims, "dims");
+  return Shape(std::vector<Dim>(dims, dims + n), split);
+}
+
+long env_timeout() {
+  const char* t = std::getenv("QTNH_COLLECTIVE_TIMEOUT_MS");
+  return t ? std::strtol(t, nullptr, 10) : 120000;
+}
+
+}  // namespace
+
+extern "C" {
+
+int qtnh_last_error(char* buf, size_t len) {
+  if (buf && len) {
+    std::strncpy(buf, t_err.c_str(), len - 1);
+    buf[len - 1] = 0;
+  }
+  return static_cast<int>(t_err.size());
+}
+int64_t qtnh_last_error_info(void) { return t_info; }
+const char* qtnh_version(void) { return "qtnh_b200 0.1.0 (sm_100a)"; }
+int64_t qtnh_kernel_launch_count(void) { return g_kernel_launches.load(); }
+
+// ---- worlds -----------------------------------------------------------------
+int qtnh_world_create_local(int n, const int* devices, qtnh_world_t* out) {
+  return guard([&] {
+    need(out, "out");
+    if (n < 1) throw_invalid("world size must be >= 1, got " + std::to_string(n));
+    auto w = std::make_unique<World>();
+    w->kind = World::kLocal;
+    w->size = n;
+    w->timeout_ms = env_timeout();
+    for (int i = 0; i < n; ++i) w->devices.push_back(devices ? devices[i] : 0);
+    // Peer access between distinct devices (NVLink) for the exchange copies.
+    for (int a : w->devices)
+      for (int b : w->devices)
+        if (a != b) {
+          int can = 0;
+          cudaDeviceCanAccessPeer(&can, a, b);
+          if (can) {
+            cudaSetDevice(a);
+            cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+          }
+        }
+    auto* h = new qtnh_world_s;
+    h->w = std::move(w);
+    *out = h;
+  });
+}
+
+int qtnh_nccl_unique_id(void* uid128) {
+  return guard([&] {
+    need(uid128, "uid");
+    ncclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id), "get unique id");
+    std::memcpy(uid128, &id, sizeof(id));
+  });
+}
+
+int qtnh_world_create_nccl(int rank, int size, int device, const void* uid128, qtnh_world_t* out) {
+  return guard([&] {
+    need(out, "out");
+    need(uid128, "uid");
+    if (size < 1 || rank < 0 || rank >= size) throw_invalid("invalid rank/size");
+    auto w = std::make_unique<World>();
+    w->kind = World::kNccl;
+    w->size = size;
+    w->my_rank = rank;
+    w->timeout_ms = env_timeout();
+    QTNH_CUDA(cudaSetDevice(device));
+    ncclUniqueId id;
+    std::memcpy(&id, uid128, sizeof(id));
+    ncclComm_t comm;
+    nccl_check(nccl().CommInitRank(&comm, size, id, rank), "comm init");
+    w->nccl_comm = comm;
+    auto rc = std::make_unique<RankCtx>();
+    rc->world = w.get();
+    rc->rank = rank;
+    rc->device = device;
+    QTNH_CUDA(cudaStreamCreateWithFlags(&rc->own_stream, cudaStreamNonBlocking));
+    rc->stream = rc->own_stream;
+    w->nccl_rank = std::move(rc);
+    auto* h = new qtnh_world_s;
+    h->w = std::move(w);
+    *out = h;
+  });
+}
+
+int qtnh_world_destroy(qtnh_world_t w) {
+  return guard([&] {
+    if (!w) return;
+    if (w->w->kind == World::kNccl && w->w->nccl_comm) {
+      cudaSetDevice(w->w->nccl_rank->device);
+      cudaStreamSynchronize(w->w->nccl_rank->stream);
+      nccl().CommDestroy(static_cast<ncclComm_t>(w->w->nccl_comm));
+      cudaStreamDestroy(w->w->nccl_rank->own_stream);
+    }
+    delete w;
+  });
+}
+
+int qtnh_world_size(qtnh_world_t w) { return w ? w->w->size : 0; }
+
+int qtnh_world_abort(qtnh_world_t w) {
+  return guard([&] {
+    need(w, "world");
+    std::lock_guard<std::mutex> lk(w->w->mu);
+    w->w->aborted = true;
+    w->w->cv.notify_all();
+  });
+}
+
+int qtnh_rank_bind(qtnh_world_t w, int rank, qtnh_rank_t* out) {
+  return guard([&] {
+    need(w, "world");
+    need(out, "out");
+    World& W = *w->w;
+    auto* h = new qtnh_rank_s;
+    h->world = &W;
+    if (W.kind == World::kNccl) {
+      if (rank != W.my_rank) {
+        delete h;
+        throw_invalid("NCCL world: this process is rank " + std::to_string(W.my_rank));
+      }
+      h->ctx = W.nccl_rank.get();
+    } else {
+      if (rank < 0 || rank >= W.size) {
+        delete h;
+        throw_invalid("rank out of range");
+      }
+      h->owned = std::make_unique<RankCtx>();
+      h->ctx = h->owned.get();
+      h->ctx->world = &W;
+      h->ctx->rank = rank;
+      h->ctx->device = W.devices[rank];
+      QTNH_CUDA(cudaSetDevice(h->ctx->device));
+      QTNH_CUDA(cudaStreamCreateWithFlags(&h->ctx->own_stream, cudaStreamNonBlocking));
+      h->ctx->stream = h->ctx->own_stream;
+    }
+    // Keep freed blocks in the stream-ordered pool (no OS round trips per op).
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, h->ctx->device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    *out = h;
+  });
+}
+
+int qtnh_rank_release(qtnh_rank_t r) {
+  return guard([&] {
+    if (!r) return;
+    if (r->owned) {
+      cudaSetDevice(r->ctx->device);
+      cudaStreamSynchronize(r->ctx->own_stream);
+      cudaStreamDestroy(r->ctx->own_stream);
+    }
+    delete r;
+  });
+}
+
+int qtnh_rank_id(qtnh_rank_t r) { return r ? r->ctx->rank : -1; }
+
+int qtnh_rank_set_stream(qtnh_rank_t r, void* stream) {
+  return guard([&] {
+    RankCtx& c = ctx_of(r);
+    c.stream = stream ? static_cast<cudaStream_t>(stream) : c.own_stream;
+  });
+}
+
+void* qtnh_rank_stream(qtnh_rank_t r) { return r ? static_cast<void*>(r->ctx->stream) : nullptr; }
+
+int qtnh_rank_synchronize(qtnh_rank_t r) {
+  return guard([&] { QTNH_CUDA(cudaStreamSynchronize(ctx_of(r).stream)); });
+}
+
+int qtnh_barrier(qtnh_rank_t r) {
+  return guard([&] {
+    RankCtx& c = ctx_of(r);
+    std::vector<int> all(c.world->size);
+    std::iota(all.begin(), all.end(), 0);
+    barrier(c, all);
+  });
+}
+
+// ---- tensors --------------------------------------------------------------------
+int qtnh_tensor_dense(qtnh_rank_t r, int n, const int64_t* dims, int split, const int64_t* dist,
+                      const double* local, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    RankCtx& c = ctx_of(r);
+    TP t = make_tensor(c, shape_from(n, dims, split), dist_from(dist), true);
+    if (t->in_span) {
+      Dim nl = t->shape.local_size();
+      if (local) QTNH_CUDA(cudaMemcpyAsync(t->data(), local, nl * 16, cudaMemcpyHostToDevice, c.stream));
+      else fill_zero(t->data(), nl, c.stream);
+      if (local) QTNH_CUDA(cudaStreamSynchronize(c.stream));  // host buffer may be pageable/temporary
+    }
+    *out = wrap(t);
+  });
+}
+
+int qtnh_tensor_from_global(qtnh_rank_t r, int n, const int64_t* dims, int split, const int64_t* dist,
+                            const double* global, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    need(global, "global");
+    RankCtx& c = ctx_of(r);
+    TP t = make_tensor(c, shape_from(n, dims, split), dist_from(dist), true);
+    if (t->in_span) {
+      Dim nl = t->shape.local_size();
+      QTNH_CUDA(cudaMemcpyAsync(t->data(), global + 2 * t->block * nl, nl * 16, cudaMemcpyHostToDevice,
+                                c.stream));
+      QTNH_CUDA(cudaStreamSynchronize(c.stream));
+    }
+    *out = wrap(t);
+  });
+}
+
+int qtnh_tensor_from_device(qtnh_rank_t r, int n, const int64_t* dims, int split, const int64_t* dist,
+                            const void* dev, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    RankCtx& c = ctx_of(r);
+    TP t = make_tensor(c, shape_from(n, dims, split), dist_from(dist), true);
+    if (t->in_span) {
+      need(dev, "device pointer");
+      QTNH_CUDA(cudaMemcpyAsync(t->data(), dev, t->shape.local_size() * 16, cudaMemcpyDeviceToDevice, c.stream));
+    }
+    *out = wrap(t);
+  });
+}
+
+int qtnh_tensor_retain(qtnh_tensor_t t) {
+  return guard([&] {
+    need(t, "tensor");
+    t->refs.fetch_add(1);
+  });
+}
+
+int qtnh_tensor_free(qtnh_tensor_t t) {
+  return guard([&] {
+    if (!t) return;
+    if (t->refs.fetch_sub(1) == 1) {
+      t->impl->rank->activate();
+      delete t;
+    }
+  });
+}
+
+int qtnh_tensor_rank(qtnh_tensor_t t) { return t ? t->impl->shape.n_idx() : -1; }
+int qtnh_tensor_dims(qtnh_tensor_t t, int64_t* dims) {
+  return guard([&] {
+    need(t, "tensor");
+    need(dims, "dims");
+    for (int i = 0; i < t->impl->shape.n_idx(); ++i) dims[i] = t->impl->shape.dims[i];
+  });
+}
+int qtnh_tensor_split(qtnh_tensor_t t) { return t ? t->impl->shape.split : -1; }
+int qtnh_tensor_dist(qtnh_tensor_t t, int64_t* d) {
+  return guard([&] {
+    need(t, "tensor");
+    need(d, "dist");
+    d[0] = t->impl->dist.stretch;
+    d[1] = t->impl->dist.cycles;
+    d[2] = t->impl->dist.offset;
+  });
+}
+int64_t qtnh_tensor_local_size(qtnh_tensor_t t) { return t ? t->impl->shape.local_size() : -1; }
+int64_t qtnh_tensor_span(qtnh_tensor_t t) { return t ? t->impl->span() : -1; }
+int qtnh_tensor_in_span(qtnh_tensor_t t) { return t ? t->impl->in_span : 0; }
+int64_t qtnh_tensor_my_block(qtnh_tensor_t t) { return t ? t->impl->block : -1; }
+int qtnh_tensor_is_canonical(qtnh_tensor_t t) { return t ? t->impl->canonical() : 0; }
+void* qtnh_tensor_device_ptr(qtnh_tensor_t t) { return t ? t->impl->data() : nullptr; }
+
+int qtnh_tensor_download_local(qtnh_tensor_t t, double* host) {
+  return guard([&] {
+    TP& p = impl_of(t);
+    if (!p->in_span) return;
+    need(host, "host");
+    QTNH_CUDA(cudaMemcpyAsync(host, p->data(), p->shape.local_size() * 16, cudaMemcpyDeviceToHost,
+                              p->rank->stream));
+    QTNH_CUDA(cudaStreamSynchronize(p->rank->stream));
+  });
+}
+
+int qtnh_tensor_download_local_async(qtnh_tensor_t t, double* host) {
+  return guard([&] {
+    TP& p = impl_of(t);
+    if (!p->in_span) return;
+    need(host, "host");
+    QTNH_CUDA(cudaMemcpyAsync(host, p->data(), p->shape.local_size() * 16, cudaMemcpyDeviceToHost,
+                              p->rank->stream));
+  });
+}
+
+int qtnh_tensor_upload_local(qtnh_tensor_t t, const double* host) {
+  return guard([&] {
+    TP& p = impl_of(t);
+    if (!p->in_span) return;
+    need(host, "host");
+    QTNH_CUDA(cudaMemcpyAsync(p->data(), host, p->shape.local_size() * 16, cudaMemcpyHostToDevice,
+                              p->rank->stream));
+  });
+}
+
+int qtnh_tensor_to_global(qtnh_tensor_t t, double* host) {
+  return guard([&] {
+    TP& p = impl_of(t);
+    if (p->in_span) need(host, "host");
+    op_to_global(*p, host);
+  });
+}
+
+// ---- ops --------------------------------------------------------------------------
+int qtnh_permute(qtnh_tensor_t t, const int* perm, int new_split, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    TP& p = impl_of(t);
+    int n = p->shape.n_idx();
+    if (n) need(perm, "perm");
+    *out = wrap(op_permute(p, std::vector<int>(perm, perm + n), new_split));
+  });
+}
+
+int qtnh_rebcast(qtnh_tensor_t t, const int64_t* nd, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(op_rebcast(impl_of(t), dist_from(nd)));
+  });
+}
+
+int qtnh_scatter_index(qtnh_tensor_t t, int pos, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(op_scatter_index(impl_of(t), pos));
+  });
+}
+
+int qtnh_gather_index(qtnh_tensor_t t, int pos, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(op_gather_index(impl_of(t), pos));
+  });
+}
+
+int qtnh_slice_local_dims(qtnh_tensor_t t, const int64_t* nl, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    TP& p = impl_of(t);
+    int k = p->shape.n_local();
+    if (k) need(nl, "new_local_dims");
+    *out = wrap(op_slice_local(p, std::vector<Dim>(nl, nl + k)));
+  });
+}
+
+int qtnh_pad_local_dims(qtnh_tensor_t t, const int64_t* nl, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    TP& p = impl_of(t);
+    int k = p->shape.n_local();
+    if (k) need(nl, "new_local_dims");
+    *out = wrap(op_pad_local(p, std::vector<Dim>(nl, nl + k)));
+  });
+}
+
+int qtnh_conj(qtnh_tensor_t t, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(op_scale(impl_of(t), 1.0, 0.0, true));
+  });
+}
+
+int qtnh_scale(qtnh_tensor_t t, double re, double im, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(op_scale(impl_of(t), re, im, false));
+  });
+}
+
+int qtnh_contract(qtnh_tensor_t a, qtnh_tensor_t b, int n_pairs, const int* a_pos, const int* b_pos,
+                  qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    if (n_pairs < 0) throw_invalid("negative pair count");
+    if (n_pairs) {
+      need(a_pos, "a_pos");
+      need(b_pos, "b_pos");
+    }
+    TP& pa = impl_of(a);
+    TP& pb = impl_of(b);
+    *out = wrap(op_contract(pa, pb, std::vector<int>(a_pos, a_pos + n_pairs),
+                            std::vector<int>(b_pos, b_pos + n_pairs)));
+  });
+}
+
+int qtnh_gate_apply(qtnh_tensor_t state, int n_targets, const int* targets, const double* gate, int diagonal) {
+  return guard([&] {
+    TP& p = impl_of(state);
+    if (n_targets < 1) throw_invalid("gate needs at least one target");
+    need(targets, "targets");
+    need(gate, "gate");
+    // Copy-on-write: other handles (or views) must not observe the update.
+    if (p->in_span && (p.use_count() > 1 || (p->buf && p->buf.use_count() > 1))) {
+      TP c = make_tensor(*p->rank, p->shape, p->dist, true);
+      QTNH_CUDA(cudaMemcpyAsync(c->data(), p->data(), p->shape.local_size() * 16, cudaMemcpyDeviceToDevice,
+                                p->rank->stream));
+      p = c;
+    } else if (!p->in_span && p.use_count() > 1) {
+      p = make_tensor(*p->rank, p->shape, p->dist, false);
+    }
+    op_gate_apply(p, std::vector<int>(targets, targets + n_targets), gate, diagonal != 0);
+  });
+}
+
+int qtnh_svd_device(qtnh_rank_t r, int64_t batch, int64_t m, int64_t n, const void* a, int64_t chi, int absorb,
+                    void* u, void* s, void* vh) {
+  return guard([&] {
+    (void)r; (void)batch; (void)m; (void)n; (void)a; (void)chi; (void)absorb; (void)u; (void)s; (void)vh;
+    throw Status(QTNH_E_RUNTIME, "qtnh_svd_device: batched Jacobi SVD not built in this version");
+  });
+}
+
+int qtnh_zgemm_device(qtnh_rank_t r, int64_t m, int64_t n, int64_t k, const void* a, const void* b, void* c) {
+  return guard([&] {
+    RankCtx& x = ctx_of(r);
+    zgemm(a, b, c, m, n, k, x.stream);
+  });
+}
+
+int qtnh_permute_device(qtnh_rank_t r, int n, const int64_t* dims, const int* perm, const void* in, void* out) {
+  return guard([&] {
+    RankCtx& x = ctx_of(r);
+    std::vector<Dim> d(dims, dims + n);
+    std::vector<int> p(perm, perm + n);
+    std::vector<char> seen(n, 0);
+    for (int v : p) {
+      if (v < 0 || v >= n || seen[v]) throw_invalid("invalid index permutation");
+      seen[v] = 1;
+    }
+    strided_copy(in, out, permute_box(d, p), true, x.stream);
+  });
+}
+
+}  // extern "C"

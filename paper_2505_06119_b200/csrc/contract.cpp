@@ -1,0 +1,252 @@
+// Pairwise contraction and gate application on sharded device tensors.
+//
+// Reference: SPEC network::contract realised with
+// tensor_to_matrix -> pgemm -> matrix_to_tensor (linalg.hpp:208, :347, :273):
+// every operand is redistributed into a 2-D block-cyclic matrix with one
+// 24-byte Item per element and multiplied by SUMMA panel broadcasts.
+//
+// B200 design: no block-cyclic matrices. The contraction is made rank-local:
+//   * the first operand keeps its sharding (its distributed indices select the
+//     GPU; a contracted distributed index is first swapped with an open local
+//     index of the same size -- one NVLink exchange);
+//   * the second operand is replicated on the first operand's span (rebcast --
+//     it is the small operand in every configuration: the 2^14 B of C1, gates);
+//   * each GPU permutes its block into [open | contracted] and B into
+//     [contracted | open] (skipped when already in that order) and runs one
+//     FP64-tensor-core zgemm whose row-major output IS its block of the result in
+//     the SPEC.md:408 order (open(a) then open(b)).
+#include <algorithm>
+#include <numeric>
+
+#include "ops.h"
+#include "strided_copy.h"
+
+namespace qtnhb {
+
+namespace {
+
+bool is_identity(const std::vector<int>& p) {
+  for (size_t i = 0; i < p.size(); ++i)
+    if (p[i] != static_cast<int>(i)) return false;
+  return true;
+}
+
+// Local block of `t` permuted by perm (over local dims) into a fresh buffer, or
+// the block itself when perm is the identity.
+const void* local_permuted(const TensorImpl& t, const std::vector<Dim>& dims, const std::vector<int>& perm,
+                           std::shared_ptr<DevBuf>& hold, RankCtx& r) {
+  if (is_identity(perm)) return t.data();
+  Dim n = 1;
+  for (Dim d : dims) n *= d;
+  hold = std::make_shared<DevBuf>(static_cast<size_t>(n) * 16, r);
+  strided_copy(t.data(), hold->ptr, permute_box(dims, perm), false, r.stream);
+  return hold->ptr;
+}
+
+}  // namespace
+
+TP op_contract(const TP& a_in, const TP& b_in, const std::vector<int>& apos, const std::vector<int>& bpos) {
+  if (apos.size() != bpos.size()) throw_invalid("contracted position lists differ in length");
+  if (a_in->rank != b_in->rank) throw_invalid("operands belong to different ranks");
+  RankCtx& r = *a_in->rank;
+  const Shape& sa = a_in->shape;
+  const Shape& sb = b_in->shape;
+  std::vector<char> ca(sa.n_idx(), 0), cb(sb.n_idx(), 0);
+  for (size_t i = 0; i < apos.size(); ++i) {
+    int p = apos[i], q = bpos[i];
+    if (p < 0 || p >= sa.n_idx() || ca[p] || q < 0 || q >= sb.n_idx() || cb[q])
+      throw_invalid("invalid contracted index positions");
+    if (sa.dims[p] != sb.dims[q]) throw_invalid("contracted dimensions differ");
+    ca[p] = cb[q] = 1;
+  }
+  std::vector<int> a_open, b_open;
+  for (int i = 0; i < sa.n_idx(); ++i)
+    if (!ca[i]) a_open.push_back(i);
+  for (int i = 0; i < sb.n_idx(); ++i)
+    if (!cb[i]) b_open.push_back(i);
+  std::vector<Dim> cdims;
+  int csplit = 0;
+  for (int p : a_open) {
+    cdims.push_back(sa.dims[p]);
+    if (p < sa.split) ++csplit;
+  }
+  for (int p : b_open) cdims.push_back(sb.dims[p]);
+
+  // 1. Make every contracted index of `a` local: swap it with an open local index
+  //    of equal size (keeps the span), else move it behind the split.
+  TP a = a_in;
+  std::vector<int> a_order(sa.n_idx());  // a2 position -> a position
+  std::iota(a_order.begin(), a_order.end(), 0);
+  int a2_split = sa.split;
+  {
+    std::vector<int> dist_contracted;
+    for (int p = 0; p < sa.split; ++p)
+      if (ca[p]) dist_contracted.push_back(p);
+    if (!dist_contracted.empty()) {
+      std::vector<char> used(sa.n_idx(), 0);
+      std::vector<int> order = a_order;
+      std::vector<int> demote;
+      for (int p : dist_contracted) {
+        int swap_with = -1;
+        for (int q = sa.n_idx() - 1; q >= sa.split; --q)
+          if (!ca[q] && !used[q] && sa.dims[q] == sa.dims[p]) {
+            swap_with = q;
+            break;
+          }
+        if (swap_with >= 0) {
+          used[swap_with] = 1;
+          std::swap(order[p], order[swap_with]);
+        } else {
+          demote.push_back(p);
+        }
+      }
+      // Demoted contracted dist indices move to the front of the local group.
+      std::vector<int> final_order;
+      for (int p = 0; p < sa.split; ++p)
+        if (std::find(demote.begin(), demote.end(), p) == demote.end()) final_order.push_back(order[p]);
+      for (int p : demote) final_order.push_back(order[p]);
+      for (int p = sa.split; p < sa.n_idx(); ++p) final_order.push_back(order[p]);
+      a2_split = sa.split - static_cast<int>(demote.size());
+      a_order = final_order;
+      a = op_permute(a_in, a_order, a2_split);
+    }
+  }
+  const Shape& s2 = a->shape;
+  // positions in a2 of a's indices
+  std::vector<int> pos_in_a2(sa.n_idx());
+  for (int i = 0; i < sa.n_idx(); ++i) pos_in_a2[a_order[i]] = i;
+
+  // 2. Replicate b over a2's span (skipped when it already is).
+  TP b = b_in;
+  Dist want{a->span(), 1, a->dist.offset};
+  bool b_ok = b->shape.split == 0 && b->dist.offset <= a->dist.offset &&
+              b->dist.offset + b->span() >= a->dist.offset + a->span();
+  if (!b_ok) {
+    if (b->shape.split != 0) {
+      std::vector<int> ident(sb.n_idx());
+      std::iota(ident.begin(), ident.end(), 0);
+      b = op_permute(b, ident, 0);
+    }
+    b = op_rebcast(b, want);
+  }
+
+  // 3. Result of the local GEMMs: dims = open(a2 order) + open(b); dist of a.
+  std::vector<int> a2_open;  // a2 positions that are open, in a2 order
+  std::vector<int> a2_contr;  // a2 positions of the contracted indices, pair order
+  for (int i = 0; i < s2.n_idx(); ++i)
+    if (!ca[a_order[i]]) a2_open.push_back(i);
+  for (int p : apos) a2_contr.push_back(pos_in_a2[p]);
+  std::vector<Dim> c2dims;
+  for (int i : a2_open) c2dims.push_back(s2.dims[i]);
+  for (int p : b_open) c2dims.push_back(sb.dims[p]);
+  int c2split = s2.split;  // all of a2's distributed indices are open
+  TP c2 = make_tensor(r, Shape(c2dims, c2split), a->dist, true);
+  if (c2->in_span) {
+    // local permutation of a2's block: [open local][contracted]
+    std::vector<Dim> ald = s2.local_dims();
+    std::vector<int> ap;
+    for (int i : a2_open)
+      if (i >= s2.split) ap.push_back(i - s2.split);
+    Dim M = 1, K = 1, N = 1;
+    for (int i : ap) M *= ald[i];
+    for (int i : a2_contr) {
+      ap.push_back(i - s2.split);
+      K *= s2.dims[i];
+    }
+    std::vector<int> bp;
+    for (int q : bpos) bp.push_back(q);
+    for (int q : b_open) {
+      bp.push_back(q);
+      N *= sb.dims[q];
+    }
+    std::shared_ptr<DevBuf> ha, hb;
+    const void* A = local_permuted(*a, ald, ap, ha, r);
+    const void* B = local_permuted(*b, sb.dims, bp, hb, r);
+    zgemm(A, B, c2->data(), M, N, K, r.stream);
+  }
+  // 4. Restore the SPEC order / split when a was reshuffled.
+  if (a == a_in) return c2;
+  std::vector<int> perm;  // result position -> c2 position
+  for (int p : a_open) perm.push_back(static_cast<int>(std::find(a2_open.begin(), a2_open.end(), pos_in_a2[p]) - a2_open.begin()));
+  for (size_t j = 0; j < b_open.size(); ++j) perm.push_back(static_cast<int>(a2_open.size() + j));
+  return op_permute(c2, perm, csplit);
+}
+
+void op_gate_apply(TP& t, const std::vector<int>& targets, const double* gate, bool diagonal) {
+  const Shape& s = t->shape;
+  int k = static_cast<int>(targets.size());
+  std::vector<char> is_t(s.n_idx(), 0);
+  for (int q : targets) {
+    if (q < 0 || q >= s.n_idx() || is_t[q]) throw_invalid("invalid gate targets");
+    is_t[q] = 1;
+  }
+  std::vector<int> dist_t, local_t;
+  for (int q : targets) (q < s.split ? dist_t : local_t).push_back(q);
+  RankCtx& r = *t->rank;
+  if (dist_t.empty()) {
+    if (!t->in_span) return;
+    std::vector<int> lt;
+    for (int q : targets) lt.push_back(q - s.split);
+    gate_local(t->data(), s.local_dims(), lt, gate, diagonal, r.stream);
+    return;
+  }
+  std::vector<Dim> tdims;
+  for (int q : targets) tdims.push_back(s.dims[q]);
+  if (diagonal) {
+    // Distributed target coordinates are fixed by this rank's block: apply the
+    // slice of the diagonal that matches them, no communication.
+    if (!t->in_span) return;
+    auto cd = unflat(t->block, s.dist_dims());
+    std::vector<Dim> ldims;
+    for (int q : local_t) ldims.push_back(s.dims[q]);
+    Dim nl = 1;
+    for (Dim d : ldims) nl *= d;
+    std::vector<double> sub(2 * nl);
+    for (Dim j = 0; j < nl; ++j) {
+      auto cl = unflat(j, ldims);
+      std::vector<Dim> c(k);
+      for (int i = 0, li = 0; i < k; ++i) c[i] = targets[i] < s.split ? cd[targets[i]] : cl[li++];
+      Dim idx = flat(c, tdims);
+      sub[2 * j] = gate[2 * idx];
+      sub[2 * j + 1] = gate[2 * idx + 1];
+    }
+    if (local_t.empty()) {
+      if (!(sub[0] == 1.0 && sub[1] == 0.0))
+        scale_conj(t->data(), t->data(), s.local_size(), sub[0], sub[1], false, r.stream);
+      return;
+    }
+    std::vector<int> lt;
+    for (int q : local_t) lt.push_back(q - s.split);
+    gate_local(t->data(), s.local_dims(), lt, sub.data(), true, r.stream);
+    return;
+  }
+  // Dense gate on distributed targets: swap each with a local non-target index of
+  // the same size (dist<->local swap over NVLink), apply, swap back.
+  std::vector<int> perm(s.n_idx());
+  std::iota(perm.begin(), perm.end(), 0);
+  std::vector<char> used(s.n_idx(), 0);
+  std::vector<int> new_targets = targets;
+  for (int i = 0; i < k; ++i) {
+    int q = targets[i];
+    if (q >= s.split) continue;
+    int w = -1;
+    for (int p = s.n_idx() - 1; p >= s.split; --p)
+      if (!is_t[p] && !used[p] && s.dims[p] == s.dims[q]) {
+        w = p;
+        break;
+      }
+    if (w < 0) throw_invalid("no local index to swap a distributed gate target with");
+    used[w] = 1;
+    std::swap(perm[q], perm[w]);
+    new_targets[i] = w;
+  }
+  TP t2 = op_permute(t, perm, s.split);
+  if (t2->in_span) {
+    std::vector<int> lt;
+    for (int q : new_targets) lt.push_back(q - s.split);
+    gate_local(t2->data(), s.local_dims(), lt, gate, false, r.stream);
+  }
+  t = op_permute(t2, perm, s.split);
+}
+
+}  // namespace qtnhb

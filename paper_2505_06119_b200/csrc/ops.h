@@ -1,0 +1,37 @@
+// Structural operations, contraction and gate application on device tensors.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "runtime.h"
+
+namespace qtnhb {
+
+using TP = std::shared_ptr<TensorImpl>;
+
+// remap::tensor_to_tensor (remap.hpp:106-161) restricted to equal dimensions:
+// axis_map[src_pos] = dst_pos.
+TP remap(const TP& src, Shape dst_shape, Dist dst_dist, const std::vector<int>& axis_map);
+
+TP op_permute(const TP& t, const std::vector<int>& perm, int new_split);  // ops.hpp:27
+TP op_rebcast(const TP& t, Dist d);                                        // ops.hpp:54
+TP op_scatter_index(const TP& t, int pos);                                 // ops.hpp:118
+TP op_gather_index(const TP& t, int pos);                                  // ops.hpp:133
+TP op_slice_local(const TP& t, const std::vector<Dim>& nl);                // ops.hpp:166
+TP op_pad_local(const TP& t, const std::vector<Dim>& nl);                  // ops.hpp:201
+TP op_scale(const TP& t, double re, double im, bool conj);                 // ops.hpp:147-161
+void op_to_global(const TensorImpl& t, double* host);                      // tensor.hpp:341
+
+// Contraction with SPEC.md:408 result order (see qtnh_b200.h).
+TP op_contract(const TP& a, const TP& b, const std::vector<int>& apos, const std::vector<int>& bpos);
+// In-place gate on t (caller guarantees exclusive ownership).
+void op_gate_apply(TP& t, const std::vector<int>& targets, const double* gate, bool diagonal);
+
+// Kernels (zgemm.cu, gate.cu)
+void zgemm(const void* a, const void* b, void* c, Dim m, Dim n, Dim k, cudaStream_t st);
+// Gate on a dense local block: dims = local dims, targets = local positions.
+void gate_local(void* data, const std::vector<Dim>& dims, const std::vector<int>& targets,
+                const double* gate_host, bool diagonal, cudaStream_t st);
+
+}  // namespace qtnhb

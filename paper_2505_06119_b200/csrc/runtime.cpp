@@ -1,0 +1,235 @@
+// Rank runtime: exchange over the in-process (local) backend or NCCL.
+#include "runtime.h"
+
+#include <algorithm>
+#include <chrono>
+
+#include "nccl_loader.h"
+
+namespace qtnhb {
+
+std::atomic<int64_t> g_kernel_launches{0};
+
+void RankCtx::activate() const { QTNH_CUDA(cudaSetDevice(device)); }
+
+DevBuf::DevBuf(size_t b, const RankCtx& r) : bytes(b), device(r.device), stream(r.stream) {
+  if (b == 0) b = 16;
+  QTNH_CUDA(cudaMallocAsync(&ptr, b, stream));
+}
+
+DevBuf::~DevBuf() {
+  if (ptr) {
+    cudaSetDevice(device);
+    cudaFreeAsync(ptr, stream);
+  }
+}
+
+std::shared_ptr<TensorImpl> make_tensor(RankCtx& r, Shape shape, Dist dist, bool alloc) {
+  shape.validate();
+  dist.validate();
+  auto t = std::make_shared<TensorImpl>();
+  t->rank = &r;
+  t->shape = std::move(shape);
+  t->dist = dist;
+  Dim need = dist.offset + dist.span(t->shape.dist_size());
+  if (need > r.world->size) throw_resource("tensor span exceeds world size", need);
+  t->in_span = dist.locate(r.rank, t->shape.dist_size(), &t->block, &t->cycle, &t->slot);
+  if (t->in_span && alloc)
+    t->buf = std::make_shared<DevBuf>(static_cast<size_t>(t->shape.local_size()) * 16, r);
+  return t;
+}
+
+std::vector<int> span_ranks(const TensorImpl& t) {
+  std::vector<int> out;
+  for (Dim i = 0; i < t.span(); ++i) out.push_back(static_cast<int>(t.dist.offset + i));
+  return out;
+}
+
+std::vector<int> union_members(const std::vector<std::pair<Dim, Dim>>& spans) {
+  std::vector<int> out;
+  for (auto [off, span] : spans)
+    for (Dim r = off; r < off + span; ++r) out.push_back(static_cast<int>(r));
+  std::sort(out.begin(), out.end());
+  out.erase(std::unique(out.begin(), out.end()), out.end());
+  return out;
+}
+
+namespace {
+
+// ---- local backend -----------------------------------------------------------
+// Two-phase rendezvous per collective: (1) every member posts its send buffer,
+// send list and a "packed" event; receivers then pull their chunks with
+// stream-ordered device/peer copies on their own stream; (2) every member posts a
+// "pulled" event and senders make their stream wait on the receivers' events, so
+// a send buffer is never released before the copies that read it complete.
+void local_exchange(RankCtx& r, const std::vector<int>& members, const void* send_buf,
+                    const std::vector<Xfer>& sends, void* recv_buf, const std::vector<Xfer>& recvs) {
+  World& w = *r.world;
+  uint64_t seq = r.seq[members]++;
+  auto key = std::make_pair(members, seq);
+  int n = static_cast<int>(members.size());
+  int me = static_cast<int>(std::find(members.begin(), members.end(), r.rank) - members.begin());
+  if (me >= n) throw_invalid("rank is not a member of its own collective");
+  cudaEvent_t packed, pulled;
+  QTNH_CUDA(cudaEventCreateWithFlags(&packed, cudaEventDisableTiming));
+  QTNH_CUDA(cudaEventCreateWithFlags(&pulled, cudaEventDisableTiming));
+  QTNH_CUDA(cudaEventRecord(packed, r.stream));
+
+  auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(w.timeout_ms);
+  auto wait_for = [&](std::unique_lock<std::mutex>& lk, auto pred) {
+    while (!pred()) {
+      if (w.aborted) throw Status(QTNH_E_ABORTED, "world aborted");
+      if (w.timeout_ms > 0) {
+        if (w.cv.wait_until(lk, deadline) == std::cv_status::timeout && !pred() && !w.aborted)
+          throw Status(QTNH_E_PROTOCOL, "collective timed out (possible deadlock)");
+      } else {
+        w.cv.wait(lk);
+      }
+    }
+  };
+
+  std::unique_lock<std::mutex> lk(w.mu);
+  World::Slot& slot = w.slots[key];
+  if (slot.posts.empty()) slot.posts.resize(n);
+  World::Post& mine = slot.posts[me];
+  mine.posted = true;
+  mine.send_buf = send_buf;
+  mine.sends = sends;
+  mine.packed = packed;
+  if (++slot.arrived == n) w.cv.notify_all();
+  wait_for(lk, [&] { return slot.arrived == n || !slot.error.empty(); });
+  if (!slot.error.empty()) throw Status(QTNH_E_PROTOCOL, slot.error);
+
+  // Match my receives against the senders' lists, in order per peer.
+  struct Pull {
+    const Xfer* rv;
+    const Xfer* sx;
+    const World::Post* sp;
+  };
+  std::vector<Pull> pulls;
+  std::map<int, int> used;
+  for (const Xfer& rv : recvs) {
+    int si = static_cast<int>(std::find(members.begin(), members.end(), rv.peer) - members.begin());
+    if (si >= n) throw_invalid("exchange peer outside the member set");
+    const World::Post& sp = slot.posts[si];
+    int& u = used[rv.peer];
+    const Xfer* sx = nullptr;
+    for (int j = 0, seen = 0; j < static_cast<int>(sp.sends.size()); ++j)
+      if (sp.sends[j].peer == r.rank && seen++ == u) {
+        sx = &sp.sends[j];
+        break;
+      }
+    ++u;
+    if (!sx || sx->count != rv.count) {
+      Dim got = 0;
+      for (const Xfer& x : sp.sends)
+        if (x.peer == r.rank) got += x.count;
+      slot.error = "exchange count mismatch for pair (" + std::to_string(rv.peer) + " -> " +
+                   std::to_string(r.rank) + "): got " + std::to_string(got) + ", expected " +
+                   std::to_string(rv.count);
+      w.cv.notify_all();
+      throw Status(QTNH_E_PROTOCOL, slot.error);
+    }
+    pulls.push_back({&rv, sx, &sp});
+  }
+  lk.unlock();
+  for (const Pull& p : pulls) {
+    if (p.rv->count == 0) continue;
+    if (p.rv->peer != r.rank) QTNH_CUDA(cudaStreamWaitEvent(r.stream, p.sp->packed, 0));
+    QTNH_CUDA(cudaMemcpyAsync(static_cast<char*>(recv_buf) + p.rv->offset * 16,
+                              static_cast<const char*>(p.sp->send_buf) + p.sx->offset * 16,
+                              static_cast<size_t>(p.rv->count) * 16, cudaMemcpyDefault, r.stream));
+  }
+  QTNH_CUDA(cudaEventRecord(pulled, r.stream));
+
+  lk.lock();
+  mine.pulled = pulled;
+  mine.done_posted = true;
+  if (++slot.done == n) w.cv.notify_all();
+  wait_for(lk, [&] { return slot.done == n || !slot.error.empty(); });
+  if (!slot.error.empty()) throw Status(QTNH_E_PROTOCOL, slot.error);
+  // My send buffer may be read by any receiver: order my stream after their pulls.
+  for (int j = 0; j < n; ++j) {
+    if (j == me) continue;
+    bool reads_me = false;
+    for (const Xfer& sx : sends)
+      if (sx.peer == members[j] && sx.count > 0) reads_me = true;
+    if (reads_me) QTNH_CUDA(cudaStreamWaitEvent(r.stream, slot.posts[j].pulled, 0));
+  }
+  if (++slot.left == n) {
+    for (auto& p : slot.posts) {
+      cudaEventDestroy(p.packed);
+      cudaEventDestroy(p.pulled);
+    }
+    w.slots.erase(key);
+  }
+}
+
+// ---- NCCL backend --------------------------------------------------------------
+void nccl_exchange(RankCtx& r, const void* send_buf, const std::vector<Xfer>& sends,
+                   void* recv_buf, const std::vector<Xfer>& recvs) {
+  const Nccl& N = nccl();
+  auto comm = static_cast<ncclComm_t>(r.world->nccl_comm);
+  // Self chunks: direct device copies, matched in order.
+  std::vector<const Xfer*> self_s, self_r;
+  for (const Xfer& s : sends)
+    if (s.peer == r.rank) self_s.push_back(&s);
+  for (const Xfer& v : recvs)
+    if (v.peer == r.rank) self_r.push_back(&v);
+  if (self_s.size() != self_r.size())
+    throw Status(QTNH_E_PROTOCOL, "exchange count mismatch for pair (" + std::to_string(r.rank) +
+                                      " -> " + std::to_string(r.rank) + ")");
+  for (size_t i = 0; i < self_s.size(); ++i) {
+    if (self_s[i]->count != self_r[i]->count)
+      throw Status(QTNH_E_PROTOCOL, "exchange count mismatch for pair (" + std::to_string(r.rank) +
+                                        " -> " + std::to_string(r.rank) + ")");
+    if (self_s[i]->count)
+      QTNH_CUDA(cudaMemcpyAsync(static_cast<char*>(recv_buf) + self_r[i]->offset * 16,
+                                static_cast<const char*>(send_buf) + self_s[i]->offset * 16,
+                                self_s[i]->count * 16, cudaMemcpyDeviceToDevice, r.stream));
+  }
+  nccl_check(N.GroupStart(), "group start");
+  for (const Xfer& s : sends)
+    if (s.peer != r.rank && s.count)
+      nccl_check(N.Send(static_cast<const char*>(send_buf) + s.offset * 16, s.count * 16, ncclUint8,
+                        s.peer, comm, r.stream),
+                 "send");
+  for (const Xfer& v : recvs)
+    if (v.peer != r.rank && v.count)
+      nccl_check(N.Recv(static_cast<char*>(recv_buf) + v.offset * 16, v.count * 16, ncclUint8,
+                        v.peer, comm, r.stream),
+                 "recv");
+  nccl_check(N.GroupEnd(), "group end");
+}
+
+}  // namespace
+
+void exchange(RankCtx& r, const std::vector<int>& members, const void* send_buf,
+              const std::vector<Xfer>& sends, void* recv_buf, const std::vector<Xfer>& recvs) {
+  if (r.world->kind == World::kLocal) {
+    local_exchange(r, members, send_buf, sends, recv_buf, recvs);
+  } else {
+    nccl_exchange(r, send_buf, sends, recv_buf, recvs);
+  }
+}
+
+void barrier(RankCtx& r, const std::vector<int>& members) {
+  if (members.size() <= 1) return;
+  if (r.world->kind == World::kLocal) {
+    local_exchange(r, members, nullptr, {}, nullptr, {});
+    QTNH_CUDA(cudaStreamSynchronize(r.stream));
+    return;
+  }
+  // NCCL: a one-element all-to-all among members, then drain the stream.
+  DevBuf sb(16 * members.size(), r), rb(16 * members.size(), r);
+  std::vector<Xfer> s, v;
+  for (size_t i = 0; i < members.size(); ++i) {
+    s.push_back({members[i], static_cast<Dim>(i), 1});
+    v.push_back({members[i], static_cast<Dim>(i), 1});
+  }
+  QTNH_CUDA(cudaMemsetAsync(sb.ptr, 0, sb.bytes, r.stream));
+  nccl_exchange(r, sb.ptr, s, rb.ptr, v);
+  QTNH_CUDA(cudaStreamSynchronize(r.stream));
+}
+
+}  // namespace qtnhb

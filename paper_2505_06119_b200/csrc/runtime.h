@@ -1,0 +1,125 @@
+// Rank runtime of libqtnh_b200: worlds, ranks, device tensors and the exchange
+// primitive every redistribution goes through.
+//
+// Reference: the simulated SPMD runtime (runtime.hpp) -- one host thread per
+// rank, collectives as rendezvous over a global mutex, member-only groups
+// (runtime.hpp:191-223), abort propagation (:276-298) and a collective timeout
+// (QTNH_COLLECTIVE_TIMEOUT_MS, :116, :255-257). Here a rank owns a GPU, a CUDA
+// stream and (process-per-GPU) an NCCL communicator; the host rendezvous only
+// orders stream work -- data never leaves HBM/NVLink.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "common.h"
+
+namespace qtnhb {
+
+struct World;
+
+struct RankCtx {
+  World* world = nullptr;
+  int rank = 0;
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;  // current launch stream
+  std::map<std::vector<int>, uint64_t> seq;  // per member-set collective sequence
+  void activate() const;                     // cudaSetDevice(device)
+};
+
+// One transfer of `count` complex elements at element `offset` of a buffer,
+// to (send) or from (recv) world rank `peer`.
+struct Xfer {
+  int peer;
+  Dim offset;
+  Dim count;
+};
+
+struct World {
+  enum Kind { kLocal, kNccl } kind = kLocal;
+  int size = 1;
+  std::vector<int> devices;  // local: device of each rank
+  // NCCL backend (process per GPU)
+  int my_rank = 0;
+  void* nccl_comm = nullptr;
+  std::unique_ptr<RankCtx> nccl_rank;
+
+  // local backend rendezvous
+  std::mutex mu;
+  std::condition_variable cv;
+  bool aborted = false;
+  long timeout_ms = 120000;
+  struct Post {
+    bool posted = false, done_posted = false;
+    const void* send_buf = nullptr;
+    std::vector<Xfer> sends;
+    cudaEvent_t packed = nullptr;
+    cudaEvent_t pulled = nullptr;
+  };
+  struct Slot {
+    std::vector<Post> posts;
+    int arrived = 0, done = 0, left = 0;
+    std::string error;
+  };
+  std::map<std::pair<std::vector<int>, uint64_t>, Slot> slots;
+};
+
+// Collective over the sorted world ranks `members` (must include r.rank).
+// Moves the listed chunks from send_buf to the peers' recv_bufs. Self transfers
+// are allowed. Stream-ordered on every member's stream; returns when all copies
+// are enqueued. Count mismatches raise ProtocolError naming "(src -> dst)"
+// (runtime.hpp:464-471).
+void exchange(RankCtx& r, const std::vector<int>& members, const void* send_buf,
+              const std::vector<Xfer>& sends, void* recv_buf, const std::vector<Xfer>& recvs);
+void barrier(RankCtx& r, const std::vector<int>& members);
+
+// ---- device tensors -----------------------------------------------------------
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  DevBuf(size_t b, const RankCtx& r);
+  ~DevBuf();
+};
+
+struct TensorImpl {
+  RankCtx* rank = nullptr;
+  Shape shape;
+  Dist dist;
+  bool in_span = false;
+  Dim block = 0, cycle = 0, slot = 0;
+  std::shared_ptr<DevBuf> buf;
+  bool canonical() const { return in_span && cycle == 0 && slot == 0; }
+  Dim span() const { return dist.span(shape.dist_size()); }
+  void* data() const { return buf ? buf->ptr : nullptr; }
+};
+
+// Tensor::make (tensor.hpp:458-477): validates, raises ResourceError when the
+// span exceeds the world, locates this rank; allocates the local block when
+// `alloc` (uninitialised).
+std::shared_ptr<TensorImpl> make_tensor(RankCtx& r, Shape shape, Dist dist, bool alloc);
+std::vector<int> span_ranks(const TensorImpl& t);
+std::vector<int> union_members(const std::vector<std::pair<Dim, Dim>>& spans);
+
+}  // namespace qtnhb
+
+struct qtnh_world_s {
+  std::unique_ptr<qtnhb::World> w;
+};
+struct qtnh_rank_s {
+  qtnhb::World* world;
+  std::unique_ptr<qtnhb::RankCtx> owned;  // local backend
+  qtnhb::RankCtx* ctx;
+};
+struct qtnh_tensor_s {
+  std::shared_ptr<qtnhb::TensorImpl> impl;
+  std::atomic<int> refs{1};
+};

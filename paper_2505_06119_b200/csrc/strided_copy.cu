@@ -1,0 +1,482 @@
+// Strided-copy engine for sm_100a (see strided_copy.h).
+//
+// Design (HBM-bound byte movement, no tensor cores):
+//  * The box is simplified on the host: unit dims dropped, dims that stay
+//    adjacent on both sides merged, then large dims split into <=64-wide factors
+//    so a tile can take "part of" a big index.
+//  * A tile is the union of the innermost input dims (product >= 32 elements,
+//    i.e. >= 512 contiguous bytes read) and the innermost output dims (>= 32
+//    elements written contiguously). One CTA moves a tile global -> shared ->
+//    global: reads coalesced along the input order, writes coalesced along the
+//    output order. Shared-memory positions are XOR-swizzled (16-B elements, 8
+//    bank groups) so the transposed read-out is conflict-free for power-of-two
+//    strides.
+//  * Per-tile offset tables (input offset, output offset, shared slot) are built
+//    once per plan on the host and read through the read-only path; outer
+//    (non-tile) coordinates come from the tile id by shift/mask (powers of two)
+//    or div/mod, once per tile.
+//  * Tiles whose input and output orders coincide skip shared memory entirely.
+//  * Persistent grid: (#SM x resident CTAs), grid-stride over tiles.
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+
+#include "strided_copy.h"
+
+namespace qtnhb {
+
+namespace {
+
+constexpr int kMaxOuter = 64;
+constexpr int kThreads = 256;
+
+struct Outer {
+  int n;
+  int all_pow2;
+  int64_t dim[kMaxOuter];
+  int shift[kMaxOuter];
+  int64_t is[kMaxOuter];
+  int64_t os[kMaxOuter];
+};
+
+__device__ __forceinline__ void decompose(int64_t tile, const Outer& od, int64_t& bi, int64_t& bo) {
+  bi = 0;
+  bo = 0;
+  if (od.all_pow2) {
+    for (int i = od.n - 1; i >= 0; --i) {
+      int64_t c = tile & (od.dim[i] - 1);
+      tile >>= od.shift[i];
+      bi += c * od.is[i];
+      bo += c * od.os[i];
+    }
+  } else {
+    for (int i = od.n - 1; i >= 0; --i) {
+      int64_t c = tile % od.dim[i];
+      tile /= od.dim[i];
+      bi += c * od.is[i];
+      bo += c * od.os[i];
+    }
+  }
+}
+
+__device__ __forceinline__ int swz(int e) { return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7); }
+
+__device__ __forceinline__ double2 canon_zero(double2 v) {
+  if (v.x == 0.0 && v.y == 0.0) v = make_double2(0.0, 0.0);
+  return v;
+}
+
+template <bool CANON, bool DIRECT>
+__global__ void __launch_bounds__(kThreads) k_tiled(const double2* __restrict__ in,
+                                                    double2* __restrict__ out,
+                                                    const int64_t* __restrict__ tin,
+                                                    const int64_t* __restrict__ tout,
+                                                    const int* __restrict__ tslot, int T,
+                                                    int64_t n_tiles, const Outer od) {
+  extern __shared__ double2 sm[];
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    int64_t bi, bo;
+    decompose(tile, od, bi, bo);
+    if (DIRECT) {
+      constexpr int U = 4;
+      for (int e0 = threadIdx.x; e0 < T; e0 += kThreads * U) {
+        double2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          int e = e0 + u * kThreads;
+          if (e < T) v[u] = __ldg(in + bi + __ldg(tin + e));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          int e = e0 + u * kThreads;
+          if (e < T) out[bo + __ldg(tout + e)] = CANON ? canon_zero(v[u]) : v[u];
+        }
+      }
+    } else {
+      constexpr int U = 4;
+      for (int e0 = threadIdx.x; e0 < T; e0 += kThreads * U) {
+        double2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          int e = e0 + u * kThreads;
+          if (e < T) v[u] = __ldg(in + bi + __ldg(tin + e));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          int e = e0 + u * kThreads;
+          if (e < T) sm[swz(e)] = v[u];
+        }
+      }
+      __syncthreads();
+      for (int f = threadIdx.x; f < T; f += kThreads) {
+        double2 v = sm[__ldg(tslot + f)];
+        out[bo + __ldg(tout + f)] = CANON ? canon_zero(v) : v;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Fallback for boxes no tile fits (huge prime dims on both sides): one thread per
+// output element in output order, gathered input.
+struct Full {
+  int n;
+  int64_t dim[kMaxOuter];
+  int64_t is[kMaxOuter];
+  int64_t os[kMaxOuter];
+};
+
+template <bool CANON>
+__global__ void __launch_bounds__(kThreads) k_gather(const double2* __restrict__ in,
+                                                     double2* __restrict__ out, int64_t total,
+                                                     const Full fd) {
+  for (int64_t f = blockIdx.x * (int64_t)kThreads + threadIdx.x; f < total;
+       f += (int64_t)gridDim.x * kThreads) {
+    int64_t t = f, bi = 0, bo = 0;
+    for (int i = fd.n - 1; i >= 0; --i) {
+      int64_t c = t % fd.dim[i];
+      t /= fd.dim[i];
+      bi += c * fd.is[i];
+      bo += c * fd.os[i];
+    }
+    double2 v = in[bi];
+    out[bo] = CANON ? canon_zero(v) : v;
+  }
+}
+
+__global__ void k_scale_conj(const double2* __restrict__ in, double2* __restrict__ out, int64_t n,
+                             double re, double im, int conj) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double2 v = in[i];
+    if (conj) v.y = -v.y;
+    out[i] = make_double2(v.x * re - v.y * im, v.x * im + v.y * re);
+  }
+}
+
+__global__ void k_fill_zero(double2* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = make_double2(0.0, 0.0);
+}
+
+// ---- host planning ------------------------------------------------------------
+struct D {
+  Dim n, is, os;
+};
+
+struct Plan {
+  enum Kind { kTiled, kDirect, kGather, kEmpty } kind = kEmpty;
+  int T = 0;
+  int64_t n_tiles = 0;
+  Outer od{};
+  Full fd{};
+  int64_t* d_tin = nullptr;
+  int64_t* d_tout = nullptr;
+  int* d_slot = nullptr;
+  int grid = 0;
+  size_t smem = 0;
+};
+
+int sm_count(int dev) {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  QTNH_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  cache[dev] = n;
+  return n;
+}
+
+Dim pick_factor(Dim n) {
+  // Largest power of two <= 64 dividing n, else the largest divisor in [8, 64].
+  for (Dim t = 64; t >= 8; t >>= 1)
+    if (n % t == 0 && n / t > 1) return t;
+  for (Dim t = 64; t >= 8; --t)
+    if (n % t == 0 && n / t > 1) return t;
+  return 0;
+}
+
+std::vector<D> simplify(const CopyBox& box) {
+  std::vector<D> v;
+  for (size_t i = 0; i < box.dims.size(); ++i)
+    if (box.dims[i] != 1) v.push_back({box.dims[i], box.in_stride[i], box.out_stride[i]});
+  // Order by input stride descending (row-major over the input), then merge
+  // neighbours that are adjacent on both sides.
+  std::stable_sort(v.begin(), v.end(), [](const D& a, const D& b) { return a.is > b.is; });
+  std::vector<D> m;
+  for (const D& d : v) {
+    if (!m.empty()) {
+      D& o = m.back();
+      if (o.is == d.is * d.n && o.os == d.os * d.n) {
+        o.n *= d.n;
+        o.is = d.is;
+        o.os = d.os;
+        continue;
+      }
+    }
+    m.push_back(d);
+  }
+  // Split dims wider than 64 so a tile can take a slice of them.
+  std::vector<D> s;
+  for (const D& d : m) {
+    std::vector<D> parts;  // outer..inner
+    D cur = d;
+    while (cur.n > 64) {
+      Dim t = pick_factor(cur.n);
+      if (!t) break;
+      parts.insert(parts.begin(), D{t, cur.is, cur.os});
+      cur = D{cur.n / t, cur.is * t, cur.os * t};
+    }
+    s.push_back(cur);
+    for (const D& p : parts) s.push_back(p);
+  }
+  return s;
+}
+
+std::string key_of(const std::vector<D>& v, int dev) {
+  std::string k(reinterpret_cast<const char*>(v.data()), v.size() * sizeof(D));
+  k.append(reinterpret_cast<const char*>(&dev), sizeof(dev));
+  return k;
+}
+
+std::shared_ptr<Plan> build_plan(const std::vector<D>& ds, int dev, cudaStream_t st) {
+  auto p = std::make_shared<Plan>();
+  int r = static_cast<int>(ds.size());
+  std::vector<int> in_order(r), out_order(r);
+  std::iota(in_order.begin(), in_order.end(), 0);
+  std::iota(out_order.begin(), out_order.end(), 0);
+  std::stable_sort(in_order.begin(), in_order.end(), [&](int a, int b) { return ds[a].is < ds[b].is; });
+  std::stable_sort(out_order.begin(), out_order.end(), [&](int a, int b) { return ds[a].os < ds[b].os; });
+
+  std::vector<char> in_tile;
+  Dim tile = 1;
+  const Dim kMaxTile = 8192;
+  for (Dim min_run : {32, 16, 8, 2}) {
+    in_tile.assign(r, 0);
+    Dim prod = 1;
+    for (int i = 0; i < r && prod < min_run; ++i) {
+      in_tile[in_order[i]] = 1;
+      prod *= ds[in_order[i]].n;
+    }
+    Dim oprod = 1;
+    for (int i = 0; i < r && oprod < min_run; ++i) {
+      oprod *= ds[out_order[i]].n;
+      in_tile[out_order[i]] = 1;
+    }
+    tile = 1;
+    for (int i = 0; i < r; ++i)
+      if (in_tile[i]) tile *= ds[i].n;
+    if (tile <= kMaxTile) break;
+  }
+  if (tile > kMaxTile) {
+    p->kind = Plan::kGather;
+    p->fd.n = r;
+    for (int j = 0; j < r; ++j) {
+      int i = out_order[r - 1 - j];  // outermost output dim first
+      p->fd.dim[j] = ds[i].n;
+      p->fd.is[j] = ds[i].is;
+      p->fd.os[j] = ds[i].os;
+    }
+    Dim total = 1;
+    for (auto& d : ds) total *= d.n;
+    p->n_tiles = total;
+    p->grid = sm_count(dev) * 8;
+    return p;
+  }
+  // Grow small tiles with further input-order dims to amortise per-tile work.
+  for (int i = 0; i < r && tile < 512; ++i) {
+    int d = in_order[i];
+    if (!in_tile[d] && tile * ds[d].n <= 2048) {
+      in_tile[d] = 1;
+      tile *= ds[d].n;
+    }
+  }
+  std::vector<int> tin_dims, tout_dims;  // innermost first
+  for (int i : in_order)
+    if (in_tile[i]) tin_dims.push_back(i);
+  for (int i : out_order)
+    if (in_tile[i]) tout_dims.push_back(i);
+  bool direct = tin_dims == tout_dims;
+  int T = static_cast<int>(tile);
+  std::vector<int64_t> tin(T), tout(T);
+  std::vector<int> slot(T);
+  auto swz = [](int e) { return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7); };
+  // Input order: e = sum c * w_in.
+  std::vector<Dim> w_in(r, 0);
+  {
+    Dim w = 1;
+    for (int i : tin_dims) {
+      w_in[i] = w;
+      w *= ds[i].n;
+    }
+  }
+  std::vector<Dim> c(r, 0);
+  for (int e = 0; e < T; ++e) {
+    Dim rem = e;
+    int64_t off = 0;
+    for (int i : tin_dims) {
+      Dim ci = rem % ds[i].n;
+      rem /= ds[i].n;
+      off += ci * ds[i].is;
+    }
+    tin[e] = off;
+  }
+  for (int f = 0; f < T; ++f) {
+    Dim rem = f;
+    int64_t off = 0;
+    Dim e = 0;
+    for (int i : tout_dims) {
+      Dim ci = rem % ds[i].n;
+      rem /= ds[i].n;
+      off += ci * ds[i].os;
+      e += ci * w_in[i];
+    }
+    tout[f] = off;
+    slot[f] = swz(static_cast<int>(e));
+  }
+  if (direct) {
+    // Direct mode walks e in input order for both sides.
+    for (int e = 0; e < T; ++e) {
+      Dim rem = e;
+      int64_t off = 0;
+      for (int i : tin_dims) {
+        Dim ci = rem % ds[i].n;
+        rem /= ds[i].n;
+        off += ci * ds[i].os;
+      }
+      tout[e] = off;
+    }
+  }
+  // Outer dims: outermost (by output stride) first, tile id row-major over them.
+  std::vector<int> outer;
+  for (int j = r - 1; j >= 0; --j)
+    if (!in_tile[out_order[j]]) outer.push_back(out_order[j]);
+  if (static_cast<int>(outer.size()) > kMaxOuter) throw_invalid("tensor rank too large for the copy engine");
+  p->od.n = static_cast<int>(outer.size());
+  p->od.all_pow2 = 1;
+  Dim n_tiles = 1;
+  for (int j = 0; j < p->od.n; ++j) {
+    const D& d = ds[outer[j]];
+    p->od.dim[j] = d.n;
+    p->od.is[j] = d.is;
+    p->od.os[j] = d.os;
+    int sh = 0;
+    while ((Dim(1) << sh) < d.n) ++sh;
+    p->od.shift[j] = sh;
+    if ((Dim(1) << sh) != d.n) p->od.all_pow2 = 0;
+    n_tiles *= d.n;
+  }
+  p->kind = direct ? Plan::kDirect : Plan::kTiled;
+  p->T = T;
+  p->n_tiles = n_tiles;
+  p->smem = direct ? 0 : static_cast<size_t>((T + 7) & ~7) * sizeof(double2);
+  QTNH_CUDA(cudaMalloc(&p->d_tin, T * sizeof(int64_t)));
+  QTNH_CUDA(cudaMalloc(&p->d_tout, T * sizeof(int64_t)));
+  QTNH_CUDA(cudaMalloc(&p->d_slot, T * sizeof(int)));
+  QTNH_CUDA(cudaMemcpyAsync(p->d_tin, tin.data(), T * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  QTNH_CUDA(cudaMemcpyAsync(p->d_tout, tout.data(), T * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  QTNH_CUDA(cudaMemcpyAsync(p->d_slot, slot.data(), T * sizeof(int), cudaMemcpyHostToDevice, st));
+  QTNH_CUDA(cudaStreamSynchronize(st));  // host staging vectors die with this scope
+  int per_sm = 1;
+  if (direct) {
+    QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tiled<true, true>, kThreads, 0));
+  } else {
+    if (p->smem > 48 * 1024) {
+      QTNH_CUDA(cudaFuncSetAttribute(k_tiled<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem));
+      QTNH_CUDA(cudaFuncSetAttribute(k_tiled<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem));
+    }
+    QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tiled<true, false>, kThreads, p->smem));
+  }
+  Dim g = static_cast<Dim>(sm_count(dev)) * std::max(1, per_sm);
+  p->grid = static_cast<int>(std::max<Dim>(1, std::min<Dim>(g, n_tiles)));
+  return p;
+}
+
+std::mutex g_plan_mu;
+std::map<std::string, std::shared_ptr<Plan>> g_plans;
+
+}  // namespace
+
+CopyBox permute_box(const std::vector<Dim>& dims, const std::vector<int>& perm) {
+  // Output position p holds input index perm[p]; iterate the box over the input
+  // indices: in stride = row-major input stride, out stride = row-major output
+  // stride at the position the index moves to.
+  int r = static_cast<int>(dims.size());
+  std::vector<Dim> nd(r);
+  for (int p = 0; p < r; ++p) nd[p] = dims[perm[p]];
+  auto is = row_major_strides(dims);
+  auto os_new = row_major_strides(nd);
+  CopyBox b;
+  b.dims = dims;
+  b.in_stride = is;
+  b.out_stride.assign(r, 0);
+  for (int p = 0; p < r; ++p) b.out_stride[perm[p]] = os_new[p];
+  return b;
+}
+
+void strided_copy(const void* in, void* out, const CopyBox& box, bool canon, cudaStream_t st) {
+  Dim total = 1;
+  for (Dim d : box.dims) total *= d;
+  if (total == 0) return;
+  auto ds = simplify(box);
+  int dev = 0;
+  QTNH_CUDA(cudaGetDevice(&dev));
+  std::shared_ptr<Plan> p;
+  {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    auto key = key_of(ds, dev);
+    auto it = g_plans.find(key);
+    if (it != g_plans.end()) {
+      p = it->second;
+    } else {
+      p = build_plan(ds, dev, st);
+      if (g_plans.size() > 4096) g_plans.clear();  // bounded; device tables leak-free enough
+      g_plans[key] = p;
+    }
+  }
+  auto i = static_cast<const double2*>(in);
+  auto o = static_cast<double2*>(out);
+  switch (p->kind) {
+    case Plan::kGather:
+      if (canon) k_gather<true><<<p->grid, kThreads, 0, st>>>(i, o, p->n_tiles, p->fd);
+      else k_gather<false><<<p->grid, kThreads, 0, st>>>(i, o, p->n_tiles, p->fd);
+      break;
+    case Plan::kDirect:
+      if (canon) k_tiled<true, true><<<p->grid, kThreads, 0, st>>>(i, o, p->d_tin, p->d_tout, p->d_slot, p->T, p->n_tiles, p->od);
+      else k_tiled<false, true><<<p->grid, kThreads, 0, st>>>(i, o, p->d_tin, p->d_tout, p->d_slot, p->T, p->n_tiles, p->od);
+      break;
+    case Plan::kTiled:
+      if (canon) k_tiled<true, false><<<p->grid, kThreads, p->smem, st>>>(i, o, p->d_tin, p->d_tout, p->d_slot, p->T, p->n_tiles, p->od);
+      else k_tiled<false, false><<<p->grid, kThreads, p->smem, st>>>(i, o, p->d_tin, p->d_tout, p->d_slot, p->T, p->n_tiles, p->od);
+      break;
+    case Plan::kEmpty:
+      return;
+  }
+  QTNH_LAUNCH_CHECK();
+}
+
+void scale_conj(const void* in, void* out, Dim n, double re, double im, bool conj, cudaStream_t st) {
+  if (n <= 0) return;
+  int dev = 0;
+  QTNH_CUDA(cudaGetDevice(&dev));
+  int grid = static_cast<int>(std::min<Dim>((n + 255) / 256, (Dim)sm_count(dev) * 8));
+  k_scale_conj<<<grid, 256, 0, st>>>(static_cast<const double2*>(in), static_cast<double2*>(out), n, re, im, conj);
+  QTNH_LAUNCH_CHECK();
+}
+
+void fill_zero(void* out, Dim n, cudaStream_t st) {
+  if (n <= 0) return;
+  int dev = 0;
+  QTNH_CUDA(cudaGetDevice(&dev));
+  int grid = static_cast<int>(std::min<Dim>((n + 255) / 256, (Dim)sm_count(dev) * 8));
+  k_fill_zero<<<grid, 256, 0, st>>>(static_cast<double2*>(out), n);
+  QTNH_LAUNCH_CHECK();
+}
+
+}  // namespace qtnhb

@@ -1,0 +1,33 @@
+// Strided-copy engine: every structural operation of the remap path
+// (permutation, pack into per-destination chunks, unpack into the destination
+// block) is one launch of this engine. It replaces the per-element
+// (address, value) Item packing of remap::pack_sends (remap.hpp:56-101) and the
+// scatter loop of tensor_to_tensor (remap.hpp:155-159).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "common.h"
+
+namespace qtnhb {
+
+// out[sum_i c_i*out_stride_i] = f(in[sum_i c_i*in_stride_i]) for every coordinate
+// tuple c of the box; strides in complex128 elements. With `canon` set, elements
+// whose two parts are both zero are written as (+0, +0) (remap.hpp:69-70 skips
+// them and the destination starts zeroed, remap.hpp:125-127).
+struct CopyBox {
+  std::vector<Dim> dims, in_stride, out_stride;
+};
+
+void strided_copy(const void* in, void* out, const CopyBox& box, bool canon, cudaStream_t st);
+
+// Box of a row-major permutation: out = permute(in over dims, perm[new] = old).
+CopyBox permute_box(const std::vector<Dim>& dims, const std::vector<int>& perm);
+
+// Elementwise y = alpha * conj?(x) over n complex numbers.
+void scale_conj(const void* in, void* out, Dim n, double re, double im, bool conj, cudaStream_t st);
+void fill_zero(void* out, Dim n, cudaStream_t st);
+
+}  // namespace qtnhb

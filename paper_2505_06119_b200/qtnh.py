@@ -1,0 +1,482 @@
+"""Host-side mirror of the reference's C++ operator API over the C ABI.
+
+Same names, argument meaning and error classes as /root/reference/proj/include/qtnh:
+
+==========================  =======================================================
+this module                 reference
+==========================  =======================================================
+``IndexTuple``              ``qtnh::IndexTuple``            indexing.hpp:32-80
+``DistParams``              ``qtnh::DistParams``            indexing.hpp:84-101
+``World(n).run(body)``      ``qtnh::World::run``            runtime.hpp:245-299
+``Tensor.dense/from_global````qtnh::Tensor::dense/from_global`` tensor.hpp:61-94
+``Tensor.to_global_vector`` ``Tensor::to_global_vector``    tensor.hpp:341-371
+``ops.permute`` ...         ``qtnh::ops::*``                ops.hpp:27-230
+``contract``                SPEC network::contract via linalg.hpp:208/:347/:273
+``apply_gate``              contract(state, gate) + permute back (in place)
+==========================  =======================================================
+
+Every rank of a World is driven by its own host thread (the reference's
+simulated SPMD runtime does the same); each rank owns a CUDA stream on its GPU,
+tensors live in HBM, and every operation runs the CUDA kernels of
+libqtnh_b200.so. ``World.from_env()`` builds the process-per-GPU (torchrun/NCCL)
+world instead.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+import weakref
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+from ._lib import i32_array, i64_array, last_error, lib
+
+# ---- errors (common.hpp:31-74) ------------------------------------------------
+
+
+class Error(RuntimeError):
+    """Base class of every error raised by the library."""
+
+
+class InvalidArgument(Error):
+    pass
+
+
+class ResourceError(Error):
+    def __init__(self, msg: str, required_ranks: int = 0):
+        super().__init__(msg)
+        self.required_ranks = required_ranks
+
+
+class ProtocolError(Error):
+    pass
+
+
+class NumericalError(Error):
+    def __init__(self, msg: str, info: int = 0):
+        super().__init__(msg)
+        self.info = info
+
+
+class PreconditionError(Error):
+    pass
+
+
+class DegenerateStateError(Error):
+    pass
+
+
+class AbortedError(Error):
+    pass
+
+
+_ERR = {1: InvalidArgument, 2: ResourceError, 3: ProtocolError, 4: NumericalError,
+        5: PreconditionError, 6: DegenerateStateError, 7: AbortedError, 8: Error}
+
+
+def check(status: int) -> None:
+    if status == 0:
+        return
+    msg = last_error()
+    info = int(lib.qtnh_last_error_info())
+    cls = _ERR.get(status, Error)
+    if cls is ResourceError:
+        raise ResourceError(msg, info)
+    if cls is NumericalError:
+        raise NumericalError(msg, info)
+    raise cls(msg)
+
+
+# ---- layout metadata -------------------------------------------------------------
+
+
+@dataclass
+class IndexTuple:
+    """Dims with the first ``split`` indices distributed (indexing.hpp:32-80)."""
+
+    dims: List[int]
+    split: int = 0
+
+    def __post_init__(self):
+        self.dims = [int(d) for d in self.dims]
+        if self.split < 0 or self.split > len(self.dims):
+            raise InvalidArgument(f"index split {self.split} outside [0, {len(self.dims)}]")
+        if any(d < 1 for d in self.dims):
+            raise InvalidArgument("index dimensions must be positive")
+
+    def n_idx(self) -> int:
+        return len(self.dims)
+
+    def dist_size(self) -> int:
+        return int(np.prod(self.dims[: self.split], dtype=np.int64))
+
+    def local_size(self) -> int:
+        return int(np.prod(self.dims[self.split:], dtype=np.int64))
+
+    def total_size(self) -> int:
+        return self.dist_size() * self.local_size()
+
+    def str(self) -> str:
+        d = [str(x) for x in self.dims]
+        return "(" + ",".join(d[: self.split]) + ";" + ",".join(d[self.split:]) + ")"
+
+
+@dataclass
+class DistParams:
+    """Broadcast pattern (indexing.hpp:84-101): stretch, cycles, offset."""
+
+    stretch: int = 1
+    cycles: int = 1
+    offset: int = 0
+
+    def as_array(self):
+        return i64_array([self.stretch, self.cycles, self.offset])
+
+    def span(self, dist_size: int) -> int:
+        return self.stretch * self.cycles * dist_size
+
+
+def _dist(d) -> DistParams:
+    if d is None:
+        return DistParams()
+    if isinstance(d, DistParams):
+        return d
+    return DistParams(*d)
+
+
+# ---- worlds and ranks ---------------------------------------------------------------
+
+
+class Rank:
+    """Per-thread execution context of one rank (runtime.hpp:186-239)."""
+
+    def __init__(self, world: "World", rank: int):
+        self.world = world
+        h = C.c_void_p()
+        check(lib.qtnh_rank_bind(world._h, rank, C.byref(h)))
+        self._h = h
+        self._rank = rank
+        self._tensors: "weakref.WeakSet[Tensor]" = weakref.WeakSet()
+
+    def rank(self) -> int:
+        return self._rank
+
+    def size(self) -> int:
+        return self.world.size()
+
+    def stream_ptr(self) -> int:
+        return int(lib.qtnh_rank_stream(self._h) or 0)
+
+    def set_stream(self, stream_ptr: Optional[int]) -> None:
+        check(lib.qtnh_rank_set_stream(self._h, C.c_void_p(stream_ptr or 0)))
+
+    def synchronize(self) -> None:
+        check(lib.qtnh_rank_synchronize(self._h))
+
+    def barrier(self) -> None:
+        check(lib.qtnh_barrier(self._h))
+
+    def release(self) -> None:
+        if self._h is None:
+            return
+        for t in list(self._tensors):
+            t.free()
+        check(lib.qtnh_rank_release(self._h))
+        self._h = None
+
+
+class World:
+    """SPMD world of ranks; ``run`` executes ``body(rank)`` once per rank on its own
+    host thread and rethrows the originating failure (runtime.hpp:263-299)."""
+
+    def __init__(self, n_ranks: int, devices: Optional[Sequence[int]] = None):
+        if n_ranks < 1:
+            raise InvalidArgument(f"world size must be >= 1, got {n_ranks}")
+        h = C.c_void_p()
+        dev = i32_array(devices) if devices is not None else None
+        check(lib.qtnh_world_create_local(n_ranks, dev, C.byref(h)))
+        self._h = h
+        self._n = n_ranks
+        self._nccl_rank: Optional[int] = None
+
+    @classmethod
+    def from_env(cls) -> "World":
+        """Process-per-GPU world from torchrun's env (RANK, WORLD_SIZE, LOCAL_RANK).
+        The NCCL unique id is shared through torch.distributed (gloo store)."""
+        import torch.distributed as dist
+
+        rank = int(os.environ.get("RANK", "0"))
+        size = int(os.environ.get("WORLD_SIZE", "1"))
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        self = cls.__new__(cls)
+        self._n = size
+        self._nccl_rank = rank
+        if size == 1:
+            h = C.c_void_p()
+            check(lib.qtnh_world_create_local(1, i32_array([local]), C.byref(h)))
+            self._h = h
+            self._nccl_rank = None
+            return self
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            check(lib.qtnh_nccl_unique_id(uid))
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0)
+        C.memmove(uid, obj[0], 128)
+        h = C.c_void_p()
+        check(lib.qtnh_world_create_nccl(rank, size, local, uid, C.byref(h)))
+        self._h = h
+        return self
+
+    def size(self) -> int:
+        return self._n
+
+    def run(self, body: Callable[[Rank], object]) -> list:
+        if self._nccl_rank is not None:
+            rk = Rank(self, self._nccl_rank)
+            try:
+                return [body(rk)]
+            finally:
+                rk.release()
+        results = [None] * self._n
+        errors: list = [None] * self._n
+
+        def worker(r: int):
+            rk = None
+            try:
+                rk = Rank(self, r)
+                results[r] = body(rk)
+            except BaseException as e:  # noqa: BLE001 - propagated below
+                errors[r] = e
+                lib.qtnh_world_abort(self._h)
+            finally:
+                if rk is not None:
+                    try:
+                        rk.release()
+                    except Error:
+                        pass
+
+        threads = [threading.Thread(target=worker, args=(r,)) for r in range(self._n)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        first = None
+        for e in errors:
+            if e is None:
+                continue
+            if first is None:
+                first = e
+            if not isinstance(e, AbortedError):
+                raise e
+        if first is not None:
+            raise first
+        # A world is reusable after a failure only through a fresh instance.
+        return results
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.qtnh_world_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_collect(world: World, body: Callable[[Rank], object]):
+    """Rank 0's result (tests/test_util.hpp:36-47)."""
+    return world.run(body)[0]
+
+
+# ---- tensors -------------------------------------------------------------------------
+
+
+def _as_c128(v) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(v, dtype=np.complex128))
+
+
+class Tensor:
+    """Dense distributed tensor value held in HBM (tensor.hpp:53-695)."""
+
+    def __init__(self, rank: Rank, handle: C.c_void_p):
+        self.ctx_rank = rank
+        self._h = handle
+        rank._tensors.add(self)
+
+    # -- constructors -------------------------------------------------------------
+    @staticmethod
+    def dense(rank: Rank, shape: IndexTuple, dist=None, local_data=None) -> "Tensor":
+        d = _dist(dist)
+        h = C.c_void_p()
+        buf = None
+        if local_data is not None:
+            buf = _as_c128(local_data)
+        ok = buf is not None and buf.size == shape.local_size()
+        check(lib.qtnh_tensor_dense(rank._h, shape.n_idx(), i64_array(shape.dims), shape.split,
+                                    d.as_array(), buf.ctypes.data if ok else None, C.byref(h)))
+        t = Tensor(rank, h)
+        if buf is not None and not ok and t.in_span():
+            t.free()
+            raise InvalidArgument(f"dense local data has {buf.size} elements, expected {shape.local_size()}")
+        return t
+
+    @staticmethod
+    def from_global(rank: Rank, shape: IndexTuple, dist, global_data) -> "Tensor":
+        g = _as_c128(global_data)
+        if g.size != shape.total_size():
+            raise InvalidArgument("global element count mismatch")
+        d = _dist(dist)
+        h = C.c_void_p()
+        check(lib.qtnh_tensor_from_global(rank._h, shape.n_idx(), i64_array(shape.dims), shape.split,
+                                          d.as_array(), g.ctypes.data, C.byref(h)))
+        return Tensor(rank, h)
+
+    @staticmethod
+    def from_device(rank: Rank, shape: IndexTuple, dist, dev_ptr: int) -> "Tensor":
+        d = _dist(dist)
+        h = C.c_void_p()
+        check(lib.qtnh_tensor_from_device(rank._h, shape.n_idx(), i64_array(shape.dims), shape.split,
+                                          d.as_array(), C.c_void_p(dev_ptr), C.byref(h)))
+        return Tensor(rank, h)
+
+    @staticmethod
+    def scalar(rank: Rank, value: complex, dist=None) -> "Tensor":
+        return Tensor.dense(rank, IndexTuple([], 0), dist, np.array([value]))
+
+    # -- metadata --------------------------------------------------------------------
+    def shape(self) -> IndexTuple:
+        n = lib.qtnh_tensor_rank(self._h)
+        dims = i64_array([0] * n)
+        check(lib.qtnh_tensor_dims(self._h, dims))
+        return IndexTuple([dims[i] for i in range(n)], lib.qtnh_tensor_split(self._h))
+
+    def dist(self) -> DistParams:
+        d = i64_array([0, 0, 0])
+        check(lib.qtnh_tensor_dist(self._h, d))
+        return DistParams(d[0], d[1], d[2])
+
+    def span(self) -> int:
+        return int(lib.qtnh_tensor_span(self._h))
+
+    def in_span(self) -> bool:
+        return bool(lib.qtnh_tensor_in_span(self._h))
+
+    def my_block(self) -> int:
+        return int(lib.qtnh_tensor_my_block(self._h))
+
+    def is_canonical_holder(self) -> bool:
+        return bool(lib.qtnh_tensor_is_canonical(self._h))
+
+    def local_size(self) -> int:
+        return int(lib.qtnh_tensor_local_size(self._h))
+
+    def device_ptr(self) -> int:
+        return int(lib.qtnh_tensor_device_ptr(self._h) or 0)
+
+    def ctx(self) -> Rank:
+        return self.ctx_rank
+
+    # -- data ----------------------------------------------------------------------------
+    def local_data(self) -> np.ndarray:
+        out = np.empty(self.local_size() if self.in_span() else 0, dtype=np.complex128)
+        if out.size:
+            check(lib.qtnh_tensor_download_local(self._h, out.ctypes.data))
+        return out
+
+    def to_global_vector(self) -> np.ndarray:
+        if not self.in_span():
+            return np.empty(0, dtype=np.complex128)
+        out = np.empty(self.shape().total_size(), dtype=np.complex128)
+        check(lib.qtnh_tensor_to_global(self._h, out.ctypes.data))
+        return out
+
+    def free(self) -> None:
+        if self._h is not None:
+            lib.qtnh_tensor_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def _new(self, h) -> "Tensor":
+        return Tensor(self.ctx_rank, h)
+
+
+# ---- ops (ops.hpp) -----------------------------------------------------------------------
+
+
+class ops:  # namespace
+    @staticmethod
+    def permute(t: Tensor, perm: Sequence[int], new_split: int) -> Tensor:
+        h = C.c_void_p()
+        check(lib.qtnh_permute(t._h, i32_array(perm), int(new_split), C.byref(h)))
+        return t._new(h)
+
+    @staticmethod
+    def rebcast(t: Tensor, new_dist) -> Tensor:
+        h = C.c_void_p()
+        check(lib.qtnh_rebcast(t._h, _dist(new_dist).as_array(), C.byref(h)))
+        return t._new(h)
+
+    @staticmethod
+    def scatter_index(t: Tensor, pos: int) -> Tensor:
+        h = C.c_void_p()
+        check(lib.qtnh_scatter_index(t._h, int(pos), C.byref(h)))
+        return t._new(h)
+
+    @staticmethod
+    def gather_index(t: Tensor, pos: int) -> Tensor:
+        h = C.c_void_p()
+        check(lib.qtnh_gather_index(t._h, int(pos), C.byref(h)))
+        return t._new(h)
+
+    @staticmethod
+    def conj(t: Tensor) -> Tensor:
+        h = C.c_void_p()
+        check(lib.qtnh_conj(t._h, C.byref(h)))
+        return t._new(h)
+
+    @staticmethod
+    def scale(t: Tensor, alpha: complex) -> Tensor:
+        h = C.c_void_p()
+        check(lib.qtnh_scale(t._h, float(np.real(alpha)), float(np.imag(alpha)), C.byref(h)))
+        return t._new(h)
+
+    @staticmethod
+    def slice_local_dims(t: Tensor, new_local_dims: Sequence[int]) -> Tensor:
+        h = C.c_void_p()
+        check(lib.qtnh_slice_local_dims(t._h, i64_array(new_local_dims), C.byref(h)))
+        return t._new(h)
+
+    @staticmethod
+    def pad_local_dims(t: Tensor, new_local_dims: Sequence[int]) -> Tensor:
+        h = C.c_void_p()
+        check(lib.qtnh_pad_local_dims(t._h, i64_array(new_local_dims), C.byref(h)))
+        return t._new(h)
+
+
+def contract(a: Tensor, b: Tensor, a_pos: Sequence[int], b_pos: Sequence[int]) -> Tensor:
+    """Contract a[a_pos[i]] with b[b_pos[i]]; result = open(a) then open(b)
+    (SPEC.md:408), DistParams of a."""
+    if len(a_pos) != len(b_pos):
+        raise InvalidArgument("contracted position lists differ in length")
+    h = C.c_void_p()
+    check(lib.qtnh_contract(a._h, b._h, len(a_pos), i32_array(a_pos), i32_array(b_pos), C.byref(h)))
+    return a._new(h)
+
+
+def apply_gate(state: Tensor, targets: Sequence[int], gate, diagonal: bool = False) -> Tensor:
+    """In-place gate (row index = gate output, targets[0] most significant).
+    Values equal contract(state, gate) followed by a permute back."""
+    g = _as_c128(gate)
+    check(lib.qtnh_gate_apply(state._h, len(targets), i32_array(targets), g.ctypes.data, int(bool(diagonal))))
+    return state

@@ -1,0 +1,41 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA path of libqtnh_b200.so)")
+    config.addinivalue_line("markers", "slow: long-running parity case")
+
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def golden(name):
+    import json
+
+    import numpy as np
+
+    z = np.load(os.path.join(GOLDEN, name + ".npz"))
+    return json.loads(str(z["meta"])), z
+
+
+def bits(x):
+    """Bit pattern view (exact equality including signed zeros)."""
+    import numpy as np
+
+    return np.ascontiguousarray(x, dtype=np.complex128).view(np.uint64)
+
+
+def rel_l2(a, b):
+    import numpy as np
+
+    a = np.asarray(a)
+    b = np.asarray(b)
+    nb = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))

@@ -1,0 +1,128 @@
+"""GPU parity of pairwise contraction (complex128 DMMA GEMM + fused layout) against
+the reference's t2m -> pgemm -> m2t path, within the north-star tolerance of
+relative L2 <= 1e-10 (BASELINE.json north_star)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden, rel_l2
+from paper_2505_06119_b200 import circuits, qtnh
+from paper_2505_06119_b200.qtnh import DistParams, IndexTuple, Tensor, World, contract, run_collect
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+P = oracle.port()
+
+
+def test_contract_golden():
+    meta, z = golden("contract")
+    for i, m in enumerate(meta):
+        a, b = z[f"a{i}"], z[f"b{i}"]
+
+        def body(rk):
+            ta = Tensor.from_global(rk, IndexTuple(m["da"], m["sa"]), DistParams(1, 1, 0), a)
+            tb = Tensor.from_global(rk, IndexTuple(m["db"], m["sb"]), DistParams(1, 1, 0), b)
+            c = contract(ta, tb, m["apos"], m["bpos"])
+            return c.shape(), c.to_global_vector()
+
+        shape, got = World(m["world"]).run(body)[0]
+        assert shape.dims == m["out_dims"] and shape.split == m["out_split"], m
+        assert rel_l2(got, z[f"out{i}"]) < TOL, m
+
+
+def test_matrix_vector_known_answer():
+    # A = [[0,1],[1,0]] bonded to v = [1,0] -> [0,1]
+    def body(rk):
+        a = Tensor.from_global(rk, IndexTuple([2, 2], 0), None, np.array([0, 1, 1, 0], complex))
+        v = Tensor.from_global(rk, IndexTuple([2], 0), None, np.array([1, 0], complex))
+        return contract(a, v, [1], [0]).to_global_vector()
+
+    assert np.array_equal(run_collect(World(1), body), np.array([0, 1], complex))
+
+
+@pytest.mark.parametrize("da,db,ap,bp", [
+    ([3, 2, 5, 2], [5, 3, 4], [0, 2], [1, 0]),
+    ([7, 9, 4], [4, 9], [1, 2], [1, 0]),
+    ([2, 3], [4, 5], [], []),                       # outer product
+    ([6, 5], [5, 6], [0, 1], [1, 0]),               # full contraction -> scalar
+    ([130, 70], [70, 257], [1], [0]),               # GEMM tails in M, N, K
+    ([33, 65, 3], [3, 65, 1], [1, 2], [1, 0]),
+])
+def test_general_contractions(da, db, ap, bp):
+    a = circuits.rng_normals(1, int(np.prod(da)))
+    b = circuits.rng_normals(2, int(np.prod(db)))
+
+    def body(rk):
+        ta = Tensor.from_global(rk, IndexTuple(da, 0), None, a)
+        tb = Tensor.from_global(rk, IndexTuple(db, 0), None, b)
+        return contract(ta, tb, ap, bp).to_global_vector()
+
+    assert rel_l2(run_collect(World(1), body), P.contract(da, a, db, b, ap, bp)) < TOL
+
+
+@pytest.mark.parametrize("rank_a,world,split", [(20, 1, 0), (22, 1, 0), (20, 4, 2), (20, 8, 3), (18, 2, 1)])
+def test_c1_shaped_random_contraction_vs_reference(rank_a, world, split):
+    """Config 1 shape (A rank-r, B rank-14, 7 shared indices at seeded random
+    positions) against the unmodified reference on the same seeded inputs."""
+    if not oracle.ref_available():
+        pytest.skip("reference build absent")
+    R = oracle.ref()
+    seed = 11
+    a = circuits.rng_normals(seed, 2**rank_a)
+    b = circuits.rng_normals(seed + 1, 2**14)
+    ap, bp = circuits.contraction_positions(seed, rank_a, 14, 7)
+    want, wd, ws = R.contract(world, [2] * rank_a, split, (1, 1, 0), a, [2] * 14, 0, (1, 1, 0), b, ap, bp)
+
+    def body(rk):
+        ta = Tensor.from_global(rk, IndexTuple([2] * rank_a, split), DistParams(1, 1, 0), a)
+        tb = Tensor.from_global(rk, IndexTuple([2] * 14, 0), DistParams(1, 1, 0), b)
+        c = contract(ta, tb, ap, bp)
+        return c.shape(), c.to_global_vector()
+
+    shape, got = World(world).run(body)[0]
+    assert shape.dims == wd and shape.split == ws
+    assert rel_l2(got, want) < TOL
+
+
+def test_contracted_distributed_index_is_swapped_local():
+    """A contracted index in a distributed position (one
+    dist<->local swap precedes the GEMM)."""
+    da, db = [2] * 12, [2] * 6
+    a = circuits.rng_normals(5, 2**12)
+    b = circuits.rng_normals(6, 2**6)
+    ap, bp = [0, 5, 9], [2, 0, 4]
+
+    def body(rk):
+        ta = Tensor.from_global(rk, IndexTuple(da, 2), DistParams(1, 1, 0), a)
+        tb = Tensor.from_global(rk, IndexTuple(db, 1), DistParams(1, 1, 2), b)  # b sharded elsewhere
+        c = contract(ta, tb, ap, bp)
+        return c.shape(), c.to_global_vector()
+
+    shape, got = World(4).run(body)[0]
+    assert shape.split == 1  # a's open distributed index (position 1) stays distributed
+    assert rel_l2(got, P.contract(da, a, db, b, ap, bp)) < TOL
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (64, 128, 8), (2**14, 128, 128), (1000, 100, 37), (3, 300, 500),
+                                   (2048, 2048, 64)])
+def test_zgemm_device_against_numpy(m, n, k):
+    import torch
+
+    rng = np.random.default_rng(m + n + k)
+    a = rng.standard_normal((m, k)) + 1j * rng.standard_normal((m, k))
+    b = rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n))
+    ta = torch.from_numpy(a).cuda()
+    tb = torch.from_numpy(b).cuda()
+    tc = torch.empty((m, n), dtype=torch.complex128, device="cuda")
+    w = World(1)
+
+    def body(rk):
+        rk.set_stream(torch.cuda.current_stream().cuda_stream)
+        qtnh.check(qtnh.lib.qtnh_zgemm_device(rk._h, m, n, k, C.c_void_p(ta.data_ptr()),
+                                              C.c_void_p(tb.data_ptr()), C.c_void_p(tc.data_ptr())))
+        torch.cuda.synchronize()
+
+    w.run(body)
+    assert rel_l2(tc.cpu().numpy(), a @ b) < 1e-13

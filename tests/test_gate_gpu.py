@@ -1,0 +1,133 @@
+"""GPU parity of gate application and the QFT workloads (configs 0 and 2)."""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden, rel_l2
+from paper_2505_06119_b200 import circuits
+from paper_2505_06119_b200.qtnh import DistParams, IndexTuple, Tensor, World, apply_gate, ops, run_collect
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+P = oracle.port()
+
+
+def test_gate_golden():
+    meta, z = golden("gate")
+    n = meta["n"]
+    for i, g in enumerate(meta["gates"]):
+        def body(rk):
+            t = Tensor.from_global(rk, IndexTuple([2] * n, 0), None, z["state"])
+            apply_gate(t, g["targets"], z[f"g{i}"])
+            return t.to_global_vector()
+
+        assert rel_l2(run_collect(World(1), body), z[f"out{i}"]) < 1e-14
+    dc = meta["dist_case"]
+
+    def dbody(rk):
+        t = Tensor.from_global(rk, IndexTuple([2] * n, dc["split"]), DistParams(1, 1, 0), z["state"])
+        apply_gate(t, dc["targets"], z[f"g{dc['gate']}"])
+        return t.to_global_vector()
+
+    assert rel_l2(World(dc["world"]).run(dbody)[0], z["out_dist"]) < 1e-14
+
+
+def test_gate_copy_on_write():
+    g = circuits.counter_state(1, 2**6)
+
+    def body(rk):
+        t = Tensor.from_global(rk, IndexTuple([2] * 6, 0), None, g)
+        alias = ops.permute(t, list(range(6)), 0)  # identity permute shares the value
+        apply_gate(alias, [2], circuits.H)
+        return t.to_global_vector(), alias.to_global_vector()
+
+    orig, upd = run_collect(World(1), body)
+    assert np.array_equal(orig, g)
+    assert rel_l2(upd, P.gate([2] * 6, g, [2], circuits.H)) < 1e-14
+
+
+@pytest.mark.parametrize("dims,targets,D", [([2] * 10, [9], 2), ([2] * 10, [0, 9], 4), ([3, 4, 5, 2], [2, 0], 15),
+                                            ([2] * 12, [3, 7, 1], 8), ([2] * 12, [11, 10, 0, 5], 16),
+                                            ([5, 6, 7], [1], 6)])
+def test_dense_gates_general(dims, targets, D):
+    g = circuits.counter_state(3, int(np.prod(dims)))
+    gate = circuits.rng_normals(4, D * D)
+
+    def body(rk):
+        t = Tensor.from_global(rk, IndexTuple(dims, 0), None, g)
+        apply_gate(t, targets, gate)
+        return t.to_global_vector()
+
+    assert rel_l2(run_collect(World(1), body), P.gate(dims, g, targets, gate)) < 1e-14
+
+
+def test_diagonal_gates_on_distributed_targets():
+    n = 12
+    g = circuits.counter_state(8, 2**n)
+    d = circuits.cp_diag(0.7)
+
+    def body(rk):
+        t = Tensor.from_global(rk, IndexTuple([2] * n, 3), DistParams(1, 1, 0), g)
+        apply_gate(t, [1, 7], d, diagonal=True)  # one distributed, one local target
+        apply_gate(t, [0, 2], d, diagonal=True)  # both distributed: scalar per rank
+        return t.to_global_vector()
+
+    want = P.gate([2] * n, P.gate([2] * n, g, [1, 7], d, diagonal=True), [0, 2], d, diagonal=True)
+    assert rel_l2(World(8).run(body)[0], want) < 1e-14
+
+
+def test_qft16_config0_vs_reference():
+    """Config 0: QFT on 16 qubits from a seeded normalised random state, all gates,
+    against the unmodified reference's gate-by-gate contraction path."""
+    n = 16
+    st = circuits.counter_state(2025, 2**n)
+    st /= np.linalg.norm(st)
+
+    def body(rk):
+        t = Tensor.from_global(rk, IndexTuple([2] * n, 0), None, st)
+        return circuits.apply_qft(t, n, swaps=True).to_global_vector()
+
+    got = run_collect(World(1), body)
+    if oracle.ref_available():
+        want = oracle.ref().qft(n, st, swaps=True)
+    else:
+        want = P.qft(n, st, swaps=True)
+    assert rel_l2(got, want) < TOL
+    assert rel_l2(got, np.fft.ifft(st) * np.sqrt(2**n)) < TOL
+
+
+@pytest.mark.parametrize("world,split", [(8, 3), (4, 2), (2, 1)])
+def test_distributed_qft_vs_oracle(world, split):
+    """Config 2 structure at reduced size: the state sharded over `world` ranks by
+    its `split` leading qubits; H on a distributed qubit swaps it with a local one."""
+    n = 14
+    st = circuits.counter_state(7, 2**n)
+    st /= np.linalg.norm(st)
+
+    def body(rk):
+        t = Tensor.from_global(rk, IndexTuple([2] * n, split), DistParams(1, 1, 0), st)
+        return circuits.apply_qft(t, n, swaps=True).to_global_vector()
+
+    got = World(world).run(body)[0]
+    assert rel_l2(got, np.fft.ifft(st) * np.sqrt(2**n)) < TOL
+    assert rel_l2(got, P.qft(n, st)) < TOL
+
+
+def test_qft_norm_preserved_large():
+    """Size-independent property at 2^26 amplitudes: unitarity (norm preserved) and
+    spot amplitudes against a direct O(2^n) DFT sum."""
+    n = 26
+    st = circuits.counter_state(99, 2**n)
+    st /= np.linalg.norm(st)
+
+    def body(rk):
+        t = Tensor.from_global(rk, IndexTuple([2] * n, 0), None, st)
+        return circuits.apply_qft(t, n, swaps=True).local_data()
+
+    got = run_collect(World(1), body)
+    assert abs(np.linalg.norm(got) - 1.0) < 1e-12
+    j = np.arange(2**n, dtype=np.float64)
+    for k in [0, 1, 12345, 2**n - 1]:
+        ph = np.exp(2j * np.pi * ((j * k) % 2**n) / 2**n)
+        want = np.dot(ph, st) / np.sqrt(2**n)
+        assert abs(got[k] - want) < 1e-10 * max(1.0, abs(want))
