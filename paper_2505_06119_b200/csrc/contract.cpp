@@ -159,10 +159,34 @@ TP op_contract(const TP& a_in, const TP& b_in, const std::vector<int>& apos, con
       bp.push_back(q);
       N *= sb.dims[q];
     }
-    std::shared_ptr<DevBuf> ha, hb;
-    const void* A = local_permuted(*a, ald, ap, ha, r);
+    std::shared_ptr<DevBuf> hb;
     const void* B = local_permuted(*b, sb.dims, bp, hb, r);
-    zgemm(A, B, c2->data(), M, N, K, r.stream);
+    if (is_identity(ap)) {
+      zgemm(a->data(), B, c2->data(), M, N, K, r.stream);
+    } else {
+      // Fused layout permutation: A(m, k) = a[rowoff[m] + coloff[k]], read
+      // straight from the tensor's block by the GEMM's operand loads.
+      auto als = row_major_strides(ald);
+      std::vector<Dim> rd, rs, cd, cs;
+      size_t n_open_local = ap.size() - a2_contr.size();
+      for (size_t i = 0; i < ap.size(); ++i) {
+        (i < n_open_local ? rd : cd).push_back(ald[ap[i]]);
+        (i < n_open_local ? rs : cs).push_back(als[ap[i]]);
+      }
+      auto min_stride = [](const std::vector<Dim>& d, const std::vector<Dim>& st) {
+        Dim m = Dim(1) << 62;
+        for (size_t i = 0; i < d.size(); ++i)
+          if (d[i] > 1) m = std::min(m, st[i]);
+        return m;
+      };
+      Dim min_r = min_stride(rd, rs), min_c = min_stride(cd, cs);
+      DevBuf tabs(static_cast<size_t>(M + K) * 8, r);
+      auto* ro = static_cast<int64_t*>(tabs.ptr);
+      auto* co = ro + M;
+      index_offsets(ro, M, rd, rs, r.stream);
+      index_offsets(co, K, cd, cs, r.stream);
+      zgemm_gather_a(a->data(), ro, co, min_r <= min_c, B, c2->data(), M, N, K, r.stream);
+    }
   }
   // 4. Restore the SPEC order / split when a was reshuffled.
   if (a == a_in) return c2;

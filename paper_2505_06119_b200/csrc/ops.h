@@ -30,6 +30,13 @@ void op_gate_apply(TP& t, const std::vector<int>& targets, const double* gate, b
 
 // Kernels (zgemm.cu, gate.cu)
 void zgemm(const void* a, const void* b, void* c, Dim m, Dim n, Dim k, cudaStream_t st);
+// zgemm with A(m, k) gathered from a + rowoff[m] + coloff[k] (elements): the
+// contraction's layout permutation fused into the operand loads.
+void zgemm_gather_a(const void* a, const int64_t* rowoff, const int64_t* coloff, bool rows_fastest,
+                    const void* b, void* c, Dim m, Dim n, Dim k, cudaStream_t st);
+// out[i] = sum_d digit_d(i) * strides[d], digits row-major over dims.
+void index_offsets(int64_t* out, Dim count, const std::vector<Dim>& dims, const std::vector<Dim>& strides,
+                   cudaStream_t st);
 // Gate on a dense local block: dims = local dims, targets = local positions.
 void gate_local(void* data, const std::vector<Dim>& dims, const std::vector<int>& targets,
                 const double* gate_host, bool diagonal, cudaStream_t st);

@@ -4,7 +4,7 @@
 // (linalg.hpp:344-400). tcgen05 has no f64 kind, so the FP64 tensor path on B200
 // is the warp-level DMMA (mma.sync ... f64; every f64 shape lowers to
 // DMMA.8x8x4 in SASS, measured 37.1 TFLOP/s peak on this part -- the same rate
-// as DFMA but 8x fewer issue slots per flop).
+// as DFMA but with 8x fewer issue slots per flop).
 //
 // C = A * B with A (M x K), B (K x N), C (M x N) row-major interleaved complex.
 // 4M formulation on real MMAs, keeping the algorithmic 8MNK flops:
@@ -12,21 +12,22 @@
 // Complex elements stay interleaved in shared memory, so one 16-byte shared load
 // gives a lane both planes of its fragment element.
 //
-// CTA: 256 threads (8 warps) own a BM x BN complex tile (warp tile 32 x 32, 64
-// fp64 accumulators per lane); K is streamed in BK = 8 complex slices through a
-// 4-stage cp.async pipeline (global reads coalesced 128 B per row; A is stored
-// k-major in shared memory with a row pitch = 2 (mod 8) x 16 B so fragment loads
-// are bank-conflict free).
+// Warp tile 32 x 32 complex (64 fp64 accumulators per lane). A CTA of
+// WARPS_M x WARPS_N warps owns a BM x BN tile; K is streamed in BK-complex
+// slices through a STAGES-deep cp.async pipeline (global reads coalesced along
+// K for A and along N for B; A is stored k-major in shared memory with a row
+// pitch = 2 (mod 8) x 16 B so fragment loads are bank-conflict free). Several
+// CTAs per SM overlap one tile's prologue/epilogue with another's DMMA stream --
+// with one CTA per SM those phases idle the tensor pipe for ~15% of the time.
 #include <algorithm>
+#include <cstdlib>
+#include <vector>
 
 #include "ops.h"
 
 namespace qtnhb {
 
 namespace {
-
-constexpr int kBK = 8;
-constexpr int kStages = 4;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -40,58 +41,96 @@ __device__ __forceinline__ void cp_wait() {
 }
 
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
 
-template <int BM, int BN>
-struct Smem {
+template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int BK_, int STAGES_, int MINB_>
+struct Cfg {
+  static constexpr int BM = BM_, BN = BN_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, BK = BK_,
+                       STAGES = STAGES_, MINB = MINB_;
+  static constexpr int THREADS = WARPS_M * WARPS_N * 32;
   static constexpr int PA = BM + 2;  // 16-B elements; = 2 (mod 8)
   static constexpr int PB = BN + 2;
-  static constexpr int A_ELEMS = kBK * PA;
-  static constexpr int B_ELEMS = kBK * PB;
-  static constexpr size_t bytes = static_cast<size_t>(kStages) * (A_ELEMS + B_ELEMS) * 16;
+  static constexpr int A_ELEMS = BK * PA;
+  static constexpr int B_ELEMS = BK * PB;
+  static constexpr size_t SMEM = static_cast<size_t>(STAGES) * (A_ELEMS + B_ELEMS) * 16;
+  static_assert(BM == WARPS_M * 32 && BN == WARPS_N * 32, "warp tile is 32 x 32");
+  static_assert((BM * BK) % THREADS == 0 && (BN * BK) % THREADS == 0, "even load split");
 };
 
-template <int BM, int BN>
-__global__ void __launch_bounds__(256, 1) k_zgemm(const double2* __restrict__ A,
-                                                  const double2* __restrict__ B,
-                                                  double2* __restrict__ C, int64_t M, int64_t N,
-                                                  int64_t K) {
-  constexpr int WM = 32, WN = 32;
-  constexpr int WARPS_N = BN / WN;
-  static_assert((BM / WM) * (BN / WN) == 8, "8 warps");
-  using S = Smem<BM, BN>;
+// MODE 0: A dense row-major (M x K).
+// MODE 1/2: A gathered: element (m, k) at A + rowoff[m] + coloff[k] -- the layout
+// permutation of the contraction fused into the operand loads (no permuted copy
+// of A in HBM). MODE 1 walks consecutive rows with consecutive threads (the
+// tensor's innermost index is open), MODE 2 consecutive k (innermost contracted).
+template <class G, int MODE>
+__global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __restrict__ A,
+                                                               const int64_t* __restrict__ rowoff,
+                                                               const int64_t* __restrict__ coloff,
+                                                               const double2* __restrict__ B,
+                                                               double2* __restrict__ C, int64_t M,
+                                                               int64_t N, int64_t K) {
+  constexpr int BM = G::BM, BN = G::BN, BK = G::BK, STAGES = G::STAGES, T = G::THREADS;
   extern __shared__ __align__(16) double2 smem[];
   double2* As = smem;                          // [stage][k][PA]
-  double2* Bs = smem + kStages * S::A_ELEMS;   // [stage][k][PB]
+  double2* Bs = smem + STAGES * G::A_ELEMS;    // [stage][k][PB]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+  const int wm = warp / G::WARPS_N, wn = warp % G::WARPS_N;
   const int64_t bm = static_cast<int64_t>(blockIdx.y) * BM;
   const int64_t bn = static_cast<int64_t>(blockIdx.x) * BN;
-  const int64_t n_kt = (K + kBK - 1) / kBK;
+  const int64_t n_kt = (K + BK - 1) / BK;
 
-  auto load_stage = [&](int stage, int64_t kt) {
-    int64_t k0 = kt * kBK;
-    double2* as = As + stage * S::A_ELEMS;
-    double2* bs = Bs + stage * S::B_ELEMS;
+  // Per-thread source rows / columns are fixed; only k advances by BK per stage.
+  constexpr int LA = (BM * BK) / T, LB = (BN * BK) / T;
+  const double2* pa[LA];
+  const double2* pb[LB];
+  int sa[LA], sb[LB], ka[LA], kb[LB];
+  bool ma[LA], nbok[LB];
+  // MODE 1 with T % BM == 0: every load of a thread hits the same row.
+  constexpr bool kRowFixed = MODE == 1 && (T % BM) == 0;
 #pragma unroll
-    for (int u = 0; u < (BM * kBK) / 256; ++u) {
-      int e = tid + u * 256;
-      int m = e / kBK, k = e % kBK;
-      int64_t gm = bm + m, gk = k0 + k;
-      bool ok = gm < M && gk < K;
-      cp_async16(as + k * S::PA + m, ok ? (A + gm * K + gk) : A, ok);
+  for (int u = 0; u < LA; ++u) {
+    int e = tid + u * T;
+    int m = MODE == 1 ? e % BM : e / BK;
+    int k = MODE == 1 ? e / BM : e % BK;
+    ka[u] = k;
+    sa[u] = k * G::PA + m;
+    if (kRowFixed && u > 0) {
+      ma[u] = ma[0];
+      pa[u] = pa[0];
+      continue;
+    }
+    ma[u] = bm + m < M;
+    if (MODE == 0) pa[u] = A + (ma[u] ? (bm + m) : 0) * K + k;
+    else pa[u] = A + (ma[u] ? __ldg(rowoff + bm + m) : 0);
+  }
+#pragma unroll
+  for (int u = 0; u < LB; ++u) {
+    int e = tid + u * T;
+    int k = e / BN, n = e % BN;
+    nbok[u] = bn + n < N;
+    kb[u] = k;
+    pb[u] = B + static_cast<int64_t>(k) * N + (nbok[u] ? bn + n : 0);
+    sb[u] = k * G::PB + n;
+  }
+  auto load_stage = [&](int stage, int64_t kt) {
+    int64_t k0 = kt * BK;
+    double2* as = As + stage * G::A_ELEMS;
+    double2* bs = Bs + stage * G::B_ELEMS;
+#pragma unroll
+    for (int u = 0; u < LA; ++u) {
+      bool ok = ma[u] && k0 + ka[u] < K;
+      const double2* src = A;
+      if (ok) src = MODE == 0 ? pa[u] + k0 : pa[u] + __ldg(coloff + k0 + ka[u]);
+      cp_async16(as + sa[u], src, ok);
     }
 #pragma unroll
-    for (int u = 0; u < (BN * kBK) / 256; ++u) {
-      int e = tid + u * 256;
-      int k = e / BN, n = e % BN;
-      int64_t gk = k0 + k, gn = bn + n;
-      bool ok = gk < K && gn < N;
-      cp_async16(bs + k * S::PB + n, ok ? (B + gk * N + gn) : B, ok);
+    for (int u = 0; u < LB; ++u) {
+      bool ok = nbok[u] && k0 + kb[u] < K;
+      cp_async16(bs + sb[u], ok ? pb[u] + k0 * N : B, ok);
     }
   };
 
@@ -105,35 +144,29 @@ __global__ void __launch_bounds__(256, 1) k_zgemm(const double2* __restrict__ A,
     }
 
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) {
+  for (int s = 0; s < STAGES - 1; ++s) {
     if (s < n_kt) load_stage(s, s);
     cp_commit();
   }
 
   const int fr = lane >> 2, fk = lane & 3;
   for (int64_t kt = 0; kt < n_kt; ++kt) {
-    cp_wait<kStages - 2>();
+    cp_wait<STAGES - 2>();
     __syncthreads();
-    // Prefetch the slice kStages-1 ahead into the slot freed last iteration.
-    {
-      int64_t nk = kt + kStages - 1;
-      if (nk < n_kt) load_stage(static_cast<int>(nk % kStages), nk);
-      cp_commit();
-    }
-    const double2* as = As + (kt % kStages) * S::A_ELEMS;
-    const double2* bs = Bs + (kt % kStages) * S::B_ELEMS;
+    const double2* as = As + (kt % STAGES) * G::A_ELEMS + wm * 32 + fr;
+    const double2* bs = Bs + (kt % STAGES) * G::B_ELEMS + wn * 32 + fr;
 #pragma unroll
-    for (int k4 = 0; k4 < kBK; k4 += 4) {
+    for (int k4 = 0; k4 < BK; k4 += 4) {
       double a_re[4], a_im[4], b_re[4], b_im[4], nb_im[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        double2 v = as[(k4 + fk) * S::PA + wm * WM + i * 8 + fr];
+        double2 v = as[(k4 + fk) * G::PA + i * 8];
         a_re[i] = v.x;
         a_im[i] = v.y;
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        double2 v = bs[(k4 + fk) * S::PB + wn * WN + j * 8 + fr];
+        double2 v = bs[(k4 + fk) * G::PB + j * 8];
         b_re[j] = v.x;
         b_im[j] = v.y;
         nb_im[j] = -v.y;
@@ -144,9 +177,22 @@ __global__ void __launch_bounds__(256, 1) k_zgemm(const double2* __restrict__ A,
         for (int j = 0; j < 4; ++j) {
           dmma(acc_re[i][j], a_re[i], b_re[j]);
           dmma(acc_im[i][j], a_re[i], b_im[j]);
+        }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
           dmma(acc_re[i][j], a_im[i], nb_im[j]);
           dmma(acc_im[i][j], a_im[i], b_re[j]);
         }
+    }
+    // Refill the slot freed at the top barrier only after this slice's DMMAs are
+    // queued: the (gather-table) address loads then stall the warp while the
+    // tensor pipe is busy, not before it is fed.
+    {
+      int64_t nk = kt + STAGES - 1;
+      if (nk < n_kt) load_stage(static_cast<int>(nk % STAGES), nk);
+      cp_commit();
     }
   }
   cp_wait<0>();
@@ -154,37 +200,123 @@ __global__ void __launch_bounds__(256, 1) k_zgemm(const double2* __restrict__ A,
   // Epilogue: lane holds C[fr][2*fk + {0,1}] of each 8x8 sub-tile.
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    int64_t row = bm + wm * WM + i * 8 + fr;
+    int64_t row = bm + wm * 32 + i * 8 + fr;
     if (row >= M) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      int64_t col = bn + wn * WN + j * 8 + 2 * fk;
+      int64_t col = bn + wn * 32 + j * 8 + 2 * fk;
       double2* dst = C + row * N + col;
-      if (col < N) dst[0] = make_double2(acc_re[i][j][0], acc_im[i][j][0]);
-      if (col + 1 < N) dst[1] = make_double2(acc_re[i][j][1], acc_im[i][j][1]);
+      if (col + 1 < N) {
+        dst[0] = make_double2(acc_re[i][j][0], acc_im[i][j][0]);
+        dst[1] = make_double2(acc_re[i][j][1], acc_im[i][j][1]);
+      } else if (col < N) {
+        dst[0] = make_double2(acc_re[i][j][0], acc_im[i][j][0]);
+      }
     }
   }
 }
 
-template <int BM, int BN>
-void launch(const double2* a, const double2* b, double2* c, Dim m, Dim n, Dim k, cudaStream_t st) {
-  size_t smem = Smem<BM, BN>::bytes;
-  QTNH_CUDA(cudaFuncSetAttribute(k_zgemm<BM, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid(static_cast<unsigned>((n + BN - 1) / BN), static_cast<unsigned>((m + BM - 1) / BM));
-  if (grid.y > 65535u) {
-    // Split along M into chunks the grid can address.
-    Dim rows = static_cast<Dim>(65535) * BM;
-    for (Dim m0 = 0; m0 < m; m0 += rows) {
-      Dim mm = std::min(rows, m - m0);
-      launch<BM, BN>(a + m0 * k, b, c + m0 * n, mm, n, k, st);
-    }
-    return;
+template <class G, int MODE>
+void launch_mode(const double2* a, const int64_t* ro, const int64_t* co, const double2* b, double2* c, Dim m,
+                 Dim n, Dim k, cudaStream_t st) {
+  QTNH_CUDA(cudaFuncSetAttribute(k_zgemm<G, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+  Dim rows = static_cast<Dim>(65535) * G::BM;
+  for (Dim m0 = 0; m0 < m; m0 += rows) {  // grid.y limit
+    Dim mm = std::min(rows, m - m0);
+    dim3 grid(static_cast<unsigned>((n + G::BN - 1) / G::BN), static_cast<unsigned>((mm + G::BM - 1) / G::BM));
+    const double2* am = MODE == 0 ? a + m0 * k : a;
+    const int64_t* rom = MODE == 0 ? ro : ro + m0;
+    k_zgemm<G, MODE><<<grid, G::THREADS, G::SMEM, st>>>(am, rom, co, b, c + m0 * n, mm, n, k);
+    QTNH_LAUNCH_CHECK();
   }
-  k_zgemm<BM, BN><<<grid, 256, smem, st>>>(a, b, c, m, n, k);
-  QTNH_LAUNCH_CHECK();
+}
+
+template <class G>
+void launch(const double2* a, const double2* b, double2* c, Dim m, Dim n, Dim k, cudaStream_t st) {
+  launch_mode<G, 0>(a, nullptr, nullptr, b, c, m, n, k, st);
+}
+
+struct MixedRadix {
+  int nd;
+  int64_t dims[64];
+  int64_t strides[64];
+};
+
+__global__ void k_mixed_offsets(int64_t* __restrict__ out, int64_t count, const __grid_constant__ MixedRadix mr) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i, off = 0;
+    for (int d = mr.nd - 1; d >= 0; --d) {
+      int64_t c = r % mr.dims[d];
+      r /= mr.dims[d];
+      off += c * mr.strides[d];
+    }
+    out[i] = off;
+  }
+}
+
+// Tuning variants (QTNH_ZGEMM_VARIANT selects one for experiments).
+using V0 = Cfg<64, 128, 2, 4, 8, 4, 1>;   // 256 thr, 1 CTA/SM
+using V1 = Cfg<64, 64, 2, 2, 8, 4, 2>;    // 128 thr, 2 CTA/SM
+using V2 = Cfg<64, 64, 2, 2, 16, 3, 2>;   // 128 thr, 2 CTA/SM, BK 16
+using V3 = Cfg<32, 64, 1, 2, 8, 4, 4>;    // 64 thr, 4 CTA/SM
+using V4 = Cfg<64, 32, 2, 1, 8, 4, 4>;    // 64 thr, 4 CTA/SM
+using V5 = Cfg<32, 32, 1, 1, 16, 4, 6>;   // 32 thr, 6 CTA/SM
+using V6 = Cfg<64, 64, 2, 2, 8, 6, 2>;    // deeper pipeline
+using V7 = Cfg<32, 64, 1, 2, 8, 3, 5>;    // 64 thr, 5 CTA/SM (<= 204 regs)
+using V8 = Cfg<32, 128, 1, 4, 8, 4, 2>;   // 128 thr, 2 CTA/SM
+using V9 = Cfg<32, 64, 1, 2, 16, 3, 4>;   // 64 thr, BK 16
+
+int variant() {
+  static int v = [] {
+    const char* e = std::getenv("QTNH_ZGEMM_VARIANT");
+    return e ? std::atoi(e) : -1;
+  }();
+  return v;
 }
 
 }  // namespace
+
+void index_offsets(int64_t* out, Dim count, const std::vector<Dim>& dims, const std::vector<Dim>& strides,
+                   cudaStream_t st) {
+  if (count <= 0) return;
+  MixedRadix mr{};
+  mr.nd = static_cast<int>(dims.size());
+  if (mr.nd > 64) throw_invalid("too many indices for an offset table");
+  for (int i = 0; i < mr.nd; ++i) {
+    mr.dims[i] = dims[i];
+    mr.strides[i] = strides[i];
+  }
+  int grid = static_cast<int>(std::min<Dim>((count + 255) / 256, 148 * 8));
+  k_mixed_offsets<<<grid, 256, 0, st>>>(out, count, mr);
+  QTNH_LAUNCH_CHECK();
+}
+
+void zgemm_gather_a(const void* a, const int64_t* rowoff, const int64_t* coloff, bool rows_fastest,
+                    const void* b, void* c, Dim m, Dim n, Dim k, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return;
+  if (k <= 0) {
+    QTNH_CUDA(cudaMemsetAsync(c, 0, static_cast<size_t>(m * n) * 16, st));
+    return;
+  }
+  auto A = static_cast<const double2*>(a);
+  auto B = static_cast<const double2*>(b);
+  auto Cp = static_cast<double2*>(c);
+  static int gv = [] {
+    const char* e = std::getenv("QTNH_ZGEMM_GATHER_VARIANT");
+    return e ? std::atoi(e) : 7;
+  }();
+  if (n > 32 && gv == 7) {
+    if (rows_fastest) launch_mode<V7, 1>(A, rowoff, coloff, B, Cp, m, n, k, st);
+    else launch_mode<V7, 2>(A, rowoff, coloff, B, Cp, m, n, k, st);
+  } else if (n > 32) {
+    if (rows_fastest) launch_mode<V3, 1>(A, rowoff, coloff, B, Cp, m, n, k, st);
+    else launch_mode<V3, 2>(A, rowoff, coloff, B, Cp, m, n, k, st);
+  } else {
+    if (rows_fastest) launch_mode<V4, 1>(A, rowoff, coloff, B, Cp, m, n, k, st);
+    else launch_mode<V4, 2>(A, rowoff, coloff, B, Cp, m, n, k, st);
+  }
+}
 
 void zgemm(const void* a, const void* b, void* c, Dim m, Dim n, Dim k, cudaStream_t st) {
   if (m <= 0 || n <= 0) return;
@@ -195,9 +327,21 @@ void zgemm(const void* a, const void* b, void* c, Dim m, Dim n, Dim k, cudaStrea
     QTNH_CUDA(cudaMemsetAsync(c, 0, static_cast<size_t>(m * n) * 16, st));
     return;
   }
-  if (n > 64) launch<64, 128>(A, B, Cp, m, n, k, st);
-  else if (n > 32) launch<128, 64>(A, B, Cp, m, n, k, st);
-  else launch<256, 32>(A, B, Cp, m, n, k, st);
+  switch (variant()) {
+    case 0: return launch<V0>(A, B, Cp, m, n, k, st);
+    case 1: return launch<V1>(A, B, Cp, m, n, k, st);
+    case 2: return launch<V2>(A, B, Cp, m, n, k, st);
+    case 3: return launch<V3>(A, B, Cp, m, n, k, st);
+    case 4: return launch<V4>(A, B, Cp, m, n, k, st);
+    case 5: return launch<V5>(A, B, Cp, m, n, k, st);
+    case 6: return launch<V6>(A, B, Cp, m, n, k, st);
+    case 7: return launch<V7>(A, B, Cp, m, n, k, st);
+    case 8: return launch<V8>(A, B, Cp, m, n, k, st);
+    case 9: return launch<V9>(A, B, Cp, m, n, k, st);
+    default: break;
+  }
+  if (n > 32) launch<V7>(A, B, Cp, m, n, k, st);
+  else launch<V4>(A, B, Cp, m, n, k, st);
 }
 
 }  // namespace qtnhb
