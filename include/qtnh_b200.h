@@ -179,6 +179,14 @@ void qtnh_counter_complex_normals(uint64_t seed, int64_t start, int64_t count, d
 /* Same stream generated on the device (CUDA log/sincos: ~1 ulp from glibc). */
 int qtnh_counter_complex_normals_device(void* stream, uint64_t seed, int64_t start, int64_t count, void* out);
 
+/* ---- host-only planning ----------------------------------------------------- */
+/* The exchange plan of rank `rank` (of `world_size`) for ops::permute(t, perm,
+ * new_split) followed by a move to `new_dist` (NULL: keep t's dist), as JSON:
+ * pack box, send/recv lists (peer, element offset, count), unpack box. No device
+ * state is touched -- this is what the multi-process CPU tests execute. */
+int qtnh_remap_plan_json(int n_idx, const int64_t* dims, int split, const int64_t* dist, const int* perm,
+                         int new_split, const int64_t* new_dist, int rank, int world_size, char* buf, size_t len);
+
 /* ---- raw kernels on device buffers (bench / integration) ------------------ */
 /* out = a(M x K) * b(K x N), row-major complex128 on the rank's stream. */
 int qtnh_zgemm_device(qtnh_rank_t r, int64_t m, int64_t n, int64_t k, const void* a,

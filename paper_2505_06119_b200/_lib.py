@@ -80,6 +80,7 @@ _SIGS = {
     "qtnh_counter_complex_normals": (None, [C.c_uint64, i64, i64, vp, i32]),
     "qtnh_counter_complex_normals_device": (i32, [vp, C.c_uint64, i64, i64, vp]),
     "qtnh_probe_fp64_peak": (i32, [vp, P_f64]),
+    "qtnh_remap_plan_json": (i32, [i32, P_i64, i32, P_i64, P_i32, i32, P_i64, i32, i32, C.c_char_p, sz]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -484,6 +484,51 @@ int qtnh_svd_device(qtnh_rank_t r, int64_t batch, int64_t m, int64_t n, const vo
   });
 }
 
+int qtnh_remap_plan_json(int n, const int64_t* dims, int split, const int64_t* dist, const int* perm,
+                         int new_split, const int64_t* new_dist, int rank, int world_size, char* buf, size_t len) {
+  return guard([&] {
+    need(buf, "buf");
+    Shape ss = shape_from(n, dims, split);
+    std::vector<int> pv(perm, perm + n), inv(n, -1);
+    for (int p = 0; p < n; ++p) {
+      if (pv[p] < 0 || pv[p] >= n || inv[pv[p]] != -1) throw_invalid("invalid index permutation");
+      inv[pv[p]] = p;
+    }
+    std::vector<Dim> nd(n);
+    for (int p = 0; p < n; ++p) nd[p] = ss.dims[pv[p]];
+    Dist sd = dist_from(dist), dd = new_dist ? dist_from(new_dist) : sd;
+    RemapPlan P = plan_remap(ss, sd, Shape(nd, new_split), dd, inv, rank, world_size);
+    auto vec = [](const std::vector<Dim>& v) {
+      std::string s = "[";
+      for (size_t i = 0; i < v.size(); ++i) s += (i ? "," : "") + std::to_string(v[i]);
+      return s + "]";
+    };
+    auto box = [&](const CopyBox& b) {
+      return "{\"dims\":" + vec(b.dims) + ",\"in_stride\":" + vec(b.in_stride) + ",\"out_stride\":" +
+             vec(b.out_stride) + "}";
+    };
+    auto xf = [](const std::vector<Xfer>& v) {
+      std::string s = "[";
+      for (size_t i = 0; i < v.size(); ++i)
+        s += (i ? "," : "") + std::string("[") + std::to_string(v[i].peer) + "," + std::to_string(v[i].offset) +
+             "," + std::to_string(v[i].count) + "]";
+      return s + "]";
+    };
+    std::vector<Dim> mem(P.members.begin(), P.members.end());
+    std::string j = "{\"members\":" + vec(mem) + ",\"member\":" + std::to_string(P.member) +
+                    ",\"local_only\":" + std::to_string(P.local_only) + ",\"direct_layout\":" +
+                    std::to_string(P.direct_layout) + ",\"src_canonical\":" + std::to_string(P.src_canonical) +
+                    ",\"dst_in_span\":" + std::to_string(P.dst_in_span) + ",\"pack_to_dst\":" +
+                    std::to_string(P.pack_to_dst) + ",\"recv_into_dst\":" + std::to_string(P.recv_into_dst) +
+                    ",\"unpack\":" + std::to_string(P.unpack) + ",\"pack\":" + box(P.pack) +
+                    ",\"unpack_box\":" + box(P.unpack_box) + ",\"pack_elems\":" + std::to_string(P.pack_elems) +
+                    ",\"recv_elems\":" + std::to_string(P.recv_elems) + ",\"sends\":" + xf(P.sends) +
+                    ",\"recvs\":" + xf(P.recvs) + "}";
+    if (j.size() + 1 > len) throw_invalid("plan buffer too small: need " + std::to_string(j.size() + 1));
+    std::memcpy(buf, j.c_str(), j.size() + 1);
+  });
+}
+
 int qtnh_zgemm_device(qtnh_rank_t r, int64_t m, int64_t n, int64_t k, const void* a, const void* b, void* c) {
   return guard([&] {
     RankCtx& x = ctx_of(r);

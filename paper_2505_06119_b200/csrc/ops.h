@@ -5,10 +5,26 @@
 #include <vector>
 
 #include "runtime.h"
+#include "strided_copy.h"
 
 namespace qtnhb {
 
 using TP = std::shared_ptr<TensorImpl>;
+
+// Host-only plan of one rank's part of a redistribution (no device state): the
+// pack box, the exchange lists and the unpack box. Shared by the device executor
+// (remap) and the CPU executor of the multi-process tests.
+struct RemapPlan {
+  std::vector<int> members;
+  bool member = false, local_only = false, direct_layout = false;
+  bool src_canonical = false, dst_in_span = false;
+  bool pack_to_dst = false, recv_into_dst = false, unpack = false;
+  CopyBox pack, unpack_box;
+  Dim pack_elems = 0, recv_elems = 0;
+  std::vector<Xfer> sends, recvs;
+};
+RemapPlan plan_remap(const Shape& ss, const Dist& sd, const Shape& ds, const Dist& dd, const std::vector<int>& am,
+                     int rank, int world_size);
 
 // remap::tensor_to_tensor (remap.hpp:106-161) restricted to equal dimensions:
 // axis_map[src_pos] = dst_pos.

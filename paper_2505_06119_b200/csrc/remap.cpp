@@ -22,15 +22,6 @@ namespace qtnhb {
 
 namespace {
 
-struct RemapPlan {
-  // index classes (src positions), see file header of DESIGN.md section "remap"
-  std::vector<int> V;  // src-local -> dst-dist   (ordered by dst position)
-  std::vector<int> W;  // src-local -> dst-local  (ordered by dst position)
-  std::vector<int> F;  // src-dist  -> dst-local  (ordered by src position)
-  std::vector<int> G;  // src-dist  -> dst-dist
-  Dim nV = 1, szW = 1, nF = 1;
-};
-
 Dim prod_dims(const std::vector<Dim>& dims, const std::vector<int>& idx) {
   Dim p = 1;
   for (int i : idx) p *= dims[i];
@@ -39,69 +30,64 @@ Dim prod_dims(const std::vector<Dim>& dims, const std::vector<int>& idx) {
 
 }  // namespace
 
-TP remap(const TP& src, Shape ds, Dist dd, const std::vector<int>& am) {
-  const Shape& ss = src->shape;
+// Index classes (src positions) of a remap:
+//   V src-local -> dst-dist   (ordered by dst position): chunk index
+//   W src-local -> dst-local  (ordered by dst position): chunk payload
+//   F src-dist  -> dst-local  (ordered by src position): chunk placement
+//   G src-dist  -> dst-dist: routing only
+RemapPlan plan_remap(const Shape& ss, const Dist& sd, const Shape& ds, const Dist& dd, const std::vector<int>& am,
+                     int rank, int world_size) {
   int n = ss.n_idx();
   if (static_cast<int>(am.size()) != n) throw_invalid("axis map size does not match tensor rank");
-  std::vector<int> inv(ds.n_idx(), -1);
+  if (ds.n_idx() != n) throw_invalid("axis map is not a bijection");
+  std::vector<int> inv(n, -1);
   for (int i = 0; i < n; ++i) {
     int p = am[i];
-    if (p < 0 || p >= ds.n_idx() || inv[p] != -1) throw_invalid("axis map is not a bijection");
+    if (p < 0 || p >= n || inv[p] != -1) throw_invalid("axis map is not a bijection");
     inv[p] = i;
     if (ds.dims[p] != ss.dims[i]) throw_invalid("remap needs equal mapped dimensions");
   }
-  if (ds.n_idx() != n) throw_invalid("axis map is not a bijection");
-  RankCtx& r = *src->rank;
-  TP dst = make_tensor(r, ds, dd, true);
-  auto members = union_members({{src->dist.offset, src->span()}, {dd.offset, dst->span()}});
-  if (!std::binary_search(members.begin(), members.end(), r.rank)) return dst;
+  Dim need = dd.offset + dd.span(ds.dist_size());
+  if (need > world_size) throw_resource("tensor span exceeds world size", need);
+  RemapPlan R;
+  Dim src_nd = ss.dist_size(), dst_nd = ds.dist_size();
+  R.members = union_members({{sd.offset, sd.span(src_nd)}, {dd.offset, dd.span(dst_nd)}});
+  R.member = std::binary_search(R.members.begin(), R.members.end(), rank);
+  Dim blk = 0, cyc = 0, slot = 0;
+  R.src_canonical = sd.locate(rank, src_nd, &blk, &cyc, &slot) && cyc == 0 && slot == 0;
+  Dim src_block = blk;
+  Dim dblk = 0, dcyc = 0, dslot = 0;
+  R.dst_in_span = dd.locate(rank, dst_nd, &dblk, &dcyc, &dslot);
+  Dim dst_block = dblk;
+  if (!R.member) return R;
 
-  RemapPlan P;
+  std::vector<int> V, W, F;
   for (int p = 0; p < n; ++p) {
     int q = inv[p];
     bool sdist = q < ss.split, ddist = p < ds.split;
-    if (!sdist && ddist) P.V.push_back(q);
-    if (!sdist && !ddist) P.W.push_back(q);
-    if (sdist && !ddist) P.F.push_back(q);
-    if (sdist && ddist) P.G.push_back(q);
+    if (!sdist && ddist) V.push_back(q);
+    if (!sdist && !ddist) W.push_back(q);
+    if (sdist && !ddist) F.push_back(q);
   }
-  std::sort(P.F.begin(), P.F.end());
-  P.nV = prod_dims(ss.dims, P.V);
-  P.szW = prod_dims(ss.dims, P.W);
-  P.nF = prod_dims(ss.dims, P.F);
-
-  const Dim src_nd = ss.dist_size(), dst_nd = ds.dist_size();
+  std::sort(F.begin(), F.end());
+  const Dim nV = prod_dims(ss.dims, V), szW = prod_dims(ss.dims, W);
   auto sdd = ss.dist_dims(), ddd = ds.dist_dims();
   auto dst_local_strides = row_major_strides(ds.local_dims());
   auto src_local_strides = row_major_strides(ss.local_dims());
-  // dst local stride of a src index q that lands at a dst-local position
   auto dls = [&](int q) { return dst_local_strides[am[q] - ds.split]; };
-
-  // dst block of src block bs, chunk v (row-major over V)
-  auto dst_block = [&](Dim bs, Dim v) {
+  std::vector<Dim> vdims;
+  for (int q : V) vdims.push_back(ss.dims[q]);
+  // destination block of source block bs, chunk v (row-major over V)
+  auto dst_block_of = [&](Dim bs, Dim v) {
     auto cs = unflat(bs, sdd);
-    std::vector<Dim> vd;
-    for (int q : P.V) vd.push_back(ss.dims[q]);
-    auto cv = unflat(v, vd);
+    auto cv = unflat(v, vdims);
     std::vector<Dim> cd(ds.split);
     for (int p = 0; p < ds.split; ++p) {
       int q = inv[p];
-      if (q < ss.split) cd[p] = cs[q];
-      else cd[p] = cv[std::find(P.V.begin(), P.V.end(), q) - P.V.begin()];
+      cd[p] = q < ss.split ? cs[q] : cv[std::find(V.begin(), V.end(), q) - V.begin()];
     }
     return flat(cd, ddd);
   };
-
-  // Is any element moving between ranks (or copies needed)? Same answer on all members.
-  bool local_only = P.V.empty() && P.F.empty() && dd.stretch * dd.cycles == 1;
-  if (local_only) {
-    for (Dim bs = 0; bs < src_nd && local_only; ++bs)
-      if (src->dist.canonical(bs) != dd.canonical(dst_block(bs, 0))) local_only = false;
-  }
-
-  cudaStream_t st = r.stream;
-  bool direct_layout = P.V.empty() && P.F.empty();  // pack layout == dst layout
-  // Pack box over my local (src-local) indices.
   auto pack_box = [&](bool to_dst_layout) {
     CopyBox b;
     for (int q = ss.split; q < n; ++q) {
@@ -112,114 +98,122 @@ TP remap(const TP& src, Shape ds, Dist dd, const std::vector<int>& am) {
     if (to_dst_layout) {
       for (int q = ss.split; q < n; ++q) b.out_stride[q - ss.split] = dls(q);
     } else {
-      Dim s = 1;
-      for (int k = static_cast<int>(P.W.size()) - 1; k >= 0; --k) {
-        b.out_stride[P.W[k] - ss.split] = s;
-        s *= ss.dims[P.W[k]];
+      Dim st = 1;
+      for (int k = static_cast<int>(W.size()) - 1; k >= 0; --k) {
+        b.out_stride[W[k] - ss.split] = st;
+        st *= ss.dims[W[k]];
       }
-      for (int k = static_cast<int>(P.V.size()) - 1; k >= 0; --k) {
-        b.out_stride[P.V[k] - ss.split] = s;
-        s *= ss.dims[P.V[k]];
+      for (int k = static_cast<int>(V.size()) - 1; k >= 0; --k) {
+        b.out_stride[V[k] - ss.split] = st;
+        st *= ss.dims[V[k]];
       }
     }
     return b;
   };
 
-  if (local_only) {
-    if (src->canonical() && dst->in_span) strided_copy(src->data(), dst->data(), pack_box(true), true, st);
-    return dst;
+  // No element changes rank and there are no broadcast copies to feed: a plain
+  // local permutation on every canonical holder. Same answer on all members.
+  R.direct_layout = V.empty() && F.empty();
+  R.local_only = R.direct_layout && dd.stretch * dd.cycles == 1;
+  for (Dim bs = 0; bs < src_nd && R.local_only; ++bs)
+    if (sd.canonical(bs) != dd.canonical(dst_block_of(bs, 0))) R.local_only = false;
+  if (R.local_only) {
+    R.pack_to_dst = true;
+    R.pack = pack_box(true);
+    return R;
   }
-
-  // ---- general path: sends ------------------------------------------------------
-  std::vector<Xfer> sends, recvs;
-  std::shared_ptr<DevBuf> packbuf, recvbuf;
-  const void* send_ptr = nullptr;
-  void* recv_ptr = nullptr;
-  bool sent_into_dst = false;
-  if (src->canonical()) {
-    bool self_home_direct = false;
-    if (direct_layout && dst->in_span && dst->block == dst_block(src->block, 0)) self_home_direct = true;
-    if (self_home_direct) {
-      strided_copy(src->data(), dst->data(), pack_box(true), true, st);
-      send_ptr = dst->data();
-      sent_into_dst = true;
-    } else {
-      packbuf = std::make_shared<DevBuf>(static_cast<size_t>(P.nV * P.szW) * 16, r);
-      strided_copy(src->data(), packbuf->ptr, pack_box(direct_layout), true, st);
-      send_ptr = packbuf->ptr;
-    }
-    for (Dim v = 0; v < P.nV; ++v) {
-      Dim bd = dst_block(src->block, v);
-      for (int h : dd.homes(bd, dst_nd)) {
-        if (sent_into_dst && h == r.rank) continue;
-        sends.push_back({h, v * P.szW, P.szW});
+  // ---- sends ------------------------------------------------------------------------
+  if (R.src_canonical) {
+    R.pack_to_dst = R.direct_layout && R.dst_in_span && dst_block == dst_block_of(src_block, 0);
+    R.pack = pack_box(R.direct_layout);
+    R.pack_elems = nV * szW;
+    for (Dim v = 0; v < nV; ++v)
+      for (int h : dd.homes(dst_block_of(src_block, v), dst_nd)) {
+        if (R.pack_to_dst && h == rank) continue;
+        R.sends.push_back({h, v * szW, szW});
       }
-    }
   }
-  // ---- receives -----------------------------------------------------------------
-  // Sources: src blocks agreeing with my dst dist coords on G; enumerated row-major
-  // over the src dist dims, i.e. row-major over F (src order).
-  std::vector<Dim> src_blocks;
-  if (dst->in_span) {
-    auto cd = unflat(dst->block, ddd);
+  // ---- receives: every source block agreeing with my dst coords on G, row-major
+  // over the src dist dims = row-major over F (src order) --------------------------------
+  if (R.dst_in_span) {
+    auto cd = unflat(dst_block, ddd);
+    Dim off = 0;
     for (Dim bs = 0; bs < src_nd; ++bs) {
       auto cs = unflat(bs, sdd);
       bool ok = true;
       for (int p = 0; p < ds.split && ok; ++p)
         if (inv[p] < ss.split && cs[inv[p]] != cd[p]) ok = false;
-      if (ok) src_blocks.push_back(bs);
+      if (!ok) continue;
+      int from = sd.canonical(bs);
+      if (R.pack_to_dst && from == rank) continue;
+      R.recvs.push_back({from, off, szW});
+      off += szW;
     }
-    // chunk index v of my block within each source's pack
-    Dim off = 0;
-    bool recv_into_dst = direct_layout;
-    for (Dim bs : src_blocks) {
-      int from = src->dist.canonical(bs);
-      if (sent_into_dst && from == r.rank) continue;
-      (void)recv_into_dst;
-      recvs.push_back({from, off, P.szW});
-      off += P.szW;
+    R.recv_into_dst = R.direct_layout;
+    R.recv_elems = off;
+    if (!R.direct_layout) {
+      // unpack box [F (src order)][W (dst order)] -> dst local
+      R.unpack = true;
+      CopyBox& b = R.unpack_box;
+      Dim st = szW;
+      std::vector<Dim> fstr(F.size()), wstr(W.size());
+      for (int k = static_cast<int>(F.size()) - 1; k >= 0; --k) {
+        fstr[k] = st;
+        st *= ss.dims[F[k]];
+      }
+      st = 1;
+      for (int k = static_cast<int>(W.size()) - 1; k >= 0; --k) {
+        wstr[k] = st;
+        st *= ss.dims[W[k]];
+      }
+      for (size_t k = 0; k < F.size(); ++k) {
+        b.dims.push_back(ss.dims[F[k]]);
+        b.in_stride.push_back(fstr[k]);
+        b.out_stride.push_back(dls(F[k]));
+      }
+      for (size_t k = 0; k < W.size(); ++k) {
+        b.dims.push_back(ss.dims[W[k]]);
+        b.in_stride.push_back(wstr[k]);
+        b.out_stride.push_back(dls(W[k]));
+      }
     }
-    if (direct_layout) {
-      recv_ptr = dst->data();  // single source, layout already final
+  }
+  return R;
+}
+
+TP remap(const TP& src, Shape ds, Dist dd, const std::vector<int>& am) {
+  RankCtx& r = *src->rank;
+  RemapPlan P = plan_remap(src->shape, src->dist, ds, dd, am, r.rank, r.world->size);
+  TP dst = make_tensor(r, ds, dd, true);
+  if (!P.member) return dst;
+  cudaStream_t st = r.stream;
+  if (P.local_only) {
+    if (P.src_canonical && dst->in_span) strided_copy(src->data(), dst->data(), P.pack, true, st);
+    return dst;
+  }
+  std::shared_ptr<DevBuf> packbuf, recvbuf;
+  const void* send_ptr = nullptr;
+  void* recv_ptr = nullptr;
+  if (P.src_canonical) {
+    if (P.pack_to_dst) {
+      strided_copy(src->data(), dst->data(), P.pack, true, st);
+      send_ptr = dst->data();
     } else {
-      recvbuf = std::make_shared<DevBuf>(static_cast<size_t>(off) * 16, r);
+      packbuf = std::make_shared<DevBuf>(static_cast<size_t>(P.pack_elems) * 16, r);
+      strided_copy(src->data(), packbuf->ptr, P.pack, true, st);
+      send_ptr = packbuf->ptr;
+    }
+  }
+  if (dst->in_span) {
+    if (P.recv_into_dst) {
+      recv_ptr = dst->data();
+    } else {
+      recvbuf = std::make_shared<DevBuf>(static_cast<size_t>(P.recv_elems) * 16, r);
       recv_ptr = recvbuf->ptr;
     }
   }
-  // chunk offsets within senders: sender list order is by v, then homes; the
-  // receiver asks for the chunk by order, so fix up sender-side offsets: each send
-  // entry already carries its own offset; receivers match in order per peer.
-  exchange(r, members, send_ptr, sends, recv_ptr, recvs);
-
-  if (dst->in_span && !direct_layout) {
-    // Unpack: box [F (src order)][W (dst order)] -> dst local.
-    CopyBox b;
-    Dim s = P.szW;
-    std::vector<Dim> fstr(P.F.size());
-    for (int k = static_cast<int>(P.F.size()) - 1; k >= 0; --k) {
-      fstr[k] = s;
-      s *= ss.dims[P.F[k]];
-    }
-    for (size_t k = 0; k < P.F.size(); ++k) {
-      b.dims.push_back(ss.dims[P.F[k]]);
-      b.in_stride.push_back(fstr[k]);
-      b.out_stride.push_back(dls(P.F[k]));
-    }
-    s = 1;
-    std::vector<Dim> wstr(P.W.size());
-    for (int k = static_cast<int>(P.W.size()) - 1; k >= 0; --k) {
-      wstr[k] = s;
-      s *= ss.dims[P.W[k]];
-    }
-    for (size_t k = 0; k < P.W.size(); ++k) {
-      b.dims.push_back(ss.dims[P.W[k]]);
-      b.in_stride.push_back(wstr[k]);
-      b.out_stride.push_back(dls(P.W[k]));
-    }
-    // Sources not present (F coords of blocks outside...) cannot happen: every
-    // src block exists, so the box covers the whole destination block.
-    strided_copy(recv_ptr, dst->data(), b, false, st);
-  }
+  exchange(r, P.members, send_ptr, P.sends, recv_ptr, P.recvs);
+  if (dst->in_span && P.unpack) strided_copy(recv_ptr, dst->data(), P.unpack_box, false, st);
   return dst;
 }
 

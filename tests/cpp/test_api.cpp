@@ -1,0 +1,75 @@
+// C++ caller of the B200 path through include/qtnh_b200.hpp, written like the
+// reference's own tests (proj/tests/test_ops.cpp:77-110) to show the drop-in.
+#include <cstdio>
+#include <cstdlib>
+
+#include "qtnh_b200.hpp"
+
+namespace qtnh = qtnh_b200;
+using qtnh::Complex;
+
+#define EXPECT(c)                                                   \
+  do {                                                              \
+    if (!(c)) {                                                     \
+      std::fprintf(stderr, "FAILED %s at line %d\n", #c, __LINE__); \
+      std::exit(1);                                                 \
+    }                                                               \
+  } while (0)
+
+int main() {
+  // matrix transpose (test_ops.cpp:77-85)
+  {
+    qtnh::World w(1);
+    std::vector<Complex> got;
+    w.run([&](qtnh::Rank& rk) {
+      auto t = qtnh::Tensor::from_global(rk, {{2, 2}, 0}, {}, {{1, 0}, {2, 0}, {3, 0}, {4, 0}});
+      got = qtnh::ops::permute(t, {1, 0}, 0).to_global_vector();
+    });
+    EXPECT((got == std::vector<Complex>{{1, 0}, {3, 0}, {2, 0}, {4, 0}}));
+  }
+  // asymmetric permutation recruits more ranks (test_ops.cpp:87-110)
+  {
+    std::vector<Complex> g(32);
+    for (int i = 0; i < 32; ++i) g[i] = {double(i + 1), 0.1 * i};
+    qtnh::World w(4);
+    std::vector<Complex> got;
+    w.run([&](qtnh::Rank& rk) {
+      auto t = qtnh::Tensor::from_global(rk, {{2, 2, 4, 2}, 1}, {1, 1, 0}, g);
+      EXPECT(t.span() == 2);
+      auto p = qtnh::ops::permute(t, {2, 0, 1, 3}, 1);
+      EXPECT(p.span() == 4);
+      auto v = p.to_global_vector();
+      if (rk.rank() == 0) got = v;
+    });
+    // element (c0,c1,c2,c3) of the source lands at (c2,c0,c1,c3)
+    for (int c0 = 0; c0 < 2; ++c0)
+      for (int c1 = 0; c1 < 2; ++c1)
+        for (int c2 = 0; c2 < 4; ++c2)
+          for (int c3 = 0; c3 < 2; ++c3)
+            EXPECT(got[((c2 * 2 + c0) * 2 + c1) * 2 + c3] == g[((c0 * 2 + c1) * 4 + c2) * 2 + c3]);
+    qtnh::World w2(2);
+    bool threw = false;
+    try {
+      w2.run([&](qtnh::Rank& rk) {
+        auto t = qtnh::Tensor::from_global(rk, {{2, 2, 4, 2}, 1}, {1, 1, 0}, g);
+        qtnh::ops::permute(t, {2, 0, 1, 3}, 1);
+      });
+    } catch (const qtnh::ResourceError& e) {
+      threw = e.required_ranks == 4;
+    }
+    EXPECT(threw);
+  }
+  // matrix-vector contraction known answer
+  {
+    qtnh::World w(1);
+    std::vector<Complex> got;
+    w.run([&](qtnh::Rank& rk) {
+      auto a = qtnh::Tensor::from_global(rk, {{2, 2}, 0}, {}, {{0, 0}, {1, 0}, {1, 0}, {0, 0}});
+      auto v = qtnh::Tensor::from_global(rk, {{2}, 0}, {}, {{1, 0}, {0, 0}});
+      got = qtnh::network::contract(a, v, {1}, {0}).to_global_vector();
+    });
+    EXPECT((got == std::vector<Complex>{{0, 0}, {1, 0}}));
+  }
+  std::printf("cpp api ok\n");
+  return 0;
+}

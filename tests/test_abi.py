@@ -57,3 +57,28 @@ def test_world_creation_is_host_only():
     w = qtnh.World(3)
     assert w.size() == 3
     w.close()
+
+
+def _build_cpp_example(tmp_path):
+    import subprocess
+
+    exe = tmp_path / "test_api"
+    subprocess.run(["g++", "-std=c++17", "-O2", f"-I{ROOT}/include", f"{ROOT}/tests/cpp/test_api.cpp",
+                    f"-L{ROOT}/paper_2505_06119_b200", "-l:libqtnh_b200.so",
+                    f"-Wl,-rpath,{ROOT}/paper_2505_06119_b200", "-lpthread", "-o", str(exe)], check=True)
+    return exe
+
+
+def test_cpp_header_layer_compiles(tmp_path):
+    """include/qtnh_b200.hpp (the reference-shaped C++ API) builds against the ABI."""
+    assert _build_cpp_example(tmp_path).exists()
+
+
+@pytest.mark.gpu
+def test_cpp_header_layer_runs(tmp_path):
+    import subprocess
+
+    exe = _build_cpp_example(tmp_path)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert "cpp api ok" in out.stdout
