@@ -187,6 +187,14 @@ int qtnh_counter_complex_normals_device(void* stream, uint64_t seed, int64_t sta
 int qtnh_remap_plan_json(int n_idx, const int64_t* dims, int split, const int64_t* dist, const int* perm,
                          int new_split, const int64_t* new_dist, int rank, int world_size, char* buf, size_t len);
 
+/* Tensor-level split (SPEC network::decompose / linalg psvd + truncate_svd +
+ * absorb_singular_*): rows = indices row_pos (in order), cols = col_pos. Outputs
+ * u with dims [row dims..., chi], vh with dims [chi, col dims...] (same DistParams
+ * as t; t must have no distributed indices), s_host (chi doubles, descending,
+ * zero-padded; may be NULL). qtnh_last_error_info() afterwards = Jacobi sweeps. */
+int qtnh_svd(qtnh_tensor_t t, int n_row, const int* row_pos, int n_col, const int* col_pos, int64_t chi,
+             int absorb, qtnh_tensor_t* u, qtnh_tensor_t* vh, double* s_host);
+
 /* ---- raw kernels on device buffers (bench / integration) ------------------ */
 /* out = a(M x K) * b(K x N), row-major complex128 on the rank's stream. */
 int qtnh_zgemm_device(qtnh_rank_t r, int64_t m, int64_t n, int64_t k, const void* a,

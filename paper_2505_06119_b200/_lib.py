@@ -73,6 +73,7 @@ _SIGS = {
     "qtnh_contract": (i32, [vp, vp, i32, P_i32, P_i32, C.POINTER(vp)]),
     "qtnh_gate_apply": (i32, [vp, i32, P_i32, vp, i32]),
     "qtnh_svd_device": (i32, [vp, i64, i64, i64, vp, i64, i32, vp, vp, vp]),
+    "qtnh_svd": (i32, [vp, i32, P_i32, i32, P_i32, i64, i32, C.POINTER(vp), C.POINTER(vp), vp]),
     "qtnh_zgemm_device": (i32, [vp, i64, i64, i64, vp, vp, vp]),
     "qtnh_permute_device": (i32, [vp, i32, P_i64, P_i32, vp, vp]),
     "qtnh_hash_counter": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64]),

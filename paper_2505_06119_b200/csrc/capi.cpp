@@ -479,8 +479,63 @@ int qtnh_gate_apply(qtnh_tensor_t state, int n_targets, const int* targets, cons
 int qtnh_svd_device(qtnh_rank_t r, int64_t batch, int64_t m, int64_t n, const void* a, int64_t chi, int absorb,
                     void* u, void* s, void* vh) {
   return guard([&] {
-    (void)r; (void)batch; (void)m; (void)n; (void)a; (void)chi; (void)absorb; (void)u; (void)s; (void)vh;
-    throw Status(QTNH_E_RUNTIME, "qtnh_svd_device: batched Jacobi SVD not built in this version");
+    RankCtx& x = ctx_of(r);
+    need(a, "a");
+    need(u, "u");
+    need(s, "s");
+    need(vh, "vh");
+    int sweeps = 0;
+    svd_batched(x, batch, m, n, a, chi, absorb, u, s, vh, &sweeps);
+    t_info = sweeps;
+  });
+}
+
+int qtnh_svd(qtnh_tensor_t t, int n_row, const int* row_pos, int n_col, const int* col_pos, int64_t chi,
+             int absorb, qtnh_tensor_t* u_out, qtnh_tensor_t* vh_out, double* s_host) {
+  return guard([&] {
+    need(u_out, "u");
+    need(vh_out, "vh");
+    TP& p = impl_of(t);
+    const Shape& sh = p->shape;
+    if (sh.split != 0) throw_invalid("svd needs a tensor without distributed indices (gather it first)");
+    if (n_row + n_col != sh.n_idx()) throw_invalid("row/col index sets must partition the tensor indices");
+    std::vector<int> perm, seen(sh.n_idx(), 0);
+    for (int i = 0; i < n_row; ++i) perm.push_back(row_pos[i]);
+    for (int i = 0; i < n_col; ++i) perm.push_back(col_pos[i]);
+    for (int q : perm) {
+      if (q < 0 || q >= sh.n_idx() || seen[q]) throw_invalid("row/col index sets must partition the tensor indices");
+      seen[q] = 1;
+    }
+    Dim m = 1, n = 1;
+    std::vector<Dim> udims, vdims;
+    for (int i = 0; i < n_row; ++i) {
+      m *= sh.dims[row_pos[i]];
+      udims.push_back(sh.dims[row_pos[i]]);
+    }
+    for (int i = 0; i < n_col; ++i) {
+      n *= sh.dims[col_pos[i]];
+      vdims.push_back(sh.dims[col_pos[i]]);
+    }
+    Dim k = std::min(m, n);
+    if (chi <= 0) chi = k;
+    udims.push_back(chi);
+    vdims.insert(vdims.begin(), chi);
+    RankCtx& r = *p->rank;
+    TP mat = op_permute(p, perm, 0);
+    TP u = make_tensor(r, Shape(udims, 0), p->dist, true);
+    TP vh = make_tensor(r, Shape(vdims, 0), p->dist, true);
+    if (p->in_span) {
+      DevBuf s(static_cast<size_t>(chi) * sizeof(double), r);
+      int sweeps = 0;
+      svd_batched(r, 1, m, n, mat->data(), chi, absorb, u->data(), s.ptr, vh->data(), &sweeps);
+      if (s_host) {
+        QTNH_CUDA(cudaMemcpyAsync(s_host, s.ptr, chi * sizeof(double), cudaMemcpyDeviceToHost, r.stream));
+        QTNH_CUDA(cudaStreamSynchronize(r.stream));
+      }
+      t_info = sweeps;
+    }
+    *u_out = wrap(u);
+    *vh_out = wrap(vh);
   });
 }
 

@@ -53,6 +53,10 @@ void zgemm_gather_a(const void* a, const int64_t* rowoff, const int64_t* coloff,
 // out[i] = sum_d digit_d(i) * strides[d], digits row-major over dims.
 void index_offsets(int64_t* out, Dim count, const std::vector<Dim>& dims, const std::vector<Dim>& strides,
                    cudaStream_t st);
+// Batched thin SVD (blocked one-sided Jacobi), truncated / zero-padded to chi,
+// singular values absorbed per QTNH_ABSORB_*; device row-major in/out.
+void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* u, void* s,
+                 void* vh, int* sweeps_out);
 // Gate on a dense local block: dims = local dims, targets = local positions.
 void gate_local(void* data, const std::vector<Dim>& dims, const std::vector<int>& targets,
                 const double* gate_host, bool diagonal, cudaStream_t st);

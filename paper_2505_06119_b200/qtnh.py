@@ -480,3 +480,23 @@ def apply_gate(state: Tensor, targets: Sequence[int], gate, diagonal: bool = Fal
     g = _as_c128(gate)
     check(lib.qtnh_gate_apply(state._h, len(targets), i32_array(targets), g.ctypes.data, int(bool(diagonal))))
     return state
+
+
+# ---- factorisation (linalg.hpp:441-523; SPEC network::decompose) ---------------------------
+ABSORB_NONE, ABSORB_LEFT, ABSORB_RIGHT, ABSORB_SPLIT = 0, 1, 2, 3
+
+
+def svd(t: Tensor, row_pos: Sequence[int], col_pos: Sequence[int], chi: int = 0, absorb: int = ABSORB_NONE):
+    """Thin SVD of t viewed as a matrix (rows = row_pos, cols = col_pos), keeping the
+    chi largest triplets and zero-padding to exactly chi (linalg.hpp:476-505), with
+    the singular values absorbed per ``absorb`` (linalg.hpp:508-523).
+    Returns (U tensor [rows..., chi], s numpy (chi,), Vh tensor [chi, cols...])."""
+    u, vh = C.c_void_p(), C.c_void_p()
+    sh = t.shape()
+    m = int(np.prod([sh.dims[p] for p in row_pos], dtype=np.int64))
+    n = int(np.prod([sh.dims[p] for p in col_pos], dtype=np.int64))
+    k = chi if chi > 0 else min(m, n)
+    s = np.zeros(k, dtype=np.float64)
+    check(lib.qtnh_svd(t._h, len(row_pos), i32_array(row_pos), len(col_pos), i32_array(col_pos), int(chi),
+                       int(absorb), C.byref(u), C.byref(vh), s.ctypes.data))
+    return t._new(u), s, t._new(vh)

@@ -1,0 +1,151 @@
+"""GPU parity of the truncated SVD split (linalg::psvd + truncate_svd + absorb,
+linalg.hpp:441-523) against the unmodified reference (zgesdd via OpenBLAS).
+
+Factors are unique only up to phases, so parity is checked on the singular
+values and on phase-invariant products: the truncated reconstruction U S Vh
+(relative L2 <= 1e-10, north star), U^H U = I, Vh Vh^H = I, and the absorbed
+factors' product."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden, rel_l2
+from paper_2505_06119_b200 import circuits, qtnh
+from paper_2505_06119_b200.qtnh import (ABSORB_LEFT, ABSORB_NONE, ABSORB_RIGHT, ABSORB_SPLIT, IndexTuple, Tensor,
+                                        World, run_collect)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def gpu_svd(a, chi=0, absorb=ABSORB_NONE):
+    m, n = a.shape
+
+    def body(rk):
+        t = Tensor.from_global(rk, IndexTuple([m, n], 0), None, a.reshape(-1))
+        u, s, vh = qtnh.svd(t, [0], [1], chi, absorb)
+        k = s.size
+        return u.to_global_vector().reshape(m, k), s, vh.to_global_vector().reshape(k, n)
+
+    return run_collect(World(1), body)
+
+
+def test_svd_golden_truncated_and_padded():
+    meta, z = golden("svd")
+    a = z["a"]
+    u, s, vh = gpu_svd(a, chi=16, absorb=ABSORB_LEFT)
+    assert np.allclose(s, z["s"], rtol=1e-12, atol=1e-13)
+    assert rel_l2(u @ vh, z["u"] @ z["vh"]) < TOL
+    u2, s2, vh2 = gpu_svd(a, chi=64, absorb=ABSORB_NONE)  # chi > rank: zero padding (linalg.hpp:488-501)
+    assert s2.shape == (64,) and np.all(s2[40:] == 0)
+    assert np.all(u2[:, 40:] == 0)
+    assert np.allclose(s2, z["s_pad"], rtol=1e-12, atol=1e-13)
+    assert rel_l2((u2 * s2) @ vh2, a) < TOL
+
+
+@pytest.mark.parametrize("m,n,chi", [(64, 64, 0), (96, 130, 40), (130, 96, 40), (1, 7, 0), (7, 1, 0),
+                                     (256, 256, 100), (33, 47, 60)])
+def test_svd_shapes_vs_numpy(m, n, chi):
+    a = circuits.rng_normals(m * 7 + n, m * n).reshape(m, n)
+    k = min(m, n)
+    u, s, vh = gpu_svd(a, chi=chi)
+    sv = np.linalg.svd(a, compute_uv=False)
+    kk = chi if chi > 0 else k
+    keep = min(kk, k)
+    assert np.allclose(s[:keep], sv[:keep], rtol=1e-12, atol=1e-12 * sv[0])
+    assert np.all(s[keep:] == 0)
+    U, S, VH = np.linalg.svd(a, full_matrices=False)
+    want = (U[:, :keep] * S[:keep]) @ VH[:keep]
+    assert rel_l2((u * s) @ vh, want) < TOL
+    assert np.allclose(u[:, :keep].conj().T @ u[:, :keep], np.eye(keep), atol=1e-12)
+    assert np.allclose(vh[:keep] @ vh[:keep].conj().T, np.eye(keep), atol=1e-12)
+
+
+def test_absorb_modes():
+    a = circuits.rng_normals(3, 50 * 40).reshape(50, 40)
+    _, s, _ = gpu_svd(a, chi=20)
+    for mode in (ABSORB_LEFT, ABSORB_RIGHT, ABSORB_SPLIT):
+        u, s2, vh = gpu_svd(a, chi=20, absorb=mode)
+        assert np.allclose(s2, s, rtol=1e-13)
+        U, S, VH = np.linalg.svd(a, full_matrices=False)
+        assert rel_l2(u @ vh, (U[:, :20] * S[:20]) @ VH[:20]) < TOL
+        if mode == ABSORB_LEFT:
+            assert np.allclose(np.linalg.norm(u, axis=0), s, rtol=1e-12)
+        if mode == ABSORB_RIGHT:
+            assert np.allclose(np.linalg.norm(vh, axis=1), s, rtol=1e-12)
+        if mode == ABSORB_SPLIT:
+            assert np.allclose(np.linalg.norm(u, axis=0), np.sqrt(s), rtol=1e-12)
+
+
+def test_rank_deficient_and_zero():
+    rng = np.random.default_rng(2)
+    b = rng.standard_normal((60, 5)) + 1j * rng.standard_normal((60, 5))
+    c = rng.standard_normal((5, 50)) + 1j * rng.standard_normal((5, 50))
+    a = b @ c  # rank 5
+    u, s, vh = gpu_svd(a, chi=8)
+    assert np.all(s[5:] < 1e-12 * s[0])
+    assert rel_l2((u * s) @ vh, a) < TOL
+    z = np.zeros((8, 6), complex)
+    u, s, vh = gpu_svd(z)
+    assert np.all(s == 0) and np.all((u * s) @ vh == 0)
+
+
+def test_svd_vs_reference_theta_like():
+    """MPS two-site theta (chi_l, d, d, chi_r) -> (chi_l d) x (d chi_r), truncated."""
+    if not oracle.ref_available():
+        pytest.skip("reference build absent")
+    R = oracle.ref()
+    chi = 64
+    a = circuits.rng_normals(77, (2 * chi) ** 2).reshape(2 * chi, 2 * chi)
+    ru, rs, rvh = R.svd(a, chi=chi, absorb=1)
+    u, s, vh = gpu_svd(a, chi=chi, absorb=ABSORB_LEFT)
+    assert np.allclose(s, rs, rtol=1e-12)
+    assert rel_l2(u @ vh, ru @ rvh) < TOL
+
+
+def test_svd_batched_device_api():
+    import torch
+
+    batch, m, n, chi = 3, 70, 90, 30
+    a = np.stack([circuits.rng_normals(10 + i, m * n).reshape(m, n) for i in range(batch)])
+    ta = torch.from_numpy(a).cuda()
+    tu = torch.empty((batch, m, chi), dtype=torch.complex128, device="cuda")
+    ts = torch.empty((batch, chi), dtype=torch.float64, device="cuda")
+    tv = torch.empty((batch, chi, n), dtype=torch.complex128, device="cuda")
+
+    def body(rk):
+        rk.set_stream(torch.cuda.current_stream().cuda_stream)
+        qtnh.check(qtnh.lib.qtnh_svd_device(rk._h, batch, m, n, C.c_void_p(ta.data_ptr()), chi, ABSORB_RIGHT,
+                                            C.c_void_p(tu.data_ptr()), C.c_void_p(ts.data_ptr()),
+                                            C.c_void_p(tv.data_ptr())))
+        torch.cuda.synchronize()
+
+    World(1).run(body)
+    for i in range(batch):
+        U, S, VH = np.linalg.svd(a[i], full_matrices=False)
+        assert np.allclose(ts[i].cpu().numpy(), S[:chi], rtol=1e-12)
+        assert rel_l2(tu[i].cpu().numpy() @ tv[i].cpu().numpy(), (U[:, :chi] * S[:chi]) @ VH[:chi]) < TOL
+
+
+@pytest.mark.slow
+def test_svd_c4_size_vs_reference():
+    """Config 4 shape: theta 2048 x 2048 truncated to chi = 1024, against zgesdd."""
+    if not oracle.ref_available():
+        pytest.skip("reference build absent")
+    import os
+
+    R = oracle.ref()
+    R.set_threads(os.cpu_count() or 1)
+    n, chi = 2048, 1024
+    # a realistic spectrum: decaying singular values (entangled MPS bond)
+    rng = np.random.default_rng(4)
+    q1, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    q2, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    sv = np.exp(-np.arange(n) / 300.0)
+    a = (q1 * sv) @ q2
+    ru, rs, rvh = R.svd(a, chi=chi, absorb=1)
+    u, s, vh = gpu_svd(a, chi=chi, absorb=ABSORB_LEFT)
+    assert np.allclose(s, rs, rtol=1e-11, atol=1e-13)
+    assert rel_l2(u @ vh, ru @ rvh) < TOL
