@@ -154,6 +154,74 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+
+def hbm_peak():
+    """Measured HBM copy peak (MEASURED_PEAKS.json, driver-written) else the
+    B200_PROFILING.md fallback."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def measure_extras(rk, stream, torch):
+    """Secondary hot-path kernels, timed with CUDA events on the rank stream:
+    gate application on a 2^30-amplitude state (HBM roofline, 32 B/amplitude per
+    gate by convention), the layout permutation, and the config-4 SVD."""
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_2505_06119_b200 import circuits, qtnh
+    from paper_2505_06119_b200.qtnh import IndexTuple, Tensor, apply_gate
+
+    peak, src = hbm_peak()
+    ex = {"hbm_peak_gbs": peak, "hbm_peak_source": src}
+    n = 30
+    st = Tensor.dense(rk, IndexTuple([2] * n, 0), None, None)
+    bytes_per_gate = 32.0 * 2**n
+    cases = [("dense_1q_H_q15", [15], circuits.H, False), ("dense_1q_H_q29", [29], circuits.H, False),
+             ("dense_2q_fsim_q3_q20", [3, 20], circuits.FSIM, False),
+             ("diag_cp_q7_q22", [7, 22], circuits.cp_diag(0.3), True)]
+    res = {}
+    for name, q, g, diag in cases:
+        for _ in range(2):
+            apply_gate(st, q, g, diagonal=diag)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        e0.record(stream)
+        for _ in range(reps):
+            apply_gate(st, q, g, diagonal=diag)
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        gbs = bytes_per_gate / (ms * 1e-3) / 1e9
+        entry = {"ms": ms, "GBps_algorithmic": gbs, "frac": gbs / peak}
+        if diag:
+            entry["note"] = "touches the 1/4 of amplitudes whose diagonal entry != 1: actual traffic 8 B/amplitude"
+        res[name] = entry
+    st.free()
+    ex["gate_apply_n30"] = res
+    # config-4 SVD: theta 2048 x 2048 -> chi 1024, absorb left
+    nn, chi = 2048, 1024
+    rng = np.random.default_rng(0)
+    a = torch.from_numpy(rng.standard_normal((nn, nn)) + 1j * rng.standard_normal((nn, nn))).cuda()
+    u = torch.empty((nn, chi), dtype=torch.complex128, device="cuda")
+    s = torch.empty((chi,), dtype=torch.float64, device="cuda")
+    vh = torch.empty((chi, nn), dtype=torch.complex128, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    qtnh.check(qtnh.lib.qtnh_svd_device(rk._h, 1, nn, nn, C.c_void_p(a.data_ptr()), chi, 1, C.c_void_p(u.data_ptr()),
+                                        C.c_void_p(s.data_ptr()), C.c_void_p(vh.data_ptr())))
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    ex["svd_2048_chi1024"] = {"ms": ms, "sweeps": int(qtnh.lib.qtnh_last_error_info()),
+                              "conv_TFLOPs": 88.0 * nn**3 / (ms * 1e-3) / 1e12,
+                              "flop_convention": "88 n^3 (BASELINE.md section 4)"}
+    del a, u, s, vh
+    return ex
+
 # ---- GPU arm -------------------------------------------------------------------------------------
 def run_gpu_arm(args):
     import numpy as np
@@ -298,6 +366,9 @@ def run_gpu_arm(args):
             result["d2h"] = 2**RANK_A * 16
             ta.free()
             tb.free()
+            torch.cuda.synchronize()
+            if not args.skip_extras:
+                result["extras"] = measure_extras(rk, stream, torch)
 
     world.run(body)
 
@@ -347,12 +418,14 @@ def run_gpu_arm(args):
                          "peak_source": "DMMA-only microbenchmark run live on this device (MEASURED_PEAKS.json "
                                         "has no FP64 entry)",
                          "traffic": traffic, "zgemm_ms": zg, "permute_ms": result["permute_ms"],
+                         "permute_GBps": 2 * 16 * 2**RANK_A / (result["permute_ms"] * 1e-3) / 1e9,
                          "zgemm_spot_rel_err": result["zgemm_spot_rel_err"]},
             "cpu_baseline": cpu,
             "e2e": {"value": total_flops / (e2e_ms * 1e-3) / 1e12, "unit": UNIT,
                     "h2d_bytes_per_step": result["h2d"], "d2h_bytes_per_step": result["d2h"],
                     "ms_per_step": e2e_ms},
             "gpu_launches": result["launches"],
+            "extras": result.get("extras"),
             "clocks": result["clocks"],
         }
         print(json.dumps(line), flush=True)
@@ -370,6 +443,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--skip-extras", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

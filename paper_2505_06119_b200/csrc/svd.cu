@@ -22,6 +22,7 @@
 //   one output kernel.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <numeric>
 #include <vector>
 
@@ -35,6 +36,13 @@ constexpr int kB = 16;        // rows per block
 constexpr int kP2 = 2 * kB;   // rows per pair (inner problem size)
 constexpr int kGramCols = 64; // column chunk of the Gram kernel
 constexpr int kUpdCols = 64;  // column tile of the update kernel
+static_assert(kB * kB == 256, "the 2x2-block eigen update maps one block per thread");
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
 
 struct PairTab {
   const int* blocks;  // [rounds][npairs][2]
@@ -205,33 +213,40 @@ __global__ void __launch_bounds__(256) k_svd_eigen(const double2* __restrict__ p
         rq_[tid] = q;
       }
       __syncthreads();
-      // columns: G <- G J, V <- V J   (J = [[c, s], [-s e^{-i phi}, c e^{-i phi}]])
-      for (int e = tid; e < kB * kP2; e += 256) {
-        int k = e / kP2, i = e % kP2;
-        int p = rp_[k], q = rq_[k];
-        double c = rot_c[k], s = rot_s[k];
-        double2 ph = rot_ph[k];
-        double2 gp = G[i][p], gq = cmul(G[i][q], ph);
-        G[i][p] = make_double2(c * gp.x - s * gq.x, c * gp.y - s * gq.y);
-        G[i][q] = make_double2(s * gp.x + c * gq.x, s * gp.y + c * gq.y);
-        double2 vp = V[i][p], vq = cmul(V[i][q], ph);
-        V[i][p] = make_double2(c * vp.x - s * vq.x, c * vp.y - s * vq.y);
-        V[i][q] = make_double2(s * vp.x + c * vq.x, s * vp.y + c * vq.y);
-      }
-      __syncthreads();
-      // rows: G <- J^H G
-      for (int e = tid; e < kB * kP2; e += 256) {
-        int k = e / kP2, j = e % kP2;
-        int p = rp_[k], q = rq_[k];
-        double c = rot_c[k], s = rot_s[k];
-        double2 phc = cconj(rot_ph[k]);  // e^{+i phi}
-        double2 gp = G[p][j], gq = cmul(G[q][j], phc);
-        G[p][j] = make_double2(c * gp.x - s * gq.x, c * gp.y - s * gq.y);
-        G[q][j] = make_double2(s * gp.x + c * gq.x, s * gp.y + c * gq.y);
+      // G <- J^H G J in one pass: thread (k, l) owns the 2x2 block rows {p_k, q_k}
+      // x cols {p_l, q_l} (pairs are disjoint, so blocks are independent);
+      // V <- V J alongside. J = [[c, s], [-s e^{-i phi}, c e^{-i phi}]].
+      {
+        const int k = tid >> 4, l = tid & 15;
+        const int pk = rp_[k], qk = rq_[k], pl = rp_[l], ql = rq_[l];
+        const double ck = rot_c[k], sk = rot_s[k], cl = rot_c[l], sl = rot_s[l];
+        const double2 ek = cconj(rot_ph[k]), el = rot_ph[l];
+        double2 a = G[pk][pl], b = G[pk][ql], c = G[qk][pl], d = G[qk][ql];
+        // right: columns
+        double2 bq = cmul(b, el), dq = cmul(d, el);
+        double2 a1 = make_double2(cl * a.x - sl * bq.x, cl * a.y - sl * bq.y);
+        double2 b1 = make_double2(sl * a.x + cl * bq.x, sl * a.y + cl * bq.y);
+        double2 c1 = make_double2(cl * c.x - sl * dq.x, cl * c.y - sl * dq.y);
+        double2 d1 = make_double2(sl * c.x + cl * dq.x, sl * c.y + cl * dq.y);
+        // left: rows
+        double2 c2 = cmul(c1, ek), d2 = cmul(d1, ek);
+        G[pk][pl] = make_double2(ck * a1.x - sk * c2.x, ck * a1.y - sk * c2.y);
+        G[pk][ql] = make_double2(ck * b1.x - sk * d2.x, ck * b1.y - sk * d2.y);
+        G[qk][pl] = make_double2(sk * a1.x + ck * c2.x, sk * a1.y + ck * c2.y);
+        G[qk][ql] = make_double2(sk * b1.x + ck * d2.x, sk * b1.y + ck * d2.y);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = tid & 31, kk = (tid >> 5) + 8 * h;
+          const int p = rp_[kk], q = rq_[kk];
+          const double cc = rot_c[kk], ss = rot_s[kk];
+          double2 vp = V[i][p], vq = cmul(V[i][q], rot_ph[kk]);
+          V[i][p] = make_double2(cc * vp.x - ss * vq.x, cc * vp.y - ss * vq.y);
+          V[i][q] = make_double2(ss * vp.x + cc * vq.x, ss * vp.y + cc * vq.y);
+        }
       }
       __syncthreads();
     }
-    if (measure() < tol * 1e-2) break;
+    if (sw + 1 < inner_sweeps && measure() < tol * 1e-2) break;
   }
   double2* out = wh + fidx * kP2 * kP2;
   for (int e = tid; e < kP2 * kP2; e += 256) {
@@ -288,6 +303,123 @@ __global__ void __launch_bounds__(256) k_svd_update(double2* __restrict__ wk, co
       if (col < W) K[row * W + col] = y[u];
     }
     __syncthreads();
+  }
+}
+
+
+// ---- DMMA variants of the two GEMM-shaped steps -----------------------------------------
+// Gram on the FP64 tensor cores: G = X X^H, X = 32 rows x (column slice). 4 warps,
+// warp w owns rows [8w, 8w+8) x all 32 columns (4 m8n8 tiles); A and B fragments
+// come from the same shared tile (B = conj of X), pitch = 4 (mod 8) x 16 B.
+constexpr int kGK = 64;  // columns per staged chunk
+__global__ void __launch_bounds__(128) k_svd_gram_mma(const double2* __restrict__ wk, double2* __restrict__ part,
+                                                      const int* __restrict__ tab, int round, int npairs,
+                                                      int splits, int64_t rp, int64_t L) {
+  const int pair = blockIdx.x, split = blockIdx.y, mat = blockIdx.z;
+  const int64_t W = L + rp;
+  const int* pr = tab + (static_cast<int64_t>(round) * npairs + pair) * 2;
+  const int bi = pr[0], bj = pr[1];
+  const double2* K = wk + static_cast<int64_t>(mat) * rp * W;
+  constexpr int PX = kGK + 4;
+  __shared__ double2 xs[kP2][PX];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  double acc_re[4][2], acc_im[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc_re[j][0] = acc_re[j][1] = acc_im[j][0] = acc_im[j][1] = 0.0;
+  int64_t per = (L + splits - 1) / splits;
+  int64_t c0 = split * per, c1 = min(L, c0 + per);
+  for (int64_t cb = c0; cb < c1; cb += kGK) {
+    for (int e = tid; e < kP2 * kGK; e += 128) {
+      int r = e / kGK, c = e % kGK;
+      int64_t row = (r < kB ? bi * kB + r : bj * kB + (r - kB));
+      int64_t col = cb + c;
+      xs[r][c] = col < c1 ? K[row * W + col] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k4 = 0; k4 < kGK; k4 += 4) {
+      double2 av = xs[warp * 8 + fr][k4 + fk];
+      double b_re[4], b_im[4], nb_im[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        double2 bv = xs[j * 8 + fr][k4 + fk];  // B = conj(X)^T: (k, j) -> conj(X[j][k])
+        b_re[j] = bv.x;
+        b_im[j] = -bv.y;
+        nb_im[j] = bv.y;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        dmma(acc_re[j], av.x, b_re[j]);
+        dmma(acc_im[j], av.x, b_im[j]);
+        dmma(acc_re[j], av.y, nb_im[j]);
+        dmma(acc_im[j], av.y, b_re[j]);
+      }
+    }
+    __syncthreads();
+  }
+  double2* out = part + ((static_cast<int64_t>(mat) * npairs + pair) * splits + split) * kP2 * kP2;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    int row = warp * 8 + fr, col = j * 8 + 2 * fk;
+    out[row * kP2 + col] = make_double2(acc_re[j][0], acc_im[j][0]);
+    out[row * kP2 + col + 1] = make_double2(acc_re[j][1], acc_im[j][1]);
+  }
+}
+
+// In-place update on the FP64 tensor cores: Y (32 x 48 cols) = W^H (32 x 32) X.
+// 4 warps, warp w owns rows [8w, 8w+8) x 48 columns (6 m8n8 tiles).
+constexpr int kUpdColsM = 48;
+__global__ void __launch_bounds__(128) k_svd_update_mma(double2* __restrict__ wk, const double2* __restrict__ wh,
+                                                        const int* __restrict__ flags, const int* __restrict__ tab,
+                                                        int round, int npairs, int64_t rp, int64_t L) {
+  const int pair = blockIdx.y, mat = blockIdx.z, tid = threadIdx.x;
+  const int64_t fidx = static_cast<int64_t>(mat) * npairs + pair;
+  if (!flags[fidx]) return;
+  const int64_t W = L + rp;
+  const int* pr = tab + (static_cast<int64_t>(round) * npairs + pair) * 2;
+  const int bi = pr[0], bj = pr[1];
+  double2* K = wk + static_cast<int64_t>(mat) * rp * W;
+  constexpr int UC = kUpdColsM, NT = UC / 8;
+  constexpr int PW = kP2 + 4, PX = UC + 2;
+  __shared__ double2 ws[kP2][PW];
+  __shared__ double2 xs[kP2][PX];
+  const int lane = tid & 31, warp = tid >> 5, fr = lane >> 2, fk = lane & 3;
+  const double2* Wh = wh + fidx * kP2 * kP2;
+  for (int e = tid; e < kP2 * kP2; e += 128) ws[e / kP2][e % kP2] = Wh[e];
+  for (int64_t cb = static_cast<int64_t>(blockIdx.x) * UC; cb < W;
+       cb += static_cast<int64_t>(gridDim.x) * UC) {
+    for (int e = tid; e < kP2 * UC; e += 128) {
+      int r = e / UC, c = e % UC;
+      int64_t row = r < kB ? bi * kB + r : bj * kB + (r - kB);
+      int64_t col = cb + c;
+      xs[r][c] = col < W ? K[row * W + col] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    double acc_re[NT][2], acc_im[NT][2];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc_re[j][0] = acc_re[j][1] = acc_im[j][0] = acc_im[j][1] = 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < kP2; k4 += 4) {
+      double2 av = ws[warp * 8 + fr][k4 + fk];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        double2 bv = xs[k4 + fk][j * 8 + fr];
+        dmma(acc_re[j], av.x, bv.x);
+        dmma(acc_im[j], av.x, bv.y);
+        dmma(acc_re[j], av.y, -bv.y);
+        dmma(acc_im[j], av.y, bv.x);
+      }
+    }
+    __syncthreads();  // all reads of xs done before any write-back
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      int r = warp * 8 + fr;
+      int64_t row = r < kB ? bi * kB + r : bj * kB + (r - kB);
+      int64_t col = cb + j * 8 + 2 * fk;
+      if (col < W) K[row * W + col] = make_double2(acc_re[j][0], acc_im[j][0]);
+      if (col + 1 < W) K[row * W + col + 1] = make_double2(acc_re[j][1], acc_im[j][1]);
+    }
   }
 }
 
@@ -356,6 +488,30 @@ __global__ void k_svd_output(const double2* __restrict__ wk, const double* __res
   }
 }
 
+int inner_sweeps() {
+  static int v = [] {
+    const char* e = std::getenv("QTNH_SVD_INNER");
+    return e ? std::max(1, std::atoi(e)) : 1;
+  }();
+  return v;
+}
+
+bool use_mma() {
+  static bool v = [] {
+    const char* e = std::getenv("QTNH_SVD_MMA");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
+double tolerance() {
+  static double v = [] {
+    const char* e = std::getenv("QTNH_SVD_TOL");
+    return e ? std::atof(e) : 1e-13;
+  }();
+  return v;
+}
+
 int sms() {
   int dev = 0, n = 148;
   cudaGetDevice(&dev);
@@ -407,7 +563,7 @@ void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, in
                                   transpose);
     QTNH_LAUNCH_CHECK();
   }
-  const double tol = 1e-13;
+  const double tol = tolerance();
   std::vector<double> off_h(batch);
   int sweep = 0;
   const int max_sweeps = 40;
@@ -415,19 +571,30 @@ void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, in
   for (; sweep < max_sweeps; ++sweep) {
     QTNH_CUDA(cudaMemsetAsync(offm.ptr, 0, batch * sizeof(double), st));
     for (int rd = 0; rd < rounds; ++rd) {
-      k_svd_gram<<<dim3(npairs, splits, static_cast<unsigned>(batch)), 256, 0, st>>>(
-          static_cast<const double2*>(wk.ptr), static_cast<double2*>(part.ptr), static_cast<const int*>(d_tab.ptr),
-          rd, npairs, splits, rp, L);
+      if (use_mma())
+        k_svd_gram_mma<<<dim3(npairs, splits, static_cast<unsigned>(batch)), 128, 0, st>>>(
+            static_cast<const double2*>(wk.ptr), static_cast<double2*>(part.ptr), static_cast<const int*>(d_tab.ptr),
+            rd, npairs, splits, rp, L);
+      else
+        k_svd_gram<<<dim3(npairs, splits, static_cast<unsigned>(batch)), 256, 0, st>>>(
+            static_cast<const double2*>(wk.ptr), static_cast<double2*>(part.ptr), static_cast<const int*>(d_tab.ptr),
+            rd, npairs, splits, rp, L);
       QTNH_LAUNCH_CHECK();
       k_svd_eigen<<<dim3(npairs, static_cast<unsigned>(batch)), 256, 0, st>>>(
           static_cast<const double2*>(part.ptr), static_cast<double2*>(whb.ptr), static_cast<int*>(flags.ptr),
-          static_cast<double*>(offm.ptr), npairs, splits, tol, 4);
+          static_cast<double*>(offm.ptr), npairs, splits, tol, inner_sweeps());
       QTNH_LAUNCH_CHECK();
-      unsigned ctiles = static_cast<unsigned>(std::min<Dim>((W + kUpdCols - 1) / kUpdCols,
-                                                            std::max<Dim>(1, 4 * sms() / (npairs * batch))));
-      k_svd_update<<<dim3(ctiles, npairs, static_cast<unsigned>(batch)), 256, 0, st>>>(
-          static_cast<double2*>(wk.ptr), static_cast<const double2*>(whb.ptr), static_cast<const int*>(flags.ptr),
-          static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L);
+      const Dim ucols = use_mma() ? kUpdColsM : kUpdCols;
+      unsigned ctiles = static_cast<unsigned>(std::min<Dim>((W + ucols - 1) / ucols,
+                                                            std::max<Dim>(1, (use_mma() ? 8 : 4) * sms() / (npairs * batch))));
+      if (use_mma())
+        k_svd_update_mma<<<dim3(ctiles, npairs, static_cast<unsigned>(batch)), 128, 0, st>>>(
+            static_cast<double2*>(wk.ptr), static_cast<const double2*>(whb.ptr), static_cast<const int*>(flags.ptr),
+            static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L);
+      else
+        k_svd_update<<<dim3(ctiles, npairs, static_cast<unsigned>(batch)), 256, 0, st>>>(
+            static_cast<double2*>(wk.ptr), static_cast<const double2*>(whb.ptr), static_cast<const int*>(flags.ptr),
+            static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L);
       QTNH_LAUNCH_CHECK();
     }
     QTNH_CUDA(cudaMemcpyAsync(off_h.data(), offm.ptr, batch * sizeof(double), cudaMemcpyDeviceToHost, st));

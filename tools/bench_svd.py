@@ -54,4 +54,6 @@ def main(shapes):
 
 if __name__ == "__main__":
     shapes = [(1, 256, 128), (1, 1024, 512), (1, 2048, 1024), (4, 1024, 512)]
+    if len(sys.argv) > 1:
+        shapes = [tuple(int(x) for x in s.split("x")) for s in sys.argv[1:]]
     main(shapes)
