@@ -156,6 +156,15 @@ int qtnh_contract(qtnh_tensor_t a, qtnh_tensor_t b, int n_pairs, const int* a_po
 int qtnh_gate_apply(qtnh_tensor_t state, int n_targets, const int* targets,
                     const double* gate, int diagonal);
 
+/* In-place exchange of two equal-size indices (values of ops::permute with the
+ * two positions swapped -- a contraction with a swap tensor, tensor.hpp:157-164);
+ * a distributed index goes through the exchange path. */
+int qtnh_swap_indices(qtnh_tensor_t t, int a, int b);
+/* Fused QFT layer j on a qubit tensor (all dims 2, qubit j = index j, index 0 most
+ * significant): H on qubit j and every CP(2 pi / 2^m) between j and qubit j+m-1
+ * (Fig. 1) in one pass over the state. */
+int qtnh_qft_layer(qtnh_tensor_t t, int j);
+
 /* ---- factorisation --------------------------------------------------------- */
 enum { QTNH_ABSORB_NONE = 0, QTNH_ABSORB_LEFT = 1, QTNH_ABSORB_RIGHT = 2, QTNH_ABSORB_SPLIT = 3 };
 /* Batched thin SVD of `batch` row-major m x n matrices stored back to back in

@@ -102,3 +102,15 @@ def apply_qft(state: "qtnh.Tensor", n: int, swaps: bool = True) -> "qtnh.Tensor"
                 state.free()
             state = nxt
     return state
+
+
+def apply_qft_fused(state: "qtnh.Tensor", n: int, swaps: bool = True) -> "qtnh.Tensor":
+    """QFT with one fused pass per layer (H_j + all its controlled phases,
+    qtnh.qft_layer) and in-place qubit swaps: n + n/2 passes instead of
+    n(n+1)/2 + n/2. Same values as apply_qft up to rounding."""
+    for j in range(n):
+        qtnh.qft_layer(state, j)
+    if swaps:
+        for j in range(n // 2):
+            qtnh.swap_indices(state, j, n - 1 - j)
+    return state

@@ -476,6 +476,36 @@ int qtnh_gate_apply(qtnh_tensor_t state, int n_targets, const int* targets, cons
   });
 }
 
+namespace {
+// Copy-on-write before an in-place update: other handles must not see it.
+void make_exclusive(TP& p) {
+  if (p->in_span && (p.use_count() > 1 || (p->buf && p->buf.use_count() > 1))) {
+    TP c = make_tensor(*p->rank, p->shape, p->dist, true);
+    QTNH_CUDA(cudaMemcpyAsync(c->data(), p->data(), p->shape.local_size() * 16, cudaMemcpyDeviceToDevice,
+                              p->rank->stream));
+    p = c;
+  } else if (!p->in_span && p.use_count() > 1) {
+    p = make_tensor(*p->rank, p->shape, p->dist, false);
+  }
+}
+}  // namespace
+
+int qtnh_swap_indices(qtnh_tensor_t t, int a, int b) {
+  return guard([&] {
+    TP& p = impl_of(t);
+    make_exclusive(p);
+    op_swap_indices(p, a, b);
+  });
+}
+
+int qtnh_qft_layer(qtnh_tensor_t t, int j) {
+  return guard([&] {
+    TP& p = impl_of(t);
+    make_exclusive(p);
+    op_qft_layer(p, j);
+  });
+}
+
 int qtnh_svd_device(qtnh_rank_t r, int64_t batch, int64_t m, int64_t n, const void* a, int64_t chi, int absorb,
                     void* u, void* s, void* vh) {
   return guard([&] {

@@ -274,3 +274,48 @@ void op_gate_apply(TP& t, const std::vector<int>& targets, const double* gate, b
 }
 
 }  // namespace qtnhb
+
+namespace qtnhb {
+
+void op_swap_indices(TP& t, int a, int b) {
+  const Shape& s = t->shape;
+  if (a < 0 || b < 0 || a >= s.n_idx() || b >= s.n_idx() || a == b) throw_invalid("invalid index pair to swap");
+  if (s.dims[a] != s.dims[b]) throw_invalid("swapped indices must have equal dimensions");
+  if (a >= s.split && b >= s.split) {
+    if (t->in_span) swap_indices_local(t->data(), s.local_dims(), a - s.split, b - s.split, t->rank->stream);
+    return;
+  }
+  std::vector<int> perm(s.n_idx());
+  std::iota(perm.begin(), perm.end(), 0);
+  std::swap(perm[a], perm[b]);
+  t = op_permute(t, perm, s.split);
+}
+
+void op_qft_layer(TP& t, int j) {
+  const Shape& s = t->shape;
+  int n = s.n_idx();
+  for (Dim d : s.dims)
+    if (d != 2) throw_invalid("qft layer needs a qubit tensor (all dims 2)");
+  if (j < 0 || j >= n) throw_invalid("qft layer qubit out of range");
+  int lb = n - s.split;
+  if (lb > 62) throw_invalid("too many local qubits");
+  RankCtx& r = *t->rank;
+  if (j >= s.split) {
+    if (t->in_span) qft_layer_local(t->data(), lb, n - 1 - j, r.stream);
+    return;
+  }
+  // distributed target: H through the dist<->local swap path, then the phases on
+  // the ranks whose block has x_j = 1 (dist bits below j enter v as a constant).
+  const double h[8] = {0.70710678118654752440, 0, 0.70710678118654752440, 0,
+                       0.70710678118654752440, 0, -0.70710678118654752440, 0};
+  op_gate_apply(t, {j}, h, false);
+  if (!t->in_span) return;
+  auto cd = unflat(t->block, t->shape.dist_dims());
+  if (cd[j] == 0) return;
+  int64_t v_off = 0;
+  for (int l = j + 1; l < s.split; ++l) v_off = (v_off << 1) | cd[l];
+  v_off <<= lb;
+  qft_phase_local(t->data(), lb, v_off, n - 1 - j, r.stream);
+}
+
+}  // namespace qtnhb

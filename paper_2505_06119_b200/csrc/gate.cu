@@ -221,4 +221,123 @@ void gate_local(void* data, const std::vector<Dim>& dims, const std::vector<int>
   QTNH_LAUNCH_CHECK();
 }
 
+namespace {
+
+// ---- fused QFT layer (diagonal fast path + gate fusion) ------------
+// Layer j of the QFT is H on qubit j followed by CP(2 pi / 2^m) between j and every
+// lower-order qubit j+m-1 (Fig. 1). All those phases are diagonal and
+// commute, and for an amplitude with x_j = 1 they multiply to
+//   exp(i pi v / 2^t),  v = value of the bits below qubit j, t = its bit position,
+// so one pass over the state applies the whole layer:
+//   y0 = (a0 + a1)/sqrt2,  y1 = (a0 - a1)/sqrt2 * exp(i pi v / 2^t).
+// 32 B/amplitude per LAYER instead of per gate (n layers vs n(n+1)/2 gates).
+__global__ void __launch_bounds__(256) k_qft_layer(double2* __restrict__ psi, int64_t n_pairs, int t) {
+  const double r = 0.70710678118654752440;
+  const int64_t lo_mask = (int64_t(1) << t) - 1;
+  const double scale = ldexp(1.0, -t);
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n_pairs;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = p & lo_mask;
+    int64_t i0 = ((p >> t) << (t + 1)) | lo;
+    int64_t i1 = i0 | (int64_t(1) << t);
+    double2 a0 = psi[i0], a1 = psi[i1];
+    double2 y0 = make_double2(r * a0.x + r * a1.x, r * a0.y + r * a1.y);
+    double2 d = make_double2(r * a0.x - r * a1.x, r * a0.y - r * a1.y);
+    double sn, cs;
+    sincospi(static_cast<double>(lo) * scale, &sn, &cs);
+    psi[i0] = y0;
+    psi[i1] = make_double2(cs * d.x - sn * d.y, cs * d.y + sn * d.x);
+  }
+}
+
+// Phases of a layer whose target is a distributed qubit with x_j = 1 on this
+// rank: every local amplitude i gets exp(i pi (v_off + i) / 2^t).
+__global__ void __launch_bounds__(256) k_qft_phase(double2* __restrict__ psi, int64_t n, int64_t v_off, int t) {
+  const double scale = ldexp(1.0, -t);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double sn, cs;
+    sincospi(static_cast<double>(v_off + i) * scale, &sn, &cs);
+    double2 a = psi[i];
+    psi[i] = make_double2(cs * a.x - sn * a.y, cs * a.y + sn * a.x);
+  }
+}
+
+// In-place exchange of two equal-size indices a, b (values of ops::permute with
+// the two positions swapped, remap.hpp zero canonicalisation included): per fiber,
+// element (i at a, j at b) <-> (j at a, i at b) for i < j.
+template <bool POW2>
+__global__ void __launch_bounds__(256) k_swap_indices(double2* __restrict__ psi, int64_t n_fibers, int d,
+                                                      int64_t sa, int64_t sb, const __grid_constant__ GateArgs a) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < n_fibers;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    int64_t base = fiber_base<POW2>(f, a);
+    for (int i = 0; i < d; ++i) {
+      int64_t oii = base + i * sa + i * sb;
+      double2 v = psi[oii];
+      if (v.x == 0.0 && v.y == 0.0 && (signbit(v.x) || signbit(v.y))) psi[oii] = make_double2(0.0, 0.0);
+      for (int j = i + 1; j < d; ++j) {
+        int64_t o1 = base + i * sa + j * sb, o2 = base + j * sa + i * sb;
+        double2 x = psi[o1], y = psi[o2];
+        if (x.x == 0.0 && x.y == 0.0) x = make_double2(0.0, 0.0);
+        if (y.x == 0.0 && y.y == 0.0) y = make_double2(0.0, 0.0);
+        psi[o1] = y;
+        psi[o2] = x;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+void qft_layer_local(void* data, int local_bits, int t, cudaStream_t st) {
+  if (t < 0 || t >= local_bits) throw_invalid("qft layer target outside the local bits");
+  int64_t n_pairs = int64_t(1) << (local_bits - 1);
+  k_qft_layer<<<grid_for(n_pairs), 256, 0, st>>>(static_cast<double2*>(data), n_pairs, t);
+  QTNH_LAUNCH_CHECK();
+}
+
+void qft_phase_local(void* data, int local_bits, int64_t v_off, int t, cudaStream_t st) {
+  int64_t n = int64_t(1) << local_bits;
+  k_qft_phase<<<grid_for(n), 256, 0, st>>>(static_cast<double2*>(data), n, v_off, t);
+  QTNH_LAUNCH_CHECK();
+}
+
+void swap_indices_local(void* data, const std::vector<Dim>& dims, int ia, int ib, cudaStream_t st) {
+  int r = static_cast<int>(dims.size());
+  if (ia < 0 || ib < 0 || ia >= r || ib >= r || ia == ib) throw_invalid("invalid index pair to swap");
+  if (dims[ia] != dims[ib]) throw_invalid("swapped indices must have equal dimensions");
+  auto strides = row_major_strides(dims);
+  GateArgs a{};
+  std::vector<std::pair<Dim, Dim>> segs;
+  for (int i = 0; i < r;) {
+    if (i == ia || i == ib) {
+      ++i;
+      continue;
+    }
+    Dim size = 1;
+    int j = i;
+    while (j < r && j != ia && j != ib) size *= dims[j++];
+    if (size > 1) segs.push_back({size, strides[j - 1]});
+    i = j;
+  }
+  a.nseg = static_cast<int>(segs.size());
+  bool pow2 = true;
+  for (int j = 0; j < a.nseg; ++j) {
+    a.seg_size[j] = segs[j].first;
+    a.seg_stride[j] = segs[j].second;
+    int sh = 0;
+    while ((Dim(1) << sh) < segs[j].first) ++sh;
+    a.seg_shift[j] = sh;
+    if ((Dim(1) << sh) != segs[j].first) pow2 = false;
+  }
+  Dim total = 1;
+  for (Dim d : dims) total *= d;
+  Dim n_f = total / (dims[ia] * dims[ib]);
+  auto* p = static_cast<double2*>(data);
+  int d = static_cast<int>(dims[ia]);
+  if (pow2) k_swap_indices<true><<<grid_for(n_f), 256, 0, st>>>(p, n_f, d, strides[ia], strides[ib], a);
+  else k_swap_indices<false><<<grid_for(n_f), 256, 0, st>>>(p, n_f, d, strides[ia], strides[ib], a);
+  QTNH_LAUNCH_CHECK();
+}
+
 }  // namespace qtnhb

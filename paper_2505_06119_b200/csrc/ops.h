@@ -44,6 +44,11 @@ TP op_contract(const TP& a, const TP& b, const std::vector<int>& apos, const std
 // In-place gate on t (caller guarantees exclusive ownership).
 void op_gate_apply(TP& t, const std::vector<int>& targets, const double* gate, bool diagonal);
 
+// In-place (local) / remapped (distributed) exchange of two equal-size indices.
+void op_swap_indices(TP& t, int a, int b);
+// Fused QFT layer j on a qubit tensor (see gate.cu k_qft_layer).
+void op_qft_layer(TP& t, int j);
+
 // Kernels (zgemm.cu, gate.cu)
 void zgemm(const void* a, const void* b, void* c, Dim m, Dim n, Dim k, cudaStream_t st);
 // zgemm with A(m, k) gathered from a + rowoff[m] + coloff[k] (elements): the
@@ -57,6 +62,12 @@ void index_offsets(int64_t* out, Dim count, const std::vector<Dim>& dims, const 
 // singular values absorbed per QTNH_ABSORB_*; device row-major in/out.
 void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* u, void* s,
                  void* vh, int* sweeps_out);
+// Fused QFT layer on a local qubit block (all dims 2): H on bit t + the layer's
+// controlled phases; phase-only variant for a distributed target with x_j = 1.
+void qft_layer_local(void* data, int local_bits, int t, cudaStream_t st);
+void qft_phase_local(void* data, int local_bits, int64_t v_off, int t, cudaStream_t st);
+// In-place exchange of two equal-size local indices.
+void swap_indices_local(void* data, const std::vector<Dim>& dims, int ia, int ib, cudaStream_t st);
 // Gate on a dense local block: dims = local dims, targets = local positions.
 void gate_local(void* data, const std::vector<Dim>& dims, const std::vector<int>& targets,
                 const double* gate_host, bool diagonal, cudaStream_t st);

@@ -482,6 +482,19 @@ def apply_gate(state: Tensor, targets: Sequence[int], gate, diagonal: bool = Fal
     return state
 
 
+def swap_indices(state: Tensor, a: int, b: int) -> Tensor:
+    """In place: exchange indices a and b (equal dims) -- the values of
+    ops::permute with the two positions swapped."""
+    check(lib.qtnh_swap_indices(state._h, int(a), int(b)))
+    return state
+
+
+def qft_layer(state: Tensor, j: int) -> Tensor:
+    """In place: H on qubit j followed by all controlled phases of QFT layer j, one pass."""
+    check(lib.qtnh_qft_layer(state._h, int(j)))
+    return state
+
+
 # ---- factorisation (linalg.hpp:441-523; SPEC network::decompose) ---------------------------
 ABSORB_NONE, ABSORB_LEFT, ABSORB_RIGHT, ABSORB_SPLIT = 0, 1, 2, 3
 

@@ -21,8 +21,9 @@ def golden(name):
 
     import numpy as np
 
-    z = np.load(os.path.join(GOLDEN, name + ".npz"))
-    return json.loads(str(z["meta"])), z
+    with np.load(os.path.join(GOLDEN, name + ".npz")) as z:  # materialise: NpzFile is not thread-safe
+        arrays = {k: z[k] for k in z.files}
+    return json.loads(str(arrays.pop("meta"))), arrays
 
 
 def bits(x):

@@ -131,3 +131,52 @@ def test_qft_norm_preserved_large():
         ph = np.exp(2j * np.pi * ((j * k) % 2**n) / 2**n)
         want = np.dot(ph, st) / np.sqrt(2**n)
         assert abs(got[k] - want) < 1e-10 * max(1.0, abs(want))
+
+
+def test_fused_qft_matches_reference_qft16():
+    """Config 0 through the fused layer path (one pass per QFT layer + in-place swaps)."""
+    n = 16
+    st = circuits.counter_state(2025, 2**n)
+    st /= np.linalg.norm(st)
+
+    def body(rk):
+        t = Tensor.from_global(rk, IndexTuple([2] * n, 0), None, st)
+        return circuits.apply_qft_fused(t, n).to_global_vector()
+
+    got = run_collect(World(1), body)
+    want = oracle.ref().qft(n, st) if oracle.ref_available() else P.qft(n, st)
+    assert rel_l2(got, want) < TOL
+
+
+@pytest.mark.parametrize("world,split", [(8, 3), (2, 1), (4, 2)])
+def test_fused_qft_distributed(world, split):
+    n = 14
+    st = circuits.counter_state(17, 2**n)
+    st /= np.linalg.norm(st)
+
+    def body(rk):
+        t = Tensor.from_global(rk, IndexTuple([2] * n, split), DistParams(1, 1, 0), st)
+        return circuits.apply_qft_fused(t, n).to_global_vector()
+
+    got = World(world).run(body)[0]
+    assert rel_l2(got, P.qft(n, st)) < TOL
+
+
+@pytest.mark.parametrize("dims,split,a,b,world", [([2] * 10, 0, 1, 8, 1), ([3, 4, 3, 2], 0, 0, 2, 1),
+                                                  ([2] * 8, 2, 0, 6, 4), ([2] * 8, 2, 3, 7, 4)])
+def test_swap_indices_bit_exact(dims, split, a, b, world):
+    g = circuits.counter_state(5, int(np.prod(dims)))
+    g[::7] = complex(-0.0, -0.0)
+    g[1::11] = complex(-0.0, 1.0)
+    perm = list(range(len(dims)))
+    perm[a], perm[b] = perm[b], perm[a]
+
+    def body(rk):
+        t = Tensor.from_global(rk, IndexTuple(dims, split), DistParams(1, 1, 0), g)
+        from paper_2505_06119_b200.qtnh import swap_indices
+        swap_indices(t, a, b)
+        return t.to_global_vector()
+
+    got = World(world).run(body)[0]
+    from conftest import bits
+    assert np.array_equal(bits(got), bits(P.permute(dims, g, perm)))
