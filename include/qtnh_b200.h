@@ -89,8 +89,11 @@ int qtnh_world_abort(qtnh_world_t w);
 int qtnh_rank_bind(qtnh_world_t w, int rank, qtnh_rank_t* out);
 int qtnh_rank_release(qtnh_rank_t r);
 int qtnh_rank_id(qtnh_rank_t r);
-/* Stream the rank launches on (cudaStream_t as void*); set NULL for the rank's own. */
+/* Stream the rank launches on (cudaStream_t as void*; NULL = the legacy default
+ * stream, e.g. torch's default stream). qtnh_rank_reset_stream restores the
+ * rank's own non-blocking stream. */
 int qtnh_rank_set_stream(qtnh_rank_t r, void* stream);
+int qtnh_rank_reset_stream(qtnh_rank_t r);
 void* qtnh_rank_stream(qtnh_rank_t r);
 int qtnh_rank_synchronize(qtnh_rank_t r);
 int qtnh_barrier(qtnh_rank_t r);

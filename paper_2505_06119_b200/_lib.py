@@ -40,6 +40,7 @@ _SIGS = {
     "qtnh_rank_release": (i32, [vp]),
     "qtnh_rank_id": (i32, [vp]),
     "qtnh_rank_set_stream": (i32, [vp, vp]),
+    "qtnh_rank_reset_stream": (i32, [vp]),
     "qtnh_rank_stream": (vp, [vp]),
     "qtnh_rank_synchronize": (i32, [vp]),
     "qtnh_barrier": (i32, [vp]),

@@ -227,7 +227,14 @@ int qtnh_rank_id(qtnh_rank_t r) { return r ? r->ctx->rank : -1; }
 int qtnh_rank_set_stream(qtnh_rank_t r, void* stream) {
   return guard([&] {
     RankCtx& c = ctx_of(r);
-    c.stream = stream ? static_cast<cudaStream_t>(stream) : c.own_stream;
+    c.stream = static_cast<cudaStream_t>(stream);  // NULL = the legacy default stream
+  });
+}
+
+int qtnh_rank_reset_stream(qtnh_rank_t r) {
+  return guard([&] {
+    RankCtx& c = ctx_of(r);
+    c.stream = c.own_stream;
   });
 }
 

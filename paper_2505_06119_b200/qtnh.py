@@ -171,7 +171,13 @@ class Rank:
         return int(lib.qtnh_rank_stream(self._h) or 0)
 
     def set_stream(self, stream_ptr: Optional[int]) -> None:
-        check(lib.qtnh_rank_set_stream(self._h, C.c_void_p(stream_ptr or 0)))
+        """Launch on this cudaStream_t (0 = the legacy default stream, which is what
+        torch.cuda.current_stream().cuda_stream returns for torch's default stream);
+        None restores the rank's own non-blocking stream."""
+        if stream_ptr is None:
+            check(lib.qtnh_rank_reset_stream(self._h))
+        else:
+            check(lib.qtnh_rank_set_stream(self._h, C.c_void_p(stream_ptr)))
 
     def synchronize(self) -> None:
         check(lib.qtnh_rank_synchronize(self._h))

@@ -1,0 +1,62 @@
+"""Config 4: 40-qubit 1-D RCS (depth 20) evolved as an MPS with chi = 1024 on one
+GPU; reports total / per-layer time, bond dimensions, the truncation fidelity
+(product of kept-weight ratios) and the amplitudes of 1024 seeded bitstrings."""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=40)
+    ap.add_argument("--depth", type=int, default=20)
+    ap.add_argument("--chi", type=int, default=1024)
+    ap.add_argument("--seed", type=int, default=2025)
+    ap.add_argument("--bitstrings", type=int, default=1024)
+    args = ap.parse_args()
+    import numpy as np
+    import torch
+
+    from paper_2505_06119_b200 import circuits, mps
+    from paper_2505_06119_b200.qtnh import World
+
+    out = {"n": args.n, "depth": args.depth, "chi": args.chi}
+    layers = mps.rcs_1d_layers(args.n, args.depth, args.seed)
+
+    def body(rk):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rk.set_stream(torch.cuda.current_stream().cuda_stream)
+        m = mps.MPS(rk, args.n, args.chi)
+        per_layer = []
+        upd = 0
+        for li, (singles, pairs) in enumerate(layers):
+            tl = time.perf_counter()
+            for q, g in enumerate(singles):
+                m.apply_1q(q, mps.SINGLE_QUBIT[g])
+            for (q, _) in pairs:
+                m.apply_2q(q, circuits.FSIM)
+                upd += 1
+            torch.cuda.synchronize()
+            per_layer.append(time.perf_counter() - tl)
+        total = time.perf_counter() - t0
+        rng = np.random.default_rng(args.seed)
+        bits = rng.integers(0, 2, size=(args.bitstrings, args.n))
+        ta = time.perf_counter()
+        amps = m.amplitudes(bits)
+        out.update(total_s=total, per_layer_s=per_layer, updates=upd, bond_dims=m.bond_dims(),
+                   fidelity=float(np.exp(m.log_fidelity)), amp_time_s=time.perf_counter() - ta,
+                   amp_norm2_sum=float(np.sum(np.abs(amps) ** 2)), amp_first=[str(a) for a in amps[:4]])
+        m.free()
+
+    World(1).run(body)
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
