@@ -1,0 +1,230 @@
+"""Tensor networks contracted pairwise on the GPU (SPEC network::contract /
+contract_order; config 3 of BASELINE.json).
+
+A network is a set of device tensors whose indices carry labels; a label shared
+by two tensors is a bond. Contracting a pair sums over all their shared labels
+with qtnh.contract (result order open(a) then open(b)). The order is
+either supplied or chosen greedily: repeatedly contract the connected pair with
+the smallest result (ties broken by a seeded hash), the order SURVEY.md 8(d)
+fixes for config 3. The order is computed once on the host (plan()) and can be
+replayed by the reference oracle for parity.
+"""
+from __future__ import annotations
+
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import circuits, qtnh
+from .qtnh import IndexTuple, Tensor
+
+
+class Network:
+    def __init__(self, rank: qtnh.Rank):
+        self.rank = rank
+        self.tensors: Dict[int, Tensor] = {}
+        self.labels: Dict[int, List[str]] = {}
+        self.dims: Dict[str, int] = {}
+        self._next = 0
+
+    def add(self, data: np.ndarray, labels: Sequence[str]) -> int:
+        data = np.ascontiguousarray(data, dtype=np.complex128)
+        shape = list(data.shape) if data.ndim else []
+        assert len(shape) == len(labels)
+        for lab, d in zip(labels, shape):
+            if self.dims.setdefault(lab, d) != d:
+                raise qtnh.InvalidArgument(f"bond {lab} has inconsistent dimensions")
+        t = Tensor.from_global(self.rank, IndexTuple(shape, 0), None, data.reshape(-1))
+        i = self._next
+        self._next += 1
+        self.tensors[i] = t
+        self.labels[i] = list(labels)
+        return i
+
+    # -- planning (host only) ------------------------------------------------------------
+    @staticmethod
+    def _greedy(labels: Dict[int, List[str]], dims: Dict[str, int], seed: int, alpha: float, temp: float,
+                rng) -> List[Tuple[int, int]]:
+        """One greedy pass: contract the connected pair minimising
+        log2|result| - alpha (log2|a| + log2|b|) (+ Gaussian noise of width temp),
+        ties broken by hash_counter(seed, a, b)."""
+        import math
+
+        labels = {k: list(v) for k, v in labels.items()}
+        lsz = {k: sum(math.log2(dims[x]) for x in v) for k, v in labels.items()}
+        owners: Dict[str, List[int]] = {}
+        for t, ls in labels.items():
+            for lab in ls:
+                owners.setdefault(lab, []).append(t)
+        nxt = max(labels) + 1 if labels else 0
+        order = []
+        while len(labels) > 1:
+            pairs = {tuple(sorted(ts)) for ts in owners.values() if len(ts) == 2}
+            if not pairs:  # disconnected pieces: outer product of the two smallest
+                ids = sorted(labels, key=lambda t: (lsz[t], t))
+                pairs = {(ids[0], ids[1])}
+            best = None
+            for a, b in pairs:
+                shared = set(labels[a]) & set(labels[b])
+                r = lsz[a] + lsz[b] - 2 * sum(math.log2(dims[x]) for x in shared)
+                key = r - alpha * (lsz[a] + lsz[b])
+                if temp > 0:
+                    key += rng.gauss(0.0, temp)
+                key = (key, circuits.hash_counter(seed, a, b))
+                if best is None or key < best[0]:
+                    best = (key, a, b)
+            _, a, b = best
+            order.append((a, b))
+            shared = set(labels[a]) & set(labels[b])
+            new = [x for x in labels[a] if x not in shared] + [x for x in labels[b] if x not in shared]
+            for lab in labels[a] + labels[b]:
+                owners[lab] = [t for t in owners.get(lab, []) if t not in (a, b)]
+                if not owners[lab]:
+                    del owners[lab]
+            del labels[a], labels[b], lsz[a], lsz[b]
+            labels[nxt] = new
+            lsz[nxt] = sum(math.log2(dims[x]) for x in new)
+            for lab in new:
+                owners.setdefault(lab, []).append(nxt)
+            nxt += 1
+        return order
+
+    @staticmethod
+    def cost(labels: Dict[int, List[str]], dims: Dict[str, int], order) -> Tuple[float, int, float]:
+        """(sum of 8MNK flops, largest intermediate, sum of 16(|A|+|B|+|C|) bytes)."""
+        import math
+
+        L = {k: list(v) for k, v in labels.items()}
+        nxt = max(L) + 1
+        fl, big, by = 0.0, 0, 0.0
+        for s, (a, b) in enumerate(order):
+            la, lb = L.pop(a), L.pop(b)
+            sh = [x for x in la if x in lb]
+            M = math.prod(dims[x] for x in la if x not in sh)
+            N = math.prod(dims[x] for x in lb if x not in sh)
+            K = math.prod(dims[x] for x in sh)
+            fl += 8.0 * M * N * K
+            by += 16.0 * (M * K + K * N + M * N)
+            big = max(big, M * N)
+            L[nxt + s] = [x for x in la if x not in sh] + [x for x in lb if x not in sh]
+        return fl, big, by
+
+    @staticmethod
+    def plan(labels: Dict[int, List[str]], dims: Dict[str, int], seed: int = 0, trials: int = 16,
+             keep_open: Sequence[str] = ()) -> List[Tuple[int, int]]:
+        """Seeded greedy order. Trial 0 is the plain smallest-result greedy
+        (SURVEY.md 8(d)); further trials are seeded randomised greedy passes
+        (alpha, noise drawn from hash_counter(seed, 99, trial)); the order with the
+        smallest largest intermediate, then fewest flops, wins. Deterministic per
+        seed; the result of step s gets id max(ids) + 1 + s."""
+        import random
+
+        best = None
+        for t in range(max(1, trials)):
+            if t == 0:
+                alpha, temp, rng = 0.0, 0.0, None
+            else:
+                rng = random.Random(circuits.hash_counter(seed, 99, t))
+                alpha, temp = rng.random(), 0.5 * rng.random()
+            order = Network._greedy(labels, dims, seed, alpha, temp, rng)
+            fl, big, _ = Network.cost(labels, dims, order)
+            key = (big, fl)
+            if best is None or key < best[0]:
+                best = (key, order)
+        return best[1]
+
+    def contract_pair(self, a: int, b: int, new_id: Optional[int] = None) -> int:
+        la, lb = self.labels[a], self.labels[b]
+        shared = [x for x in la if x in lb]
+        apos = [la.index(x) for x in shared]
+        bpos = [lb.index(x) for x in shared]
+        c = qtnh.contract(self.tensors[a], self.tensors[b], apos, bpos)
+        new = [x for x in la if x not in shared] + [x for x in lb if x not in shared]
+        self.tensors.pop(a).free()
+        self.tensors.pop(b).free()
+        del self.labels[a], self.labels[b]
+        i = new_id if new_id is not None else self._next
+        self._next = max(self._next, i + 1)
+        self.tensors[i] = c
+        self.labels[i] = new
+        return i
+
+    def contract_order(self, order: Sequence[Tuple[int, int]]) -> int:
+        nxt = max(self.tensors) + 1
+        last = None
+        for s, (a, b) in enumerate(order):
+            if a not in self.tensors or b not in self.tensors:
+                raise qtnh.InvalidArgument("order references consumed ids")
+            last = self.contract_pair(a, b, nxt + s)
+        return last
+
+
+# ---- config 3: random circuit on a grid as a tensor network ---------------------------------
+def grid_pairs(pattern: str, rows: int, cols: int) -> List[Tuple[int, int]]:
+    """Entangling patterns: A/B horizontal (row parity
+    alternating), C/D vertical (column parity alternating); sites row-major."""
+    out = []
+    if pattern in "AB":
+        for r in range(rows):
+            c0 = (r + (0 if pattern == "A" else 1)) % 2
+            for c in range(c0, cols - 1, 2):
+                out.append((r * cols + c, r * cols + c + 1))
+    else:
+        for c in range(cols):
+            r0 = (c + (0 if pattern == "C" else 1)) % 2
+            for r in range(r0, rows - 1, 2):
+                out.append((r * cols + c, (r + 1) * cols + c))
+    return out
+
+
+def rcs_grid_circuit(rows: int, cols: int, depth: int, seed: int):
+    """Per layer: one of {sqrt X, sqrt Y, sqrt W} per qubit by
+    hash_counter(seed, layer, qubit) % 3, then fSim on the layer's pattern in the
+    cyclic order ABCDCDAB."""
+    seq = "ABCDCDAB"
+    gates = []
+    for layer in range(depth):
+        for q in range(rows * cols):
+            gates.append(("1q", (q,), circuits.hash_counter(seed, layer, q) % 3))
+        for a, b in grid_pairs(seq[layer % len(seq)], rows, cols):
+            gates.append(("fsim", (a, b), None))
+    return gates
+
+
+def output_bits(n: int, n_open: int, seed: int):
+    """Which qubits stay open (n_open of them, seeded) and the fixed bit of the rest."""
+    order = circuits.fisher_yates(seed, 11, n)
+    open_q = sorted(order[:n_open])
+    fixed = {q: circuits.hash_counter(seed, 12, q) % 2 for q in range(n) if q not in open_q}
+    return open_q, fixed
+
+
+def build_rcs_network(rank: qtnh.Rank, rows: int, cols: int, depth: int, seed: int, n_open: int = 6):
+    from .mps import SINGLE_QUBIT
+
+    n = rows * cols
+    net = Network(rank)
+    wire = [f"q{q}.0" for q in range(n)]
+    ver = [0] * n
+    for q in range(n):
+        net.add(np.array([1, 0], complex), [wire[q]])
+    for kind, qs, g in rcs_grid_circuit(rows, cols, depth, seed):
+        if kind == "1q":
+            q = qs[0]
+            ver[q] += 1
+            new = f"q{q}.{ver[q]}"
+            net.add(SINGLE_QUBIT[g], [new, wire[q]])  # (out, in)
+            wire[q] = new
+        else:
+            a, b = qs
+            ver[a] += 1
+            ver[b] += 1
+            na, nb = f"q{a}.{ver[a]}", f"q{b}.{ver[b]}"
+            net.add(circuits.FSIM.reshape(2, 2, 2, 2), [na, nb, wire[a], wire[b]])
+            wire[a], wire[b] = na, nb
+    open_q, fixed = output_bits(n, n_open, seed)
+    for q, bit in fixed.items():
+        v = np.zeros(2, complex)
+        v[bit] = 1
+        net.add(v, [wire[q]])
+    return net, [wire[q] for q in open_q], open_q, fixed
