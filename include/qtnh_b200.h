@@ -150,6 +150,16 @@ int qtnh_scale(qtnh_tensor_t t, double re, double im, qtnh_tensor_t* out);
 int qtnh_contract(qtnh_tensor_t a, qtnh_tensor_t b, int n_pairs, const int* a_pos,
                   const int* b_pos, qtnh_tensor_t* out);
 
+/* Contraction with both operands and the result in HOST memory (the reference's
+ * contract takes host-resident std::vector tensors): A is streamed through the GPU
+ * in chunks of its leading open indices; H2D of chunk i+1, the GEMM of chunk i and
+ * the D2H of chunk i-1 overlap on three streams (use pinned memory for overlap).
+ * Result order/values as qtnh_contract on undistributed tensors; c_dims receives
+ * the result dims (may be NULL). Completes on the rank's stream. */
+int qtnh_contract_host(qtnh_rank_t r, int na, const int64_t* dims_a, const double* a, int nb,
+                       const int64_t* dims_b, const double* b, int n_pairs, const int* a_pos, const int* b_pos,
+                       double* c, int64_t* c_dims);
+
 /* In-place gate application on a state whose indices all have the same role as
  * in contract(state, gate) followed by a permute that puts the gate outputs back
  * at `targets`. gate: host row-major D x D complex matrix, D = prod dims[targets],

@@ -497,6 +497,28 @@ void make_exclusive(TP& p) {
 }
 }  // namespace
 
+int qtnh_contract_host(qtnh_rank_t r, int na, const int64_t* dims_a, const double* a, int nb,
+                       const int64_t* dims_b, const double* b, int n_pairs, const int* a_pos, const int* b_pos,
+                       double* c, int64_t* c_dims) {
+  return guard([&] {
+    RankCtx& x = ctx_of(r);
+    need(a, "a");
+    need(b, "b");
+    need(c, "c");
+    if (na > 0) need(dims_a, "dims_a");
+    if (nb > 0) need(dims_b, "dims_b");
+    std::vector<Dim> da(dims_a, dims_a + na), db(dims_b, dims_b + nb), cd;
+    for (Dim d : da)
+      if (d < 1) throw_invalid("index dimensions must be positive");
+    for (Dim d : db)
+      if (d < 1) throw_invalid("index dimensions must be positive");
+    contract_host(x, da, a, db, b, std::vector<int>(a_pos, a_pos + n_pairs), std::vector<int>(b_pos, b_pos + n_pairs),
+                  c, &cd, 16);
+    if (c_dims)
+      for (size_t i = 0; i < cd.size(); ++i) c_dims[i] = cd[i];
+  });
+}
+
 int qtnh_swap_indices(qtnh_tensor_t t, int a, int b) {
   return guard([&] {
     TP& p = impl_of(t);

@@ -16,6 +16,8 @@
 //     FP64-tensor-core zgemm whose row-major output IS its block of the result in
 //     the SPEC.md:408 order (open(a) then open(b)).
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <numeric>
 
 #include "ops.h"
@@ -316,6 +318,172 @@ void op_qft_layer(TP& t, int j) {
   for (int l = j + 1; l < s.split; ++l) v_off = (v_off << 1) | cd[l];
   v_off <<= lb;
   qft_phase_local(t->data(), lb, v_off, n - 1 - j, r.stream);
+}
+
+}  // namespace qtnhb
+
+// ---- host-buffer contraction, streamed through the GPU --------------------------------
+namespace qtnhb {
+
+namespace {
+struct PipeRes {
+  cudaStream_t s[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev[3][3];  // [slot][h2d, comp, d2h]
+  int device = -1;
+};
+std::mutex g_pipe_mu;
+std::map<const RankCtx*, PipeRes> g_pipes;  // per rank (ranks may share a device)
+
+PipeRes& pipes(const RankCtx& r) {
+  std::lock_guard<std::mutex> lk(g_pipe_mu);
+  PipeRes& p = g_pipes[&r];
+  if (p.device < 0) {
+    p.device = r.device;
+    for (int i = 0; i < 3; ++i) QTNH_CUDA(cudaStreamCreateWithFlags(&p.s[i], cudaStreamNonBlocking));
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) QTNH_CUDA(cudaEventCreateWithFlags(&p.ev[i][j], cudaEventDisableTiming));
+  }
+  return p;
+}
+}  // namespace
+
+// C = contract(A, B) (SPEC.md:408 order) with A, B, C in host memory. A is cut
+// along its leading open indices into chunks whose host memory is a few long
+// runs and whose results are contiguous slices of C; three streams overlap the
+// H2D of chunk i+1, the gather-GEMM of chunk i and the D2H of chunk i-1.
+void contract_host(RankCtx& r, const std::vector<Dim>& da, const double* a, const std::vector<Dim>& db,
+                   const double* b, const std::vector<int>& apos, const std::vector<int>& bpos, double* c,
+                   std::vector<Dim>* c_dims, int target_chunks) {
+  int na = static_cast<int>(da.size()), nb = static_cast<int>(db.size());
+  std::vector<char> ca(na, 0), cb(nb, 0);
+  if (apos.size() != bpos.size()) throw_invalid("contracted position lists differ in length");
+  for (size_t i = 0; i < apos.size(); ++i) {
+    int p = apos[i], q = bpos[i];
+    if (p < 0 || p >= na || ca[p] || q < 0 || q >= nb || cb[q]) throw_invalid("invalid contracted index positions");
+    if (da[p] != db[q]) throw_invalid("contracted dimensions differ");
+    ca[p] = cb[q] = 1;
+  }
+  std::vector<int> a_open, b_open;
+  for (int i = 0; i < na; ++i)
+    if (!ca[i]) a_open.push_back(i);
+  for (int i = 0; i < nb; ++i)
+    if (!cb[i]) b_open.push_back(i);
+  Dim M = 1, N = 1, K = 1;
+  for (int p : a_open) M *= da[p];
+  for (int q : b_open) N *= db[q];
+  for (int p : apos) K *= da[p];
+  if (c_dims) {
+    c_dims->clear();
+    for (int p : a_open) c_dims->push_back(da[p]);
+    for (int q : b_open) c_dims->push_back(db[q]);
+  }
+  // chunk positions: leading positions 0..D-1; their open ones index the chunks
+  int D = 0;
+  Dim nchunks = 1, runs = 1;
+  while (D < na && nchunks < target_chunks && runs <= 16) {
+    if (ca[D]) runs *= da[D];
+    else nchunks *= da[D];
+    ++D;
+  }
+  auto sa = row_major_strides(da);
+  std::vector<int> lead_open, lead_contr;
+  for (int p = 0; p < D; ++p) (ca[p] ? lead_contr : lead_open).push_back(p);
+  // chunk sub-tensor: dims [lead contracted..., da[D:]...]
+  std::vector<Dim> sub_dims;
+  std::vector<int> sub_pos_of(na, -1);
+  for (int p : lead_contr) {
+    sub_pos_of[p] = static_cast<int>(sub_dims.size());
+    sub_dims.push_back(da[p]);
+  }
+  for (int p = D; p < na; ++p) {
+    sub_pos_of[p] = static_cast<int>(sub_dims.size());
+    sub_dims.push_back(da[p]);
+  }
+  Dim tail = 1;
+  for (int p = D; p < na; ++p) tail *= da[p];
+  const Dim chunk_elems = runs * tail, Mc = M / nchunks;
+  auto sub_strides = row_major_strides(sub_dims);
+  // gather tables of the chunk's A(m, k): rows = its open indices, cols = pairs
+  std::vector<Dim> rd, rs, cd, cs;
+  for (int p : a_open)
+    if (p >= D) {
+      rd.push_back(da[p]);
+      rs.push_back(sub_strides[sub_pos_of[p]]);
+    }
+  for (int p : apos) {
+    cd.push_back(da[p]);
+    cs.push_back(sub_strides[sub_pos_of[p]]);
+  }
+  auto min_stride = [](const std::vector<Dim>& d, const std::vector<Dim>& st) {
+    Dim m = Dim(1) << 62;
+    for (size_t i = 0; i < d.size(); ++i)
+      if (d[i] > 1) m = std::min(m, st[i]);
+    return m;
+  };
+  bool rows_fastest = min_stride(rd, rs) <= min_stride(cd, cs);
+  PipeRes& pr = pipes(r);
+  cudaStream_t s_in = pr.s[0], s_cmp = pr.s[1], s_out = pr.s[2];
+  // the caller's stream orders before us
+  QTNH_CUDA(cudaEventRecord(pr.ev[0][0], r.stream));
+  for (int i = 0; i < 3; ++i) QTNH_CUDA(cudaStreamWaitEvent(pr.s[i], pr.ev[0][0], 0));
+  // resident B, permuted to [contracted (pair order) | open]
+  DevBuf dB(static_cast<size_t>(K * N) * 16, r), dBp(static_cast<size_t>(K * N) * 16, r);
+  DevBuf tabs(static_cast<size_t>(Mc + K) * 8, r);
+  auto* ro = static_cast<int64_t*>(tabs.ptr);
+  auto* co = ro + Mc;
+  QTNH_CUDA(cudaMemcpyAsync(dB.ptr, b, K * N * 16, cudaMemcpyHostToDevice, r.stream));
+  std::vector<int> bp(bpos.begin(), bpos.end());
+  bp.insert(bp.end(), b_open.begin(), b_open.end());
+  strided_copy(dB.ptr, dBp.ptr, permute_box(db, bp), false, r.stream);
+  index_offsets(ro, Mc, rd, rs, r.stream);
+  index_offsets(co, K, cd, cs, r.stream);
+  QTNH_CUDA(cudaEventRecord(pr.ev[1][0], r.stream));
+  QTNH_CUDA(cudaStreamWaitEvent(s_cmp, pr.ev[1][0], 0));
+  const int slots = 3;
+  std::vector<std::unique_ptr<DevBuf>> abuf, cbuf;
+  for (int i = 0; i < slots && i < nchunks; ++i) {
+    abuf.emplace_back(new DevBuf(static_cast<size_t>(chunk_elems) * 16, r));
+    cbuf.emplace_back(new DevBuf(static_cast<size_t>(Mc * N) * 16, r));
+  }
+  // the slot buffers were allocated on r.stream: make the pipeline streams wait
+  QTNH_CUDA(cudaEventRecord(pr.ev[2][0], r.stream));
+  for (int i = 0; i < 3; ++i) QTNH_CUDA(cudaStreamWaitEvent(pr.s[i], pr.ev[2][0], 0));
+  std::vector<Dim> lo_dims;
+  for (int p : lead_open) lo_dims.push_back(da[p]);
+  std::vector<Dim> lc_dims;
+  for (int p : lead_contr) lc_dims.push_back(da[p]);
+  std::vector<bool> used(slots, false);
+  for (Dim ch = 0; ch < nchunks; ++ch) {
+    int sl = static_cast<int>(ch % slots);
+    auto co_open = unflat(ch, lo_dims);
+    Dim base = 0;
+    for (size_t i = 0; i < lead_open.size(); ++i) base += co_open[i] * sa[lead_open[i]];
+    // H2D: after the compute that last read this slot
+    if (used[sl]) QTNH_CUDA(cudaStreamWaitEvent(s_in, pr.ev[sl][1], 0));
+    for (Dim rr = 0; rr < runs; ++rr) {
+      auto cr = unflat(rr, lc_dims);
+      Dim off = base;
+      for (size_t i = 0; i < lead_contr.size(); ++i) off += cr[i] * sa[lead_contr[i]];
+      QTNH_CUDA(cudaMemcpyAsync(static_cast<char*>(abuf[sl]->ptr) + rr * tail * 16, a + 2 * off, tail * 16,
+                                cudaMemcpyHostToDevice, s_in));
+    }
+    QTNH_CUDA(cudaEventRecord(pr.ev[sl][0], s_in));
+    // compute: after the H2D of this chunk and the D2H that last read the slot
+    QTNH_CUDA(cudaStreamWaitEvent(s_cmp, pr.ev[sl][0], 0));
+    if (used[sl]) QTNH_CUDA(cudaStreamWaitEvent(s_cmp, pr.ev[sl][2], 0));
+    zgemm_gather_a(abuf[sl]->ptr, ro, co, rows_fastest, dBp.ptr, cbuf[sl]->ptr, Mc, N, K, s_cmp);
+    QTNH_CUDA(cudaEventRecord(pr.ev[sl][1], s_cmp));
+    // D2H of the contiguous C slice
+    QTNH_CUDA(cudaStreamWaitEvent(s_out, pr.ev[sl][1], 0));
+    QTNH_CUDA(cudaMemcpyAsync(c + 2 * ch * Mc * N, cbuf[sl]->ptr, Mc * N * 16, cudaMemcpyDeviceToHost, s_out));
+    QTNH_CUDA(cudaEventRecord(pr.ev[sl][2], s_out));
+    used[sl] = true;
+  }
+  // the caller's stream (and the buffers' release) come after the pipeline
+  for (int i = 0; i < 3; ++i) {
+    QTNH_CUDA(cudaEventRecord(pr.ev[i][0], pr.s[i]));
+    QTNH_CUDA(cudaStreamWaitEvent(r.stream, pr.ev[i][0], 0));
+  }
 }
 
 }  // namespace qtnhb

@@ -49,6 +49,11 @@ void op_swap_indices(TP& t, int a, int b);
 // Fused QFT layer j on a qubit tensor (see gate.cu k_qft_layer).
 void op_qft_layer(TP& t, int j);
 
+// Contraction with host operands/result, pipelined H2D / GEMM / D2H (single rank).
+void contract_host(RankCtx& r, const std::vector<Dim>& da, const double* a, const std::vector<Dim>& db,
+                   const double* b, const std::vector<int>& apos, const std::vector<int>& bpos, double* c,
+                   std::vector<Dim>* c_dims, int target_chunks);
+
 // Kernels (zgemm.cu, gate.cu)
 void zgemm(const void* a, const void* b, void* c, Dim m, Dim n, Dim k, cudaStream_t st);
 // zgemm with A(m, k) gathered from a + rowoff[m] + coloff[k] (elements): the

@@ -480,6 +480,24 @@ def contract(a: Tensor, b: Tensor, a_pos: Sequence[int], b_pos: Sequence[int]) -
     return a._new(h)
 
 
+def contract_host(rank: Rank, a: np.ndarray, b: np.ndarray, a_pos: Sequence[int], b_pos: Sequence[int],
+                  out: Optional[np.ndarray] = None) -> np.ndarray:
+    """Contraction of host arrays (open(a) then open(b) order), streamed through the
+    GPU with H2D / GEMM / D2H overlapped; pass pinned arrays for full overlap."""
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    b = np.ascontiguousarray(b, dtype=np.complex128)
+    if len(a_pos) != len(b_pos):
+        raise InvalidArgument("contracted position lists differ in length")
+    odims = [a.shape[i] for i in range(a.ndim) if i not in a_pos] + [b.shape[i] for i in range(b.ndim) if i not in b_pos]
+    if out is None:
+        out = np.empty(odims, dtype=np.complex128)
+    cd = i64_array([0] * max(1, len(odims)))
+    check(lib.qtnh_contract_host(rank._h, a.ndim, i64_array(a.shape), a.ctypes.data, b.ndim, i64_array(b.shape),
+                                 b.ctypes.data, len(a_pos), i32_array(a_pos), i32_array(b_pos), out.ctypes.data, cd))
+    rank.synchronize()
+    return out.reshape(odims)
+
+
 def apply_gate(state: Tensor, targets: Sequence[int], gate, diagonal: bool = False) -> Tensor:
     """In-place gate (row index = gate output, targets[0] most significant).
     Values equal contract(state, gate) followed by a permute back."""

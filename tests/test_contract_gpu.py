@@ -126,3 +126,21 @@ def test_zgemm_device_against_numpy(m, n, k):
 
     w.run(body)
     assert rel_l2(tc.cpu().numpy(), a @ b) < 1e-13
+
+
+@pytest.mark.parametrize("da,db,ap,bp", [
+    ([2] * 16, [2] * 6, [1, 4, 9], [0, 2, 5]),        # leading contracted position inside the chunk runs
+    ([2] * 14, [2] * 6, [3, 13], [1, 0]),             # chunks over the first open positions
+    ([3, 5, 4, 6], [6, 4, 7], [2, 3], [1, 0]),
+    ([4, 3], [3, 2], [1], [0]),
+])
+def test_contract_host_pipeline(da, db, ap, bp):
+    a = circuits.rng_normals(8, int(np.prod(da))).reshape(da)
+    b = circuits.rng_normals(9, int(np.prod(db))).reshape(db)
+
+    def body(rk):
+        return qtnh.contract_host(rk, a, b, ap, bp)
+
+    got = run_collect(World(1), body)
+    want = P.contract(da, a.reshape(-1), db, b.reshape(-1), ap, bp)
+    assert rel_l2(got.reshape(-1), want) < TOL
