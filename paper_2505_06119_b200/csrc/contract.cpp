@@ -19,6 +19,7 @@
 #include <map>
 #include <mutex>
 #include <numeric>
+#include <tuple>
 
 #include "ops.h"
 #include "strided_copy.h"
@@ -43,6 +44,48 @@ const void* local_permuted(const TensorImpl& t, const std::vector<Dim>& dims, co
   hold = std::make_shared<DevBuf>(static_cast<size_t>(n) * 16, r);
   strided_copy(t.data(), hold->ptr, permute_box(dims, perm), false, r.stream);
   return hold->ptr;
+}
+
+// Offset tables of the fused-gather GEMM, cached per (device, dims, strides):
+// a contraction repeated with the same layout (every bench step, every MPS
+// update of a saturated bond) reuses them instead of regenerating 16 MB.
+struct TableKey {
+  int device;
+  std::vector<Dim> dims, strides;
+  bool operator<(const TableKey& o) const {
+    return std::tie(device, dims, strides) < std::tie(o.device, o.dims, o.strides);
+  }
+};
+struct TableVal {
+  int64_t* ptr = nullptr;
+  size_t bytes = 0;
+};
+std::mutex g_tab_mu;
+std::map<TableKey, TableVal> g_tabs;
+size_t g_tab_bytes = 0;
+
+const int64_t* gather_table(RankCtx& r, const std::vector<Dim>& dims, const std::vector<Dim>& strides) {
+  TableKey key{r.device, dims, strides};
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  auto it = g_tabs.find(key);
+  if (it != g_tabs.end()) return it->second.ptr;
+  Dim count = 1;
+  for (Dim d : dims) count *= d;
+  if (g_tab_bytes > (size_t(1) << 30)) {  // bounded: drop everything (tables are cheap to rebuild)
+    QTNH_CUDA(cudaStreamSynchronize(r.stream));
+    for (auto& kv : g_tabs) cudaFree(kv.second.ptr);
+    g_tabs.clear();
+    g_tab_bytes = 0;
+  }
+  TableVal v;
+  v.bytes = static_cast<size_t>(std::max<Dim>(1, count)) * 8;
+  QTNH_CUDA(cudaMalloc(&v.ptr, v.bytes));
+  index_offsets(v.ptr, count, dims, strides, r.stream);
+  // other ranks (streams) on this device may pick the table up right away
+  QTNH_CUDA(cudaStreamSynchronize(r.stream));
+  g_tabs[key] = v;
+  g_tab_bytes += v.bytes;
+  return v.ptr;
 }
 
 }  // namespace
@@ -182,11 +225,8 @@ TP op_contract(const TP& a_in, const TP& b_in, const std::vector<int>& apos, con
         return m;
       };
       Dim min_r = min_stride(rd, rs), min_c = min_stride(cd, cs);
-      DevBuf tabs(static_cast<size_t>(M + K) * 8, r);
-      auto* ro = static_cast<int64_t*>(tabs.ptr);
-      auto* co = ro + M;
-      index_offsets(ro, M, rd, rs, r.stream);
-      index_offsets(co, K, cd, cs, r.stream);
+      const int64_t* ro = gather_table(r, rd, rs);
+      const int64_t* co = gather_table(r, cd, cs);
       zgemm_gather_a(a->data(), ro, co, min_r <= min_c, B, c2->data(), M, N, K, r.stream);
     }
   }

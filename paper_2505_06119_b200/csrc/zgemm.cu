@@ -46,17 +46,19 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int BK_, int STAGES_, int MINB_>
+template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int BK_, int STAGES_, int MINB_, int WTM_ = 32,
+          int WTN_ = 32>
 struct Cfg {
   static constexpr int BM = BM_, BN = BN_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, BK = BK_,
                        STAGES = STAGES_, MINB = MINB_;
+  static constexpr int WTM = WTM_, WTN = WTN_, MI = WTM / 8, NJ = WTN / 8;  // warp tile
   static constexpr int THREADS = WARPS_M * WARPS_N * 32;
   static constexpr int PA = BM + 2;  // 16-B elements; = 2 (mod 8)
   static constexpr int PB = BN + 2;
   static constexpr int A_ELEMS = BK * PA;
   static constexpr int B_ELEMS = BK * PB;
   static constexpr size_t SMEM = static_cast<size_t>(STAGES) * (A_ELEMS + B_ELEMS) * 16;
-  static_assert(BM == WARPS_M * 32 && BN == WARPS_N * 32, "warp tile is 32 x 32");
+  static_assert(BM == WARPS_M * WTM && BN == WARPS_N * WTN, "CTA tile = warps x warp tile");
   static_assert((BM * BK) % THREADS == 0 && (BN * BK) % THREADS == 0, "even load split");
 };
 
@@ -79,8 +81,12 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / G::WARPS_N, wn = warp % G::WARPS_N;
-  const int64_t bm = static_cast<int64_t>(blockIdx.y) * BM;
-  const int64_t bn = static_cast<int64_t>(blockIdx.x) * BN;
+  // 1-D grid, N tiles fastest: the CTAs sharing a row block of A run together
+  // (A read once from HBM), and M is not limited by gridDim.y.
+  const int64_t n_tiles_n = (N + BN - 1) / BN;
+  const int64_t tile = blockIdx.x;
+  const int64_t bm = (tile / n_tiles_n) * BM;
+  const int64_t bn = (tile % n_tiles_n) * BN;
   const int64_t n_kt = (K + BK - 1) / BK;
 
   // Per-thread source rows / columns are fixed; only k advances by BK per stage.
@@ -134,11 +140,12 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
     }
   };
 
-  double acc_re[4][4][2], acc_im[4][4][2];
+  constexpr int MI = G::MI, NJ = G::NJ;
+  double acc_re[MI][NJ][2], acc_im[MI][NJ][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       acc_re[i][j][0] = acc_re[i][j][1] = 0.0;
       acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
     }
@@ -153,35 +160,35 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
   for (int64_t kt = 0; kt < n_kt; ++kt) {
     cp_wait<STAGES - 2>();
     __syncthreads();
-    const double2* as = As + (kt % STAGES) * G::A_ELEMS + wm * 32 + fr;
-    const double2* bs = Bs + (kt % STAGES) * G::B_ELEMS + wn * 32 + fr;
+    const double2* as = As + (kt % STAGES) * G::A_ELEMS + wm * G::WTM + fr;
+    const double2* bs = Bs + (kt % STAGES) * G::B_ELEMS + wn * G::WTN + fr;
 #pragma unroll
     for (int k4 = 0; k4 < BK; k4 += 4) {
-      double a_re[4], a_im[4], b_re[4], b_im[4], nb_im[4];
+      double a_re[MI], a_im[MI], b_re[NJ], b_im[NJ], nb_im[NJ];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < MI; ++i) {
         double2 v = as[(k4 + fk) * G::PA + i * 8];
         a_re[i] = v.x;
         a_im[i] = v.y;
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < NJ; ++j) {
         double2 v = bs[(k4 + fk) * G::PB + j * 8];
         b_re[j] = v.x;
         b_im[j] = v.y;
         nb_im[j] = -v.y;
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < NJ; ++j) {
           dmma(acc_re[i][j], a_re[i], b_re[j]);
           dmma(acc_im[i][j], a_re[i], b_im[j]);
         }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < NJ; ++j) {
           dmma(acc_re[i][j], a_im[i], nb_im[j]);
           dmma(acc_im[i][j], a_im[i], b_re[j]);
         }
@@ -199,12 +206,12 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
 
   // Epilogue: lane holds C[fr][2*fk + {0,1}] of each 8x8 sub-tile.
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int64_t row = bm + wm * 32 + i * 8 + fr;
+  for (int i = 0; i < MI; ++i) {
+    int64_t row = bm + wm * G::WTM + i * 8 + fr;
     if (row >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int64_t col = bn + wn * 32 + j * 8 + 2 * fk;
+    for (int j = 0; j < NJ; ++j) {
+      int64_t col = bn + wn * G::WTN + j * 8 + 2 * fk;
       double2* dst = C + row * N + col;
       if (col + 1 < N) {
         dst[0] = make_double2(acc_re[i][j][0], acc_im[i][j][0]);
@@ -220,15 +227,10 @@ template <class G, int MODE>
 void launch_mode(const double2* a, const int64_t* ro, const int64_t* co, const double2* b, double2* c, Dim m,
                  Dim n, Dim k, cudaStream_t st) {
   QTNH_CUDA(cudaFuncSetAttribute(k_zgemm<G, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
-  Dim rows = static_cast<Dim>(65535) * G::BM;
-  for (Dim m0 = 0; m0 < m; m0 += rows) {  // grid.y limit
-    Dim mm = std::min(rows, m - m0);
-    dim3 grid(static_cast<unsigned>((n + G::BN - 1) / G::BN), static_cast<unsigned>((mm + G::BM - 1) / G::BM));
-    const double2* am = MODE == 0 ? a + m0 * k : a;
-    const int64_t* rom = MODE == 0 ? ro : ro + m0;
-    k_zgemm<G, MODE><<<grid, G::THREADS, G::SMEM, st>>>(am, rom, co, b, c + m0 * n, mm, n, k);
-    QTNH_LAUNCH_CHECK();
-  }
+  Dim tiles = ((m + G::BM - 1) / G::BM) * ((n + G::BN - 1) / G::BN);
+  if (tiles > 0x7fffffff) throw_invalid("zgemm problem too large for one launch");
+  k_zgemm<G, MODE><<<static_cast<unsigned>(tiles), G::THREADS, G::SMEM, st>>>(a, ro, co, b, c, m, n, k);
+  QTNH_LAUNCH_CHECK();
 }
 
 template <class G>
@@ -266,6 +268,10 @@ using V6 = Cfg<64, 64, 2, 2, 8, 6, 2>;    // deeper pipeline
 using V7 = Cfg<32, 64, 1, 2, 8, 3, 5>;    // 64 thr, 5 CTA/SM (<= 204 regs)
 using V8 = Cfg<32, 128, 1, 4, 8, 4, 2>;   // 128 thr, 2 CTA/SM
 using V9 = Cfg<32, 64, 1, 2, 16, 3, 4>;   // 64 thr, BK 16
+using V10 = Cfg<32, 64, 1, 4, 8, 3, 4, 32, 16>;   // warp tile 32x16, 128 thr, 16 warps/SM
+using V11 = Cfg<64, 64, 2, 4, 8, 3, 2, 32, 16>;   // warp tile 32x16, 256 thr
+using V12 = Cfg<32, 64, 2, 2, 8, 3, 4, 16, 32>;   // warp tile 16x32, 128 thr
+using V13 = Cfg<32, 32, 2, 2, 8, 4, 6, 16, 16>;   // warp tile 16x16, 128 thr, 24 warps/SM
 
 int variant() {
   static int v = [] {
@@ -304,14 +310,14 @@ void zgemm_gather_a(const void* a, const int64_t* rowoff, const int64_t* coloff,
   auto Cp = static_cast<double2*>(c);
   static int gv = [] {
     const char* e = std::getenv("QTNH_ZGEMM_GATHER_VARIANT");
-    return e ? std::atoi(e) : 7;
+    return e ? std::atoi(e) : 12;
   }();
   if (n > 32 && gv == 7) {
     if (rows_fastest) launch_mode<V7, 1>(A, rowoff, coloff, B, Cp, m, n, k, st);
     else launch_mode<V7, 2>(A, rowoff, coloff, B, Cp, m, n, k, st);
   } else if (n > 32) {
-    if (rows_fastest) launch_mode<V3, 1>(A, rowoff, coloff, B, Cp, m, n, k, st);
-    else launch_mode<V3, 2>(A, rowoff, coloff, B, Cp, m, n, k, st);
+    if (rows_fastest) launch_mode<V12, 1>(A, rowoff, coloff, B, Cp, m, n, k, st);
+    else launch_mode<V12, 2>(A, rowoff, coloff, B, Cp, m, n, k, st);
   } else {
     if (rows_fastest) launch_mode<V4, 1>(A, rowoff, coloff, B, Cp, m, n, k, st);
     else launch_mode<V4, 2>(A, rowoff, coloff, B, Cp, m, n, k, st);
@@ -338,9 +344,13 @@ void zgemm(const void* a, const void* b, void* c, Dim m, Dim n, Dim k, cudaStrea
     case 7: return launch<V7>(A, B, Cp, m, n, k, st);
     case 8: return launch<V8>(A, B, Cp, m, n, k, st);
     case 9: return launch<V9>(A, B, Cp, m, n, k, st);
+    case 10: return launch<V10>(A, B, Cp, m, n, k, st);
+    case 11: return launch<V11>(A, B, Cp, m, n, k, st);
+    case 12: return launch<V12>(A, B, Cp, m, n, k, st);
+    case 13: return launch<V13>(A, B, Cp, m, n, k, st);
     default: break;
   }
-  if (n > 32) launch<V7>(A, B, Cp, m, n, k, st);
+  if (n > 32) launch<V12>(A, B, Cp, m, n, k, st);
   else launch<V4>(A, B, Cp, m, n, k, st);
 }
 
