@@ -179,6 +179,11 @@ struct Plan {
   int* d_slot = nullptr;
   int grid = 0;
   size_t smem = 0;
+  ~Plan() {  // only on cache eviction (cudaFree synchronises the device)
+    if (d_tin) cudaFree(d_tin);
+    if (d_tout) cudaFree(d_tout);
+    if (d_slot) cudaFree(d_slot);
+  }
 };
 
 int sm_count(int dev) {

@@ -22,6 +22,7 @@
 //   one output kernel.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <numeric>
 #include <vector>
@@ -32,6 +33,9 @@ namespace qtnhb {
 
 namespace {
 
+#ifndef QTNH_SVD_SORT_ROWS
+#define QTNH_SVD_SORT_ROWS 0
+#endif
 constexpr int kB = 16;        // rows per block
 constexpr int kP2 = 2 * kB;   // rows per pair (inner problem size)
 constexpr int kGramCols = 64; // column chunk of the Gram kernel
@@ -55,8 +59,8 @@ __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -
 
 // ---- init: WK = [A or A^H (zero-padded rows) | I] ------------------------------------
 __global__ void k_svd_init(const double2* __restrict__ a, double2* __restrict__ wk, int64_t m, int64_t n,
-                           int64_t rows, int64_t rp, int64_t L, int transpose) {
-  const int64_t W = L + rp;
+                           int64_t rows, int64_t rp, int64_t L, int64_t qw, int transpose) {
+  const int64_t W = L + qw;
   const int64_t mat = blockIdx.y;
   const double2* A = a + mat * m * n;
   double2* K = wk + mat * rp * W;
@@ -66,7 +70,7 @@ __global__ void k_svd_init(const double2* __restrict__ a, double2* __restrict__ 
     double2 v = make_double2(0.0, 0.0);
     if (j < L) {
       if (i < rows) v = transpose ? cconj(A[j * n + i]) : A[i * n + j];
-    } else if (j - L == i) {
+    } else if (qw > 0 && j - L == i) {
       v = make_double2(1.0, 0.0);
     }
     K[e] = v;
@@ -76,9 +80,9 @@ __global__ void k_svd_init(const double2* __restrict__ a, double2* __restrict__ 
 // ---- Gram partials: part[mat][pair][split] = X_pair[:, cols] X_pair[:, cols]^H ------
 __global__ void __launch_bounds__(256) k_svd_gram(const double2* __restrict__ wk, double2* __restrict__ part,
                                                   const int* __restrict__ tab, int round, int npairs, int splits,
-                                                  int64_t rp, int64_t L) {
+                                                  int64_t rp, int64_t L, int64_t qw) {
   const int pair = blockIdx.x, split = blockIdx.y, mat = blockIdx.z;
-  const int64_t W = L + rp;
+  const int64_t W = L + qw;
   const int* pr = tab + (static_cast<int64_t>(round) * npairs + pair) * 2;
   const int bi = pr[0], bj = pr[1];
   const double2* K = wk + static_cast<int64_t>(mat) * rp * W;
@@ -122,6 +126,8 @@ __global__ void __launch_bounds__(256) k_svd_gram(const double2* __restrict__ wk
 }
 
 // ---- inner eigensolver: W with W^H G W diagonal; writes W^H ----------------------------
+__device__ __forceinline__ bool sort_rows() { return QTNH_SVD_SORT_ROWS; }
+
 __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
   // non-negative doubles order like their bit patterns
   atomicMax(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(__double_as_longlong(v)));
@@ -129,8 +135,13 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 
 __global__ void __launch_bounds__(256) k_svd_eigen(const double2* __restrict__ part, double2* __restrict__ wh,
                                                    int* __restrict__ flags, double* __restrict__ off_max,
-                                                   int npairs, int splits, double tol, int inner_sweeps) {
+                                                   int npairs, int splits, double tol, int inner_sweeps,
+                                                   const double* __restrict__ floor_abs) {
   const int pair = blockIdx.x, mat = blockIdx.y, tid = threadIdx.x;
+  // Rows whose norms are negligible against ||A||_F (absolute floor, the accuracy
+  // class of the reference's zgesdd: errors O(eps sigma_max)) stop steering the
+  // convergence test; everything above the floor is held to a relative test.
+  const double fl = floor_abs[mat];
   __shared__ double2 G[kP2][kP2 + 1];
   __shared__ double2 V[kP2][kP2 + 1];
   __shared__ double rot_c[kB], rot_s[kB];
@@ -155,9 +166,10 @@ __global__ void __launch_bounds__(256) k_svd_eigen(const double2* __restrict__ p
     for (int e = tid; e < kP2 * kP2; e += 256) {
       int i = e / kP2, j = e % kP2;
       if (i >= j) continue;
-      double d = G[i][i].x * G[j][j].x;
+      double d = sqrt(fmax(G[i][i].x * G[j][j].x, 0.0));
       double g = hypot(G[i][j].x, G[i][j].y);
-      if (d > 0.0) mx = fmax(mx, g / sqrt(d));
+      double den = fmax(d, fl);
+      if (den > 0.0) mx = fmax(mx, g / den);
       else if (g > 0.0) mx = fmax(mx, 1.0);
     }
     red[tid] = mx;
@@ -248,10 +260,24 @@ __global__ void __launch_bounds__(256) k_svd_eigen(const double2* __restrict__ p
     }
     if (sw + 1 < inner_sweeps && measure() < tol * 1e-2) break;
   }
+  // de Rijk-style ordering: output rows sorted by the new row norms (diag of
+  // W^H G W), largest first, so large singular values collect in low blocks and
+  // the sweeps converge faster.
+  __shared__ int dst_of[kP2];
+  if (tid < kP2) {
+    double di = G[tid][tid].x;
+    int rank = 0;
+    for (int j = 0; j < kP2; ++j) {
+      double dj = G[j][j].x;
+      rank += (dj > di) || (dj == di && j < tid);
+    }
+    dst_of[tid] = sort_rows() ? rank : tid;
+  }
+  __syncthreads();
   double2* out = wh + fidx * kP2 * kP2;
   for (int e = tid; e < kP2 * kP2; e += 256) {
     int i = e / kP2, j = e % kP2;
-    out[e] = cconj(V[j][i]);  // W^H
+    out[dst_of[i] * kP2 + j] = cconj(V[j][i]);  // row i of W^H -> its sorted slot
   }
   if (tid == 0) flags[fidx] = 1;
 }
@@ -259,11 +285,11 @@ __global__ void __launch_bounds__(256) k_svd_eigen(const double2* __restrict__ p
 // ---- in-place row update: WK_pair <- W^H WK_pair -----------------------------------------
 __global__ void __launch_bounds__(256) k_svd_update(double2* __restrict__ wk, const double2* __restrict__ wh,
                                                     const int* __restrict__ flags, const int* __restrict__ tab,
-                                                    int round, int npairs, int64_t rp, int64_t L) {
+                                                    int round, int npairs, int64_t rp, int64_t L, int64_t qw) {
   const int pair = blockIdx.y, mat = blockIdx.z, tid = threadIdx.x;
   const int64_t fidx = static_cast<int64_t>(mat) * npairs + pair;
   if (!flags[fidx]) return;
-  const int64_t W = L + rp;
+  const int64_t W = L + qw;
   const int* pr = tab + (static_cast<int64_t>(round) * npairs + pair) * 2;
   const int bi = pr[0], bj = pr[1];
   double2* K = wk + static_cast<int64_t>(mat) * rp * W;
@@ -314,9 +340,9 @@ __global__ void __launch_bounds__(256) k_svd_update(double2* __restrict__ wk, co
 constexpr int kGK = 64;  // columns per staged chunk
 __global__ void __launch_bounds__(128) k_svd_gram_mma(const double2* __restrict__ wk, double2* __restrict__ part,
                                                       const int* __restrict__ tab, int round, int npairs,
-                                                      int splits, int64_t rp, int64_t L) {
+                                                      int splits, int64_t rp, int64_t L, int64_t qw) {
   const int pair = blockIdx.x, split = blockIdx.y, mat = blockIdx.z;
-  const int64_t W = L + rp;
+  const int64_t W = L + qw;
   const int* pr = tab + (static_cast<int64_t>(round) * npairs + pair) * 2;
   const int bi = pr[0], bj = pr[1];
   const double2* K = wk + static_cast<int64_t>(mat) * rp * W;
@@ -372,11 +398,11 @@ __global__ void __launch_bounds__(128) k_svd_gram_mma(const double2* __restrict_
 constexpr int kUpdColsM = 48;
 __global__ void __launch_bounds__(128) k_svd_update_mma(double2* __restrict__ wk, const double2* __restrict__ wh,
                                                         const int* __restrict__ flags, const int* __restrict__ tab,
-                                                        int round, int npairs, int64_t rp, int64_t L) {
+                                                        int round, int npairs, int64_t rp, int64_t L, int64_t qw) {
   const int pair = blockIdx.y, mat = blockIdx.z, tid = threadIdx.x;
   const int64_t fidx = static_cast<int64_t>(mat) * npairs + pair;
   if (!flags[fidx]) return;
-  const int64_t W = L + rp;
+  const int64_t W = L + qw;
   const int* pr = tab + (static_cast<int64_t>(round) * npairs + pair) * 2;
   const int bi = pr[0], bj = pr[1];
   double2* K = wk + static_cast<int64_t>(mat) * rp * W;
@@ -423,9 +449,25 @@ __global__ void __launch_bounds__(128) k_svd_update_mma(double2* __restrict__ wk
   }
 }
 
+// ---- ||A||_F^2 per matrix -> the absolute convergence floor ------------------------------
+__global__ void k_svd_fro(const double2* __restrict__ a, int64_t count, double* __restrict__ out, double rel) {
+  const int64_t mat = blockIdx.x;
+  const double2* A = a + mat * count;
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) s += A[i].x * A[i].x + A[i].y * A[i].y;
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[mat] = rel * red[0];
+}
+
 // ---- row norms of the X part -----------------------------------------------------------------
-__global__ void k_svd_norms(const double2* __restrict__ wk, double* __restrict__ sig, int64_t rp, int64_t L) {
-  const int64_t W = L + rp;
+__global__ void k_svd_norms(const double2* __restrict__ wk, double* __restrict__ sig, int64_t rp, int64_t L, int64_t qw) {
+  const int64_t W = L + qw;
   const int64_t row = blockIdx.x, mat = blockIdx.y;
   const double2* X = wk + (mat * rp + row) * W;
   __shared__ double red[256];
@@ -445,9 +487,9 @@ __global__ void k_svd_norms(const double2* __restrict__ wk, double* __restrict__
 // transposed (rows = n):     U[:, c] = conj(X[perm c, :])^T / s, Vh[c, :] = Q[perm c, :]
 __global__ void k_svd_output(const double2* __restrict__ wk, const double* __restrict__ sig,
                              const int* __restrict__ perm, double2* __restrict__ u, double* __restrict__ s,
-                             double2* __restrict__ vh, int64_t m, int64_t n, int64_t rows, int64_t rp, int64_t L,
+                             double2* __restrict__ vh, int64_t m, int64_t n, int64_t rows, int64_t rp, int64_t L, int64_t qw,
                              int64_t chi, int transpose, int absorb) {
-  const int64_t W = L + rp;
+  const int64_t W = L + qw;
   const int64_t mat = blockIdx.y;
   const double2* K = wk + mat * rp * W;
   const double* sg = sig + mat * rp;
@@ -488,10 +530,76 @@ __global__ void k_svd_output(const double2* __restrict__ wk, const double* __res
   }
 }
 
+
+// no-Q output: s, Vh (absorbed for right/split), and B[b][x][c] = conj(unit vh_c[x])
+__global__ void k_svd_output_vh(const double2* __restrict__ wk, const double* __restrict__ sig,
+                                const int* __restrict__ perm, double* __restrict__ s, double2* __restrict__ vh,
+                                double2* __restrict__ bt, int64_t n, int64_t rows, int64_t rp, int64_t L, int64_t qw,
+                                int64_t chi, int absorb) {
+  const int64_t W = L + qw;
+  const int64_t mat = blockIdx.y;
+  const double2* K = wk + mat * rp * W;
+  const double* sg = sig + mat * rp;
+  const int* pm = perm + mat * rp;
+  double2* VH = vh + mat * chi * n;
+  double2* BT = bt + mat * n * chi;
+  const int64_t nv = chi * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nv + chi;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e >= nv) {
+      int64_t c = e - nv;
+      s[mat * chi + c] = c < rows ? sg[pm[c]] : 0.0;
+      continue;
+    }
+    int64_t c = e / n, x = e % n;
+    double2 v = make_double2(0.0, 0.0), unit = v;
+    if (c < rows) {
+      int64_t r = pm[c];
+      double sv = sg[r];
+      double inv = sv > 0.0 ? 1.0 / sv : 0.0;
+      double2 xv = K[r * W + x];
+      unit = make_double2(xv.x * inv, xv.y * inv);
+      double f = absorb == QTNH_ABSORB_RIGHT ? sv : (absorb == QTNH_ABSORB_SPLIT ? sqrt(sv) : 1.0);
+      v = make_double2(unit.x * f, unit.y * f);
+    }
+    VH[c * n + x] = v;
+    BT[x * chi + c] = cconj(unit);
+  }
+}
+
+// U = (A Vh^H) / sigma^p per column: p = 1 (none, right), 1/2 (split); 0 for sigma = 0
+__global__ void k_svd_scale_u(double2* __restrict__ u, const double* __restrict__ s, int64_t m, int64_t chi,
+                              int absorb) {
+  const int64_t mat = blockIdx.y;
+  double2* U = u + mat * m * chi;
+  const double* S = s + mat * chi;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * chi; e += (int64_t)gridDim.x * blockDim.x) {
+    double sv = S[e % chi];
+    double f = sv > 0.0 ? (absorb == QTNH_ABSORB_SPLIT ? 1.0 / sqrt(sv) : 1.0 / sv) : 0.0;
+    U[e] = make_double2(U[e].x * f, U[e].y * f);
+  }
+}
+
 int inner_sweeps() {
   static int v = [] {
     const char* e = std::getenv("QTNH_SVD_INNER");
     return e ? std::max(1, std::atoi(e)) : 1;
+  }();
+  return v;
+}
+
+double floor_rel() {
+  static double v = [] {
+    const char* e = std::getenv("QTNH_SVD_FLOOR");
+    return e ? std::atof(e) : 1e-14;
+  }();
+  return v;
+}
+
+bool accumulate_q() {
+  static bool v = [] {
+    const char* e = std::getenv("QTNH_SVD_ACCUMULATE_Q");
+    return e ? std::atoi(e) != 0 : false;
   }();
   return v;
 }
@@ -532,7 +640,12 @@ void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, in
   const Dim nblk2 = ((rows + kP2 - 1) / kP2) * 2;  // 2P blocks of kB rows
   const Dim rp = nblk2 * kB;
   const int npairs = static_cast<int>(nblk2 / 2), rounds = static_cast<int>(nblk2 - 1);
-  const Dim W = L + rp;
+  // Without a transpose the left factor is recovered at the end as U S = A Vh^H
+  // (one GEMM; exact for absorb-left, no division by sigma), so the row
+  // transforms need not be recorded: the update touches L columns, not L + rp.
+  const bool acc_q = transpose || accumulate_q();
+  const Dim qw = acc_q ? rp : 0;
+  const Dim W = L + qw;
   // tournament table (circle method, block nblk2-1 fixed)
   std::vector<int> tab(static_cast<size_t>(rounds) * npairs * 2);
   for (int rd = 0; rd < rounds; ++rd)
@@ -560,10 +673,14 @@ void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, in
   {
     dim3 g(static_cast<unsigned>(std::min<Dim>((rp * W + 255) / 256, 4096)), static_cast<unsigned>(batch));
     k_svd_init<<<g, 256, 0, st>>>(static_cast<const double2*>(a), static_cast<double2*>(wk.ptr), m, n, rows, rp, L,
-                                  transpose);
+                                  qw, transpose);
     QTNH_LAUNCH_CHECK();
   }
   const double tol = tolerance();
+  DevBuf floor_abs(static_cast<size_t>(batch) * sizeof(double), r);
+  k_svd_fro<<<static_cast<unsigned>(batch), 256, 0, st>>>(static_cast<const double2*>(a), m * n,
+                                                         static_cast<double*>(floor_abs.ptr), floor_rel());
+  QTNH_LAUNCH_CHECK();
   std::vector<double> off_h(batch);
   int sweep = 0;
   const int max_sweeps = 40;
@@ -574,15 +691,16 @@ void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, in
       if (use_mma())
         k_svd_gram_mma<<<dim3(npairs, splits, static_cast<unsigned>(batch)), 128, 0, st>>>(
             static_cast<const double2*>(wk.ptr), static_cast<double2*>(part.ptr), static_cast<const int*>(d_tab.ptr),
-            rd, npairs, splits, rp, L);
+            rd, npairs, splits, rp, L, qw);
       else
         k_svd_gram<<<dim3(npairs, splits, static_cast<unsigned>(batch)), 256, 0, st>>>(
             static_cast<const double2*>(wk.ptr), static_cast<double2*>(part.ptr), static_cast<const int*>(d_tab.ptr),
-            rd, npairs, splits, rp, L);
+            rd, npairs, splits, rp, L, qw);
       QTNH_LAUNCH_CHECK();
       k_svd_eigen<<<dim3(npairs, static_cast<unsigned>(batch)), 256, 0, st>>>(
           static_cast<const double2*>(part.ptr), static_cast<double2*>(whb.ptr), static_cast<int*>(flags.ptr),
-          static_cast<double*>(offm.ptr), npairs, splits, tol, inner_sweeps());
+          static_cast<double*>(offm.ptr), npairs, splits, tol, inner_sweeps(),
+          static_cast<const double*>(floor_abs.ptr));
       QTNH_LAUNCH_CHECK();
       const Dim ucols = use_mma() ? kUpdColsM : kUpdCols;
       unsigned ctiles = static_cast<unsigned>(std::min<Dim>((W + ucols - 1) / ucols,
@@ -590,16 +708,17 @@ void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, in
       if (use_mma())
         k_svd_update_mma<<<dim3(ctiles, npairs, static_cast<unsigned>(batch)), 128, 0, st>>>(
             static_cast<double2*>(wk.ptr), static_cast<const double2*>(whb.ptr), static_cast<const int*>(flags.ptr),
-            static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L);
+            static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
       else
         k_svd_update<<<dim3(ctiles, npairs, static_cast<unsigned>(batch)), 256, 0, st>>>(
             static_cast<double2*>(wk.ptr), static_cast<const double2*>(whb.ptr), static_cast<const int*>(flags.ptr),
-            static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L);
+            static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
       QTNH_LAUNCH_CHECK();
     }
     QTNH_CUDA(cudaMemcpyAsync(off_h.data(), offm.ptr, batch * sizeof(double), cudaMemcpyDeviceToHost, st));
     QTNH_CUDA(cudaStreamSynchronize(st));
     double mx = *std::max_element(off_h.begin(), off_h.end());
+    if (std::getenv("QTNH_SVD_DEBUG")) std::fprintf(stderr, "svd sweep %d max_off %.3e\n", sweep, mx);
     if (mx < tol) {
       converged = true;
       ++sweep;
@@ -611,7 +730,7 @@ void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, in
   if (sweeps_out) *sweeps_out = sweep;
   DevBuf sig(static_cast<size_t>(batch * rp) * sizeof(double), r);
   k_svd_norms<<<dim3(static_cast<unsigned>(rp), static_cast<unsigned>(batch)), 256, 0, st>>>(
-      static_cast<const double2*>(wk.ptr), static_cast<double*>(sig.ptr), rp, L);
+      static_cast<const double2*>(wk.ptr), static_cast<double*>(sig.ptr), rp, L, qw);
   QTNH_LAUNCH_CHECK();
   std::vector<double> sh(batch * rp);
   QTNH_CUDA(cudaMemcpyAsync(sh.data(), sig.ptr, sh.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -625,14 +744,33 @@ void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, in
   }
   DevBuf d_perm(perm.size() * sizeof(int), r);
   QTNH_CUDA(cudaMemcpyAsync(d_perm.ptr, perm.data(), perm.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-  {
+  if (acc_q) {
     Dim total = m * chi + chi * n + chi;
     dim3 g(static_cast<unsigned>(std::min<Dim>((total + 255) / 256, 8192)), static_cast<unsigned>(batch));
     k_svd_output<<<g, 256, 0, st>>>(static_cast<const double2*>(wk.ptr), static_cast<const double*>(sig.ptr),
                                     static_cast<const int*>(d_perm.ptr), static_cast<double2*>(u),
-                                    static_cast<double*>(s), static_cast<double2*>(vh), m, n, rows, rp, L, chi,
+                                    static_cast<double*>(s), static_cast<double2*>(vh), m, n, rows, rp, L, qw, chi,
                                     transpose, absorb);
     QTNH_LAUNCH_CHECK();
+  } else {
+    // s, Vh (absorbed per mode) and B = unit-Vh^H; then U S = A B on the tensor
+    // cores and a per-column rescale of U for the non-left modes.
+    DevBuf bt(static_cast<size_t>(batch * n * chi) * 16, r);
+    Dim total = chi * n + chi;
+    dim3 g(static_cast<unsigned>(std::min<Dim>((total + 255) / 256, 8192)), static_cast<unsigned>(batch));
+    k_svd_output_vh<<<g, 256, 0, st>>>(static_cast<const double2*>(wk.ptr), static_cast<const double*>(sig.ptr),
+                                       static_cast<const int*>(d_perm.ptr), static_cast<double*>(s),
+                                       static_cast<double2*>(vh), static_cast<double2*>(bt.ptr), n, rows, rp, L, qw,
+                                       chi, absorb);
+    QTNH_LAUNCH_CHECK();
+    for (Dim b = 0; b < batch; ++b)
+      zgemm(static_cast<const double2*>(a) + b * m * n, static_cast<const double2*>(bt.ptr) + b * n * chi,
+            static_cast<double2*>(u) + b * m * chi, m, chi, n, st);
+    if (absorb != QTNH_ABSORB_LEFT) {
+      dim3 g2(static_cast<unsigned>(std::min<Dim>((m * chi + 255) / 256, 8192)), static_cast<unsigned>(batch));
+      k_svd_scale_u<<<g2, 256, 0, st>>>(static_cast<double2*>(u), static_cast<const double*>(s), m, chi, absorb);
+      QTNH_LAUNCH_CHECK();
+    }
   }
   QTNH_CUDA(cudaStreamSynchronize(st));  // host vectors (perm) are staged; keep it simple
 }

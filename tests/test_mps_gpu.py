@@ -70,8 +70,9 @@ def amplitudes_np(sites, bits):
     return np.array(out)
 
 
-@pytest.mark.parametrize("n,depth,chi", [(8, 6, 4), (10, 8, 8), (12, 6, 64)])
-def test_mps_rcs_vs_reference(n, depth, chi):
+@pytest.mark.parametrize("n,depth,chi,batched", [(8, 6, 4, False), (10, 8, 8, True), (12, 6, 64, True),
+                                                 (10, 8, 8, False)])
+def test_mps_rcs_vs_reference(n, depth, chi, batched):
     if not oracle.ref_available():
         pytest.skip("reference build absent")
     seed = 40
@@ -82,7 +83,7 @@ def test_mps_rcs_vs_reference(n, depth, chi):
     want = amplitudes_np(ref_sites, bits)
 
     def body(rk):
-        m, recs = mps.run_rcs_mps(rk, n, depth, chi, seed, layers=layers)
+        m, recs = mps.run_rcs_mps(rk, n, depth, chi, seed, layers=layers, batched=batched)
         amps = m.amplitudes(bits)
         res = (amps, m.log_fidelity, [r[3] for r in recs], m.bond_dims())
         m.free()

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--chi", type=int, default=1024)
     ap.add_argument("--seed", type=int, default=2025)
     ap.add_argument("--bitstrings", type=int, default=1024)
+    ap.add_argument("--sequential", action="store_true", help="one SVD per update instead of batched layers")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -39,9 +40,12 @@ def main():
             tl = time.perf_counter()
             for q, g in enumerate(singles):
                 m.apply_1q(q, mps.SINGLE_QUBIT[g])
-            for (q, _) in pairs:
-                m.apply_2q(q, circuits.FSIM)
-                upd += 1
+            if args.sequential:
+                for (q, _) in pairs:
+                    m.apply_2q(q, circuits.FSIM)
+            else:
+                m.apply_layer(pairs, circuits.FSIM)
+            upd += len(pairs)
             torch.cuda.synchronize()
             per_layer.append(time.perf_counter() - tl)
         total = time.perf_counter() - t0
