@@ -178,6 +178,12 @@ int qtnh_swap_indices(qtnh_tensor_t t, int a, int b);
  * (Fig. 1) in one pass over the state. */
 int qtnh_qft_layer(qtnh_tensor_t t, int j);
 
+/* The whole QFT circuit of PAPER.md Fig. 1 on a qubit tensor, in place: layers on
+ * distributed qubits one by one, local layers cache-blocked (the lowest 11 in
+ * shared memory, upper ones in register groups), final SWAP network as one
+ * in-place bit reversal when nothing is distributed. */
+int qtnh_qft(qtnh_tensor_t t, int swaps);
+
 /* ---- factorisation --------------------------------------------------------- */
 enum { QTNH_ABSORB_NONE = 0, QTNH_ABSORB_LEFT = 1, QTNH_ABSORB_RIGHT = 2, QTNH_ABSORB_SPLIT = 3 };
 /* Batched thin SVD of `batch` row-major m x n matrices stored back to back in

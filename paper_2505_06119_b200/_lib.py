@@ -76,6 +76,7 @@ _SIGS = {
     "qtnh_swap_indices": (i32, [vp, i32, i32]),
     "qtnh_contract_host": (i32, [vp, i32, P_i64, vp, i32, P_i64, vp, i32, P_i32, P_i32, vp, P_i64]),
     "qtnh_qft_layer": (i32, [vp, i32]),
+    "qtnh_qft": (i32, [vp, i32]),
     "qtnh_svd_device": (i32, [vp, i64, i64, i64, vp, i64, i32, vp, vp, vp]),
     "qtnh_svd": (i32, [vp, i32, P_i32, i32, P_i32, i64, i32, C.POINTER(vp), C.POINTER(vp), vp]),
     "qtnh_zgemm_device": (i32, [vp, i64, i64, i64, vp, vp, vp]),

@@ -535,6 +535,14 @@ int qtnh_qft_layer(qtnh_tensor_t t, int j) {
   });
 }
 
+int qtnh_qft(qtnh_tensor_t t, int swaps) {
+  return guard([&] {
+    TP& p = impl_of(t);
+    make_exclusive(p);
+    op_qft(p, swaps != 0);
+  });
+}
+
 int qtnh_svd_device(qtnh_rank_t r, int64_t batch, int64_t m, int64_t n, const void* a, int64_t chi, int absorb,
                     void* u, void* s, void* vh) {
   return guard([&] {

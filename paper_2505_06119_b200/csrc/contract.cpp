@@ -350,14 +350,32 @@ void op_qft_layer(TP& t, int j) {
   // the ranks whose block has x_j = 1 (dist bits below j enter v as a constant).
   const double h[8] = {0.70710678118654752440, 0, 0.70710678118654752440, 0,
                        0.70710678118654752440, 0, -0.70710678118654752440, 0};
+  const int split = s.split;  // s refers to the tensor op_gate_apply may replace
   op_gate_apply(t, {j}, h, false);
   if (!t->in_span) return;
   auto cd = unflat(t->block, t->shape.dist_dims());
   if (cd[j] == 0) return;
   int64_t v_off = 0;
-  for (int l = j + 1; l < s.split; ++l) v_off = (v_off << 1) | cd[l];
+  for (int l = j + 1; l < split; ++l) v_off = (v_off << 1) | cd[l];
   v_off <<= lb;
   qft_phase_local(t->data(), lb, v_off, n - 1 - j, r.stream);
+}
+
+void op_qft(TP& t, bool swaps) {
+  // t may be replaced by the distributed-layer path: copy the metadata first
+  const int n = t->shape.n_idx(), split = t->shape.split;
+  for (Dim d : t->shape.dims)
+    if (d != 2) throw_invalid("qft needs a qubit tensor (all dims 2)");
+  int nb = n - split;
+  if (nb > 62) throw_invalid("too many local qubits");
+  for (int j = 0; j < split; ++j) op_qft_layer(t, j);  // distributed targets
+  if (t->in_span && nb > 0) qft_local_fused(t->data(), nb, nb - 1, t->rank->stream);
+  if (!swaps) return;
+  if (t->shape.split == 0 && nb >= 10) {
+    if (t->in_span) bitrev_local(t->data(), nb, t->rank->stream);
+    return;
+  }
+  for (int j = 0; j < n / 2; ++j) op_swap_indices(t, j, n - 1 - j);
 }
 
 }  // namespace qtnhb

@@ -12,6 +12,7 @@
 // one write of the state per gate: 32 B/element, the HBM roofline.
 // Diagonal gates touch only the fibers' elements whose diagonal entry is not 1.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 
 #include "ops.h"
@@ -337,6 +338,183 @@ void swap_indices_local(void* data, const std::vector<Dim>& dims, int ia, int ib
   int d = static_cast<int>(dims[ia]);
   if (pow2) k_swap_indices<true><<<grid_for(n_f), 256, 0, st>>>(p, n_f, d, strides[ia], strides[ib], a);
   else k_swap_indices<false><<<grid_for(n_f), 256, 0, st>>>(p, n_f, d, strides[ia], strides[ib], a);
+  QTNH_LAUNCH_CHECK();
+}
+
+namespace {
+
+// ---- cache-blocked QFT ---------------------------------------------------------------
+// Layer j (bit t = n-1-j): H on bit t, then exp(i pi v / 2^t) on amplitudes with
+// bit t set, v = the bits below t. Layers run in order j = 0..n-1.
+//  * k_qft_low: the lowest L layers touch only the lowest L bits, so one pass over
+//    contiguous 2^L-element chunks staged in shared memory applies all of them
+//    (twiddles e^{i pi v / 2^t}, v < 2^t, tabulated once per CTA).
+//  * k_qft_group: g consecutive upper layers (bits T..B, B >= L) in registers: a
+//    thread owns the 2^g amplitudes that differ in those bits; the phase splits
+//    into a per-layer table e^{i pi k / 2^u} (k < 2^u, u = t - B) and one
+//    sincospi of the fixed low bits per layer.
+//  * k_bitrev: the final SWAP network reverses the bit order -- one in-place pass
+//    that exchanges 32 x 32 tiles (a, m, b) <-> (rev b, rev m, rev a).
+constexpr int kQftLowMax = 11;
+
+__device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+__global__ void __launch_bounds__(256) k_qft_low(double2* __restrict__ psi, int64_t n_chunks, int L) {
+  extern __shared__ double2 smq[];
+  double2* data = smq;             // 2^L amplitudes
+  double2* tw = smq + (1 << L);    // tw[2^t + v] = e^{i pi v / 2^t}, t < L
+  const int C = 1 << L, H = C >> 1;
+  const double r = 0.70710678118654752440;
+  for (int e = threadIdx.x; e < C; e += blockDim.x) {
+    if (e == 0) continue;
+    int t = 31 - __clz(e);
+    int v = e - (1 << t);
+    double sn, cs;
+    sincospi(static_cast<double>(v) * ldexp(1.0, -t), &sn, &cs);
+    tw[e] = make_double2(cs, sn);
+  }
+  for (int64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+    double2* g = psi + ch * C;
+    __syncthreads();
+    for (int e = threadIdx.x; e < C; e += blockDim.x) data[e] = g[e];
+    __syncthreads();
+    for (int t = L - 1; t >= 0; --t) {
+      const int lo_mask = (1 << t) - 1;
+      for (int p = threadIdx.x; p < H; p += blockDim.x) {
+        int lo = p & lo_mask;
+        int i0 = ((p >> t) << (t + 1)) | lo, i1 = i0 | (1 << t);
+        double2 a0 = data[i0], a1 = data[i1];
+        double2 y0 = make_double2(r * a0.x + r * a1.x, r * a0.y + r * a1.y);
+        double2 d = make_double2(r * a0.x - r * a1.x, r * a0.y - r * a1.y);
+        data[i0] = y0;
+        data[i1] = t > 0 ? cmul2(d, tw[(1 << t) + lo]) : d;
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < C; e += blockDim.x) g[e] = data[e];
+  }
+}
+
+struct QftGroupArgs {
+  double2 tab[32];  // tab[2^u + k] = e^{i pi k / 2^u}, k < 2^u, u < 5
+};
+
+template <int G>
+__global__ void __launch_bounds__(256) k_qft_group(double2* __restrict__ psi, int64_t n_fibers, int B,
+                                                   const __grid_constant__ QftGroupArgs ga) {
+  const double r = 0.70710678118654752440;
+  const int64_t lo_mask = (int64_t(1) << B) - 1;
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < n_fibers;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = f & lo_mask, hi = f >> B;
+    int64_t base = (hi << (B + G)) | lo;
+    double2 x[1 << G];
+#pragma unroll
+    for (int k = 0; k < (1 << G); ++k) x[k] = psi[base + (int64_t(k) << B)];
+#pragma unroll
+    for (int u = G - 1; u >= 0; --u) {
+      double sn, cs;
+      sincospi(static_cast<double>(lo) * ldexp(1.0, -(B + u)), &sn, &cs);
+      const double2 lof = make_double2(cs, sn);
+#pragma unroll
+      for (int k = 0; k < (1 << G); ++k) {
+        if (k & (1 << u)) continue;
+        const int k1 = k | (1 << u);
+        double2 a0 = x[k], a1 = x[k1];
+        x[k] = make_double2(r * a0.x + r * a1.x, r * a0.y + r * a1.y);
+        double2 d = make_double2(r * a0.x - r * a1.x, r * a0.y - r * a1.y);
+        const int kl = k & ((1 << u) - 1);
+        double2 ph = u > 0 ? cmul2(ga.tab[(1 << u) + kl], lof) : lof;
+        x[k1] = cmul2(d, ph);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < (1 << G); ++k) psi[base + (int64_t(k) << B)] = x[k];
+  }
+}
+
+__device__ __forceinline__ unsigned rev_bits(unsigned x, int bits) { return __brev(x) >> (32 - bits); }
+__device__ __forceinline__ uint64_t rev_bits64(uint64_t x, int bits) { return __brevll(x) >> (64 - bits); }
+
+__device__ __forceinline__ double2 canon2(double2 v) {
+  if (v.x == 0.0 && v.y == 0.0) v = make_double2(0.0, 0.0);
+  return v;
+}
+
+// n >= 10: x = (a: top 5 bits, m: middle n-10 bits, b: low 5 bits).
+__global__ void __launch_bounds__(256) k_bitrev(double2* __restrict__ psi, int n, int64_t n_mid) {
+  __shared__ double2 t1[32][33], t2[32][33];
+  const int mbits = n - 10;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int64_t m = blockIdx.x; m < n_mid; m += gridDim.x) {
+    int64_t mr = static_cast<int64_t>(rev_bits64(static_cast<uint64_t>(m), mbits));
+    if (mr < m) continue;  // the pair is handled by its smaller member
+    __syncthreads();
+    for (int a = ty; a < 32; a += 8) {
+      t1[a][tx] = psi[(int64_t(a) << (n - 5)) | (m << 5) | tx];
+      t2[a][tx] = psi[(int64_t(a) << (n - 5)) | (mr << 5) | tx];
+    }
+    __syncthreads();
+    for (int a = ty; a < 32; a += 8) {
+      int ra = rev_bits(a, 5), rb = rev_bits(tx, 5);
+      // new (a, m, b) = old (rev b, rev m, rev a) = t2[rev b][rev a]
+      psi[(int64_t(a) << (n - 5)) | (m << 5) | tx] = canon2(t2[rb][ra]);
+      if (mr != m) psi[(int64_t(a) << (n - 5)) | (mr << 5) | tx] = canon2(t1[rb][ra]);
+    }
+  }
+}
+
+}  // namespace
+
+void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
+  // Layers with target bits first_layer_bit .. 0 (descending), all local.
+  auto* p = static_cast<double2*>(data);
+  int L = std::min(nb, kQftLowMax);
+  int top = first_layer_bit;
+  while (top >= L) {
+    int g = std::min(4, top - L + 1);  // 5 spills at 255 registers
+    int B = top - g + 1;
+    QftGroupArgs ga{};
+    for (int u = 0; u < 5; ++u)
+      for (int k = 0; k < (1 << u); ++k) {
+        double ang = M_PI * k / std::ldexp(1.0, u);
+        ga.tab[(1 << u) + k] = make_double2(std::cos(ang), std::sin(ang));
+      }
+    int64_t n_f = int64_t(1) << (nb - g);
+    int grid = grid_for(n_f);
+    switch (g) {
+      case 4: k_qft_group<4><<<grid, 256, 0, st>>>(p, n_f, B, ga); break;
+      case 3: k_qft_group<3><<<grid, 256, 0, st>>>(p, n_f, B, ga); break;
+      case 2: k_qft_group<2><<<grid, 256, 0, st>>>(p, n_f, B, ga); break;
+      default: k_qft_group<1><<<grid, 256, 0, st>>>(p, n_f, B, ga); break;
+    }
+    QTNH_LAUNCH_CHECK();
+    top = B - 1;
+  }
+  if (top >= 0) {
+    // remaining layers: bits top..0 with top = L - 1 (all of the low chunk)
+    int Lc = top + 1;
+    size_t smem = static_cast<size_t>(2) << Lc;  // data + twiddles, in double2
+    smem *= sizeof(double2);
+    static bool attr = false;
+    if (!attr) {
+      QTNH_CUDA(cudaFuncSetAttribute(k_qft_low, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16 << kQftLowMax));
+      attr = true;
+    }
+    int64_t n_chunks = int64_t(1) << (nb - Lc);
+    int grid = static_cast<int>(std::min<int64_t>(n_chunks, 148 * 6));
+    k_qft_low<<<grid, 256, smem, st>>>(p, n_chunks, Lc);
+    QTNH_LAUNCH_CHECK();
+  }
+}
+
+void bitrev_local(void* data, int nb, cudaStream_t st) {
+  if (nb < 10) throw_invalid("in-place bit reversal needs at least 10 local qubits");
+  int64_t n_mid = int64_t(1) << (nb - 10);
+  int grid = static_cast<int>(std::min<int64_t>(n_mid, 148 * 8));
+  k_bitrev<<<grid, 256, 0, st>>>(static_cast<double2*>(data), nb, n_mid);
   QTNH_LAUNCH_CHECK();
 }
 

@@ -48,6 +48,9 @@ void op_gate_apply(TP& t, const std::vector<int>& targets, const double* gate, b
 void op_swap_indices(TP& t, int a, int b);
 // Fused QFT layer j on a qubit tensor (see gate.cu k_qft_layer).
 void op_qft_layer(TP& t, int j);
+// Whole QFT: distributed layers one by one, local layers cache-blocked, final
+// SWAP network as an in-place bit reversal (undistributed) or index swaps.
+void op_qft(TP& t, bool swaps);
 
 // Contraction with host operands/result, pipelined H2D / GEMM / D2H (single rank).
 void contract_host(RankCtx& r, const std::vector<Dim>& da, const double* a, const std::vector<Dim>& db,
@@ -71,6 +74,11 @@ void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, in
 // controlled phases; phase-only variant for a distributed target with x_j = 1.
 void qft_layer_local(void* data, int local_bits, int t, cudaStream_t st);
 void qft_phase_local(void* data, int local_bits, int64_t v_off, int t, cudaStream_t st);
+// Cache-blocked QFT layers on a local block of nb qubits: layers whose target
+// bits are first_layer_bit..0 (the low bits staged in shared memory, upper bits
+// in register groups of 5); in-place bit reversal (the final SWAP network).
+void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st);
+void bitrev_local(void* data, int nb, cudaStream_t st);
 // In-place exchange of two equal-size local indices.
 void swap_indices_local(void* data, const std::vector<Dim>& dims, int ia, int ib, cudaStream_t st);
 // Gate on a dense local block: dims = local dims, targets = local positions.

@@ -519,6 +519,12 @@ def qft_layer(state: Tensor, j: int) -> Tensor:
     return state
 
 
+def qft(state: Tensor, swaps: bool = True) -> Tensor:
+    """In place: the whole QFT (cache-blocked layers + bit-reversal SWAP network)."""
+    check(lib.qtnh_qft(state._h, int(bool(swaps))))
+    return state
+
+
 # ---- factorisation (linalg.hpp:441-523; SPEC network::decompose) ---------------------------
 ABSORB_NONE, ABSORB_LEFT, ABSORB_RIGHT, ABSORB_SPLIT = 0, 1, 2, 3
 

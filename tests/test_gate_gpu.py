@@ -180,3 +180,25 @@ def test_swap_indices_bit_exact(dims, split, a, b, world):
     got = World(world).run(body)[0]
     from conftest import bits
     assert np.array_equal(bits(got), bits(P.permute(dims, g, perm)))
+
+
+@pytest.mark.parametrize("n,split,world", [(8, 0, 1), (11, 0, 1), (16, 0, 1), (21, 0, 1), (14, 2, 4), (13, 3, 8)])
+def test_blocked_qft(n, split, world):
+    """Cache-blocked whole-QFT kernel path (qtnh_qft) against the oracle QFT."""
+    from paper_2505_06119_b200.qtnh import qft
+    st = circuits.counter_state(23 + n, 2**n)
+    st /= np.linalg.norm(st)
+
+    def body(rk):
+        t = Tensor.from_global(rk, IndexTuple([2] * n, split), DistParams(1, 1, 0), st)
+        qft(t, swaps=True)
+        return t.to_global_vector()
+
+    got = World(world).run(body)[0]
+    assert rel_l2(got, P.qft(n, st)) < TOL
+    if n <= 16:
+        def body2(rk):
+            t = Tensor.from_global(rk, IndexTuple([2] * n, split), DistParams(1, 1, 0), st)
+            qft(t, swaps=False)
+            return t.to_global_vector()
+        assert rel_l2(World(world).run(body2)[0], P.qft(n, st, swaps=False)) < TOL

@@ -106,7 +106,26 @@ def main():
             out["gate_by_gate_estimate_s"] = (n_h * gates["H_dense_q16"] + n_cp * gates["CP_diag_q3_q20"]
                                               + n_sw * gates["SWAP_inplace_q2_qn-3"]) / 1e3
             out["gate_counts"] = {"H": n_h, "CP": n_cp, "SWAP": n_sw, "total": n_h + n_cp + n_sw}
-            # the full QFT, fused path
+            # the full QFT, cache-blocked path (qtnh_qft)
+            torch.cuda.synchronize()
+            e0b, e1b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0b.record(st)
+            qtnh.qft(t, swaps=True)
+            e1b.record(st)
+            e1b.synchronize()
+            msb = e0b.elapsed_time(e1b)
+            out["qft_blocked_s"] = msb / 1e3
+            out["qft_blocked_effective_GBps"] = (n_h + n_cp + n_sw) * 32.0 * N / (msb * 1e-3) / 1e9
+            errs_b = {}
+            for k, w in want.items():
+                g = complex(psi[k].item())
+                errs_b[str(k)] = abs(g - w) / max(abs(w), 1e-300)
+            out["blocked_spot_rel_err"] = errs_b
+            # restore the input for the layer-by-layer run
+            qtnh.check(qtnh.lib.qtnh_counter_complex_normals_device(C.c_void_p(st.cuda_stream), args.seed, 0, N,
+                                                                    C.c_void_p(t.device_ptr())))
+            psi.mul_(1.0 / math.sqrt(nrm2))
+            # the full QFT, fused layer-by-layer path
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
