@@ -30,6 +30,7 @@ _SIGS = {
     "qtnh_last_error_info": (i64, []),
     "qtnh_version": (C.c_char_p, []),
     "qtnh_kernel_launch_count": (i64, []),
+    "qtnh_set_option": (i32, [C.c_char_p, f64]),
     "qtnh_world_create_local": (i32, [i32, P_i32, C.POINTER(vp)]),
     "qtnh_nccl_unique_id": (i32, [vp]),
     "qtnh_world_create_nccl": (i32, [i32, i32, i32, vp, C.POINTER(vp)]),

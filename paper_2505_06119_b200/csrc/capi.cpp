@@ -535,6 +535,15 @@ int qtnh_qft_layer(qtnh_tensor_t t, int j) {
   });
 }
 
+int qtnh_set_option(const char* name, double value) {
+  return guard([&] {
+    need(name, "name");
+    std::string n(name);
+    if (n == "swap_chunk_bytes") set_swap_chunk_bytes(static_cast<Dim>(value));
+    else throw_invalid("unknown option " + n);
+  });
+}
+
 int qtnh_qft(qtnh_tensor_t t, int swaps) {
   return guard([&] {
     TP& p = impl_of(t);

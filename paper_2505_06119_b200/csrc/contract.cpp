@@ -16,6 +16,8 @@
 //     FP64-tensor-core zgemm whose row-major output IS its block of the result in
 //     the SPEC.md:408 order (open(a) then open(b)).
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <numeric>
@@ -25,6 +27,8 @@
 #include "strided_copy.h"
 
 namespace qtnhb {
+
+Dim swap_chunk_bytes();
 
 namespace {
 
@@ -306,18 +310,33 @@ void op_gate_apply(TP& t, const std::vector<int>& targets, const double* gate, b
     std::swap(perm[q], perm[w]);
     new_targets[i] = w;
   }
-  TP t2 = op_permute(t, perm, s.split);
-  if (t2->in_span) {
+  // in place: exchange each distributed target with its local partner, apply,
+  // exchange back (no second copy of the state; only the moving halves travel)
+  const int split = s.split;
+  const std::vector<Dim> ldims = s.local_dims();
+  std::vector<std::pair<int, int>> swaps;
+  for (int i = 0; i < k; ++i)
+    if (targets[i] < split) swaps.push_back({targets[i], new_targets[i]});
+  for (auto& sw : swaps) op_swap_dist_local_inplace(t, sw.first, sw.second, swap_chunk_bytes());
+  if (t->in_span) {
     std::vector<int> lt;
-    for (int q : new_targets) lt.push_back(q - s.split);
-    gate_local(t2->data(), s.local_dims(), lt, gate, false, r.stream);
+    for (int q : new_targets) lt.push_back(q - split);
+    gate_local(t->data(), ldims, lt, gate, false, r.stream);
   }
-  t = op_permute(t2, perm, s.split);
+  for (auto it = swaps.rbegin(); it != swaps.rend(); ++it)
+    op_swap_dist_local_inplace(t, it->first, it->second, swap_chunk_bytes());
 }
 
 }  // namespace qtnhb
 
 namespace qtnhb {
+
+std::atomic<Dim> g_swap_chunk_bytes{[] {
+  const char* e = std::getenv("QTNH_SWAP_CHUNK_BYTES");
+  return e ? static_cast<Dim>(std::atoll(e)) : (Dim(1) << 31);
+}()};
+Dim swap_chunk_bytes() { return g_swap_chunk_bytes.load(); }
+void set_swap_chunk_bytes(Dim v) { g_swap_chunk_bytes.store(std::max<Dim>(16, v)); }
 
 void op_swap_indices(TP& t, int a, int b) {
   const Shape& s = t->shape;
@@ -325,6 +344,11 @@ void op_swap_indices(TP& t, int a, int b) {
   if (s.dims[a] != s.dims[b]) throw_invalid("swapped indices must have equal dimensions");
   if (a >= s.split && b >= s.split) {
     if (t->in_span) swap_indices_local(t->data(), s.local_dims(), a - s.split, b - s.split, t->rank->stream);
+    return;
+  }
+  if ((a < s.split) != (b < s.split)) {
+    int da = a < s.split ? a : b, lb = a < s.split ? b : a;
+    op_swap_dist_local_inplace(t, da, lb, swap_chunk_bytes());
     return;
   }
   std::vector<int> perm(s.n_idx());

@@ -44,6 +44,10 @@ TP op_contract(const TP& a, const TP& b, const std::vector<int>& apos, const std
 // In-place gate on t (caller guarantees exclusive ownership).
 void op_gate_apply(TP& t, const std::vector<int>& targets, const double* gate, bool diagonal);
 
+// In-place exchange of a distributed index a with a local index b (equal size),
+// pairwise NVLink/NCCL exchange through a staging buffer of ~chunk_bytes.
+void op_swap_dist_local_inplace(TP& t, int a, int b, Dim chunk_bytes);
+void set_swap_chunk_bytes(Dim v);
 // In-place (local) / remapped (distributed) exchange of two equal-size indices.
 void op_swap_indices(TP& t, int a, int b);
 // Fused QFT layer j on a qubit tensor (see gate.cu k_qft_layer).

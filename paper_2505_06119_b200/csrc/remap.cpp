@@ -336,3 +336,103 @@ void op_to_global(const TensorImpl& t, double* host) {
 }
 
 }  // namespace qtnhb
+
+// ---- in-place distributed <-> local index swap ------------------------------------------
+namespace qtnhb {
+
+// Exchange a distributed index a with a local index b of the same size d, in
+// place: on the rank whose block has coordinate i at a, the local region b = j
+// (j != i) is sent to the partner block (a = j) and replaced by the partner's
+// region b = i. Only the (d-1)/d of each block that moves is touched, through a
+// bounded staging buffer (chunks of the region's outer indices), so a 128 GiB
+// shard swaps without a second copy of the tensor. Values equal ops::permute with
+// a and b exchanged (zero canonicalisation included).
+void op_swap_dist_local_inplace(TP& t, int a, int b, Dim chunk_bytes) {
+  const Shape& s = t->shape;
+  if (!(a < s.split && b >= s.split)) throw_invalid("swap_dist_local needs a distributed a and a local b");
+  const Dim d = s.dims[a];
+  if (s.dims[b] != d) throw_invalid("swapped indices must have equal dimensions");
+  RankCtx& r = *t->rank;
+  auto members = span_ranks(*t);
+  if (!t->in_span) return;
+  const int lb = b - s.split;
+  auto ld = s.local_dims();
+  auto ls = row_major_strides(ld);
+  const Dim nd = s.dist_size();
+  auto ddims = s.dist_dims();
+  auto cd = unflat(t->block, ddims);
+  const Dim my_i = cd[a];
+  // region (b fixed) dims / strides, outermost first
+  std::vector<Dim> rdims, rstr;
+  for (int q = 0; q < static_cast<int>(ld.size()); ++q)
+    if (q != lb) {
+      rdims.push_back(ld[q]);
+      rstr.push_back(ls[q]);
+    }
+  Dim region = 1;
+  for (Dim x : rdims) region *= x;
+  // chunk the region over its outer dims: chunk = product of the innermost dims
+  // that fit in chunk_bytes (at least one full innermost run)
+  Dim per_chunk = 1;
+  int split_at = static_cast<int>(rdims.size());
+  while (split_at > 0 && per_chunk * rdims[split_at - 1] * 16 <= chunk_bytes) per_chunk *= rdims[--split_at];
+  if (split_at == static_cast<int>(rdims.size()) && !rdims.empty()) {
+    per_chunk = rdims.back();  // a run bigger than the budget: one run per chunk
+    split_at = static_cast<int>(rdims.size()) - 1;
+  }
+  std::vector<Dim> odims(rdims.begin(), rdims.begin() + split_at), idims(rdims.begin() + split_at, rdims.end());
+  std::vector<Dim> ostr(rstr.begin(), rstr.begin() + split_at), istr(rstr.begin() + split_at, rstr.end());
+  Dim n_chunks = 1;
+  for (Dim x : odims) n_chunks *= x;
+  auto irow = row_major_strides(idims);
+  const int partners = static_cast<int>(d - 1);
+  DevBuf sbuf(static_cast<size_t>(per_chunk * std::max(1, partners)) * 16, r);
+  DevBuf rbuf(static_cast<size_t>(per_chunk * std::max(1, partners)) * 16, r);
+  // canonicalise the region that stays (b = my_i): in place, element by element
+  {
+    CopyBox keep;
+    keep.dims = rdims;
+    keep.in_stride = rstr;
+    keep.out_stride = rstr;
+    char* base = static_cast<char*>(t->data()) + my_i * ls[lb] * 16;
+    strided_copy(base, base, keep, true, r.stream);
+  }
+  for (Dim ch = 0; ch < n_chunks; ++ch) {
+    auto oc = unflat(ch, odims);
+    Dim obase = 0;
+    for (size_t k = 0; k < oc.size(); ++k) obase += oc[k] * ostr[k];
+    std::vector<Xfer> sends, recvs;
+    int slot = 0;
+    for (Dim j = 0; j < d; ++j) {
+      if (j == my_i) continue;
+      // my region b = j (offset j * stride_b) -> staging slot
+      CopyBox pk;
+      pk.dims = idims;
+      pk.in_stride = istr;
+      pk.out_stride = irow;
+      const char* src = static_cast<const char*>(t->data()) + (obase + j * ls[lb]) * 16;
+      strided_copy(src, static_cast<char*>(sbuf.ptr) + slot * per_chunk * 16, pk, true, r.stream);
+      auto pc = cd;
+      pc[a] = j;
+      Dim pblock = flat(pc, ddims);
+      int peer = t->dist.home(pblock, nd, t->cycle, t->slot);
+      sends.push_back({peer, slot * per_chunk, per_chunk});
+      recvs.push_back({peer, slot * per_chunk, per_chunk});
+      ++slot;
+    }
+    exchange(r, members, sbuf.ptr, sends, rbuf.ptr, recvs);
+    slot = 0;
+    for (Dim j = 0; j < d; ++j) {
+      if (j == my_i) continue;
+      CopyBox up;
+      up.dims = idims;
+      up.in_stride = irow;
+      up.out_stride = istr;
+      char* dst = static_cast<char*>(t->data()) + (obase + j * ls[lb]) * 16;
+      strided_copy(static_cast<char*>(rbuf.ptr) + slot * per_chunk * 16, dst, up, false, r.stream);
+      ++slot;
+    }
+  }
+}
+
+}  // namespace qtnhb

@@ -202,3 +202,31 @@ def test_blocked_qft(n, split, world):
             qft(t, swaps=False)
             return t.to_global_vector()
         assert rel_l2(World(world).run(body2)[0], P.qft(n, st, swaps=False)) < TOL
+
+
+@pytest.mark.parametrize("dims,split,a,b,world,chunk", [
+    ([2] * 12, 2, 0, 9, 4, 1 << 30),      # one chunk
+    ([2] * 12, 2, 1, 4, 4, 256),          # many chunks (16 elements each)
+    ([3, 3, 2, 3, 2], 1, 0, 3, 3, 96),    # dim-3 indices: two partners per rank
+    ([2] * 10, 3, 2, 3, 8, 1 << 30),      # local index right after the split
+])
+def test_inplace_distributed_swap(dims, split, a, b, world, chunk):
+    """Distributed <-> local index swap done in place through a bounded staging
+    buffer: bit-exact against ops::permute semantics."""
+    from conftest import bits
+    from paper_2505_06119_b200.qtnh import check, lib, swap_indices
+    g = circuits.counter_state(31, int(np.prod(dims)))
+    g[::9] = complex(-0.0, -0.0)
+    perm = list(range(len(dims)))
+    perm[a], perm[b] = perm[b], perm[a]
+    check(lib.qtnh_set_option(b"swap_chunk_bytes", float(chunk)))
+    try:
+        def body(rk):
+            t = Tensor.from_global(rk, IndexTuple(dims, split), DistParams(1, 1, 0), g)
+            swap_indices(t, a, b)
+            return t.to_global_vector()
+
+        got = World(world).run(body)[0]
+    finally:
+        check(lib.qtnh_set_option(b"swap_chunk_bytes", float(1 << 31)))
+    assert np.array_equal(bits(got), bits(P.permute(dims, g, perm)))
