@@ -13,6 +13,7 @@
 // Diagonal gates touch only the fibers' elements whose diagonal entry is not 1.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "ops.h"
@@ -397,12 +398,89 @@ __global__ void __launch_bounds__(256) k_qft_low(double2* __restrict__ psi, int6
   }
 }
 
+
+// Low layers, version 2: the chunk sits in shared memory and the L layers run in
+// rounds of up to 4 bits; a thread owns the 2^g amplitudes of one fiber in
+// registers for a round, so a round costs one shared load + store per amplitude
+// and one twiddle lookup per amplitude and layer, with one barrier per round.
+__device__ const double2 kQftSmallTw[15] = {{1.0, 0.0}, {1.0, 0.0}, {6.123233995736766e-17, 1.0}, {1.0, 0.0}, {0.7071067811865476, 0.7071067811865475}, {6.123233995736766e-17, 1.0}, {-0.7071067811865475, 0.7071067811865476}, {1.0, 0.0}, {0.9238795325112867, 0.3826834323650898}, {0.7071067811865476, 0.7071067811865475}, {0.38268343236508984, 0.9238795325112867}, {6.123233995736766e-17, 1.0}, {-0.3826834323650897, 0.9238795325112867}, {-0.7071067811865475, 0.7071067811865476}, {-0.9238795325112867, 0.3826834323650899}};  // e^{i pi k / 2^u}, index 2^u - 1 + k
+
+__device__ __forceinline__ int swz8(int i) { return i ^ ((i >> 3) & 7); }  // conflict-free 16-B rows
+
+template <int G>
+__device__ __forceinline__ void qft_low_round(double2* __restrict__ data, const double2* __restrict__ tw, int L,
+                                              int B) {
+  const double r = 0.70710678118654752440;
+  const int nf = 1 << (L - G);
+  for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+    const int lo = f & ((1 << B) - 1), hi = f >> B;
+    const int base = (hi << (B + G)) | lo;
+    double2 x[1 << G];
+#pragma unroll
+    for (int k = 0; k < (1 << G); ++k) x[k] = data[swz8(base + (k << B))];
+    // phase of layer t = B + u for in-fiber index k: e^{i pi klow / 2^u} * e^{i pi lo / 2^t}
+    double2 lof[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) lof[u] = (B + u) > 0 ? tw[(1 << (B + u)) + lo] : make_double2(1.0, 0.0);
+#pragma unroll
+    for (int u = G - 1; u >= 0; --u) {
+#pragma unroll
+      for (int k = 0; k < (1 << G); ++k) {
+        if (k & (1 << u)) continue;
+        const int k1 = k | (1 << u);
+        double2 a0 = x[k], a1 = x[k1];
+        x[k] = make_double2(r * a0.x + r * a1.x, r * a0.y + r * a1.y);
+        double2 d = make_double2(r * a0.x - r * a1.x, r * a0.y - r * a1.y);
+        const int kl = k & ((1 << u) - 1);
+        double2 ph = kl ? cmul2(kQftSmallTw[(1 << u) - 1 + kl], lof[u]) : lof[u];
+        x[k1] = cmul2(d, ph);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < (1 << G); ++k) data[swz8(base + (k << B))] = x[k];
+  }
+}
+
+__global__ void __launch_bounds__(128) k_qft_low2(double2* __restrict__ psi, int64_t n_chunks, int L) {
+  extern __shared__ double2 smq2[];
+  double2* data = smq2;
+  double2* tw = smq2 + (1 << L);
+  const int C = 1 << L;
+  for (int e = threadIdx.x; e < C; e += blockDim.x) {
+    if (e == 0) continue;
+    int t = 31 - __clz(e);
+    int v = e - (1 << t);
+    double sn, cs;
+    sincospi(static_cast<double>(v) * ldexp(1.0, -t), &sn, &cs);
+    tw[e] = make_double2(cs, sn);
+  }
+  for (int64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+    double2* g = psi + ch * C;
+    __syncthreads();
+    for (int e = threadIdx.x; e < C; e += blockDim.x) data[swz8(e)] = g[e];
+    __syncthreads();
+    for (int T = L - 1; T >= 0;) {
+      int gg = T + 1 >= 4 ? 4 : T + 1;
+      int B = T - gg + 1;
+      switch (gg) {
+        case 4: qft_low_round<4>(data, tw, L, B); break;
+        case 3: qft_low_round<3>(data, tw, L, B); break;
+        case 2: qft_low_round<2>(data, tw, L, B); break;
+        default: qft_low_round<1>(data, tw, L, B); break;
+      }
+      __syncthreads();
+      T = B - 1;
+    }
+    for (int e = threadIdx.x; e < C; e += blockDim.x) g[e] = data[swz8(e)];
+  }
+}
+
 struct QftGroupArgs {
   double2 tab[32];  // tab[2^u + k] = e^{i pi k / 2^u}, k < 2^u, u < 5
 };
 
 template <int G>
-__global__ void __launch_bounds__(256) k_qft_group(double2* __restrict__ psi, int64_t n_fibers, int B,
+__global__ void __launch_bounds__(256, (G >= 4 ? 1 : 2)) k_qft_group(double2* __restrict__ psi, int64_t n_fibers, int B,
                                                    const __grid_constant__ QftGroupArgs ga) {
   const double r = 0.70710678118654752440;
   const int64_t lo_mask = (int64_t(1) << B) - 1;
@@ -468,13 +546,22 @@ __global__ void __launch_bounds__(256) k_bitrev(double2* __restrict__ psi, int n
 
 }  // namespace
 
+int qft_group_max() {
+  static int v = [] {
+    const char* e = std::getenv("QTNH_QFT_G");
+    int g = e ? std::atoi(e) : 4;
+    return std::max(1, std::min(4, g));
+  }();
+  return v;
+}
+
 void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
   // Layers with target bits first_layer_bit .. 0 (descending), all local.
   auto* p = static_cast<double2*>(data);
   int L = std::min(nb, kQftLowMax);
   int top = first_layer_bit;
   while (top >= L) {
-    int g = std::min(4, top - L + 1);  // 5 spills at 255 registers
+    int g = std::min(qft_group_max(), top - L + 1);  // 5 spills at 255 registers
     int B = top - g + 1;
     QftGroupArgs ga{};
     for (int u = 0; u < 5; ++u)
@@ -500,12 +587,12 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
     smem *= sizeof(double2);
     static bool attr = false;
     if (!attr) {
-      QTNH_CUDA(cudaFuncSetAttribute(k_qft_low, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16 << kQftLowMax));
+      QTNH_CUDA(cudaFuncSetAttribute(k_qft_low2, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16 << kQftLowMax));
       attr = true;
     }
     int64_t n_chunks = int64_t(1) << (nb - Lc);
-    int grid = static_cast<int>(std::min<int64_t>(n_chunks, 148 * 6));
-    k_qft_low<<<grid, 256, smem, st>>>(p, n_chunks, Lc);
+    int grid = static_cast<int>(std::min<int64_t>(n_chunks, 148 * 8));
+    k_qft_low2<<<grid, 128, smem, st>>>(p, n_chunks, Lc);
     QTNH_LAUNCH_CHECK();
   }
 }
