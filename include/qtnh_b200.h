@@ -100,6 +100,17 @@ void* qtnh_rank_stream(qtnh_rank_t r);
 int qtnh_rank_synchronize(qtnh_rank_t r);
 int qtnh_barrier(qtnh_rank_t r);
 
+/* Group::all_to_all_v (runtime.hpp:448-475) on device buffers of complex128
+ * elements: member i receives send_counts[i] elements from send_buf+send_displs[i];
+ * this rank receives recv_counts[i] elements from member i into
+ * recv_buf+recv_displs[i]. Collective over `members` (world ranks; member-only,
+ * runtime.hpp:191-223). Each sender's count must equal the receiver's expected
+ * count, else QTNH_E_PROTOCOL naming the "(src -> dst)" pair (runtime.hpp:464-471);
+ * a zero count means "nothing to/from that member". Stream-ordered. */
+int qtnh_all_to_all_v(qtnh_rank_t r, int n_members, const int* members, const void* send_buf,
+                      const int64_t* send_counts, const int64_t* send_displs, void* recv_buf,
+                      const int64_t* recv_counts, const int64_t* recv_displs);
+
 /* ---- tensors ------------------------------------------------------------- */
 /* Dense tensor; `local` holds local_size complex numbers of this rank's block
  * (host memory, NULL = zeros). Ranks outside the span ignore `local`. */

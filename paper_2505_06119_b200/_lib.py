@@ -45,6 +45,7 @@ _SIGS = {
     "qtnh_rank_stream": (vp, [vp]),
     "qtnh_rank_synchronize": (i32, [vp]),
     "qtnh_barrier": (i32, [vp]),
+    "qtnh_all_to_all_v": (i32, [vp, i32, P_i32, vp, P_i64, P_i64, vp, P_i64, P_i64]),
     "qtnh_tensor_dense": (i32, [vp, i32, P_i64, i32, P_i64, vp, C.POINTER(vp)]),
     "qtnh_tensor_from_global": (i32, [vp, i32, P_i64, i32, P_i64, vp, C.POINTER(vp)]),
     "qtnh_tensor_from_device": (i32, [vp, i32, P_i64, i32, P_i64, vp, C.POINTER(vp)]),

@@ -1,4 +1,5 @@
 // extern "C" boundary of libqtnh_b200.so (declared in include/qtnh_b200.h).
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -532,6 +533,30 @@ int qtnh_qft_layer(qtnh_tensor_t t, int j) {
     TP& p = impl_of(t);
     make_exclusive(p);
     op_qft_layer(p, j);
+  });
+}
+
+int qtnh_all_to_all_v(qtnh_rank_t r, int n_members, const int* members, const void* send_buf,
+                      const int64_t* send_counts, const int64_t* send_displs, void* recv_buf,
+                      const int64_t* recv_counts, const int64_t* recv_displs) {
+  return guard([&] {
+    RankCtx& x = ctx_of(r);
+    if (n_members < 1) throw_invalid("group members must be non-empty");
+    need(members, "members");
+    std::vector<int> mem(members, members + n_members);
+    std::vector<int> sorted = mem;
+    std::sort(sorted.begin(), sorted.end());
+    if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end()) throw_invalid("duplicate group member");
+    for (int m : mem)
+      if (m < 0 || m >= x.world->size) throw_invalid("group member " + std::to_string(m) + " out of range");
+    if (!std::binary_search(sorted.begin(), sorted.end(), x.rank))
+      throw_invalid("rank " + std::to_string(x.rank) + " cannot open a group it is not a member of");
+    std::vector<Xfer> sends, recvs;
+    for (int i = 0; i < n_members; ++i) {
+      if (send_counts && send_counts[i] > 0) sends.push_back({mem[i], send_displs ? send_displs[i] : 0, send_counts[i]});
+      if (recv_counts && recv_counts[i] > 0) recvs.push_back({mem[i], recv_displs ? recv_displs[i] : 0, recv_counts[i]});
+    }
+    exchange(x, sorted, send_buf, sends, recv_buf, recvs);
   });
 }
 
