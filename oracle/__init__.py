@@ -78,6 +78,8 @@ class _Ref:
         L.qref_gate.argtypes = [i32, i32, i32, P64, vp, i32, P32, vp, vp]
         L.qref_qft.argtypes = [i32, i32, i32, vp, i32, i32, vp, vp]
         L.qref_svd.argtypes = [i32, i64, i64, vp, i64, i32, vp, vp, vp, vp]
+        L.qref_save.argtypes = [i32, i32, P64, i32, P64, vp, C.c_char_p]
+        L.qref_load.argtypes = [i32, C.c_char_p, P64, P32, P32, P64, vp, i64]
 
     def _check(self, rc):
         if rc:
@@ -159,6 +161,19 @@ class _Ref:
         self._check(self.lib.qref_qft(world, n, split, state.ctypes.data, int(swaps), gate_limit,
                                       out.ctypes.data, t))
         return (out, t[0]) if timing else out
+
+    def save(self, world, dims, split, dist, data, path):
+        data = _c128(data)
+        self._check(self.lib.qref_save(world, len(dims), _i64(dims), split, _i64(dist or (1, 1, 0)),
+                                       data.ctypes.data, path.encode()))
+
+    def load(self, world, path, cap=1 << 24):
+        dims, nd, split, dist = _i64([0] * 64), (C.c_int * 1)(), (C.c_int * 1)(), _i64([0, 0, 0])
+        out = np.empty(cap, np.complex128)
+        self._check(self.lib.qref_load(world, path.encode(), dims, nd, split, dist, out.ctypes.data, cap))
+        n = nd[0]
+        d = [dims[i] for i in range(n)]
+        return d, split[0], (dist[0], dist[1], dist[2]), out[: int(np.prod(d)) if d else 1].copy()
 
     def svd(self, a: np.ndarray, chi: int = 0, absorb: int = 0, world: int = 1, timing=False):
         a = _c128(a)

@@ -354,6 +354,46 @@ int qref_qft(int world, int n, int split, const double* in, int swaps, int gate_
   });
 }
 
+// ---- serialization (tensor.hpp:373-446): QTNHTEN1 files ----------------------------
+int qref_save(int world, int nd, const int64_t* dims, int split, const int64_t* dist, const double* in,
+              const char* path) {
+  return guarded([&] {
+    IndexTuple shape = make_shape(nd, dims, split);
+    auto global = to_cvec(in, shape.total_size());
+    std::string p(path);
+    World w(world);
+    w.run([&](Rank& rk) {
+      Tensor t = Tensor::from_global(rk, shape, make_dist(dist), global);
+      t.save(p);
+    });
+  });
+}
+
+/// Loads on World(world); writes dims (up to 64), split, dist and the global vector.
+int qref_load(int world, const char* path, int64_t* dims, int* nd, int* split, int64_t* dist, double* out,
+              int64_t cap) {
+  return guarded([&] {
+    std::string p(path);
+    std::mutex mu;
+    World w(world);
+    w.run([&](Rank& rk) {
+      Tensor t = Tensor::load(rk, p);
+      auto g = t.to_global_vector();
+      if (t.in_span() && rk.rank() == t.dist().offset) {
+        std::lock_guard<std::mutex> lk(mu);
+        *nd = t.shape().n_idx();
+        *split = t.shape().split;
+        for (int i = 0; i < t.shape().n_idx(); ++i) dims[i] = t.shape().dims[i];
+        dist[0] = t.dist().stretch;
+        dist[1] = t.dist().cycles;
+        dist[2] = t.dist().offset;
+        if (static_cast<int64_t>(g.size()) > cap) throw Error("output capacity too small");
+        from_cvec(g, out);
+      }
+    });
+  });
+}
+
 // ---- SVD / truncation / absorption (linalg.hpp:402-523) -------------------------
 /// a: m x n ROW-major. Outputs ROW-major u (m x chi), s (chi), vh (chi x n).
 /// chi <= 0 means no truncation (chi = min(m, n)). absorb: 0 none, 1 left

@@ -402,6 +402,88 @@ class Tensor:
         check(lib.qtnh_tensor_to_global(self._h, out.ctypes.data))
         return out
 
+    # -- serialization (tensor.hpp:373-446) --------------------------------------------------
+    _MAGIC = b"QTNHTEN1"
+
+    def save(self, path: str) -> None:
+        """Span-collective save in the reference's QTNHTEN1 format (dense variant):
+        magic, u32 variant, u32 rank, u32 split, i64 stretch/cycles/offset, i64 dims,
+        u64 payload count, LE f64 (re, im) pairs in global row-major order; only the
+        first span rank writes."""
+        import struct
+
+        g = self.to_global_vector()
+        if not self.in_span() or self.ctx_rank.rank() != self.dist().offset:
+            return
+        sh, d = self.shape(), self.dist()
+        with open(path, "wb") as f:
+            f.write(self._MAGIC)
+            f.write(struct.pack("<III", 0, sh.n_idx(), sh.split))
+            f.write(struct.pack("<qqq", d.stretch, d.cycles, d.offset))
+            f.write(struct.pack("<%dq" % sh.n_idx(), *sh.dims))
+            f.write(struct.pack("<Q", g.size))
+            f.write(np.ascontiguousarray(g, dtype="<c16").tobytes())
+
+    @staticmethod
+    def load(rank: "Rank", path: str) -> "Tensor":
+        """Read a QTNHTEN1 file (every rank reads it independently, tensor.hpp:399-440).
+        Dense and symmetric payloads load as they are; diagonal, identity and swap
+        variants are materialised densely (tensor.hpp:282-296)."""
+        import struct
+
+        with open(path, "rb") as f:
+            blob = f.read()
+        if blob[:8] != Tensor._MAGIC:
+            raise Error("not a qtnh tensor stream")
+        off = 8
+        try:
+            var, r, split = struct.unpack_from("<III", blob, off)
+            off += 12
+            st, cy, of = struct.unpack_from("<qqq", blob, off)
+            off += 24
+            dims = list(struct.unpack_from("<%dq" % r, blob, off))
+            off += 8 * r
+        except struct.error:
+            raise Error("truncated tensor stream")
+        shape = IndexTuple(dims, split)
+        total = shape.total_size()
+        if var in (3, 4):  # identity / swap: pairs (in, out) of positions
+            (npairs,) = struct.unpack_from("<Q", blob, off)
+            off += 8
+            pr = struct.unpack_from("<%dq" % (2 * npairs), blob, off)
+            pin, pout = list(pr[0::2]), list(pr[1::2])
+            if var == 4:
+                pout[0], pout[1] = pout[1], pout[0]
+            idx = np.indices(dims).reshape(r, -1)
+            ok = np.ones(total, bool)
+            for a, b in zip(pin, pout):
+                ok &= idx[a] == idx[b]
+            g = ok.astype(np.complex128)
+        else:
+            (count,) = struct.unpack_from("<Q", blob, off)
+            off += 8
+            if len(blob) < off + 16 * count:
+                raise Error("truncated tensor stream")
+            payload = np.frombuffer(blob, dtype="<c16", count=count, offset=off).astype(np.complex128)
+            if var in (0, 1):
+                g = payload
+            elif var == 2:  # diagonal over the half-split (in, out) layout
+                kd, kl = split // 2, (r - split) // 2
+                in_dims = dims[:kd] + dims[split:split + kl]
+                idx = np.indices(dims).reshape(r, -1)
+                on = np.ones(total, bool)
+                for i in range(kd):
+                    on &= idx[i] == idx[kd + i]
+                for i in range(kl):
+                    on &= idx[split + i] == idx[split + kl + i]
+                flat_in = np.zeros(total, np.int64)
+                for pos in list(range(kd)) + list(range(split, split + kl)):
+                    flat_in = flat_in * dims[pos] + idx[pos]
+                g = np.where(on, payload[np.minimum(flat_in, count - 1)], 0)
+            else:
+                raise Error("corrupt tensor stream")
+        return Tensor.from_global(rank, shape, DistParams(st, cy, of), g)
+
     def free(self) -> None:
         if self._h is not None:
             lib.qtnh_tensor_free(self._h)
