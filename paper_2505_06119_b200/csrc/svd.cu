@@ -33,9 +33,6 @@ namespace qtnhb {
 
 namespace {
 
-#ifndef QTNH_SVD_SORT_ROWS
-#define QTNH_SVD_SORT_ROWS 0
-#endif
 constexpr int kB = 16;        // rows per block
 constexpr int kP2 = 2 * kB;   // rows per pair (inner problem size)
 constexpr int kGramCols = 64; // column chunk of the Gram kernel
@@ -126,160 +123,9 @@ __global__ void __launch_bounds__(256) k_svd_gram(const double2* __restrict__ wk
 }
 
 // ---- inner eigensolver: W with W^H G W diagonal; writes W^H ----------------------------
-__device__ __forceinline__ bool sort_rows() { return QTNH_SVD_SORT_ROWS; }
-
 __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
   // non-negative doubles order like their bit patterns
   atomicMax(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(__double_as_longlong(v)));
-}
-
-__global__ void __launch_bounds__(256) k_svd_eigen(const double2* __restrict__ part, double2* __restrict__ wh,
-                                                   int* __restrict__ flags, double* __restrict__ off_max,
-                                                   int npairs, int splits, double tol, int inner_sweeps,
-                                                   const double* __restrict__ floor_abs) {
-  const int pair = blockIdx.x, mat = blockIdx.y, tid = threadIdx.x;
-  // Rows whose norms are negligible against ||A||_F (absolute floor, the accuracy
-  // class of the reference's zgesdd: errors O(eps sigma_max)) stop steering the
-  // convergence test; everything above the floor is held to a relative test.
-  const double fl = floor_abs[mat];
-  __shared__ double2 G[kP2][kP2 + 1];
-  __shared__ double2 V[kP2][kP2 + 1];
-  __shared__ double rot_c[kB], rot_s[kB];
-  __shared__ double2 rot_ph[kB];  // e^{-i phi}
-  __shared__ int rp_[kB], rq_[kB];
-  __shared__ double red[256];
-  const double2* P = part + (static_cast<int64_t>(mat) * npairs + pair) * splits * kP2 * kP2;
-  for (int e = tid; e < kP2 * kP2; e += 256) {
-    int i = e / kP2, j = e % kP2;
-    double2 s = make_double2(0.0, 0.0);
-    for (int sp = 0; sp < splits; ++sp) {
-      double2 v = P[sp * kP2 * kP2 + e];
-      s.x += v.x;
-      s.y += v.y;
-    }
-    G[i][j] = s;
-    V[i][j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-  }
-  __syncthreads();
-  auto measure = [&]() {
-    double mx = 0.0;
-    for (int e = tid; e < kP2 * kP2; e += 256) {
-      int i = e / kP2, j = e % kP2;
-      if (i >= j) continue;
-      double d = sqrt(fmax(G[i][i].x * G[j][j].x, 0.0));
-      double g = hypot(G[i][j].x, G[i][j].y);
-      double den = fmax(d, fl);
-      if (den > 0.0) mx = fmax(mx, g / den);
-      else if (g > 0.0) mx = fmax(mx, 1.0);
-    }
-    red[tid] = mx;
-    __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
-      if (tid < s) red[tid] = fmax(red[tid], red[tid + s]);
-      __syncthreads();
-    }
-    double r = red[0];
-    __syncthreads();
-    return r;
-  };
-  double off = measure();
-  if (tid == 0) atomic_max_nonneg(off_max + mat, off);
-  const int64_t fidx = static_cast<int64_t>(mat) * npairs + pair;
-  if (off < tol) {
-    if (tid == 0) flags[fidx] = 0;
-    return;
-  }
-  for (int sw = 0; sw < inner_sweeps; ++sw) {
-    for (int step = 0; step < kP2 - 1; ++step) {
-      if (tid < kB) {
-        // circle method over kP2 indices: fixed kP2-1, others rotate
-        int p, q;
-        if (tid == 0) {
-          p = step;
-          q = kP2 - 1;
-        } else {
-          p = (step + tid) % (kP2 - 1);
-          q = (step - tid + (kP2 - 1)) % (kP2 - 1);
-        }
-        if (p > q) {
-          int t = p;
-          p = q;
-          q = t;
-        }
-        double a = G[p][p].x, b = G[q][q].x;
-        double2 x = G[p][q];
-        double ax = hypot(x.x, x.y);
-        double c = 1.0, s = 0.0;
-        double2 ph = make_double2(1.0, 0.0);
-        if (ax > 0.0 && ax > 1e-300 && !(ax <= 1e-17 * sqrt(fabs(a * b)))) {
-          ph = make_double2(x.x / ax, -x.y / ax);  // e^{-i phi}
-          double tau = (b - a) / (2.0 * ax);
-          double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-          c = 1.0 / sqrt(1.0 + t * t);
-          s = t * c;
-        }
-        rot_c[tid] = c;
-        rot_s[tid] = s;
-        rot_ph[tid] = ph;
-        rp_[tid] = p;
-        rq_[tid] = q;
-      }
-      __syncthreads();
-      // G <- J^H G J in one pass: thread (k, l) owns the 2x2 block rows {p_k, q_k}
-      // x cols {p_l, q_l} (pairs are disjoint, so blocks are independent);
-      // V <- V J alongside. J = [[c, s], [-s e^{-i phi}, c e^{-i phi}]].
-      {
-        const int k = tid >> 4, l = tid & 15;
-        const int pk = rp_[k], qk = rq_[k], pl = rp_[l], ql = rq_[l];
-        const double ck = rot_c[k], sk = rot_s[k], cl = rot_c[l], sl = rot_s[l];
-        const double2 ek = cconj(rot_ph[k]), el = rot_ph[l];
-        double2 a = G[pk][pl], b = G[pk][ql], c = G[qk][pl], d = G[qk][ql];
-        // right: columns
-        double2 bq = cmul(b, el), dq = cmul(d, el);
-        double2 a1 = make_double2(cl * a.x - sl * bq.x, cl * a.y - sl * bq.y);
-        double2 b1 = make_double2(sl * a.x + cl * bq.x, sl * a.y + cl * bq.y);
-        double2 c1 = make_double2(cl * c.x - sl * dq.x, cl * c.y - sl * dq.y);
-        double2 d1 = make_double2(sl * c.x + cl * dq.x, sl * c.y + cl * dq.y);
-        // left: rows
-        double2 c2 = cmul(c1, ek), d2 = cmul(d1, ek);
-        G[pk][pl] = make_double2(ck * a1.x - sk * c2.x, ck * a1.y - sk * c2.y);
-        G[pk][ql] = make_double2(ck * b1.x - sk * d2.x, ck * b1.y - sk * d2.y);
-        G[qk][pl] = make_double2(sk * a1.x + ck * c2.x, sk * a1.y + ck * c2.y);
-        G[qk][ql] = make_double2(sk * b1.x + ck * d2.x, sk * b1.y + ck * d2.y);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int i = tid & 31, kk = (tid >> 5) + 8 * h;
-          const int p = rp_[kk], q = rq_[kk];
-          const double cc = rot_c[kk], ss = rot_s[kk];
-          double2 vp = V[i][p], vq = cmul(V[i][q], rot_ph[kk]);
-          V[i][p] = make_double2(cc * vp.x - ss * vq.x, cc * vp.y - ss * vq.y);
-          V[i][q] = make_double2(ss * vp.x + cc * vq.x, ss * vp.y + cc * vq.y);
-        }
-      }
-      __syncthreads();
-    }
-    if (sw + 1 < inner_sweeps && measure() < tol * 1e-2) break;
-  }
-  // de Rijk-style ordering: output rows sorted by the new row norms (diag of
-  // W^H G W), largest first, so large singular values collect in low blocks and
-  // the sweeps converge faster.
-  __shared__ int dst_of[kP2];
-  if (tid < kP2) {
-    double di = G[tid][tid].x;
-    int rank = 0;
-    for (int j = 0; j < kP2; ++j) {
-      double dj = G[j][j].x;
-      rank += (dj > di) || (dj == di && j < tid);
-    }
-    dst_of[tid] = sort_rows() ? rank : tid;
-  }
-  __syncthreads();
-  double2* out = wh + fidx * kP2 * kP2;
-  for (int e = tid; e < kP2 * kP2; e += 256) {
-    int i = e / kP2, j = e % kP2;
-    out[dst_of[i] * kP2 + j] = cconj(V[j][i]);  // row i of W^H -> its sorted slot
-  }
-  if (tid == 0) flags[fidx] = 1;
 }
 
 // ---- in-place row update: WK_pair <- W^H WK_pair -----------------------------------------
@@ -333,72 +179,194 @@ __global__ void __launch_bounds__(256) k_svd_update(double2* __restrict__ wk, co
 }
 
 
-// ---- DMMA variants of the two GEMM-shaped steps -----------------------------------------
-// Gram on the FP64 tensor cores: G = X X^H, X = 32 rows x (column slice). 4 warps,
-// warp w owns rows [8w, 8w+8) x all 32 columns (4 m8n8 tiles); A and B fragments
-// come from the same shared tile (B = conj of X), pitch = 4 (mod 8) x 16 B.
-constexpr int kGK = 64;  // columns per staged chunk
-__global__ void __launch_bounds__(128) k_svd_gram_mma(const double2* __restrict__ wk, double2* __restrict__ part,
-                                                      const int* __restrict__ tab, int round, int npairs,
-                                                      int splits, int64_t rp, int64_t L, int64_t qw) {
+// ---- block-size templated kernels (B rows per block, pair of 2B rows) ------------------
+// Dynamic shared memory: the pair's Gram matrix G and eigenvectors V (2B x 2B+1).
+template <int B>
+__global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__ part, double2* __restrict__ wh,
+                                                     int* __restrict__ flags, double* __restrict__ off_max,
+                                                     int npairs, int splits, double tol, int inner_sweeps,
+                                                     const double* __restrict__ floor_abs) {
+  constexpr int P2 = 2 * B, LD = P2 + 1;
+  const int pair = blockIdx.x, mat = blockIdx.y, tid = threadIdx.x;
+  const double fl = floor_abs[mat];
+  extern __shared__ double2 esm[];
+  double2* G = esm;            // [P2][LD]
+  double2* V = esm + P2 * LD;  // [P2][LD]
+  __shared__ double rot_c[B], rot_s[B];
+  __shared__ double2 rot_ph[B];
+  __shared__ int rp_[B], rq_[B];
+  __shared__ double red[256];
+  const double2* P = part + (static_cast<int64_t>(mat) * npairs + pair) * splits * P2 * P2;
+  for (int e = tid; e < P2 * P2; e += 256) {
+    int i = e / P2, j = e % P2;
+    double2 sm = make_double2(0.0, 0.0);
+    for (int sp = 0; sp < splits; ++sp) {
+      double2 v = P[static_cast<int64_t>(sp) * P2 * P2 + e];
+      sm.x += v.x;
+      sm.y += v.y;
+    }
+    G[i * LD + j] = sm;
+    V[i * LD + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  auto measure = [&]() {
+    double mx = 0.0;
+    for (int e = tid; e < P2 * P2; e += 256) {
+      int i = e / P2, j = e % P2;
+      if (i >= j) continue;
+      double d = sqrt(fmax(G[i * LD + i].x * G[j * LD + j].x, 0.0));
+      double2 gij = G[i * LD + j];
+      double g = hypot(gij.x, gij.y);
+      double den = fmax(d, fl);
+      if (den > 0.0) mx = fmax(mx, g / den);
+      else if (g > 0.0) mx = fmax(mx, 1.0);
+    }
+    red[tid] = mx;
+    __syncthreads();
+    for (int st = 128; st > 0; st >>= 1) {
+      if (tid < st) red[tid] = fmax(red[tid], red[tid + st]);
+      __syncthreads();
+    }
+    double res = red[0];
+    __syncthreads();
+    return res;
+  };
+  double off = measure();
+  if (tid == 0) atomic_max_nonneg(off_max + mat, off);
+  const int64_t fidx = static_cast<int64_t>(mat) * npairs + pair;
+  if (off < tol) {
+    if (tid == 0) flags[fidx] = 0;
+    return;
+  }
+  for (int sw = 0; sw < inner_sweeps; ++sw) {
+    for (int step = 0; step < P2 - 1; ++step) {
+      if (tid < B) {
+        int p, q;
+        if (tid == 0) {
+          p = step;
+          q = P2 - 1;
+        } else {
+          p = (step + tid) % (P2 - 1);
+          q = (step - tid + (P2 - 1)) % (P2 - 1);
+        }
+        if (p > q) {
+          int tt = p;
+          p = q;
+          q = tt;
+        }
+        double a = G[p * LD + p].x, b = G[q * LD + q].x;
+        double2 x = G[p * LD + q];
+        double ax = hypot(x.x, x.y);
+        double c = 1.0, sn = 0.0;
+        double2 ph = make_double2(1.0, 0.0);
+        if (ax > 1e-300 && !(ax <= 1e-17 * sqrt(fabs(a * b)))) {
+          ph = make_double2(x.x / ax, -x.y / ax);
+          double tau = (b - a) / (2.0 * ax);
+          double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+          c = 1.0 / sqrt(1.0 + t * t);
+          sn = t * c;
+        }
+        rot_c[tid] = c;
+        rot_s[tid] = sn;
+        rot_ph[tid] = ph;
+        rp_[tid] = p;
+        rq_[tid] = q;
+      }
+      __syncthreads();
+      for (int task = tid; task < B * B; task += 256) {
+        const int k = task / B, l = task % B;
+        const int pk = rp_[k], qk = rq_[k], pl = rp_[l], ql = rq_[l];
+        const double ck = rot_c[k], sk = rot_s[k], cl = rot_c[l], sl = rot_s[l];
+        const double2 ek = cconj(rot_ph[k]), el = rot_ph[l];
+        double2 a = G[pk * LD + pl], b = G[pk * LD + ql], c = G[qk * LD + pl], d = G[qk * LD + ql];
+        double2 bq = cmul(b, el), dq = cmul(d, el);
+        double2 a1 = make_double2(cl * a.x - sl * bq.x, cl * a.y - sl * bq.y);
+        double2 b1 = make_double2(sl * a.x + cl * bq.x, sl * a.y + cl * bq.y);
+        double2 c1 = make_double2(cl * c.x - sl * dq.x, cl * c.y - sl * dq.y);
+        double2 d1 = make_double2(sl * c.x + cl * dq.x, sl * c.y + cl * dq.y);
+        double2 c2 = cmul(c1, ek), d2 = cmul(d1, ek);
+        G[pk * LD + pl] = make_double2(ck * a1.x - sk * c2.x, ck * a1.y - sk * c2.y);
+        G[pk * LD + ql] = make_double2(ck * b1.x - sk * d2.x, ck * b1.y - sk * d2.y);
+        G[qk * LD + pl] = make_double2(sk * a1.x + ck * c2.x, sk * a1.y + ck * c2.y);
+        G[qk * LD + ql] = make_double2(sk * b1.x + ck * d2.x, sk * b1.y + ck * d2.y);
+      }
+      for (int task = tid; task < P2 * B; task += 256) {
+        const int i = task % P2, kk = task / P2;
+        const int p = rp_[kk], q = rq_[kk];
+        const double cc = rot_c[kk], ss = rot_s[kk];
+        double2 vp = V[i * LD + p], vq = cmul(V[i * LD + q], rot_ph[kk]);
+        V[i * LD + p] = make_double2(cc * vp.x - ss * vq.x, cc * vp.y - ss * vq.y);
+        V[i * LD + q] = make_double2(ss * vp.x + cc * vq.x, ss * vp.y + cc * vq.y);
+      }
+      __syncthreads();
+    }
+    if (sw + 1 < inner_sweeps && measure() < tol * 1e-2) break;
+  }
+  double2* out = wh + fidx * P2 * P2;
+  for (int e = tid; e < P2 * P2; e += 256) {
+    int i = e / P2, j = e % P2;
+    out[e] = cconj(V[j * LD + i]);  // W^H
+  }
+  if (tid == 0) flags[fidx] = 1;
+}
+
+// Gram of a row-block pair on DMMA: P2/8 warps, warp w owns rows [8w, 8w+8) x P2.
+template <int B>
+__global__ void __launch_bounds__(B * 8) k_svd_gram_mma_t(const double2* __restrict__ wk, double2* __restrict__ part,
+                                                          const int* __restrict__ tab, int round, int npairs,
+                                                          int splits, int64_t rp, int64_t L, int64_t qw) {
+  constexpr int P2 = 2 * B, NT = P2 / 8, T = B * 8, GK = B >= 32 ? 32 : 64, PX = GK + 4;
   const int pair = blockIdx.x, split = blockIdx.y, mat = blockIdx.z;
   const int64_t W = L + qw;
   const int* pr = tab + (static_cast<int64_t>(round) * npairs + pair) * 2;
   const int bi = pr[0], bj = pr[1];
   const double2* K = wk + static_cast<int64_t>(mat) * rp * W;
-  constexpr int PX = kGK + 4;
-  __shared__ double2 xs[kP2][PX];
+  __shared__ double2 xs[P2][PX];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int fr = lane >> 2, fk = lane & 3;
-  double acc_re[4][2], acc_im[4][2];
+  double acc_re[NT][2], acc_im[NT][2];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) acc_re[j][0] = acc_re[j][1] = acc_im[j][0] = acc_im[j][1] = 0.0;
+  for (int j = 0; j < NT; ++j) acc_re[j][0] = acc_re[j][1] = acc_im[j][0] = acc_im[j][1] = 0.0;
   int64_t per = (L + splits - 1) / splits;
   int64_t c0 = split * per, c1 = min(L, c0 + per);
-  for (int64_t cb = c0; cb < c1; cb += kGK) {
-    for (int e = tid; e < kP2 * kGK; e += 128) {
-      int r = e / kGK, c = e % kGK;
-      int64_t row = (r < kB ? bi * kB + r : bj * kB + (r - kB));
+  for (int64_t cb = c0; cb < c1; cb += GK) {
+    for (int e = tid; e < P2 * GK; e += T) {
+      int r = e / GK, c = e % GK;
+      int64_t row = (r < B ? bi * B + r : bj * B + (r - B));
       int64_t col = cb + c;
       xs[r][c] = col < c1 ? K[row * W + col] : make_double2(0.0, 0.0);
     }
     __syncthreads();
 #pragma unroll
-    for (int k4 = 0; k4 < kGK; k4 += 4) {
+    for (int k4 = 0; k4 < GK; k4 += 4) {
       double2 av = xs[warp * 8 + fr][k4 + fk];
-      double b_re[4], b_im[4], nb_im[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        double2 bv = xs[j * 8 + fr][k4 + fk];  // B = conj(X)^T: (k, j) -> conj(X[j][k])
-        b_re[j] = bv.x;
-        b_im[j] = -bv.y;
-        nb_im[j] = bv.y;
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        dmma(acc_re[j], av.x, b_re[j]);
-        dmma(acc_im[j], av.x, b_im[j]);
-        dmma(acc_re[j], av.y, nb_im[j]);
-        dmma(acc_im[j], av.y, b_re[j]);
+      for (int j = 0; j < NT; ++j) {
+        double2 bv = xs[j * 8 + fr][k4 + fk];
+        dmma(acc_re[j], av.x, bv.x);
+        dmma(acc_im[j], av.x, -bv.y);
+        dmma(acc_re[j], av.y, bv.y);
+        dmma(acc_im[j], av.y, bv.x);
       }
     }
     __syncthreads();
   }
-  double2* out = part + ((static_cast<int64_t>(mat) * npairs + pair) * splits + split) * kP2 * kP2;
+  double2* out = part + ((static_cast<int64_t>(mat) * npairs + pair) * splits + split) * P2 * P2;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
+  for (int j = 0; j < NT; ++j) {
     int row = warp * 8 + fr, col = j * 8 + 2 * fk;
-    out[row * kP2 + col] = make_double2(acc_re[j][0], acc_im[j][0]);
-    out[row * kP2 + col + 1] = make_double2(acc_re[j][1], acc_im[j][1]);
+    out[row * P2 + col] = make_double2(acc_re[j][0], acc_im[j][0]);
+    out[row * P2 + col + 1] = make_double2(acc_re[j][1], acc_im[j][1]);
   }
 }
 
-// In-place update on the FP64 tensor cores: Y (32 x 48 cols) = W^H (32 x 32) X.
-// 4 warps, warp w owns rows [8w, 8w+8) x 48 columns (6 m8n8 tiles).
-constexpr int kUpdColsM = 48;
-__global__ void __launch_bounds__(128) k_svd_update_mma(double2* __restrict__ wk, const double2* __restrict__ wh,
-                                                        const int* __restrict__ flags, const int* __restrict__ tab,
-                                                        int round, int npairs, int64_t rp, int64_t L, int64_t qw) {
+// In-place update on DMMA: Y (P2 x 48 cols) = W^H (P2 x P2) X; dynamic smem.
+template <int B>
+__global__ void __launch_bounds__(B * 8) k_svd_update_mma_t(double2* __restrict__ wk, const double2* __restrict__ wh,
+                                                            const int* __restrict__ flags,
+                                                            const int* __restrict__ tab, int round, int npairs,
+                                                            int64_t rp, int64_t L, int64_t qw) {
+  constexpr int P2 = 2 * B, T = B * 8, UC = 48, NT = UC / 8, PW = P2 + 4, PX = UC + 2;
   const int pair = blockIdx.y, mat = blockIdx.z, tid = threadIdx.x;
   const int64_t fidx = static_cast<int64_t>(mat) * npairs + pair;
   if (!flags[fidx]) return;
@@ -406,42 +374,40 @@ __global__ void __launch_bounds__(128) k_svd_update_mma(double2* __restrict__ wk
   const int* pr = tab + (static_cast<int64_t>(round) * npairs + pair) * 2;
   const int bi = pr[0], bj = pr[1];
   double2* K = wk + static_cast<int64_t>(mat) * rp * W;
-  constexpr int UC = kUpdColsM, NT = UC / 8;
-  constexpr int PW = kP2 + 4, PX = UC + 2;
-  __shared__ double2 ws[kP2][PW];
-  __shared__ double2 xs[kP2][PX];
+  extern __shared__ double2 usm[];
+  double2* ws = usm;            // [P2][PW]
+  double2* xs = usm + P2 * PW;  // [P2][PX]
   const int lane = tid & 31, warp = tid >> 5, fr = lane >> 2, fk = lane & 3;
-  const double2* Wh = wh + fidx * kP2 * kP2;
-  for (int e = tid; e < kP2 * kP2; e += 128) ws[e / kP2][e % kP2] = Wh[e];
-  for (int64_t cb = static_cast<int64_t>(blockIdx.x) * UC; cb < W;
-       cb += static_cast<int64_t>(gridDim.x) * UC) {
-    for (int e = tid; e < kP2 * UC; e += 128) {
+  const double2* Wh = wh + fidx * P2 * P2;
+  for (int e = tid; e < P2 * P2; e += T) ws[(e / P2) * PW + e % P2] = Wh[e];
+  for (int64_t cb = static_cast<int64_t>(blockIdx.x) * UC; cb < W; cb += static_cast<int64_t>(gridDim.x) * UC) {
+    for (int e = tid; e < P2 * UC; e += T) {
       int r = e / UC, c = e % UC;
-      int64_t row = r < kB ? bi * kB + r : bj * kB + (r - kB);
+      int64_t row = r < B ? bi * B + r : bj * B + (r - B);
       int64_t col = cb + c;
-      xs[r][c] = col < W ? K[row * W + col] : make_double2(0.0, 0.0);
+      xs[r * PX + c] = col < W ? K[row * W + col] : make_double2(0.0, 0.0);
     }
     __syncthreads();
     double acc_re[NT][2], acc_im[NT][2];
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc_re[j][0] = acc_re[j][1] = acc_im[j][0] = acc_im[j][1] = 0.0;
-#pragma unroll
-    for (int k4 = 0; k4 < kP2; k4 += 4) {
-      double2 av = ws[warp * 8 + fr][k4 + fk];
+#pragma unroll 4
+    for (int k4 = 0; k4 < P2; k4 += 4) {
+      double2 av = ws[(warp * 8 + fr) * PW + k4 + fk];
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
-        double2 bv = xs[k4 + fk][j * 8 + fr];
+        double2 bv = xs[(k4 + fk) * PX + j * 8 + fr];
         dmma(acc_re[j], av.x, bv.x);
         dmma(acc_im[j], av.x, bv.y);
         dmma(acc_re[j], av.y, -bv.y);
         dmma(acc_im[j], av.y, bv.x);
       }
     }
-    __syncthreads();  // all reads of xs done before any write-back
+    __syncthreads();
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       int r = warp * 8 + fr;
-      int64_t row = r < kB ? bi * kB + r : bj * kB + (r - kB);
+      int64_t row = r < B ? bi * B + r : bj * B + (r - B);
       int64_t col = cb + j * 8 + 2 * fk;
       if (col < W) K[row * W + col] = make_double2(acc_re[j][0], acc_im[j][0]);
       if (col + 1 < W) K[row * W + col + 1] = make_double2(acc_re[j][1], acc_im[j][1]);
@@ -451,18 +417,19 @@ __global__ void __launch_bounds__(128) k_svd_update_mma(double2* __restrict__ wk
 
 // ---- ||A||_F^2 per matrix -> the absolute convergence floor ------------------------------
 __global__ void k_svd_fro(const double2* __restrict__ a, int64_t count, double* __restrict__ out, double rel) {
-  const int64_t mat = blockIdx.x;
+  const int64_t mat = blockIdx.y;
   const double2* A = a + mat * count;
   __shared__ double red[256];
   double s = 0.0;
-  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) s += A[i].x * A[i].x + A[i].y * A[i].y;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    s += A[i].x * A[i].x + A[i].y * A[i].y;
   red[threadIdx.x] = s;
   __syncthreads();
   for (int k = blockDim.x / 2; k > 0; k >>= 1) {
     if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
     __syncthreads();
   }
-  if (threadIdx.x == 0) out[mat] = rel * red[0];
+  if (threadIdx.x == 0) atomicAdd(out + mat, rel * red[0]);  // order-independent enough for a floor
 }
 
 // ---- row norms of the X part -----------------------------------------------------------------
@@ -629,16 +596,27 @@ int sms() {
 
 }  // namespace
 
-void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* u, void* s,
-                 void* vh, int* sweeps_out) {
-  if (batch < 1 || m < 1 || n < 1) throw_invalid("svd needs positive batch and matrix dimensions");
-  if (absorb < 0 || absorb > 3) throw_invalid("invalid absorb mode");
+namespace {
+
+int block_rows() {
+  static int v = [] {
+    const char* e = std::getenv("QTNH_SVD_B");
+    int b = e ? std::atoi(e) : 16;
+    return b == 32 ? 32 : 16;
+  }();
+  return v;
+}
+
+template <int B>
+void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* u, void* s, void* vh,
+              int* sweeps_out) {
+  constexpr int P2 = 2 * B;
   cudaStream_t st = r.stream;
   const Dim rows = std::min(m, n), L = std::max(m, n);
   const int transpose = m > n ? 1 : 0;
   if (chi <= 0) chi = rows;
-  const Dim nblk2 = ((rows + kP2 - 1) / kP2) * 2;  // 2P blocks of kB rows
-  const Dim rp = nblk2 * kB;
+  const Dim nblk2 = ((rows + P2 - 1) / P2) * 2;  // 2P blocks of B rows
+  const Dim rp = nblk2 * B;
   const int npairs = static_cast<int>(nblk2 / 2), rounds = static_cast<int>(nblk2 - 1);
   // Without a transpose the left factor is recovered at the end as U S = A Vh^H
   // (one GEMM; exact for absorb-left, no division by sigma), so the row
@@ -646,6 +624,7 @@ void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, in
   const bool acc_q = transpose || accumulate_q();
   const Dim qw = acc_q ? rp : 0;
   const Dim W = L + qw;
+  const bool mma = use_mma() || B != 16;
   // tournament table (circle method, block nblk2-1 fixed)
   std::vector<int> tab(static_cast<size_t>(rounds) * npairs * 2);
   for (int rd = 0; rd < rounds; ++rd)
@@ -665,8 +644,8 @@ void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, in
                                                                 (L + kGramCols - 1) / kGramCols)));
   DevBuf wk(static_cast<size_t>(batch * rp * W) * 16, r);
   DevBuf d_tab(tab.size() * sizeof(int), r);
-  DevBuf part(static_cast<size_t>(batch * npairs * splits) * kP2 * kP2 * 16, r);
-  DevBuf whb(static_cast<size_t>(batch * npairs) * kP2 * kP2 * 16, r);
+  DevBuf part(static_cast<size_t>(batch * npairs * splits) * P2 * P2 * 16, r);
+  DevBuf whb(static_cast<size_t>(batch * npairs) * P2 * P2 * 16, r);
   DevBuf flags(static_cast<size_t>(batch * npairs) * sizeof(int), r);
   DevBuf offm(static_cast<size_t>(batch) * sizeof(double), r);
   QTNH_CUDA(cudaMemcpyAsync(d_tab.ptr, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice, st));
@@ -678,18 +657,25 @@ void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, in
   }
   const double tol = tolerance();
   DevBuf floor_abs(static_cast<size_t>(batch) * sizeof(double), r);
-  k_svd_fro<<<static_cast<unsigned>(batch), 256, 0, st>>>(static_cast<const double2*>(a), m * n,
-                                                         static_cast<double*>(floor_abs.ptr), floor_rel());
+  QTNH_CUDA(cudaMemsetAsync(floor_abs.ptr, 0, batch * sizeof(double), st));
+  k_svd_fro<<<dim3(64, static_cast<unsigned>(batch)), 256, 0, st>>>(static_cast<const double2*>(a), m * n,
+                                                                   static_cast<double*>(floor_abs.ptr), floor_rel());
   QTNH_LAUNCH_CHECK();
+  const size_t eig_smem = static_cast<size_t>(2) * P2 * (P2 + 1) * 16;
+  const size_t upd_smem = static_cast<size_t>(P2) * ((P2 + 4) + (48 + 2)) * 16;
+  QTNH_CUDA(cudaFuncSetAttribute(k_svd_eigen_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_smem));
+  QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
   std::vector<double> off_h(batch);
   int sweep = 0;
   const int max_sweeps = 40;
   bool converged = false;
+  const unsigned ctiles = static_cast<unsigned>(
+      std::min<Dim>((W + 47) / 48, std::max<Dim>(1, (B == 16 ? 8 : 4) * sms() / (npairs * batch))));
   for (; sweep < max_sweeps; ++sweep) {
     QTNH_CUDA(cudaMemsetAsync(offm.ptr, 0, batch * sizeof(double), st));
     for (int rd = 0; rd < rounds; ++rd) {
-      if (use_mma())
-        k_svd_gram_mma<<<dim3(npairs, splits, static_cast<unsigned>(batch)), 128, 0, st>>>(
+      if (mma)
+        k_svd_gram_mma_t<B><<<dim3(npairs, splits, static_cast<unsigned>(batch)), B * 8, 0, st>>>(
             static_cast<const double2*>(wk.ptr), static_cast<double2*>(part.ptr), static_cast<const int*>(d_tab.ptr),
             rd, npairs, splits, rp, L, qw);
       else
@@ -697,16 +683,13 @@ void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, in
             static_cast<const double2*>(wk.ptr), static_cast<double2*>(part.ptr), static_cast<const int*>(d_tab.ptr),
             rd, npairs, splits, rp, L, qw);
       QTNH_LAUNCH_CHECK();
-      k_svd_eigen<<<dim3(npairs, static_cast<unsigned>(batch)), 256, 0, st>>>(
-          static_cast<const double2*>(part.ptr), static_cast<double2*>(whb.ptr), static_cast<int*>(flags.ptr),
-          static_cast<double*>(offm.ptr), npairs, splits, tol, inner_sweeps(),
-          static_cast<const double*>(floor_abs.ptr));
+      k_svd_eigen_t<B><<<dim3(npairs, static_cast<unsigned>(batch)), 256, eig_smem, st>>>(
+            static_cast<const double2*>(part.ptr), static_cast<double2*>(whb.ptr), static_cast<int*>(flags.ptr),
+            static_cast<double*>(offm.ptr), npairs, splits, tol, inner_sweeps(),
+            static_cast<const double*>(floor_abs.ptr));
       QTNH_LAUNCH_CHECK();
-      const Dim ucols = use_mma() ? kUpdColsM : kUpdCols;
-      unsigned ctiles = static_cast<unsigned>(std::min<Dim>((W + ucols - 1) / ucols,
-                                                            std::max<Dim>(1, (use_mma() ? 8 : 4) * sms() / (npairs * batch))));
-      if (use_mma())
-        k_svd_update_mma<<<dim3(ctiles, npairs, static_cast<unsigned>(batch)), 128, 0, st>>>(
+      if (mma)
+        k_svd_update_mma_t<B><<<dim3(ctiles, npairs, static_cast<unsigned>(batch)), B * 8, upd_smem, st>>>(
             static_cast<double2*>(wk.ptr), static_cast<const double2*>(whb.ptr), static_cast<const int*>(flags.ptr),
             static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
       else
@@ -753,8 +736,6 @@ void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, in
                                     transpose, absorb);
     QTNH_LAUNCH_CHECK();
   } else {
-    // s, Vh (absorbed per mode) and B = unit-Vh^H; then U S = A B on the tensor
-    // cores and a per-column rescale of U for the non-left modes.
     DevBuf bt(static_cast<size_t>(batch * n * chi) * 16, r);
     Dim total = chi * n + chi;
     dim3 g(static_cast<unsigned>(std::min<Dim>((total + 255) / 256, 8192)), static_cast<unsigned>(batch));
@@ -773,6 +754,17 @@ void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, in
     }
   }
   QTNH_CUDA(cudaStreamSynchronize(st));  // host vectors (perm) are staged; keep it simple
+}
+
+}  // namespace
+
+void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* u, void* s,
+                 void* vh, int* sweeps_out) {
+  if (batch < 1 || m < 1 || n < 1) throw_invalid("svd needs positive batch and matrix dimensions");
+  if (absorb < 0 || absorb > 3) throw_invalid("invalid absorb mode");
+  // Small problems keep 16-row blocks (more pairs per round); large ones can use 32.
+  if (block_rows() == 32 && std::min(m, n) >= 256) svd_impl<32>(r, batch, m, n, a, chi, absorb, u, s, vh, sweeps_out);
+  else svd_impl<16>(r, batch, m, n, a, chi, absorb, u, s, vh, sweeps_out);
 }
 
 }  // namespace qtnhb
