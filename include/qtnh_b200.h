@@ -66,7 +66,10 @@ typedef struct qtnh_tensor_s* qtnh_tensor_t;
 int qtnh_last_error(char* buf, size_t len);
 int64_t qtnh_last_error_info(void);
 const char* qtnh_version(void);
-/* Tunables: "swap_chunk_bytes" = staging size of the in-place distributed swap. */
+/* Tunables: "swap_chunk_bytes" = staging size of the in-place distributed swap;
+   "peer_direct" (1 default) = in a local world whose ranks can address each
+   other's HBM, redistribute by peer-memory kernels (push remap, pairwise
+   in-place swap) instead of pack -> exchange -> unpack. */
 int qtnh_set_option(const char* name, double value);
 /* Number of this library's kernels launched so far by the calling process. */
 int64_t qtnh_kernel_launch_count(void);

@@ -94,16 +94,31 @@ int qtnh_world_create_local(int n, const int* devices, qtnh_world_t* out) {
     w->size = n;
     w->timeout_ms = env_timeout();
     for (int i = 0; i < n; ++i) w->devices.push_back(devices ? devices[i] : 0);
-    // Peer access between distinct devices (NVLink) for the exchange copies.
+    // Peer access between distinct devices (NVLink) for the exchange copies and
+    // the peer-memory kernels (remap push, in-place swaps).
+    w->peer_ok = true;
     for (int a : w->devices)
       for (int b : w->devices)
         if (a != b) {
           int can = 0;
           cudaDeviceCanAccessPeer(&can, a, b);
+          if (!can) w->peer_ok = false;
           if (can) {
             cudaSetDevice(a);
             cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
             if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            // tensors come from b's stream-ordered pool: map it for a as well
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, b) == cudaSuccess) {
+              cudaMemAccessDesc acc{};
+              acc.location.type = cudaMemLocationTypeDevice;
+              acc.location.id = a;
+              acc.flags = cudaMemAccessFlagsProtReadWrite;
+              if (cudaMemPoolSetAccess(pool, &acc, 1) != cudaSuccess) {
+                cudaGetLastError();
+                w->peer_ok = false;
+              }
+            }
           }
         }
     auto* h = new qtnh_world_s;
@@ -565,6 +580,7 @@ int qtnh_set_option(const char* name, double value) {
     need(name, "name");
     std::string n(name);
     if (n == "swap_chunk_bytes") set_swap_chunk_bytes(static_cast<Dim>(value));
+    else if (n == "peer_direct") set_peer_direct(value != 0);
     else throw_invalid("unknown option " + n);
   });
 }
@@ -679,7 +695,11 @@ int qtnh_remap_plan_json(int n, const int64_t* dims, int split, const int64_t* d
                     ",\"unpack\":" + std::to_string(P.unpack) + ",\"pack\":" + box(P.pack) +
                     ",\"unpack_box\":" + box(P.unpack_box) + ",\"pack_elems\":" + std::to_string(P.pack_elems) +
                     ",\"recv_elems\":" + std::to_string(P.recv_elems) + ",\"sends\":" + xf(P.sends) +
-                    ",\"recvs\":" + xf(P.recvs) + "}";
+                    ",\"recvs\":" + xf(P.recvs) + ",\"push_box\":" + box(P.push_box) + ",\"pushes\":[";
+    for (size_t i = 0; i < P.pushes.size(); ++i)
+      j += (i ? ",[" : "[") + std::to_string(P.pushes[i].peer) + "," + std::to_string(P.pushes[i].src_off) + "," +
+           std::to_string(P.pushes[i].dst_off) + "]";
+    j += "]}";
     if (j.size() + 1 > len) throw_invalid("plan buffer too small: need " + std::to_string(j.size() + 1));
     std::memcpy(buf, j.c_str(), j.size() + 1);
   });

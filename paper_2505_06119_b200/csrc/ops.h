@@ -22,6 +22,15 @@ struct RemapPlan {
   CopyBox pack, unpack_box;
   Dim pack_elems = 0, recv_elems = 0;
   std::vector<Xfer> sends, recvs;
+  // Peer-memory form (local world): this rank writes each chunk straight into
+  // the destination block of every home: dst(peer) + dst_off <- src + src_off
+  // over push_box (W indices), zero canonicalised.
+  struct Push {
+    int peer;
+    Dim src_off, dst_off;
+  };
+  std::vector<Push> pushes;
+  CopyBox push_box;
 };
 RemapPlan plan_remap(const Shape& ss, const Dist& sd, const Shape& ds, const Dist& dd, const std::vector<int>& am,
                      int rank, int world_size);

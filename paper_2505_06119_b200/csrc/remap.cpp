@@ -122,6 +122,23 @@ RemapPlan plan_remap(const Shape& ss, const Dist& sd, const Shape& ds, const Dis
     R.pack = pack_box(true);
     return R;
   }
+  // ---- pushes (peer-memory form) -------------------------------------------------------
+  if (R.src_canonical) {
+    for (int q : W) {
+      R.push_box.dims.push_back(ss.dims[q]);
+      R.push_box.in_stride.push_back(src_local_strides[q - ss.split]);
+      R.push_box.out_stride.push_back(dls(q));
+    }
+    auto cs = unflat(src_block, sdd);
+    Dim dst_off = 0;
+    for (int q : F) dst_off += cs[q] * dls(q);
+    for (Dim v = 0; v < nV; ++v) {
+      auto cv = unflat(v, vdims);
+      Dim src_off = 0;
+      for (size_t k = 0; k < V.size(); ++k) src_off += cv[k] * src_local_strides[V[k] - ss.split];
+      for (int h : dd.homes(dst_block_of(src_block, v), dst_nd)) R.pushes.push_back({h, src_off, dst_off});
+    }
+  }
   // ---- sends ------------------------------------------------------------------------
   if (R.src_canonical) {
     R.pack_to_dst = R.direct_layout && R.dst_in_span && dst_block == dst_block_of(src_block, 0);
@@ -189,6 +206,21 @@ TP remap(const TP& src, Shape ds, Dist dd, const std::vector<int>& am) {
   cudaStream_t st = r.stream;
   if (P.local_only) {
     if (P.src_canonical && dst->in_span) strided_copy(src->data(), dst->data(), P.pack, true, st);
+    return dst;
+  }
+  if (peer_direct(r)) {
+    // One pass: every canonical holder stores its chunks into the homes'
+    // destination blocks over NVLink; the second all-gather is the fence.
+    auto ptrs = peer_pointers(r, P.members, dst->in_span ? dst->data() : nullptr);
+    for (const auto& p : P.pushes) {
+      int j = static_cast<int>(std::lower_bound(P.members.begin(), P.members.end(), p.peer) - P.members.begin());
+      if (j >= static_cast<int>(P.members.size()) || P.members[j] != p.peer || !ptrs[j])
+        throw Status(QTNH_E_PROTOCOL, "peer remap target missing for pair (" + std::to_string(r.rank) + " -> " +
+                                          std::to_string(p.peer) + ")");
+      strided_copy(static_cast<const char*>(src->data()) + p.src_off * 16,
+                   static_cast<char*>(ptrs[j]) + p.dst_off * 16, P.push_box, true, st);
+    }
+    peer_pointers(r, P.members, nullptr);
     return dst;
   }
   std::shared_ptr<DevBuf> packbuf, recvbuf;
@@ -388,6 +420,35 @@ void op_swap_dist_local_inplace(TP& t, int a, int b, Dim chunk_bytes) {
   const int partners = static_cast<int>(d - 1);
   DevBuf sbuf(static_cast<size_t>(per_chunk * std::max(1, partners)) * 16, r);
   DevBuf rbuf(static_cast<size_t>(per_chunk * std::max(1, partners)) * 16, r);
+  if (peer_direct(r)) {
+    // Peer-memory form: each pair of partner blocks exchanges its two regions
+    // with one swap kernel over NVLink, no staging; the lower coordinate swaps
+    // the first half of the pair's elements, the higher one the second half.
+    Dim region_n = 1;
+    for (Dim x : rdims) region_n *= x;
+    {
+      CopyBox keep;
+      keep.dims = rdims;
+      keep.in_stride = rstr;
+      keep.out_stride = rstr;
+      char* base = static_cast<char*>(t->data()) + my_i * ls[lb] * 16;
+      strided_copy(base, base, keep, true, r.stream);
+    }
+    auto ptrs = peer_pointers(r, members, t->data());
+    for (Dim j = 0; j < d; ++j) {
+      if (j == my_i) continue;
+      auto pc = cd;
+      pc[a] = j;
+      int peer = t->dist.home(flat(pc, ddims), nd, t->cycle, t->slot);
+      void* pb = ptrs[peer - members.front()];
+      Dim half = region_n / 2;
+      Dim lo = my_i < j ? 0 : half, hi = my_i < j ? half : region_n;
+      swap_regions(static_cast<char*>(t->data()) + j * ls[lb] * 16, static_cast<char*>(pb) + my_i * ls[lb] * 16,
+                   rdims, rstr, lo, hi, r.stream);
+    }
+    peer_pointers(r, members, nullptr);
+    return;
+  }
   // canonicalise the region that stays (b = my_i): in place, element by element
   {
     CopyBox keep;

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 
 #include "nccl_loader.h"
 
@@ -203,6 +204,59 @@ void nccl_exchange(RankCtx& r, const void* send_buf, const std::vector<Xfer>& se
 }
 
 }  // namespace
+
+namespace {
+std::atomic<bool> g_peer_direct{[] {
+  const char* e = std::getenv("QTNH_PEER_DIRECT");
+  return !(e && e[0] == '0');
+}()};
+}  // namespace
+
+void set_peer_direct(bool on) { g_peer_direct.store(on); }
+
+bool peer_direct(const RankCtx& r) {
+  return r.world->kind == World::kLocal && r.world->peer_ok && g_peer_direct.load();
+}
+
+std::vector<void*> peer_pointers(RankCtx& r, const std::vector<int>& members, void* mine) {
+  World& w = *r.world;
+  int n = static_cast<int>(members.size());
+  int me = static_cast<int>(std::find(members.begin(), members.end(), r.rank) - members.begin());
+  if (me >= n) throw_invalid("rank is not a member of its own collective");
+  if (n == 1) return {mine};
+  uint64_t seq = r.seq[members]++;
+  auto key = std::make_pair(members, seq);
+  cudaEvent_t ready;
+  QTNH_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  QTNH_CUDA(cudaEventRecord(ready, r.stream));
+  auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(w.timeout_ms);
+  std::unique_lock<std::mutex> lk(w.mu);
+  World::Slot& slot = w.slots[key];
+  if (slot.posts.empty()) slot.posts.resize(n);
+  slot.posts[me].posted = true;
+  slot.posts[me].send_buf = mine;
+  slot.posts[me].packed = ready;
+  if (++slot.arrived == n) w.cv.notify_all();
+  while (slot.arrived != n) {
+    if (w.aborted) throw Status(QTNH_E_ABORTED, "world aborted");
+    if (w.timeout_ms > 0) {
+      if (w.cv.wait_until(lk, deadline) == std::cv_status::timeout && slot.arrived != n && !w.aborted)
+        throw Status(QTNH_E_PROTOCOL, "collective timed out (possible deadlock)");
+    } else {
+      w.cv.wait(lk);
+    }
+  }
+  std::vector<void*> out(n);
+  for (int j = 0; j < n; ++j) {
+    out[j] = const_cast<void*>(slot.posts[j].send_buf);
+    if (j != me) QTNH_CUDA(cudaStreamWaitEvent(r.stream, slot.posts[j].packed, 0));
+  }
+  if (++slot.left == n) {
+    for (auto& p : slot.posts) cudaEventDestroy(p.packed);
+    w.slots.erase(key);
+  }
+  return out;
+}
 
 void exchange(RankCtx& r, const std::vector<int>& members, const void* send_buf,
               const std::vector<Xfer>& sends, void* recv_buf, const std::vector<Xfer>& recvs) {

@@ -46,6 +46,7 @@ struct World {
   enum Kind { kLocal, kNccl } kind = kLocal;
   int size = 1;
   std::vector<int> devices;  // local: device of each rank
+  bool peer_ok = false;      // local: every rank can load/store every other rank's HBM
   // NCCL backend (process per GPU)
   int my_rank = 0;
   void* nccl_comm = nullptr;
@@ -79,6 +80,16 @@ struct World {
 void exchange(RankCtx& r, const std::vector<int>& members, const void* send_buf,
               const std::vector<Xfer>& sends, void* recv_buf, const std::vector<Xfer>& recvs);
 void barrier(RankCtx& r, const std::vector<int>& members);
+
+// Peer-memory collectives (local world with peer_ok): kernels read and write
+// the other members' device buffers directly over NVLink instead of staging
+// through pack/exchange/unpack.
+bool peer_direct(const RankCtx& r);
+void set_peer_direct(bool on);  // option "peer_direct" / QTNH_PEER_DIRECT=0
+// All-gather of one device pointer per member (in member order). Stream-ordered:
+// on return my stream waits for the work every member enqueued before its call,
+// so a second call after the peer kernels acts as the completion fence.
+std::vector<void*> peer_pointers(RankCtx& r, const std::vector<int>& members, void* mine);
 
 // ---- device tensors -----------------------------------------------------------
 struct DevBuf {

@@ -475,6 +475,63 @@ void scale_conj(const void* in, void* out, Dim n, double re, double im, bool con
   QTNH_LAUNCH_CHECK();
 }
 
+struct Region {
+  int nd;
+  int64_t dims[8];
+  int64_t strides[8];
+};
+
+// One thread per element pair, 16-byte accesses; the region is pre-merged to at
+// most a few dims so the offset arithmetic stays off the critical path.
+__global__ void k_swap_regions(double2* __restrict__ a, double2* __restrict__ b, int64_t begin, int64_t end,
+                               const __grid_constant__ Region rg) {
+  for (int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < end;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i, off = 0;
+    for (int d = rg.nd - 1; d > 0; --d) {
+      int64_t c = r % rg.dims[d];
+      r /= rg.dims[d];
+      off += c * rg.strides[d];
+    }
+    off += r * rg.strides[0];
+    double2 x = a[off], y = b[off];
+    if (x.x == 0.0 && x.y == 0.0) x = make_double2(0.0, 0.0);
+    if (y.x == 0.0 && y.y == 0.0) y = make_double2(0.0, 0.0);
+    a[off] = y;
+    b[off] = x;
+  }
+}
+
+void swap_regions(void* a, void* b, const std::vector<Dim>& dims, const std::vector<Dim>& strides, Dim begin,
+                  Dim end, cudaStream_t st) {
+  if (end <= begin) return;
+  // merge row-major neighbours (outer stride == inner stride * inner dim)
+  std::vector<std::pair<Dim, Dim>> m;
+  for (size_t i = 0; i < dims.size(); ++i) {
+    if (dims[i] == 1) continue;
+    if (!m.empty() && m.back().second == strides[i] * dims[i]) {
+      m.back().first *= dims[i];
+      m.back().second = strides[i];
+    } else {
+      m.push_back({dims[i], strides[i]});
+    }
+  }
+  if (m.empty()) m.push_back({1, 1});
+  if (m.size() > 8) throw_invalid("swap region has too many non-mergeable dims");
+  Region rg{};
+  rg.nd = static_cast<int>(m.size());
+  for (int i = 0; i < rg.nd; ++i) {
+    rg.dims[i] = m[i].first;
+    rg.strides[i] = m[i].second;
+  }
+  int dev = 0;
+  QTNH_CUDA(cudaGetDevice(&dev));
+  Dim n = end - begin;
+  int grid = static_cast<int>(std::min<Dim>((n + 255) / 256, (Dim)sm_count(dev) * 8));
+  k_swap_regions<<<grid, 256, 0, st>>>(static_cast<double2*>(a), static_cast<double2*>(b), begin, end, rg);
+  QTNH_LAUNCH_CHECK();
+}
+
 void fill_zero(void* out, Dim n, cudaStream_t st) {
   if (n <= 0) return;
   int dev = 0;

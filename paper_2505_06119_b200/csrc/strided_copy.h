@@ -30,4 +30,10 @@ CopyBox permute_box(const std::vector<Dim>& dims, const std::vector<int>& perm);
 void scale_conj(const void* in, void* out, Dim n, double re, double im, bool conj, cudaStream_t st);
 void fill_zero(void* out, Dim n, cudaStream_t st);
 
+// In-place exchange of two equally shaped strided regions (elements [begin, end)
+// of the row-major enumeration of `dims`): a[off] <-> b[off], zero canonicalised.
+// a and b may live on different devices (NVLink peer pointers).
+void swap_regions(void* a, void* b, const std::vector<Dim>& dims, const std::vector<Dim>& strides, Dim begin,
+                  Dim end, cudaStream_t st);
+
 }  // namespace qtnhb

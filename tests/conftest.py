@@ -40,3 +40,15 @@ def rel_l2(a, b):
     b = np.asarray(b)
     nb = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
+
+
+@pytest.fixture(params=[1, 0], ids=["peer", "exchange"])
+def peer_mode(request):
+    """Run a multi-rank test through both redistribution forms of the local
+    world: peer-memory kernels (push remap, pairwise in-place swap) and the
+    pack -> exchange -> unpack path the NCCL world uses."""
+    from paper_2505_06119_b200.qtnh import check, lib
+
+    check(lib.qtnh_set_option(b"peer_direct", float(request.param)))
+    yield request.param
+    check(lib.qtnh_set_option(b"peer_direct", 1.0))

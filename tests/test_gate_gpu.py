@@ -210,7 +210,7 @@ def test_blocked_qft(n, split, world):
     ([3, 3, 2, 3, 2], 1, 0, 3, 3, 96),    # dim-3 indices: two partners per rank
     ([2] * 10, 3, 2, 3, 8, 1 << 30),      # local index right after the split
 ])
-def test_inplace_distributed_swap(dims, split, a, b, world, chunk):
+def test_inplace_distributed_swap(dims, split, a, b, world, chunk, peer_mode):
     """Distributed <-> local index swap done in place through a bounded staging
     buffer: bit-exact against ops::permute semantics."""
     from conftest import bits

@@ -85,6 +85,36 @@ def simulate(dims, split, dist, perm, new_split, new_dist, world, g):
     return glob
 
 
+def simulate_push(dims, split, dist, perm, new_split, new_dist, world, g):
+    """Peer-memory form: every canonical source holder stores its chunks straight
+    into the homes' destination blocks."""
+    total = int(np.prod(dims))
+    snd = int(np.prod(dims[:split]))
+    nl_src = total // snd
+    ndims = [dims[p] for p in perm]
+    dnd = int(np.prod(ndims[:new_split]))
+    nl_dst = total // dnd
+    dst = {r: np.full(nl_dst, np.nan + 0j) for r in range(world) if locate(r, dnd, new_dist)}
+    for r in range(world):
+        p = plan(dims, split, dist, perm, new_split, new_dist, r, world)
+        if not p["member"]:
+            continue
+        loc = locate(r, snd, dist)
+        src = g[loc[0] * nl_src:(loc[0] + 1) * nl_src] if loc else None
+        if p["local_only"]:  # same single-launch path as the exchange form
+            if p["src_canonical"] and r in dst:
+                strided_copy(src, dst[r], p["pack"], True)
+            continue
+        for peer, so, do in p["pushes"]:
+            box = p["push_box"]
+            strided_copy(src[so:], dst[peer][do:], box, True)
+    glob = np.full(dnd * nl_dst, np.nan + 0j)
+    for r, d in dst.items():
+        b = locate(r, dnd, new_dist)[0]
+        glob[b * nl_dst:(b + 1) * nl_dst] = d
+    return glob
+
+
 def test_random_plans_bit_exact():
     import oracle
 
@@ -125,5 +155,7 @@ def test_random_plans_bit_exact():
         got = simulate(dims, split, (st, cy, off), perm, new_split, (nst, ncy, noff), world, g)
         want = P.permute(dims, g, perm)
         assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (dims, split, perm, new_split, world)
+        got = simulate_push(dims, split, (st, cy, off), perm, new_split, (nst, ncy, noff), world, g)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), ("push", dims, split, perm, world)
         checked += 1
     assert checked > 150 and raised > 10

@@ -49,7 +49,7 @@ def test_matrix_transpose():
     assert np.array_equal(run_collect(World(1), body), np.array([1, 3, 2, 4], complex))
 
 
-def test_asymmetric_permutation_recruits_more_ranks():
+def test_asymmetric_permutation_recruits_more_ranks(peer_mode):
     g = iota_global(32)
 
     def body(rk):
@@ -72,7 +72,7 @@ def test_asymmetric_permutation_recruits_more_ranks():
     assert e.value.required_ranks == 4
 
 
-def test_golden_permutations_bit_exact():
+def test_golden_permutations_bit_exact(peer_mode):
     meta, z = golden("permute")
     for i, m in enumerate(meta):
         gin = z[f"in{i}"]
@@ -88,7 +88,7 @@ def test_golden_permutations_bit_exact():
         assert np.array_equal(bits(got), bits(z[f"out{i}"])), f"case {i}: {m}"
 
 
-def test_permutation_round_trip_and_composition():
+def test_permutation_round_trip_and_composition(peer_mode):
     # test_ops.cpp:112-159
     for seed in range(8):
         def body(rk, seed=seed):
@@ -138,7 +138,7 @@ def test_permutation_round_trip_and_composition():
         World(4).run(body)
 
 
-def test_rebcast_changes_the_pattern_and_keeps_values():
+def test_rebcast_changes_the_pattern_and_keeps_values(peer_mode):
     # test_ops.cpp:161-192
     g = iota_global(4)
     meta, z = golden("rebcast")
@@ -169,7 +169,7 @@ def test_rebcast_changes_the_pattern_and_keeps_values():
     World(4).run(body)
 
 
-def test_scatter_and_gather_indices():
+def test_scatter_and_gather_indices(peer_mode):
     # test_ops.cpp:218-248
     g = iota_global(4)
 
@@ -285,7 +285,7 @@ def test_general_dims_permutation(dims, perm):
 
 
 @pytest.mark.parametrize("world,split,new_split", [(8, 3, 3), (8, 3, 2), (4, 2, 3), (8, 3, 0)])
-def test_distributed_swaps_bit_exact(world, split, new_split):
+def test_distributed_swaps_bit_exact(world, split, new_split, peer_mode):
     n = 18
     g = circuits.counter_state(5, 2**n)
     perm = circuits.fisher_yates(5 + world + new_split, 10, n)
