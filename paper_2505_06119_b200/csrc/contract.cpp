@@ -299,8 +299,10 @@ void op_gate_apply(TP& t, const std::vector<int>& targets, const double* gate, b
   for (int i = 0; i < k; ++i) {
     int q = targets[i];
     if (q >= s.split) continue;
+    // outermost free local index: the moving and staying regions are then
+    // contiguous halves of the block (coalesced peer swap)
     int w = -1;
-    for (int p = s.n_idx() - 1; p >= s.split; --p)
+    for (int p = s.split; p < s.n_idx(); ++p)
       if (!is_t[p] && !used[p] && s.dims[p] == s.dims[q]) {
         w = p;
         break;

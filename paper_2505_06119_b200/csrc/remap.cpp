@@ -424,40 +424,28 @@ void op_swap_dist_local_inplace(TP& t, int a, int b, Dim chunk_bytes) {
     // Peer-memory form: each pair of partner blocks exchanges its two regions
     // with one swap kernel over NVLink, no staging; the lower coordinate swaps
     // the first half of the pair's elements, the higher one the second half.
+    // For d = 2 the same launch canonicalises both staying regions.
     Dim region_n = 1;
     for (Dim x : rdims) region_n *= x;
-    {
-      CopyBox keep;
-      keep.dims = rdims;
-      keep.in_stride = rstr;
-      keep.out_stride = rstr;
-      char* base = static_cast<char*>(t->data()) + my_i * ls[lb] * 16;
-      strided_copy(base, base, keep, true, r.stream);
-    }
+    char* keep = static_cast<char*>(t->data()) + my_i * ls[lb] * 16;
+    if (d != 2) canon_region(keep, rdims, rstr, r.stream);
     auto ptrs = peer_pointers(r, members, t->data());
     for (Dim j = 0; j < d; ++j) {
       if (j == my_i) continue;
       auto pc = cd;
       pc[a] = j;
       int peer = t->dist.home(flat(pc, ddims), nd, t->cycle, t->slot);
-      void* pb = ptrs[peer - members.front()];
+      char* pb = static_cast<char*>(ptrs[peer - members.front()]);
       Dim half = region_n / 2;
       Dim lo = my_i < j ? 0 : half, hi = my_i < j ? half : region_n;
-      swap_regions(static_cast<char*>(t->data()) + j * ls[lb] * 16, static_cast<char*>(pb) + my_i * ls[lb] * 16,
-                   rdims, rstr, lo, hi, r.stream);
+      swap_regions(static_cast<char*>(t->data()) + j * ls[lb] * 16, pb + my_i * ls[lb] * 16, rdims, rstr, lo, hi,
+                   r.stream, d == 2 ? keep : nullptr, d == 2 ? pb + j * ls[lb] * 16 : nullptr);
     }
     peer_pointers(r, members, nullptr);
     return;
   }
-  // canonicalise the region that stays (b = my_i): in place, element by element
-  {
-    CopyBox keep;
-    keep.dims = rdims;
-    keep.in_stride = rstr;
-    keep.out_stride = rstr;
-    char* base = static_cast<char*>(t->data()) + my_i * ls[lb] * 16;
-    strided_copy(base, base, keep, true, r.stream);
-  }
+  // canonicalise the region that stays (b = my_i) in place
+  canon_region(static_cast<char*>(t->data()) + my_i * ls[lb] * 16, rdims, rstr, r.stream);
   for (Dim ch = 0; ch < n_chunks; ++ch) {
     auto oc = unflat(ch, odims);
     Dim obase = 0;

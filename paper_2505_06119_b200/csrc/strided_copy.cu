@@ -481,30 +481,49 @@ struct Region {
   int64_t strides[8];
 };
 
+__device__ __forceinline__ int64_t region_offset(int64_t i, const Region& rg) {
+  int64_t off = 0;
+  for (int d = rg.nd - 1; d > 0; --d) {
+    int64_t c = i % rg.dims[d];
+    i /= rg.dims[d];
+    off += c * rg.strides[d];
+  }
+  return off + i * rg.strides[0];
+}
+
+// Zero canonicalisation in place: a write only where a zero is not +0 + 0i, so
+// the pass costs a read of the region.
+__device__ __forceinline__ void canon_in_place(double2* p) {
+  double2 v = *p;
+  if (v.x == 0.0 && v.y == 0.0 && (__double_as_longlong(v.x) | __double_as_longlong(v.y)) != 0)
+    *p = make_double2(0.0, 0.0);
+}
+
 // One thread per element pair, 16-byte accesses; the region is pre-merged to at
-// most a few dims so the offset arithmetic stays off the critical path.
-__global__ void k_swap_regions(double2* __restrict__ a, double2* __restrict__ b, int64_t begin, int64_t end,
-                               const __grid_constant__ Region rg) {
+// most a few dims so the offset arithmetic stays off the critical path. With
+// keep_a/keep_b set, the elements at the same region offset in the two staying
+// regions are canonicalised in the same pass.
+__global__ void k_swap_regions(double2* __restrict__ a, double2* __restrict__ b, double2* keep_a, double2* keep_b,
+                               int64_t begin, int64_t end, const __grid_constant__ Region rg) {
   for (int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < end;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i, off = 0;
-    for (int d = rg.nd - 1; d > 0; --d) {
-      int64_t c = r % rg.dims[d];
-      r /= rg.dims[d];
-      off += c * rg.strides[d];
-    }
-    off += r * rg.strides[0];
+    int64_t off = region_offset(i, rg);
     double2 x = a[off], y = b[off];
     if (x.x == 0.0 && x.y == 0.0) x = make_double2(0.0, 0.0);
     if (y.x == 0.0 && y.y == 0.0) y = make_double2(0.0, 0.0);
     a[off] = y;
     b[off] = x;
+    if (keep_a) canon_in_place(keep_a + off);
+    if (keep_b) canon_in_place(keep_b + off);
   }
 }
 
-void swap_regions(void* a, void* b, const std::vector<Dim>& dims, const std::vector<Dim>& strides, Dim begin,
-                  Dim end, cudaStream_t st) {
-  if (end <= begin) return;
+__global__ void k_canon_region(double2* __restrict__ p, int64_t n, const __grid_constant__ Region rg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    canon_in_place(p + region_offset(i, rg));
+}
+
+Region merged_region(const std::vector<Dim>& dims, const std::vector<Dim>& strides) {
   // merge row-major neighbours (outer stride == inner stride * inner dim)
   std::vector<std::pair<Dim, Dim>> m;
   for (size_t i = 0; i < dims.size(); ++i) {
@@ -524,11 +543,31 @@ void swap_regions(void* a, void* b, const std::vector<Dim>& dims, const std::vec
     rg.dims[i] = m[i].first;
     rg.strides[i] = m[i].second;
   }
+  return rg;
+}
+
+void swap_regions(void* a, void* b, const std::vector<Dim>& dims, const std::vector<Dim>& strides, Dim begin,
+                  Dim end, cudaStream_t st, void* keep_a, void* keep_b) {
+  if (end <= begin) return;
+  Region rg = merged_region(dims, strides);
   int dev = 0;
   QTNH_CUDA(cudaGetDevice(&dev));
   Dim n = end - begin;
   int grid = static_cast<int>(std::min<Dim>((n + 255) / 256, (Dim)sm_count(dev) * 8));
-  k_swap_regions<<<grid, 256, 0, st>>>(static_cast<double2*>(a), static_cast<double2*>(b), begin, end, rg);
+  k_swap_regions<<<grid, 256, 0, st>>>(static_cast<double2*>(a), static_cast<double2*>(b),
+                                       static_cast<double2*>(keep_a), static_cast<double2*>(keep_b), begin, end, rg);
+  QTNH_LAUNCH_CHECK();
+}
+
+void canon_region(void* p, const std::vector<Dim>& dims, const std::vector<Dim>& strides, cudaStream_t st) {
+  Dim n = 1;
+  for (Dim d : dims) n *= d;
+  if (n <= 0) return;
+  Region rg = merged_region(dims, strides);
+  int dev = 0;
+  QTNH_CUDA(cudaGetDevice(&dev));
+  int grid = static_cast<int>(std::min<Dim>((n + 255) / 256, (Dim)sm_count(dev) * 8));
+  k_canon_region<<<grid, 256, 0, st>>>(static_cast<double2*>(p), n, rg);
   QTNH_LAUNCH_CHECK();
 }
 

@@ -32,8 +32,11 @@ void fill_zero(void* out, Dim n, cudaStream_t st);
 
 // In-place exchange of two equally shaped strided regions (elements [begin, end)
 // of the row-major enumeration of `dims`): a[off] <-> b[off], zero canonicalised.
-// a and b may live on different devices (NVLink peer pointers).
+// a and b may live on different devices (NVLink peer pointers). keep_a / keep_b
+// (optional) are canonicalised in place at the same offsets.
 void swap_regions(void* a, void* b, const std::vector<Dim>& dims, const std::vector<Dim>& strides, Dim begin,
-                  Dim end, cudaStream_t st);
+                  Dim end, cudaStream_t st, void* keep_a = nullptr, void* keep_b = nullptr);
+// Zero canonicalisation of a strided region in place (writes only non-canonical zeros).
+void canon_region(void* p, const std::vector<Dim>& dims, const std::vector<Dim>& strides, cudaStream_t st);
 
 }  // namespace qtnhb

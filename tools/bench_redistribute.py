@@ -25,25 +25,29 @@ def body(rk):
     st = torch.cuda.Stream()
     rk.set_stream(st.cuda_stream)
     t = Tensor.dense(rk, IndexTuple([2] * n, k), DistParams(1, 1, 0), None)
-    perm = list(range(n))
-    perm[0], perm[n - 1] = perm[n - 1], perm[0]
+    perms = {}
+    for lb in (n - 1, k):
+        perm = list(range(n))
+        perm[0], perm[lb] = perm[lb], perm[0]
+        perms[lb] = perm
     for mode in (1, 0):
-        if rk.id == 0:
+        if rk.rank() == 0:
             check(lib.qtnh_set_option(b"peer_direct", float(mode)))
         rk.barrier()
-        for op in ("swap", "permute"):
+        for op in ("swap", "permute", "swap_outer", "permute_outer"):
             for rep in range(4):
                 rk.barrier()
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(st)
-                if op == "swap":
-                    qtnh.swap_indices(t, 0, n - 1)
+                lb = k if op.endswith("outer") else n - 1
+                if op.startswith("swap"):
+                    qtnh.swap_indices(t, 0, lb)
                 else:
-                    u = qtnh.ops.permute(t, perm, k)
+                    u = qtnh.ops.permute(t, perms[lb], k)
                 e1.record(st)
                 e1.synchronize()
-                if op == "permute":
+                if op.startswith("permute"):
                     u.free()
                 ms = e0.elapsed_time(e1)
                 if rep == 3:
@@ -56,6 +60,6 @@ World(w).run(body)
 tot = 16 * 2**n
 for (mode, op), v in sorted(res.items()):
     ms = max(v)
-    moved = tot if op == "permute" else tot * (1 - 1 / 2)  # swap touches the half that moves
-    print(f"{'peer' if mode else 'exchange':8s} {op:8s} n={n} world={w}: {ms:8.3f} ms  "
+    moved = tot if op.startswith("permute") else tot * (1 - 1 / 2)  # swap moves half the state
+    print(f"{'peer' if mode else 'exchange':8s} {op:14s} n={n} world={w}: {ms:8.3f} ms  "
           f"(algorithmic r+w {2 * moved / ms / 1e6:7.1f} GB/s on one device)")
