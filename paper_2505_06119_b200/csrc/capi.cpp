@@ -94,6 +94,7 @@ int qtnh_world_create_local(int n, const int* devices, qtnh_world_t* out) {
     w->size = n;
     w->timeout_ms = env_timeout();
     for (int i = 0; i < n; ++i) w->devices.push_back(devices ? devices[i] : 0);
+    for (int d : w->devices) keep_pool(d);
     // Peer access between distinct devices (NVLink) for the exchange copies and
     // the peer-memory kernels (remap push, in-place swaps).
     w->peer_ok = true;
@@ -147,6 +148,7 @@ int qtnh_world_create_nccl(int rank, int size, int device, const void* uid128, q
     w->my_rank = rank;
     w->timeout_ms = env_timeout();
     QTNH_CUDA(cudaSetDevice(device));
+    keep_pool(device);
     ncclUniqueId id;
     std::memcpy(&id, uid128, sizeof(id));
     ncclComm_t comm;
@@ -174,7 +176,11 @@ int qtnh_world_destroy(qtnh_world_t w) {
       nccl().CommDestroy(static_cast<ncclComm_t>(w->w->nccl_comm));
       cudaStreamDestroy(w->w->nccl_rank->own_stream);
     }
+    std::vector<int> devs = w->w->kind == World::kNccl ? std::vector<int>{w->w->nccl_rank->device} : w->w->devices;
     delete w;
+    std::sort(devs.begin(), devs.end());
+    devs.erase(std::unique(devs.begin(), devs.end()), devs.end());
+    for (int d : devs) trim_pool(d);
   });
 }
 

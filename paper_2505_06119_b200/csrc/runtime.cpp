@@ -13,6 +13,44 @@ std::atomic<int64_t> g_kernel_launches{0};
 
 void RankCtx::activate() const { QTNH_CUDA(cudaSetDevice(device)); }
 
+// Tensors come from the device's stream-ordered pool. The default release
+// threshold (0) hands freed pages back to the driver at every synchronisation,
+// so the next same-sized tensor pays a fresh mapping; a world keeps its pool
+// warm for its lifetime and trims it when destroyed.
+namespace {
+std::mutex g_pool_mu;
+std::map<int, int> g_pool_users;  // live worlds per device
+}  // namespace
+
+void keep_pool(int device) {
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (g_pool_users[device]++ > 0) return;
+  }
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  uint64_t keep = UINT64_MAX;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+}
+
+void trim_pool(int device) {
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (--g_pool_users[device] > 0) return;
+  }
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  uint64_t zero = 0;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &zero);
+  cudaMemPoolTrimTo(pool, 0);
+}
+
 DevBuf::DevBuf(size_t b, const RankCtx& r) : bytes(b), device(r.device), stream(r.stream) {
   if (b == 0) b = 16;
   QTNH_CUDA(cudaMallocAsync(&ptr, b, stream));

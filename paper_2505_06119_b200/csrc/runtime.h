@@ -92,6 +92,8 @@ void set_peer_direct(bool on);  // option "peer_direct" / QTNH_PEER_DIRECT=0
 std::vector<void*> peer_pointers(RankCtx& r, const std::vector<int>& members, void* mine);
 
 // ---- device tensors -----------------------------------------------------------
+void keep_pool(int device);  // stream-ordered pool keeps freed blocks (world lifetime)
+void trim_pool(int device);  // return unused pool memory to the driver
 struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
