@@ -401,6 +401,13 @@ void op_qft(TP& t, bool swaps) {
     if (t->in_span) bitrev_local(t->data(), nb, t->rank->stream);
     return;
   }
+  if (t->shape.split == split && 2 * split <= n) {
+    // distributed qubit j <-> local qubit n-1-j (the k innermost), then one
+    // in-place pass reversing the middle qubits [k, n-k) = the top n-2k local bits
+    for (int j = 0; j < split; ++j) op_swap_indices(t, j, n - 1 - j);
+    if (t->in_span) bitrev_hi_local(t->data(), n - 2 * split, split, t->rank->stream);
+    return;
+  }
   for (int j = 0; j < n / 2; ++j) op_swap_indices(t, j, n - 1 - j);
 }
 

@@ -544,7 +544,57 @@ __global__ void __launch_bounds__(256) k_bitrev(double2* __restrict__ psi, int n
   }
 }
 
+// Bit reversal of the top nh bits of the local index with the low k bits held
+// (the distributed QFT's final swaps once its k distributed qubits have been
+// exchanged with the k innermost local ones): element (hi, lo) <- (rev hi, lo).
+// Tiles of 2^B x 2^B "rows" of 2^k contiguous amplitudes (2^(2B+k) <= 2048) are
+// exchanged between hi = (a, m, b) and (rev b, rev m, rev a) through shared memory.
+__global__ void __launch_bounds__(256) k_bitrev_hi(double2* __restrict__ psi, int nh, int k, int B, int64_t n_mid) {
+  extern __shared__ double2 smb[];
+  const int R = 1 << B, RE = R << k, row = RE + 1;
+  double2* t1 = smb;
+  double2* t2 = smb + R * row;
+  const int mbits = nh - 2 * B;
+  const int tile = R * RE;
+  auto base = [&](int a, int64_t m) { return ((int64_t(a) << (nh - B)) | (m << B)) << k; };
+  for (int64_t m = blockIdx.x; m < n_mid; m += gridDim.x) {
+    int64_t mr = mbits > 0 ? static_cast<int64_t>(rev_bits64(static_cast<uint64_t>(m), mbits)) : m;
+    if (mr < m) continue;
+    __syncthreads();
+    for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+      int a = e / RE, rest = e - a * RE;
+      t1[a * row + rest] = psi[base(a, m) + rest];
+      t2[a * row + rest] = psi[base(a, mr) + rest];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+      int a = e / RE, rest = e - a * RE;
+      int b = rest >> k, lo = rest & ((1 << k) - 1);
+      int ra = B ? rev_bits(a, B) : 0, rb = B ? rev_bits(b, B) : 0;
+      int src = rb * row + ((ra << k) | lo);
+      psi[base(a, m) + rest] = canon2(t2[src]);
+      if (mr != m) psi[base(a, mr) + rest] = canon2(t1[src]);
+    }
+  }
+}
+
 }  // namespace
+
+void bitrev_hi_local(void* data, int nh, int k, cudaStream_t st) {
+  if (nh <= 1) return;
+  int B = std::min((11 - k) / 2, nh / 2);
+  if (B < 1) throw_invalid("bit reversal: too many held low bits");
+  int64_t n_mid = int64_t(1) << (nh - 2 * B);
+  size_t smem = size_t(2) * (size_t(1) << B) * ((size_t(1) << (B + k)) + 1) * sizeof(double2);
+  static bool attr = [] {
+    cudaFuncSetAttribute(k_bitrev_hi, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    return true;
+  }();
+  (void)attr;
+  int grid = static_cast<int>(std::min<int64_t>(n_mid, 148 * 8));
+  k_bitrev_hi<<<grid, 256, smem, st>>>(static_cast<double2*>(data), nh, k, B, n_mid);
+  QTNH_LAUNCH_CHECK();
+}
 
 int qft_group_max() {
   static int v = [] {

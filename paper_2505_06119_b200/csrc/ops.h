@@ -92,6 +92,8 @@ void qft_phase_local(void* data, int local_bits, int64_t v_off, int t, cudaStrea
 // in register groups of 5); in-place bit reversal (the final SWAP network).
 void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st);
 void bitrev_local(void* data, int nb, cudaStream_t st);
+// Reverse the top nh bits of the local index, holding the low k bits.
+void bitrev_hi_local(void* data, int nh, int k, cudaStream_t st);
 // In-place exchange of two equal-size local indices.
 void swap_indices_local(void* data, const std::vector<Dim>& dims, int ia, int ib, cudaStream_t st);
 // Gate on a dense local block: dims = local dims, targets = local positions.
