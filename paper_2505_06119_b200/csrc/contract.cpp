@@ -290,6 +290,42 @@ void op_gate_apply(TP& t, const std::vector<int>& targets, const double* gate, b
     gate_local(t->data(), s.local_dims(), lt, sub.data(), true, r.stream);
     return;
   }
+  if (dist_t.size() == 1 && s.dims[dist_t[0]] == 2 && peer_direct(r)) {
+    // Gate fused with the exchange over peer memory: the two ranks whose blocks
+    // differ only in the distributed target's bit see the pair as one virtual
+    // tensor [2][local...] whose leading stride is the distance between their
+    // buffers; each applies the gate to half of the fibers, loading and storing
+    // the partner's amplitudes in place over NVLink. One pass instead of
+    // swap -> apply -> swap back.
+    auto members = span_ranks(*t);
+    if (!t->in_span) return;
+    const int q = dist_t[0];
+    auto ddims = s.dist_dims();
+    auto cd = unflat(t->block, ddims);
+    const Dim nd = s.dist_size();
+    auto ptrs = peer_pointers(r, members, t->data());
+    char* grp[2];
+    for (Dim j = 0; j < 2; ++j) {
+      auto pc = cd;
+      pc[q] = j;
+      grp[j] = static_cast<char*>(ptrs[t->dist.home(flat(pc, ddims), nd, t->cycle, t->slot) - members.front()]);
+    }
+    auto ld = s.local_dims();
+    std::vector<Dim> vdims{2}, vstr{(grp[1] - grp[0]) / 16};
+    auto ls = row_major_strides(ld);
+    vdims.insert(vdims.end(), ld.begin(), ld.end());
+    vstr.insert(vstr.end(), ls.begin(), ls.end());
+    std::vector<int> vt;
+    Dim D = 1;
+    for (int x : targets) {
+      vt.push_back(x < s.split ? 0 : x - s.split + 1);
+      D *= s.dims[x];
+    }
+    const Dim n_fib = 2 * s.local_size() / D, half = n_fib / 2;
+    gate_strided(grp[0], vdims, vstr, vt, gate, false, r.stream, cd[q] == 0 ? 0 : half, cd[q] == 0 ? half : n_fib);
+    peer_pointers(r, members, nullptr);
+    return;
+  }
   // Dense gate on distributed targets: swap each with a local non-target index of
   // the same size (dist<->local swap over NVLink), apply, swap back.
   std::vector<int> perm(s.n_idx());

@@ -34,6 +34,7 @@ struct GateArgs {
   int64_t off[kMaxD * 4];      // element offsets of the D (or listed diagonal) entries
   double2 g[kMaxD * kMaxD];    // row-major gate, or diagonal values
   int nd;                      // diagonal: number of listed entries
+  int64_t f0;                  // first fiber of this launch
 };
 
 template <bool POW2>
@@ -59,7 +60,7 @@ __global__ void __launch_bounds__(256) k_gate_dense(double2* __restrict__ psi, i
                                                     const __grid_constant__ GateArgs a) {
   for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < n_fibers;
        f += (int64_t)gridDim.x * blockDim.x) {
-    int64_t base = fiber_base<POW2>(f, a);
+    int64_t base = fiber_base<POW2>(f + a.f0, a);
     double2 x[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) x[d] = psi[base + a.off[d]];
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(256) k_gate_generic(double2* __restrict__ psi,
                                                       const __grid_constant__ GateArgs a) {
   for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < n_fibers;
        f += (int64_t)gridDim.x * blockDim.x) {
-    int64_t base = fiber_base<POW2>(f, a);
+    int64_t base = fiber_base<POW2>(f + a.f0, a);
     double2 x[kMaxD];
     for (int d = 0; d < a.D; ++d) x[d] = psi[base + a.off[d]];
     for (int i = 0; i < a.D; ++i) {
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(256) k_gate_diag(double2* __restrict__ psi, in
                                                    const __grid_constant__ GateArgs a) {
   for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < n_fibers;
        f += (int64_t)gridDim.x * blockDim.x) {
-    int64_t base = fiber_base<POW2>(f, a);
+    int64_t base = fiber_base<POW2>(f + a.f0, a);
     for (int j = 0; j < a.nd; ++j) {
       double2 v = psi[base + a.off[j]];
       double2 g = a.g[j];
@@ -131,6 +132,12 @@ int grid_for(int64_t work) {
 
 void gate_local(void* data, const std::vector<Dim>& dims, const std::vector<int>& targets,
                 const double* gh, bool diagonal, cudaStream_t st) {
+  gate_strided(data, dims, row_major_strides(dims), targets, gh, diagonal, st, 0, -1);
+}
+
+void gate_strided(void* data, const std::vector<Dim>& dims, const std::vector<Dim>& strides,
+                  const std::vector<int>& targets, const double* gh, bool diagonal, cudaStream_t st, Dim f_begin,
+                  Dim f_end) {
   int r = static_cast<int>(dims.size());
   int k = static_cast<int>(targets.size());
   if (k == 0) throw_invalid("gate needs at least one target");
@@ -139,7 +146,6 @@ void gate_local(void* data, const std::vector<Dim>& dims, const std::vector<int>
     if (t < 0 || t >= r || is_t[t]) throw_invalid("invalid gate targets");
     is_t[t] = 1;
   }
-  auto strides = row_major_strides(dims);
   GateArgs a{};
   Dim D = 1;
   for (int t : targets) D *= dims[t];
@@ -147,6 +153,10 @@ void gate_local(void* data, const std::vector<Dim>& dims, const std::vector<int>
   for (Dim d : dims) total *= d;
   if (total == 0) return;
   Dim n_fibers = total / D;
+  if (f_end < 0 || f_end > n_fibers) f_end = n_fibers;
+  if (f_begin >= f_end) return;
+  a.f0 = f_begin;
+  n_fibers = f_end - f_begin;
   // segments of consecutive non-target positions
   std::vector<std::pair<Dim, Dim>> segs;  // (size, stride of innermost position)
   for (int i = 0; i < r;) {
@@ -272,7 +282,7 @@ __global__ void __launch_bounds__(256) k_swap_indices(double2* __restrict__ psi,
                                                       int64_t sa, int64_t sb, const __grid_constant__ GateArgs a) {
   for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < n_fibers;
        f += (int64_t)gridDim.x * blockDim.x) {
-    int64_t base = fiber_base<POW2>(f, a);
+    int64_t base = fiber_base<POW2>(f + a.f0, a);
     for (int i = 0; i < d; ++i) {
       int64_t oii = base + i * sa + i * sb;
       double2 v = psi[oii];

@@ -99,5 +99,10 @@ void swap_indices_local(void* data, const std::vector<Dim>& dims, int ia, int ib
 // Gate on a dense local block: dims = local dims, targets = local positions.
 void gate_local(void* data, const std::vector<Dim>& dims, const std::vector<int>& targets,
                 const double* gate_host, bool diagonal, cudaStream_t st);
+// gate_local over explicit element strides, fibers [f_begin, f_end) only
+// (f_end < 0: all); strides may span buffers (peer pointers).
+void gate_strided(void* data, const std::vector<Dim>& dims, const std::vector<Dim>& strides,
+                  const std::vector<int>& targets, const double* gh, bool diagonal, cudaStream_t st, Dim f_begin,
+                  Dim f_end);
 
 }  // namespace qtnhb

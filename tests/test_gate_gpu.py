@@ -61,6 +61,34 @@ def test_dense_gates_general(dims, targets, D):
     assert rel_l2(run_collect(World(1), body), P.gate(dims, g, targets, gate)) < 1e-14
 
 
+@pytest.mark.parametrize("dims,split,dist,targets,world", [
+    ([2] * 12, 1, (1, 1, 0), [0], 2),             # single distributed qubit
+    ([2] * 12, 3, (1, 1, 0), [1], 8),
+    ([2] * 12, 3, (1, 1, 0), [2, 7], 8),          # one distributed + one local target
+    ([2] * 12, 2, (1, 1, 0), [9, 0, 4], 4),       # distributed target in the middle of the list
+    ([2] * 12, 2, (1, 1, 0), [0, 1], 4),          # both distributed: swap path
+    ([2] * 11, 1, (2, 1, 1), [0, 5], 6),          # stretched copies, offset
+    ([2] * 11, 2, (1, 2, 0), [1], 8),             # cyclic copies
+    ([3, 2, 4, 2], 2, (1, 1, 0), [1, 2], 6),      # non-qubit local dims
+])
+def test_dense_gates_on_distributed_targets(dims, split, dist, targets, world, peer_mode):
+    """Dense gates with distributed targets: fused peer-memory gate (one
+    distributed qubit target) or swap -> apply -> swap back, against the oracle."""
+    g = circuits.counter_state(41, int(np.prod(dims)))
+    D = int(np.prod([dims[q] for q in targets]))
+    gate = circuits.rng_normals(42, D * D)
+
+    def body(rk):
+        t = Tensor.from_global(rk, IndexTuple(dims, split), DistParams(*dist), g)
+        apply_gate(t, targets, gate)
+        return t.to_global_vector()
+
+    outs = [o for o in World(world).run(body) if o.size]
+    want = P.gate(dims, g, targets, gate)
+    for o in outs:
+        assert rel_l2(o, want) < 1e-14
+
+
 def test_diagonal_gates_on_distributed_targets():
     n = 12
     g = circuits.counter_state(8, 2**n)
