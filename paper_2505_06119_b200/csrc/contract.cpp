@@ -430,9 +430,37 @@ void op_qft(TP& t, bool swaps) {
     if (d != 2) throw_invalid("qft needs a qubit tensor (all dims 2)");
   int nb = n - split;
   if (nb > 62) throw_invalid("too many local qubits");
-  for (int j = 0; j < split; ++j) op_qft_layer(t, j);  // distributed targets
-  if (t->in_span && nb > 0) qft_local_fused(t->data(), nb, nb - 1, t->rank->stream);
+  RankCtx& r = *t->rank;
+  // Peer-memory form: the layers of all distributed qubits in one pass, and the
+  // distributed half of the bit reversal in another (see gate.cu).
+  const bool fused = split >= 1 && split <= 4 && nb >= split && peer_direct(r);
+  std::vector<void*> grp;
+  Dim my_x = 0;
+  if (fused && t->in_span) {
+    auto members = span_ranks(*t);
+    auto ptrs = peer_pointers(r, members, t->data());
+    const Dim X = Dim(1) << split;
+    for (Dim x = 0; x < X; ++x)
+      grp.push_back(ptrs[t->dist.home(x, X, t->cycle, t->slot) - members.front()]);
+    my_x = t->block;
+    const Dim L = t->shape.local_size();
+    qft_dist_layers(grp.data(), split, nb, my_x * L / X, (my_x + 1) * L / X, r.stream);
+    peer_pointers(r, members, nullptr);
+  } else if (!fused) {
+    for (int j = 0; j < split; ++j) op_qft_layer(t, j);  // distributed targets
+  }
+  if (t->in_span && nb > 0) qft_local_fused(t->data(), nb, nb - 1, r.stream);
   if (!swaps) return;
+  if (fused) {
+    if (!t->in_span) return;
+    auto members = span_ranks(*t);
+    peer_pointers(r, members, t->data());  // the local layers of every member are done
+    const Dim X = Dim(1) << split, M = t->shape.local_size() >> split;
+    dist_bitrev(grp.data(), split, my_x * M / X, (my_x + 1) * M / X, r.stream);
+    peer_pointers(r, members, nullptr);
+    bitrev_hi_local(t->data(), n - 2 * split, split, r.stream);
+    return;
+  }
   if (t->shape.split == 0 && nb >= 10) {
     if (t->in_span) bitrev_local(t->data(), nb, t->rank->stream);
     return;

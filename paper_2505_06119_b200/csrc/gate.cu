@@ -588,7 +588,134 @@ __global__ void __launch_bounds__(256) k_bitrev_hi(double2* __restrict__ psi, in
   }
 }
 
+// ---- distributed QFT over peer memory ---------------------------------------------------
+// The 2^K ranks of a copy group hold the blocks x = 0 .. 2^K-1 of a state whose K
+// leading qubits are distributed. Each rank takes a slice of the local indices
+// and, for every local index i in it, loads the 2^K amplitudes (x, i) from all
+// group members (peer loads over NVLink), applies the QFT layers of the K
+// distributed qubits in registers and stores them back: the layers' H and
+// controlled phases fused with the exchange, one pass over the state.
+// Layer j (qubit j = bit K-1-j of x, bit position t = nb + K-1-j of the index):
+//   y0 = (a0 + a1)/sqrt2, y1 = (a0 - a1)/sqrt2 * exp(i pi v / 2^t),
+//   v / 2^t = (x mod 2^b)/2^b + i / 2^(nb+b),  b = K-1-j;
+// the i-dependent factor is w^(2^(K-1-b)) with w = exp(i pi i / 2^(nb+K-1)).
+struct PeerGroup {
+  double2* p[16];
+};
+
+template <int K>
+__global__ void __launch_bounds__(256) k_qft_dist_layers(const __grid_constant__ PeerGroup g, int nb, int64_t i0,
+                                                         int64_t i1) {
+  constexpr int X = 1 << K;
+  const double r = 0.70710678118654752440;
+  for (int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < i1;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double2 a[X];
+#pragma unroll
+    for (int x = 0; x < X; ++x) a[x] = g.p[x][i];
+    double2 w[K];  // w[b] = exp(i pi i / 2^(nb+b))
+    {
+      double sn, cs;
+      sincospi(static_cast<double>(i) * ldexp(1.0, -(nb + K - 1)), &sn, &cs);
+      w[K - 1] = make_double2(cs, sn);
+#pragma unroll
+      for (int b = K - 1; b > 0; --b) w[b - 1] = cmul2(w[b], w[b]);
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int b = K - 1 - j;
+#pragma unroll
+      for (int x = 0; x < X; ++x) {
+        if (x & (1 << b)) continue;
+        const int x1 = x | (1 << b);
+        double2 a0 = a[x], a1 = a[x1];
+        a[x] = make_double2(r * a0.x + r * a1.x, r * a0.y + r * a1.y);
+        double2 d = make_double2(r * a0.x - r * a1.x, r * a0.y - r * a1.y);
+        double2 ph = w[b];
+        const int xl = x & ((1 << b) - 1);
+        if (xl) ph = cmul2(ph, kQftSmallTw[(1 << b) - 1 + xl]);  // e^{i pi xl / 2^b}
+        a[x1] = cmul2(d, ph);
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < X; ++x) g.p[x][i] = a[x];
+  }
+}
+
+// Final bit reversal, distributed part: with the local index i = (mid, l), l its
+// K low bits, element (x, mid, l) moves to (rev l, mid, rev x) -- the K
+// distributed qubits trade places with the K innermost local ones, each group
+// reversed. For one mid the 2^K x 2^K elements form a closed set, so a CTA loads
+// MB mids from all members (runs of MB * 2^K contiguous amplitudes per member),
+// and stores them transposed; mids are split over the group. The middle qubits
+// are reversed afterwards by k_bitrev_hi on every rank.
+template <int K>
+__global__ void __launch_bounds__(256) k_dist_bitrev(const __grid_constant__ PeerGroup g, int64_t m0, int64_t m1) {
+  constexpr int X = 1 << K;
+  constexpr int MB = 256 / X;   // mids per tile -> X * MB * X amplitudes
+  constexpr int ROW = MB * X + 1;
+  extern __shared__ double2 smd[];
+  for (int64_t mt = m0 + int64_t(blockIdx.x) * MB; mt < m1; mt += int64_t(gridDim.x) * MB) {
+    const int nm = static_cast<int>((m1 - mt < MB ? m1 - mt : int64_t(MB)));
+    __syncthreads();
+    for (int x = 0; x < X; ++x)
+      for (int e = threadIdx.x; e < nm * X; e += blockDim.x) smd[x * ROW + e] = g.p[x][mt * X + e];
+    __syncthreads();
+    for (int x = 0; x < X; ++x) {
+      const int rx = K ? static_cast<int>(__brev(x) >> (32 - K)) : 0;
+      for (int e = threadIdx.x; e < nm * X; e += blockDim.x) {
+        const int mb = e / X, l = e % X;
+        const int rl = static_cast<int>(__brev(l) >> (32 - K));
+        g.p[x][mt * X + e] = canon2(smd[rl * ROW + mb * X + rx]);
+      }
+    }
+  }
+}
+
 }  // namespace
+
+void qft_dist_layers(void* const* ptrs, int k, int nb, Dim i0, Dim i1, cudaStream_t st) {
+  if (i1 <= i0) return;
+  PeerGroup g{};
+  for (int x = 0; x < (1 << k); ++x) g.p[x] = static_cast<double2*>(ptrs[x]);
+  int grid = grid_for(i1 - i0);
+  switch (k) {
+    case 1: k_qft_dist_layers<1><<<grid, 256, 0, st>>>(g, nb, i0, i1); break;
+    case 2: k_qft_dist_layers<2><<<grid, 256, 0, st>>>(g, nb, i0, i1); break;
+    case 3: k_qft_dist_layers<3><<<grid, 256, 0, st>>>(g, nb, i0, i1); break;
+    case 4: k_qft_dist_layers<4><<<grid, 256, 0, st>>>(g, nb, i0, i1); break;
+    default: throw_invalid("fused distributed QFT layers need 1..4 distributed qubits");
+  }
+  QTNH_LAUNCH_CHECK();
+}
+
+void dist_bitrev(void* const* ptrs, int k, Dim m0, Dim m1, cudaStream_t st) {
+  if (m1 <= m0) return;
+  PeerGroup g{};
+  for (int x = 0; x < (1 << k); ++x) g.p[x] = static_cast<double2*>(ptrs[x]);
+  const int X = 1 << k, MB = 256 / X;
+  size_t smem = size_t(X) * (MB * X + 1) * sizeof(double2);
+  int grid = static_cast<int>(std::min<Dim>((m1 - m0 + MB - 1) / MB, 148 * 8));
+  switch (k) {
+#define QTNH_DBR(KK)                                                                                    \
+  case KK: {                                                                                            \
+    static bool attr = [] {                                                                             \
+      cudaFuncSetAttribute(k_dist_bitrev<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024); \
+      return true;                                                                                      \
+    }();                                                                                                \
+    (void)attr;                                                                                         \
+    k_dist_bitrev<KK><<<grid, 256, smem, st>>>(g, m0, m1);                                              \
+    break;                                                                                              \
+  }
+    QTNH_DBR(1)
+    QTNH_DBR(2)
+    QTNH_DBR(3)
+    QTNH_DBR(4)
+#undef QTNH_DBR
+    default: throw_invalid("distributed bit reversal needs 1..4 distributed qubits");
+  }
+  QTNH_LAUNCH_CHECK();
+}
 
 void bitrev_hi_local(void* data, int nh, int k, cudaStream_t st) {
   if (nh <= 1) return;

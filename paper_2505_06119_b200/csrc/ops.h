@@ -94,6 +94,10 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st);
 void bitrev_local(void* data, int nb, cudaStream_t st);
 // Reverse the top nh bits of the local index, holding the low k bits.
 void bitrev_hi_local(void* data, int nh, int k, cudaStream_t st);
+// Peer-memory distributed QFT pieces; ptrs = the 2^k group members' blocks by
+// distributed coordinate (see gate.cu).
+void qft_dist_layers(void* const* ptrs, int k, int nb, Dim i0, Dim i1, cudaStream_t st);
+void dist_bitrev(void* const* ptrs, int k, Dim m0, Dim m1, cudaStream_t st);
 // In-place exchange of two equal-size local indices.
 void swap_indices_local(void* data, const std::vector<Dim>& dims, int ia, int ib, cudaStream_t st);
 // Gate on a dense local block: dims = local dims, targets = local positions.

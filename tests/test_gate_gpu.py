@@ -233,6 +233,27 @@ def test_blocked_qft(n, split, world, peer_mode):
         assert rel_l2(World(world).run(body2)[0], P.qft(n, st, swaps=False)) < TOL
 
 
+@pytest.mark.parametrize("n,split,dist,world", [(12, 2, (2, 1, 0), 8), (12, 2, (1, 2, 0), 8), (11, 1, (1, 1, 3), 6),
+                                               (12, 3, (1, 1, 0), 9)])
+def test_qft_with_broadcast_copies(n, split, dist, world, peer_mode):
+    """Whole QFT on a state with stretched / cyclic copies or an offset: every
+    copy ends up with the oracle's result."""
+    from paper_2505_06119_b200.qtnh import qft
+    st = circuits.counter_state(5 + n, 2**n)
+    st /= np.linalg.norm(st)
+
+    def body(rk):
+        t = Tensor.from_global(rk, IndexTuple([2] * n, split), DistParams(*dist), st)
+        qft(t, swaps=True)
+        return t.to_global_vector()
+
+    want = P.qft(n, st)
+    outs = [o for o in World(world).run(body) if o.size]
+    assert len(outs) == dist[0] * dist[1] * 2**split
+    for o in outs:
+        assert rel_l2(o, want) < TOL
+
+
 @pytest.mark.parametrize("dims,split,a,b,world,chunk", [
     ([2] * 12, 2, 0, 9, 4, 1 << 30),      # one chunk
     ([2] * 12, 2, 1, 4, 4, 256),          # many chunks (16 elements each)
