@@ -417,10 +417,12 @@ __device__ const double2 kQftSmallTw[15] = {{1.0, 0.0}, {1.0, 0.0}, {6.123233995
 
 __device__ __forceinline__ int swz8(int i) { return i ^ ((i >> 3) & 7); }  // conflict-free 16-B rows
 
+// The butterflies are unnormalised (y0 = a0 + a1, y1 = (a0 - a1) w): the L
+// factors of 1/sqrt2 are applied once when the chunk is written back, which
+// takes a third of the FP64 work out of a pass that is FP64-issue bound.
 template <int G>
 __device__ __forceinline__ void qft_low_round(double2* __restrict__ data, const double2* __restrict__ tw, int L,
                                               int B) {
-  const double r = 0.70710678118654752440;
   const int nf = 1 << (L - G);
   for (int f = threadIdx.x; f < nf; f += blockDim.x) {
     const int lo = f & ((1 << B) - 1), hi = f >> B;
@@ -439,11 +441,11 @@ __device__ __forceinline__ void qft_low_round(double2* __restrict__ data, const 
         if (k & (1 << u)) continue;
         const int k1 = k | (1 << u);
         double2 a0 = x[k], a1 = x[k1];
-        x[k] = make_double2(r * a0.x + r * a1.x, r * a0.y + r * a1.y);
-        double2 d = make_double2(r * a0.x - r * a1.x, r * a0.y - r * a1.y);
+        x[k] = make_double2(a0.x + a1.x, a0.y + a1.y);
+        double2 d = make_double2(a0.x - a1.x, a0.y - a1.y);
         const int kl = k & ((1 << u) - 1);
         double2 ph = kl ? cmul2(kQftSmallTw[(1 << u) - 1 + kl], lof[u]) : lof[u];
-        x[k1] = cmul2(d, ph);
+        x[k1] = (B + u) > 0 || kl ? cmul2(d, ph) : d;
       }
     }
 #pragma unroll
@@ -481,7 +483,76 @@ __global__ void __launch_bounds__(128) k_qft_low2(double2* __restrict__ psi, int
       __syncthreads();
       T = B - 1;
     }
-    for (int e = threadIdx.x; e < C; e += blockDim.x) g[e] = data[swz8(e)];
+    const double sc = ldexp(1.0, -(L / 2)) * (L & 1 ? 0.70710678118654752440 : 1.0);
+    for (int e = threadIdx.x; e < C; e += blockDim.x) {
+      double2 v = data[swz8(e)];
+      g[e] = make_double2(v.x * sc, v.y * sc);
+    }
+  }
+}
+
+// Version 3: the same rounds, with the chunks streamed through two shared-memory
+// buffers by cp.async (16-byte LDGSTS, swizzled destination): chunk c+1 is in
+// flight while chunk c is transformed and written back, so the global loads no
+// longer serialise behind the shared-memory rounds (v2 was long-scoreboard bound
+// at ~25% of HBM bandwidth).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+__global__ void __launch_bounds__(128) k_qft_low3(double2* __restrict__ psi, int64_t n_chunks, int S, int L) {
+  extern __shared__ double2 smq3[];
+  // a chunk of 2^S amplitudes holds 2^(S-L) independent L-bit transforms, so the
+  // rounds keep all threads busy for small L
+  const int C = 1 << S;
+  double2* buf0 = smq3;
+  double2* buf1 = smq3 + C;
+  double2* tw = smq3 + 2 * C;
+  for (int e = threadIdx.x; e < (1 << L); e += blockDim.x) {
+    if (e == 0) continue;
+    int t = 31 - __clz(e);
+    int v = e - (1 << t);
+    double sn, cs;
+    sincospi(static_cast<double>(v) * ldexp(1.0, -t), &sn, &cs);
+    tw[e] = make_double2(cs, sn);
+  }
+  int64_t ch = blockIdx.x;
+  if (ch < n_chunks)
+    for (int e = threadIdx.x; e < C; e += blockDim.x) cp_async16(buf0 + swz8(e), psi + ch * C + e);
+  cp_async_commit();
+  int cur = 0;
+  for (; ch < n_chunks; ch += gridDim.x) {
+    double2* data = cur ? buf1 : buf0;
+    double2* next = cur ? buf0 : buf1;
+    const int64_t nx = ch + gridDim.x;
+    if (nx < n_chunks)
+      for (int e = threadIdx.x; e < C; e += blockDim.x) cp_async16(next + swz8(e), psi + nx * C + e);
+    cp_async_commit();
+    cp_async_wait1();  // this chunk has landed (the next one may still be in flight)
+    __syncthreads();
+    for (int T = L - 1; T >= 0;) {
+      int gg = T + 1 >= 4 ? 4 : T + 1;
+      int B = T - gg + 1;
+      switch (gg) {
+        case 4: qft_low_round<4>(data, tw, S, B); break;
+        case 3: qft_low_round<3>(data, tw, S, B); break;
+        case 2: qft_low_round<2>(data, tw, S, B); break;
+        default: qft_low_round<1>(data, tw, S, B); break;
+      }
+      __syncthreads();
+      T = B - 1;
+    }
+    double2* g = psi + ch * C;
+    const double sc = ldexp(1.0, -(L / 2)) * (L & 1 ? 0.70710678118654752440 : 1.0);  // (1/sqrt2)^L
+    for (int e = threadIdx.x; e < C; e += blockDim.x) {
+      double2 v = data[swz8(e)];
+      g[e] = make_double2(v.x * sc, v.y * sc);
+    }
+    __syncthreads();  // buffer free before it is refilled two chunks on
+    cur ^= 1;
   }
 }
 
@@ -551,6 +622,61 @@ __global__ void __launch_bounds__(256) k_bitrev(double2* __restrict__ psi, int n
       psi[(int64_t(a) << (n - 5)) | (m << 5) | tx] = canon2(t2[rb][ra]);
       if (mr != m) psi[(int64_t(a) << (n - 5)) | (mr << 5) | tx] = canon2(t1[rb][ra]);
     }
+  }
+}
+
+// Version 2 of the in-place bit reversal: the two 32 x 32 tiles of a pair are
+// staged by cp.async into a double buffer (the next pair is in flight while this
+// one is written back), and the tile columns are XOR-swizzled with bits 2..4 of
+// the row so the bit-reversed column reads (lanes -> rows rev(tx)) hit eight
+// distinct 16-byte bank groups (v1's padded layout was 4-way conflicted).
+__device__ __forceinline__ int bswz(int row, int col) { return row * 32 + (col ^ ((row >> 2) & 7)); }
+
+__global__ void __launch_bounds__(256) k_bitrev2(double2* __restrict__ psi, int n, int64_t n_mid) {
+  extern __shared__ double2 sbr[];  // [stage][tile][32 x 32]
+  const int mbits = n - 10;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  auto rev_m = [&](int64_t m) {
+    return mbits > 0 ? static_cast<int64_t>(rev_bits64(static_cast<uint64_t>(m), mbits)) : m;
+  };
+  auto next_valid = [&](int64_t m) {
+    while (m < n_mid && rev_m(m) < m) m += gridDim.x;  // a pair is handled by its smaller member
+    return m;
+  };
+  auto issue = [&](int stage, int64_t m) {
+    double2* t1 = sbr + stage * 2048;
+    double2* t2 = t1 + 1024;
+    const int64_t mr = rev_m(m);
+#pragma unroll
+    for (int a = ty; a < 32; a += 8) {
+      cp_async16(t1 + bswz(a, tx), psi + ((int64_t(a) << (n - 5)) | (m << 5) | tx));
+      cp_async16(t2 + bswz(a, tx), psi + ((int64_t(a) << (n - 5)) | (mr << 5) | tx));
+    }
+  };
+  int64_t m = next_valid(blockIdx.x);
+  if (m < n_mid) issue(0, m);
+  cp_async_commit();
+  int stage = 0;
+  while (m < n_mid) {
+    const int64_t mn = next_valid(m + gridDim.x);
+    if (mn < n_mid) issue(stage ^ 1, mn);
+    cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();
+    const double2* t1 = sbr + stage * 2048;
+    const double2* t2 = t1 + 1024;
+    const int64_t mr = rev_m(m);
+    const int rb = rev_bits(tx, 5);
+#pragma unroll
+    for (int a = ty; a < 32; a += 8) {
+      const int ra = rev_bits(a, 5);
+      // new (a, m, b) = old (rev b, rev m, rev a)
+      psi[(int64_t(a) << (n - 5)) | (m << 5) | tx] = canon2(t2[bswz(rb, ra)]);
+      if (mr != m) psi[(int64_t(a) << (n - 5)) | (mr << 5) | tx] = canon2(t1[bswz(rb, ra)]);
+    }
+    __syncthreads();
+    stage ^= 1;
+    m = mn;
   }
 }
 
@@ -745,8 +871,22 @@ int qft_group_max() {
 void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
   // Layers with target bits first_layer_bit .. 0 (descending), all local.
   auto* p = static_cast<double2*>(data);
-  int L = std::min(nb, kQftLowMax);
+  static const int lmax = [] {
+    const char* e = std::getenv("QTNH_QFT_L");
+    int v = e ? std::atoi(e) : kQftLowMax;
+    return std::max(4, std::min(kQftLowMax, v));
+  }();
+  // Low-chunk size: fewest strided group passes first, then fewest shared-memory
+  // rounds in the low pass (e.g. 28 bits: L = 8 -> 5 group passes of 4 layers +
+  // a 2-round low pass, instead of L = 11 -> 4 + 1 passes and 3 rounds).
   int top = first_layer_bit;
+  const int layers = top + 1, gmax = qft_group_max();
+  int L = std::min(layers, lmax);
+  {
+    auto key = [&](int l) { return std::make_pair((layers - l + gmax - 1) / gmax, (l + 3) / 4); };
+    for (int l = std::min(layers, lmax); l >= 1; --l)
+      if (key(l) < key(L)) L = l;
+  }
   while (top >= L) {
     int g = std::min(qft_group_max(), top - L + 1);  // 5 spills at 255 registers
     int B = top - g + 1;
@@ -770,16 +910,36 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
   if (top >= 0) {
     // remaining layers: bits top..0 with top = L - 1 (all of the low chunk)
     int Lc = top + 1;
-    size_t smem = static_cast<size_t>(2) << Lc;  // data + twiddles, in double2
-    smem *= sizeof(double2);
-    static bool attr = false;
-    if (!attr) {
-      QTNH_CUDA(cudaFuncSetAttribute(k_qft_low2, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16 << kQftLowMax));
-      attr = true;
-    }
     int64_t n_chunks = int64_t(1) << (nb - Lc);
-    int grid = static_cast<int>(std::min<int64_t>(n_chunks, 148 * 8));
-    k_qft_low2<<<grid, 128, smem, st>>>(p, n_chunks, Lc);
+    static const bool v2 = [] {
+      const char* e = std::getenv("QTNH_QFT_LOW");
+      return e && e[0] == '2';
+    }();
+    if (v2) {
+      size_t smem = (static_cast<size_t>(2) << Lc) * sizeof(double2);  // data + twiddles
+      static bool attr2 = [] {
+        cudaFuncSetAttribute(k_qft_low2, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16 << kQftLowMax);
+        return true;
+      }();
+      (void)attr2;
+      int grid = static_cast<int>(std::min<int64_t>(n_chunks, 148 * 8));
+      k_qft_low2<<<grid, 128, smem, st>>>(p, n_chunks, Lc);
+    } else {
+      const int S = std::max(Lc, std::min(nb, kQftLowMax));
+      n_chunks = int64_t(1) << (nb - S);
+      size_t smem = ((static_cast<size_t>(2) << S) + (size_t(1) << Lc)) * sizeof(double2);  // 2 buffers + twiddles
+      static int per_sm = [] {
+        cudaFuncSetAttribute(k_qft_low3, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 16 << kQftLowMax);
+        return 0;
+      }();
+      int dev = 0, occ = 0, sms = 0;
+      QTNH_CUDA(cudaGetDevice(&dev));
+      QTNH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qft_low3, 128, smem));
+      (void)per_sm;
+      int grid = static_cast<int>(std::min<int64_t>(n_chunks, (int64_t)sms * std::max(1, occ)));
+      k_qft_low3<<<grid, 128, smem, st>>>(p, n_chunks, S, Lc);
+    }
     QTNH_LAUNCH_CHECK();
   }
 }
@@ -787,8 +947,27 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
 void bitrev_local(void* data, int nb, cudaStream_t st) {
   if (nb < 10) throw_invalid("in-place bit reversal needs at least 10 local qubits");
   int64_t n_mid = int64_t(1) << (nb - 10);
-  int grid = static_cast<int>(std::min<int64_t>(n_mid, 148 * 8));
-  k_bitrev<<<grid, 256, 0, st>>>(static_cast<double2*>(data), nb, n_mid);
+  static const bool v1 = [] {
+    const char* e = std::getenv("QTNH_BITREV");
+    return e && e[0] == '1';
+  }();
+  if (v1) {
+    int grid = static_cast<int>(std::min<int64_t>(n_mid, 148 * 8));
+    k_bitrev<<<grid, 256, 0, st>>>(static_cast<double2*>(data), nb, n_mid);
+  } else {
+    const size_t smem = 4 * 1024 * sizeof(double2);  // 2 stages x 2 tiles
+    static bool attr = [] {
+      cudaFuncSetAttribute(k_bitrev2, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      return true;
+    }();
+    (void)attr;
+    int dev = 0, occ = 0, sms = 0;
+    QTNH_CUDA(cudaGetDevice(&dev));
+    QTNH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bitrev2, 256, smem));
+    int grid = static_cast<int>(std::min<int64_t>(n_mid, (int64_t)sms * std::max(1, occ)));
+    k_bitrev2<<<grid, 256, smem, st>>>(static_cast<double2*>(data), nb, n_mid);
+  }
   QTNH_LAUNCH_CHECK();
 }
 
