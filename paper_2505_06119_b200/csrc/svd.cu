@@ -185,7 +185,8 @@ template <int B>
 __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__ part, double2* __restrict__ wh,
                                                      int* __restrict__ flags, double* __restrict__ off_max,
                                                      int npairs, int splits, double tol, int inner_sweeps,
-                                                     const double* __restrict__ floor_abs) {
+                                                     const double* __restrict__ floor_abs,
+                                                     const double* __restrict__ thr, double* __restrict__ off_top) {
   constexpr int P2 = 2 * B, LD = P2 + 1;
   const int pair = blockIdx.x, mat = blockIdx.y, tid = threadIdx.x;
   const double fl = floor_abs[mat];
@@ -231,6 +232,29 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
     __syncthreads();
     return res;
   };
+  if (thr) {  // statistics: off-diagonal measure over pairs touching a row above thr
+    const double th = thr[mat];
+    double mx = 0.0;
+    for (int e = tid; e < P2 * P2; e += 256) {
+      int i = e / P2, j = e % P2;
+      if (i >= j) continue;
+      if (fmax(G[i * LD + i].x, G[j * LD + j].x) < th) continue;
+      double d = sqrt(fmax(G[i * LD + i].x * G[j * LD + j].x, 0.0));
+      double2 gij = G[i * LD + j];
+      double g = hypot(gij.x, gij.y);
+      double den = fmax(d, fl);
+      if (den > 0.0) mx = fmax(mx, g / den);
+      else if (g > 0.0) mx = fmax(mx, 1.0);
+    }
+    red[tid] = mx;
+    __syncthreads();
+    for (int st = 128; st > 0; st >>= 1) {
+      if (tid < st) red[tid] = fmax(red[tid], red[tid + st]);
+      __syncthreads();
+    }
+    if (tid == 0) atomic_max_nonneg(off_top + mat, red[0]);
+    __syncthreads();
+  }
   double off = measure();
   if (tid == 0) atomic_max_nonneg(off_max + mat, off);
   const int64_t fidx = static_cast<int64_t>(mat) * npairs + pair;
@@ -671,8 +695,26 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   bool converged = false;
   const unsigned ctiles = static_cast<unsigned>(
       std::min<Dim>((W + 47) / 48, std::max<Dim>(1, (B == 16 ? 8 : 4) * sms() / (npairs * batch))));
+  const bool stats = std::getenv("QTNH_SVD_DEBUG") && chi < rows;
+  DevBuf thr_d(static_cast<size_t>(batch) * sizeof(double), r), offt(static_cast<size_t>(batch) * sizeof(double), r);
+  DevBuf sig0(static_cast<size_t>(batch * rp) * sizeof(double), r);
+  std::vector<double> thr_h(batch), offt_h(batch);
   for (; sweep < max_sweeps; ++sweep) {
     QTNH_CUDA(cudaMemsetAsync(offm.ptr, 0, batch * sizeof(double), st));
+    if (stats) {
+      QTNH_CUDA(cudaMemsetAsync(offt.ptr, 0, batch * sizeof(double), st));
+      k_svd_norms<<<dim3(static_cast<unsigned>(rp), static_cast<unsigned>(batch)), 256, 0, st>>>(
+          static_cast<const double2*>(wk.ptr), static_cast<double*>(sig0.ptr), rp, L, qw);
+      std::vector<double> nh(batch * rp);
+      QTNH_CUDA(cudaMemcpyAsync(nh.data(), sig0.ptr, nh.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+      QTNH_CUDA(cudaStreamSynchronize(st));
+      for (Dim b = 0; b < batch; ++b) {
+        std::vector<double> v(nh.begin() + b * rp, nh.begin() + (b + 1) * rp);
+        std::nth_element(v.begin(), v.begin() + (chi - 1), v.end(), std::greater<double>());
+        thr_h[b] = 0.5 * v[chi - 1] * v[chi - 1];
+      }
+      QTNH_CUDA(cudaMemcpyAsync(thr_d.ptr, thr_h.data(), batch * sizeof(double), cudaMemcpyHostToDevice, st));
+    }
     for (int rd = 0; rd < rounds; ++rd) {
       if (mma)
         k_svd_gram_mma_t<B><<<dim3(npairs, splits, static_cast<unsigned>(batch)), B * 8, 0, st>>>(
@@ -686,7 +728,8 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
       k_svd_eigen_t<B><<<dim3(npairs, static_cast<unsigned>(batch)), 256, eig_smem, st>>>(
             static_cast<const double2*>(part.ptr), static_cast<double2*>(whb.ptr), static_cast<int*>(flags.ptr),
             static_cast<double*>(offm.ptr), npairs, splits, tol, inner_sweeps(),
-            static_cast<const double*>(floor_abs.ptr));
+            static_cast<const double*>(floor_abs.ptr), stats ? static_cast<const double*>(thr_d.ptr) : nullptr,
+            static_cast<double*>(offt.ptr));
       QTNH_LAUNCH_CHECK();
       if (mma)
         k_svd_update_mma_t<B><<<dim3(ctiles, npairs, static_cast<unsigned>(batch)), B * 8, upd_smem, st>>>(
@@ -701,7 +744,13 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
     QTNH_CUDA(cudaMemcpyAsync(off_h.data(), offm.ptr, batch * sizeof(double), cudaMemcpyDeviceToHost, st));
     QTNH_CUDA(cudaStreamSynchronize(st));
     double mx = *std::max_element(off_h.begin(), off_h.end());
-    if (std::getenv("QTNH_SVD_DEBUG")) std::fprintf(stderr, "svd sweep %d max_off %.3e\n", sweep, mx);
+    if (stats) {
+      QTNH_CUDA(cudaMemcpy(offt_h.data(), offt.ptr, batch * sizeof(double), cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "svd sweep %d max_off %.3e top_off %.3e thr %.3e\n", sweep, mx,
+                   *std::max_element(offt_h.begin(), offt_h.end()), thr_h[0]);
+    } else if (std::getenv("QTNH_SVD_DEBUG")) {
+      std::fprintf(stderr, "svd sweep %d max_off %.3e\n", sweep, mx);
+    }
     if (mx < tol) {
       converged = true;
       ++sweep;
