@@ -65,6 +65,11 @@ def hash_counter(seed: int, k0: int = 0, k1: int = 0, k2: int = 0) -> int:
     return int(lib.qtnh_hash_counter(seed, k0, k1, k2))
 
 
+def u64_to_unit(u: int) -> float:
+    """common.hpp:103-105: top 53 bits -> [0, 1)."""
+    return float(u >> 11) * 2.0**-53
+
+
 def fisher_yates(seed: int, tag: int, r: int) -> List[int]:
     """Seeded Fisher-Yates on hash_counter(seed, tag, i) (test_ops.cpp:124-129)."""
     p = list(range(r))

@@ -17,7 +17,7 @@ from typing import List, Sequence, Tuple
 import numpy as np
 
 from . import circuits, qtnh
-from .qtnh import ABSORB_LEFT, IndexTuple, Tensor
+from .qtnh import ABSORB_LEFT, ABSORB_RIGHT, IndexTuple, Tensor
 
 SINGLE_QUBIT = [circuits.SQRT_X, circuits.SQRT_Y, circuits.SQRT_W]
 
@@ -49,6 +49,7 @@ class MPS:
         self.sites: List[Tensor] = []
         self.log_fidelity = 0.0
         self.discarded = []
+        self.centre = None
         for _ in range(n):  # |0...0>, bond dimension 1
             v = np.zeros(d, dtype=np.complex128)
             v[0] = 1.0
@@ -136,6 +137,160 @@ class MPS:
 
     def bond_dims(self) -> List[int]:
         return [t.shape().dims[2] for t in self.sites[:-1]]
+
+    # ---- SPEC mps operations either side of the two-site update ------------
+    # All of them run on the device through the hot-path ops: qtnh.contract (DMMA zgemm),
+    # qtnh.svd (Jacobi SVD), ops.conj / ops.scale. Bonds are stored at their effective
+    # dimension; the reference's zero padding to chi adds only zeros, so
+    # every quantity below is identical.
+
+    @classmethod
+    def bitstring(cls, rank: qtnh.Rank, bits: Sequence[int], chi: int, d: int = 2) -> "MPS":
+        """mps_bitstring: amplitude 1 on `bits`, bond dimension 1."""
+        m = cls(rank, len(bits), chi, d)
+        for q, b in enumerate(bits):
+            if not 0 <= int(b) < d:
+                raise qtnh.InvalidArgument("bit value outside the physical dimension")
+            v = np.zeros(d, dtype=np.complex128)
+            v[int(b)] = 1.0
+            m.sites[q].free()
+            m.sites[q] = Tensor.from_global(rank, IndexTuple([1, d, 1], 0), None, v)
+        return m
+
+    @classmethod
+    def random(cls, rank: qtnh.Rank, n: int, chi_eff: int, seed: int, chi: int = 0, d: int = 2) -> "MPS":
+        """mps_random: seeded complex normal sites with effective bond
+        dimension min(chi_eff, d^q, d^(n-q)) at bond q, normalised to norm2 = 1. Site q
+        draws from the counter-based stream (seed, q) of common.hpp."""
+        chi = chi or chi_eff
+        if chi_eff > chi:
+            raise qtnh.InvalidArgument("chi_eff exceeds chi")
+        m = cls(rank, n, chi, d)
+        bonds = [1] + [min(chi_eff, d ** (q + 1), d ** (n - q - 1)) for q in range(n - 1)] + [1]
+        for q in range(n):
+            l, r = bonds[q], bonds[q + 1]
+            v = circuits.counter_state(circuits.hash_counter(seed, 31, q), l * d * r)
+            m.sites[q].free()
+            m.sites[q] = Tensor.from_global(rank, IndexTuple([l, d, r], 0), None, v)
+        m.renormalise()
+        return m
+
+    def _set(self, q: int, t: Tensor) -> None:
+        self.sites[q].free()
+        self.sites[q] = t
+
+    def canonicalize(self, centre: int) -> "MPS":
+        """Mixed canonical form at `centre`: sites left of it are
+        left-orthonormal (U of an SVD over (left, phys) x right, S Vh pushed right),
+        sites right of it right-orthonormal (Vh, U S pushed left). No truncation, so
+        the statevector is unchanged up to rounding."""
+        if not 0 <= centre < self.n:
+            raise qtnh.InvalidArgument("canonical centre outside the chain")
+        for q in range(centre):
+            u, _, svh = qtnh.svd(self.sites[q], [0, 1], [2], absorb=ABSORB_RIGHT)
+            nxt = qtnh.contract(svh, self.sites[q + 1], [1], [0])  # (k, d, r)
+            svh.free()
+            self._set(q, u)
+            self._set(q + 1, nxt)
+        for q in range(self.n - 1, centre, -1):
+            us, _, vh = qtnh.svd(self.sites[q], [0], [1, 2], absorb=ABSORB_LEFT)
+            prv = qtnh.contract(self.sites[q - 1], us, [2], [0])  # (l, d, k)
+            us.free()
+            self._set(q, vh)
+            self._set(q - 1, prv)
+        self.centre = centre
+        return self
+
+    def overlap(self, other: "MPS") -> complex:
+        """<other|self> by the transfer-matrix contraction left to right:
+        E(a, b) <- sum over (a, s, b) of E(a, b) A_s(a, a') conj(B_s(b, b'))."""
+        if other.n != self.n or other.d != self.d:
+            raise qtnh.InvalidArgument("overlap needs MPS of equal length and physical dimension")
+        env = Tensor.from_global(self.rank, IndexTuple([1, 1], 0), None, np.ones(1, dtype=np.complex128))
+        for q in range(self.n):
+            t1 = qtnh.contract(env, self.sites[q], [0], [0])  # (b, s, a')
+            bc = qtnh.ops.conj(other.sites[q])
+            env.free()
+            env = qtnh.contract(t1, bc, [0, 1], [0, 1])  # (a', b')
+            t1.free()
+            bc.free()
+        out = complex(env.to_global_vector()[0])
+        env.free()
+        return out
+
+    def norm2(self) -> float:
+        """SPEC.md:505-513: overlap(m, m).real."""
+        return float(self.overlap(self).real)
+
+    def renormalise(self) -> "MPS":
+        """Scale every site by the same factor so norm2 = 1 (SPEC.md:508);
+        DegenerateStateError for a zero state."""
+        n2 = self.norm2()
+        if not n2 > 0.0:
+            raise qtnh.DegenerateStateError("renormalise of a zero-norm MPS")
+        f = n2 ** (-0.5 / self.n)
+        for q in range(self.n):
+            self._set(q, qtnh.ops.scale(self.sites[q], f))
+        return self
+
+    def effective_bond_dims(self, tol: float = 1e-12) -> List[int]:
+        """Per-bond count of Schmidt values above tol: right-canonical
+        form, then the centre walks right and each bond's SVD gives its spectrum."""
+        self.canonicalize(0)
+        out = []
+        for q in range(self.n - 1):
+            u, sv, svh = qtnh.svd(self.sites[q], [0, 1], [2], absorb=ABSORB_RIGHT)
+            out.append(int(np.sum(sv > tol)))
+            nxt = qtnh.contract(svh, self.sites[q + 1], [1], [0])
+            svh.free()
+            self._set(q, u)
+            self._set(q + 1, nxt)
+        self.centre = self.n - 1
+        return out
+
+    def sample(self, sites: Sequence[int], seed: int, draw: int = 0) -> List[int]:
+        """One draw from the marginal on `sites`: right-canonical form,
+        then sequential conditional sampling left to right over ALL sites (SPEC design
+        decision), the requested subset projected from the full draw.
+        Site q's uniform is u64_to_unit(hash_counter(seed, draw, q))."""
+        n2 = self.norm2()
+        if abs(n2 - 1.0) > 1e-8:
+            raise qtnh.PreconditionError("sample needs a normalised MPS (norm2 = %.3e)" % n2)
+        self.canonicalize(0)
+        env = Tensor.from_global(self.rank, IndexTuple([1], 0), None, np.ones(1, dtype=np.complex128))
+        bits = []
+        for q in range(self.n):
+            v = qtnh.contract(env, self.sites[q], [0], [0])  # (d, r)
+            d, r = v.shape().dims
+            vh = v.to_global_vector().reshape(d, r)
+            v.free()
+            p = np.sum(np.abs(vh) ** 2, axis=1)
+            tot = float(np.sum(p))
+            u = circuits.u64_to_unit(circuits.hash_counter(seed, draw, q)) * tot
+            s = int(min(np.searchsorted(np.cumsum(p), u, side="right"), d - 1))
+            while p[s] == 0.0 and s > 0:  # never collapse onto a zero-probability outcome
+                s -= 1
+            bits.append(s)
+            env.free()
+            env = Tensor.from_global(self.rank, IndexTuple([r], 0), None, vh[s] / np.sqrt(p[s]))
+        env.free()
+        return [bits[q] for q in sites]
+
+    def to_statevector(self) -> np.ndarray:
+        """mps_to_statevector, qubit 0 most significant; n <= 26."""
+        if self.n > 26:
+            raise qtnh.ResourceError("statevector of more than 26 sites", 0)
+        acc = self.sites[0]
+        owned = False
+        for q in range(1, self.n):
+            nxt = qtnh.contract(acc, self.sites[q], [acc.shape().n_idx() - 1], [0])
+            if owned:
+                acc.free()
+            acc, owned = nxt, True
+        out = acc.to_global_vector()
+        if owned:
+            acc.free()
+        return out
 
     def amplitudes(self, bitstrings: np.ndarray) -> np.ndarray:
         """<b|psi> for each row of `bitstrings` (n bits, qubit 0 first): a left-to-

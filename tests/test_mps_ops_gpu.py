@@ -1,0 +1,197 @@
+"""GPU: the MPS operations either side of the two-site update (SURVEY.md 8(f) rank 4,
+SPEC.md:441-543) -- bitstring / random construction, canonical forms, overlap,
+norm2 / renormalise, effective bond dimensions, sampling -- against a dense
+statevector oracle (numpy) on small chains."""
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+from paper_2505_06119_b200 import circuits, qtnh
+from paper_2505_06119_b200.mps import MPS
+from paper_2505_06119_b200.qtnh import World, run_collect
+
+pytestmark = pytest.mark.gpu
+
+
+def dense_from_sites(sites):
+    acc = sites[0]
+    for s in sites[1:]:
+        acc = np.tensordot(acc, s, axes=([acc.ndim - 1], [0]))
+    return acc.reshape(-1)
+
+
+def site_arrays(m):
+    return [t.to_global_vector().reshape(t.shape().dims) for t in m.sites]
+
+
+def test_bitstring_statevector_norm_and_bonds():
+    def body(rk):
+        m = MPS.bitstring(rk, [1, 0, 1], chi=4)
+        sv = m.to_statevector()
+        out = (sv, m.norm2(), m.effective_bond_dims())
+        m.free()
+        return out
+
+    sv, n2, bonds = run_collect(World(1), body)
+    want = np.zeros(8, complex)
+    want[0b101] = 1
+    assert np.array_equal(sv, want)
+    assert n2 == 1.0
+    assert bonds == [1, 1]
+
+
+def test_random_mps_is_normalised_and_deterministic():
+    def body(rk):
+        a = MPS.random(rk, 6, 4, seed=9)
+        b = MPS.random(rk, 6, 4, seed=9)
+        out = (a.to_statevector(), b.to_statevector(), a.bond_dims())
+        a.free()
+        b.free()
+        return out
+
+    va, vb, bonds = run_collect(World(1), body)
+    assert np.array_equal(va, vb)
+    assert abs(np.linalg.norm(va) - 1) < 1e-12
+    assert bonds == [2, 4, 4, 4, 2]
+
+
+@pytest.mark.parametrize("n,chi_eff,centre", [(6, 4, 0), (6, 4, 3), (7, 8, 6), (5, 3, 2)])
+def test_canonicalize_keeps_state_and_orthonormalises(n, chi_eff, centre):
+    def body(rk):
+        m = MPS.random(rk, n, chi_eff, seed=n + centre)
+        before = m.to_statevector()
+        m.canonicalize(centre)
+        after = m.to_statevector()
+        sites = site_arrays(m)
+        m.free()
+        return before, after, sites
+
+    before, after, sites = run_collect(World(1), body)
+    assert rel_l2(after, before) < 1e-12
+    for q, a in enumerate(sites):
+        l, d, r = a.shape
+        if q < centre:  # left-orthonormal: sum_{l,s} conj(A) A = I_r
+            g = np.einsum("lsr,lsk->rk", a.conj(), a)
+            assert np.allclose(g, np.eye(r), atol=1e-10)
+        elif q > centre:  # right-orthonormal: sum_{s,r} A conj(A) = I_l
+            g = np.einsum("lsr,ksr->lk", a, a.conj())
+            assert np.allclose(g, np.eye(l), atol=1e-10)
+
+
+def test_overlap_matches_dense_inner_product():
+    def body(rk):
+        a = MPS.random(rk, 6, 4, seed=1)
+        b = MPS.random(rk, 6, 3, seed=2)
+        out = (a.overlap(b), b.overlap(a), a.overlap(a), a.to_statevector(), b.to_statevector())
+        z = MPS.bitstring(rk, [0] * 6, 4)
+        o = MPS.bitstring(rk, [1] + [0] * 5, 4)
+        out += (z.overlap(o),)
+        for m in (a, b, z, o):
+            m.free()
+        return out
+
+    ab, ba, aa, va, vb, zo = run_collect(World(1), body)
+    assert abs(ab - np.vdot(vb, va)) < 1e-12
+    assert abs(ba - np.vdot(va, vb)) < 1e-12
+    assert abs(aa - 1) < 1e-12
+    assert zo == 0
+
+
+def test_norm2_scaling_and_renormalise():
+    def body(rk):
+        m = MPS.bitstring(rk, [0, 1, 1, 0], 2)
+        m._set(2, qtnh.ops.scale(m.sites[2], 2.0))
+        n4 = m.norm2()
+        m.renormalise()
+        n1 = m.norm2()
+        m.free()
+        z = MPS.bitstring(rk, [0, 0], 2)
+        z._set(0, qtnh.ops.scale(z.sites[0], 0.0))
+        try:
+            z.renormalise()
+            err = None
+        except qtnh.DegenerateStateError as e:
+            err = e
+        z.free()
+        return n4, n1, err
+
+    n4, n1, err = run_collect(World(1), body)
+    assert n4 == 4.0
+    assert abs(n1 - 1) < 1e-12
+    assert isinstance(err, qtnh.DegenerateStateError)
+
+
+def test_truncation_lowers_norm():
+    """a two-site update truncated below the Schmidt rank loses weight."""
+    def body(rk):
+        m = MPS.random(rk, 8, 8, seed=4, chi=8)
+        m.canonicalize(3)  # orthonormal environment: the norm loss is the discarded weight
+        m.chi = 2
+        s, frac = m.apply_2q(3, circuits.FSIM.reshape(4, 4))
+        out = (frac, m.norm2())
+        m.free()
+        return out
+
+    frac, n2 = run_collect(World(1), body)
+    assert frac < 1.0 and n2 < 1.0
+    assert abs(n2 - frac) < 1e-10
+
+
+def test_effective_bond_dims_bell_and_random():
+    def body(rk):
+        bell = MPS.bitstring(rk, [0, 0, 0, 0], 4)
+        bell.apply_1q(1, circuits.H)
+        cnot = np.eye(4, dtype=complex)[[0, 1, 3, 2]]
+        bell.apply_2q(1, cnot)  # (|00> + |11>)/sqrt2 on sites 1, 2
+        out = bell.effective_bond_dims()
+        bell.free()
+        r = MPS.random(rk, 8, 4, seed=5)
+        out2 = r.effective_bond_dims()
+        r.free()
+        return out, out2
+
+    b, r = run_collect(World(1), body)
+    assert b == [1, 2, 1]
+    assert r == [2, 4, 4, 4, 4, 4, 2]
+
+
+def test_sampling_distributions():
+    def body(rk):
+        bits = MPS.bitstring(rk, [1, 0, 1, 1], 2)
+        det = [bits.sample([0, 1, 2, 3], seed=3, draw=i) for i in range(5)]
+        sub = bits.sample([3, 0], seed=3)
+        bits.free()
+        bell = MPS.bitstring(rk, [0, 0], 2)
+        bell.apply_1q(0, circuits.H)
+        bell.apply_2q(0, np.eye(4, dtype=complex)[[0, 1, 3, 2]])
+        bd = [tuple(bell.sample([0, 1], seed=7, draw=i)) for i in range(200)]
+        bell.free()
+        uni = MPS.bitstring(rk, [0, 0], 2)
+        uni.apply_1q(0, circuits.H)
+        uni.apply_1q(1, circuits.H)
+        ud = [tuple(uni.sample([0, 1], seed=11, draw=i)) for i in range(2000)]
+        uni.free()
+        return det, sub, bd, ud
+
+    det, sub, bd, ud = run_collect(World(1), body)
+    assert all(d == [1, 0, 1, 1] for d in det)
+    assert sub == [1, 1]
+    assert set(bd) <= {(0, 0), (1, 1)} and len(set(bd)) == 2
+    for o in [(0, 0), (0, 1), (1, 0), (1, 1)]:
+        f = ud.count(o) / len(ud)
+        assert abs(f - 0.25) < 0.04  # 4 sigma at 2000 draws
+
+
+def test_sample_requires_normalised_state():
+    def body(rk):
+        m = MPS.bitstring(rk, [0, 1], 2)
+        m._set(0, qtnh.ops.scale(m.sites[0], 3.0))
+        try:
+            m.sample([0], seed=1)
+            e = None
+        except qtnh.PreconditionError as ex:
+            e = ex
+        m.free()
+        return e
+
+    assert isinstance(run_collect(World(1), body), qtnh.PreconditionError)
