@@ -276,6 +276,113 @@ class MPS:
         env.free()
         return [bits[q] for q in sites]
 
+    def _reshape(self, t: Tensor, dims: Sequence[int]) -> Tensor:
+        """Same row-major values under new dims (one device copy)."""
+        out = Tensor.from_device(self.rank, IndexTuple(list(dims), 0), None, t.device_ptr())
+        t.free()
+        return out
+
+    def _split_range(self, theta: Tensor, first: int, last: int, chi: int) -> None:
+        """Write theta (l, d x (last-first+1), r) back as sites first..last by
+        repeated SVDs truncated to chi (S pushed right, kept-weight into
+        log_fidelity), then move the centre back to `first`."""
+        for q in range(first, last):
+            dims = theta.shape().dims
+            m = dims[0] * dims[1]
+            k = min(m, int(np.prod(dims[2:])))
+            keep = min(chi, k)
+            u, sv, rest = qtnh.svd(theta, [0, 1], list(range(2, len(dims))), chi=k, absorb=ABSORB_RIGHT)
+            theta.free()
+            if keep < k:
+                tot = float(np.sum(sv**2))
+                if tot > 0:
+                    self.log_fidelity += np.log(float(np.sum(sv[:keep] ** 2)) / tot)
+                u2 = qtnh.ops.slice_local_dims(u, [dims[0], dims[1], keep])
+                r2 = qtnh.ops.slice_local_dims(rest, [keep] + list(dims[2:]))
+                u.free()
+                rest.free()
+                u, rest = u2, r2
+            self._set(q, u)
+            theta = self._reshape(rest, [rest.shape().dims[0]] + list(rest.shape().dims[1:]))
+        self._set(last, theta)
+        for q in range(last, first, -1):
+            us, _, vh = qtnh.svd(self.sites[q], [0], [1, 2], absorb=ABSORB_LEFT)
+            prv = qtnh.contract(self.sites[q - 1], us, [2], [0])
+            us.free()
+            self._set(q, vh)
+            self._set(q - 1, prv)
+        self.centre = first
+
+    def apply_gate_sites(self, targets: Sequence[int], gate: np.ndarray) -> "MPS":
+        """apply_raw_gate: contract the inclusive site range of the
+        sorted targets into one tensor, apply the gate there (identities on the
+        intermediate sites), re-decompose by repeated SVD truncated to chi, and leave
+        the canonical centre at the first target."""
+        targets = [int(t) for t in targets]
+        if targets != sorted(set(targets)) or not targets or targets[0] < 0 or targets[-1] >= self.n:
+            raise qtnh.InvalidArgument("apply_raw_gate needs sorted distinct targets inside the chain")
+        g = np.asarray(gate, dtype=np.complex128)
+        D = self.d ** len(targets)
+        if g.size != D * D:
+            raise qtnh.InvalidArgument("gate dimension does not match the number of targets")
+        first, last = targets[0], targets[-1]
+        theta = qtnh.contract(self.sites[first], self.sites[first + 1], [2], [0]) if last > first else None
+        if theta is None:
+            theta = qtnh.ops.scale(self.sites[first], 1.0)
+        for q in range(first + 2, last + 1):
+            nxt = qtnh.contract(theta, self.sites[q], [theta.shape().n_idx() - 1], [0])
+            theta.free()
+            theta = nxt
+        qtnh.apply_gate(theta, [1 + t - first for t in targets], g.reshape(-1))
+        self._split_range(theta, first, last, self.chi)
+        return self
+
+    def apply_mpo(self, mpo: Sequence[np.ndarray], first: int = 0) -> "MPS":
+        """apply_mpo: MPO sites W (wl, d_out, d_in, wr) on the
+        contiguous support first..first+len-1; each MPS site becomes
+        (l wl, d_out, r wr) = sum_{d_in} A(l, d_in, r) W(wl, d_out, d_in, wr), then one
+        left-canonical sweep and a right-to-left compression sweep back to chi, centre
+        restored at the first MPO site."""
+        if first < 0 or first + len(mpo) > self.n:
+            raise qtnh.InvalidArgument("MPO support outside the chain")
+        for i, w in enumerate(mpo):
+            w = np.asarray(w, dtype=np.complex128)
+            if w.ndim != 4 or w.shape[1] != self.d or w.shape[2] != self.d:
+                raise qtnh.InvalidArgument("MPO site needs shape (wl, d, d, wr) with the physical dimension")
+            if (i == 0 and w.shape[0] != 1) or (i == len(mpo) - 1 and w.shape[3] != 1):
+                raise qtnh.InvalidArgument("MPO boundary bonds must be 1")
+            q = first + i
+            a = self.sites[q]
+            l, _, r = a.shape().dims
+            wt = Tensor.from_global(self.rank, IndexTuple(list(w.shape), 0), None, w.reshape(-1))
+            c = qtnh.contract(a, wt, [1], [2])  # (l, r, wl, d_out, wr)
+            wt.free()
+            p = qtnh.ops.permute(c, [0, 2, 3, 1, 4], 0)  # (l, wl, d_out, r, wr)
+            c.free()
+            self._set(q, self._reshape(p, [l * w.shape[0], self.d, r * w.shape[3]]))
+        # compression: left-canonical form, then truncating right-to-left sweep
+        self.canonicalize(self.n - 1)
+        for q in range(self.n - 1, 0, -1):
+            dims = self.sites[q].shape().dims
+            k = min(dims[0], dims[1] * dims[2])
+            keep = min(self.chi, k)
+            us, sv, vh = qtnh.svd(self.sites[q], [0], [1, 2], chi=k, absorb=ABSORB_LEFT)
+            if keep < k:
+                tot = float(np.sum(sv**2))
+                if tot > 0:
+                    self.log_fidelity += np.log(float(np.sum(sv[:keep] ** 2)) / tot)
+                us2 = qtnh.ops.slice_local_dims(us, [dims[0], keep])
+                vh2 = qtnh.ops.slice_local_dims(vh, [keep, dims[1], dims[2]])
+                us.free()
+                vh.free()
+                us, vh = us2, vh2
+            prv = qtnh.contract(self.sites[q - 1], us, [2], [0])
+            us.free()
+            self._set(q, vh)
+            self._set(q - 1, prv)
+        self.canonicalize(first)
+        return self
+
     def to_statevector(self) -> np.ndarray:
         """mps_to_statevector, qubit 0 most significant; n <= 26."""
         if self.n > 26:
@@ -324,6 +431,24 @@ class MPS:
     def free(self):
         for t in self.sites:
             t.free()
+
+
+def mpo_from_operator(op: np.ndarray, k: int, d: int = 2) -> List[np.ndarray]:
+    """Exact k-site MPO (wl, d_out, d_in, wr) of a d^k x d^k operator (row = output,
+    site 0 most significant) by successive SVDs on the host (small operators)."""
+    t = np.asarray(op, dtype=np.complex128).reshape([d] * (2 * k))
+    # interleave (out_i, in_i) per site
+    t = t.transpose([x for i in range(k) for x in (i, k + i)])
+    sites, wl = [], 1
+    rest = t.reshape(wl * d * d, -1)
+    for i in range(k - 1):
+        u, s, vh = np.linalg.svd(rest, full_matrices=False)
+        r = int(np.sum(s > 1e-14 * s[0])) if s.size else 0
+        sites.append(u[:, :r].reshape(wl, d, d, r))
+        rest = (s[:r, None] * vh[:r]).reshape(r * d * d, -1)
+        wl = r
+    sites.append(rest.reshape(wl, d, d, 1))
+    return sites
 
 
 class _DevView:

@@ -195,3 +195,110 @@ def test_sample_requires_normalised_state():
         return e
 
     assert isinstance(run_collect(World(1), body), qtnh.PreconditionError)
+
+
+def dense_apply(sv, n, targets, gate):
+    """Apply a gate on `targets` (qubit 0 most significant) to a dense statevector."""
+    k = len(targets)
+    t = sv.reshape([2] * n)
+    g = gate.reshape([2] * (2 * k))
+    t = np.tensordot(g, t, axes=(list(range(k, 2 * k)), targets))
+    rest = [q for q in range(n) if q not in targets]
+    order = list(targets) + rest
+    return np.transpose(t, np.argsort(order)).reshape(-1)
+
+
+@pytest.mark.parametrize("targets", [[2], [1, 2], [1, 3], [0, 2, 5], [4, 5]])
+def test_apply_raw_gate_non_adjacent_vs_dense(targets):
+    k = len(targets)
+    gate = circuits.rng_normals(30 + k, 4**k).reshape(2**k, 2**k)
+    gate, _ = np.linalg.qr(gate)  # unitary
+
+    def body(rk):
+        m = MPS.random(rk, 6, 4, seed=12, chi=64)
+        before = m.to_statevector()
+        m.apply_gate_sites(targets, gate)
+        after = m.to_statevector()
+        centre = m.centre
+        m.free()
+        return before, after, centre
+
+    before, after, centre = run_collect(World(1), body)
+    assert rel_l2(after, dense_apply(before, 6, targets, gate)) < 1e-10
+    assert centre == targets[0]
+
+
+def test_apply_raw_gate_identity_and_errors():
+    def body(rk):
+        m = MPS.random(rk, 5, 4, seed=3, chi=16)
+        before = m.to_statevector()
+        m.apply_gate_sites([1, 3], np.eye(4))
+        after = m.to_statevector()
+        errs = []
+        for t, g in (([3, 1], np.eye(4)), ([1, 2], np.eye(2))):
+            try:
+                m.apply_gate_sites(t, g)
+            except qtnh.InvalidArgument as e:
+                errs.append(e)
+        m.free()
+        return before, after, errs
+
+    before, after, errs = run_collect(World(1), body)
+    assert rel_l2(after, before) < 1e-12
+    assert len(errs) == 2
+
+
+@pytest.mark.parametrize("first,k", [(0, 2), (2, 3), (1, 4)])
+def test_apply_mpo_vs_dense(first, k):
+    from paper_2505_06119_b200.mps import mpo_from_operator
+    op = circuits.rng_normals(50 + k, 4**k).reshape(2**k, 2**k)
+    mpo = mpo_from_operator(op, k)
+
+    def body(rk):
+        m = MPS.random(rk, 6, 4, seed=21, chi=64)
+        before = m.to_statevector()
+        m.apply_mpo(mpo, first)
+        after = m.to_statevector()
+        centre = m.centre
+        m.free()
+        return before, after, centre
+
+    before, after, centre = run_collect(World(1), body)
+    assert rel_l2(after, dense_apply(before, 6, list(range(first, first + k)), op)) < 1e-9
+    assert centre == first
+
+
+def test_apply_mpo_fsim_phase_and_identity():
+    """identity MPO leaves the state; fSim on |11> gives e^{-i pi/6}."""
+    from paper_2505_06119_b200.mps import mpo_from_operator
+
+    def body(rk):
+        m = MPS.bitstring(rk, [1, 1], 4)
+        m.apply_mpo(mpo_from_operator(circuits.FSIM, 2))
+        sv = m.to_statevector()
+        m.free()
+        r = MPS.random(rk, 4, 2, seed=8, chi=8)
+        before = r.to_statevector()
+        r.apply_mpo(mpo_from_operator(np.eye(4), 2), 1)
+        after = r.to_statevector()
+        r.free()
+        return sv, before, after
+
+    sv, before, after = run_collect(World(1), body)
+    assert abs(sv[3] - np.exp(-1j * np.pi / 6)) < 1e-12 and np.allclose(sv[:3], 0)
+    assert rel_l2(after, before) < 1e-12
+
+
+def test_truncated_mpo_lowers_norm():
+    from paper_2505_06119_b200.mps import mpo_from_operator
+    op, _ = np.linalg.qr(circuits.rng_normals(77, 64).reshape(8, 8))
+
+    def body(rk):
+        m = MPS.random(rk, 8, 4, seed=31, chi=4)
+        m.apply_mpo(mpo_from_operator(op, 3), 2)
+        out = (m.norm2(), m.log_fidelity, max(m.bond_dims()))
+        m.free()
+        return out
+
+    n2, logf, bmax = run_collect(World(1), body)
+    assert n2 < 1.0 and logf < 0.0 and bmax <= 4
