@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
-from typing import List, Tuple
+from typing import List, Sequence, Tuple
 
 import numpy as np
 
@@ -118,4 +118,94 @@ def apply_qft_fused(state: "qtnh.Tensor", n: int, swaps: bool = True) -> "qtnh.T
     if swaps:
         for j in range(n // 2):
             qtnh.swap_indices(state, j, n - 1 - j)
+    return state
+
+
+# ---- gate fusion (grouping gates cuts state passes) -------------------
+def _embed(block_qubits: List[int], gate_qubits: Sequence[int], g: np.ndarray) -> np.ndarray:
+    """The 2^k x 2^k matrix of gate g (on gate_qubits, first most significant) acting on
+    the block's qubits (sorted, first most significant)."""
+    k, kg = len(block_qubits), len(gate_qubits)
+    t = np.eye(2**k, dtype=np.complex128).reshape([2] * (2 * k))
+    pos = [block_qubits.index(q) for q in gate_qubits]
+    gt = np.asarray(g, dtype=np.complex128).reshape([2] * (2 * kg))
+    # out[o..] = sum_i g[o_pos, i_pos] t[i_pos..]
+    t = np.tensordot(gt, t, axes=(list(range(kg, 2 * kg)), pos))
+    rest = [a for a in range(2 * k) if a not in pos]
+    order = pos + rest  # current axis order of t in terms of original axes
+    return np.transpose(t, np.argsort(order)).reshape(2**k, 2**k)
+
+
+class FusedGate:
+    __slots__ = ("qubits", "matrix", "diagonal", "count")
+
+    def __init__(self, qubits, matrix, count):
+        self.qubits = list(qubits)
+        self.matrix = matrix
+        self.count = count
+        off = matrix - np.diag(np.diag(matrix))
+        self.diagonal = not np.any(off)
+
+
+def fuse_gates(gates: Sequence[Tuple[Sequence[int], np.ndarray]], max_qubits: int = 4) -> List[FusedGate]:
+    """Group a gate sequence into blocks of at most `max_qubits` qubits (the dense gate
+    kernel's D <= 16), preserving the circuit's action: every qubit belongs to at most
+    one open block; a gate merges all open blocks it touches when the union fits,
+    otherwise those blocks are emitted and the gate opens a new block. Blocks on
+    disjoint qubits commute, so emission order only follows shared qubits. Each
+    fused block costs one state pass instead of one per gate (diagonal blocks touch
+    only their non-unit entries)."""
+    out: List[FusedGate] = []
+    open_of: dict = {}  # qubit -> block id
+    blocks: dict = {}   # id -> [qubits(sorted), matrix, count]
+    nid = 0
+
+    def close(bid):
+        qs, m, c = blocks.pop(bid)
+        for q in qs:
+            open_of.pop(q, None)
+        out.append(FusedGate(qs, m, c))
+
+    for qs, g in gates:
+        qs = [int(q) for q in qs]
+        if len(set(qs)) != len(qs):
+            raise ValueError("gate with repeated qubits")
+        touching = sorted({open_of[q] for q in qs if q in open_of})
+        union = sorted(set(qs).union(*[blocks[b][0] for b in touching]))
+        if len(qs) > max_qubits:
+            for b in touching:
+                close(b)
+            out.append(FusedGate(qs, np.asarray(g, dtype=np.complex128).reshape(2 ** len(qs), -1), 1))
+            continue
+        if len(union) <= max_qubits:
+            m = np.eye(2 ** len(union), dtype=np.complex128)
+            c = 0
+            for b in touching:  # disjoint open blocks commute: any order
+                bq, bm, bc = blocks.pop(b)
+                m = _embed(union, bq, bm) @ m
+                c += bc
+            m = _embed(union, qs, g) @ m
+            blocks[nid] = [union, m, c + 1]
+            for q in union:
+                open_of[q] = nid
+            nid += 1
+        else:
+            for b in touching:
+                close(b)
+            blocks[nid] = [sorted(qs), _embed(sorted(qs), qs, g), 1]
+            for q in qs:
+                open_of[q] = nid
+            nid += 1
+    for b in sorted(blocks):
+        close(b)
+    return out
+
+
+def apply_fused(state: "qtnh.Tensor", fused: Sequence[FusedGate]) -> "qtnh.Tensor":
+    """Apply fused blocks with the dense (D <= 16) or diagonal gate kernels."""
+    for f in fused:
+        if f.diagonal:
+            qtnh.apply_gate(state, f.qubits, np.diag(f.matrix).copy(), diagonal=True)
+        else:
+            qtnh.apply_gate(state, f.qubits, f.matrix.reshape(-1))
     return state

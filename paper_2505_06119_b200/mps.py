@@ -303,7 +303,7 @@ class MPS:
                 rest.free()
                 u, rest = u2, r2
             self._set(q, u)
-            theta = self._reshape(rest, [rest.shape().dims[0]] + list(rest.shape().dims[1:]))
+            theta = rest
         self._set(last, theta)
         for q in range(last, first, -1):
             us, _, vh = qtnh.svd(self.sites[q], [0], [1, 2], absorb=ABSORB_LEFT)
