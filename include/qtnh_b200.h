@@ -147,6 +147,14 @@ int qtnh_tensor_upload_local(qtnh_tensor_t t, const double* host);
 /* Span-collective gather of the full global vector into `host` (total_size complex)
  * on every span rank (tensor.hpp:341-371). */
 int qtnh_tensor_to_global(qtnh_tensor_t t, double* host);
+/* QTNHTEN1 files (tensor.hpp:373-446), byte-identical to the reference's. Save is
+ * span-collective (Tensor::save(path), tensor.hpp:388-397): the first span rank
+ * writes the header, every canonical holder writes its own block at its offset
+ * straight from HBM (no gather). Load (Tensor::load(Rank&, path), tensor.hpp:
+ * 399-446) reads only this rank's block; dense / symmetric variants (0, 1) --
+ * others return QTNH_E_INVALID_ARGUMENT and are materialised by the host layer. */
+int qtnh_tensor_save(qtnh_tensor_t t, const char* path);
+int qtnh_tensor_load(qtnh_rank_t r, const char* path, qtnh_tensor_t* out);
 
 /* ---- structural ops (ops.hpp) --------------------------------------------- */
 int qtnh_permute(qtnh_tensor_t t, const int* perm, int new_split, qtnh_tensor_t* out);

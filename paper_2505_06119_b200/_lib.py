@@ -65,6 +65,8 @@ _SIGS = {
     "qtnh_tensor_download_local_async": (i32, [vp, vp]),
     "qtnh_tensor_upload_local": (i32, [vp, vp]),
     "qtnh_tensor_to_global": (i32, [vp, vp]),
+    "qtnh_tensor_save": (i32, [vp, C.c_char_p]),
+    "qtnh_tensor_load": (i32, [vp, C.c_char_p, C.POINTER(vp)]),
     "qtnh_permute": (i32, [vp, P_i32, i32, C.POINTER(vp)]),
     "qtnh_rebcast": (i32, [vp, P_i64, C.POINTER(vp)]),
     "qtnh_scatter_index": (i32, [vp, i32, C.POINTER(vp)]),

@@ -404,6 +404,21 @@ int qtnh_tensor_to_global(qtnh_tensor_t t, double* host) {
   });
 }
 
+int qtnh_tensor_save(qtnh_tensor_t t, const char* path) {
+  return guard([&] {
+    need(path, "path");
+    op_save(*impl_of(t), path);
+  });
+}
+
+int qtnh_tensor_load(qtnh_rank_t r, const char* path, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(path, "path");
+    need(out, "out");
+    *out = wrap(op_load(ctx_of(r), path));
+  });
+}
+
 // ---- ops --------------------------------------------------------------------------
 int qtnh_permute(qtnh_tensor_t t, const int* perm, int new_split, qtnh_tensor_t* out) {
   return guard([&] {

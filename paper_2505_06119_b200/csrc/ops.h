@@ -2,6 +2,7 @@
 #pragma once
 
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "runtime.h"
@@ -47,6 +48,8 @@ TP op_slice_local(const TP& t, const std::vector<Dim>& nl);                // op
 TP op_pad_local(const TP& t, const std::vector<Dim>& nl);                  // ops.hpp:201
 TP op_scale(const TP& t, double re, double im, bool conj);                 // ops.hpp:147-161
 void op_to_global(const TensorImpl& t, double* host);                      // tensor.hpp:341
+void op_save(const TensorImpl& t, const std::string& path);                // tensor.hpp:388-397
+TP op_load(RankCtx& r, const std::string& path);                           // tensor.hpp:399-446 (dense)
 
 // Contraction with SPEC.md:408 result order (see qtnh_b200.h).
 TP op_contract(const TP& a, const TP& b, const std::vector<int>& apos, const std::vector<int>& bpos);

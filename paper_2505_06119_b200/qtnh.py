@@ -408,21 +408,9 @@ class Tensor:
     def save(self, path: str) -> None:
         """Span-collective save in the reference's QTNHTEN1 format (dense variant):
         magic, u32 variant, u32 rank, u32 split, i64 stretch/cycles/offset, i64 dims,
-        u64 payload count, LE f64 (re, im) pairs in global row-major order; only the
-        first span rank writes."""
-        import struct
-
-        g = self.to_global_vector()
-        if not self.in_span() or self.ctx_rank.rank() != self.dist().offset:
-            return
-        sh, d = self.shape(), self.dist()
-        with open(path, "wb") as f:
-            f.write(self._MAGIC)
-            f.write(struct.pack("<III", 0, sh.n_idx(), sh.split))
-            f.write(struct.pack("<qqq", d.stretch, d.cycles, d.offset))
-            f.write(struct.pack("<%dq" % sh.n_idx(), *sh.dims))
-            f.write(struct.pack("<Q", g.size))
-            f.write(np.ascontiguousarray(g, dtype="<c16").tobytes())
+        u64 payload count, LE f64 (re, im) pairs in global row-major order. Every
+        canonical holder writes its block straight from HBM (qtnh_tensor_save)."""
+        check(lib.qtnh_tensor_save(self._h, os.fsencode(path)))
 
     @staticmethod
     def load(rank: "Rank", path: str) -> "Tensor":
@@ -431,6 +419,13 @@ class Tensor:
         variants are materialised densely (tensor.hpp:282-296)."""
         import struct
 
+        with open(path, "rb") as f:
+            head = f.read(12)
+        if head[:8] == Tensor._MAGIC and len(head) == 12 and struct.unpack_from("<I", head, 8)[0] in (0, 1):
+            # dense / symmetric payload: each rank reads only its block into HBM
+            h = C.c_void_p()
+            check(lib.qtnh_tensor_load(rank._h, os.fsencode(path), C.byref(h)))
+            return Tensor(rank, h)
         with open(path, "rb") as f:
             blob = f.read()
         if blob[:8] != Tensor._MAGIC:
