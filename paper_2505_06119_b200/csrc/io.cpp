@@ -6,10 +6,9 @@
 // i.e. the blocks concatenated in block order (tensor.hpp:341-371), so here every
 // canonical holder writes ITS block at its byte offset (pwrite) and every span rank
 // reads only its own block (pread): no gather, no global host copy, the files are
-// byte-identical. Blocks move through two device + two pinned staging chunks so
-// the D2H/H2D copy of one chunk overlaps the file I/O of the other; the save path
-// canonicalises zeros on the device like the reference's visit_my_nonzeros
-// (tensor.hpp:345-350, zero-skipping into a zeroed vector).
+// byte-identical. Blocks move through two pinned staging chunks so the D2H/H2D
+// copy of one chunk overlaps the file I/O of the other. Values are raw (signed
+// zeros kept), as the reference's dense visit (tensor.hpp:300-311) writes them.
 #include <fcntl.h>
 #include <sys/stat.h>
 #include <unistd.h>
@@ -17,7 +16,6 @@
 #include <cstring>
 
 #include "ops.h"
-#include "strided_copy.h"
 
 namespace qtnhb {
 
@@ -103,7 +101,6 @@ void op_save(const TensorImpl& t, const std::string& path) {
     f.fd = ::open(path.c_str(), O_WRONLY);
     if (f.fd < 0) throw Status(QTNH_E_RUNTIME, "cannot open " + path + " for writing");
     const Dim ch = std::min(nl, kChunk);
-    DevBuf dstage(static_cast<size_t>(2 * ch) * 16, r);
     Pinned host(static_cast<size_t>(2 * ch) * 16);
     cudaEvent_t ev[2];
     for (auto& e : ev) QTNH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -112,13 +109,8 @@ void op_save(const TensorImpl& t, const std::string& path) {
     auto issue = [&](Dim c) {
       const int s = static_cast<int>(c & 1);
       const Dim n = std::min(ch, nl - c * ch);
-      CopyBox b;
-      b.dims = {n};
-      b.in_stride = {1};
-      b.out_stride = {1};
-      char* ds = static_cast<char*>(dstage.ptr) + s * ch * 16;
-      strided_copy(static_cast<const char*>(t.data()) + c * ch * 16, ds, b, true, r.stream);
-      QTNH_CUDA(cudaMemcpyAsync(static_cast<char*>(host.p) + s * ch * 16, ds, n * 16, cudaMemcpyDeviceToHost,
+      QTNH_CUDA(cudaMemcpyAsync(static_cast<char*>(host.p) + s * ch * 16,
+                                static_cast<const char*>(t.data()) + c * ch * 16, n * 16, cudaMemcpyDeviceToHost,
                                 r.stream));
       QTNH_CUDA(cudaEventRecord(ev[s], r.stream));
     };

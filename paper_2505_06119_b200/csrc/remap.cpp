@@ -351,16 +351,10 @@ void op_to_global(const TensorImpl& t, double* host) {
   if (!t.in_span) return;
   RankCtx& r = *t.rank;
   Dim nl = t.shape.local_size(), nd = t.shape.dist_size();
-  // (±0, ±0) -> (+0, +0) like the reference's zero-skipping fill into a zeroed
-  // vector (tensor.hpp:345-350)
-  CopyBox flat1;
-  flat1.in_stride = {1};
-  flat1.out_stride = {1};
+  // raw values: the reference visits every dense element, zeros included
+  // (visit_my_nonzeros, tensor.hpp:300-311), so signed zeros survive
   if (t.span() == 1) {
-    DevBuf c(static_cast<size_t>(nl) * 16, r);
-    flat1.dims = {nl};
-    strided_copy(t.data(), c.ptr, flat1, true, r.stream);
-    QTNH_CUDA(cudaMemcpyAsync(host, c.ptr, nl * 16, cudaMemcpyDeviceToHost, r.stream));
+    QTNH_CUDA(cudaMemcpyAsync(host, t.data(), nl * 16, cudaMemcpyDeviceToHost, r.stream));
     QTNH_CUDA(cudaStreamSynchronize(r.stream));
     return;
   }
@@ -371,8 +365,6 @@ void op_to_global(const TensorImpl& t, double* host) {
   for (Dim b = 0; b < nd; ++b) recvs.push_back({t.dist.canonical(b), b * nl, nl});
   DevBuf all(static_cast<size_t>(nd * nl) * 16, r);
   exchange(r, members, t.data(), sends, all.ptr, recvs);
-  flat1.dims = {nd * nl};
-  strided_copy(all.ptr, all.ptr, flat1, true, r.stream);
   QTNH_CUDA(cudaMemcpyAsync(host, all.ptr, nd * nl * 16, cudaMemcpyDeviceToHost, r.stream));
   QTNH_CUDA(cudaStreamSynchronize(r.stream));
 }
