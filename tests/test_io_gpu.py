@@ -71,6 +71,7 @@ def test_device_save_load_matches_reference(tmp_path, dims, split, dist, world):
     def body(rk):
         t = Tensor.from_global(rk, IndexTuple(dims, split), DistParams(*dist), g)
         t.save(ours)
+        rk.barrier()  # save is span-collective; ranks outside the span must not read early
         u = Tensor.load(rk, ours)
         out = u.to_global_vector() if u.in_span() else None
         return out
