@@ -357,14 +357,14 @@ namespace {
 // ---- cache-blocked QFT ---------------------------------------------------------------
 // Layer j (bit t = n-1-j): H on bit t, then exp(i pi v / 2^t) on amplitudes with
 // bit t set, v = the bits below t. Layers run in order j = 0..n-1.
-//  * k_qft_low: the lowest L layers touch only the lowest L bits, so one pass over
-//    contiguous 2^L-element chunks staged in shared memory applies all of them
-//    (twiddles e^{i pi v / 2^t}, v < 2^t, tabulated once per CTA).
+//  * k_qft_low3: the lowest L layers touch only the lowest L bits, so one pass over
+//    contiguous chunks staged in shared memory applies all of them (twiddles
+//    e^{i pi v / 2^t}, v < 2^t, tabulated once per CTA).
 //  * k_qft_group: g consecutive upper layers (bits T..B, B >= L) in registers: a
 //    thread owns the 2^g amplitudes that differ in those bits; the phase splits
 //    into a per-layer table e^{i pi k / 2^u} (k < 2^u, u = t - B) and one
 //    sincospi of the fixed low bits per layer.
-//  * k_bitrev: the final SWAP network reverses the bit order -- one in-place pass
+//  * k_bitrev2: the final SWAP network reverses the bit order -- one in-place pass
 //    that exchanges 32 x 32 tiles (a, m, b) <-> (rev b, rev m, rev a).
 constexpr int kQftLowMax = 11;
 
@@ -372,44 +372,9 @@ __device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
-__global__ void __launch_bounds__(256) k_qft_low(double2* __restrict__ psi, int64_t n_chunks, int L) {
-  extern __shared__ double2 smq[];
-  double2* data = smq;             // 2^L amplitudes
-  double2* tw = smq + (1 << L);    // tw[2^t + v] = e^{i pi v / 2^t}, t < L
-  const int C = 1 << L, H = C >> 1;
-  const double r = 0.70710678118654752440;
-  for (int e = threadIdx.x; e < C; e += blockDim.x) {
-    if (e == 0) continue;
-    int t = 31 - __clz(e);
-    int v = e - (1 << t);
-    double sn, cs;
-    sincospi(static_cast<double>(v) * ldexp(1.0, -t), &sn, &cs);
-    tw[e] = make_double2(cs, sn);
-  }
-  for (int64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
-    double2* g = psi + ch * C;
-    __syncthreads();
-    for (int e = threadIdx.x; e < C; e += blockDim.x) data[e] = g[e];
-    __syncthreads();
-    for (int t = L - 1; t >= 0; --t) {
-      const int lo_mask = (1 << t) - 1;
-      for (int p = threadIdx.x; p < H; p += blockDim.x) {
-        int lo = p & lo_mask;
-        int i0 = ((p >> t) << (t + 1)) | lo, i1 = i0 | (1 << t);
-        double2 a0 = data[i0], a1 = data[i1];
-        double2 y0 = make_double2(r * a0.x + r * a1.x, r * a0.y + r * a1.y);
-        double2 d = make_double2(r * a0.x - r * a1.x, r * a0.y - r * a1.y);
-        data[i0] = y0;
-        data[i1] = t > 0 ? cmul2(d, tw[(1 << t) + lo]) : d;
-      }
-      __syncthreads();
-    }
-    for (int e = threadIdx.x; e < C; e += blockDim.x) g[e] = data[e];
-  }
-}
 
 
-// Low layers, version 2: the chunk sits in shared memory and the L layers run in
+// Low layers: the chunk sits in shared memory and the L layers run in
 // rounds of up to 4 bits; a thread owns the 2^g amplitudes of one fiber in
 // registers for a round, so a round costs one shared load + store per amplitude
 // and one twiddle lookup per amplitude and layer, with one barrier per round.
@@ -453,49 +418,12 @@ __device__ __forceinline__ void qft_low_round(double2* __restrict__ data, const 
   }
 }
 
-__global__ void __launch_bounds__(128) k_qft_low2(double2* __restrict__ psi, int64_t n_chunks, int L) {
-  extern __shared__ double2 smq2[];
-  double2* data = smq2;
-  double2* tw = smq2 + (1 << L);
-  const int C = 1 << L;
-  for (int e = threadIdx.x; e < C; e += blockDim.x) {
-    if (e == 0) continue;
-    int t = 31 - __clz(e);
-    int v = e - (1 << t);
-    double sn, cs;
-    sincospi(static_cast<double>(v) * ldexp(1.0, -t), &sn, &cs);
-    tw[e] = make_double2(cs, sn);
-  }
-  for (int64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
-    double2* g = psi + ch * C;
-    __syncthreads();
-    for (int e = threadIdx.x; e < C; e += blockDim.x) data[swz8(e)] = g[e];
-    __syncthreads();
-    for (int T = L - 1; T >= 0;) {
-      int gg = T + 1 >= 4 ? 4 : T + 1;
-      int B = T - gg + 1;
-      switch (gg) {
-        case 4: qft_low_round<4>(data, tw, L, B); break;
-        case 3: qft_low_round<3>(data, tw, L, B); break;
-        case 2: qft_low_round<2>(data, tw, L, B); break;
-        default: qft_low_round<1>(data, tw, L, B); break;
-      }
-      __syncthreads();
-      T = B - 1;
-    }
-    const double sc = ldexp(1.0, -(L / 2)) * (L & 1 ? 0.70710678118654752440 : 1.0);
-    for (int e = threadIdx.x; e < C; e += blockDim.x) {
-      double2 v = data[swz8(e)];
-      g[e] = make_double2(v.x * sc, v.y * sc);
-    }
-  }
-}
 
-// Version 3: the same rounds, with the chunks streamed through two shared-memory
+// k_qft_low3 runs these rounds with the chunks streamed through two shared-memory
 // buffers by cp.async (16-byte LDGSTS, swizzled destination): chunk c+1 is in
 // flight while chunk c is transformed and written back, so the global loads no
-// longer serialise behind the shared-memory rounds (v2 was long-scoreboard bound
-// at ~25% of HBM bandwidth).
+// longer serialise behind the shared-memory rounds (the single-buffer version was
+// long-scoreboard bound at ~25% of HBM bandwidth).
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
@@ -603,33 +531,12 @@ __device__ __forceinline__ double2 canon2(double2 v) {
 }
 
 // n >= 10: x = (a: top 5 bits, m: middle n-10 bits, b: low 5 bits).
-__global__ void __launch_bounds__(256) k_bitrev(double2* __restrict__ psi, int n, int64_t n_mid) {
-  __shared__ double2 t1[32][33], t2[32][33];
-  const int mbits = n - 10;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  for (int64_t m = blockIdx.x; m < n_mid; m += gridDim.x) {
-    int64_t mr = static_cast<int64_t>(rev_bits64(static_cast<uint64_t>(m), mbits));
-    if (mr < m) continue;  // the pair is handled by its smaller member
-    __syncthreads();
-    for (int a = ty; a < 32; a += 8) {
-      t1[a][tx] = psi[(int64_t(a) << (n - 5)) | (m << 5) | tx];
-      t2[a][tx] = psi[(int64_t(a) << (n - 5)) | (mr << 5) | tx];
-    }
-    __syncthreads();
-    for (int a = ty; a < 32; a += 8) {
-      int ra = rev_bits(a, 5), rb = rev_bits(tx, 5);
-      // new (a, m, b) = old (rev b, rev m, rev a) = t2[rev b][rev a]
-      psi[(int64_t(a) << (n - 5)) | (m << 5) | tx] = canon2(t2[rb][ra]);
-      if (mr != m) psi[(int64_t(a) << (n - 5)) | (mr << 5) | tx] = canon2(t1[rb][ra]);
-    }
-  }
-}
 
-// Version 2 of the in-place bit reversal: the two 32 x 32 tiles of a pair are
+// In-place bit reversal: the two 32 x 32 tiles of a pair are
 // staged by cp.async into a double buffer (the next pair is in flight while this
 // one is written back), and the tile columns are XOR-swizzled with bits 2..4 of
 // the row so the bit-reversed column reads (lanes -> rows rev(tx)) hit eight
-// distinct 16-byte bank groups (v1's padded layout was 4-way conflicted).
+// distinct 16-byte bank groups (a padded layout is 4-way conflicted).
 __device__ __forceinline__ int bswz(int row, int col) { return row * 32 + (col ^ ((row >> 2) & 7)); }
 
 __global__ void __launch_bounds__(256) k_bitrev2(double2* __restrict__ psi, int n, int64_t n_mid) {
@@ -910,36 +817,20 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
   if (top >= 0) {
     // remaining layers: bits top..0 with top = L - 1 (all of the low chunk)
     int Lc = top + 1;
-    int64_t n_chunks = int64_t(1) << (nb - Lc);
-    static const bool v2 = [] {
-      const char* e = std::getenv("QTNH_QFT_LOW");
-      return e && e[0] == '2';
+    const int S = std::max(Lc, std::min(nb, kQftLowMax));
+    const int64_t n_chunks = int64_t(1) << (nb - S);
+    size_t smem = ((static_cast<size_t>(2) << S) + (size_t(1) << Lc)) * sizeof(double2);  // 2 buffers + twiddles
+    static bool attr = [] {
+      cudaFuncSetAttribute(k_qft_low3, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 16 << kQftLowMax);
+      return true;
     }();
-    if (v2) {
-      size_t smem = (static_cast<size_t>(2) << Lc) * sizeof(double2);  // data + twiddles
-      static bool attr2 = [] {
-        cudaFuncSetAttribute(k_qft_low2, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16 << kQftLowMax);
-        return true;
-      }();
-      (void)attr2;
-      int grid = static_cast<int>(std::min<int64_t>(n_chunks, 148 * 8));
-      k_qft_low2<<<grid, 128, smem, st>>>(p, n_chunks, Lc);
-    } else {
-      const int S = std::max(Lc, std::min(nb, kQftLowMax));
-      n_chunks = int64_t(1) << (nb - S);
-      size_t smem = ((static_cast<size_t>(2) << S) + (size_t(1) << Lc)) * sizeof(double2);  // 2 buffers + twiddles
-      static int per_sm = [] {
-        cudaFuncSetAttribute(k_qft_low3, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 16 << kQftLowMax);
-        return 0;
-      }();
-      int dev = 0, occ = 0, sms = 0;
-      QTNH_CUDA(cudaGetDevice(&dev));
-      QTNH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qft_low3, 128, smem));
-      (void)per_sm;
-      int grid = static_cast<int>(std::min<int64_t>(n_chunks, (int64_t)sms * std::max(1, occ)));
-      k_qft_low3<<<grid, 128, smem, st>>>(p, n_chunks, S, Lc);
-    }
+    (void)attr;
+    int dev = 0, occ = 0, sms = 0;
+    QTNH_CUDA(cudaGetDevice(&dev));
+    QTNH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qft_low3, 128, smem));
+    int grid = static_cast<int>(std::min<int64_t>(n_chunks, (int64_t)sms * std::max(1, occ)));
+    k_qft_low3<<<grid, 128, smem, st>>>(p, n_chunks, S, Lc);
     QTNH_LAUNCH_CHECK();
   }
 }
@@ -947,27 +838,18 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
 void bitrev_local(void* data, int nb, cudaStream_t st) {
   if (nb < 10) throw_invalid("in-place bit reversal needs at least 10 local qubits");
   int64_t n_mid = int64_t(1) << (nb - 10);
-  static const bool v1 = [] {
-    const char* e = std::getenv("QTNH_BITREV");
-    return e && e[0] == '1';
+  const size_t smem = 4 * 1024 * sizeof(double2);  // 2 stages x 2 tiles
+  static bool attr = [] {
+    cudaFuncSetAttribute(k_bitrev2, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    return true;
   }();
-  if (v1) {
-    int grid = static_cast<int>(std::min<int64_t>(n_mid, 148 * 8));
-    k_bitrev<<<grid, 256, 0, st>>>(static_cast<double2*>(data), nb, n_mid);
-  } else {
-    const size_t smem = 4 * 1024 * sizeof(double2);  // 2 stages x 2 tiles
-    static bool attr = [] {
-      cudaFuncSetAttribute(k_bitrev2, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      return true;
-    }();
-    (void)attr;
-    int dev = 0, occ = 0, sms = 0;
-    QTNH_CUDA(cudaGetDevice(&dev));
-    QTNH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bitrev2, 256, smem));
-    int grid = static_cast<int>(std::min<int64_t>(n_mid, (int64_t)sms * std::max(1, occ)));
-    k_bitrev2<<<grid, 256, smem, st>>>(static_cast<double2*>(data), nb, n_mid);
-  }
+  (void)attr;
+  int dev = 0, occ = 0, sms = 0;
+  QTNH_CUDA(cudaGetDevice(&dev));
+  QTNH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bitrev2, 256, smem));
+  int grid = static_cast<int>(std::min<int64_t>(n_mid, (int64_t)sms * std::max(1, occ)));
+  k_bitrev2<<<grid, 256, smem, st>>>(static_cast<double2*>(data), nb, n_mid);
   QTNH_LAUNCH_CHECK();
 }
 
