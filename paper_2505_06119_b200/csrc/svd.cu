@@ -74,110 +74,11 @@ __global__ void k_svd_init(const double2* __restrict__ a, double2* __restrict__ 
   }
 }
 
-// ---- Gram partials: part[mat][pair][split] = X_pair[:, cols] X_pair[:, cols]^H ------
-__global__ void __launch_bounds__(256) k_svd_gram(const double2* __restrict__ wk, double2* __restrict__ part,
-                                                  const int* __restrict__ tab, int round, int npairs, int splits,
-                                                  int64_t rp, int64_t L, int64_t qw) {
-  const int pair = blockIdx.x, split = blockIdx.y, mat = blockIdx.z;
-  const int64_t W = L + qw;
-  const int* pr = tab + (static_cast<int64_t>(round) * npairs + pair) * 2;
-  const int bi = pr[0], bj = pr[1];
-  const double2* K = wk + static_cast<int64_t>(mat) * rp * W;
-  __shared__ double2 xs[kP2][kGramCols + 1];
-  const int tid = threadIdx.x;
-  // each thread owns 4 of the 32 x 32 entries
-  double2 acc[4];
-  int ei[4], ej[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    int e = tid + u * 256;
-    ei[u] = e / kP2;
-    ej[u] = e % kP2;
-    acc[u] = make_double2(0.0, 0.0);
-  }
-  int64_t per = (L + splits - 1) / splits;
-  int64_t c0 = split * per, c1 = min(L, c0 + per);
-  for (int64_t cb = c0; cb < c1; cb += kGramCols) {
-    for (int e = tid; e < kP2 * kGramCols; e += 256) {
-      int r = e / kGramCols, c = e % kGramCols;
-      int64_t row = (r < kB ? bi * kB + r : bj * kB + (r - kB));
-      int64_t col = cb + c;
-      xs[r][c] = col < c1 ? K[row * W + col] : make_double2(0.0, 0.0);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      double re = acc[u].x, im = acc[u].y;
-      for (int c = 0; c < kGramCols; ++c) {
-        double2 x = xs[ei[u]][c], y = xs[ej[u]][c];  // x * conj(y)
-        re = fma(x.x, y.x, fma(x.y, y.y, re));
-        im = fma(x.y, y.x, fma(-x.x, y.y, im));
-      }
-      acc[u] = make_double2(re, im);
-    }
-    __syncthreads();
-  }
-  double2* out = part + ((static_cast<int64_t>(mat) * npairs + pair) * splits + split) * kP2 * kP2;
-#pragma unroll
-  for (int u = 0; u < 4; ++u) out[ei[u] * kP2 + ej[u]] = acc[u];
-}
-
 // ---- inner eigensolver: W with W^H G W diagonal; writes W^H ----------------------------
 __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
   // non-negative doubles order like their bit patterns
   atomicMax(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(__double_as_longlong(v)));
 }
-
-// ---- in-place row update: WK_pair <- W^H WK_pair -----------------------------------------
-__global__ void __launch_bounds__(256) k_svd_update(double2* __restrict__ wk, const double2* __restrict__ wh,
-                                                    const int* __restrict__ flags, const int* __restrict__ tab,
-                                                    int round, int npairs, int64_t rp, int64_t L, int64_t qw) {
-  const int pair = blockIdx.y, mat = blockIdx.z, tid = threadIdx.x;
-  const int64_t fidx = static_cast<int64_t>(mat) * npairs + pair;
-  if (!flags[fidx]) return;
-  const int64_t W = L + qw;
-  const int* pr = tab + (static_cast<int64_t>(round) * npairs + pair) * 2;
-  const int bi = pr[0], bj = pr[1];
-  double2* K = wk + static_cast<int64_t>(mat) * rp * W;
-  __shared__ double2 ws[kP2][kP2];
-  __shared__ double2 xs[kP2][kUpdCols];
-  const double2* Wh = wh + fidx * kP2 * kP2;
-  for (int e = tid; e < kP2 * kP2; e += 256) ws[e / kP2][e % kP2] = Wh[e];
-  for (int64_t cb = static_cast<int64_t>(blockIdx.x) * kUpdCols; cb < W; cb += static_cast<int64_t>(gridDim.x) * kUpdCols) {
-    for (int e = tid; e < kP2 * kUpdCols; e += 256) {
-      int r = e / kUpdCols, c = e % kUpdCols;
-      int64_t row = r < kB ? bi * kB + r : bj * kB + (r - kB);
-      int64_t col = cb + c;
-      xs[r][c] = col < W ? K[row * W + col] : make_double2(0.0, 0.0);
-    }
-    __syncthreads();
-    double2 y[kP2 * kUpdCols / 256];
-#pragma unroll
-    for (int u = 0; u < kP2 * kUpdCols / 256; ++u) {
-      int e = tid + u * 256;
-      int r = e / kUpdCols, c = e % kUpdCols;
-      double re = 0.0, im = 0.0;
-#pragma unroll 8
-      for (int k = 0; k < kP2; ++k) {
-        double2 w = ws[r][k], x = xs[k][c];
-        re = fma(w.x, x.x, fma(-w.y, x.y, re));
-        im = fma(w.x, x.y, fma(w.y, x.x, im));
-      }
-      y[u] = make_double2(re, im);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < kP2 * kUpdCols / 256; ++u) {
-      int e = tid + u * 256;
-      int r = e / kUpdCols, c = e % kUpdCols;
-      int64_t row = r < kB ? bi * kB + r : bj * kB + (r - kB);
-      int64_t col = cb + c;
-      if (col < W) K[row * W + col] = y[u];
-    }
-    __syncthreads();
-  }
-}
-
 
 // ---- block-size templated kernels (B rows per block, pair of 2B rows) ------------------
 // Dynamic shared memory: the pair's Gram matrix G and eigenvectors V (2B x 2B+1).
@@ -595,13 +496,6 @@ bool accumulate_q() {
   return v;
 }
 
-bool use_mma() {
-  static bool v = [] {
-    const char* e = std::getenv("QTNH_SVD_MMA");
-    return e ? std::atoi(e) != 0 : true;
-  }();
-  return v;
-}
 
 double tolerance() {
   static double v = [] {
@@ -648,7 +542,6 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   const bool acc_q = transpose || accumulate_q();
   const Dim qw = acc_q ? rp : 0;
   const Dim W = L + qw;
-  const bool mma = use_mma() || B != 16;
   // tournament table (circle method, block nblk2-1 fixed)
   std::vector<int> tab(static_cast<size_t>(rounds) * npairs * 2);
   for (int rd = 0; rd < rounds; ++rd)
@@ -716,14 +609,9 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
       QTNH_CUDA(cudaMemcpyAsync(thr_d.ptr, thr_h.data(), batch * sizeof(double), cudaMemcpyHostToDevice, st));
     }
     for (int rd = 0; rd < rounds; ++rd) {
-      if (mma)
-        k_svd_gram_mma_t<B><<<dim3(npairs, splits, static_cast<unsigned>(batch)), B * 8, 0, st>>>(
-            static_cast<const double2*>(wk.ptr), static_cast<double2*>(part.ptr), static_cast<const int*>(d_tab.ptr),
-            rd, npairs, splits, rp, L, qw);
-      else
-        k_svd_gram<<<dim3(npairs, splits, static_cast<unsigned>(batch)), 256, 0, st>>>(
-            static_cast<const double2*>(wk.ptr), static_cast<double2*>(part.ptr), static_cast<const int*>(d_tab.ptr),
-            rd, npairs, splits, rp, L, qw);
+      k_svd_gram_mma_t<B><<<dim3(npairs, splits, static_cast<unsigned>(batch)), B * 8, 0, st>>>(
+          static_cast<const double2*>(wk.ptr), static_cast<double2*>(part.ptr), static_cast<const int*>(d_tab.ptr),
+          rd, npairs, splits, rp, L, qw);
       QTNH_LAUNCH_CHECK();
       k_svd_eigen_t<B><<<dim3(npairs, static_cast<unsigned>(batch)), 256, eig_smem, st>>>(
             static_cast<const double2*>(part.ptr), static_cast<double2*>(whb.ptr), static_cast<int*>(flags.ptr),
@@ -731,14 +619,9 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
             static_cast<const double*>(floor_abs.ptr), stats ? static_cast<const double*>(thr_d.ptr) : nullptr,
             static_cast<double*>(offt.ptr));
       QTNH_LAUNCH_CHECK();
-      if (mma)
-        k_svd_update_mma_t<B><<<dim3(ctiles, npairs, static_cast<unsigned>(batch)), B * 8, upd_smem, st>>>(
-            static_cast<double2*>(wk.ptr), static_cast<const double2*>(whb.ptr), static_cast<const int*>(flags.ptr),
-            static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
-      else
-        k_svd_update<<<dim3(ctiles, npairs, static_cast<unsigned>(batch)), 256, 0, st>>>(
-            static_cast<double2*>(wk.ptr), static_cast<const double2*>(whb.ptr), static_cast<const int*>(flags.ptr),
-            static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
+      k_svd_update_mma_t<B><<<dim3(ctiles, npairs, static_cast<unsigned>(batch)), B * 8, upd_smem, st>>>(
+          static_cast<double2*>(wk.ptr), static_cast<const double2*>(whb.ptr), static_cast<const int*>(flags.ptr),
+          static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
       QTNH_LAUNCH_CHECK();
     }
     QTNH_CUDA(cudaMemcpyAsync(off_h.data(), offm.ptr, batch * sizeof(double), cudaMemcpyDeviceToHost, st));
