@@ -47,10 +47,11 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 }
 
 template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int BK_, int STAGES_, int MINB_, int WTM_ = 32,
-          int WTN_ = 32>
+          int WTN_ = 32, bool GAUSS_ = false>
 struct Cfg {
   static constexpr int BM = BM_, BN = BN_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, BK = BK_,
                        STAGES = STAGES_, MINB = MINB_;
+  static constexpr bool GAUSS = GAUSS_;  // 3 real products per complex MAC
   static constexpr int WTM = WTM_, WTN = WTN_, MI = WTM / 8, NJ = WTN / 8;  // warp tile
   static constexpr int THREADS = WARPS_M * WARPS_N * 32;
   static constexpr int PA = BM + 2;  // 16-B elements; = 2 (mod 8)
@@ -141,13 +142,17 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
   };
 
   constexpr int MI = G::MI, NJ = G::NJ;
-  double acc_re[MI][NJ][2], acc_im[MI][NJ][2];
+  // 4M: acc_re = Re, acc_im = Im. Gauss (3M): acc_re = sum a_re b_re, acc_im =
+  // sum a_im b_im, acc_s = sum (a_re + a_im)(b_re + b_im); Re = acc_re - acc_im,
+  // Im = acc_s - acc_re - acc_im.
+  double acc_re[MI][NJ][2], acc_im[MI][NJ][2], acc_s[G::GAUSS ? MI : 1][G::GAUSS ? NJ : 1][2];
 #pragma unroll
   for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
       acc_re[i][j][0] = acc_re[i][j][1] = 0.0;
       acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
+      if (G::GAUSS) acc_s[G::GAUSS ? i : 0][G::GAUSS ? j : 0][0] = acc_s[G::GAUSS ? i : 0][G::GAUSS ? j : 0][1] = 0.0;
     }
 
 #pragma unroll
@@ -178,20 +183,36 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
         b_im[j] = v.y;
         nb_im[j] = -v.y;
       }
+      if constexpr (G::GAUSS) {
+        double a_s[MI], b_s[NJ];
 #pragma unroll
-      for (int i = 0; i < MI; ++i)
+        for (int i = 0; i < MI; ++i) a_s[i] = a_re[i] + a_im[i];
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-          dmma(acc_re[i][j], a_re[i], b_re[j]);
-          dmma(acc_im[i][j], a_re[i], b_im[j]);
-        }
+        for (int j = 0; j < NJ; ++j) b_s[j] = b_re[j] + b_im[j];
 #pragma unroll
-      for (int i = 0; i < MI; ++i)
+        for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-          dmma(acc_re[i][j], a_im[i], nb_im[j]);
-          dmma(acc_im[i][j], a_im[i], b_re[j]);
-        }
+          for (int j = 0; j < NJ; ++j) {
+            dmma(acc_re[i][j], a_re[i], b_re[j]);
+            dmma(acc_im[i][j], a_im[i], b_im[j]);
+            dmma(acc_s[i][j], a_s[i], b_s[j]);
+          }
+      } else {
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) {
+            dmma(acc_re[i][j], a_re[i], b_re[j]);
+            dmma(acc_im[i][j], a_re[i], b_im[j]);
+          }
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) {
+            dmma(acc_re[i][j], a_im[i], nb_im[j]);
+            dmma(acc_im[i][j], a_im[i], b_re[j]);
+          }
+      }
     }
     // Refill the slot freed at the top barrier only after this slice's DMMAs are
     // queued: the (gather-table) address loads then stall the warp while the
@@ -203,6 +224,18 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
     }
   }
   cp_wait<0>();
+  if constexpr (G::GAUSS) {
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double rr = acc_re[i][j][h], ii = acc_im[i][j][h];
+          acc_re[i][j][h] = rr - ii;
+          acc_im[i][j][h] = acc_s[i][j][h] - rr - ii;
+        }
+  }
 
   // Epilogue: lane holds C[fr][2*fk + {0,1}] of each 8x8 sub-tile.
 #pragma unroll
@@ -263,6 +296,12 @@ __global__ void k_mixed_offsets(int64_t* __restrict__ out, int64_t count, const 
 using V4 = Cfg<64, 32, 2, 1, 8, 4, 4>;    // 64 thr, 4 CTA/SM: narrow N (<= 32)
 using V7 = Cfg<32, 64, 1, 2, 8, 3, 5>;    // 64 thr, 5 CTA/SM (<= 204 regs)
 using V12 = Cfg<32, 64, 2, 2, 8, 3, 4, 16, 32>;   // warp tile 16x32, 128 thr
+// Gauss (3M) candidates: 3 DMMAs per complex k-step instead of 4
+using G1 = Cfg<32, 64, 2, 2, 8, 3, 3, 16, 32, true>;
+using G2 = Cfg<32, 32, 2, 2, 8, 4, 5, 16, 16, true>;
+using G3 = Cfg<32, 64, 2, 2, 8, 3, 4, 16, 32, true>;
+using G4 = Cfg<64, 32, 2, 1, 8, 4, 3, 32, 32, true>;
+using G5 = Cfg<32, 64, 1, 2, 8, 3, 4, 32, 32, true>;
 
 int variant() {
   static int v = [] {
@@ -328,6 +367,11 @@ void zgemm(const void* a, const void* b, void* c, Dim m, Dim n, Dim k, cudaStrea
     case 4: return launch<V4>(A, B, Cp, m, n, k, st);
     case 7: return launch<V7>(A, B, Cp, m, n, k, st);
     case 12: return launch<V12>(A, B, Cp, m, n, k, st);
+    case 101: return launch<G1>(A, B, Cp, m, n, k, st);
+    case 102: return launch<G2>(A, B, Cp, m, n, k, st);
+    case 103: return launch<G3>(A, B, Cp, m, n, k, st);
+    case 104: return launch<G4>(A, B, Cp, m, n, k, st);
+    case 105: return launch<G5>(A, B, Cp, m, n, k, st);
     default: break;
   }
   if (n > 32) launch<V12>(A, B, Cp, m, n, k, st);
