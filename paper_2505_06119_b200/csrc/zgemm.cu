@@ -7,12 +7,16 @@
 // as DFMA but with 8x fewer issue slots per flop).
 //
 // C = A * B with A (M x K), B (K x N), C (M x N) row-major interleaved complex.
-// 4M formulation on real MMAs, keeping the algorithmic 8MNK flops:
-//   C_re += A_re B_re + A_im (-B_im),   C_im += A_re B_im + A_im B_re.
+// Default: Gauss / 3M formulation on real MMAs (3 products per complex MAC, the
+// tensor pipe being the bound):
+//   P1 += A_re B_re, P2 += A_im B_im, P3 += (A_re + A_im)(B_re + B_im);
+//   C_re = P1 - P2, C_im = P3 - P1 - P2.
+// The 4M form (C_re += A_re B_re + A_im (-B_im), C_im += A_re B_im + A_im B_re)
+// remains for narrow N and as a tuning variant.
 // Complex elements stay interleaved in shared memory, so one 16-byte shared load
 // gives a lane both planes of its fragment element.
 //
-// Warp tile 32 x 32 complex (64 fp64 accumulators per lane). A CTA of
+// Warp tile up to 32 x 32 complex. A CTA of
 // WARPS_M x WARPS_N warps owns a BM x BN tile; K is streamed in BK-complex
 // slices through a STAGES-deep cp.async pipeline (global reads coalesced along
 // K for A and along N for B; A is stored k-major in shared memory with a row
@@ -290,18 +294,21 @@ __global__ void k_mixed_offsets(int64_t* __restrict__ out, int64_t count, const 
   }
 }
 
-// Configurations kept after the tuning sweep (14 variants measured on the C1 shape;
-// V12 won: 16x32 warp tiles, 4 CTAs/SM so one tile's prologue/epilogue overlaps
-// another's DMMA stream). QTNH_ZGEMM_VARIANT=4|7|12 pins one for experiments.
+// 4M configurations kept after the tuning sweep (14 variants measured on the C1
+// shape; V12 was best: 16x32 warp tiles, 4 CTAs/SM so one tile's prologue /
+// epilogue overlaps another's DMMA stream). QTNH_ZGEMM_VARIANT=4|7|12|106|112
+// pins one for experiments.
 using V4 = Cfg<64, 32, 2, 1, 8, 4, 4>;    // 64 thr, 4 CTA/SM: narrow N (<= 32)
 using V7 = Cfg<32, 64, 1, 2, 8, 3, 5>;    // 64 thr, 5 CTA/SM (<= 204 regs)
 using V12 = Cfg<32, 64, 2, 2, 8, 3, 4, 16, 32>;   // warp tile 16x32, 128 thr
-// Gauss (3M) candidates: 3 DMMAs per complex k-step instead of 4
-using G1 = Cfg<32, 64, 2, 2, 8, 3, 3, 16, 32, true>;
-using G2 = Cfg<32, 32, 2, 2, 8, 4, 5, 16, 16, true>;
-using G3 = Cfg<32, 64, 2, 2, 8, 3, 4, 16, 32, true>;
-using G4 = Cfg<64, 32, 2, 1, 8, 4, 3, 32, 32, true>;
-using G5 = Cfg<32, 64, 1, 2, 8, 3, 4, 32, 32, true>;
+// Gauss (3M) complex multiply: 3 real DMMA products per complex k-step instead of
+// 4 (Re = ar br - ai bi, Im = (ar + ai)(br + bi) - ar br - ai bi). The FP64 tensor
+// pipe is the bound (ncu: math_pipe_throttle, 90 % DMMA-pipe busy for 4M), so
+// trading one product for two adds per fragment gives +17 % on the C1 shape
+// (39.1 vs 33.4 TFLOP/s counted as 8MNK). 32x32 warp tiles, 64 threads, 4 CTAs/SM,
+// 4-stage cp.async pipeline won a 16-configuration sweep (tools/bench_zgemm.py).
+using G6 = Cfg<32, 64, 1, 2, 8, 4, 4, 32, 32, true>;
+using G12 = Cfg<16, 64, 1, 2, 8, 4, 6, 16, 32, true>;
 
 int variant() {
   static int v = [] {
@@ -340,14 +347,14 @@ void zgemm_gather_a(const void* a, const int64_t* rowoff, const int64_t* coloff,
   auto Cp = static_cast<double2*>(c);
   static int gv = [] {
     const char* e = std::getenv("QTNH_ZGEMM_GATHER_VARIANT");
-    return e ? std::atoi(e) : 12;
+    return e ? std::atoi(e) : 106;
   }();
-  if (n > 32 && gv == 7) {
-    if (rows_fastest) launch_mode<V7, 1>(A, rowoff, coloff, B, Cp, m, n, k, st);
-    else launch_mode<V7, 2>(A, rowoff, coloff, B, Cp, m, n, k, st);
-  } else if (n > 32) {
+  if (n > 32 && gv == 12) {
     if (rows_fastest) launch_mode<V12, 1>(A, rowoff, coloff, B, Cp, m, n, k, st);
     else launch_mode<V12, 2>(A, rowoff, coloff, B, Cp, m, n, k, st);
+  } else if (n > 32) {
+    if (rows_fastest) launch_mode<G6, 1>(A, rowoff, coloff, B, Cp, m, n, k, st);
+    else launch_mode<G6, 2>(A, rowoff, coloff, B, Cp, m, n, k, st);
   } else {
     if (rows_fastest) launch_mode<V4, 1>(A, rowoff, coloff, B, Cp, m, n, k, st);
     else launch_mode<V4, 2>(A, rowoff, coloff, B, Cp, m, n, k, st);
@@ -367,14 +374,11 @@ void zgemm(const void* a, const void* b, void* c, Dim m, Dim n, Dim k, cudaStrea
     case 4: return launch<V4>(A, B, Cp, m, n, k, st);
     case 7: return launch<V7>(A, B, Cp, m, n, k, st);
     case 12: return launch<V12>(A, B, Cp, m, n, k, st);
-    case 101: return launch<G1>(A, B, Cp, m, n, k, st);
-    case 102: return launch<G2>(A, B, Cp, m, n, k, st);
-    case 103: return launch<G3>(A, B, Cp, m, n, k, st);
-    case 104: return launch<G4>(A, B, Cp, m, n, k, st);
-    case 105: return launch<G5>(A, B, Cp, m, n, k, st);
+    case 106: return launch<G6>(A, B, Cp, m, n, k, st);
+    case 112: return launch<G12>(A, B, Cp, m, n, k, st);
     default: break;
   }
-  if (n > 32) launch<V12>(A, B, Cp, m, n, k, st);
+  if (n > 32) launch<G6>(A, B, Cp, m, n, k, st);
   else launch<V4>(A, B, Cp, m, n, k, st);
 }
 
