@@ -50,6 +50,8 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+constexpr int kCoSmemMax = 512;  // K up to which a gather kernel stages coloff in shared memory
+
 template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int BK_, int STAGES_, int MINB_, int WTM_ = 32,
           int WTN_ = 32, bool GAUSS_ = false>
 struct Cfg {
@@ -85,6 +87,15 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
   double2* Bs = smem + STAGES * G::A_ELEMS;    // [stage][k][PB]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // Gather modes: the column-offset table of a short K sits in shared memory, so a
+  // stage's address lookups never wait on global memory (with few warps per
+  // scheduler those waits idled the tensor pipe).
+  int64_t* co_s = reinterpret_cast<int64_t*>(Bs + STAGES * G::B_ELEMS);
+  const bool co_in_smem = MODE != 0 && K <= kCoSmemMax;
+  if (co_in_smem) {
+    for (int64_t i = tid; i < K; i += T) co_s[i] = __ldg(coloff + i);
+    __syncthreads();
+  }
   const int wm = warp / G::WARPS_N, wn = warp % G::WARPS_N;
   // 1-D grid, N tiles fastest: the CTAs sharing a row block of A run together
   // (A read once from HBM), and M is not limited by gridDim.y.
@@ -135,7 +146,7 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
     for (int u = 0; u < LA; ++u) {
       bool ok = ma[u] && k0 + ka[u] < K;
       const double2* src = A;
-      if (ok) src = MODE == 0 ? pa[u] + k0 : pa[u] + __ldg(coloff + k0 + ka[u]);
+      if (ok) src = MODE == 0 ? pa[u] + k0 : pa[u] + (co_in_smem ? co_s[k0 + ka[u]] : __ldg(coloff + k0 + ka[u]));
       cp_async16(as + sa[u], src, ok);
     }
 #pragma unroll
@@ -263,10 +274,12 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
 template <class G, int MODE>
 void launch_mode(const double2* a, const int64_t* ro, const int64_t* co, const double2* b, double2* c, Dim m,
                  Dim n, Dim k, cudaStream_t st) {
-  QTNH_CUDA(cudaFuncSetAttribute(k_zgemm<G, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+  const size_t smem = G::SMEM + (MODE != 0 && k <= kCoSmemMax ? static_cast<size_t>(k) * 8 : 0);
+  QTNH_CUDA(cudaFuncSetAttribute(k_zgemm<G, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(G::SMEM + kCoSmemMax * 8)));
   Dim tiles = ((m + G::BM - 1) / G::BM) * ((n + G::BN - 1) / G::BN);
   if (tiles > 0x7fffffff) throw_invalid("zgemm problem too large for one launch");
-  k_zgemm<G, MODE><<<static_cast<unsigned>(tiles), G::THREADS, G::SMEM, st>>>(a, ro, co, b, c, m, n, k);
+  k_zgemm<G, MODE><<<static_cast<unsigned>(tiles), G::THREADS, smem, st>>>(a, ro, co, b, c, m, n, k);
   QTNH_LAUNCH_CHECK();
 }
 
@@ -297,7 +310,7 @@ __global__ void k_mixed_offsets(int64_t* __restrict__ out, int64_t count, const 
 // 4M configurations kept after the tuning sweep (14 variants measured on the C1
 // shape; V12 was best: 16x32 warp tiles, 4 CTAs/SM so one tile's prologue /
 // epilogue overlaps another's DMMA stream). QTNH_ZGEMM_VARIANT=4|7|12|106|112
-// pins one for experiments.
+// pins one for experiments (106 = G6, 122 = G22).
 using V4 = Cfg<64, 32, 2, 1, 8, 4, 4>;    // 64 thr, 4 CTA/SM: narrow N (<= 32)
 using V7 = Cfg<32, 64, 1, 2, 8, 3, 5>;    // 64 thr, 5 CTA/SM (<= 204 regs)
 using V12 = Cfg<32, 64, 2, 2, 8, 3, 4, 16, 32>;   // warp tile 16x32, 128 thr
@@ -308,7 +321,9 @@ using V12 = Cfg<32, 64, 2, 2, 8, 3, 4, 16, 32>;   // warp tile 16x32, 128 thr
 // (39.1 vs 33.4 TFLOP/s counted as 8MNK). 32x32 warp tiles, 64 threads, 4 CTAs/SM,
 // 4-stage cp.async pipeline won a 16-configuration sweep (tools/bench_zgemm.py).
 using G6 = Cfg<32, 64, 1, 2, 8, 4, 4, 32, 32, true>;
-using G12 = Cfg<16, 64, 1, 2, 8, 4, 6, 16, 32, true>;
+// Fewer, fatter CTAs for grids of a few waves (e.g. 2048 x 2048 x 1024: 39.2 vs
+// 35.9 TFLOP/s with G6): 16x32 warp tiles, BK 4, 8 stages, 3 CTAs/SM.
+using G22 = Cfg<32, 64, 2, 2, 4, 8, 3, 16, 32, true>;
 
 int variant() {
   static int v = [] {
@@ -375,11 +390,13 @@ void zgemm(const void* a, const void* b, void* c, Dim m, Dim n, Dim k, cudaStrea
     case 7: return launch<V7>(A, B, Cp, m, n, k, st);
     case 12: return launch<V12>(A, B, Cp, m, n, k, st);
     case 106: return launch<G6>(A, B, Cp, m, n, k, st);
-    case 112: return launch<G12>(A, B, Cp, m, n, k, st);
+    case 122: return launch<G22>(A, B, Cp, m, n, k, st);
     default: break;
   }
-  if (n > 32) launch<G6>(A, B, Cp, m, n, k, st);
-  else launch<V4>(A, B, Cp, m, n, k, st);
+  const Dim tiles = ((m + 31) / 32) * ((n + 63) / 64);
+  if (n <= 32) launch<V4>(A, B, Cp, m, n, k, st);
+  else if (tiles < 8192) launch<G22>(A, B, Cp, m, n, k, st);
+  else launch<G6>(A, B, Cp, m, n, k, st);
 }
 
 }  // namespace qtnhb

@@ -62,7 +62,7 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "one":
         run_one()
         sys.exit(0)
-    variants = sys.argv[1:] or ["4", "7", "12"]
+    variants = sys.argv[1:] or ["12", "106", "122"]
     for v in variants:
         env = dict(os.environ, QTNH_ZGEMM_VARIANT=v)
         r = subprocess.run([sys.executable, __file__, "one"], env=env, capture_output=True, text=True)
