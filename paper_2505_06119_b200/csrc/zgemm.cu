@@ -309,7 +309,7 @@ __global__ void k_mixed_offsets(int64_t* __restrict__ out, int64_t count, const 
 
 // 4M configurations kept after the tuning sweep (14 variants measured on the C1
 // shape; V12 was best: 16x32 warp tiles, 4 CTAs/SM so one tile's prologue /
-// epilogue overlaps another's DMMA stream). QTNH_ZGEMM_VARIANT=4|7|12|106|112
+// epilogue overlaps another's DMMA stream). QTNH_ZGEMM_VARIANT=4|7|12|106|122
 // pins one for experiments (106 = G6, 122 = G22).
 using V4 = Cfg<64, 32, 2, 1, 8, 4, 4>;    // 64 thr, 4 CTA/SM: narrow N (<= 32)
 using V7 = Cfg<32, 64, 1, 2, 8, 3, 5>;    // 64 thr, 5 CTA/SM (<= 204 regs)
