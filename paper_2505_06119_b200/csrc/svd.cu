@@ -249,9 +249,12 @@ __global__ void __launch_bounds__(B * 8) k_svd_gram_mma_t(const double2* __restr
   __shared__ double2 xs[P2][PX];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int fr = lane >> 2, fk = lane & 3;
-  double acc_re[NT][2], acc_im[NT][2];
+  // Gauss (3M) form of a conj(b): p1 = sum ar br, p2 = sum ai bi, p3 = sum (ar + ai)(br - bi);
+  // Re = p1 + p2, Im = p3 - p1 + p2 (3 DMMAs per complex product instead of 4).
+  double acc_re[NT][2], acc_im[NT][2], acc_s[NT][2];
 #pragma unroll
-  for (int j = 0; j < NT; ++j) acc_re[j][0] = acc_re[j][1] = acc_im[j][0] = acc_im[j][1] = 0.0;
+  for (int j = 0; j < NT; ++j)
+    acc_re[j][0] = acc_re[j][1] = acc_im[j][0] = acc_im[j][1] = acc_s[j][0] = acc_s[j][1] = 0.0;
   int64_t per = (L + splits - 1) / splits;
   int64_t c0 = split * per, c1 = min(L, c0 + per);
   for (int64_t cb = c0; cb < c1; cb += GK) {
@@ -265,13 +268,13 @@ __global__ void __launch_bounds__(B * 8) k_svd_gram_mma_t(const double2* __restr
 #pragma unroll
     for (int k4 = 0; k4 < GK; k4 += 4) {
       double2 av = xs[warp * 8 + fr][k4 + fk];
+      const double as = av.x + av.y;
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
         double2 bv = xs[j * 8 + fr][k4 + fk];
         dmma(acc_re[j], av.x, bv.x);
-        dmma(acc_im[j], av.x, -bv.y);
-        dmma(acc_re[j], av.y, bv.y);
-        dmma(acc_im[j], av.y, bv.x);
+        dmma(acc_im[j], av.y, bv.y);
+        dmma(acc_s[j], as, bv.x - bv.y);
       }
     }
     __syncthreads();
@@ -280,8 +283,9 @@ __global__ void __launch_bounds__(B * 8) k_svd_gram_mma_t(const double2* __restr
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
     int row = warp * 8 + fr, col = j * 8 + 2 * fk;
-    out[row * P2 + col] = make_double2(acc_re[j][0], acc_im[j][0]);
-    out[row * P2 + col + 1] = make_double2(acc_re[j][1], acc_im[j][1]);
+    out[row * P2 + col] = make_double2(acc_re[j][0] + acc_im[j][0], acc_s[j][0] - acc_re[j][0] + acc_im[j][0]);
+    out[row * P2 + col + 1] =
+        make_double2(acc_re[j][1] + acc_im[j][1], acc_s[j][1] - acc_re[j][1] + acc_im[j][1]);
   }
 }
 
@@ -313,19 +317,22 @@ __global__ void __launch_bounds__(B * 8) k_svd_update_mma_t(double2* __restrict_
       xs[r * PX + c] = col < W ? K[row * W + col] : make_double2(0.0, 0.0);
     }
     __syncthreads();
-    double acc_re[NT][2], acc_im[NT][2];
+    // Gauss (3M): p1 = sum wr xr, p2 = sum wi xi, p3 = sum (wr + wi)(xr + xi);
+    // Re = p1 - p2, Im = p3 - p1 - p2.
+    double acc_re[NT][2], acc_im[NT][2], acc_s[NT][2];
 #pragma unroll
-    for (int j = 0; j < NT; ++j) acc_re[j][0] = acc_re[j][1] = acc_im[j][0] = acc_im[j][1] = 0.0;
+    for (int j = 0; j < NT; ++j)
+      acc_re[j][0] = acc_re[j][1] = acc_im[j][0] = acc_im[j][1] = acc_s[j][0] = acc_s[j][1] = 0.0;
 #pragma unroll 4
     for (int k4 = 0; k4 < P2; k4 += 4) {
       double2 av = ws[(warp * 8 + fr) * PW + k4 + fk];
+      const double as = av.x + av.y;
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
         double2 bv = xs[(k4 + fk) * PX + j * 8 + fr];
         dmma(acc_re[j], av.x, bv.x);
-        dmma(acc_im[j], av.x, bv.y);
-        dmma(acc_re[j], av.y, -bv.y);
-        dmma(acc_im[j], av.y, bv.x);
+        dmma(acc_im[j], av.y, bv.y);
+        dmma(acc_s[j], as, bv.x + bv.y);
       }
     }
     __syncthreads();
@@ -334,8 +341,11 @@ __global__ void __launch_bounds__(B * 8) k_svd_update_mma_t(double2* __restrict_
       int r = warp * 8 + fr;
       int64_t row = r < B ? bi * B + r : bj * B + (r - B);
       int64_t col = cb + j * 8 + 2 * fk;
-      if (col < W) K[row * W + col] = make_double2(acc_re[j][0], acc_im[j][0]);
-      if (col + 1 < W) K[row * W + col + 1] = make_double2(acc_re[j][1], acc_im[j][1]);
+      if (col < W)
+        K[row * W + col] = make_double2(acc_re[j][0] - acc_im[j][0], acc_s[j][0] - acc_re[j][0] - acc_im[j][0]);
+      if (col + 1 < W)
+        K[row * W + col + 1] =
+            make_double2(acc_re[j][1] - acc_im[j][1], acc_s[j][1] - acc_re[j][1] - acc_im[j][1]);
     }
   }
 }
