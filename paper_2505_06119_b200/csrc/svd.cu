@@ -39,6 +39,13 @@ constexpr int kGramCols = 64; // column chunk of the Gram kernel
 constexpr int kUpdCols = 64;  // column tile of the update kernel
 static_assert(kB * kB == 256, "the 2x2-block eigen update maps one block per thread");
 
+__device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, bool pred) {
+  unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(pred ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_commit_() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1_() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(d[0]), "+d"(d[1])
@@ -246,7 +253,9 @@ __global__ void __launch_bounds__(B * 8) k_svd_gram_mma_t(const double2* __restr
   const int* pr = tab + (static_cast<int64_t>(round) * npairs + pair) * 2;
   const int bi = pr[0], bj = pr[1];
   const double2* K = wk + static_cast<int64_t>(mat) * rp * W;
-  __shared__ double2 xs[P2][PX];
+  // column chunks stream through a cp.async double buffer: chunk c+1 loads while
+  // chunk c feeds the DMMAs (dynamic smem: 2 x P2 x PX)
+  extern __shared__ double2 gsm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int fr = lane >> 2, fk = lane & 3;
   // Gauss (3M) form of a conj(b): p1 = sum ar br, p2 = sum ai bi, p3 = sum (ar + ai)(br - bi);
@@ -255,29 +264,40 @@ __global__ void __launch_bounds__(B * 8) k_svd_gram_mma_t(const double2* __restr
 #pragma unroll
   for (int j = 0; j < NT; ++j)
     acc_re[j][0] = acc_re[j][1] = acc_im[j][0] = acc_im[j][1] = acc_s[j][0] = acc_s[j][1] = 0.0;
-  int64_t per = (L + splits - 1) / splits;
-  int64_t c0 = split * per, c1 = min(L, c0 + per);
-  for (int64_t cb = c0; cb < c1; cb += GK) {
+  const int64_t per = (L + splits - 1) / splits;
+  const int64_t c0 = split * per, c1 = min(L, c0 + per);
+  auto issue = [&](int buf, int64_t cb) {
+    double2* xs = gsm + buf * P2 * PX;
     for (int e = tid; e < P2 * GK; e += T) {
-      int r = e / GK, c = e % GK;
-      int64_t row = (r < B ? bi * B + r : bj * B + (r - B));
-      int64_t col = cb + c;
-      xs[r][c] = col < c1 ? K[row * W + col] : make_double2(0.0, 0.0);
+      const int r = e / GK, c = e % GK;
+      const int64_t row = (r < B ? bi * B + r : bj * B + (r - B));
+      const int64_t col = cb + c;
+      const bool ok = col < c1;
+      cp_async16z(xs + r * PX + c, ok ? K + row * W + col : K, ok);
     }
+  };
+  if (c0 < c1) issue(0, c0);
+  cp_async_commit_();
+  int it = 0;
+  for (int64_t cb = c0; cb < c1; cb += GK, ++it) {
+    if (cb + GK < c1) issue((it + 1) & 1, cb + GK);
+    cp_async_commit_();
+    cp_async_wait1_();
     __syncthreads();
+    const double2* xs = gsm + (it & 1) * P2 * PX;
 #pragma unroll
     for (int k4 = 0; k4 < GK; k4 += 4) {
-      double2 av = xs[warp * 8 + fr][k4 + fk];
+      double2 av = xs[(warp * 8 + fr) * PX + k4 + fk];
       const double as = av.x + av.y;
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
-        double2 bv = xs[j * 8 + fr][k4 + fk];
+        double2 bv = xs[(j * 8 + fr) * PX + k4 + fk];
         dmma(acc_re[j], av.x, bv.x);
         dmma(acc_im[j], av.y, bv.y);
         dmma(acc_s[j], as, bv.x - bv.y);
       }
     }
-    __syncthreads();
+    __syncthreads();  // buffer it & 1 is refilled two chunks on
   }
   double2* out = part + ((static_cast<int64_t>(mat) * npairs + pair) * splits + split) * P2 * P2;
 #pragma unroll
@@ -305,18 +325,30 @@ __global__ void __launch_bounds__(B * 8) k_svd_update_mma_t(double2* __restrict_
   double2* K = wk + static_cast<int64_t>(mat) * rp * W;
   extern __shared__ double2 usm[];
   double2* ws = usm;            // [P2][PW]
-  double2* xs = usm + P2 * PW;  // [P2][PX]
+  double2* xsb = usm + P2 * PW;  // [2][P2][PX]: column tiles double-buffered by cp.async
   const int lane = tid & 31, warp = tid >> 5, fr = lane >> 2, fk = lane & 3;
   const double2* Wh = wh + fidx * P2 * P2;
   for (int e = tid; e < P2 * P2; e += T) ws[(e / P2) * PW + e % P2] = Wh[e];
-  for (int64_t cb = static_cast<int64_t>(blockIdx.x) * UC; cb < W; cb += static_cast<int64_t>(gridDim.x) * UC) {
+  const int64_t step = static_cast<int64_t>(gridDim.x) * UC;
+  auto issue = [&](int buf, int64_t cb) {
+    double2* xs = xsb + buf * P2 * PX;
     for (int e = tid; e < P2 * UC; e += T) {
-      int r = e / UC, c = e % UC;
-      int64_t row = r < B ? bi * B + r : bj * B + (r - B);
-      int64_t col = cb + c;
-      xs[r * PX + c] = col < W ? K[row * W + col] : make_double2(0.0, 0.0);
+      const int r = e / UC, c = e % UC;
+      const int64_t row = r < B ? bi * B + r : bj * B + (r - B);
+      const int64_t col = cb + c;
+      const bool ok = col < W;
+      cp_async16z(xs + r * PX + c, ok ? K + row * W + col : K, ok);
     }
+  };
+  int64_t cb = static_cast<int64_t>(blockIdx.x) * UC;
+  if (cb < W) issue(0, cb);
+  cp_async_commit_();
+  for (int it = 0; cb < W; cb += step, ++it) {
+    if (cb + step < W) issue((it + 1) & 1, cb + step);
+    cp_async_commit_();
+    cp_async_wait1_();
     __syncthreads();
+    const double2* xs = xsb + (it & 1) * P2 * PX;
     // Gauss (3M): p1 = sum wr xr, p2 = sum wi xi, p3 = sum (wr + wi)(xr + xi);
     // Re = p1 - p2, Im = p3 - p1 - p2.
     double acc_re[NT][2], acc_im[NT][2], acc_s[NT][2];
@@ -335,7 +367,6 @@ __global__ void __launch_bounds__(B * 8) k_svd_update_mma_t(double2* __restrict_
         dmma(acc_s[j], as, bv.x + bv.y);
       }
     }
-    __syncthreads();
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       int r = warp * 8 + fr;
@@ -347,6 +378,7 @@ __global__ void __launch_bounds__(B * 8) k_svd_update_mma_t(double2* __restrict_
         K[row * W + col + 1] =
             make_double2(acc_re[j][1] - acc_im[j][1], acc_s[j][1] - acc_re[j][1] - acc_im[j][1]);
     }
+    __syncthreads();  // buffer it & 1 is refilled two tiles on
   }
 }
 
@@ -589,9 +621,11 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
                                                                    static_cast<double*>(floor_abs.ptr), floor_rel());
   QTNH_LAUNCH_CHECK();
   const size_t eig_smem = static_cast<size_t>(2) * P2 * (P2 + 1) * 16;
-  const size_t upd_smem = static_cast<size_t>(P2) * ((P2 + 4) + (48 + 2)) * 16;
+  const size_t upd_smem = static_cast<size_t>(P2) * ((P2 + 4) + 2 * (48 + 2)) * 16;
+  const size_t gram_smem = static_cast<size_t>(2) * P2 * ((B >= 32 ? 32 : 64) + 4) * 16;
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_eigen_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_smem));
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
+  QTNH_CUDA(cudaFuncSetAttribute(k_svd_gram_mma_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem));
   std::vector<double> off_h(batch);
   int sweep = 0;
   const int max_sweeps = 40;
@@ -619,7 +653,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
       QTNH_CUDA(cudaMemcpyAsync(thr_d.ptr, thr_h.data(), batch * sizeof(double), cudaMemcpyHostToDevice, st));
     }
     for (int rd = 0; rd < rounds; ++rd) {
-      k_svd_gram_mma_t<B><<<dim3(npairs, splits, static_cast<unsigned>(batch)), B * 8, 0, st>>>(
+      k_svd_gram_mma_t<B><<<dim3(npairs, splits, static_cast<unsigned>(batch)), B * 8, gram_smem, st>>>(
           static_cast<const double2*>(wk.ptr), static_cast<double2*>(part.ptr), static_cast<const int*>(d_tab.ptr),
           rd, npairs, splits, rp, L, qw);
       QTNH_LAUNCH_CHECK();
