@@ -230,8 +230,24 @@ TP op_contract(const TP& a_in, const TP& b_in, const std::vector<int>& apos, con
       };
       Dim min_r = min_stride(rd, rs), min_c = min_stride(cd, cs);
       const int64_t* ro = gather_table(r, rd, rs);
-      const int64_t* co = gather_table(r, cd, cs);
-      zgemm_gather_a(a->data(), ro, co, min_r <= min_c, B, c2->data(), M, N, K, r.stream);
+      // A long K keeps its column offsets in shared memory as two small tables:
+      // coloff(k) = hi[k >> sh] + lo[k & (2^sh - 1)] (inner digits -> lo).
+      const int64_t* co = nullptr;
+      const int64_t* cohi = nullptr;
+      int co_sh = 0;
+      if (K > 512) {
+        for (size_t sp = 1; sp < cd.size() && !cohi; ++sp) {
+          Dim lo = 1, hi = 1;
+          for (size_t i = 0; i < cd.size(); ++i) (i < sp ? hi : lo) *= cd[i];
+          if ((lo & (lo - 1)) == 0 && lo + hi <= 512) {
+            co = gather_table(r, {cd.begin() + sp, cd.end()}, {cs.begin() + sp, cs.end()});
+            cohi = gather_table(r, {cd.begin(), cd.begin() + sp}, {cs.begin(), cs.begin() + sp});
+            while ((Dim(1) << co_sh) < lo) ++co_sh;
+          }
+        }
+      }
+      if (!co) co = gather_table(r, cd, cs);
+      zgemm_gather_a(a->data(), ro, co, min_r <= min_c, B, c2->data(), M, N, K, r.stream, cohi, co_sh);
     }
   }
   // 4. Restore the SPEC order / split when a was reshuffled.

@@ -80,7 +80,8 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
                                                                const int64_t* __restrict__ coloff,
                                                                const double2* __restrict__ B,
                                                                double2* __restrict__ C, int64_t M,
-                                                               int64_t N, int64_t K) {
+                                                               int64_t N, int64_t K,
+                                                               const int64_t* __restrict__ cohi, int co_sh) {
   constexpr int BM = G::BM, BN = G::BN, BK = G::BK, STAGES = G::STAGES, T = G::THREADS;
   extern __shared__ __align__(16) double2 smem[];
   double2* As = smem;                          // [stage][k][PA]
@@ -90,12 +91,24 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
   // Gather modes: the column-offset table of a short K sits in shared memory, so a
   // stage's address lookups never wait on global memory (with few warps per
   // scheduler those waits idled the tensor pipe).
+  // A long K whose column offsets factor as hi[k >> co_sh] + lo[k & (2^co_sh - 1)]
+  // (row-major digits split in two) keeps both halves there instead.
   int64_t* co_s = reinterpret_cast<int64_t*>(Bs + STAGES * G::B_ELEMS);
-  const bool co_in_smem = MODE != 0 && K <= kCoSmemMax;
+  const bool co_split = MODE != 0 && cohi != nullptr;
+  const bool co_in_smem = MODE != 0 && (K <= kCoSmemMax || co_split);
+  const int64_t co_lo_n = co_split ? (int64_t(1) << co_sh) : K;
+  const int64_t co_mask = co_lo_n - 1;
   if (co_in_smem) {
-    for (int64_t i = tid; i < K; i += T) co_s[i] = __ldg(coloff + i);
+    for (int64_t i = tid; i < co_lo_n; i += T) co_s[i] = __ldg(coloff + i);
+    if (co_split)
+      for (int64_t i = tid; i < (K >> co_sh); i += T) co_s[co_lo_n + i] = __ldg(cohi + i);
     __syncthreads();
   }
+  auto col_off = [&](int64_t k) -> int64_t {
+    if (!co_in_smem) return __ldg(coloff + k);
+    if (co_split) return co_s[co_lo_n + (k >> co_sh)] + co_s[k & co_mask];
+    return co_s[k];
+  };
   const int wm = warp / G::WARPS_N, wn = warp % G::WARPS_N;
   // 1-D grid, N tiles fastest: the CTAs sharing a row block of A run together
   // (A read once from HBM), and M is not limited by gridDim.y.
@@ -146,7 +159,7 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
     for (int u = 0; u < LA; ++u) {
       bool ok = ma[u] && k0 + ka[u] < K;
       const double2* src = A;
-      if (ok) src = MODE == 0 ? pa[u] + k0 : pa[u] + (co_in_smem ? co_s[k0 + ka[u]] : __ldg(coloff + k0 + ka[u]));
+      if (ok) src = MODE == 0 ? pa[u] + k0 : pa[u] + col_off(k0 + ka[u]);
       cp_async16(as + sa[u], src, ok);
     }
 #pragma unroll
@@ -273,13 +286,17 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
 
 template <class G, int MODE>
 void launch_mode(const double2* a, const int64_t* ro, const int64_t* co, const double2* b, double2* c, Dim m,
-                 Dim n, Dim k, cudaStream_t st) {
-  const size_t smem = G::SMEM + (MODE != 0 && k <= kCoSmemMax ? static_cast<size_t>(k) * 8 : 0);
+                 Dim n, Dim k, cudaStream_t st, const int64_t* cohi = nullptr, int co_sh = 0) {
+  size_t co_bytes = 0;
+  if (MODE != 0 && cohi) co_bytes = static_cast<size_t>((Dim(1) << co_sh) + (k >> co_sh)) * 8;
+  else if (MODE != 0 && k <= kCoSmemMax) co_bytes = static_cast<size_t>(k) * 8;
+  if (co_bytes > kCoSmemMax * 8) throw_invalid("column offset split exceeds its shared-memory budget");
+  const size_t smem = G::SMEM + co_bytes;
   QTNH_CUDA(cudaFuncSetAttribute(k_zgemm<G, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(G::SMEM + kCoSmemMax * 8)));
   Dim tiles = ((m + G::BM - 1) / G::BM) * ((n + G::BN - 1) / G::BN);
   if (tiles > 0x7fffffff) throw_invalid("zgemm problem too large for one launch");
-  k_zgemm<G, MODE><<<static_cast<unsigned>(tiles), G::THREADS, smem, st>>>(a, ro, co, b, c, m, n, k);
+  k_zgemm<G, MODE><<<static_cast<unsigned>(tiles), G::THREADS, smem, st>>>(a, ro, co, b, c, m, n, k, cohi, co_sh);
   QTNH_LAUNCH_CHECK();
 }
 
@@ -351,7 +368,7 @@ void index_offsets(int64_t* out, Dim count, const std::vector<Dim>& dims, const 
 }
 
 void zgemm_gather_a(const void* a, const int64_t* rowoff, const int64_t* coloff, bool rows_fastest,
-                    const void* b, void* c, Dim m, Dim n, Dim k, cudaStream_t st) {
+                    const void* b, void* c, Dim m, Dim n, Dim k, cudaStream_t st, const int64_t* cohi, int co_sh) {
   if (m <= 0 || n <= 0) return;
   if (k <= 0) {
     QTNH_CUDA(cudaMemsetAsync(c, 0, static_cast<size_t>(m * n) * 16, st));
@@ -365,14 +382,14 @@ void zgemm_gather_a(const void* a, const int64_t* rowoff, const int64_t* coloff,
     return e ? std::atoi(e) : 106;
   }();
   if (n > 32 && gv == 12) {
-    if (rows_fastest) launch_mode<V12, 1>(A, rowoff, coloff, B, Cp, m, n, k, st);
-    else launch_mode<V12, 2>(A, rowoff, coloff, B, Cp, m, n, k, st);
+    if (rows_fastest) launch_mode<V12, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh);
+    else launch_mode<V12, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh);
   } else if (n > 32) {
-    if (rows_fastest) launch_mode<G6, 1>(A, rowoff, coloff, B, Cp, m, n, k, st);
-    else launch_mode<G6, 2>(A, rowoff, coloff, B, Cp, m, n, k, st);
+    if (rows_fastest) launch_mode<G6, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh);
+    else launch_mode<G6, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh);
   } else {
-    if (rows_fastest) launch_mode<V4, 1>(A, rowoff, coloff, B, Cp, m, n, k, st);
-    else launch_mode<V4, 2>(A, rowoff, coloff, B, Cp, m, n, k, st);
+    if (rows_fastest) launch_mode<V4, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh);
+    else launch_mode<V4, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh);
   }
 }
 

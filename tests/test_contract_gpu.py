@@ -105,6 +105,23 @@ def test_contracted_distributed_index_is_swapped_local():
     assert rel_l2(got, P.contract(da, a, db, b, ap, bp)) < TOL
 
 
+@pytest.mark.parametrize("da,db,ap,bp", [
+    ([2] * 20, [2] * 12, [0, 2, 3, 5, 7, 8, 11, 13, 16, 19], list(range(10))),   # K = 1024: split column table
+    ([2] * 19, [2] * 13, [1, 4, 5, 6, 9, 10, 12, 14, 15, 17, 18], [12, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9]),  # K = 2048
+    ([3] * 9, [3] * 7, [0, 2, 4, 5, 7, 8], [5, 4, 3, 2, 1, 0]),                  # K = 729: global table
+])
+def test_long_k_gather_contractions(da, db, ap, bp):
+    a = circuits.rng_normals(31, int(np.prod(da)))
+    b = circuits.rng_normals(32, int(np.prod(db)))
+
+    def body(rk):
+        ta = Tensor.from_global(rk, IndexTuple(da, 0), None, a)
+        tb = Tensor.from_global(rk, IndexTuple(db, 0), None, b)
+        return contract(ta, tb, ap, bp).to_global_vector()
+
+    assert rel_l2(run_collect(World(1), body), P.contract(da, a, db, b, ap, bp)) < TOL
+
+
 @pytest.mark.parametrize("m,n,k", [(1, 1, 1), (64, 128, 8), (2**14, 128, 128), (1000, 100, 37), (3, 300, 500),
                                    (2048, 2048, 64)])
 def test_zgemm_device_against_numpy(m, n, k):
