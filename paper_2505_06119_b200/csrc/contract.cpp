@@ -229,7 +229,34 @@ TP op_contract(const TP& a_in, const TP& b_in, const std::vector<int>& apos, con
         return m;
       };
       Dim min_r = min_stride(rd, rs), min_c = min_stride(cd, cs);
-      const int64_t* ro = gather_table(r, rd, rs);
+      // Row offsets: for a long M two small tables, rowoff(m) = hi[m >> sh] +
+      // lo[m & (2^sh - 1)], instead of an M-entry table (16 MB at C1).
+      const int64_t* ro = nullptr;
+      const int64_t* rohi = nullptr;
+      int ro_sh = 0;
+      if (M > 4096) {
+        Dim best = 0;
+        size_t best_sp = 0;
+        for (size_t sp = 1; sp < rd.size(); ++sp) {
+          Dim lo = 1, hi = 1;
+          for (size_t i = 0; i < rd.size(); ++i) (i < sp ? hi : lo) *= rd[i];
+          if ((lo & (lo - 1)) != 0) continue;
+          Dim cost = std::max(lo, hi);
+          if (!best || cost < best) {
+            best = cost;
+            best_sp = sp;
+          }
+        }
+        if (best && best <= (Dim(1) << 16)) {
+          const size_t sp = best_sp;
+          ro = gather_table(r, {rd.begin() + sp, rd.end()}, {rs.begin() + sp, rs.end()});
+          rohi = gather_table(r, {rd.begin(), rd.begin() + sp}, {rs.begin(), rs.begin() + sp});
+          Dim lo = 1;
+          for (size_t i = sp; i < rd.size(); ++i) lo *= rd[i];
+          while ((Dim(1) << ro_sh) < lo) ++ro_sh;
+        }
+      }
+      if (!ro) ro = gather_table(r, rd, rs);
       // A long K keeps its column offsets in shared memory as two small tables:
       // coloff(k) = hi[k >> sh] + lo[k & (2^sh - 1)] (inner digits -> lo).
       const int64_t* co = nullptr;
@@ -247,7 +274,8 @@ TP op_contract(const TP& a_in, const TP& b_in, const std::vector<int>& apos, con
         }
       }
       if (!co) co = gather_table(r, cd, cs);
-      zgemm_gather_a(a->data(), ro, co, min_r <= min_c, B, c2->data(), M, N, K, r.stream, cohi, co_sh);
+      zgemm_gather_a(a->data(), ro, co, min_r <= min_c, B, c2->data(), M, N, K, r.stream, cohi, co_sh, rohi,
+                     ro_sh);
     }
   }
   // 4. Restore the SPEC order / split when a was reshuffled.

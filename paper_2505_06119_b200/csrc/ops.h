@@ -79,7 +79,7 @@ void zgemm(const void* a, const void* b, void* c, Dim m, Dim n, Dim k, cudaStrea
 // contraction's layout permutation fused into the operand loads.
 void zgemm_gather_a(const void* a, const int64_t* rowoff, const int64_t* coloff, bool rows_fastest,
                     const void* b, void* c, Dim m, Dim n, Dim k, cudaStream_t st, const int64_t* cohi = nullptr,
-                    int co_sh = 0);
+                    int co_sh = 0, const int64_t* rohi = nullptr, int ro_sh = 0);
 // out[i] = sum_d digit_d(i) * strides[d], digits row-major over dims.
 void index_offsets(int64_t* out, Dim count, const std::vector<Dim>& dims, const std::vector<Dim>& strides,
                    cudaStream_t st);

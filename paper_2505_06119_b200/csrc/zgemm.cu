@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
                                                                const double2* __restrict__ B,
                                                                double2* __restrict__ C, int64_t M,
                                                                int64_t N, int64_t K,
-                                                               const int64_t* __restrict__ cohi, int co_sh) {
+                                                               const int64_t* __restrict__ cohi, int co_sh,
+                                                               const int64_t* __restrict__ rohi, int ro_sh) {
   constexpr int BM = G::BM, BN = G::BN, BK = G::BK, STAGES = G::STAGES, T = G::THREADS;
   extern __shared__ __align__(16) double2 smem[];
   double2* As = smem;                          // [stage][k][PA]
@@ -139,8 +140,16 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
       continue;
     }
     ma[u] = bm + m < M;
-    if (MODE == 0) pa[u] = A + (ma[u] ? (bm + m) : 0) * K + k;
-    else pa[u] = A + (ma[u] ? __ldg(rowoff + bm + m) : 0);
+    if (MODE == 0) {
+      pa[u] = A + (ma[u] ? (bm + m) : 0) * K + k;
+    } else {
+      // row offsets: one table, or hi[m >> ro_sh] + lo[m & (2^ro_sh - 1)]
+      const int64_t row = bm + m;
+      int64_t off = 0;
+      if (ma[u]) off = rohi ? __ldg(rohi + (row >> ro_sh)) + __ldg(rowoff + (row & ((int64_t(1) << ro_sh) - 1)))
+                            : __ldg(rowoff + row);
+      pa[u] = A + off;
+    }
   }
 #pragma unroll
   for (int u = 0; u < LB; ++u) {
@@ -286,7 +295,8 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
 
 template <class G, int MODE>
 void launch_mode(const double2* a, const int64_t* ro, const int64_t* co, const double2* b, double2* c, Dim m,
-                 Dim n, Dim k, cudaStream_t st, const int64_t* cohi = nullptr, int co_sh = 0) {
+                 Dim n, Dim k, cudaStream_t st, const int64_t* cohi = nullptr, int co_sh = 0,
+                 const int64_t* rohi = nullptr, int ro_sh = 0) {
   size_t co_bytes = 0;
   if (MODE != 0 && cohi) co_bytes = static_cast<size_t>((Dim(1) << co_sh) + (k >> co_sh)) * 8;
   else if (MODE != 0 && k <= kCoSmemMax) co_bytes = static_cast<size_t>(k) * 8;
@@ -296,7 +306,8 @@ void launch_mode(const double2* a, const int64_t* ro, const int64_t* co, const d
                                  (int)(G::SMEM + kCoSmemMax * 8)));
   Dim tiles = ((m + G::BM - 1) / G::BM) * ((n + G::BN - 1) / G::BN);
   if (tiles > 0x7fffffff) throw_invalid("zgemm problem too large for one launch");
-  k_zgemm<G, MODE><<<static_cast<unsigned>(tiles), G::THREADS, smem, st>>>(a, ro, co, b, c, m, n, k, cohi, co_sh);
+  k_zgemm<G, MODE><<<static_cast<unsigned>(tiles), G::THREADS, smem, st>>>(a, ro, co, b, c, m, n, k, cohi, co_sh, rohi,
+                                                                                  ro_sh);
   QTNH_LAUNCH_CHECK();
 }
 
@@ -368,7 +379,8 @@ void index_offsets(int64_t* out, Dim count, const std::vector<Dim>& dims, const 
 }
 
 void zgemm_gather_a(const void* a, const int64_t* rowoff, const int64_t* coloff, bool rows_fastest,
-                    const void* b, void* c, Dim m, Dim n, Dim k, cudaStream_t st, const int64_t* cohi, int co_sh) {
+                    const void* b, void* c, Dim m, Dim n, Dim k, cudaStream_t st, const int64_t* cohi, int co_sh,
+                    const int64_t* rohi, int ro_sh) {
   if (m <= 0 || n <= 0) return;
   if (k <= 0) {
     QTNH_CUDA(cudaMemsetAsync(c, 0, static_cast<size_t>(m * n) * 16, st));
@@ -382,14 +394,14 @@ void zgemm_gather_a(const void* a, const int64_t* rowoff, const int64_t* coloff,
     return e ? std::atoi(e) : 106;
   }();
   if (n > 32 && gv == 12) {
-    if (rows_fastest) launch_mode<V12, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh);
-    else launch_mode<V12, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh);
+    if (rows_fastest) launch_mode<V12, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
+    else launch_mode<V12, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
   } else if (n > 32) {
-    if (rows_fastest) launch_mode<G6, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh);
-    else launch_mode<G6, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh);
+    if (rows_fastest) launch_mode<G6, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
+    else launch_mode<G6, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
   } else {
-    if (rows_fastest) launch_mode<V4, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh);
-    else launch_mode<V4, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh);
+    if (rows_fastest) launch_mode<V4, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
+    else launch_mode<V4, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
   }
 }
 

@@ -34,12 +34,15 @@ def main():
                 N = math.prod(net.dims[x] for x in lb if x not in sh)
                 K = math.prod(net.dims[x] for x in sh)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                geo = {"a_dims": net.tensors[a].shape().dims, "b_dims": net.tensors[b].shape().dims,
+                       "apos": [la.index(x) for x in sh], "bpos": [lb.index(x) for x in sh]}
                 e0.record()
                 net.contract_pair(a, b, nxt + s)
                 e1.record()
-                recs.append((e0, e1, M, N, K))
+                recs.append((e0, e1, M, N, K, geo))
             torch.cuda.synchronize()
-            res["recs"] = [(e0.elapsed_time(e1), M, N, K) for e0, e1, M, N, K in recs]
+            res["recs"] = [(e0.elapsed_time(e1), M, N, K) for e0, e1, M, N, K, _ in recs]
+            res["geo"] = [g for *_, g in recs]
             for t in list(net.tensors.values()):
                 t.free()
 
@@ -56,9 +59,12 @@ def main():
         cats[c][2] += by
     out["by_class"] = {k: {"ms": v[0], "TFLOPs": v[1] / max(v[0], 1e-9) / 1e9, "GBps": v[2] / max(v[0], 1e-9) / 1e6}
                        for k, v in cats.items()}
-    top = sorted(recs, reverse=True)[:20]
-    out["top"] = [{"ms": ms, "M": M, "N": N, "K": K, "TFLOPs": 8.0 * M * N * K / ms / 1e9,
-                   "GBps": 16.0 * (M * K + K * N + M * N) / ms / 1e6} for ms, M, N, K in top]
+    idx = sorted(range(len(recs)), key=lambda i: -recs[i][0])[:12]
+    out["top"] = []
+    for i in idx:
+        ms, M, N, K = recs[i]
+        out["top"].append({"ms": ms, "M": M, "N": N, "K": K, "TFLOPs": 8.0 * M * N * K / ms / 1e9,
+                           "GBps": 16.0 * (M * K + K * N + M * N) / ms / 1e6, **res["geo"][i]})
     print(json.dumps(out, indent=1))
 
 
