@@ -69,7 +69,10 @@ const char* qtnh_version(void);
 /* Tunables: "swap_chunk_bytes" = staging size of the in-place distributed swap;
    "peer_direct" (1 default) = in a local world whose ranks can address each
    other's HBM, redistribute by peer-memory kernels (push remap, pairwise
-   in-place swap) instead of pack -> exchange -> unpack. */
+   in-place swap) instead of pack -> exchange -> unpack;
+   "pool_reserve_gb" (0 default) = GiB of the device's stream-ordered pool to map
+   when the next world is created (long sequences of varying tensor sizes then
+   never wait on new mappings). */
 int qtnh_set_option(const char* name, double value);
 /* Number of this library's kernels launched so far by the calling process. */
 int64_t qtnh_kernel_launch_count(void);

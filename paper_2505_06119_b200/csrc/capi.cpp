@@ -602,6 +602,7 @@ int qtnh_set_option(const char* name, double value) {
     std::string n(name);
     if (n == "swap_chunk_bytes") set_swap_chunk_bytes(static_cast<Dim>(value));
     else if (n == "peer_direct") set_peer_direct(value != 0);
+    else if (n == "pool_reserve_gb") set_pool_reserve_gb(value);
     else throw_invalid("unknown option " + n);
   });
 }

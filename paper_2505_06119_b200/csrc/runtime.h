@@ -93,6 +93,7 @@ std::vector<void*> peer_pointers(RankCtx& r, const std::vector<int>& members, vo
 
 // ---- device tensors -----------------------------------------------------------
 void keep_pool(int device);  // stream-ordered pool keeps freed blocks (world lifetime)
+void set_pool_reserve_gb(double gb);  // reserve (map) this much at the next world creation
 void trim_pool(int device);  // return unused pool memory to the driver
 struct DevBuf {
   void* ptr = nullptr;

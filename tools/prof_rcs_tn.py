@@ -13,7 +13,9 @@ def main():
     import torch
 
     from paper_2505_06119_b200 import network
-    from paper_2505_06119_b200.qtnh import World
+    from paper_2505_06119_b200.qtnh import World, check, lib
+
+    check(lib.qtnh_set_option(b"pool_reserve_gb", float(os.environ.get("RESERVE_GB", "120"))))
 
     rows, cols, depth, seed, n_open = 5, 6, 14, 2025, 6
     res = {}

@@ -19,12 +19,17 @@ def main():
     ap.add_argument("--seed", type=int, default=2025)
     ap.add_argument("--bitstrings", type=int, default=1024)
     ap.add_argument("--sequential", action="store_true", help="one SVD per update instead of batched layers")
+    ap.add_argument("--reserve-gb", type=float, default=48,
+                    help="map this much of the stream-ordered pool up front (option pool_reserve_gb)")
     args = ap.parse_args()
     import numpy as np
     import torch
 
     from paper_2505_06119_b200 import circuits, mps
     from paper_2505_06119_b200.qtnh import World
+    from paper_2505_06119_b200 import qtnh as _q
+
+    _q.check(_q.lib.qtnh_set_option(b"pool_reserve_gb", float(args.reserve_gb)))
 
     out = {"n": args.n, "depth": args.depth, "chi": args.chi}
     layers = mps.rcs_1d_layers(args.n, args.depth, args.seed)

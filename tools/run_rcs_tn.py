@@ -23,12 +23,17 @@ def main():
     ap.add_argument("--seed", type=int, default=2025)
     ap.add_argument("--no-statevector", action="store_true")
     ap.add_argument("--trials", type=int, default=24)
+    ap.add_argument("--reserve-gb", type=float, default=120,
+                    help="map this much of the stream-ordered pool up front (option pool_reserve_gb)")
     args = ap.parse_args()
     import numpy as np
     import torch
 
     from paper_2505_06119_b200 import circuits, mps, network
     from paper_2505_06119_b200.qtnh import IndexTuple, Tensor, World, apply_gate
+    from paper_2505_06119_b200 import qtnh as _q
+
+    _q.check(_q.lib.qtnh_set_option(b"pool_reserve_gb", float(args.reserve_gb)))
 
     out = {"rows": args.rows, "cols": args.cols, "depth": args.depth, "open": args.open}
 
