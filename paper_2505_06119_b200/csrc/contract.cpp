@@ -234,7 +234,11 @@ TP op_contract(const TP& a_in, const TP& b_in, const std::vector<int>& apos, con
       const int64_t* ro = nullptr;
       const int64_t* rohi = nullptr;
       int ro_sh = 0;
-      if (M > 4096) {
+      static const bool row_split = [] {
+        const char* e = std::getenv("QTNH_ROW_SPLIT");
+        return !(e && e[0] == '0');
+      }();
+      if (M > 4096 && row_split) {
         Dim best = 0;
         size_t best_sp = 0;
         for (size_t sp = 1; sp < rd.size(); ++sp) {
