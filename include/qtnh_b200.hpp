@@ -181,6 +181,14 @@ class Tensor {  // tensor.hpp:53-695 (dense)
   }
   qtnh_tensor_t h() const { return p_.get(); }
 
+  // serialization (tensor.hpp:388-446), QTNHTEN1 byte-identical to the reference
+  void save(const std::string& path) const { check(qtnh_tensor_save(h(), path.c_str())); }
+  static Tensor load(Rank& r, const std::string& path) {
+    qtnh_tensor_t o;
+    check(qtnh_tensor_load(r.handle(), path.c_str(), &o));
+    return Tensor(o);
+  }
+
  private:
   explicit Tensor(qtnh_tensor_t h) : p_(h, [](qtnh_tensor_t x) { qtnh_tensor_free(x); }) {}
   std::shared_ptr<qtnh_tensor_s> p_;
@@ -211,7 +219,61 @@ inline Tensor gather_index(const Tensor& t, int pos) {
   check(qtnh_gather_index(t.h(), pos, &o));
   return wrap(o);
 }
+inline Tensor slice_local_dims(const Tensor& t, const std::vector<Dim>& new_local) {  // ops.hpp:166
+  qtnh_tensor_t o;
+  check(qtnh_slice_local_dims(t.h(), new_local.data(), &o));
+  return wrap(o);
+}
+inline Tensor pad_local_dims(const Tensor& t, const std::vector<Dim>& new_local) {  // ops.hpp:201
+  qtnh_tensor_t o;
+  check(qtnh_pad_local_dims(t.h(), new_local.data(), &o));
+  return wrap(o);
+}
+inline Tensor conj(const Tensor& t) {  // ops.hpp:147
+  qtnh_tensor_t o;
+  check(qtnh_conj(t.h(), &o));
+  return wrap(o);
+}
+inline Tensor scale(const Tensor& t, Complex a) {  // ops.hpp:155
+  qtnh_tensor_t o;
+  check(qtnh_scale(t.h(), a.real(), a.imag(), &o));
+  return wrap(o);
+}
 }  // namespace ops
+
+namespace linalg {  // psvd -> truncate_svd -> absorb_singular_* (linalg.hpp:441-523)
+enum class Absorb { none = QTNH_ABSORB_NONE, left = QTNH_ABSORB_LEFT, right = QTNH_ABSORB_RIGHT,
+                    split = QTNH_ABSORB_SPLIT };
+struct Svd {
+  Tensor u, vh;
+  std::vector<double> s;
+};
+inline Svd svd(const Tensor& t, const std::vector<int>& row_pos, const std::vector<int>& col_pos, Dim chi = 0,
+               Absorb absorb = Absorb::none) {
+  auto sh = t.shape();
+  Dim m = 1, n = 1;
+  for (int p : row_pos) m *= sh.dims[p];
+  for (int p : col_pos) n *= sh.dims[p];
+  Svd r;
+  r.s.assign(chi > 0 ? chi : std::min(m, n), 0.0);
+  qtnh_tensor_t u, vh;
+  check(qtnh_svd(t.h(), static_cast<int>(row_pos.size()), row_pos.data(), static_cast<int>(col_pos.size()),
+                 col_pos.data(), chi, static_cast<int>(absorb), &u, &vh, r.s.data()));
+  r.u = wrap(u);
+  r.vh = wrap(vh);
+  return r;
+}
+}  // namespace linalg
+
+namespace gates {  // contract(state, gate) + permute back, in place (copy-on-write)
+inline void apply(Tensor& state, const std::vector<int>& targets, const std::vector<Complex>& gate,
+                  bool diagonal = false) {
+  check(qtnh_gate_apply(state.h(), static_cast<int>(targets.size()), targets.data(),
+                        reinterpret_cast<const double*>(gate.data()), diagonal ? 1 : 0));
+}
+inline void swap_indices(Tensor& state, int a, int b) { check(qtnh_swap_indices(state.h(), a, b)); }
+inline void qft(Tensor& state, bool swaps = true) { check(qtnh_qft(state.h(), swaps ? 1 : 0)); }
+}  // namespace gates
 
 namespace network {  // SPEC.md:361-369, result order SPEC.md:408
 inline Tensor contract(const Tensor& a, const Tensor& b, const std::vector<int>& a_pos,

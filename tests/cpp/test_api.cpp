@@ -1,6 +1,8 @@
 // C++ caller of the B200 path through include/qtnh_b200.hpp, written like the
 // reference's own tests (proj/tests/test_ops.cpp:77-110) to show the drop-in.
+#include <cmath>
 #include <cstdio>
+#include <string>
 #include <cstdlib>
 
 #include "qtnh_b200.hpp"
@@ -69,6 +71,30 @@ int main() {
       got = qtnh::network::contract(a, v, {1}, {0}).to_global_vector();
     });
     EXPECT((got == std::vector<Complex>{{0, 0}, {1, 0}}));
+  }
+  // truncated SVD reconstruction + QTNHTEN1 round trip through the C++ layer
+  {
+    qtnh::World w(1);
+    double err = 1.0;
+    bool same = false;
+    w.run([&](qtnh::Rank& rk) {
+      std::vector<Complex> g(6 * 4);
+      for (int i = 0; i < 24; ++i) g[i] = {std::cos(1.3 * i), std::sin(0.7 * i * i)};
+      auto t = qtnh::Tensor::from_global(rk, {{6, 4}, 0}, {}, g);
+      auto f = qtnh::linalg::svd(t, {0}, {1}, 0, qtnh::linalg::Absorb::left);
+      auto back = qtnh::network::contract(f.u, f.vh, {1}, {0}).to_global_vector();
+      double num = 0, den = 0;
+      for (int i = 0; i < 24; ++i) {
+        num += std::norm(back[i] - g[i]);
+        den += std::norm(g[i]);
+      }
+      err = std::sqrt(num / den);
+      const std::string path = "/tmp/qtnh_cpp_api_test.qtt";
+      t.save(path);
+      same = qtnh::Tensor::load(rk, path).to_global_vector() == g;
+    });
+    EXPECT(err < 1e-12);
+    EXPECT(same);
   }
   std::printf("cpp api ok\n");
   return 0;
