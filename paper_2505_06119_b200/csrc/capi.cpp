@@ -549,8 +549,12 @@ int qtnh_contract_host(qtnh_rank_t r, int na, const int64_t* dims_a, const doubl
       if (d < 1) throw_invalid("index dimensions must be positive");
     for (Dim d : db)
       if (d < 1) throw_invalid("index dimensions must be positive");
+    static const int chunks = [] {
+      const char* e = std::getenv("QTNH_HOST_CHUNKS");
+      return e ? std::max(1, std::atoi(e)) : 16;
+    }();
     contract_host(x, da, a, db, b, std::vector<int>(a_pos, a_pos + n_pairs), std::vector<int>(b_pos, b_pos + n_pairs),
-                  c, &cd, 16);
+                  c, &cd, chunks);
     if (c_dims)
       for (size_t i = 0; i < cd.size(); ++i) c_dims[i] = cd[i];
   });
