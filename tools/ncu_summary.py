@@ -44,4 +44,7 @@ def summarise(path):
 
 
 if __name__ == "__main__":
-    print(json.dumps(summarise(sys.argv[1]), indent=1))
+    out = []
+    for path in sys.argv[1:]:
+        out.extend(summarise(path))
+    print(json.dumps(out, indent=1))
