@@ -121,48 +121,6 @@ __global__ void __launch_bounds__(kThreads) k_tiled(const double2* __restrict__ 
   }
 }
 
-// Double-buffered form of the transposing path: tile t+grid is fetched by
-// cp.async (16-byte LDGSTS into the swizzled slots) while tile t is written out,
-// so the loads of one tile overlap the stores of the previous one instead of
-// alternating with them behind a barrier.
-__device__ __forceinline__ void cp_async16_sc(void* smem, const void* gmem) {
-  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-
-template <bool CANON>
-__global__ void __launch_bounds__(kThreads) k_tiled_db(const double2* __restrict__ in, double2* __restrict__ out,
-                                                       const int64_t* __restrict__ tin,
-                                                       const int64_t* __restrict__ tout,
-                                                       const int* __restrict__ tslot, int T, int Tpad,
-                                                       int64_t n_tiles, const Outer od) {
-  extern __shared__ double2 sm[];
-  auto issue = [&](int buf, int64_t tile) {
-    int64_t bi, bo;
-    decompose(tile, od, bi, bo);
-    double2* b = sm + buf * Tpad;
-    for (int e = threadIdx.x; e < T; e += kThreads) cp_async16_sc(b + swz(e), in + bi + __ldg(tin + e));
-  };
-  int64_t tile = blockIdx.x;
-  if (tile < n_tiles) issue(0, tile);
-  asm volatile("cp.async.commit_group;\n" ::);
-  for (int it = 0; tile < n_tiles; tile += gridDim.x, ++it) {
-    const int64_t nx = tile + gridDim.x;
-    if (nx < n_tiles) issue((it + 1) & 1, nx);
-    asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 1;\n" ::);
-    __syncthreads();
-    int64_t bi, bo;
-    decompose(tile, od, bi, bo);
-    const double2* b = sm + (it & 1) * Tpad;
-    for (int f = threadIdx.x; f < T; f += kThreads) {
-      double2 v = b[__ldg(tslot + f)];
-      out[bo + __ldg(tout + f)] = CANON ? canon_zero(v) : v;
-    }
-    __syncthreads();  // this buffer is refilled two tiles on
-  }
-}
-
 // Fallback for boxes no tile fits (huge prime dims on both sides): one thread per
 // output element in output order, gathered input.
 struct Full {
@@ -222,7 +180,6 @@ struct Plan {
   int* d_slot = nullptr;
   int grid = 0;
   size_t smem = 0;
-  bool double_buffer = false;  // k_tiled_db (2 x smem)
   ~Plan() {  // only on cache eviction (cudaFree synchronises the device)
     if (d_tin) cudaFree(d_tin);
     if (d_tout) cudaFree(d_tout);
@@ -306,7 +263,11 @@ std::shared_ptr<Plan> build_plan(const std::vector<D>& ds, int dev, cudaStream_t
   std::vector<char> in_tile;
   Dim tile = 1;
   const Dim kMaxTile = 8192;
-  for (Dim min_run : {32, 16, 8, 2}) {
+  static const Dim first_run = [] {
+    const char* e = std::getenv("QTNH_COPY_RUN");
+    return e ? static_cast<Dim>(std::atoi(e)) : 32;
+  }();
+  for (Dim min_run : {first_run, Dim(32), Dim(16), Dim(8), Dim(2)}) {
     in_tile.assign(r, 0);
     Dim prod = 1;
     for (int i = 0; i < r && prod < min_run; ++i) {
@@ -436,25 +397,11 @@ std::shared_ptr<Plan> build_plan(const std::vector<D>& ds, int dev, cudaStream_t
   if (direct) {
     QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tiled<true, true>, kThreads, 0));
   } else {
-    static const bool db_enabled = [] {
-      const char* e = std::getenv("QTNH_COPY_DB");
-      return !(e && e[0] == '0');
-    }();
-    p->double_buffer = db_enabled && 2 * p->smem <= 96 * 1024;
-    if (p->double_buffer) {
-      const int sm2 = static_cast<int>(2 * p->smem);
-      if (sm2 > 48 * 1024) {
-        QTNH_CUDA(cudaFuncSetAttribute(k_tiled_db<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2));
-        QTNH_CUDA(cudaFuncSetAttribute(k_tiled_db<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2));
-      }
-      QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tiled_db<true>, kThreads, 2 * p->smem));
-    } else {
-      if (p->smem > 48 * 1024) {
-        QTNH_CUDA(cudaFuncSetAttribute(k_tiled<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem));
-        QTNH_CUDA(cudaFuncSetAttribute(k_tiled<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem));
-      }
-      QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tiled<true, false>, kThreads, p->smem));
+    if (p->smem > 48 * 1024) {
+      QTNH_CUDA(cudaFuncSetAttribute(k_tiled<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem));
+      QTNH_CUDA(cudaFuncSetAttribute(k_tiled<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem));
     }
+    QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tiled<true, false>, kThreads, p->smem));
   }
   Dim g = static_cast<Dim>(sm_count(dev)) * std::max(1, per_sm);
   p->grid = static_cast<int>(std::max<Dim>(1, std::min<Dim>(g, n_tiles)));
@@ -515,14 +462,8 @@ void strided_copy(const void* in, void* out, const CopyBox& box, bool canon, cud
       else k_tiled<false, true><<<p->grid, kThreads, 0, st>>>(i, o, p->d_tin, p->d_tout, p->d_slot, p->T, p->n_tiles, p->od);
       break;
     case Plan::kTiled:
-      if (p->double_buffer) {
-        const int tpad = static_cast<int>(p->smem / sizeof(double2));
-        if (canon) k_tiled_db<true><<<p->grid, kThreads, 2 * p->smem, st>>>(i, o, p->d_tin, p->d_tout, p->d_slot, p->T, tpad, p->n_tiles, p->od);
-        else k_tiled_db<false><<<p->grid, kThreads, 2 * p->smem, st>>>(i, o, p->d_tin, p->d_tout, p->d_slot, p->T, tpad, p->n_tiles, p->od);
-      } else {
-        if (canon) k_tiled<true, false><<<p->grid, kThreads, p->smem, st>>>(i, o, p->d_tin, p->d_tout, p->d_slot, p->T, p->n_tiles, p->od);
-        else k_tiled<false, false><<<p->grid, kThreads, p->smem, st>>>(i, o, p->d_tin, p->d_tout, p->d_slot, p->T, p->n_tiles, p->od);
-      }
+      if (canon) k_tiled<true, false><<<p->grid, kThreads, p->smem, st>>>(i, o, p->d_tin, p->d_tout, p->d_slot, p->T, p->n_tiles, p->od);
+      else k_tiled<false, false><<<p->grid, kThreads, p->smem, st>>>(i, o, p->d_tin, p->d_tout, p->d_slot, p->T, p->n_tiles, p->od);
       break;
     case Plan::kEmpty:
       return;
