@@ -433,6 +433,64 @@ class MPS:
             t.free()
 
 
+class DistMPS(MPS):
+    """the chain's sites sharded over the world's ranks, rank r
+    owning the contiguous range [lo, hi). A layer's two-site updates on pairs inside
+    a range run as one batched SVD per rank; a pair straddling a boundary
+    (q = hi - 1 here, q + 1 on rank r + 1) is computed here after one site exchange
+    (Rank.exchange_tensors), and the new right site is sent back -- one exchange
+    step per layer each way. Updates act on disjoint pairs, so the result equals the
+    single-rank run (up to the batched SVD's rounding)."""
+
+    def __init__(self, rank: qtnh.Rank, n: int, chi: int, d: int = 2):
+        self.rank, self.n, self.chi, self.d = rank, n, chi, d
+        P, r = rank.size(), rank.rank()
+        if n < 2 * P:
+            raise qtnh.InvalidArgument("DistMPS needs at least two sites per rank")
+        self.lo, self.hi = (r * n) // P, ((r + 1) * n) // P
+        self.log_fidelity = 0.0
+        self.discarded = []
+        self.centre = None
+        self.sites = {}
+        for q in range(self.lo, self.hi):
+            v = np.zeros(d, dtype=np.complex128)
+            v[0] = 1.0
+            self.sites[q] = Tensor.from_global(rank, IndexTuple([1, d, 1], 0), None, v)
+
+    def apply_1q(self, q: int, g: np.ndarray) -> None:
+        if self.lo <= q < self.hi:
+            super().apply_1q(q, g)
+
+    def apply_layer(self, pairs, g):
+        r = self.rank.rank()
+        qs = [q for (q, _) in pairs]
+        inside = [(q, q + 1) for q in qs if self.lo <= q and q + 1 < self.hi]
+        left = [(q, q + 1) for q in qs if q == self.hi - 1 and q + 1 < self.n]   # I compute
+        right = [(q, q + 1) for q in qs if q + 1 == self.lo]                     # rank r-1 computes
+        got = self.rank.exchange_tensors({r - 1: self.sites[self.lo]} if right else {}, [r + 1] if left else [])
+        if left:
+            self.sites[self.hi] = got[r + 1]
+        res = MPS.apply_layer(self, inside + left, g)
+        back = self.rank.exchange_tensors({r + 1: self.sites[self.hi]} if left else {}, [r - 1] if right else [])
+        if left:
+            self.sites.pop(self.hi).free()
+        if right:
+            self.sites[self.lo].free()
+            self.sites[self.lo] = back[r - 1]
+        return res
+
+    def bond_dims(self) -> List[int]:
+        return [self.sites[q].shape().dims[2] for q in range(self.lo, self.hi) if q < self.n - 1]
+
+    def local_sites(self):
+        """{q: numpy array (l, d, r)} of the owned sites."""
+        return {q: t.to_global_vector().reshape(t.shape().dims) for q, t in self.sites.items()}
+
+    def free(self):
+        for t in self.sites.values():
+            t.free()
+
+
 def mpo_from_operator(op: np.ndarray, k: int, d: int = 2) -> List[np.ndarray]:
     """Exact k-site MPO (wl, d_out, d_in, wr) of a d^k x d^k operator (row = output,
     site 0 most significant) by successive SVDs on the host (small operators)."""
@@ -457,19 +515,25 @@ class _DevView:
 
 
 def run_rcs_mps(rank: qtnh.Rank, n: int, depth: int, chi: int, seed: int, layers=None, timer=None,
-                batched: bool = True):
+                batched: bool = True, distributed: bool = False):
     """Evolve |0..0> through the 1-D RCS brickwork; returns the MPS and per-update
-    records (layer, pair, kept fraction)."""
+    records (layer, pair, kept fraction). `distributed`: sites sharded over the
+    world's ranks (DistMPS); records then cover the pairs this rank computed."""
     import torch
 
     rank.set_stream(torch.cuda.current_stream().cuda_stream)
-    m = MPS(rank, n, chi)
+    m = DistMPS(rank, n, chi) if distributed else MPS(rank, n, chi)
     layers = layers if layers is not None else rcs_1d_layers(n, depth, seed)
     recs = []
     for li, (singles, pairs) in enumerate(layers):
         for q, g in enumerate(singles):
             m.apply_1q(q, SINGLE_QUBIT[g])
-        if batched:
+        if distributed:
+            qs = [q for (q, _) in pairs]
+            mine = [q for q in qs if m.lo <= q and q + 1 < m.hi] + [q for q in qs if q == m.hi - 1 and q + 1 < n]
+            for q, (s, frac) in zip(mine, m.apply_layer(pairs, circuits.FSIM)):
+                recs.append((li, q, frac, s))
+        elif batched:
             for (q, _), (s, frac) in zip(pairs, m.apply_layer(pairs, circuits.FSIM)):
                 recs.append((li, q, frac, s))
         else:

@@ -28,7 +28,7 @@ import os
 import threading
 import weakref
 from dataclasses import dataclass, field
-from typing import Callable, List, Optional, Sequence
+from typing import Callable, Dict, List, Optional, Sequence
 
 import numpy as np
 
@@ -147,6 +147,13 @@ def _dist(d) -> DistParams:
     return DistParams(*d)
 
 
+class _DevView:
+    """__cuda_array_interface__ over a device block of complex128."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<c16", "data": (ptr, False), "version": 3}
+
+
 # ---- worlds and ranks ---------------------------------------------------------------
 
 
@@ -184,6 +191,62 @@ class Rank:
 
     def barrier(self) -> None:
         check(lib.qtnh_barrier(self._h))
+
+    def all_to_all_v(self, members: Sequence[int], send_ptr: int, send_counts: Sequence[int],
+                     send_displs: Sequence[int], recv_ptr: int, recv_counts: Sequence[int],
+                     recv_displs: Sequence[int]) -> None:
+        """Group::all_to_all_v (runtime.hpp:448-475) on device buffers of complex128
+        elements, stream-ordered; counts per member in member order."""
+        n = len(members)
+        check(lib.qtnh_all_to_all_v(self._h, n, i32_array(members), C.c_void_p(send_ptr or 0),
+                                    i64_array(send_counts), i64_array(send_displs), C.c_void_p(recv_ptr or 0),
+                                    i64_array(recv_counts), i64_array(recv_displs)))
+
+    def exchange_tensors(self, sends: Dict[int, "Tensor"], recv_from: Sequence[int]) -> Dict[int, "Tensor"]:
+        """Pairwise exchange of undistributed tensors (rank <= 4, any shape) with
+        neighbour ranks. Collective over this rank and its peers; every relation must
+        appear on both sides (if p expects a tensor from this rank, this rank sends
+        one). Two all_to_all_v calls: a 4-element shape header per peer, then the
+        payloads staged through one device buffer per direction."""
+        import torch
+
+        peers = sorted(set(sends) | set(recv_from) | {self._rank})
+        idx = {p: i for i, p in enumerate(peers)}
+        n = len(peers)
+        hdr = np.zeros(4 * n, dtype=np.complex128)
+        for p, t in sends.items():
+            dims = t.shape().dims
+            if len(dims) > 3:
+                raise InvalidArgument("exchange_tensors supports tensors of rank <= 3")
+            hdr[4 * idx[p]:4 * idx[p] + 1 + len(dims)] = [len(dims)] + list(dims)
+        hdr_s = torch.from_numpy(hdr).cuda()
+        hdr_r = torch.zeros(4 * n, dtype=torch.complex128, device="cuda")
+        disp = [4 * i for i in range(n)]
+        torch.cuda.synchronize()
+        self.all_to_all_v(peers, hdr_s.data_ptr(), [4 if p in sends else 0 for p in peers], disp,
+                          hdr_r.data_ptr(), [4 if p in recv_from else 0 for p in peers], disp)
+        self.synchronize()
+        h = hdr_r.cpu().numpy().real.astype(np.int64)
+        shapes = {p: [int(x) for x in h[4 * idx[p] + 1:4 * idx[p] + 1 + int(h[4 * idx[p]])]] for p in recv_from}
+        s_sizes = [int(np.prod(sends[p].shape().dims)) if p in sends else 0 for p in peers]
+        r_sizes = [int(np.prod(shapes[p])) if p in shapes else 0 for p in peers]
+        s_disp = [int(x) for x in np.concatenate([[0], np.cumsum(s_sizes)[:-1]])]
+        r_disp = [int(x) for x in np.concatenate([[0], np.cumsum(r_sizes)[:-1]])]
+        sbuf = torch.empty(max(1, sum(s_sizes)), dtype=torch.complex128, device="cuda")
+        rbuf = torch.empty(max(1, sum(r_sizes)), dtype=torch.complex128, device="cuda")
+        for p, t in sends.items():
+            k = idx[p]
+            sbuf[s_disp[k]:s_disp[k] + s_sizes[k]].copy_(
+                torch.as_tensor(_DevView(t.device_ptr(), s_sizes[k]), device="cuda"))
+        torch.cuda.synchronize()
+        self.all_to_all_v(peers, sbuf.data_ptr(), s_sizes, s_disp, rbuf.data_ptr(), r_sizes, r_disp)
+        self.synchronize()
+        out = {}
+        for p in recv_from:
+            k = idx[p]
+            out[p] = Tensor.from_device(self, IndexTuple(shapes[p], 0), None, rbuf[r_disp[k]:].data_ptr())
+        self.synchronize()  # from_device copies before rbuf dies
+        return out
 
     def release(self) -> None:
         if self._h is None:
