@@ -50,6 +50,7 @@ class MPS:
         self.log_fidelity = 0.0
         self.discarded = []
         self.centre = None
+        self.dist = None  # DistParams of the site tensors (DistMPS: the owning rank)
         for _ in range(n):  # |0...0>, bond dimension 1
             v = np.zeros(d, dtype=np.complex128)
             v[0] = 1.0
@@ -125,8 +126,8 @@ class MPS:
                     self.log_fidelity += np.log(frac)
                 ui = u[i, :, :keep].contiguous()
                 vi = vh[i, :keep, :].contiguous()
-                nu = Tensor.from_device(self.rank, IndexTuple([l, d1, keep], 0), None, ui.data_ptr())
-                nv = Tensor.from_device(self.rank, IndexTuple([keep, d2, r], 0), None, vi.data_ptr())
+                nu = Tensor.from_device(self.rank, IndexTuple([l, d1, keep], 0), self.dist, ui.data_ptr())
+                nv = Tensor.from_device(self.rank, IndexTuple([keep, d2, r], 0), self.dist, vi.data_ptr())
                 self.rank.synchronize()  # the torch temporaries die at the end of the loop
                 self.sites[q].free()
                 self.sites[q + 1].free()
@@ -206,7 +207,7 @@ class MPS:
         E(a, b) <- sum over (a, s, b) of E(a, b) A_s(a, a') conj(B_s(b, b'))."""
         if other.n != self.n or other.d != self.d:
             raise qtnh.InvalidArgument("overlap needs MPS of equal length and physical dimension")
-        env = Tensor.from_global(self.rank, IndexTuple([1, 1], 0), None, np.ones(1, dtype=np.complex128))
+        env = Tensor.from_global(self.rank, IndexTuple([1, 1], 0), self.dist, np.ones(1, dtype=np.complex128))
         for q in range(self.n):
             t1 = qtnh.contract(env, self.sites[q], [0], [0])  # (b, s, a')
             bc = qtnh.ops.conj(other.sites[q])
@@ -257,7 +258,7 @@ class MPS:
         if abs(n2 - 1.0) > 1e-8:
             raise qtnh.PreconditionError("sample needs a normalised MPS (norm2 = %.3e)" % n2)
         self.canonicalize(0)
-        env = Tensor.from_global(self.rank, IndexTuple([1], 0), None, np.ones(1, dtype=np.complex128))
+        env = Tensor.from_global(self.rank, IndexTuple([1], 0), self.dist, np.ones(1, dtype=np.complex128))
         bits = []
         for q in range(self.n):
             v = qtnh.contract(env, self.sites[q], [0], [0])  # (d, r)
@@ -272,13 +273,13 @@ class MPS:
                 s -= 1
             bits.append(s)
             env.free()
-            env = Tensor.from_global(self.rank, IndexTuple([r], 0), None, vh[s] / np.sqrt(p[s]))
+            env = Tensor.from_global(self.rank, IndexTuple([r], 0), self.dist, vh[s] / np.sqrt(p[s]))
         env.free()
         return [bits[q] for q in sites]
 
     def _reshape(self, t: Tensor, dims: Sequence[int]) -> Tensor:
         """Same row-major values under new dims (one device copy)."""
-        out = Tensor.from_device(self.rank, IndexTuple(list(dims), 0), None, t.device_ptr())
+        out = Tensor.from_device(self.rank, IndexTuple(list(dims), 0), self.dist, t.device_ptr())
         t.free()
         return out
 
@@ -354,7 +355,7 @@ class MPS:
             q = first + i
             a = self.sites[q]
             l, _, r = a.shape().dims
-            wt = Tensor.from_global(self.rank, IndexTuple(list(w.shape), 0), None, w.reshape(-1))
+            wt = Tensor.from_global(self.rank, IndexTuple(list(w.shape), 0), self.dist, w.reshape(-1))
             c = qtnh.contract(a, wt, [1], [2])  # (l, r, wl, d_out, wr)
             wt.free()
             p = qtnh.ops.permute(c, [0, 2, 3, 1, 4], 0)  # (l, wl, d_out, r, wr)
@@ -451,11 +452,12 @@ class DistMPS(MPS):
         self.log_fidelity = 0.0
         self.discarded = []
         self.centre = None
+        self.dist = qtnh.DistParams(1, 1, r)  # every site lives on its owner alone
         self.sites = {}
         for q in range(self.lo, self.hi):
             v = np.zeros(d, dtype=np.complex128)
             v[0] = 1.0
-            self.sites[q] = Tensor.from_global(rank, IndexTuple([1, d, 1], 0), None, v)
+            self.sites[q] = Tensor.from_global(rank, IndexTuple([1, d, 1], 0), self.dist, v)
 
     def apply_1q(self, q: int, g: np.ndarray) -> None:
         if self.lo <= q < self.hi:
@@ -467,11 +469,13 @@ class DistMPS(MPS):
         inside = [(q, q + 1) for q in qs if self.lo <= q and q + 1 < self.hi]
         left = [(q, q + 1) for q in qs if q == self.hi - 1 and q + 1 < self.n]   # I compute
         right = [(q, q + 1) for q in qs if q + 1 == self.lo]                     # rank r-1 computes
-        got = self.rank.exchange_tensors({r - 1: self.sites[self.lo]} if right else {}, [r + 1] if left else [])
+        got = self.rank.exchange_tensors({r - 1: self.sites[self.lo]} if right else {}, [r + 1] if left else [],
+                                         self.dist)
         if left:
             self.sites[self.hi] = got[r + 1]
         res = MPS.apply_layer(self, inside + left, g)
-        back = self.rank.exchange_tensors({r + 1: self.sites[self.hi]} if left else {}, [r - 1] if right else [])
+        back = self.rank.exchange_tensors({r + 1: self.sites[self.hi]} if left else {}, [r - 1] if right else [],
+                                          self.dist)
         if left:
             self.sites.pop(self.hi).free()
         if right:

@@ -202,14 +202,19 @@ class Rank:
                                     i64_array(send_counts), i64_array(send_displs), C.c_void_p(recv_ptr or 0),
                                     i64_array(recv_counts), i64_array(recv_displs)))
 
-    def exchange_tensors(self, sends: Dict[int, "Tensor"], recv_from: Sequence[int]) -> Dict[int, "Tensor"]:
+    def exchange_tensors(self, sends: Dict[int, "Tensor"], recv_from: Sequence[int],
+                         dist=None) -> Dict[int, "Tensor"]:
         """Pairwise exchange of undistributed tensors (rank <= 4, any shape) with
         neighbour ranks. Collective over this rank and its peers; every relation must
         appear on both sides (if p expects a tensor from this rank, this rank sends
         one). Two all_to_all_v calls: a 4-element shape header per peer, then the
-        payloads staged through one device buffer per direction."""
+        payloads staged through one device buffer per direction. Received tensors get
+        `dist` (e.g. DistParams(1, 1, my rank) so they live on this rank)."""
         import torch
 
+        # the tensors' blocks come from the rank stream's pool: drain it before torch
+        # (another stream) touches them
+        self.synchronize()
         peers = sorted(set(sends) | set(recv_from) | {self._rank})
         idx = {p: i for i, p in enumerate(peers)}
         n = len(peers)
@@ -244,7 +249,7 @@ class Rank:
         out = {}
         for p in recv_from:
             k = idx[p]
-            out[p] = Tensor.from_device(self, IndexTuple(shapes[p], 0), None, rbuf[r_disp[k]:].data_ptr())
+            out[p] = Tensor.from_device(self, IndexTuple(shapes[p], 0), dist, rbuf[r_disp[k]:].data_ptr())
         self.synchronize()  # from_device copies before rbuf dies
         return out
 
