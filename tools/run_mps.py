@@ -19,6 +19,9 @@ def main():
     ap.add_argument("--seed", type=int, default=2025)
     ap.add_argument("--bitstrings", type=int, default=1024)
     ap.add_argument("--sequential", action="store_true", help="one SVD per update instead of batched layers")
+    ap.add_argument("--world", type=int, default=1,
+                    help="ranks (thread per rank, round-robin over the visible GPUs); > 1 shards the sites "
+                         "(DistMPS, one site exchange per boundary per layer)")
     ap.add_argument("--reserve-gb", type=float, default=48,
                     help="map this much of the stream-ordered pool up front (option pool_reserve_gb)")
     args = ap.parse_args()
@@ -34,11 +37,14 @@ def main():
     out = {"n": args.n, "depth": args.depth, "chi": args.chi}
     layers = mps.rcs_1d_layers(args.n, args.depth, args.seed)
 
+    logf = {}
+
     def body(rk):
         torch.cuda.synchronize()
+        rk.barrier()
         t0 = time.perf_counter()
         rk.set_stream(torch.cuda.current_stream().cuda_stream)
-        m = mps.MPS(rk, args.n, args.chi)
+        m = mps.DistMPS(rk, args.n, args.chi) if args.world > 1 else mps.MPS(rk, args.n, args.chi)
         per_layer = []
         upd = 0
         for li, (singles, pairs) in enumerate(layers):
@@ -53,7 +59,14 @@ def main():
             upd += len(pairs)
             torch.cuda.synchronize()
             per_layer.append(time.perf_counter() - tl)
+        rk.barrier()
         total = time.perf_counter() - t0
+        logf[rk.rank()] = m.log_fidelity
+        if args.world > 1:
+            if rk.rank() == 0:
+                out.update(total_s=total, per_layer_s=per_layer, updates=upd, world=args.world)
+            m.free()
+            return
         rng = np.random.default_rng(args.seed)
         bits = rng.integers(0, 2, size=(args.bitstrings, args.n))
         ta = time.perf_counter()
@@ -63,7 +76,11 @@ def main():
                    amp_norm2_sum=float(np.sum(np.abs(amps) ** 2)), amp_first=[str(a) for a in amps[:4]])
         m.free()
 
-    World(1).run(body)
+    ngpu = max(1, torch.cuda.device_count())
+    World(args.world, devices=[r % ngpu for r in range(args.world)]).run(body)
+    if args.world > 1:
+        out["fidelity"] = float(np.exp(sum(logf.values())))
+        out["gpus"] = min(ngpu, args.world)
     print(json.dumps(out))
 
 
