@@ -469,18 +469,20 @@ class DistMPS(MPS):
         inside = [(q, q + 1) for q in qs if self.lo <= q and q + 1 < self.hi]
         left = [(q, q + 1) for q in qs if q == self.hi - 1 and q + 1 < self.n]   # I compute
         right = [(q, q + 1) for q in qs if q + 1 == self.lo]                     # rank r-1 computes
-        got = self.rank.exchange_tensors({r - 1: self.sites[self.lo]} if right else {}, [r + 1] if left else [],
-                                         self.dist)
+        # pairwise collectives, the one with the left neighbour first: a rank that
+        # meets both neighbours in one layer finishes with r - 1 before r + 1, so
+        # the waits form a chain, never a cycle
+        if right:
+            self.rank.exchange_tensors({r - 1: self.sites[self.lo]}, [], self.dist)
         if left:
-            self.sites[self.hi] = got[r + 1]
+            self.sites[self.hi] = self.rank.exchange_tensors({}, [r + 1], self.dist)[r + 1]
         res = MPS.apply_layer(self, inside + left, g)
-        back = self.rank.exchange_tensors({r + 1: self.sites[self.hi]} if left else {}, [r - 1] if right else [],
-                                          self.dist)
-        if left:
-            self.sites.pop(self.hi).free()
         if right:
             self.sites[self.lo].free()
-            self.sites[self.lo] = back[r - 1]
+            self.sites[self.lo] = self.rank.exchange_tensors({}, [r - 1], self.dist)[r - 1]
+        if left:
+            self.rank.exchange_tensors({r + 1: self.sites[self.hi]}, [], self.dist)
+            self.sites.pop(self.hi).free()
         return res
 
     def bond_dims(self) -> List[int]:

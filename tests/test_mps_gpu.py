@@ -121,7 +121,8 @@ def test_mps_untruncated_matches_statevector():
     assert rel_l2(amps, psi) < TOL
 
 
-@pytest.mark.parametrize("world,n,chi", [(2, 10, 8), (3, 10, 4), (4, 12, 16)])
+@pytest.mark.parametrize("world,n,chi", [(2, 10, 8), (3, 10, 4), (4, 12, 16),
+                                         (4, 16, 8)])  # boundaries 3, 7, 11: both neighbours per layer
 def test_distributed_mps_matches_single_rank(world, n, chi):
     """sites sharded over ranks, boundary pairs after one site
     exchange per layer; the final state and the total kept weight equal the
