@@ -20,12 +20,23 @@ from .qtnh import IndexTuple, Tensor
 
 
 class Network:
-    def __init__(self, rank: qtnh.Rank):
+    """Labelled tensors on one rank, or -- in a world of P > 1 ranks (SURVEY.md 8(e)
+    C3) -- replicated on every rank (DistParams(1, P, 0)): small contractions then
+    run as replicas, and a contraction of at least `shard_flops` is M-sharded like
+    C1: its first operand gets log2 P of its open qubit indices distributed
+    (rebcast to one copy, permute with a new split), the other operand stays
+    replicated, and the result stays sharded for the next steps (a contraction
+    of two sharded operands replicates the smaller one first)."""
+
+    def __init__(self, rank: qtnh.Rank, shard_flops: float = 1e11):
         self.rank = rank
         self.tensors: Dict[int, Tensor] = {}
         self.labels: Dict[int, List[str]] = {}
         self.dims: Dict[str, int] = {}
         self._next = 0
+        self.world = rank.size()
+        self.shard_flops = shard_flops
+        self.rep = qtnh.DistParams(1, self.world, 0)
 
     def add(self, data: np.ndarray, labels: Sequence[str]) -> int:
         data = np.ascontiguousarray(data, dtype=np.complex128)
@@ -34,7 +45,7 @@ class Network:
         for lab, d in zip(labels, shape):
             if self.dims.setdefault(lab, d) != d:
                 raise qtnh.InvalidArgument(f"bond {lab} has inconsistent dimensions")
-        t = Tensor.from_global(self.rank, IndexTuple(shape, 0), None, data.reshape(-1))
+        t = Tensor.from_global(self.rank, IndexTuple(shape, 0), self.rep, data.reshape(-1))
         i = self._next
         self._next += 1
         self.tensors[i] = t
@@ -133,12 +144,63 @@ class Network:
                 best = (key, order)
         return best[1]
 
+    # ---- multi-rank placement ---------------------------------------------------------
+    def _replicate(self, t: Tensor) -> Tensor:
+        """A copy of t on every rank (split 0, DistParams(1, P, 0))."""
+        u = qtnh.ops.permute(t, list(range(t.shape().n_idx())), 0) if t.shape().split else t
+        v = qtnh.ops.rebcast(u, self.rep)
+        if u is not t:
+            u.free()
+        return v
+
+    def _shard(self, t: Tensor, labels: List[str], avoid) -> Tuple[Optional[Tensor], List[str]]:
+        """Distribute open indices of t (product = P) over the world; None if the
+        labels do not allow it."""
+        P, pick, prod = self.world, [], 1
+        for i, lab in enumerate(labels):
+            if lab in avoid or prod * self.dims[lab] > P:
+                continue
+            pick.append(i)
+            prod *= self.dims[lab]
+            if prod == P:
+                break
+        if prod != P:
+            return None, labels
+        perm = pick + [i for i in range(len(labels)) if i not in pick]
+        one = qtnh.ops.rebcast(t, qtnh.DistParams(1, 1, 0))
+        out = qtnh.ops.permute(one, perm, len(pick))
+        one.free()
+        return out, [labels[i] for i in perm]
+
     def contract_pair(self, a: int, b: int, new_id: Optional[int] = None) -> int:
         la, lb = self.labels[a], self.labels[b]
+        ta, tb = self.tensors[a], self.tensors[b]
+        temps = []
+        if self.world > 1:
+            sa, sb = ta.shape().split, tb.shape().split
+            if sb > 0 and sa == 0:  # the sharded operand goes first (its open indices lead the result)
+                la, lb, ta, tb = lb, la, tb, ta
+                sa, sb = sb, sa
+            if sa > 0 and sb > 0:  # replicate the smaller, keep the larger sharded
+                if int(np.prod(tb.shape().dims)) > int(np.prod(ta.shape().dims)):
+                    la, lb, ta, tb = lb, la, tb, ta
+                tb = self._replicate(tb)
+                temps.append(tb)
+            elif sa == 0:
+                shared = set(la) & set(lb)
+                flops = 8.0 * float(np.prod([self.dims[x] for x in la if x not in shared] or [1])) * \
+                    float(np.prod([self.dims[x] for x in lb] or [1]))
+                if flops >= self.shard_flops:
+                    s_t, s_l = self._shard(ta, la, shared)
+                    if s_t is not None:
+                        ta, la = s_t, s_l
+                        temps.append(s_t)
         shared = [x for x in la if x in lb]
         apos = [la.index(x) for x in shared]
         bpos = [lb.index(x) for x in shared]
-        c = qtnh.contract(self.tensors[a], self.tensors[b], apos, bpos)
+        c = qtnh.contract(ta, tb, apos, bpos)
+        for t in temps:
+            t.free()
         new = [x for x in la if x not in shared] + [x for x in lb if x not in shared]
         self.tensors.pop(a).free()
         self.tensors.pop(b).free()
@@ -199,11 +261,12 @@ def output_bits(n: int, n_open: int, seed: int):
     return open_q, fixed
 
 
-def build_rcs_network(rank: qtnh.Rank, rows: int, cols: int, depth: int, seed: int, n_open: int = 6):
+def build_rcs_network(rank: qtnh.Rank, rows: int, cols: int, depth: int, seed: int, n_open: int = 6,
+                      shard_flops: float = 1e11):
     from .mps import SINGLE_QUBIT
 
     n = rows * cols
-    net = Network(rank)
+    net = Network(rank, shard_flops)
     wire = [f"q{q}.0" for q in range(n)]
     ver = [0] * n
     for q in range(n):

@@ -76,6 +76,35 @@ def test_grid_tn_vs_statevector_and_reference(rows, cols, depth, n_open):
     assert rel_l2(got, ref) < TOL
 
 
+@pytest.mark.parametrize("world,shard_flops", [(2, 0.0), (4, 0.0), (4, 1e6), (8, 1e5)])
+def test_sharded_network_contraction(world, shard_flops):
+    """replicated small contractions, M-sharded large ones (a
+    sharded result stays sharded; two sharded operands replicate the smaller)."""
+    rows, cols, depth, n_open, seed = 3, 3, 6, 3, 7
+
+    def body(rk):
+        net, open_labels, open_q, fixed = network.build_rcs_network(rk, rows, cols, depth, seed, n_open,
+                                                                    shard_flops=shard_flops)
+        order = network.Network.plan(net.labels, net.dims, seed)
+        last = net.contract_order(order)
+        res_labels = net.labels[last]
+        v = net.tensors[last].to_global_vector()
+        net.tensors[last].free()
+        if v.size == 0:
+            return None
+        out = v.reshape([2] * len(res_labels))
+        out = np.transpose(out, [res_labels.index(l) for l in open_labels]).reshape(-1)
+        return out, open_q, fixed
+
+    res = [r for r in World(world).run(body) if r is not None]
+    assert res
+    P = oracle.port()
+    _, open_q, fixed = res[0]
+    want = statevector_amplitudes(rows, cols, depth, seed, open_q, fixed, P)
+    for got, _, _ in res:
+        assert rel_l2(got, want) < TOL
+
+
 def test_grid_patterns():
     # SPEC.md:652-656 examples
     assert network.grid_pairs("A", 1, 2) == [(0, 1)]
