@@ -37,6 +37,8 @@ class Network:
         self.world = rank.size()
         self.shard_flops = shard_flops
         self.rep = qtnh.DistParams(1, self.world, 0)
+        self.n_sharded = 0      # contractions run M-sharded
+        self.n_replicated = 0   # sharded operands gathered back to replicas
 
     def add(self, data: np.ndarray, labels: Sequence[str]) -> int:
         data = np.ascontiguousarray(data, dtype=np.complex128)
@@ -186,6 +188,7 @@ class Network:
                     la, lb, ta, tb = lb, la, tb, ta
                 tb = self._replicate(tb)
                 temps.append(tb)
+                self.n_replicated += 1
             elif sa == 0:
                 shared = set(la) & set(lb)
                 flops = 8.0 * float(np.prod([self.dims[x] for x in la if x not in shared] or [1])) * \
@@ -195,6 +198,8 @@ class Network:
                     if s_t is not None:
                         ta, la = s_t, s_l
                         temps.append(s_t)
+            if ta.shape().split > 0:
+                self.n_sharded += 1
         shared = [x for x in la if x in lb]
         apos = [la.index(x) for x in shared]
         bpos = [lb.index(x) for x in shared]

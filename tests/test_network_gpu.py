@@ -94,14 +94,15 @@ def test_sharded_network_contraction(world, shard_flops):
             return None
         out = v.reshape([2] * len(res_labels))
         out = np.transpose(out, [res_labels.index(l) for l in open_labels]).reshape(-1)
-        return out, open_q, fixed
+        return out, open_q, fixed, net.n_sharded, net.n_replicated
 
     res = [r for r in World(world).run(body) if r is not None]
     assert res
+    assert res[0][3] > 0  # some contractions ran sharded
     P = oracle.port()
-    _, open_q, fixed = res[0]
+    _, open_q, fixed, _, _ = res[0]
     want = statevector_amplitudes(rows, cols, depth, seed, open_q, fixed, P)
-    for got, _, _ in res:
+    for got, *_ in res:
         assert rel_l2(got, want) < TOL
 
 
