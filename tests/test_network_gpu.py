@@ -76,7 +76,7 @@ def test_grid_tn_vs_statevector_and_reference(rows, cols, depth, n_open):
     assert rel_l2(got, ref) < TOL
 
 
-@pytest.mark.parametrize("world,shard_flops", [(2, 0.0), (4, 0.0), (4, 1e6), (8, 1e5)])
+@pytest.mark.parametrize("world,shard_flops", [(2, 0.0), (4, 0.0), (4, 1e4), (8, 0.0)])
 def test_sharded_network_contraction(world, shard_flops):
     """replicated small contractions, M-sharded large ones (a
     sharded result stays sharded; two sharded operands replicate the smaller)."""
