@@ -23,6 +23,10 @@ def main():
     ap.add_argument("--seed", type=int, default=2025)
     ap.add_argument("--no-statevector", action="store_true")
     ap.add_argument("--trials", type=int, default=24)
+    ap.add_argument("--world", type=int, default=1,
+                    help="ranks (thread per rank over the visible GPUs): tensors replicated, contractions of "
+                         ">= --shard-flops M-sharded")
+    ap.add_argument("--shard-flops", type=float, default=1e11)
     ap.add_argument("--reserve-gb", type=float, default=120,
                     help="map this much of the stream-ordered pool up front (option pool_reserve_gb)")
     args = ap.parse_args()
@@ -37,14 +41,28 @@ def main():
 
     out = {"rows": args.rows, "cols": args.cols, "depth": args.depth, "open": args.open}
 
+    import threading
+
+    planned = threading.Event()
+    shared = {}
+
     def body(rk):
         rk.set_stream(torch.cuda.current_stream().cuda_stream)
         net, open_labels, open_q, fixed = network.build_rcs_network(rk, args.rows, args.cols, args.depth,
-                                                                    args.seed, args.open)
-        out["n_tensors"] = len(net.tensors)
-        t0 = time.perf_counter()
-        order = network.Network.plan(net.labels, net.dims, args.seed, trials=args.trials)
-        out["plan_s"] = time.perf_counter() - t0
+                                                                    args.seed, args.open, args.shard_flops)
+        if rk.rank() == 0:  # the order is host-only and identical on every rank: plan once
+            out["n_tensors"] = len(net.tensors)
+            t0 = time.perf_counter()
+            shared["order"] = network.Network.plan(net.labels, net.dims, args.seed, trials=args.trials)
+            out["plan_s"] = time.perf_counter() - t0
+            planned.set()
+        planned.wait()
+        order = shared["order"]
+        if rk.rank() != 0:
+            last = net.contract_order(order)
+            net.tensors[last].to_global_vector()  # collective when the result is sharded
+            net.tensors[last].free()
+            return
         # cost of the order (SURVEY.md 8(d) C3 convention)
         labels = {k: list(v) for k, v in net.labels.items()}
         nxt = max(labels) + 1
@@ -69,6 +87,8 @@ def main():
         last = net.contract_order(order)
         e1.record()
         e1.synchronize()
+        out["world"] = args.world
+        out["sharded_contractions"] = net.n_sharded
         out["contract_s_wall"] = time.perf_counter() - t0
         out["contract_s_device"] = e0.elapsed_time(e1) / 1e3
         out["achieved_TFLOPs"] = flops / out["contract_s_device"] / 1e12
@@ -77,7 +97,7 @@ def main():
         amp = np.transpose(amp, [res_labels.index(l) for l in open_labels]).reshape(-1)
         net.tensors[last].free()
         out["amp_norm2"] = float(np.sum(np.abs(amp) ** 2))
-        if not args.no_statevector:
+        if not args.no_statevector and args.world == 1:
             n = args.rows * args.cols
             st = Tensor.dense(rk, IndexTuple([2] * n, 0), None, None)
             one = torch.zeros(1, dtype=torch.complex128)
@@ -98,7 +118,8 @@ def main():
             out["rel_l2_vs_statevector"] = float(np.linalg.norm(amp - want) / np.linalg.norm(want))
             st.free()
 
-    World(1).run(body)
+    ngpu = max(1, torch.cuda.device_count())
+    World(args.world, devices=[r % ngpu for r in range(args.world)]).run(body)
     print(json.dumps(out))
 
 
