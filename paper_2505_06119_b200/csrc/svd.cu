@@ -93,8 +93,7 @@ template <int B>
 __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__ part, double2* __restrict__ wh,
                                                      int* __restrict__ flags, double* __restrict__ off_max,
                                                      int npairs, int splits, double tol, int inner_sweeps,
-                                                     const double* __restrict__ floor_abs,
-                                                     const double* __restrict__ thr, double* __restrict__ off_top) {
+                                                     const double* __restrict__ floor_abs) {
   constexpr int P2 = 2 * B, LD = P2 + 1;
   const int pair = blockIdx.x, mat = blockIdx.y, tid = threadIdx.x;
   const double fl = floor_abs[mat];
@@ -140,29 +139,6 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
     __syncthreads();
     return res;
   };
-  if (thr) {  // statistics: off-diagonal measure over pairs touching a row above thr
-    const double th = thr[mat];
-    double mx = 0.0;
-    for (int e = tid; e < P2 * P2; e += 256) {
-      int i = e / P2, j = e % P2;
-      if (i >= j) continue;
-      if (fmax(G[i * LD + i].x, G[j * LD + j].x) < th) continue;
-      double d = sqrt(fmax(G[i * LD + i].x * G[j * LD + j].x, 0.0));
-      double2 gij = G[i * LD + j];
-      double g = hypot(gij.x, gij.y);
-      double den = fmax(d, fl);
-      if (den > 0.0) mx = fmax(mx, g / den);
-      else if (g > 0.0) mx = fmax(mx, 1.0);
-    }
-    red[tid] = mx;
-    __syncthreads();
-    for (int st = 128; st > 0; st >>= 1) {
-      if (tid < st) red[tid] = fmax(red[tid], red[tid + st]);
-      __syncthreads();
-    }
-    if (tid == 0) atomic_max_nonneg(off_top + mat, red[0]);
-    __syncthreads();
-  }
   double off = measure();
   if (tid == 0) atomic_max_nonneg(off_max + mat, off);
   const int64_t fidx = static_cast<int64_t>(mat) * npairs + pair;
@@ -599,7 +575,8 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
       tab[(rd * npairs + k) * 2] = p;
       tab[(rd * npairs + k) * 2 + 1] = q;
     }
-  int splits = static_cast<int>(std::max<Dim>(1, std::min<Dim>((2 * sms() + npairs * batch - 1) / (npairs * batch),
+  const Dim per_group = batch >= 2 ? (batch + 1) / 2 : batch;  // see the two-stream split below
+  int splits = static_cast<int>(std::max<Dim>(1, std::min<Dim>((2 * sms() + npairs * per_group - 1) / (npairs * per_group),
                                                                 (L + kGramCols - 1) / kGramCols)));
   DevBuf wk(static_cast<size_t>(batch * rp * W) * 16, r);
   DevBuf d_tab(tab.size() * sizeof(int), r);
@@ -626,67 +603,105 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_eigen_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_smem));
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_gram_mma_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem));
-  std::vector<double> off_h(batch);
-  int sweep = 0;
-  const int max_sweeps = 40;
-  bool converged = false;
-  const unsigned ctiles = static_cast<unsigned>(
-      std::min<Dim>((W + 47) / 48, std::max<Dim>(1, (B == 16 ? 8 : 4) * sms() / (npairs * batch))));
-  const bool stats = std::getenv("QTNH_SVD_DEBUG") && chi < rows;
-  DevBuf thr_d(static_cast<size_t>(batch) * sizeof(double), r), offt(static_cast<size_t>(batch) * sizeof(double), r);
-  DevBuf sig0(static_cast<size_t>(batch * rp) * sizeof(double), r);
-  std::vector<double> thr_h(batch), offt_h(batch);
-  for (; sweep < max_sweeps; ++sweep) {
-    QTNH_CUDA(cudaMemsetAsync(offm.ptr, 0, batch * sizeof(double), st));
-    if (stats) {
-      QTNH_CUDA(cudaMemsetAsync(offt.ptr, 0, batch * sizeof(double), st));
-      k_svd_norms<<<dim3(static_cast<unsigned>(rp), static_cast<unsigned>(batch)), 256, 0, st>>>(
-          static_cast<const double2*>(wk.ptr), static_cast<double*>(sig0.ptr), rp, L, qw);
-      std::vector<double> nh(batch * rp);
-      QTNH_CUDA(cudaMemcpyAsync(nh.data(), sig0.ptr, nh.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
-      QTNH_CUDA(cudaStreamSynchronize(st));
-      for (Dim b = 0; b < batch; ++b) {
-        std::vector<double> v(nh.begin() + b * rp, nh.begin() + (b + 1) * rp);
-        std::nth_element(v.begin(), v.begin() + (chi - 1), v.end(), std::greater<double>());
-        thr_h[b] = 0.5 * v[chi - 1] * v[chi - 1];
-      }
-      QTNH_CUDA(cudaMemcpyAsync(thr_d.ptr, thr_h.data(), batch * sizeof(double), cudaMemcpyHostToDevice, st));
-    }
-    for (int rd = 0; rd < rounds; ++rd) {
-      k_svd_gram_mma_t<B><<<dim3(npairs, splits, static_cast<unsigned>(batch)), B * 8, gram_smem, st>>>(
-          static_cast<const double2*>(wk.ptr), static_cast<double2*>(part.ptr), static_cast<const int*>(d_tab.ptr),
-          rd, npairs, splits, rp, L, qw);
-      QTNH_LAUNCH_CHECK();
-      k_svd_eigen_t<B><<<dim3(npairs, static_cast<unsigned>(batch)), 256, eig_smem, st>>>(
-            static_cast<const double2*>(part.ptr), static_cast<double2*>(whb.ptr), static_cast<int*>(flags.ptr),
-            static_cast<double*>(offm.ptr), npairs, splits, tol, inner_sweeps(),
-            static_cast<const double*>(floor_abs.ptr), stats ? static_cast<const double*>(thr_d.ptr) : nullptr,
-            static_cast<double*>(offt.ptr));
-      QTNH_LAUNCH_CHECK();
-      k_svd_update_mma_t<B><<<dim3(ctiles, npairs, static_cast<unsigned>(batch)), B * 8, upd_smem, st>>>(
-          static_cast<double2*>(wk.ptr), static_cast<const double2*>(whb.ptr), static_cast<const int*>(flags.ptr),
-          static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
-      QTNH_LAUNCH_CHECK();
-    }
-    QTNH_CUDA(cudaMemcpyAsync(off_h.data(), offm.ptr, batch * sizeof(double), cudaMemcpyDeviceToHost, st));
-    QTNH_CUDA(cudaStreamSynchronize(st));
-    double mx = *std::max_element(off_h.begin(), off_h.end());
-    if (stats) {
-      QTNH_CUDA(cudaMemcpy(offt_h.data(), offt.ptr, batch * sizeof(double), cudaMemcpyDeviceToHost));
-      std::fprintf(stderr, "svd sweep %d max_off %.3e top_off %.3e thr %.3e\n", sweep, mx,
-                   *std::max_element(offt_h.begin(), offt_h.end()), thr_h[0]);
-    } else if (std::getenv("QTNH_SVD_DEBUG")) {
-      std::fprintf(stderr, "svd sweep %d max_off %.3e\n", sweep, mx);
-    }
-    if (mx < tol) {
-      converged = true;
-      ++sweep;
-      break;
+  // The batch runs as two independent halves on two streams when it has >= 2
+  // matrices: the latency-bound eigen step of one half overlaps the other half's
+  // Gram / update DMMA work, and a half that converges stops early.
+  const int ngroups = batch >= 2 ? 2 : 1;
+  struct Group {
+    Dim base = 0, cnt = 0;
+    cudaStream_t s = nullptr;
+    bool done = false;
+    int sweeps = 0;
+  };
+  std::vector<Group> grp(ngroups);
+  std::vector<cudaEvent_t> evs(ngroups + 1);
+  for (auto& e : evs) QTNH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  QTNH_CUDA(cudaEventRecord(evs[ngroups], st));
+  for (int g = 0; g < ngroups; ++g) {
+    grp[g].base = g * batch / ngroups;
+    grp[g].cnt = (g + 1) * batch / ngroups - grp[g].base;
+    if (ngroups == 1) {
+      grp[g].s = st;
+    } else {
+      QTNH_CUDA(cudaStreamCreateWithFlags(&grp[g].s, cudaStreamNonBlocking));
+      QTNH_CUDA(cudaStreamWaitEvent(grp[g].s, evs[ngroups], 0));
     }
   }
+  std::vector<double> off_h(batch);
+  const int max_sweeps = 40;
+  const Dim gmax = (batch + ngroups - 1) / ngroups;
+  const unsigned ctiles = static_cast<unsigned>(
+      std::min<Dim>((W + 47) / 48, std::max<Dim>(1, (B == 16 ? 8 : 4) * sms() / (npairs * gmax))));
+  auto cleanup = [&] {
+    for (int g = 0; g < ngroups; ++g) {
+      if (ngroups > 1) {
+        cudaEventRecord(evs[g], grp[g].s);
+        cudaStreamWaitEvent(st, evs[g], 0);
+      }
+    }
+    cudaStreamSynchronize(st);
+    for (int g = 0; g < ngroups; ++g)
+      if (ngroups > 1) cudaStreamDestroy(grp[g].s);
+    for (auto& e : evs) cudaEventDestroy(e);
+  };
+  int sweep = 0;
+  try {
+    for (; sweep < max_sweeps; ++sweep) {
+      for (auto& G : grp)
+        if (!G.done) QTNH_CUDA(cudaMemsetAsync(static_cast<double*>(offm.ptr) + G.base, 0, G.cnt * 8, G.s));
+      for (int rd = 0; rd < rounds; ++rd)
+        for (auto& G : grp) {
+          if (G.done) continue;
+          const unsigned cnt = static_cast<unsigned>(G.cnt);
+          double2* wkg = static_cast<double2*>(wk.ptr) + G.base * rp * W;
+          double2* partg = static_cast<double2*>(part.ptr) + G.base * npairs * splits * P2 * P2;
+          double2* whg = static_cast<double2*>(whb.ptr) + G.base * npairs * P2 * P2;
+          int* flg = static_cast<int*>(flags.ptr) + G.base * npairs;
+          k_svd_gram_mma_t<B><<<dim3(npairs, splits, cnt), B * 8, gram_smem, G.s>>>(
+              wkg, partg, static_cast<const int*>(d_tab.ptr), rd, npairs, splits, rp, L, qw);
+          QTNH_LAUNCH_CHECK();
+          k_svd_eigen_t<B><<<dim3(npairs, cnt), 256, eig_smem, G.s>>>(
+              partg, whg, flg, static_cast<double*>(offm.ptr) + G.base, npairs, splits, tol, inner_sweeps(),
+              static_cast<const double*>(floor_abs.ptr) + G.base);
+          QTNH_LAUNCH_CHECK();
+          k_svd_update_mma_t<B><<<dim3(ctiles, npairs, cnt), B * 8, upd_smem, G.s>>>(
+              wkg, whg, flg, static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
+          QTNH_LAUNCH_CHECK();
+        }
+      for (auto& G : grp)
+        if (!G.done)
+          QTNH_CUDA(cudaMemcpyAsync(off_h.data() + G.base, static_cast<double*>(offm.ptr) + G.base, G.cnt * 8,
+                                    cudaMemcpyDeviceToHost, G.s));
+      bool all = true;
+      for (auto& G : grp) {
+        if (G.done) continue;
+        QTNH_CUDA(cudaStreamSynchronize(G.s));
+        const double mx = *std::max_element(off_h.begin() + G.base, off_h.begin() + G.base + G.cnt);
+        if (std::getenv("QTNH_SVD_DEBUG")) std::fprintf(stderr, "svd sweep %d group %d max_off %.3e\n", sweep,
+                                                       static_cast<int>(&G - grp.data()), mx);
+        if (mx < tol) {
+          G.done = true;
+          G.sweeps = sweep + 1;
+        } else {
+          all = false;
+        }
+      }
+      if (all) break;
+    }
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+  int sw = 0;
+  bool converged = true;
+  for (auto& G : grp) {
+    converged = converged && G.done;
+    sw = std::max(sw, G.done ? G.sweeps : max_sweeps);
+  }
   if (!converged)
-    throw Status(QTNH_E_NUMERICAL, "SVD failed to converge (info=" + std::to_string(sweep) + ")", sweep);
-  if (sweeps_out) *sweeps_out = sweep;
+    throw Status(QTNH_E_NUMERICAL, "SVD failed to converge (info=" + std::to_string(sw) + ")", sw);
+  if (sweeps_out) *sweeps_out = sw;
   DevBuf sig(static_cast<size_t>(batch * rp) * sizeof(double), r);
   k_svd_norms<<<dim3(static_cast<unsigned>(rp), static_cast<unsigned>(batch)), 256, 0, st>>>(
       static_cast<const double2*>(wk.ptr), static_cast<double*>(sig.ptr), rp, L, qw);
