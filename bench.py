@@ -133,6 +133,18 @@ def cpu_reference_sample(budget_s: float = 15.0, rank_a: int = 22):
             "reference")
 
 
+def c1_config(world_size: int) -> dict:
+    """The workload both arms report (BASELINE.json configs[1], weak-scaled)."""
+    s = (world_size - 1).bit_length() if world_size > 1 else 0
+    rank_a_global = RANK_A + s
+    return {"workload": "C1: A rank-%d (dims 2, %d distributed) x B rank-14, 7 shared indices at "
+                        "seeded random positions; result rank-%d in open(A),open(B) order"
+                        % (rank_a_global, s, rank_a_global),
+            "global_batch": 1, "per_gpu_elements_A": 2**RANK_A,
+            "parallelism": f"M-sharded over {world_size} GPU(s) (A's leading open indices)",
+            "l2": "inputs (4 GiB A, 4 GiB result per GPU) exceed the 126 MB L2"}
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -148,8 +160,10 @@ def run_reference_arm(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (seeded counter-based normals)",
-            "config": {"workload": "C1 sample: rank-22 A x rank-14 B, 7 shared indices (host cores)"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+            "config": c1_config(args.gpus),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": sample + "; each step is this bounded sample of the config's workload "
+                                                "(same seeded generator, positions and B)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -423,12 +437,7 @@ def run_gpu_arm(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "c128 (f64)",
             "data": "synthetic (seeded counter-based complex normals, common.hpp hash_counter + Box-Muller)",
-            "config": {"workload": "C1: A rank-%d (dims 2, %d distributed) x B rank-14, 7 shared indices at "
-                                   "seeded random positions; result rank-%d in open(A),open(B) order"
-                                   % (rank_a_global, s, rank_a_global),
-                       "global_batch": 1, "per_gpu_elements_A": 2**RANK_A,
-                       "parallelism": f"M-sharded over {world_size} GPU(s) (A's leading open indices)",
-                       "l2": "inputs (4 GiB A, 4 GiB result per GPU) exceed the 126 MB L2"},
+            "config": c1_config(world_size),
             "roofline": {"bound": "tensor", "kernel": kname,
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "peak_source": "DMMA-only microbenchmark run live on this device (MEASURED_PEAKS.json "
