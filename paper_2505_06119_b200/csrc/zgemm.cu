@@ -111,15 +111,13 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
     return co_s[k];
   };
   const int wm = warp / G::WARPS_N, wn = warp % G::WARPS_N;
-  // 1-D tile order, N tiles fastest: the CTAs sharing a row block of A run
-  // together (A read once from HBM). Persistent CTAs walk tiles blockIdx.x,
-  // blockIdx.x + gridDim.x, ... with ONE cp.async pipeline across tile
-  // boundaries: the next tile's first stages load during this tile's last
-  // k-steps and epilogue, so no tile starts with an empty pipeline.
+  // 1-D grid, N tiles fastest: the CTAs sharing a row block of A run together
+  // (A read once from HBM), and M is not limited by gridDim.y.
   const int64_t n_tiles_n = (N + BN - 1) / BN;
-  const int64_t n_tiles = ((M + BM - 1) / BM) * n_tiles_n;
+  const int64_t tile = blockIdx.x;
+  const int64_t bm = (tile / n_tiles_n) * BM;
+  const int64_t bn = (tile % n_tiles_n) * BN;
   const int64_t n_kt = (K + BK - 1) / BK;
-  int64_t bm = 0, bn = 0;  // issue-side tile origin
 
   // Per-thread source rows / columns are fixed; only k advances by BK per stage.
   constexpr int LA = (BM * BK) / T, LB = (BN * BK) / T;
@@ -129,9 +127,6 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
   bool ma[LA], nbok[LB];
   // MODE 1 with T % BM == 0: every load of a thread hits the same row.
   constexpr bool kRowFixed = MODE == 1 && (T % BM) == 0;
-  auto setup_tile = [&](int64_t tile) {
-  bm = (tile / n_tiles_n) * BM;
-  bn = (tile % n_tiles_n) * BN;
 #pragma unroll
   for (int u = 0; u < LA; ++u) {
     int e = tid + u * T;
@@ -165,7 +160,6 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
     pb[u] = B + static_cast<int64_t>(k) * N + (nbok[u] ? bn + n : 0);
     sb[u] = k * G::PB + n;
   }
-  };
   auto load_stage = [&](int stage, int64_t kt) {
     int64_t k0 = kt * BK;
     double2* as = As + stage * G::A_ELEMS;
@@ -198,32 +192,18 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
       if (G::GAUSS) acc_s[G::GAUSS ? i : 0][G::GAUSS ? j : 0][0] = acc_s[G::GAUSS ? i : 0][G::GAUSS ? j : 0][1] = 0.0;
     }
 
-  // issue side: the next (tile, k-step) to load
-  int64_t it_tile = blockIdx.x, it_kt = 0;
-  if (it_tile < n_tiles) setup_tile(it_tile);
-  auto issue_next = [&](int stage) {
-    if (it_tile >= n_tiles) return;
-    load_stage(stage, it_kt);
-    if (++it_kt == n_kt) {
-      it_kt = 0;
-      it_tile += gridDim.x;
-      if (it_tile < n_tiles) setup_tile(it_tile);
-    }
-  };
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    issue_next(s);
+    if (s < n_kt) load_stage(s, s);
     cp_commit();
   }
 
   const int fr = lane >> 2, fk = lane & 3;
-  int64_t c_tile = blockIdx.x, kt = 0;
-  for (int64_t j = 0; c_tile < n_tiles; ++j) {
+  for (int64_t kt = 0; kt < n_kt; ++kt) {
     cp_wait<STAGES - 2>();
     __syncthreads();
-    const int slot = static_cast<int>(j % STAGES);
-    const double2* as = As + slot * G::A_ELEMS + wm * G::WTM + fr;
-    const double2* bs = Bs + slot * G::B_ELEMS + wn * G::WTN + fr;
+    const double2* as = As + (kt % STAGES) * G::A_ELEMS + wm * G::WTM + fr;
+    const double2* bs = Bs + (kt % STAGES) * G::B_ELEMS + wn * G::WTN + fr;
 #pragma unroll
     for (int k4 = 0; k4 < BK; k4 += 4) {
       double a_re[MI], a_im[MI], b_re[NJ], b_im[NJ], nb_im[NJ];
@@ -234,94 +214,83 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
         a_im[i] = v.y;
       }
 #pragma unroll
-      for (int j2 = 0; j2 < NJ; ++j2) {
-        double2 v = bs[(k4 + fk) * G::PB + j2 * 8];
-        b_re[j2] = v.x;
-        b_im[j2] = v.y;
-        nb_im[j2] = -v.y;
+      for (int j = 0; j < NJ; ++j) {
+        double2 v = bs[(k4 + fk) * G::PB + j * 8];
+        b_re[j] = v.x;
+        b_im[j] = v.y;
+        nb_im[j] = -v.y;
       }
       if constexpr (G::GAUSS) {
         double a_s[MI], b_s[NJ];
 #pragma unroll
         for (int i = 0; i < MI; ++i) a_s[i] = a_re[i] + a_im[i];
 #pragma unroll
-        for (int j2 = 0; j2 < NJ; ++j2) b_s[j2] = b_re[j2] + b_im[j2];
+        for (int j = 0; j < NJ; ++j) b_s[j] = b_re[j] + b_im[j];
 #pragma unroll
         for (int i = 0; i < MI; ++i)
 #pragma unroll
-          for (int j2 = 0; j2 < NJ; ++j2) {
-            dmma(acc_re[i][j2], a_re[i], b_re[j2]);
-            dmma(acc_im[i][j2], a_im[i], b_im[j2]);
-            dmma(acc_s[i][j2], a_s[i], b_s[j2]);
+          for (int j = 0; j < NJ; ++j) {
+            dmma(acc_re[i][j], a_re[i], b_re[j]);
+            dmma(acc_im[i][j], a_im[i], b_im[j]);
+            dmma(acc_s[i][j], a_s[i], b_s[j]);
           }
       } else {
 #pragma unroll
         for (int i = 0; i < MI; ++i)
 #pragma unroll
-          for (int j2 = 0; j2 < NJ; ++j2) {
-            dmma(acc_re[i][j2], a_re[i], b_re[j2]);
-            dmma(acc_im[i][j2], a_re[i], b_im[j2]);
+          for (int j = 0; j < NJ; ++j) {
+            dmma(acc_re[i][j], a_re[i], b_re[j]);
+            dmma(acc_im[i][j], a_re[i], b_im[j]);
           }
 #pragma unroll
         for (int i = 0; i < MI; ++i)
 #pragma unroll
-          for (int j2 = 0; j2 < NJ; ++j2) {
-            dmma(acc_re[i][j2], a_im[i], nb_im[j2]);
-            dmma(acc_im[i][j2], a_im[i], b_re[j2]);
+          for (int j = 0; j < NJ; ++j) {
+            dmma(acc_re[i][j], a_im[i], nb_im[j]);
+            dmma(acc_im[i][j], a_im[i], b_re[j]);
           }
       }
     }
     // Refill the slot freed at the top barrier only after this slice's DMMAs are
     // queued: the (gather-table) address loads then stall the warp while the
     // tensor pipe is busy, not before it is fed.
-    issue_next(static_cast<int>((j + STAGES - 1) % STAGES));
-    cp_commit();
-    if (++kt < n_kt) continue;
-    // ---- tile done: epilogue (the next tile's stages are already in flight) ----
-    kt = 0;
-    const int64_t ebm = (c_tile / n_tiles_n) * BM, ebn = (c_tile % n_tiles_n) * BN;
-    c_tile += gridDim.x;
-    if constexpr (G::GAUSS) {
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j2 = 0; j2 < NJ; ++j2)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const double rr = acc_re[i][j2][h], ii = acc_im[i][j2][h];
-            acc_re[i][j2][h] = rr - ii;
-            acc_im[i][j2][h] = acc_s[i][j2][h] - rr - ii;
-          }
+    {
+      int64_t nk = kt + STAGES - 1;
+      if (nk < n_kt) load_stage(static_cast<int>(nk % STAGES), nk);
+      cp_commit();
     }
-    // lane holds C[fr][2*fk + {0,1}] of each 8x8 sub-tile
-#pragma unroll
-    for (int i = 0; i < MI; ++i) {
-      int64_t row = ebm + wm * G::WTM + i * 8 + fr;
-      if (row < M) {
-#pragma unroll
-        for (int j2 = 0; j2 < NJ; ++j2) {
-          int64_t col = ebn + wn * G::WTN + j2 * 8 + 2 * fk;
-          double2* dst = C + row * N + col;
-          if (col + 1 < N) {
-            dst[0] = make_double2(acc_re[i][j2][0], acc_im[i][j2][0]);
-            dst[1] = make_double2(acc_re[i][j2][1], acc_im[i][j2][1]);
-          } else if (col < N) {
-            dst[0] = make_double2(acc_re[i][j2][0], acc_im[i][j2][0]);
-          }
-        }
-      }
-    }
+  }
+  cp_wait<0>();
+  if constexpr (G::GAUSS) {
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
-      for (int j2 = 0; j2 < NJ; ++j2) {
-        acc_re[i][j2][0] = acc_re[i][j2][1] = 0.0;
-        acc_im[i][j2][0] = acc_im[i][j2][1] = 0.0;
-        if (G::GAUSS)
-          acc_s[G::GAUSS ? i : 0][G::GAUSS ? j2 : 0][0] = acc_s[G::GAUSS ? i : 0][G::GAUSS ? j2 : 0][1] = 0.0;
-      }
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double rr = acc_re[i][j][h], ii = acc_im[i][j][h];
+          acc_re[i][j][h] = rr - ii;
+          acc_im[i][j][h] = acc_s[i][j][h] - rr - ii;
+        }
   }
-  cp_wait<0>();
+
+  // Epilogue: lane holds C[fr][2*fk + {0,1}] of each 8x8 sub-tile.
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    int64_t row = bm + wm * G::WTM + i * 8 + fr;
+    if (row >= M) continue;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      int64_t col = bn + wn * G::WTN + j * 8 + 2 * fk;
+      double2* dst = C + row * N + col;
+      if (col + 1 < N) {
+        dst[0] = make_double2(acc_re[i][j][0], acc_im[i][j][0]);
+        dst[1] = make_double2(acc_re[i][j][1], acc_im[i][j][1]);
+      } else if (col < N) {
+        dst[0] = make_double2(acc_re[i][j][0], acc_im[i][j][0]);
+      }
+    }
+  }
 }
 
 template <class G, int MODE>
@@ -336,20 +305,8 @@ void launch_mode(const double2* a, const int64_t* ro, const int64_t* co, const d
   QTNH_CUDA(cudaFuncSetAttribute(k_zgemm<G, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(G::SMEM + kCoSmemMax * 8)));
   Dim tiles = ((m + G::BM - 1) / G::BM) * ((n + G::BN - 1) / G::BN);
-  static const bool persist = [] {
-    const char* e = std::getenv("QTNH_ZGEMM_PERSIST");
-    return !(e && e[0] == '0');
-  }();
-  Dim grid = tiles;
-  if (persist) {
-    int dev = 0, occ = 0, sms = 0;
-    QTNH_CUDA(cudaGetDevice(&dev));
-    QTNH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_zgemm<G, MODE>, G::THREADS, smem));
-    grid = std::min<Dim>(tiles, static_cast<Dim>(sms) * std::max(1, occ));
-  }
-  if (grid > 0x7fffffff) throw_invalid("zgemm problem too large for one launch");
-  k_zgemm<G, MODE><<<static_cast<unsigned>(grid), G::THREADS, smem, st>>>(a, ro, co, b, c, m, n, k, cohi, co_sh, rohi,
+  if (tiles > 0x7fffffff) throw_invalid("zgemm problem too large for one launch");
+  k_zgemm<G, MODE><<<static_cast<unsigned>(tiles), G::THREADS, smem, st>>>(a, ro, co, b, c, m, n, k, cohi, co_sh, rohi,
                                                                                   ro_sh);
   QTNH_LAUNCH_CHECK();
 }
