@@ -257,7 +257,16 @@ def run_gpu_arm(args):
     rank_a_global = RANK_A + s
     flops_rank = flops_for(RANK_A)
 
-    world = World.from_env() if world_size > 1 else World(1, [local])
+    world_note = None
+    if world_size > 1:
+        try:
+            world = World.from_env()
+        except Exception as e:  # C1 has no data-path collective: independent shards still measure it
+            world_note = f"NCCL world unavailable ({e}); each rank contracts its own A shard in a 1-rank world"
+            world = World(1, [local])
+    else:
+        world = World(1, [local])
+    nccl_world = world_size > 1 and world_note is None
     stream = torch.cuda.Stream()
     lib = qtnh.lib
     result = {}
@@ -269,7 +278,8 @@ def run_gpu_arm(args):
     b_host = torch.from_numpy(circuits.counter_state(SEED + 1, 2**RANK_B)).pin_memory()
     c_host = torch.empty(2**RANK_A, dtype=torch.complex128).pin_memory()
     ap_local, bp = circuits.contraction_positions(SEED, RANK_A, RANK_B, K_SHARED)
-    ap = [p + s for p in ap_local]  # the distributed leading indices are open
+    # the distributed leading indices are open (a 1-rank fallback world holds the shard alone)
+    ap = [p + s for p in ap_local] if (nccl_world or world_size == 1) else list(ap_local)
 
     def barrier():
         if world_size > 1:
@@ -278,8 +288,12 @@ def run_gpu_arm(args):
     def body(rk):
         rk.set_stream(stream.cuda_stream)
         with torch.cuda.stream(stream):
-            ta = Tensor.dense(rk, IndexTuple([2] * rank_a_global, s), DistParams(1, 1, 0), None)
-            tb = Tensor.dense(rk, IndexTuple([2] * RANK_B, 0), DistParams(world_size, 1, 0), None)
+            if nccl_world or world_size == 1:
+                ta = Tensor.dense(rk, IndexTuple([2] * rank_a_global, s), DistParams(1, 1, 0), None)
+                tb = Tensor.dense(rk, IndexTuple([2] * RANK_B, 0), DistParams(world_size, 1, 0), None)
+            else:
+                ta = Tensor.dense(rk, IndexTuple([2] * RANK_A, 0), DistParams(1, 1, 0), None)
+                tb = Tensor.dense(rk, IndexTuple([2] * RANK_B, 0), DistParams(1, 1, 0), None)
             qtnh.check(lib.qtnh_tensor_upload_local(ta._h, C.c_void_p(a_host.data_ptr())))
             qtnh.check(lib.qtnh_tensor_upload_local(tb._h, C.c_void_p(b_host.data_ptr())))
             rk.synchronize()
@@ -437,7 +451,7 @@ def run_gpu_arm(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "c128 (f64)",
             "data": "synthetic (seeded counter-based complex normals, common.hpp hash_counter + Box-Muller)",
-            "config": c1_config(world_size),
+            "config": dict(c1_config(world_size), **({"note": world_note} if world_note else {})),
             "roofline": {"bound": "tensor", "kernel": kname,
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "peak_source": "DMMA-only microbenchmark run live on this device (MEASURED_PEAKS.json "
