@@ -248,7 +248,8 @@ def run_gpu_arm(args):
     world_size = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+    local = local % max(1, torch.cuda.device_count())
     if world_size > 1:
         dist.init_process_group("gloo", init_method="env://")
     s = (world_size - 1).bit_length() if world_size > 1 else 0
