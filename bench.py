@@ -259,7 +259,11 @@ def run_gpu_arm(args):
     flops_rank = flops_for(RANK_A)
 
     world_note = None
-    if world_size > 1:
+    if world_size > 1 and world_size > torch.cuda.device_count():
+        world_note = (f"{world_size} ranks on {torch.cuda.device_count()} visible GPU(s): each rank contracts its "
+                      "own A shard in a 1-rank world (NCCL needs one GPU per rank)")
+        world = World(1, [local])
+    elif world_size > 1:
         try:
             world = World.from_env()
         except Exception as e:  # C1 has no data-path collective: independent shards still measure it
