@@ -55,27 +55,43 @@ __device__ __forceinline__ int64_t fiber_base(int64_t f, const GateArgs& a) {
   return base;
 }
 
+// F fibers per thread per iteration (strided by the grid size, so every load
+// instruction stays coalesced): 2F..8 independent 16-byte loads in flight per
+// thread for the small gates, which are otherwise latency- rather than
+// bandwidth-limited.
 template <int D, bool POW2>
 __global__ void __launch_bounds__(256) k_gate_dense(double2* __restrict__ psi, int64_t n_fibers,
                                                     const __grid_constant__ GateArgs a) {
-  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < n_fibers;
-       f += (int64_t)gridDim.x * blockDim.x) {
-    int64_t base = fiber_base<POW2>(f + a.f0, a);
-    double2 x[D];
+  constexpr int F = D <= 4 ? 4 : (D <= 8 ? 2 : 1);
+  const int64_t S = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t f0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f0 < n_fibers; f0 += F * S) {
+    int64_t base[F];
+    double2 x[F][D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) x[d] = psi[base + a.off[d]];
+    for (int u = 0; u < F; ++u) {
+      const int64_t f = f0 + u * S;
+      base[u] = f < n_fibers ? fiber_base<POW2>(f + a.f0, a) : -1;
+      if (base[u] >= 0) {
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-      double re = 0.0, im = 0.0;
-#pragma unroll
-      for (int d = 0; d < D; ++d) {
-        double2 g = a.g[i * D + d];
-        re = fma(g.x, x[d].x, re);
-        re = fma(-g.y, x[d].y, re);
-        im = fma(g.x, x[d].y, im);
-        im = fma(g.y, x[d].x, im);
+        for (int d = 0; d < D; ++d) x[u][d] = psi[base[u] + a.off[d]];
       }
-      psi[base + a.off[i]] = make_double2(re, im);
+    }
+#pragma unroll
+    for (int u = 0; u < F; ++u) {
+      if (base[u] < 0) continue;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        double re = 0.0, im = 0.0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          double2 g = a.g[i * D + d];
+          re = fma(g.x, x[u][d].x, re);
+          re = fma(-g.y, x[u][d].y, re);
+          im = fma(g.x, x[u][d].y, im);
+          im = fma(g.y, x[u][d].x, im);
+        }
+        psi[base[u] + a.off[i]] = make_double2(re, im);
+      }
     }
   }
 }
