@@ -89,6 +89,12 @@ int qtnh_world_create_local(int n_ranks, const int* devices, qtnh_world_t* out);
  * rank 0 and shared out of band. NCCL is loaded lazily (dlopen). */
 int qtnh_nccl_unique_id(void* uid128);
 int qtnh_world_create_nccl(int rank, int size, int device, const void* uid128, qtnh_world_t* out);
+/* Process-per-GPU world without NCCL (one process per GPU, one node): every
+ * collective is a CUDA-IPC peer-memory operation -- exportable stream-ordered
+ * pools shared once over Unix sockets under `dir`, interprocess events for
+ * stream ordering, pointer-export records per collective; the fused peer kernels
+ * (push remap, pairwise swap, distributed gate / QFT) run across processes. */
+int qtnh_world_create_ipc(int rank, int size, int device, const char* dir, qtnh_world_t* out);
 int qtnh_world_destroy(qtnh_world_t w);
 int qtnh_world_size(qtnh_world_t w);
 /* Abort all pending and future collectives of the world (AbortedError on peers). */

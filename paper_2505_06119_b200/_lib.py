@@ -34,6 +34,7 @@ _SIGS = {
     "qtnh_world_create_local": (i32, [i32, P_i32, C.POINTER(vp)]),
     "qtnh_nccl_unique_id": (i32, [vp]),
     "qtnh_world_create_nccl": (i32, [i32, i32, i32, vp, C.POINTER(vp)]),
+    "qtnh_world_create_ipc": (i32, [i32, i32, i32, C.c_char_p, C.POINTER(vp)]),
     "qtnh_world_destroy": (i32, [vp]),
     "qtnh_world_size": (i32, [vp]),
     "qtnh_world_abort": (i32, [vp]),

@@ -160,7 +160,33 @@ int qtnh_world_create_nccl(int rank, int size, int device, const void* uid128, q
     rc->device = device;
     QTNH_CUDA(cudaStreamCreateWithFlags(&rc->own_stream, cudaStreamNonBlocking));
     rc->stream = rc->own_stream;
-    w->nccl_rank = std::move(rc);
+    w->proc_rank = std::move(rc);
+    auto* h = new qtnh_world_s;
+    h->w = std::move(w);
+    *out = h;
+  });
+}
+
+int qtnh_world_create_ipc(int rank, int size, int device, const char* dir, qtnh_world_t* out) {
+  return guard([&] {
+    need(out, "out");
+    need(dir, "dir");
+    if (size < 1 || rank < 0 || rank >= size) throw_invalid("invalid rank/size");
+    auto w = std::make_unique<World>();
+    w->kind = World::kIpc;
+    w->size = size;
+    w->my_rank = rank;
+    w->timeout_ms = env_timeout();
+    w->peer_ok = true;
+    QTNH_CUDA(cudaSetDevice(device));
+    auto rc = std::make_unique<RankCtx>();
+    rc->world = w.get();
+    rc->rank = rank;
+    rc->device = device;
+    QTNH_CUDA(cudaStreamCreateWithFlags(&rc->own_stream, cudaStreamNonBlocking));
+    rc->stream = rc->own_stream;
+    w->proc_rank = std::move(rc);
+    ipc_init(*w, rank, size, device, dir);
     auto* h = new qtnh_world_s;
     h->w = std::move(w);
     *out = h;
@@ -170,13 +196,21 @@ int qtnh_world_create_nccl(int rank, int size, int device, const void* uid128, q
 int qtnh_world_destroy(qtnh_world_t w) {
   return guard([&] {
     if (!w) return;
-    if (w->w->kind == World::kNccl && w->w->nccl_comm) {
-      cudaSetDevice(w->w->nccl_rank->device);
-      cudaStreamSynchronize(w->w->nccl_rank->stream);
-      nccl().CommDestroy(static_cast<ncclComm_t>(w->w->nccl_comm));
-      cudaStreamDestroy(w->w->nccl_rank->own_stream);
+    if (w->w->kind == World::kIpc) {
+      cudaSetDevice(w->w->proc_rank->device);
+      cudaStreamSynchronize(w->w->proc_rank->stream);
+      ipc_destroy(*w->w);
+      cudaStreamDestroy(w->w->proc_rank->own_stream);
+      delete w;
+      return;
     }
-    std::vector<int> devs = w->w->kind == World::kNccl ? std::vector<int>{w->w->nccl_rank->device} : w->w->devices;
+    if (w->w->kind == World::kNccl && w->w->nccl_comm) {
+      cudaSetDevice(w->w->proc_rank->device);
+      cudaStreamSynchronize(w->w->proc_rank->stream);
+      nccl().CommDestroy(static_cast<ncclComm_t>(w->w->nccl_comm));
+      cudaStreamDestroy(w->w->proc_rank->own_stream);
+    }
+    std::vector<int> devs = w->w->kind == World::kNccl ? std::vector<int>{w->w->proc_rank->device} : w->w->devices;
     delete w;
     std::sort(devs.begin(), devs.end());
     devs.erase(std::unique(devs.begin(), devs.end()), devs.end());
@@ -202,12 +236,12 @@ int qtnh_rank_bind(qtnh_world_t w, int rank, qtnh_rank_t* out) {
     World& W = *w->w;
     auto* h = new qtnh_rank_s;
     h->world = &W;
-    if (W.kind == World::kNccl) {
+    if (W.kind == World::kNccl || W.kind == World::kIpc) {
       if (rank != W.my_rank) {
         delete h;
-        throw_invalid("NCCL world: this process is rank " + std::to_string(W.my_rank));
+        throw_invalid("process-per-GPU world: this process is rank " + std::to_string(W.my_rank));
       }
-      h->ctx = W.nccl_rank.get();
+      h->ctx = W.proc_rank.get();
     } else {
       if (rank < 0 || rank >= W.size) {
         delete h;

@@ -502,7 +502,11 @@ void op_qft(TP& t, bool swaps) {
   if (fused) {
     if (!t->in_span) return;
     auto members = span_ranks(*t);
-    peer_pointers(r, members, t->data());  // the local layers of every member are done
+    // the local layers of every member are done; pointers are valid until the
+    // next peer_pointers call (IPC worlds re-import them), so regroup
+    auto ptrs = peer_pointers(r, members, t->data());
+    const Dim Xg = Dim(1) << split;
+    for (Dim x = 0; x < Xg; ++x) grp[x] = ptrs[t->dist.home(x, Xg, t->cycle, t->slot) - members.front()];
     const Dim X = Dim(1) << split, M = t->shape.local_size() >> split;
     dist_bitrev(grp.data(), split, my_x * M / X, (my_x + 1) * M / X, r.stream);
     peer_pointers(r, members, nullptr);

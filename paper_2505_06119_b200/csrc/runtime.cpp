@@ -278,10 +278,11 @@ std::atomic<bool> g_peer_direct{[] {
 void set_peer_direct(bool on) { g_peer_direct.store(on); }
 
 bool peer_direct(const RankCtx& r) {
-  return r.world->kind == World::kLocal && r.world->peer_ok && g_peer_direct.load();
+  return (r.world->kind == World::kLocal || r.world->kind == World::kIpc) && r.world->peer_ok && g_peer_direct.load();
 }
 
 std::vector<void*> peer_pointers(RankCtx& r, const std::vector<int>& members, void* mine) {
+  if (r.world->kind == World::kIpc) return ipc_peer_pointers(r, members, mine);
   World& w = *r.world;
   int n = static_cast<int>(members.size());
   int me = static_cast<int>(std::find(members.begin(), members.end(), r.rank) - members.begin());
@@ -325,6 +326,8 @@ void exchange(RankCtx& r, const std::vector<int>& members, const void* send_buf,
               const std::vector<Xfer>& sends, void* recv_buf, const std::vector<Xfer>& recvs) {
   if (r.world->kind == World::kLocal) {
     local_exchange(r, members, send_buf, sends, recv_buf, recvs);
+  } else if (r.world->kind == World::kIpc) {
+    ipc_exchange(r, members, send_buf, sends, recv_buf, recvs);
   } else {
     nccl_exchange(r, send_buf, sends, recv_buf, recvs);
   }
@@ -332,6 +335,11 @@ void exchange(RankCtx& r, const std::vector<int>& members, const void* send_buf,
 
 void barrier(RankCtx& r, const std::vector<int>& members) {
   if (members.size() <= 1) return;
+  if (r.world->kind == World::kIpc) {
+    QTNH_CUDA(cudaStreamSynchronize(r.stream));
+    ipc_allgather(r, members, std::string());
+    return;
+  }
   if (r.world->kind == World::kLocal) {
     local_exchange(r, members, nullptr, {}, nullptr, {});
     QTNH_CUDA(cudaStreamSynchronize(r.stream));

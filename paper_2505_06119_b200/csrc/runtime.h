@@ -16,6 +16,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "common.h"
@@ -42,15 +43,29 @@ struct Xfer {
   Dim count;
 };
 
+// Process-per-GPU world over CUDA IPC (ipc.cpp): sockets to every peer, this
+// process's exportable pool and the peers' imported pools, interprocess event rings.
+struct IpcState {
+  std::vector<int> fd;
+  cudaMemPool_t pool = nullptr;
+  std::vector<cudaMemPool_t> peer_pool;
+  std::vector<int> peer_dev;
+  std::vector<cudaEvent_t> my_ev;
+  std::vector<std::vector<cudaEvent_t>> peer_ev;
+  uint64_t ev_next = 0;
+  std::vector<void*> imports;  // pointers imported by the last peer_pointers call
+};
+
 struct World {
-  enum Kind { kLocal, kNccl } kind = kLocal;
+  enum Kind { kLocal, kNccl, kIpc } kind = kLocal;
   int size = 1;
   std::vector<int> devices;  // local: device of each rank
   bool peer_ok = false;      // local: every rank can load/store every other rank's HBM
-  // NCCL backend (process per GPU)
+  // process-per-GPU backends (NCCL or IPC): this process's rank
   int my_rank = 0;
   void* nccl_comm = nullptr;
-  std::unique_ptr<RankCtx> nccl_rank;
+  std::unique_ptr<RankCtx> proc_rank;
+  std::unique_ptr<IpcState> ipc;
 
   // local backend rendezvous
   std::mutex mu;
@@ -88,8 +103,17 @@ bool peer_direct(const RankCtx& r);
 void set_peer_direct(bool on);  // option "peer_direct" / QTNH_PEER_DIRECT=0
 // All-gather of one device pointer per member (in member order). Stream-ordered:
 // on return my stream waits for the work every member enqueued before its call,
-// so a second call after the peer kernels acts as the completion fence.
+// so a second call after the peer kernels acts as the completion fence. The
+// returned peer pointers are valid until this rank's next peer_pointers call.
 std::vector<void*> peer_pointers(RankCtx& r, const std::vector<int>& members, void* mine);
+
+// IPC backend (ipc.cpp)
+void ipc_init(World& w, int rank, int size, int device, const std::string& dir);
+void ipc_destroy(World& w);
+std::vector<std::string> ipc_allgather(RankCtx& r, const std::vector<int>& members, const std::string& mine);
+std::vector<void*> ipc_peer_pointers(RankCtx& r, const std::vector<int>& members, void* mine);
+void ipc_exchange(RankCtx& r, const std::vector<int>& members, const void* send_buf, const std::vector<Xfer>& sends,
+                  void* recv_buf, const std::vector<Xfer>& recvs);
 
 // ---- device tensors -----------------------------------------------------------
 void keep_pool(int device);  // stream-ordered pool keeps freed blocks (world lifetime)

@@ -305,6 +305,27 @@ class World:
         self._h = h
         return self
 
+    @classmethod
+    def from_env_ipc(cls, rendezvous_dir: Optional[str] = None) -> "World":
+        """Process-per-GPU world over CUDA IPC (no NCCL): RANK / WORLD_SIZE /
+        LOCAL_RANK from the environment (torchrun); the processes meet through
+        Unix sockets under `rendezvous_dir` (default $QTNH_IPC_DIR or
+        /tmp/qtnh_ipc_<MASTER_PORT>). Collectives run as peer-memory kernels."""
+        import torch
+
+        rank = int(os.environ.get("RANK", "0"))
+        size = int(os.environ.get("WORLD_SIZE", "1"))
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        device = local % max(1, torch.cuda.device_count())
+        d = rendezvous_dir or os.environ.get("QTNH_IPC_DIR") or f"/tmp/qtnh_ipc_{os.environ.get('MASTER_PORT', '0')}"
+        self = cls.__new__(cls)
+        self._n = size
+        self._nccl_rank = rank
+        h = C.c_void_p()
+        check(lib.qtnh_world_create_ipc(rank, size, device, os.fsencode(d), C.byref(h)))
+        self._h = h
+        return self
+
     def size(self) -> int:
         return self._n
 
