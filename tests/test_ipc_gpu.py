@@ -29,5 +29,5 @@ def test_ipc_world_ops(tmp_path, nproc):
                 q.kill()
             raise
         outs.append((p.returncode, out))
-    for rc, out in outs:
-        assert rc == 0 and "ipc rank ok" in out, out[-3000:]
+    bad = [f"rank {r} rc={rc}:\n{out[-2500:]}" for r, (rc, out) in enumerate(outs) if rc != 0 or "ipc rank ok" not in out]
+    assert not bad, "\n".join(bad)
