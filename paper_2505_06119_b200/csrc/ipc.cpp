@@ -26,6 +26,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 
@@ -292,12 +294,15 @@ constexpr size_t kExportLen = 1 + sizeof(cudaMemPoolPtrExportData);
 // releases the imports of the first, stream-ordered after the peer kernels.
 std::vector<void*> ipc_peer_pointers(RankCtx& r, const std::vector<int>& members, void* mine) {
   IpcState& S = *r.world->ipc;
+  static const bool dbg = std::getenv("QTNH_IPC_DEBUG") != nullptr;
+  if (dbg) std::fprintf(stderr, "[ipc %d] peer_pointers mine=%p releasing %zu\n", r.rank, mine, S.imports.size());
   for (void* p : S.imports) QTNH_CUDA(cudaFreeAsync(p, r.stream));
   S.imports.clear();
   int k = ipc_record(r);
   std::string rec = ipc_export(mine);
   rec.append(reinterpret_cast<const char*>(&k), sizeof(k));
   auto all = ipc_allgather(r, members, rec);
+  if (dbg) std::fprintf(stderr, "[ipc %d] gathered\n", r.rank);
   std::vector<void*> out(members.size());
   for (size_t i = 0; i < members.size(); ++i) {
     if (members[i] == r.rank) {
@@ -309,6 +314,7 @@ std::vector<void*> ipc_peer_pointers(RankCtx& r, const std::vector<int>& members
     std::memcpy(&pk, m.data() + kExportLen, sizeof(pk));
     ipc_wait(r, members[i], pk);
     out[i] = ipc_import(r, members[i], m.data());
+    if (dbg) std::fprintf(stderr, "[ipc %d] imported %p from %d\n", r.rank, out[i], members[i]);
     if (out[i]) S.imports.push_back(out[i]);
   }
   return out;
