@@ -269,26 +269,60 @@ void ipc_wait(RankCtx& r, int peer, int k) {
   QTNH_CUDA(cudaStreamWaitEvent(r.stream, r.world->ipc->peer_ev[peer][k], 0));
 }
 
+// Export record: kind byte (0 none, 1 pool pointer, 2 legacy IPC handle) + data.
+constexpr size_t kExportData = sizeof(cudaMemPoolPtrExportData) > sizeof(cudaIpcMemHandle_t)
+                                   ? sizeof(cudaMemPoolPtrExportData)
+                                   : sizeof(cudaIpcMemHandle_t);
+
 std::string ipc_export(const void* p) {
-  std::string s(1 + sizeof(cudaMemPoolPtrExportData), '\0');
+  std::string s(1 + kExportData, '\0');
   if (!p) return s;
-  s[0] = 1;
   cudaMemPoolPtrExportData d;
-  QTNH_CUDA(cudaMemPoolExportPointer(&d, const_cast<void*>(p)));
-  std::memcpy(&s[1], &d, sizeof(d));
+  if (cudaMemPoolExportPointer(&d, const_cast<void*>(p)) == cudaSuccess) {
+    s[0] = 1;
+    std::memcpy(&s[1], &d, sizeof(d));
+    return s;
+  }
+  cudaGetLastError();  // not a pool block: a large cudaMalloc block (kIpcLegacyMinBytes)
+  cudaIpcMemHandle_t h;
+  QTNH_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(p)));
+  s[0] = 2;
+  std::memcpy(&s[1], &h, sizeof(h));
   return s;
 }
 
-void* ipc_import(RankCtx& r, int peer, const char* rec) {
-  if (!rec[0]) return nullptr;
-  cudaMemPoolPtrExportData d;
-  std::memcpy(&d, rec + 1, sizeof(d));
+std::pair<void*, int> ipc_import(RankCtx& r, int peer, const char* rec) {
+  if (!rec[0]) return {nullptr, 0};
   void* p = nullptr;
-  QTNH_CUDA(cudaMemPoolImportPointer(&p, r.world->ipc->peer_pool[peer], &d));
-  return p;
+  if (rec[0] == 1) {
+    cudaMemPoolPtrExportData d;
+    std::memcpy(&d, rec + 1, sizeof(d));
+    QTNH_CUDA(cudaMemPoolImportPointer(&p, r.world->ipc->peer_pool[peer], &d));
+    return {p, 1};
+  }
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, rec + 1, sizeof(h));
+  QTNH_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  return {p, 2};
 }
 
-constexpr size_t kExportLen = 1 + sizeof(cudaMemPoolPtrExportData);
+// Release imports after the stream work that used them: pool imports are freed
+// stream-ordered; legacy mappings are closed after the stream drains.
+void ipc_release(RankCtx& r, std::vector<std::pair<void*, int>>& v) {
+  bool legacy = false;
+  for (auto& pi : v) {
+    if (pi.second == 1) QTNH_CUDA(cudaFreeAsync(pi.first, r.stream));
+    legacy |= pi.second == 2;
+  }
+  if (legacy) {
+    QTNH_CUDA(cudaStreamSynchronize(r.stream));
+    for (auto& pi : v)
+      if (pi.second == 2) QTNH_CUDA(cudaIpcCloseMemHandle(pi.first));
+  }
+  v.clear();
+}
+
+constexpr size_t kExportLen = 1 + kExportData;
 
 // peer_pointers for the IPC world: the second call of a pair (the fence) first
 // releases the imports of the first, stream-ordered after the peer kernels.
@@ -296,8 +330,7 @@ std::vector<void*> ipc_peer_pointers(RankCtx& r, const std::vector<int>& members
   IpcState& S = *r.world->ipc;
   static const bool dbg = std::getenv("QTNH_IPC_DEBUG") != nullptr;
   if (dbg) std::fprintf(stderr, "[ipc %d] peer_pointers mine=%p releasing %zu\n", r.rank, mine, S.imports.size());
-  for (void* p : S.imports) QTNH_CUDA(cudaFreeAsync(p, r.stream));
-  S.imports.clear();
+  ipc_release(r, S.imports);
   int k = ipc_record(r);
   std::string rec = ipc_export(mine);
   rec.append(reinterpret_cast<const char*>(&k), sizeof(k));
@@ -313,9 +346,10 @@ std::vector<void*> ipc_peer_pointers(RankCtx& r, const std::vector<int>& members
     int pk;
     std::memcpy(&pk, m.data() + kExportLen, sizeof(pk));
     ipc_wait(r, members[i], pk);
-    out[i] = ipc_import(r, members[i], m.data());
-    if (dbg) std::fprintf(stderr, "[ipc %d] imported %p from %d\n", r.rank, out[i], members[i]);
-    if (out[i]) S.imports.push_back(out[i]);
+    auto im = ipc_import(r, members[i], m.data());
+    out[i] = im.first;
+    if (dbg) std::fprintf(stderr, "[ipc %d] imported %p (kind %d) from %d\n", r.rank, out[i], im.second, members[i]);
+    if (out[i]) S.imports.push_back(im);
   }
   return out;
 }
@@ -334,6 +368,7 @@ void ipc_exchange(RankCtx& r, const std::vector<int>& members, const void* send_
   std::map<int, size_t> idx;
   for (size_t i = 0; i < members.size(); ++i) idx[members[i]] = i;
   std::map<int, void*> imported;
+  std::vector<std::pair<void*, int>> held;
   std::map<int, int> used;
   for (const Xfer& rv : recvs) {
     auto it = idx.find(rv.peer);
@@ -363,7 +398,9 @@ void ipc_exchange(RankCtx& r, const std::vector<int>& members, const void* send_
       auto im = imported.find(rv.peer);
       if (im == imported.end()) {
         ipc_wait(r, rv.peer, pk);
-        im = imported.emplace(rv.peer, ipc_import(r, rv.peer, m.data())).first;
+        auto got = ipc_import(r, rv.peer, m.data());
+        held.push_back(got);
+        im = imported.emplace(rv.peer, got.first).first;
       }
       src = im->second;
     }
@@ -371,7 +408,7 @@ void ipc_exchange(RankCtx& r, const std::vector<int>& members, const void* send_
                               static_cast<const char*>(src) + sx->offset * 16, rv.count * 16, cudaMemcpyDefault,
                               r.stream));
   }
-  for (auto& kv : imported) QTNH_CUDA(cudaFreeAsync(kv.second, r.stream));
+  ipc_release(r, held);
   int k2 = ipc_record(r);
   std::string rec2(reinterpret_cast<const char*>(&k2), sizeof(k2));
   auto all2 = ipc_allgather(r, members, rec2);

@@ -78,13 +78,20 @@ void trim_pool(int device) {
 
 DevBuf::DevBuf(size_t b, const RankCtx& r) : bytes(b), device(r.device), stream(r.stream) {
   if (b == 0) b = 16;
+  if (r.world && r.world->kind == World::kIpc && b >= kIpcLegacyMinBytes) {
+    QTNH_CUDA(cudaStreamSynchronize(stream));  // cudaMalloc is not stream-ordered
+    QTNH_CUDA(cudaMalloc(&ptr, b));
+    legacy_ipc = true;
+    return;
+  }
   QTNH_CUDA(cudaMallocAsync(&ptr, b, stream));
 }
 
 DevBuf::~DevBuf() {
   if (ptr) {
     cudaSetDevice(device);
-    cudaFreeAsync(ptr, stream);
+    if (legacy_ipc) cudaFree(ptr);  // synchronises the device: no pending reader remains
+    else cudaFreeAsync(ptr, stream);
   }
 }
 

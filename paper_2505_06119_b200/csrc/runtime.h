@@ -53,7 +53,7 @@ struct IpcState {
   std::vector<cudaEvent_t> my_ev;
   std::vector<std::vector<cudaEvent_t>> peer_ev;
   uint64_t ev_next = 0;
-  std::vector<void*> imports;  // pointers imported by the last peer_pointers call
+  std::vector<std::pair<void*, int>> imports;  // (pointer, kind 1 pool / 2 legacy) of the last peer_pointers call
 };
 
 struct World {
@@ -124,9 +124,13 @@ struct DevBuf {
   size_t bytes = 0;
   int device = 0;
   cudaStream_t stream = nullptr;
+  bool legacy_ipc = false;  // IPC world, large block: cudaMalloc (legacy IPC handle), not the pool
   DevBuf(size_t b, const RankCtx& r);
   ~DevBuf();
 };
+// Blocks at least this large in an IPC world are shared through legacy CUDA IPC
+// handles: importing multi-GiB stream-ordered-pool allocations crashed the driver.
+constexpr size_t kIpcLegacyMinBytes = size_t(2) << 30;
 
 struct TensorImpl {
   RankCtx* rank = nullptr;
