@@ -76,9 +76,17 @@ void trim_pool(int device) {
   cudaMemPoolTrimTo(pool, 0);
 }
 
+size_t ipc_legacy_min_bytes() {
+  static const size_t v = [] {
+    const char* e = std::getenv("QTNH_IPC_LEGACY_MIN");
+    return e ? static_cast<size_t>(std::atoll(e)) : (size_t(2) << 30);
+  }();
+  return v;
+}
+
 DevBuf::DevBuf(size_t b, const RankCtx& r) : bytes(b), device(r.device), stream(r.stream) {
   if (b == 0) b = 16;
-  if (r.world && r.world->kind == World::kIpc && b >= kIpcLegacyMinBytes) {
+  if (r.world && r.world->kind == World::kIpc && b >= ipc_legacy_min_bytes()) {
     QTNH_CUDA(cudaStreamSynchronize(stream));  // cudaMalloc is not stream-ordered
     QTNH_CUDA(cudaMalloc(&ptr, b));
     legacy_ipc = true;

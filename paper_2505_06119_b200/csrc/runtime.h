@@ -130,7 +130,8 @@ struct DevBuf {
 };
 // Blocks at least this large in an IPC world are shared through legacy CUDA IPC
 // handles: importing multi-GiB stream-ordered-pool allocations crashed the driver.
-constexpr size_t kIpcLegacyMinBytes = size_t(2) << 30;
+// Default 2 GiB; QTNH_IPC_LEGACY_MIN (bytes) overrides it (tests force 0).
+size_t ipc_legacy_min_bytes();
 
 struct TensorImpl {
   RankCtx* rank = nullptr;

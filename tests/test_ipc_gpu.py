@@ -11,10 +11,14 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("nproc", [2, 4])
-def test_ipc_world_ops(tmp_path, nproc):
+@pytest.mark.parametrize("nproc,legacy_min", [(2, None), (4, None), (2, "0")])
+def test_ipc_world_ops(tmp_path, nproc, legacy_min):
+    """legacy_min "0": every block goes through legacy IPC handles (the path of
+    multi-GiB shards)."""
     env_base = dict(os.environ, WORLD_SIZE=str(nproc), QTNH_IPC_DIR=str(tmp_path / "rdv"),
                     QTNH_COLLECTIVE_TIMEOUT_MS="60000")
+    if legacy_min is not None:
+        env_base["QTNH_IPC_LEGACY_MIN"] = legacy_min
     procs = []
     for r in range(nproc):
         env = dict(env_base, RANK=str(r), LOCAL_RANK=str(r))
