@@ -168,6 +168,12 @@ int qtnh_tensor_load(qtnh_rank_t r, const char* path, qtnh_tensor_t* out);
 /* ---- structural ops (ops.hpp) --------------------------------------------- */
 int qtnh_permute(qtnh_tensor_t t, const int* perm, int new_split, qtnh_tensor_t* out);
 int qtnh_rebcast(qtnh_tensor_t t, const int64_t* new_dist, qtnh_tensor_t* out);
+/* remap::tensor_to_tensor (remap.hpp:106-161), dense: axis_map[src_pos] = dst_pos,
+ * destination dims >= the mapped source dims (larger local dims zero-embed;
+ * larger distributed dims are rejected), new split and DistParams (NULL: keep).
+ * One redistribution pass (plus a local pad when embedding). */
+int qtnh_remap(qtnh_tensor_t t, const int* axis_map, int n_dst, const int64_t* dst_dims, int dst_split,
+               const int64_t* dst_dist, qtnh_tensor_t* out);
 int qtnh_scatter_index(qtnh_tensor_t t, int pos, qtnh_tensor_t* out);
 int qtnh_gather_index(qtnh_tensor_t t, int pos, qtnh_tensor_t* out);
 int qtnh_slice_local_dims(qtnh_tensor_t t, const int64_t* new_local_dims, qtnh_tensor_t* out);

@@ -70,6 +70,7 @@ _SIGS = {
     "qtnh_tensor_load": (i32, [vp, C.c_char_p, C.POINTER(vp)]),
     "qtnh_permute": (i32, [vp, P_i32, i32, C.POINTER(vp)]),
     "qtnh_rebcast": (i32, [vp, P_i64, C.POINTER(vp)]),
+    "qtnh_remap": (i32, [vp, P_i32, i32, P_i64, i32, P_i64, C.POINTER(vp)]),
     "qtnh_scatter_index": (i32, [vp, i32, C.POINTER(vp)]),
     "qtnh_gather_index": (i32, [vp, i32, C.POINTER(vp)]),
     "qtnh_slice_local_dims": (i32, [vp, P_i64, C.POINTER(vp)]),

@@ -471,6 +471,42 @@ int qtnh_rebcast(qtnh_tensor_t t, const int64_t* nd, qtnh_tensor_t* out) {
   });
 }
 
+int qtnh_remap(qtnh_tensor_t t, const int* axis_map, int n_dst, const int64_t* dst_dims, int dst_split,
+               const int64_t* dst_dist, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    TP& p = impl_of(t);
+    const Shape& ss = p->shape;
+    const int n = ss.n_idx();
+    if (n) need(axis_map, "axis_map");
+    if (n_dst != n) throw_invalid("axis map is not a bijection");
+    Shape ds = shape_from(n_dst, dst_dims, dst_split);
+    std::vector<int> am(axis_map, axis_map + n);
+    std::vector<char> seen(n, 0);
+    bool embed = false;
+    for (int i = 0; i < n; ++i) {
+      int q = am[i];
+      if (q < 0 || q >= n || seen[q]) throw_invalid("axis map is not a bijection");
+      seen[q] = 1;
+      if (ds.dims[q] < ss.dims[i]) throw_invalid("destination dimension smaller than source");
+      if (ds.dims[q] > ss.dims[i]) {
+        if (q < dst_split) throw_invalid("zero-embedding into a larger distributed index is not supported");
+        embed = true;
+      }
+    }
+    Dist dd = dst_dist ? dist_from(dst_dist) : p->dist;
+    if (!embed) {
+      *out = wrap(remap(p, ds, dd, am));
+      return;
+    }
+    // remap onto the source dimensions, then zero-embed the local ones
+    std::vector<Dim> eq(n);
+    for (int i = 0; i < n; ++i) eq[am[i]] = ss.dims[i];
+    TP mid = remap(p, Shape(eq, dst_split), dd, am);
+    *out = wrap(op_pad_local(mid, ds.local_dims()));
+  });
+}
+
 int qtnh_scatter_index(qtnh_tensor_t t, int pos, qtnh_tensor_t* out) {
   return guard([&] {
     need(out, "out");

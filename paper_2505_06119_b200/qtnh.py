@@ -594,6 +594,15 @@ class ops:  # namespace
         return t._new(h)
 
     @staticmethod
+    def remap(t: Tensor, axis_map: Sequence[int], dst: IndexTuple, dst_dist=None) -> Tensor:
+        """remap::tensor_to_tensor (remap.hpp:106-161), dense variant: axis_map[src]
+        = dst position; local destination dims may exceed the source's (zeros)."""
+        h = C.c_void_p()
+        dd = _dist(dst_dist).as_array() if dst_dist is not None else None
+        check(lib.qtnh_remap(t._h, i32_array(axis_map), dst.n_idx(), i64_array(dst.dims), dst.split, dd, C.byref(h)))
+        return t._new(h)
+
+    @staticmethod
     def rebcast(t: Tensor, new_dist) -> Tensor:
         h = C.c_void_p()
         check(lib.qtnh_rebcast(t._h, _dist(new_dist).as_array(), C.byref(h)))

@@ -313,3 +313,40 @@ def test_rank_failure_aborts_the_world():
 
     with pytest.raises(ValueError):
         World(4).run(body)
+
+
+@pytest.mark.parametrize("dims,split,dist,amap,dsplit,ddist,world,ddims", [
+    ([2, 3, 4, 2], 1, (1, 1, 0), [2, 0, 3, 1], 2, (1, 1, 0), 8, None),     # permute + new split in one pass
+    ([2, 2, 4, 2], 1, (1, 2, 0), [0, 1, 2, 3], 1, (2, 1, 1), 6, None),     # rebcast (stretch, offset)
+    ([2, 3, 2, 2], 2, (1, 1, 0), [3, 2, 1, 0], 1, (1, 1, 2), 8, None),     # both at once
+    ([2, 3, 4], 1, (1, 1, 0), [0, 2, 1], 1, (1, 1, 0), 2, [2, 5, 3]),       # zero-embedding of local dims
+])
+def test_tensor_to_tensor_remap(dims, split, dist, amap, dsplit, ddist, world, ddims, peer_mode):
+    """remap::tensor_to_tensor (remap.hpp:106-161): axis map, new split and new
+    DistParams in one redistribution; larger local destination dims zero-embed."""
+    from paper_2505_06119_b200.qtnh import ops
+    n = len(dims)
+    g = circuits.counter_state(9, int(np.prod(dims)))
+    g[::4] = complex(-0.0, -0.0)
+    nd = [0] * n
+    for i, q in enumerate(amap):
+        nd[q] = dims[i]
+    out_dims = ddims or nd
+
+    def body(rk):
+        t = Tensor.from_global(rk, IndexTuple(dims, split), DistParams(*dist), g)
+        u = ops.remap(t, amap, IndexTuple(out_dims, dsplit), DistParams(*ddist))
+        assert u.shape().dims == out_dims and u.shape().split == dsplit
+        d = u.dist()
+        assert (d.stretch, d.cycles, d.offset) == tuple(ddist)
+        return u.to_global_vector() if u.in_span() else None
+
+    outs = [o for o in World(world).run(body) if o is not None]
+    perm = [amap.index(p) for p in range(n)]  # new position p holds old index perm[p]
+    want = P.permute(dims, g, perm).reshape(nd)
+    if ddims:
+        pad = np.zeros(ddims, complex)
+        pad[tuple(slice(0, x) for x in nd)] = want
+        want = pad
+    for o in outs:
+        assert np.array_equal(bits(o), bits(want.reshape(-1)))
