@@ -219,6 +219,13 @@ inline Tensor gather_index(const Tensor& t, int pos) {
   check(qtnh_gather_index(t.h(), pos, &o));
   return wrap(o);
 }
+// remap::tensor_to_tensor (remap.hpp:106): axis_map[src] = dst position
+inline Tensor tensor_to_tensor(const Tensor& t, const IndexTuple& dst, DistParams d, const std::vector<int>& axis_map) {
+  qtnh_tensor_t o;
+  int64_t dd[3] = {d.stretch, d.cycles, d.offset};
+  check(qtnh_remap(t.h(), axis_map.data(), dst.n_idx(), dst.dims.data(), dst.split, dd, &o));
+  return wrap(o);
+}
 inline Tensor slice_local_dims(const Tensor& t, const std::vector<Dim>& new_local) {  // ops.hpp:166
   qtnh_tensor_t o;
   check(qtnh_slice_local_dims(t.h(), new_local.data(), &o));
