@@ -248,6 +248,10 @@ inline Tensor scale(const Tensor& t, Complex a) {  // ops.hpp:155
 }
 }  // namespace ops
 
+namespace remap {  // remap.hpp
+using ops::tensor_to_tensor;
+}  // namespace remap
+
 namespace linalg {  // psvd -> truncate_svd -> absorb_singular_* (linalg.hpp:441-523)
 enum class Absorb { none = QTNH_ABSORB_NONE, left = QTNH_ABSORB_LEFT, right = QTNH_ABSORB_RIGHT,
                     split = QTNH_ABSORB_SPLIT };
