@@ -394,7 +394,7 @@ __device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
 // rounds of up to 4 bits; a thread owns the 2^g amplitudes of one fiber in
 // registers for a round, so a round costs one shared load + store per amplitude
 // and one twiddle lookup per amplitude and layer, with one barrier per round.
-__device__ const double2 kQftSmallTw[15] = {{1.0, 0.0}, {1.0, 0.0}, {6.123233995736766e-17, 1.0}, {1.0, 0.0}, {0.7071067811865476, 0.7071067811865475}, {6.123233995736766e-17, 1.0}, {-0.7071067811865475, 0.7071067811865476}, {1.0, 0.0}, {0.9238795325112867, 0.3826834323650898}, {0.7071067811865476, 0.7071067811865475}, {0.38268343236508984, 0.9238795325112867}, {6.123233995736766e-17, 1.0}, {-0.3826834323650897, 0.9238795325112867}, {-0.7071067811865475, 0.7071067811865476}, {-0.9238795325112867, 0.3826834323650899}};  // e^{i pi k / 2^u}, index 2^u - 1 + k
+__constant__ double2 kQftSmallTw[15] = {{1.0, 0.0}, {1.0, 0.0}, {6.123233995736766e-17, 1.0}, {1.0, 0.0}, {0.7071067811865476, 0.7071067811865475}, {6.123233995736766e-17, 1.0}, {-0.7071067811865475, 0.7071067811865476}, {1.0, 0.0}, {0.9238795325112867, 0.3826834323650898}, {0.7071067811865476, 0.7071067811865475}, {0.38268343236508984, 0.9238795325112867}, {6.123233995736766e-17, 1.0}, {-0.3826834323650897, 0.9238795325112867}, {-0.7071067811865475, 0.7071067811865476}, {-0.9238795325112867, 0.3826834323650899}};  // e^{i pi k / 2^u}, index 2^u - 1 + k
 
 __device__ __forceinline__ int swz8(int i) { return i ^ ((i >> 3) & 7); }  // conflict-free 16-B rows
 
