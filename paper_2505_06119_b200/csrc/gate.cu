@@ -500,6 +500,90 @@ __global__ void __launch_bounds__(128) k_qft_low3(double2* __restrict__ psi, int
   }
 }
 
+// Variant: the chunk's first (top) round reads straight from global memory into
+// registers (16 independent loads per thread) and writes the shared chunk, so
+// one shared-memory write + read of the chunk and the staging copy disappear;
+// single buffer, occupancy hides the load latency.
+template <int G>
+__device__ __forceinline__ void qft_low_round_from_global(const double2* __restrict__ g, double2* __restrict__ data,
+                                                          const double2* __restrict__ tw, int S, int B) {
+  const int nf = 1 << (S - G);
+  for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+    const int lo = f & ((1 << B) - 1), hi = f >> B;
+    const int base = (hi << (B + G)) | lo;
+    double2 x[1 << G];
+#pragma unroll
+    for (int k = 0; k < (1 << G); ++k) x[k] = g[base + (k << B)];
+    double2 lof[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) lof[u] = (B + u) > 0 ? tw[(1 << (B + u)) + lo] : make_double2(1.0, 0.0);
+#pragma unroll
+    for (int u = G - 1; u >= 0; --u) {
+#pragma unroll
+      for (int k = 0; k < (1 << G); ++k) {
+        if (k & (1 << u)) continue;
+        const int k1 = k | (1 << u);
+        double2 a0 = x[k], a1 = x[k1];
+        x[k] = make_double2(a0.x + a1.x, a0.y + a1.y);
+        double2 d = make_double2(a0.x - a1.x, a0.y - a1.y);
+        const int kl = k & ((1 << u) - 1);
+        double2 ph = kl ? cmul2(kQftSmallTw[(1 << u) - 1 + kl], lof[u]) : lof[u];
+        x[k1] = (B + u) > 0 || kl ? cmul2(d, ph) : d;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < (1 << G); ++k) data[swz8(base + (k << B))] = x[k];
+  }
+}
+
+__global__ void __launch_bounds__(128) k_qft_low4(double2* __restrict__ psi, int64_t n_chunks, int S, int L) {
+  extern __shared__ double2 smq4[];
+  const int C = 1 << S;
+  double2* data = smq4;
+  double2* tw = smq4 + C;
+  for (int e = threadIdx.x; e < (1 << L); e += blockDim.x) {
+    if (e == 0) continue;
+    int t = 31 - __clz(e);
+    int v = e - (1 << t);
+    double sn, cs;
+    sincospi(static_cast<double>(v) * ldexp(1.0, -t), &sn, &cs);
+    tw[e] = make_double2(cs, sn);
+  }
+  __syncthreads();
+  const double sc = ldexp(1.0, -(L / 2)) * (L & 1 ? 0.70710678118654752440 : 1.0);  // (1/sqrt2)^L
+  for (int64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+    double2* g = psi + ch * C;
+    int T = L - 1;
+    {
+      const int gg = T + 1 >= 4 ? 4 : T + 1, B = T - gg + 1;
+      switch (gg) {
+        case 4: qft_low_round_from_global<4>(g, data, tw, S, B); break;
+        case 3: qft_low_round_from_global<3>(g, data, tw, S, B); break;
+        case 2: qft_low_round_from_global<2>(g, data, tw, S, B); break;
+        default: qft_low_round_from_global<1>(g, data, tw, S, B); break;
+      }
+      T = B - 1;
+    }
+    __syncthreads();
+    while (T >= 0) {
+      const int gg = T + 1 >= 4 ? 4 : T + 1, B = T - gg + 1;
+      switch (gg) {
+        case 4: qft_low_round<4>(data, tw, S, B); break;
+        case 3: qft_low_round<3>(data, tw, S, B); break;
+        case 2: qft_low_round<2>(data, tw, S, B); break;
+        default: qft_low_round<1>(data, tw, S, B); break;
+      }
+      __syncthreads();
+      T = B - 1;
+    }
+    for (int e = threadIdx.x; e < C; e += blockDim.x) {
+      double2 v = data[swz8(e)];
+      g[e] = make_double2(v.x * sc, v.y * sc);
+    }
+    __syncthreads();
+  }
+}
+
 struct QftGroupArgs {
   double2 tab[32];  // tab[2^u + k] = e^{i pi k / 2^u}, k < 2^u, u < 5
 };
@@ -846,7 +930,24 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
     QTNH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qft_low3, 128, smem));
     int grid = static_cast<int>(std::min<int64_t>(n_chunks, (int64_t)sms * std::max(1, occ)));
-    k_qft_low3<<<grid, 128, smem, st>>>(p, n_chunks, S, Lc);
+    static const bool v4 = [] {
+      const char* e = std::getenv("QTNH_QFT_LOW");
+      return e && e[0] == '4';
+    }();
+    if (v4) {
+      const size_t smem4 = ((size_t(1) << S) + (size_t(1) << Lc)) * sizeof(double2);
+      static bool attr4 = [] {
+        cudaFuncSetAttribute(k_qft_low4, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16 << kQftLowMax);
+        return true;
+      }();
+      (void)attr4;
+      int occ4 = 0;
+      QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, k_qft_low4, 128, smem4));
+      int grid4 = static_cast<int>(std::min<int64_t>(n_chunks, (int64_t)sms * std::max(1, occ4)));
+      k_qft_low4<<<grid4, 128, smem4, st>>>(p, n_chunks, S, Lc);
+    } else {
+      k_qft_low3<<<grid, 128, smem, st>>>(p, n_chunks, S, Lc);
+    }
     QTNH_LAUNCH_CHECK();
   }
 }
