@@ -930,9 +930,9 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
     QTNH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qft_low3, 128, smem));
     int grid = static_cast<int>(std::min<int64_t>(n_chunks, (int64_t)sms * std::max(1, occ)));
-    static const bool v4 = [] {
+    static const bool v4 = [] {  // default; QTNH_QFT_LOW=3 selects the double-buffered staging form
       const char* e = std::getenv("QTNH_QFT_LOW");
-      return e && e[0] == '4';
+      return !(e && e[0] == '3');
     }();
     if (v4) {
       const size_t smem4 = ((size_t(1) << S) + (size_t(1) << Lc)) * sizeof(double2);
