@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("nproc,legacy_min", [(2, None), (4, None), (2, "0")])
+@pytest.mark.parametrize("nproc,legacy_min", [(2, None), (3, None), (4, None), (2, "0")])
 def test_ipc_world_ops(tmp_path, nproc, legacy_min):
     """legacy_min "0": every block goes through legacy IPC handles (the path of
     multi-GiB shards)."""
