@@ -37,21 +37,29 @@ def main():
             t = Tensor.from_global(rk, IndexTuple([2] * n, k), DistParams(1, 1, 0), g)
             u = qtnh.ops.permute(t, perm, k)
             got = u.to_global_vector()
-            assert np.array_equal(bits(got), bits(P.permute([2] * n, g, perm))), ("permute", mode)
+            inside = t.in_span()  # with a non-power-of-two world some ranks hold nothing
+            if inside:
+                assert np.array_equal(bits(got), bits(P.permute([2] * n, g, perm))), ("permute", mode)
             # in-place distributed <-> local swap
             qtnh.swap_indices(t, 0, n - 1)
             sp = list(range(n))
             sp[0], sp[n - 1] = sp[n - 1], sp[0]
-            assert np.array_equal(bits(t.to_global_vector()), bits(P.permute([2] * n, g, sp))), ("swap", mode)
+            v = t.to_global_vector()
+            if inside:
+                assert np.array_equal(bits(v), bits(P.permute([2] * n, g, sp))), ("swap", mode)
             # dense gate on a distributed qubit (fused peer gate)
             s = Tensor.from_global(rk, IndexTuple([2] * n, k), DistParams(1, 1, 0), st)
             qtnh.apply_gate(s, [0, 5], circuits.FSIM)
             want = P.gate([2] * n, st, [0, 5], circuits.FSIM.reshape(-1))
-            assert np.linalg.norm(s.to_global_vector() - want) < 1e-12, ("gate", mode)
+            v = s.to_global_vector()
+            if inside:
+                assert np.linalg.norm(v - want) < 1e-12, ("gate", mode)
             # whole QFT (fused distributed layers + distributed bit reversal)
             q = Tensor.from_global(rk, IndexTuple([2] * n, k), DistParams(1, 1, 0), st)
             qtnh.qft(q, swaps=True)
-            assert np.linalg.norm(q.to_global_vector() - P.qft(n, st)) < 1e-12, ("qft", mode)
+            v = q.to_global_vector()
+            if inside:
+                assert np.linalg.norm(v - P.qft(n, st)) < 1e-12, ("qft", mode)
             # contraction with A sharded on open indices and a contracted one
             a = circuits.rng_normals(5, 2**n)
             b = circuits.rng_normals(6, 2**5)
