@@ -576,29 +576,8 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
       tab[(rd * npairs + k) * 2 + 1] = q;
     }
   const Dim per_group = batch >= 2 ? (batch + 1) / 2 : batch;  // see the two-stream split below
-  // Split a per-pair loop (K columns of the Gram, column tiles of the update) in
-  // `x` pieces so the grid fills whole waves: minimise waves(x) / x over x, where
-  // waves(x) = ceil(x * items / resident slots) -- a partial last wave of a
-  // multi-wave grid otherwise leaves up to half the GPU idle each round.
-  auto balance = [&](Dim items, Dim slots, Dim xmax) {
-    Dim best = 1;
-    double best_cost = 1e300;
-    for (Dim x = 1; x <= std::max<Dim>(1, xmax); ++x) {
-      const double waves = static_cast<double>((x * items + slots - 1) / slots);
-      const double cost = waves / static_cast<double>(x) * (1.0 + 0.02 * static_cast<double>(x));  // per-piece overhead
-      if (cost < best_cost - 1e-12) {
-        best_cost = cost;
-        best = x;
-      }
-    }
-    return best;
-  };
-  const size_t gram_smem_b = static_cast<size_t>(2) * P2 * ((B >= 32 ? 32 : 64) + 4) * 16;
-  int gram_occ = 1;
-  QTNH_CUDA(cudaFuncSetAttribute(k_svd_gram_mma_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem_b));
-  QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gram_occ, k_svd_gram_mma_t<B>, B * 8, gram_smem_b));
-  int splits = static_cast<int>(balance(npairs * per_group, static_cast<Dim>(sms()) * std::max(1, gram_occ),
-                                        std::min<Dim>(16, (L + kGramCols - 1) / kGramCols)));
+  int splits = static_cast<int>(std::max<Dim>(1, std::min<Dim>((2 * sms() + npairs * per_group - 1) / (npairs * per_group),
+                                                                (L + kGramCols - 1) / kGramCols)));
   DevBuf wk(static_cast<size_t>(batch * rp * W) * 16, r);
   DevBuf d_tab(tab.size() * sizeof(int), r);
   DevBuf part(static_cast<size_t>(batch * npairs * splits) * P2 * P2 * 16, r);
@@ -651,10 +630,8 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   std::vector<double> off_h(batch);
   const int max_sweeps = 40;
   const Dim gmax = (batch + ngroups - 1) / ngroups;
-  int upd_occ = 1;
-  QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&upd_occ, k_svd_update_mma_t<B>, B * 8, upd_smem));
   const unsigned ctiles = static_cast<unsigned>(
-      balance(npairs * gmax, static_cast<Dim>(sms()) * std::max(1, upd_occ), std::min<Dim>(16, (W + 47) / 48)));
+      std::min<Dim>((W + 47) / 48, std::max<Dim>(1, (B == 16 ? 8 : 4) * sms() / (npairs * gmax))));
   auto cleanup = [&] {
     for (int g = 0; g < ngroups; ++g) {
       if (ngroups > 1) {
