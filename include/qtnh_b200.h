@@ -162,6 +162,11 @@ int qtnh_tensor_to_global(qtnh_tensor_t t, double* host);
  * straight from HBM (no gather). Load (Tensor::load(Rank&, path), tensor.hpp:
  * 399-446) reads only this rank's block; dense / symmetric variants (0, 1) --
  * others return QTNH_E_INVALID_ARGUMENT and are materialised by the host layer. */
+/* Tensor::identity / Tensor::swap_tensor (tensor.hpp:144-164): element = 1 iff
+ * coords[in_pos[k]] == coords[out_pos[k]] for every pair (crossed != 0: swap, the
+ * two outputs exchanged; exactly two pairs), materialised densely on the device. */
+int qtnh_tensor_paired(qtnh_rank_t r, int n, const int64_t* dims, int split, const int64_t* dist, int n_pairs,
+                       const int* in_pos, const int* out_pos, int crossed, qtnh_tensor_t* out);
 int qtnh_tensor_save(qtnh_tensor_t t, const char* path);
 int qtnh_tensor_load(qtnh_rank_t r, const char* path, qtnh_tensor_t* out);
 

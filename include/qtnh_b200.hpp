@@ -152,6 +152,16 @@ class Tensor {  // tensor.hpp:53-695 (dense)
     return Tensor(h);
   }
 
+  // Tensor::identity / swap_tensor (tensor.hpp:144-164), dense on the device
+  static Tensor identity(Rank& r, const IndexTuple& s, DistParams d, const std::vector<int>& in_pos,
+                         const std::vector<int>& out_pos) {
+    return paired(r, s, d, in_pos, out_pos, 0);
+  }
+  static Tensor swap_tensor(Rank& r, const IndexTuple& s, DistParams d, const std::vector<int>& in_pos,
+                            const std::vector<int>& out_pos) {
+    return paired(r, s, d, in_pos, out_pos, 1);
+  }
+
   IndexTuple shape() const {
     IndexTuple s;
     s.dims.resize(qtnh_tensor_rank(h()));
@@ -183,6 +193,15 @@ class Tensor {  // tensor.hpp:53-695 (dense)
 
   // serialization (tensor.hpp:388-446), QTNHTEN1 byte-identical to the reference
   void save(const std::string& path) const { check(qtnh_tensor_save(h(), path.c_str())); }
+  static Tensor paired(Rank& r, const IndexTuple& s, DistParams d, const std::vector<int>& in_pos,
+                       const std::vector<int>& out_pos, int crossed) {
+    if (in_pos.size() != out_pos.size()) throw InvalidArgument("input/output position lists differ in length");
+    qtnh_tensor_t o;
+    int64_t dd[3] = {d.stretch, d.cycles, d.offset};
+    check(qtnh_tensor_paired(r.handle(), s.n_idx(), s.dims.data(), s.split, dd, static_cast<int>(in_pos.size()),
+                             in_pos.data(), out_pos.data(), crossed, &o));
+    return Tensor(o);
+  }
   static Tensor load(Rank& r, const std::string& path) {
     qtnh_tensor_t o;
     check(qtnh_tensor_load(r.handle(), path.c_str(), &o));

@@ -438,6 +438,36 @@ int qtnh_tensor_to_global(qtnh_tensor_t t, double* host) {
   });
 }
 
+int qtnh_tensor_paired(qtnh_rank_t r, int n, const int64_t* dims, int split, const int64_t* dist, int n_pairs,
+                       const int* in_pos, const int* out_pos, int crossed, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    RankCtx& x = ctx_of(r);
+    Shape s = shape_from(n, dims, split);
+    if (n_pairs) {
+      need(in_pos, "in_pos");
+      need(out_pos, "out_pos");
+    }
+    if (crossed && n_pairs != 2) throw_invalid("swap pairs exactly two indices");
+    std::vector<int> in(in_pos, in_pos + n_pairs), outp(out_pos, out_pos + n_pairs);
+    std::vector<char> used(n, 0);
+    auto chk = [&](int p) {
+      if (p < 0 || p >= n || used[p]) throw_invalid("invalid index pairing");
+      used[p] = 1;
+    };
+    for (int p : in) chk(p);
+    for (int p : outp) chk(p);
+    if (2 * n_pairs != n) throw_invalid("every index must belong to exactly one pair");
+    std::vector<int> eq_out = outp;
+    if (crossed) std::swap(eq_out[0], eq_out[1]);
+    for (int k = 0; k < n_pairs; ++k)
+      if (s.dims[in[k]] != s.dims[eq_out[k]]) throw_invalid("paired indices must have equal dimensions");
+    TP t = make_tensor(x, s, dist ? dist_from(dist) : Dist{}, true);
+    if (t->in_span) fill_paired(t->data(), t->shape.local_size(), t->block, t->shape.dims, t->shape.split, in, eq_out, x.stream);
+    *out = wrap(t);
+  });
+}
+
 int qtnh_tensor_save(qtnh_tensor_t t, const char* path) {
   return guard([&] {
     need(path, "path");

@@ -576,6 +576,53 @@ void canon_region(void* p, const std::vector<Dim>& dims, const std::vector<Dim>&
   QTNH_LAUNCH_CHECK();
 }
 
+struct PairSpec {
+  int n, npairs;
+  int64_t dims[32];
+  int eq_in[16], eq_out[16];
+};
+
+// Identity / swap tensors (tensor.hpp:144-164, 491-514) materialised densely: the
+// local element whose global coordinates satisfy every pairing is 1, else 0.
+__global__ void k_fill_paired(double2* __restrict__ out, int64_t nl, int64_t block, int split,
+                              const __grid_constant__ PairSpec ps) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nl; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c[32];
+    int64_t r = e;
+    for (int i = ps.n - 1; i >= split; --i) {
+      c[i] = r % ps.dims[i];
+      r /= ps.dims[i];
+    }
+    r = block;
+    for (int i = split - 1; i >= 0; --i) {
+      c[i] = r % ps.dims[i];
+      r /= ps.dims[i];
+    }
+    bool one = true;
+    for (int k = 0; k < ps.npairs; ++k) one &= c[ps.eq_in[k]] == c[ps.eq_out[k]];
+    out[e] = make_double2(one ? 1.0 : 0.0, 0.0);
+  }
+}
+
+void fill_paired(void* out, Dim nl, Dim block, const std::vector<Dim>& dims, int split, const std::vector<int>& eq_in,
+                 const std::vector<int>& eq_out, cudaStream_t st) {
+  if (nl <= 0) return;
+  PairSpec ps{};
+  ps.n = static_cast<int>(dims.size());
+  ps.npairs = static_cast<int>(eq_in.size());
+  if (ps.n > 32 || ps.npairs > 16) throw_invalid("paired tensor rank too large");
+  for (int i = 0; i < ps.n; ++i) ps.dims[i] = dims[i];
+  for (int k = 0; k < ps.npairs; ++k) {
+    ps.eq_in[k] = eq_in[k];
+    ps.eq_out[k] = eq_out[k];
+  }
+  int dev = 0;
+  QTNH_CUDA(cudaGetDevice(&dev));
+  int grid = static_cast<int>(std::min<Dim>((nl + 255) / 256, (Dim)sm_count(dev) * 8));
+  k_fill_paired<<<grid, 256, 0, st>>>(static_cast<double2*>(out), nl, block, split, ps);
+  QTNH_LAUNCH_CHECK();
+}
+
 void fill_zero(void* out, Dim n, cudaStream_t st) {
   if (n <= 0) return;
   int dev = 0;

@@ -29,6 +29,10 @@ CopyBox permute_box(const std::vector<Dim>& dims, const std::vector<int>& perm);
 // Elementwise y = alpha * conj?(x) over n complex numbers.
 void scale_conj(const void* in, void* out, Dim n, double re, double im, bool conj, cudaStream_t st);
 void fill_zero(void* out, Dim n, cudaStream_t st);
+// Dense materialisation of an identity / swap tensor's local block (1 where every
+// pairing eq_in[k] == eq_out[k] holds on the global coordinates).
+void fill_paired(void* out, Dim nl, Dim block, const std::vector<Dim>& dims, int split, const std::vector<int>& eq_in,
+                 const std::vector<int>& eq_out, cudaStream_t st);
 
 // In-place exchange of two equally shaped strided regions (elements [begin, end)
 // of the row-major enumeration of `dims`): a[off] <-> b[off], zero canonicalised.

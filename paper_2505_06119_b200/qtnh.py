@@ -441,6 +441,24 @@ class Tensor:
         return Tensor(rank, h)
 
     @staticmethod
+    def identity(rank: Rank, shape: IndexTuple, dist, in_pos: Sequence[int], out_pos: Sequence[int]) -> "Tensor":
+        """Tensor::identity (tensor.hpp:144-153), materialised densely on the device."""
+        h = C.c_void_p()
+        check(lib.qtnh_tensor_paired(rank._h, shape.n_idx(), i64_array(shape.dims), shape.split,
+                                     _dist(dist).as_array(), len(in_pos), i32_array(in_pos), i32_array(out_pos), 0,
+                                     C.byref(h)))
+        return Tensor(rank, h)
+
+    @staticmethod
+    def swap_tensor(rank: Rank, shape: IndexTuple, dist, in_pos: Sequence[int], out_pos: Sequence[int]) -> "Tensor":
+        """Tensor::swap_tensor (tensor.hpp:155-164): outputs are the transposed inputs."""
+        h = C.c_void_p()
+        check(lib.qtnh_tensor_paired(rank._h, shape.n_idx(), i64_array(shape.dims), shape.split,
+                                     _dist(dist).as_array(), len(in_pos), i32_array(in_pos), i32_array(out_pos), 1,
+                                     C.byref(h)))
+        return Tensor(rank, h)
+
+    @staticmethod
     def scalar(rank: Rank, value: complex, dist=None) -> "Tensor":
         return Tensor.dense(rank, IndexTuple([], 0), dist, np.array([value]))
 

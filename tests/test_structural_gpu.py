@@ -350,3 +350,51 @@ def test_tensor_to_tensor_remap(dims, split, dist, amap, dsplit, ddist, world, d
         want = pad
     for o in outs:
         assert np.array_equal(bits(o), bits(want.reshape(-1)))
+
+
+def _paired_dense(dims, pairs_in, pairs_out, crossed):
+    eq_out = list(pairs_out)
+    if crossed:
+        eq_out[0], eq_out[1] = eq_out[1], eq_out[0]
+    idx = np.indices(dims).reshape(len(dims), -1)
+    ok = np.ones(idx.shape[1], bool)
+    for a, b in zip(pairs_in, eq_out):
+        ok &= idx[a] == idx[b]
+    return ok.astype(np.complex128)
+
+
+@pytest.mark.parametrize("dims,split,pin,pout,crossed,world", [
+    ([2, 3, 2, 3], 0, [0, 1], [2, 3], False, 1),
+    ([3, 2, 3, 2], 1, [0, 3], [2, 1], False, 3),       # pairs of different index types (scatter/gather form)
+    ([2, 2, 2, 2], 2, [0, 1], [2, 3], True, 4),         # swap tensor, distributed
+    ([4, 3, 3, 4], 0, [0, 1], [3, 2], True, 1),
+])
+def test_identity_and_swap_tensors(dims, split, pin, pout, crossed, world):
+    """Tensor::identity / swap_tensor (tensor.hpp:144-164) materialised on the device."""
+    def body(rk):
+        mk = Tensor.swap_tensor if crossed else Tensor.identity
+        t = mk(rk, IndexTuple(dims, split), DistParams(1, 1, 0), pin, pout)
+        return t.to_global_vector() if t.in_span() else None
+
+    outs = [o for o in World(world).run(body) if o is not None]
+    want = _paired_dense(dims, pin, pout, crossed)
+    for o in outs:
+        assert np.array_equal(o, want)
+
+
+def test_contracting_a_swap_tensor_is_a_permutation():
+    """SPEC: contraction with a swap tensor = index exchange (tensor.hpp:157-164)."""
+    from paper_2505_06119_b200.qtnh import contract
+    n = 6
+    g = circuits.counter_state(4, 2**n)
+
+    def body(rk):
+        st = Tensor.from_global(rk, IndexTuple([2] * n, 0), None, g)
+        sw = Tensor.swap_tensor(rk, IndexTuple([2, 2, 2, 2], 0), None, [0, 1], [2, 3])
+        c = contract(st, sw, [1, 4], [0, 1])  # result: open(state) then the swap outputs
+        return c.to_global_vector()
+
+    got = run_collect(World(1), body)
+    # result order: state qubits 0,2,3,5 then outputs (2 = in1 -> q4, 3 = in0 -> q1)
+    want = g.reshape([2] * n).transpose([0, 2, 3, 5, 4, 1]).reshape(-1)
+    assert np.array_equal(got, want)
