@@ -367,7 +367,7 @@ def _paired_dense(dims, pairs_in, pairs_out, crossed):
     ([2, 3, 2, 3], 0, [0, 1], [2, 3], False, 1),
     ([3, 2, 3, 2], 1, [0, 3], [2, 1], False, 3),       # pairs of different index types (scatter/gather form)
     ([2, 2, 2, 2], 2, [0, 1], [2, 3], True, 4),         # swap tensor, distributed
-    ([4, 3, 3, 4], 0, [0, 1], [3, 2], True, 1),
+    ([4, 3, 3, 4], 0, [0, 1], [2, 3], True, 1),         # crossed: in0 pairs with out1
 ])
 def test_identity_and_swap_tensors(dims, split, pin, pout, crossed, world):
     """Tensor::identity / swap_tensor (tensor.hpp:144-164) materialised on the device."""
