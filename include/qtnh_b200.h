@@ -167,6 +167,12 @@ int qtnh_tensor_to_global(qtnh_tensor_t t, double* host);
  * two outputs exchanged; exactly two pairs), materialised densely on the device. */
 int qtnh_tensor_paired(qtnh_rank_t r, int n, const int64_t* dims, int split, const int64_t* dist, int n_pairs,
                        const int* in_pos, const int* out_pos, int crossed, qtnh_tensor_t* out);
+/* Tensor::diagonal (tensor.hpp:114-142) over the symmetric half-split layout
+ * (in_dist, out_dist; in_local, out_local), materialised densely: only blocks with
+ * equal input / output distributed coordinates carry their slice of the diagonal
+ * (`count` complex values, row-major over the input coordinates). */
+int qtnh_tensor_diagonal(qtnh_rank_t r, int n, const int64_t* dims, int split, const int64_t* dist,
+                         const double* diag_global, int64_t count, qtnh_tensor_t* out);
 int qtnh_tensor_save(qtnh_tensor_t t, const char* path);
 int qtnh_tensor_load(qtnh_rank_t r, const char* path, qtnh_tensor_t* out);
 

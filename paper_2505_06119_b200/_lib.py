@@ -67,6 +67,7 @@ _SIGS = {
     "qtnh_tensor_upload_local": (i32, [vp, vp]),
     "qtnh_tensor_to_global": (i32, [vp, vp]),
     "qtnh_tensor_paired": (i32, [vp, i32, P_i64, i32, P_i64, i32, P_i32, P_i32, i32, C.POINTER(vp)]),
+    "qtnh_tensor_diagonal": (i32, [vp, i32, P_i64, i32, P_i64, vp, i64, C.POINTER(vp)]),
     "qtnh_tensor_save": (i32, [vp, C.c_char_p]),
     "qtnh_tensor_load": (i32, [vp, C.c_char_p, C.POINTER(vp)]),
     "qtnh_permute": (i32, [vp, P_i32, i32, C.POINTER(vp)]),

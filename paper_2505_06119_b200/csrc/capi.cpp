@@ -468,6 +468,55 @@ int qtnh_tensor_paired(qtnh_rank_t r, int n, const int64_t* dims, int split, con
   });
 }
 
+namespace {
+void check_symmetric_shape(const Shape& s) {  // tensor.hpp:479-489
+  const int split = s.split, nl = s.n_idx() - s.split;
+  if (split % 2 != 0 || nl % 2 != 0) throw_invalid("symmetric tensors split both index groups in half");
+  for (int i = 0; i < split / 2; ++i)
+    if (s.dims[i] != s.dims[split / 2 + i]) throw_invalid("symmetric distributed dimensions differ");
+  for (int i = 0; i < nl / 2; ++i)
+    if (s.dims[split + i] != s.dims[split + nl / 2 + i]) throw_invalid("symmetric local dimensions differ");
+}
+}  // namespace
+
+int qtnh_tensor_diagonal(qtnh_rank_t r, int n, const int64_t* dims, int split, const int64_t* dist,
+                         const double* diag_global, int64_t count, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    RankCtx& x = ctx_of(r);
+    Shape s = shape_from(n, dims, split);
+    check_symmetric_shape(s);
+    Dim nd_in = 1, nl_in = 1;
+    for (int i = 0; i < split / 2; ++i) nd_in *= s.dims[i];
+    const int nl = n - split;
+    for (int i = 0; i < nl / 2; ++i) nl_in *= s.dims[split + i];
+    if (count != nd_in * nl_in) throw_invalid("diagonal payload has wrong length");
+    if (count) need(diag_global, "diag_global");
+    TP t = make_tensor(x, s, dist ? dist_from(dist) : Dist{}, true);
+    if (t->in_span) {
+      fill_zero(t->data(), t->shape.local_size(), x.stream);
+      auto dc = unflat(t->block, t->shape.dist_dims());
+      const int k = split / 2;
+      bool on_diag = true;
+      for (int i = 0; i < k; ++i) on_diag &= dc[i] == dc[k + i];
+      if (on_diag && nl_in > 0) {
+        Dim b_in = flat(std::vector<Dim>(dc.begin(), dc.begin() + k),
+                        std::vector<Dim>(s.dims.begin(), s.dims.begin() + k));
+        DevBuf tmp(static_cast<size_t>(nl_in) * 16, x);
+        QTNH_CUDA(cudaMemcpyAsync(tmp.ptr, diag_global + 2 * b_in * nl_in, nl_in * 16, cudaMemcpyHostToDevice,
+                                  x.stream));
+        CopyBox b;  // local block (in, out) row-major: diagonal at j * (nl_in + 1)
+        b.dims = {nl_in};
+        b.in_stride = {1};
+        b.out_stride = {nl_in + 1};
+        strided_copy(tmp.ptr, t->data(), b, false, x.stream);
+        QTNH_CUDA(cudaStreamSynchronize(x.stream));  // host payload and staging die here
+      }
+    }
+    *out = wrap(t);
+  });
+}
+
 int qtnh_tensor_save(qtnh_tensor_t t, const char* path) {
   return guard([&] {
     need(path, "path");

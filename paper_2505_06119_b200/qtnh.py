@@ -459,6 +459,15 @@ class Tensor:
         return Tensor(rank, h)
 
     @staticmethod
+    def diagonal(rank: Rank, shape: IndexTuple, dist, diag_global) -> "Tensor":
+        """Tensor::diagonal (tensor.hpp:114-142), materialised densely on the device."""
+        d = _as_c128(diag_global)
+        h = C.c_void_p()
+        check(lib.qtnh_tensor_diagonal(rank._h, shape.n_idx(), i64_array(shape.dims), shape.split,
+                                       _dist(dist).as_array(), d.ctypes.data, d.size, C.byref(h)))
+        return Tensor(rank, h)
+
+    @staticmethod
     def scalar(rank: Rank, value: complex, dist=None) -> "Tensor":
         return Tensor.dense(rank, IndexTuple([], 0), dist, np.array([value]))
 

@@ -398,3 +398,30 @@ def test_contracting_a_swap_tensor_is_a_permutation():
     # result order: state qubits 0,2,3,5 then outputs (2 = in1 -> q4, 3 = in0 -> q1)
     want = g.reshape([2] * n).transpose([0, 2, 3, 5, 4, 1]).reshape(-1)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("dims,split,world", [([2, 3, 2, 3], 0, 1), ([2, 2, 3, 3], 2, 4), ([3, 3, 2, 4, 2, 4], 2, 9)])
+def test_diagonal_tensor(dims, split, world):
+    """Tensor::diagonal (tensor.hpp:114-142) on the symmetric half-split layout."""
+    r = len(dims)
+    kd, kl = split // 2, (r - split) // 2
+    in_pos = list(range(kd)) + list(range(split, split + kl))
+    n_in = int(np.prod([dims[p] for p in in_pos]))
+    diag = circuits.rng_normals(12, n_in)
+    idx = np.indices(dims).reshape(r, -1)
+    on = np.ones(idx.shape[1], bool)
+    for i in range(kd):
+        on &= idx[i] == idx[kd + i]
+    for i in range(kl):
+        on &= idx[split + i] == idx[split + kl + i]
+    flat_in = np.zeros(idx.shape[1], np.int64)
+    for p in in_pos:
+        flat_in = flat_in * dims[p] + idx[p]
+    want = np.where(on, diag[np.minimum(flat_in, n_in - 1)], 0)
+
+    def body(rk):
+        t = Tensor.diagonal(rk, IndexTuple(dims, split), DistParams(1, 1, 0), diag)
+        return t.to_global_vector() if t.in_span() else None
+
+    for o in [o for o in World(world).run(body) if o is not None]:
+        assert np.array_equal(o, want)
