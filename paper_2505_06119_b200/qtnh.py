@@ -531,8 +531,9 @@ class Tensor:
     @staticmethod
     def load(rank: "Rank", path: str) -> "Tensor":
         """Read a QTNHTEN1 file (every rank reads it independently, tensor.hpp:399-440).
-        Dense and symmetric payloads load as they are; diagonal, identity and swap
-        variants are materialised densely (tensor.hpp:282-296)."""
+        Dense and symmetric payloads go straight into HBM (qtnh_tensor_load);
+        diagonal, identity and swap variants are materialised densely on the device
+        by their constructors (tensor.hpp:282-296)."""
         import struct
 
         with open(path, "rb") as f:
@@ -558,42 +559,23 @@ class Tensor:
             raise Error("truncated tensor stream")
         shape = IndexTuple(dims, split)
         total = shape.total_size()
-        if var in (3, 4):  # identity / swap: pairs (in, out) of positions
+        dist = DistParams(st, cy, of)
+        if var in (3, 4):  # identity / swap: pairs (in, out) of positions, built on the device
             (npairs,) = struct.unpack_from("<Q", blob, off)
             off += 8
             pr = struct.unpack_from("<%dq" % (2 * npairs), blob, off)
             pin, pout = list(pr[0::2]), list(pr[1::2])
-            if var == 4:
-                pout[0], pout[1] = pout[1], pout[0]
-            idx = np.indices(dims).reshape(r, -1)
-            ok = np.ones(total, bool)
-            for a, b in zip(pin, pout):
-                ok &= idx[a] == idx[b]
-            g = ok.astype(np.complex128)
-        else:
-            (count,) = struct.unpack_from("<Q", blob, off)
-            off += 8
-            if len(blob) < off + 16 * count:
-                raise Error("truncated tensor stream")
-            payload = np.frombuffer(blob, dtype="<c16", count=count, offset=off).astype(np.complex128)
-            if var in (0, 1):
-                g = payload
-            elif var == 2:  # diagonal over the half-split (in, out) layout
-                kd, kl = split // 2, (r - split) // 2
-                in_dims = dims[:kd] + dims[split:split + kl]
-                idx = np.indices(dims).reshape(r, -1)
-                on = np.ones(total, bool)
-                for i in range(kd):
-                    on &= idx[i] == idx[kd + i]
-                for i in range(kl):
-                    on &= idx[split + i] == idx[split + kl + i]
-                flat_in = np.zeros(total, np.int64)
-                for pos in list(range(kd)) + list(range(split, split + kl)):
-                    flat_in = flat_in * dims[pos] + idx[pos]
-                g = np.where(on, payload[np.minimum(flat_in, count - 1)], 0)
-            else:
-                raise Error("corrupt tensor stream")
-        return Tensor.from_global(rank, shape, DistParams(st, cy, of), g)
+            return (Tensor.swap_tensor if var == 4 else Tensor.identity)(rank, shape, dist, pin, pout)
+        (count,) = struct.unpack_from("<Q", blob, off)
+        off += 8
+        if len(blob) < off + 16 * count:
+            raise Error("truncated tensor stream")
+        payload = np.frombuffer(blob, dtype="<c16", count=count, offset=off).astype(np.complex128)
+        if var in (0, 1):
+            return Tensor.from_global(rank, shape, dist, payload)
+        if var == 2:  # diagonal over the half-split (in, out) layout, built on the device
+            return Tensor.diagonal(rank, shape, dist, payload)
+        raise Error("corrupt tensor stream")
 
     def free(self) -> None:
         if self._h is not None:
