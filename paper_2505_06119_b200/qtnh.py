@@ -558,7 +558,6 @@ class Tensor:
         except struct.error:
             raise Error("truncated tensor stream")
         shape = IndexTuple(dims, split)
-        total = shape.total_size()
         dist = DistParams(st, cy, of)
         if var in (3, 4):  # identity / swap: pairs (in, out) of positions, built on the device
             (npairs,) = struct.unpack_from("<Q", blob, off)
