@@ -110,6 +110,16 @@ int qtnh_rank_set_stream(qtnh_rank_t r, void* stream);
 int qtnh_rank_reset_stream(qtnh_rank_t r);
 void* qtnh_rank_stream(qtnh_rank_t r);
 int qtnh_rank_synchronize(qtnh_rank_t r);
+/* CUDA-graph capture of a launch-bound sequence of in-place, rank-local ops on
+ * existing tensors (gate applications, qubit swaps, QFT layers): everything the
+ * rank launches between begin and end is recorded on its stream (thread-local
+ * capture mode) and replayed with one qtnh_graph_launch. Collectives, host
+ * copies and ops that allocate result tensors must stay outside a capture. */
+typedef struct qtnh_graph_s* qtnh_graph_t;
+int qtnh_rank_capture_begin(qtnh_rank_t r);
+int qtnh_rank_capture_end(qtnh_rank_t r, qtnh_graph_t* out);
+int qtnh_graph_launch(qtnh_rank_t r, qtnh_graph_t g);
+int qtnh_graph_destroy(qtnh_graph_t g);
 int qtnh_barrier(qtnh_rank_t r);
 
 /* Group::all_to_all_v (runtime.hpp:448-475) on device buffers of complex128

@@ -44,6 +44,10 @@ _SIGS = {
     "qtnh_rank_set_stream": (i32, [vp, vp]),
     "qtnh_rank_reset_stream": (i32, [vp]),
     "qtnh_rank_stream": (vp, [vp]),
+    "qtnh_rank_capture_begin": (i32, [vp]),
+    "qtnh_rank_capture_end": (i32, [vp, C.POINTER(vp)]),
+    "qtnh_graph_launch": (i32, [vp, vp]),
+    "qtnh_graph_destroy": (i32, [vp]),
     "qtnh_rank_synchronize": (i32, [vp]),
     "qtnh_barrier": (i32, [vp]),
     "qtnh_all_to_all_v": (i32, [vp, i32, P_i32, vp, P_i64, P_i64, vp, P_i64, P_i64]),

@@ -296,6 +296,56 @@ int qtnh_rank_reset_stream(qtnh_rank_t r) {
 
 void* qtnh_rank_stream(qtnh_rank_t r) { return r ? static_cast<void*>(r->ctx->stream) : nullptr; }
 
+struct qtnh_graph_s {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+int qtnh_rank_capture_begin(qtnh_rank_t r) {
+  return guard([&] {
+    RankCtx& c = ctx_of(r);
+    if (c.stream == nullptr) throw_invalid("stream capture needs a non-default rank stream");
+    QTNH_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+  });
+}
+
+int qtnh_rank_capture_end(qtnh_rank_t r, qtnh_graph_t* out) {
+  return guard([&] {
+    need(out, "out");
+    RankCtx& c = ctx_of(r);
+    auto* g = new qtnh_graph_s;
+    cudaError_t e = cudaStreamEndCapture(c.stream, &g->graph);
+    if (e != cudaSuccess) {
+      delete g;
+      QTNH_CUDA(e);
+    }
+    e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+    if (e != cudaSuccess) {
+      cudaGraphDestroy(g->graph);
+      delete g;
+      QTNH_CUDA(e);
+    }
+    *out = g;
+  });
+}
+
+int qtnh_graph_launch(qtnh_rank_t r, qtnh_graph_t g) {
+  return guard([&] {
+    need(g, "graph");
+    QTNH_CUDA(cudaGraphLaunch(g->exec, ctx_of(r).stream));
+    g_kernel_launches.fetch_add(1);
+  });
+}
+
+int qtnh_graph_destroy(qtnh_graph_t g) {
+  return guard([&] {
+    if (!g) return;
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+  });
+}
+
 int qtnh_rank_synchronize(qtnh_rank_t r) {
   return guard([&] { QTNH_CUDA(cudaStreamSynchronize(ctx_of(r).stream)); });
 }

@@ -192,6 +192,11 @@ class Rank:
     def barrier(self) -> None:
         check(lib.qtnh_barrier(self._h))
 
+    def capture(self) -> "Graph":
+        """Record the rank-local, in-place ops issued inside ``with rk.capture() as g:``
+        into a CUDA graph; ``g.launch()`` replays them with one launch."""
+        return Graph(self)
+
     def all_to_all_v(self, members: Sequence[int], send_ptr: int, send_counts: Sequence[int],
                      send_displs: Sequence[int], recv_ptr: int, recv_counts: Sequence[int],
                      recv_displs: Sequence[int]) -> None:
@@ -260,6 +265,39 @@ class Rank:
             t.free()
         check(lib.qtnh_rank_release(self._h))
         self._h = None
+
+
+class Graph:
+    """CUDA graph of a captured, launch-bound op sequence (qtnh_rank_capture_*)."""
+
+    def __init__(self, rank: "Rank"):
+        self.rank = rank
+        self._h = None
+
+    def __enter__(self) -> "Graph":
+        check(lib.qtnh_rank_capture_begin(self.rank._h))
+        return self
+
+    def __exit__(self, exc_type, exc, tb) -> None:
+        h = C.c_void_p()
+        status = lib.qtnh_rank_capture_end(self.rank._h, C.byref(h))
+        if exc_type is None:
+            check(status)
+            self._h = h
+
+    def launch(self) -> None:
+        check(lib.qtnh_graph_launch(self.rank._h, self._h))
+
+    def free(self) -> None:
+        if self._h is not None:
+            lib.qtnh_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 class World:

@@ -280,3 +280,47 @@ def test_inplace_distributed_swap(dims, split, a, b, world, chunk, peer_mode):
     finally:
         check(lib.qtnh_set_option(b"swap_chunk_bytes", float(1 << 31)))
     assert np.array_equal(bits(got), bits(P.permute(dims, g, perm)))
+
+
+def test_cuda_graph_of_a_gate_sequence():
+    """A launch-bound gate sequence (config 0's QFT-16 gate by gate: 16 H, 120 CP,
+    8 in-place SWAPs) captured once into a CUDA graph and replayed matches the
+    direct sequence, and replays are repeatable."""
+    from paper_2505_06119_b200.qtnh import swap_indices
+    n = 16
+    st = circuits.counter_state(61, 2**n)
+    st /= np.linalg.norm(st)
+    gates = circuits.qft_gates(n, swaps=True)
+
+    def seq(t):
+        for kind, q, g in gates:
+            if kind == "h":
+                apply_gate(t, q, g)
+            elif kind == "cp":
+                apply_gate(t, q, g, diagonal=True)
+            else:
+                swap_indices(t, q[0], q[1])
+
+    def body(rk):
+        a = Tensor.from_global(rk, IndexTuple([2] * n, 0), None, st)
+        seq(a)
+        direct = a.to_global_vector()
+        b = Tensor.from_global(rk, IndexTuple([2] * n, 0), None, st)
+        rk.synchronize()
+        with rk.capture() as g:
+            seq(b)
+        rk.synchronize()
+        untouched = b.to_global_vector()  # capture records, it does not run
+        g.launch()
+        once = b.to_global_vector()
+        g.launch()
+        twice = b.to_global_vector()
+        g.free()
+        return direct, untouched, once, twice
+
+    direct, untouched, once, twice = run_collect(World(1), body)
+    assert np.array_equal(untouched, st)
+    assert np.array_equal(once, direct)
+    assert rel_l2(direct, P.qft(n, st)) < TOL
+    seq2 = P.qft(n, P.qft(n, st))
+    assert rel_l2(twice, seq2) < 1e-10
