@@ -202,6 +202,15 @@ int qtnh_pad_local_dims(qtnh_tensor_t t, const int64_t* new_local_dims, qtnh_ten
 int qtnh_conj(qtnh_tensor_t t, qtnh_tensor_t* out);
 int qtnh_scale(qtnh_tensor_t t, double re, double im, qtnh_tensor_t* out);
 
+/* Contraction order of a labelled network (SPEC network::contract_order,
+ * SPEC.md:391-399): tensor t has labels[label_offsets[t] .. label_offsets[t+1]),
+ * label l has log2 dimension label_log2[l]; a label shared by two tensors is a bond.
+ * Seeded randomised greedy (trial 0: smallest result first, ties by hash), best of
+ * `trials` by (largest intermediate, flops). order_out receives n_tensors - 1
+ * pairs; the result of step s gets id n_tensors + s. */
+int qtnh_plan_order(int n_tensors, const int* label_offsets, const int* labels, int n_labels,
+                    const double* label_log2, uint64_t seed, int trials, int* order_out);
+
 /* ---- contraction ----------------------------------------------------------- */
 /* Contract a[a_pos[i]] with b[b_pos[i]] for i < n_pairs. Result indices: open
  * indices of a, then open indices of b, each in operand order;

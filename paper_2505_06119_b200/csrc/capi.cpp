@@ -582,6 +582,27 @@ int qtnh_tensor_load(qtnh_rank_t r, const char* path, qtnh_tensor_t* out) {
   });
 }
 
+int qtnh_plan_order(int n_tensors, const int* label_offsets, const int* labels, int n_labels,
+                    const double* label_log2, uint64_t seed, int trials, int* order_out) {
+  return guard([&] {
+    if (n_tensors < 1) throw_invalid("empty network");
+    need(label_offsets, "label_offsets");
+    need(order_out, "order_out");
+    std::vector<std::vector<int>> lab(n_tensors);
+    for (int t = 0; t < n_tensors; ++t)
+      for (int j = label_offsets[t]; j < label_offsets[t + 1]; ++j) {
+        if (labels[j] < 0 || labels[j] >= n_labels) throw_invalid("label id out of range");
+        lab[t].push_back(labels[j]);
+      }
+    std::vector<double> lg(label_log2, label_log2 + n_labels);
+    auto order = plan_order(lab, lg, seed, trials);
+    for (size_t i = 0; i < order.size(); ++i) {
+      order_out[2 * i] = order[i].first;
+      order_out[2 * i + 1] = order[i].second;
+    }
+  });
+}
+
 // ---- ops --------------------------------------------------------------------------
 int qtnh_permute(qtnh_tensor_t t, const int* perm, int new_split, qtnh_tensor_t* out) {
   return guard([&] {

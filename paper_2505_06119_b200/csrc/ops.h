@@ -48,6 +48,10 @@ TP op_slice_local(const TP& t, const std::vector<Dim>& nl);                // op
 TP op_pad_local(const TP& t, const std::vector<Dim>& nl);                  // ops.hpp:201
 TP op_scale(const TP& t, double re, double im, bool conj);                 // ops.hpp:147-161
 void op_to_global(const TensorImpl& t, double* host);                      // tensor.hpp:341
+// Contraction order of a labelled network (plan.cpp); ids of results continue
+// after the n input tensors in step order.
+std::vector<std::pair<int, int>> plan_order(const std::vector<std::vector<int>>& labels, const std::vector<double>& lg,
+                                            uint64_t seed, int trials);
 void op_save(const TensorImpl& t, const std::string& path);                // tensor.hpp:388-397
 TP op_load(RankCtx& r, const std::string& path);                           // tensor.hpp:399-446 (dense)
 

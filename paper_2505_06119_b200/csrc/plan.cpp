@@ -1,0 +1,162 @@
+// Native contraction-order planner for tensor networks (SPEC network::contract_order,
+// SPEC.md:391-399; smallest result first, ties by a seeded hash).
+//
+// Trial 0 is the plain greedy: repeatedly contract the connected pair whose
+// result has the fewest elements (log2 size), ties broken by hash_counter(seed,
+// a, b). Further trials are randomised greedy passes: key = log2|C| -
+// alpha (log2|A| + log2|B|) + Gaussian noise of width temp, alpha and temp drawn
+// per trial from the counter-based generator. The order with the smallest largest
+// intermediate, then the fewest flops, wins. Pair keys live in an ordered set and
+// only the pairs of a merged tensor are recomputed, so a 645-tensor network plans
+// in milliseconds per trial (the Python greedy took ~0.6 s per trial).
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <map>
+#include <set>
+#include <tuple>
+#include <vector>
+
+#include "common.h"
+
+namespace qtnhb {
+
+namespace {
+
+uint64_t splitmix(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+uint64_t hash3(uint64_t s, uint64_t a, uint64_t b) { return splitmix(splitmix(splitmix(s) ^ a) ^ b); }
+double unit(uint64_t u) { return static_cast<double>(u >> 11) * 0x1.0p-53; }
+
+struct Trial {
+  std::vector<std::pair<int, int>> order;
+  double peak = 0, flops = 0;
+};
+
+Trial greedy(const std::vector<std::vector<int>>& labels0, const std::vector<double>& lg, int n_ids, uint64_t seed,
+             double alpha, double temp, uint64_t noise_seed) {
+  std::map<int, std::vector<int>> lab;  // tensor id -> labels
+  std::map<int, double> lsz;
+  std::vector<std::vector<int>> owners(lg.size());
+  for (int t = 0; t < static_cast<int>(labels0.size()); ++t) {
+    lab[t] = labels0[t];
+    double s = 0;
+    for (int l : labels0[t]) {
+      s += lg[l];
+      owners[l].push_back(t);
+    }
+    lsz[t] = s;
+  }
+  uint64_t ncount = 0;
+  auto noise = [&]() {
+    if (temp <= 0) return 0.0;
+    double u1 = unit(hash3(noise_seed, ncount, 1)), u2 = unit(hash3(noise_seed, ncount, 2));
+    ++ncount;
+    if (u1 < 1e-300) u1 = 1e-300;
+    return temp * std::sqrt(-2.0 * std::log(u1)) * std::cos(2 * M_PI * u2);
+  };
+  auto shared_lg = [&](int a, int b) {
+    const auto& la = lab[a];
+    const auto& lb = lab[b];
+    double s = 0;
+    for (int x : la)
+      if (std::find(lb.begin(), lb.end(), x) != lb.end()) s += lg[x];
+    return s;
+  };
+  using Key = std::tuple<double, uint64_t, int, int>;  // key, tie hash, a, b (a < b)
+  std::set<Key> pq;
+  std::map<std::pair<int, int>, Key> keyof;
+  auto add_pair = [&](int a, int b) {
+    if (a > b) std::swap(a, b);
+    if (keyof.count({a, b})) return;
+    double r = lsz[a] + lsz[b] - 2 * shared_lg(a, b);
+    Key k{r - alpha * (lsz[a] + lsz[b]) + noise(), hash3(seed, static_cast<uint64_t>(a), static_cast<uint64_t>(b)), a, b};
+    pq.insert(k);
+    keyof[{a, b}] = k;
+  };
+  auto drop_pairs_of = [&](int t) {
+    for (auto it = keyof.begin(); it != keyof.end();) {
+      if (it->first.first == t || it->first.second == t) {
+        pq.erase(it->second);
+        it = keyof.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  };
+  for (int l = 0; l < static_cast<int>(owners.size()); ++l)
+    if (owners[l].size() == 2) add_pair(owners[l][0], owners[l][1]);
+  Trial tr;
+  int next = n_ids;
+  while (lab.size() > 1) {
+    int a, b;
+    if (pq.empty()) {  // disconnected pieces: outer product of the two smallest
+      std::vector<std::pair<double, int>> v;
+      for (auto& kv : lab) v.push_back({lsz[kv.first], kv.first});
+      std::sort(v.begin(), v.end());
+      a = std::min(v[0].second, v[1].second);
+      b = std::max(v[0].second, v[1].second);
+    } else {
+      auto k = *pq.begin();
+      a = std::get<2>(k);
+      b = std::get<3>(k);
+    }
+    const double sh = shared_lg(a, b);
+    const double M = lsz[a] - sh, N = lsz[b] - sh;
+    tr.flops += 8.0 * std::exp2(M + N + sh);
+    tr.peak = std::max(tr.peak, M + N);
+    tr.order.push_back({a, b});
+    std::vector<int> nl;
+    for (int x : lab[a])
+      if (std::find(lab[b].begin(), lab[b].end(), x) == lab[b].end()) nl.push_back(x);
+    for (int x : lab[b])
+      if (std::find(lab[a].begin(), lab[a].end(), x) == lab[a].end()) nl.push_back(x);
+    drop_pairs_of(a);
+    drop_pairs_of(b);
+    for (int x : lab[a]) owners[x].erase(std::remove(owners[x].begin(), owners[x].end(), a), owners[x].end());
+    for (int x : lab[b]) owners[x].erase(std::remove(owners[x].begin(), owners[x].end(), b), owners[x].end());
+    lab.erase(a);
+    lab.erase(b);
+    lsz.erase(a);
+    lsz.erase(b);
+    const int c = next++;
+    lab[c] = nl;
+    double s = 0;
+    for (int x : nl) {
+      s += lg[x];
+      owners[x].push_back(c);
+    }
+    lsz[c] = s;
+    for (int x : nl)
+      if (owners[x].size() == 2) add_pair(owners[x][0], owners[x][1]);
+  }
+  return tr;
+}
+
+}  // namespace
+
+std::vector<std::pair<int, int>> plan_order(const std::vector<std::vector<int>>& labels, const std::vector<double>& lg,
+                                            uint64_t seed, int trials) {
+  const int n = static_cast<int>(labels.size());
+  Trial best;
+  bool have = false;
+  for (int t = 0; t < std::max(1, trials); ++t) {
+    double alpha = 0, temp = 0;
+    if (t > 0) {
+      alpha = unit(hash3(seed, 99, static_cast<uint64_t>(t)));
+      temp = 0.5 * unit(hash3(seed, 98, static_cast<uint64_t>(t)));
+    }
+    Trial tr = greedy(labels, lg, n, seed, alpha, temp, hash3(seed, 97, static_cast<uint64_t>(t)));
+    if (!have || std::make_pair(tr.peak, tr.flops) < std::make_pair(best.peak, best.flops)) {
+      best = std::move(tr);
+      have = true;
+    }
+  }
+  return best.order;
+}
+
+}  // namespace qtnhb

@@ -56,53 +56,6 @@ class Network:
 
     # -- planning (host only) ------------------------------------------------------------
     @staticmethod
-    def _greedy(labels: Dict[int, List[str]], dims: Dict[str, int], seed: int, alpha: float, temp: float,
-                rng) -> List[Tuple[int, int]]:
-        """One greedy pass: contract the connected pair minimising
-        log2|result| - alpha (log2|a| + log2|b|) (+ Gaussian noise of width temp),
-        ties broken by hash_counter(seed, a, b)."""
-        import math
-
-        labels = {k: list(v) for k, v in labels.items()}
-        lsz = {k: sum(math.log2(dims[x]) for x in v) for k, v in labels.items()}
-        owners: Dict[str, List[int]] = {}
-        for t, ls in labels.items():
-            for lab in ls:
-                owners.setdefault(lab, []).append(t)
-        nxt = max(labels) + 1 if labels else 0
-        order = []
-        while len(labels) > 1:
-            pairs = {tuple(sorted(ts)) for ts in owners.values() if len(ts) == 2}
-            if not pairs:  # disconnected pieces: outer product of the two smallest
-                ids = sorted(labels, key=lambda t: (lsz[t], t))
-                pairs = {(ids[0], ids[1])}
-            best = None
-            for a, b in pairs:
-                shared = set(labels[a]) & set(labels[b])
-                r = lsz[a] + lsz[b] - 2 * sum(math.log2(dims[x]) for x in shared)
-                key = r - alpha * (lsz[a] + lsz[b])
-                if temp > 0:
-                    key += rng.gauss(0.0, temp)
-                key = (key, circuits.hash_counter(seed, a, b))
-                if best is None or key < best[0]:
-                    best = (key, a, b)
-            _, a, b = best
-            order.append((a, b))
-            shared = set(labels[a]) & set(labels[b])
-            new = [x for x in labels[a] if x not in shared] + [x for x in labels[b] if x not in shared]
-            for lab in labels[a] + labels[b]:
-                owners[lab] = [t for t in owners.get(lab, []) if t not in (a, b)]
-                if not owners[lab]:
-                    del owners[lab]
-            del labels[a], labels[b], lsz[a], lsz[b]
-            labels[nxt] = new
-            lsz[nxt] = sum(math.log2(dims[x]) for x in new)
-            for lab in new:
-                owners.setdefault(lab, []).append(nxt)
-            nxt += 1
-        return order
-
-    @staticmethod
     def cost(labels: Dict[int, List[str]], dims: Dict[str, int], order) -> Tuple[float, int, float]:
         """(sum of 8MNK flops, largest intermediate, sum of 16(|A|+|B|+|C|) bytes)."""
         import math
@@ -123,28 +76,32 @@ class Network:
         return fl, big, by
 
     @staticmethod
-    def plan(labels: Dict[int, List[str]], dims: Dict[str, int], seed: int = 0, trials: int = 16,
+    def plan(labels: Dict[int, List[str]], dims: Dict[str, int], seed: int = 0, trials: int = 64,
              keep_open: Sequence[str] = ()) -> List[Tuple[int, int]]:
-        """Seeded greedy order. Trial 0 is the plain smallest-result greedy
-        (SURVEY.md 8(d)); further trials are seeded randomised greedy passes
-        (alpha, noise drawn from hash_counter(seed, 99, trial)); the order with the
+        """Seeded greedy contraction order, planned natively (csrc/plan.cpp via
+        qtnh_plan_order): trial 0 is the plain smallest-result greedy (SURVEY.md
+        8(d)), further trials seeded randomised greedy passes; the order with the
         smallest largest intermediate, then fewest flops, wins. Deterministic per
-        seed; the result of step s gets id max(ids) + 1 + s."""
-        import random
+        seed; tensor ids must be 0..n-1 and the result of step s gets id n + s."""
+        import math
 
-        best = None
-        for t in range(max(1, trials)):
-            if t == 0:
-                alpha, temp, rng = 0.0, 0.0, None
-            else:
-                rng = random.Random(circuits.hash_counter(seed, 99, t))
-                alpha, temp = rng.random(), 0.5 * rng.random()
-            order = Network._greedy(labels, dims, seed, alpha, temp, rng)
-            fl, big, _ = Network.cost(labels, dims, order)
-            key = (big, fl)
-            if best is None or key < best[0]:
-                best = (key, order)
-        return best[1]
+        from ._lib import i32_array
+
+        ids = sorted(labels)
+        if ids != list(range(len(ids))):
+            raise qtnh.InvalidArgument("plan needs tensor ids 0..n-1")
+        names = sorted({x for v in labels.values() for x in v})
+        lid = {x: i for i, x in enumerate(names)}
+        offs, flat = [0], []
+        for t in ids:
+            flat.extend(lid[x] for x in labels[t])
+            offs.append(len(flat))
+        lg = np.array([math.log2(dims[x]) for x in names], dtype=np.float64)
+        out = np.zeros(2 * max(1, len(ids) - 1), dtype=np.int32)
+        qtnh.check(qtnh.lib.qtnh_plan_order(len(ids), i32_array(offs), i32_array(flat or [0]), len(names),
+                                            lg.ctypes.data, int(seed) & (2**64 - 1), int(trials),
+                                            out.ctypes.data_as(qtnh.C.POINTER(qtnh.C.c_int))))
+        return [(int(out[2 * s]), int(out[2 * s + 1])) for s in range(len(ids) - 1)]
 
     # ---- multi-rank placement ---------------------------------------------------------
     def _replicate(self, t: Tensor) -> Tensor:
@@ -266,33 +223,43 @@ def output_bits(n: int, n_open: int, seed: int):
     return open_q, fixed
 
 
-def build_rcs_network(rank: qtnh.Rank, rows: int, cols: int, depth: int, seed: int, n_open: int = 6,
-                      shard_flops: float = 1e11):
+def rcs_network_spec(rows: int, cols: int, depth: int, seed: int, n_open: int = 6):
+    """Host description of config 3's network: [(array, labels)] in insertion order,
+    the open labels (ascending qubit), the open qubits and the fixed output bits."""
     from .mps import SINGLE_QUBIT
 
     n = rows * cols
-    net = Network(rank, shard_flops)
+    items = []
     wire = [f"q{q}.0" for q in range(n)]
     ver = [0] * n
     for q in range(n):
-        net.add(np.array([1, 0], complex), [wire[q]])
+        items.append((np.array([1, 0], complex), [wire[q]]))
     for kind, qs, g in rcs_grid_circuit(rows, cols, depth, seed):
         if kind == "1q":
             q = qs[0]
             ver[q] += 1
             new = f"q{q}.{ver[q]}"
-            net.add(SINGLE_QUBIT[g], [new, wire[q]])  # (out, in)
+            items.append((SINGLE_QUBIT[g], [new, wire[q]]))  # (out, in)
             wire[q] = new
         else:
             a, b = qs
             ver[a] += 1
             ver[b] += 1
             na, nb = f"q{a}.{ver[a]}", f"q{b}.{ver[b]}"
-            net.add(circuits.FSIM.reshape(2, 2, 2, 2), [na, nb, wire[a], wire[b]])
+            items.append((circuits.FSIM.reshape(2, 2, 2, 2), [na, nb, wire[a], wire[b]]))
             wire[a], wire[b] = na, nb
     open_q, fixed = output_bits(n, n_open, seed)
     for q, bit in fixed.items():
         v = np.zeros(2, complex)
         v[bit] = 1
-        net.add(v, [wire[q]])
-    return net, [wire[q] for q in open_q], open_q, fixed
+        items.append((v, [wire[q]]))
+    return items, [wire[q] for q in open_q], open_q, fixed
+
+
+def build_rcs_network(rank: qtnh.Rank, rows: int, cols: int, depth: int, seed: int, n_open: int = 6,
+                      shard_flops: float = 1e11):
+    net = Network(rank, shard_flops)
+    items, open_labels, open_q, fixed = rcs_network_spec(rows, cols, depth, seed, n_open)
+    for arr, labs in items:
+        net.add(arr, labs)
+    return net, open_labels, open_q, fixed

@@ -26,7 +26,7 @@ def main():
         for rep in range(2):
             net, *_ = network.build_rcs_network(rk, rows, cols, depth, seed, n_open)
             if order is None:
-                order = network.Network.plan(net.labels, net.dims, seed, trials=24)
+                order = network.Network.plan(net.labels, net.dims, seed, trials=64)
             nxt = max(net.tensors) + 1
             recs = []
             for s, (a, b) in enumerate(order):

@@ -22,7 +22,7 @@ def main():
     ap.add_argument("--open", type=int, default=6)
     ap.add_argument("--seed", type=int, default=2025)
     ap.add_argument("--no-statevector", action="store_true")
-    ap.add_argument("--trials", type=int, default=24)
+    ap.add_argument("--trials", type=int, default=64)
     ap.add_argument("--world", type=int, default=1,
                     help="ranks (thread per rank over the visible GPUs): tensors replicated, contractions of "
                          ">= --shard-flops M-sharded")
