@@ -397,10 +397,12 @@ std::shared_ptr<Plan> build_plan(const std::vector<D>& ds, int dev, cudaStream_t
   if (direct) {
     QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tiled<true, true>, kThreads, 0));
   } else {
-    if (p->smem > 48 * 1024) {
-      QTNH_CUDA(cudaFuncSetAttribute(k_tiled<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem));
-      QTNH_CUDA(cudaFuncSetAttribute(k_tiled<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem));
-    }
+    // the attribute is per kernel, not per plan: always allow the largest tile
+    // (kMaxTile elements), or a later small-tile plan would shrink the limit under
+    // an earlier large-tile plan
+    const int max_smem = static_cast<int>(kMaxTile * sizeof(double2));
+    QTNH_CUDA(cudaFuncSetAttribute(k_tiled<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+    QTNH_CUDA(cudaFuncSetAttribute(k_tiled<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
     QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tiled<true, false>, kThreads, p->smem));
   }
   Dim g = static_cast<Dim>(sm_count(dev)) * std::max(1, per_sm);

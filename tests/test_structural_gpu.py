@@ -425,3 +425,31 @@ def test_diagonal_tensor(dims, split, world):
 
     for o in [o for o in World(world).run(body) if o is not None]:
         assert np.array_equal(o, want)
+
+
+def test_many_plan_shapes_interleaved():
+    """Plans of different tile sizes interleaved (the copy kernel's dynamic shared
+    memory limit is per kernel: a small-tile plan must not shrink it under a
+    large-tile one)."""
+    rng = np.random.default_rng(3)
+    cases = []
+    for _ in range(14):
+        r = int(rng.integers(3, 8))
+        dims = [int(x) for x in rng.choice([2, 3, 4, 5, 6, 8, 16, 64], size=r)]
+        while int(np.prod(dims)) > 2**21:
+            dims[int(np.argmax(dims))] //= 2
+        cases.append((dims, [int(x) for x in rng.permutation(r)]))
+    cases = cases + cases[::-1]
+
+    def body(rk):
+        outs = []
+        for dims, perm in cases:
+            g = circuits.counter_state(len(dims), int(np.prod(dims)))
+            t = Tensor.from_global(rk, IndexTuple(dims, 0), None, g)
+            outs.append(ops.permute(t, perm, 0).to_global_vector())
+        return outs
+
+    outs = run_collect(World(1), body)
+    for (dims, perm), got in zip(cases, outs):
+        g = circuits.counter_state(len(dims), int(np.prod(dims)))
+        assert np.array_equal(bits(got), bits(P.permute(dims, g, perm)))
