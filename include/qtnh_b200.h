@@ -219,6 +219,14 @@ int qtnh_plan_order(int n_tensors, const int* label_offsets, const int* labels, 
 int qtnh_contract(qtnh_tensor_t a, qtnh_tensor_t b, int n_pairs, const int* a_pos,
                   const int* b_pos, qtnh_tensor_t* out);
 
+/* A whole contraction order in one call (network::contract_order):
+ * ids 0..n_inputs-1 are `inputs`, step s contracts step_ab[2s] with step_ab[2s+1]
+ * over step_npairs[s] position pairs (consecutive in a_pos / b_pos) and its result
+ * gets id n_inputs + s; intermediates are released as soon as they are consumed.
+ * `out` receives the last result (the inputs' handles stay valid). */
+int qtnh_contract_chain(int n_inputs, const qtnh_tensor_t* inputs, int n_steps, const int* step_ab,
+                        const int* step_npairs, const int* a_pos, const int* b_pos, qtnh_tensor_t* out);
+
 /* Contraction with both operands and the result in HOST memory (the reference's
  * contract takes host-resident std::vector tensors): A is streamed through the GPU
  * in chunks of its leading open indices; H2D of chunk i+1, the GEMM of chunk i and

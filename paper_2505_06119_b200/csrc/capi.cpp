@@ -705,6 +705,36 @@ int qtnh_scale(qtnh_tensor_t t, double re, double im, qtnh_tensor_t* out) {
   });
 }
 
+int qtnh_contract_chain(int n_inputs, const qtnh_tensor_t* inputs, int n_steps, const int* step_ab,
+                        const int* step_npairs, const int* a_pos, const int* b_pos, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    if (n_inputs < 1 || n_steps < 0) throw_invalid("invalid chain sizes");
+    need(inputs, "inputs");
+    if (n_steps) {
+      need(step_ab, "step_ab");
+      need(step_npairs, "step_npairs");
+    }
+    std::vector<TP> live(n_inputs + n_steps);
+    for (int i = 0; i < n_inputs; ++i) live[i] = impl_of(inputs[i]);
+    size_t off = 0;
+    int last = n_inputs - 1;
+    for (int s = 0; s < n_steps; ++s) {
+      const int a = step_ab[2 * s], b = step_ab[2 * s + 1], k = step_npairs[s];
+      if (a < 0 || b < 0 || a >= n_inputs + s || b >= n_inputs + s || a == b || !live[a] || !live[b])
+        throw_invalid("chain step " + std::to_string(s) + " references a consumed or unknown tensor");
+      if (k && (!a_pos || !b_pos)) throw_invalid("missing contracted positions");
+      live[n_inputs + s] = op_contract(live[a], live[b], std::vector<int>(a_pos + off, a_pos + off + k),
+                                       std::vector<int>(b_pos + off, b_pos + off + k));
+      off += static_cast<size_t>(k);
+      live[a].reset();  // intermediates die as soon as they are consumed
+      live[b].reset();
+      last = n_inputs + s;
+    }
+    *out = wrap(live[last]);
+  });
+}
+
 int qtnh_contract(qtnh_tensor_t a, qtnh_tensor_t b, int n_pairs, const int* a_pos, const int* b_pos,
                   qtnh_tensor_t* out) {
   return guard([&] {

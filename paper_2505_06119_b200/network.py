@@ -173,6 +173,42 @@ class Network:
         self.labels[i] = new
         return i
 
+    def contract_order_native(self, order: Sequence[Tuple[int, int]]) -> int:
+        """The whole order in one native call (qtnh_contract_chain): positions are
+        derived on the host from the labels, the C++ runtime runs the contractions
+        back to back (single-rank networks; multi-rank ones use contract_order)."""
+        from ._lib import i32_array
+
+        ids = sorted(self.tensors)
+        if ids != list(range(len(ids))) or self.world > 1:
+            raise qtnh.InvalidArgument("contract_order_native needs ids 0..n-1 on a single rank")
+        L = {k: list(v) for k, v in self.labels.items()}
+        n = len(ids)
+        ab, npairs, ap, bp = [], [], [], []
+        for s, (a, b) in enumerate(order):
+            if a not in L or b not in L:
+                raise qtnh.InvalidArgument("order references consumed ids")  # SPEC.md:397
+            la, lb = L.pop(a), L.pop(b)
+            sh = [x for x in la if x in lb]
+            ab += [a, b]
+            npairs.append(len(sh))
+            ap += [la.index(x) for x in sh]
+            bp += [lb.index(x) for x in sh]
+            L[n + s] = [x for x in la if x not in sh] + [x for x in lb if x not in sh]
+        handles = (qtnh.C.c_void_p * n)(*[self.tensors[i]._h for i in ids])
+        h = qtnh.C.c_void_p()
+        qtnh.check(qtnh.lib.qtnh_contract_chain(n, handles, len(order), i32_array(ab or [0]),
+                                                i32_array(npairs or [0]), i32_array(ap or [0]), i32_array(bp or [0]),
+                                                qtnh.C.byref(h)))
+        last = n + len(order) - 1
+        result = Tensor(self.rank, h)
+        for i in ids:
+            self.tensors.pop(i).free()
+        self.labels = {last: L[last]}
+        self.tensors = {last: result}
+        self._next = last + 1
+        return last
+
     def contract_order(self, order: Sequence[Tuple[int, int]]) -> int:
         nxt = max(self.tensors) + 1
         last = None

@@ -113,3 +113,23 @@ def test_grid_patterns():
     h = sorted(network.grid_pairs("A", 3, 3) + network.grid_pairs("B", 3, 3))
     assert len(h) == 6 and len(set(h)) == 6
     assert all(b - a == 3 for a, b in network.grid_pairs("C", 3, 3))
+
+
+@pytest.mark.parametrize("rows,cols,depth,n_open", [(3, 3, 6, 3), (3, 4, 5, 4)])
+def test_native_chain_executor(rows, cols, depth, n_open):
+    """The whole order through one qtnh_contract_chain call equals the statevector."""
+    seed = 7
+
+    def body(rk):
+        net, open_labels, open_q, fixed = network.build_rcs_network(rk, rows, cols, depth, seed, n_open)
+        order = network.Network.plan(net.labels, net.dims, seed)
+        last = net.contract_order_native(order)
+        res_labels = net.labels[last]
+        out = net.tensors[last].to_global_vector().reshape([2] * len(res_labels))
+        out = np.transpose(out, [res_labels.index(l) for l in open_labels]).reshape(-1)
+        net.tensors[last].free()
+        return out, open_q, fixed
+
+    got, open_q, fixed = World(1).run(body)[0]
+    want = statevector_amplitudes(rows, cols, depth, seed, open_q, fixed, oracle.port())
+    assert rel_l2(got, want) < TOL

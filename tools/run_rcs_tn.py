@@ -84,10 +84,11 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
         e0.record()
-        last = net.contract_order(order)
+        last = net.contract_order_native(order) if args.world == 1 else net.contract_order(order)
         e1.record()
         e1.synchronize()
         out["world"] = args.world
+        out["executor"] = "native chain (qtnh_contract_chain)" if args.world == 1 else "python loop"
         out["sharded_contractions"] = net.n_sharded
         out["contract_s_wall"] = time.perf_counter() - t0
         out["contract_s_device"] = e0.elapsed_time(e1) / 1e3
