@@ -285,13 +285,13 @@ __global__ void __launch_bounds__(B * 8) k_svd_gram_mma_t(const double2* __restr
   }
 }
 
-// In-place update on DMMA: Y (P2 x 48 cols) = W^H (P2 x P2) X; dynamic smem.
-template <int B>
+// In-place update on DMMA: Y (P2 x UC cols) = W^H (P2 x P2) X; dynamic smem.
+template <int B, int UC>
 __global__ void __launch_bounds__(B * 8) k_svd_update_mma_t(double2* __restrict__ wk, const double2* __restrict__ wh,
                                                             const int* __restrict__ flags,
                                                             const int* __restrict__ tab, int round, int npairs,
                                                             int64_t rp, int64_t L, int64_t qw) {
-  constexpr int P2 = 2 * B, T = B * 8, UC = 48, NT = UC / 8, PW = P2 + 4, PX = UC + 2;
+  constexpr int P2 = 2 * B, T = B * 8, NT = UC / 8, PW = P2 + 4, PX = UC + 2;
   const int pair = blockIdx.y, mat = blockIdx.z, tid = threadIdx.x;
   const int64_t fidx = static_cast<int64_t>(mat) * npairs + pair;
   if (!flags[fidx]) return;
@@ -598,10 +598,17 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
                                                                    static_cast<double*>(floor_abs.ptr), floor_rel());
   QTNH_LAUNCH_CHECK();
   const size_t eig_smem = static_cast<size_t>(2) * P2 * (P2 + 1) * 16;
-  const size_t upd_smem = static_cast<size_t>(P2) * ((P2 + 4) + 2 * (48 + 2)) * 16;
+  static const int uc = [] {
+    const char* e = std::getenv("QTNH_SVD_UC");
+    int v = e ? std::atoi(e) : 48;
+    return v == 32 || v == 64 ? v : 48;
+  }();
+  const size_t upd_smem = static_cast<size_t>(P2) * ((P2 + 4) + 2 * (uc + 2)) * 16;
   const size_t gram_smem = static_cast<size_t>(2) * P2 * ((B >= 32 ? 32 : 64) + 4) * 16;
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_eigen_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_smem));
-  QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
+  QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
+  QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
+  QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_gram_mma_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem));
   // The batch runs as two independent halves on two streams when it has >= 2
   // matrices: the latency-bound eigen step of one half overlaps the other half's
@@ -631,7 +638,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   const int max_sweeps = 40;
   const Dim gmax = (batch + ngroups - 1) / ngroups;
   const unsigned ctiles = static_cast<unsigned>(
-      std::min<Dim>((W + 47) / 48, std::max<Dim>(1, (B == 16 ? 8 : 4) * sms() / (npairs * gmax))));
+      std::min<Dim>((W + uc - 1) / uc, std::max<Dim>(1, (B == 16 ? 8 : 4) * sms() / (npairs * gmax))));
   auto cleanup = [&] {
     for (int g = 0; g < ngroups; ++g) {
       if (ngroups > 1) {
@@ -664,8 +671,15 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
               partg, whg, flg, static_cast<double*>(offm.ptr) + G.base, npairs, splits, tol, inner_sweeps(),
               static_cast<const double*>(floor_abs.ptr) + G.base);
           QTNH_LAUNCH_CHECK();
-          k_svd_update_mma_t<B><<<dim3(ctiles, npairs, cnt), B * 8, upd_smem, G.s>>>(
-              wkg, whg, flg, static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
+          if (uc == 32)
+            k_svd_update_mma_t<B, 32><<<dim3(ctiles, npairs, cnt), B * 8, upd_smem, G.s>>>(
+                wkg, whg, flg, static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
+          else if (uc == 64)
+            k_svd_update_mma_t<B, 64><<<dim3(ctiles, npairs, cnt), B * 8, upd_smem, G.s>>>(
+                wkg, whg, flg, static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
+          else
+            k_svd_update_mma_t<B, 48><<<dim3(ctiles, npairs, cnt), B * 8, upd_smem, G.s>>>(
+                wkg, whg, flg, static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
           QTNH_LAUNCH_CHECK();
         }
       for (auto& G : grp)
