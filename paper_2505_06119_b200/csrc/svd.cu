@@ -162,16 +162,19 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
           p = q;
           q = tt;
         }
+        // one reciprocal square root instead of hypot and three divisions: these
+        // 16 threads are the critical path of every step (the rest wait at the barrier)
         double a = G[p * LD + p].x, b = G[q * LD + q].x;
         double2 x = G[p * LD + q];
-        double ax = hypot(x.x, x.y);
+        const double r2 = fma(x.x, x.x, x.y * x.y);
         double c = 1.0, sn = 0.0;
         double2 ph = make_double2(1.0, 0.0);
-        if (ax > 1e-300 && !(ax <= 1e-17 * sqrt(fabs(a * b)))) {
-          ph = make_double2(x.x / ax, -x.y / ax);
-          double tau = (b - a) / (2.0 * ax);
-          double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-          c = 1.0 / sqrt(1.0 + t * t);
+        if (r2 > 1e-600 && !(r2 <= 1e-34 * fabs(a * b))) {
+          const double inv_ax = rsqrt(r2);
+          ph = make_double2(x.x * inv_ax, -x.y * inv_ax);
+          const double tau = 0.5 * (b - a) * inv_ax;
+          const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
+          c = rsqrt(fma(t, t, 1.0));
           sn = t * c;
         }
         rot_c[tid] = c;
