@@ -96,6 +96,83 @@ __global__ void __launch_bounds__(256) k_gate_dense(double2* __restrict__ psi, i
   }
 }
 
+// 2x2 gate on the innermost index (the pair is two adjacent amplitudes): one
+// 32-byte vector load / store per pair instead of two strided 16-byte accesses.
+__device__ __forceinline__ double4 ld256(const double4* p) {
+  double4 v;
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st256(double4* p, const double4& v) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
+}
+
+__global__ void __launch_bounds__(256) k_gate_inner2(double2* __restrict__ psi, int64_t n_pairs,
+                                                     const __grid_constant__ GateArgs a) {
+  const double2 g00 = a.g[0], g01 = a.g[1], g10 = a.g[2], g11 = a.g[3];
+  double4* v4 = reinterpret_cast<double4*>(psi);
+  const int64_t S = (int64_t)gridDim.x * blockDim.x;
+  const int64_t end = n_pairs + a.f0;
+  for (int64_t f0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + a.f0; f0 < end; f0 += 4 * S) {
+    double4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (f0 + u * S < end) v[u] = ld256(v4 + f0 + u * S);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (f0 + u * S >= end) continue;
+      const double xr = v[u].x, xi = v[u].y, yr = v[u].z, yi = v[u].w;
+      double4 o;
+      o.x = fma(g00.x, xr, fma(-g00.y, xi, fma(g01.x, yr, -g01.y * yi)));
+      o.y = fma(g00.x, xi, fma(g00.y, xr, fma(g01.x, yi, g01.y * yr)));
+      o.z = fma(g10.x, xr, fma(-g10.y, xi, fma(g11.x, yr, -g11.y * yi)));
+      o.w = fma(g10.x, xi, fma(g10.y, xr, fma(g11.x, yi, g11.y * yr)));
+      st256(v4 + f0 + u * S, o);
+    }
+  }
+}
+
+// Same gate, two neighbouring fibers per thread when the innermost non-target
+// index is contiguous (stride 1, even extent): fibers 2p and 2p+1 sit next to
+// each other at every target offset, so each pair of amplitudes moves as one
+// 32-byte access (LDG/STG.256) and a warp touches 1 KiB contiguous per offset.
+template <int D, bool POW2>
+__global__ void __launch_bounds__(256) k_gate_dense_v2(double2* __restrict__ psi, int64_t n_pairs,
+                                                       const __grid_constant__ GateArgs a) {
+  constexpr int F = D <= 2 ? 4 : 2;
+  const int64_t S = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p0 < n_pairs; p0 += F * S) {
+    int64_t base[F];
+    double4 x[F][D];
+#pragma unroll
+    for (int u = 0; u < F; ++u) {
+      const int64_t q = p0 + u * S;
+      base[u] = q < n_pairs ? fiber_base<POW2>(2 * q + a.f0, a) : -1;
+      if (base[u] >= 0) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) x[u][d] = ld256(reinterpret_cast<const double4*>(psi + base[u] + a.off[d]));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < F; ++u) {
+      if (base[u] < 0) continue;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        double r0 = 0.0, i0 = 0.0, r1 = 0.0, i1 = 0.0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const double2 g = a.g[i * D + d];
+          r0 = fma(g.x, x[u][d].x, fma(-g.y, x[u][d].y, r0));
+          i0 = fma(g.x, x[u][d].y, fma(g.y, x[u][d].x, i0));
+          r1 = fma(g.x, x[u][d].z, fma(-g.y, x[u][d].w, r1));
+          i1 = fma(g.x, x[u][d].w, fma(g.y, x[u][d].z, i1));
+        }
+        st256(reinterpret_cast<double4*>(psi + base[u] + a.off[i]), make_double4(r0, i0, r1, i1));
+      }
+    }
+  }
+}
+
 // Generic D (non power of two, or > kMaxD handled by host splitting): loops.
 template <bool POW2>
 __global__ void __launch_bounds__(256) k_gate_generic(double2* __restrict__ psi, int64_t n_fibers,
@@ -231,6 +308,32 @@ void gate_strided(void* data, const std::vector<Dim>& dims, const std::vector<Di
   for (Dim j = 0; j < D; ++j) a.off[j] = offset_of(j);
   for (Dim j = 0; j < D * D; ++j) a.g[j] = make_double2(gh[2 * j], gh[2 * j + 1]);
   auto* p = static_cast<double2*>(data);
+  // innermost-index 2x2 gate on a contiguous (dense row-major) buffer: vector path
+  if (D == 2 && a.nseg == 1 && a.seg_stride[0] == 2 && a.off[0] == 0 && a.off[1] == 1 &&
+      (reinterpret_cast<uintptr_t>(data) & 31) == 0) {
+    k_gate_inner2<<<grid, 256, 0, st>>>(p, n_fibers, a);
+    QTNH_LAUNCH_CHECK();
+    return;
+  }
+  // two neighbouring fibers per thread (see k_gate_dense_v2)
+  if ((D == 2 || D == 4) && a.nseg >= 1 && a.seg_stride[a.nseg - 1] == 1 && (a.seg_size[a.nseg - 1] & 1) == 0 &&
+      (n_fibers & 1) == 0 && (a.f0 & 1) == 0 && (reinterpret_cast<uintptr_t>(data) & 31) == 0) {
+    bool even = true;
+    for (int d = 0; d < D; ++d) even = even && (a.off[d] & 1) == 0;
+    if (even) {
+      const int64_t n_pairs = n_fibers / 2;
+      const int g2 = grid_for(n_pairs);
+      if (D == 2) {
+        if (pow2) k_gate_dense_v2<2, true><<<g2, 256, 0, st>>>(p, n_pairs, a);
+        else k_gate_dense_v2<2, false><<<g2, 256, 0, st>>>(p, n_pairs, a);
+      } else {
+        if (pow2) k_gate_dense_v2<4, true><<<g2, 256, 0, st>>>(p, n_pairs, a);
+        else k_gate_dense_v2<4, false><<<g2, 256, 0, st>>>(p, n_pairs, a);
+      }
+      QTNH_LAUNCH_CHECK();
+      return;
+    }
+  }
 #define QTNH_GATE_CASE(DD)                                                          \
   case DD:                                                                          \
     if (pow2) k_gate_dense<DD, true><<<grid, 256, 0, st>>>(p, n_fibers, a);         \
