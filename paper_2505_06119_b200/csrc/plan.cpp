@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <map>
 #include <set>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -142,21 +143,34 @@ Trial greedy(const std::vector<std::vector<int>>& labels0, const std::vector<dou
 std::vector<std::pair<int, int>> plan_order(const std::vector<std::vector<int>>& labels, const std::vector<double>& lg,
                                             uint64_t seed, int trials) {
   const int n = static_cast<int>(labels.size());
-  Trial best;
-  bool have = false;
-  for (int t = 0; t < std::max(1, trials); ++t) {
-    double alpha = 0, temp = 0;
-    if (t > 0) {
-      alpha = unit(hash3(seed, 99, static_cast<uint64_t>(t)));
-      temp = 0.5 * unit(hash3(seed, 98, static_cast<uint64_t>(t)));
+  const int nt = std::max(1, trials);
+  // Trials are independent: run them on the host cores (trial t on worker
+  // t mod W). The winner is the smallest (peak, flops, t), so the result does
+  // not depend on the worker count.
+  std::vector<Trial> res(nt);
+  auto run = [&](int w, int W) {
+    for (int t = w; t < nt; t += W) {
+      double alpha = 0, temp = 0;
+      if (t > 0) {
+        alpha = unit(hash3(seed, 99, static_cast<uint64_t>(t)));
+        temp = 0.5 * unit(hash3(seed, 98, static_cast<uint64_t>(t)));
+      }
+      res[t] = greedy(labels, lg, n, seed, alpha, temp, hash3(seed, 97, static_cast<uint64_t>(t)));
     }
-    Trial tr = greedy(labels, lg, n, seed, alpha, temp, hash3(seed, 97, static_cast<uint64_t>(t)));
-    if (!have || std::make_pair(tr.peak, tr.flops) < std::make_pair(best.peak, best.flops)) {
-      best = std::move(tr);
-      have = true;
-    }
+  };
+  const int W = std::min<int>(nt, std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+  if (W <= 1) {
+    run(0, 1);
+  } else {
+    std::vector<std::thread> th;
+    for (int w = 1; w < W; ++w) th.emplace_back(run, w, W);
+    run(0, W);
+    for (auto& x : th) x.join();
   }
-  return best.order;
+  int best = 0;
+  for (int t = 1; t < nt; ++t)
+    if (std::make_pair(res[t].peak, res[t].flops) < std::make_pair(res[best].peak, res[best].flops)) best = t;
+  return res[best].order;
 }
 
 }  // namespace qtnhb
