@@ -11,12 +11,16 @@ replayed by the reference oracle for parity.
 """
 from __future__ import annotations
 
+import math
+import os
 from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
 from . import circuits, qtnh
 from .qtnh import IndexTuple, Tensor
+
+_BIG_FIRST = os.environ.get("QTNH_NET_BIG_FIRST", "1") != "0"
 
 
 class Network:
@@ -131,6 +135,15 @@ class Network:
         one.free()
         return out, [labels[i] for i in perm]
 
+    def _big_first(self, la: List[str], lb: List[str]) -> bool:
+        """Operand order of one step: the larger tensor goes first. contract()
+        reads its first operand through the gather GEMM (layout permutation fused
+        into the operand loads) and permutes the second into a dense K x N panel,
+        so the big one is never copied; the result labels follow the order."""
+        if not _BIG_FIRST:
+            return False
+        return sum(math.log2(self.dims[x]) for x in lb) > sum(math.log2(self.dims[x]) for x in la)
+
     def contract_pair(self, a: int, b: int, new_id: Optional[int] = None) -> int:
         la, lb = self.labels[a], self.labels[b]
         ta, tb = self.tensors[a], self.tensors[b]
@@ -157,6 +170,8 @@ class Network:
                         temps.append(s_t)
             if ta.shape().split > 0:
                 self.n_sharded += 1
+        elif self._big_first(la, lb):
+            la, lb, ta, tb = lb, la, tb, ta
         shared = [x for x in la if x in lb]
         apos = [la.index(x) for x in shared]
         bpos = [lb.index(x) for x in shared]
@@ -189,6 +204,8 @@ class Network:
             if a not in L or b not in L:
                 raise qtnh.InvalidArgument("order references consumed ids")
             la, lb = L.pop(a), L.pop(b)
+            if self._big_first(la, lb):
+                a, b, la, lb = b, a, lb, la
             sh = [x for x in la if x in lb]
             ab += [a, b]
             npairs.append(len(sh))
