@@ -22,6 +22,40 @@ __global__ void dmma_loop(double* out, double seed){
   double s=0; for(int j=0;j<8;j++) s+=acc[j][0]+acc[j][1];
   if(s==1.2345) out[0]=s;
 }
+__global__ void dmma16_loop(double* out, double seed, int shape, int ITER){
+  double a[8], b[4];
+  #pragma unroll
+  for(int j=0;j<8;j++) a[j]=seed+threadIdx.x+j;
+  #pragma unroll
+  for(int j=0;j<4;j++) b[j]=seed*2+j;
+  double acc[8][4];
+  #pragma unroll
+  for(int j=0;j<8;j++){acc[j][0]=0;acc[j][1]=0;acc[j][2]=0;acc[j][3]=0;}
+  if(shape==4){
+    for(int i=0;i<ITER;i++){
+      #pragma unroll
+      for(int j=0;j<8;j++)
+        asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+          : "+d"(acc[j][0]),"+d"(acc[j][1]),"+d"(acc[j][2]),"+d"(acc[j][3]) : "d"(a[0]),"d"(a[1]),"d"(b[0]));
+    }
+  } else if(shape==8){
+    for(int i=0;i<ITER;i++){
+      #pragma unroll
+      for(int j=0;j<8;j++)
+        asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+          : "+d"(acc[j][0]),"+d"(acc[j][1]),"+d"(acc[j][2]),"+d"(acc[j][3]) : "d"(a[0]),"d"(a[1]),"d"(a[2]),"d"(a[3]),"d"(b[0]),"d"(b[1]));
+    }
+  } else {
+    for(int i=0;i<ITER;i++){
+      #pragma unroll
+      for(int j=0;j<8;j++)
+        asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};"
+          : "+d"(acc[j][0]),"+d"(acc[j][1]),"+d"(acc[j][2]),"+d"(acc[j][3]) : "d"(a[0]),"d"(a[1]),"d"(a[2]),"d"(a[3]),"d"(a[4]),"d"(a[5]),"d"(a[6]),"d"(a[7]),"d"(b[0]),"d"(b[1]),"d"(b[2]),"d"(b[3]));
+    }
+  }
+  double s=0; for(int j=0;j<8;j++) s+=acc[j][0]+acc[j][1]+acc[j][2]+acc[j][3];
+  if(s==1.2345) out[0]=s;
+}
 template<int ITER>
 __global__ void dfma_loop(double* out, double seed){
   double x[8]; double a=seed+threadIdx.x, b=1.0000001;
@@ -50,6 +84,14 @@ int main(){
     float ms; cudaEventElapsedTime(&ms,e0,e1);
     double flops=5.0*blocks*warps*(double)IT*8*(8*8*4*2);
     printf("DMMA m8n8k4: blocks=%d warps/blk=%d  %.2f TFLOP/s\n",blocks,warps,flops/ms/1e9);
+  }
+  for(int shape: {4,8,16}) for(int warps: {4,8}){
+    int blocks=p.multiProcessorCount*4; const int IT2=IT/ (shape/4);
+    dmma16_loop<<<blocks,warps*32>>>(out,1.0,shape,IT2); CK(cudaDeviceSynchronize());
+    cudaEventRecord(e0); for(int r=0;r<5;r++) dmma16_loop<<<blocks,warps*32>>>(out,1.0,shape,IT2); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+    float ms; cudaEventElapsedTime(&ms,e0,e1);
+    double flops=5.0*blocks*warps*(double)IT2*8*(16*8*shape*2);
+    printf("DMMA m16n8k%d: blocks=%d warps/blk=%d  %.2f TFLOP/s\n",shape,blocks,warps,flops/ms/1e9);
   }
   for(int thr: {256,512,1024}){
     int blocks=p.multiProcessorCount*2;
