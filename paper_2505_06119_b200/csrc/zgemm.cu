@@ -293,6 +293,172 @@ __global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm(const double2* __
   }
 }
 
+// Gauss kernel for tile-aligned problems (M % BM = N % BN = K % BK = 0, the
+// contraction shapes of every configuration): no bounds predicates, the
+// column-offset table form (CO: 0 = one shared-memory table, 1 = hi/lo split in
+// shared memory, 2 = global) a template parameter, and the next stage's cp.async
+// loads interleaved with the first k4 step's DMMAs (one piece per warp-tile row)
+// instead of issued as a block after them. In k_zgemm a warp's refill phase
+// (~400 address / branch instructions with shared- and global-load latencies)
+// stalls its DMMA stream, and with two warps per sub-partition both are often in
+// that phase at once: ncu showed the DMMA pipe 76 % busy although one warp with
+// two independent accumulators saturates it (tools/microbench/dmma_issue.cu).
+template <class G, int MODE, int CO>
+__global__ void __launch_bounds__(G::THREADS, G::MINB) k_zgemm_even(const double2* __restrict__ A,
+                                                                    const int64_t* __restrict__ rowoff,
+                                                                    const int64_t* __restrict__ coloff,
+                                                                    const double2* __restrict__ B,
+                                                                    double2* __restrict__ C, int64_t M,
+                                                                    int64_t N, int64_t K,
+                                                                    const int64_t* __restrict__ cohi, int co_sh,
+                                                                    const int64_t* __restrict__ rohi, int ro_sh) {
+  static_assert(G::GAUSS, "Gauss kernel");
+  constexpr int BM = G::BM, BN = G::BN, BK = G::BK, STAGES = G::STAGES, T = G::THREADS;
+  extern __shared__ __align__(16) double2 smem[];
+  double2* As = smem;
+  double2* Bs = smem + STAGES * G::A_ELEMS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int64_t* co_s = reinterpret_cast<int64_t*>(Bs + STAGES * G::B_ELEMS);
+  const int64_t co_lo_n = CO == 1 ? (int64_t(1) << co_sh) : K;
+  const int64_t co_mask = co_lo_n - 1;
+  if (MODE != 0 && CO != 2) {
+    for (int64_t i = tid; i < co_lo_n; i += T) co_s[i] = __ldg(coloff + i);
+    if (CO == 1)
+      for (int64_t i = tid; i < (K >> co_sh); i += T) co_s[co_lo_n + i] = __ldg(cohi + i);
+    __syncthreads();
+  }
+  auto col_off = [&](int64_t k) -> int64_t {
+    if (CO == 2) return __ldg(coloff + k);
+    if (CO == 1) return co_s[co_lo_n + (k >> co_sh)] + co_s[k & co_mask];
+    return co_s[k];
+  };
+  const int wm = warp / G::WARPS_N, wn = warp % G::WARPS_N;
+  const int64_t n_tiles_n = N / BN;
+  const int64_t bm = (blockIdx.x / n_tiles_n) * BM;
+  const int64_t bn = (blockIdx.x % n_tiles_n) * BN;
+  const int64_t n_kt = K / BK;
+
+  constexpr int LA = (BM * BK) / T, LB = (BN * BK) / T, LT = LA + LB;
+  constexpr bool kRowFixed = MODE == 1 && (T % BM) == 0;
+  constexpr bool kColFixed = MODE == 2 && (T % BK) == 0;
+  const double2* pa[kRowFixed ? 1 : LA];
+  int sa[LA], ka[LA];
+#pragma unroll
+  for (int u = 0; u < LA; ++u) {
+    const int e = tid + u * T;
+    const int m = MODE == 1 ? e % BM : e / BK;
+    const int k = MODE == 1 ? e / BM : e % BK;
+    ka[u] = k;
+    sa[u] = k * G::PA + m;
+    if (kRowFixed && u > 0) continue;
+    if (MODE == 0) {
+      pa[u] = A + (bm + m) * K + k;
+    } else {
+      const int64_t row = bm + m;
+      const int64_t off = rohi ? __ldg(rohi + (row >> ro_sh)) + __ldg(rowoff + (row & ((int64_t(1) << ro_sh) - 1)))
+                               : __ldg(rowoff + row);
+      pa[u] = A + off;
+    }
+  }
+  // B(k, n): thread t loads column bn + t % BN of rows (t + u T) / BN.
+  const double2* pb = B + bn + (tid % BN) + static_cast<int64_t>(tid / BN) * N;
+  const int sb0 = (tid / BN) * G::PB + (tid % BN);
+  constexpr int B_ROWS_PER_U = T / BN;  // rows between consecutive u (T % BN == 0 asserted below)
+  static_assert(T % BN == 0, "B loads: whole rows per pass");
+
+  auto load_one = [&](int q, int stage, int64_t k0, bool ok) {
+    if (q < LA) {
+      const int u = q;
+      const double2* src;
+      if (MODE == 0) src = pa[u] + k0;
+      else if (kRowFixed) src = pa[0] + col_off(k0 + ka[u]);
+      else if (kColFixed) src = pa[u] + col_off(k0 + ka[0]);
+      else src = pa[u] + col_off(k0 + ka[u]);
+      cp_async16(As + stage * G::A_ELEMS + sa[u], ok ? src : A, ok);
+    } else {
+      const int u = q - LA;
+      const double2* src = pb + (k0 + u * B_ROWS_PER_U) * N;
+      cp_async16(Bs + stage * G::B_ELEMS + sb0 + u * B_ROWS_PER_U * G::PB, ok ? src : B, ok);
+    }
+  };
+
+  constexpr int MI = G::MI, NJ = G::NJ;
+  double acc_re[MI][NJ][2], acc_im[MI][NJ][2], acc_s[MI][NJ][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) acc_re[i][j][h] = acc_im[i][j][h] = acc_s[i][j][h] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    const bool ok = s < n_kt;
+#pragma unroll
+    for (int q = 0; q < LT; ++q) load_one(q, s, ok ? int64_t(s) * BK : 0, ok);
+    cp_commit();
+  }
+
+  constexpr int PER = (LT + MI - 1) / MI;  // loads issued after each warp-tile row of k4 = 0
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int64_t kt = 0; kt < n_kt; ++kt) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    const int64_t nk = kt + STAGES - 1;
+    const bool refill = nk < n_kt;
+    const int nslot = static_cast<int>(nk % STAGES);
+    const int64_t nk0 = refill ? nk * BK : 0;  // past the end: keep table lookups in range
+    const double2* as = As + (kt % STAGES) * G::A_ELEMS + wm * G::WTM + fr;
+    const double2* bs = Bs + (kt % STAGES) * G::B_ELEMS + wn * G::WTN + fr;
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double a_re[MI], a_im[MI], a_s[MI], b_re[NJ], b_im[NJ], b_s[NJ];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const double2 v = bs[(k4 + fk) * G::PB + j * 8];
+        b_re[j] = v.x;
+        b_im[j] = v.y;
+        b_s[j] = v.x + v.y;
+      }
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        const double2 v = as[(k4 + fk) * G::PA + i * 8];
+        a_re[i] = v.x;
+        a_im[i] = v.y;
+        a_s[i] = v.x + v.y;
+      }
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          dmma(acc_re[i][j], a_re[i], b_re[j]);
+          dmma(acc_im[i][j], a_im[i], b_im[j]);
+          dmma(acc_s[i][j], a_s[i], b_s[j]);
+        }
+        if (k4 == 0) {
+#pragma unroll
+          for (int q = i * PER; q < (i + 1) * PER && q < LT; ++q) load_one(q, nslot, nk0, refill);
+        }
+      }
+    }
+    cp_commit();
+  }
+  cp_wait<0>();
+
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    const int64_t row = bm + wm * G::WTM + i * 8 + fr;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int64_t col = bn + wn * G::WTN + j * 8 + 2 * fk;
+      double2* dst = C + row * N + col;
+      const double r0 = acc_re[i][j][0], i0 = acc_im[i][j][0], r1 = acc_re[i][j][1], i1 = acc_im[i][j][1];
+      dst[0] = make_double2(r0 - i0, acc_s[i][j][0] - r0 - i0);
+      dst[1] = make_double2(r1 - i1, acc_s[i][j][1] - r1 - i1);
+    }
+  }
+}
+
 template <class G, int MODE>
 void launch_mode(const double2* a, const int64_t* ro, const int64_t* co, const double2* b, double2* c, Dim m,
                  Dim n, Dim k, cudaStream_t st, const int64_t* cohi = nullptr, int co_sh = 0,
@@ -311,8 +477,52 @@ void launch_mode(const double2* a, const int64_t* ro, const int64_t* co, const d
   QTNH_LAUNCH_CHECK();
 }
 
+bool even_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("QTNH_ZGEMM_EVEN");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <class G>
+bool even_shape(Dim m, Dim n, Dim k) {
+  return even_enabled() && m % G::BM == 0 && n % G::BN == 0 && k % G::BK == 0;
+}
+
+template <class G, int MODE, int CO>
+void launch_even_co(const double2* a, const int64_t* ro, const int64_t* co, const double2* b, double2* c, Dim m,
+                    Dim n, Dim k, cudaStream_t st, const int64_t* cohi, int co_sh, const int64_t* rohi, int ro_sh,
+                    size_t co_bytes) {
+  QTNH_CUDA(cudaFuncSetAttribute(k_zgemm_even<G, MODE, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(G::SMEM + kCoSmemMax * 8)));
+  const Dim tiles = (m / G::BM) * (n / G::BN);
+  if (tiles > 0x7fffffff) throw_invalid("zgemm problem too large for one launch");
+  k_zgemm_even<G, MODE, CO><<<static_cast<unsigned>(tiles), G::THREADS, G::SMEM + co_bytes, st>>>(
+      a, ro, co, b, c, m, n, k, cohi, co_sh, rohi, ro_sh);
+  QTNH_LAUNCH_CHECK();
+}
+
+template <class G, int MODE>
+void launch_even(const double2* a, const int64_t* ro, const int64_t* co, const double2* b, double2* c, Dim m, Dim n,
+                 Dim k, cudaStream_t st, const int64_t* cohi = nullptr, int co_sh = 0, const int64_t* rohi = nullptr,
+                 int ro_sh = 0) {
+  if (MODE == 0) return launch_even_co<G, 0, 2>(a, ro, co, b, c, m, n, k, st, cohi, co_sh, rohi, ro_sh, 0);
+  if (cohi) {
+    const size_t co_bytes = static_cast<size_t>((Dim(1) << co_sh) + (k >> co_sh)) * 8;
+    if (co_bytes > kCoSmemMax * 8) throw_invalid("column offset split exceeds its shared-memory budget");
+    return launch_even_co<G, MODE, 1>(a, ro, co, b, c, m, n, k, st, cohi, co_sh, rohi, ro_sh, co_bytes);
+  }
+  if (k <= kCoSmemMax)
+    return launch_even_co<G, MODE, 0>(a, ro, co, b, c, m, n, k, st, cohi, co_sh, rohi, ro_sh,
+                                      static_cast<size_t>(k) * 8);
+  return launch_even_co<G, MODE, 2>(a, ro, co, b, c, m, n, k, st, cohi, co_sh, rohi, ro_sh, 0);
+}
+
 template <class G>
 void launch(const double2* a, const double2* b, double2* c, Dim m, Dim n, Dim k, cudaStream_t st) {
+  if constexpr (G::GAUSS)
+    if (even_shape<G>(m, n, k)) return launch_even<G, 0>(a, nullptr, nullptr, b, c, m, n, k, st);
   launch_mode<G, 0>(a, nullptr, nullptr, b, c, m, n, k, st);
 }
 
@@ -352,6 +562,10 @@ using G6 = Cfg<32, 64, 1, 2, 8, 4, 4, 32, 32, true>;
 // Fewer, fatter CTAs for grids of a few waves (e.g. 2048 x 2048 x 1024: 39.2 vs
 // 35.9 TFLOP/s with G6): 16x32 warp tiles, BK 4, 8 stages, 3 CTAs/SM.
 using G22 = Cfg<32, 64, 2, 2, 4, 8, 3, 16, 32, true>;
+// Tile-aligned experiments (k_zgemm_even only): full-N 32 x 128 tiles (A read
+// once per row block) and 64 x 64 tiles (A and B fragments each shared by two warps).
+using G7 = Cfg<32, 128, 1, 4, 8, 4, 2, 32, 32, true>;
+using G8 = Cfg<64, 64, 2, 2, 8, 4, 2, 32, 32, true>;
 
 int variant() {
   static int v = [] {
@@ -396,6 +610,15 @@ void zgemm_gather_a(const void* a, const int64_t* rowoff, const int64_t* coloff,
   if (n > 32 && gv == 12) {
     if (rows_fastest) launch_mode<V12, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
     else launch_mode<V12, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
+  } else if (n > 32 && gv == 107 && even_shape<G7>(m, n, k)) {
+    if (rows_fastest) launch_even<G7, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
+    else launch_even<G7, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
+  } else if (n > 32 && gv == 108 && even_shape<G8>(m, n, k)) {
+    if (rows_fastest) launch_even<G8, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
+    else launch_even<G8, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
+  } else if (n > 32 && even_shape<G6>(m, n, k)) {
+    if (rows_fastest) launch_even<G6, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
+    else launch_even<G6, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
   } else if (n > 32) {
     if (rows_fastest) launch_mode<G6, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
     else launch_mode<G6, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
