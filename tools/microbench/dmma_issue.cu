@@ -47,6 +47,46 @@ int run(double* out, int sms, cudaEvent_t e0, cudaEvent_t e1) {
   return 0;
 }
 
+
+// DMMA stream with NADD independent DADDs per 8 DMMAs: does a DADD cost the
+// DMMA pipe more than its 64 flops?
+template <int NADD>
+__global__ void dmma_dadd(double* out, double seed, int iters) {
+  double a0 = seed + threadIdx.x, b0 = seed * 2;
+  double acc[8][2], x[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) { acc[j][0] = acc[j][1] = 0; x[j] = j; }
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(acc[j][0]), "+d"(acc[j][1]) : "d"(a0), "d"(b0));
+      if (j < NADD) asm volatile("add.f64 %0, %0, %1;" : "+d"(x[j]) : "d"(b0));
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; j++) s += acc[j][0] + acc[j][1] + x[j];
+  if (s == 1.2345) out[0] = s;
+}
+template <int NADD>
+int run_add(double* out, int sms, cudaEvent_t e0, cudaEvent_t e1) {
+  for (int wps : {1, 2}) {
+    int warps = 4 * wps, iters = 4096;
+    dmma_dadd<NADD><<<sms, warps * 32>>>(out, 1.0, iters);
+    CK(cudaDeviceSynchronize());
+    cudaEventRecord(e0);
+    for (int r = 0; r < 5; r++) dmma_dadd<NADD><<<sms, warps * 32>>>(out, 1.0, iters);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double n_dmma = 5.0 * sms * warps * (double)iters * 8;
+    printf("DADD/8DMMA=%d warps/SMSP=%d  DMMA %.2f TFLOP/s\n", NADD, wps, n_dmma * 512 / ms / 1e9);
+  }
+  return 0;
+}
+
 int main() {
   cudaDeviceProp p;
   CK(cudaGetDeviceProperties(&p, 0));
@@ -58,7 +98,10 @@ int main() {
   cudaEventCreate(&e1);
   int sms = p.multiProcessorCount;
   if (run<1>(out, sms, e0, e1) || run<2>(out, sms, e0, e1) || run<4>(out, sms, e0, e1) ||
-      run<8>(out, sms, e0, e1) || run<16>(out, sms, e0, e1) || run<48>(out, sms, e0, e1))
+      run<8>(out, sms, e0, e1) || run<16>(out, sms, e0, e1))
+    return 1;
+  if (run_add<0>(out, sms, e0, e1) || run_add<1>(out, sms, e0, e1) || run_add<2>(out, sms, e0, e1) ||
+      run_add<4>(out, sms, e0, e1) || run_add<8>(out, sms, e0, e1))
     return 1;
   return 0;
 }
