@@ -566,6 +566,10 @@ using G22 = Cfg<32, 64, 2, 2, 4, 8, 3, 16, 32, true>;
 // once per row block) and 64 x 64 tiles (A and B fragments each shared by two warps).
 using G7 = Cfg<32, 128, 1, 4, 8, 4, 2, 32, 32, true>;
 using G8 = Cfg<64, 64, 2, 2, 8, 4, 2, 32, 32, true>;
+// Default tile-aligned gather config: G6 with 3 stages (the interleaved refill
+// needs less lead; C1 41.6 vs 41.3 TFLOP/s with 4 stages). A pre-summed B plane
+// (4 instead of 8 DADDs per warp k4 step) spilled at 255 registers and lost 11 %.
+using G9 = Cfg<32, 64, 1, 2, 8, 3, 4, 32, 32, true>;
 
 int variant() {
   static int v = [] {
@@ -605,7 +609,7 @@ void zgemm_gather_a(const void* a, const int64_t* rowoff, const int64_t* coloff,
   auto Cp = static_cast<double2*>(c);
   static int gv = [] {
     const char* e = std::getenv("QTNH_ZGEMM_GATHER_VARIANT");
-    return e ? std::atoi(e) : 106;
+    return e ? std::atoi(e) : 109;
   }();
   if (n > 32 && gv == 12) {
     if (rows_fastest) launch_mode<V12, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
@@ -616,9 +620,12 @@ void zgemm_gather_a(const void* a, const int64_t* rowoff, const int64_t* coloff,
   } else if (n > 32 && gv == 108 && even_shape<G8>(m, n, k)) {
     if (rows_fastest) launch_even<G8, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
     else launch_even<G8, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
-  } else if (n > 32 && even_shape<G6>(m, n, k)) {
+  } else if (n > 32 && gv == 106 && even_shape<G6>(m, n, k)) {
     if (rows_fastest) launch_even<G6, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
     else launch_even<G6, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
+  } else if (n > 32 && even_shape<G9>(m, n, k)) {
+    if (rows_fastest) launch_even<G9, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
+    else launch_even<G9, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
   } else if (n > 32) {
     if (rows_fastest) launch_mode<G6, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
     else launch_mode<G6, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
@@ -643,6 +650,7 @@ void zgemm(const void* a, const void* b, void* c, Dim m, Dim n, Dim k, cudaStrea
     case 12: return launch<V12>(A, B, Cp, m, n, k, st);
     case 106: return launch<G6>(A, B, Cp, m, n, k, st);
     case 122: return launch<G22>(A, B, Cp, m, n, k, st);
+    case 109: return launch<G9>(A, B, Cp, m, n, k, st);
     default: break;
   }
   const Dim tiles = ((m + 31) / 32) * ((n + 63) / 64);
