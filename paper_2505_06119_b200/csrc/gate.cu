@@ -691,23 +691,33 @@ struct QftGroupArgs {
   double2 tab[32];  // tab[2^u + k] = e^{i pi k / 2^u}, k < 2^u, u < 5
 };
 
+// G = 5 (32 amplitudes = 128 registers per thread) runs one fiber per thread: in a
+// grid-stride loop the compiler hoists the 31 loop-invariant table twiddles into
+// registers and spills.
 template <int G>
 __global__ void __launch_bounds__(256, (G >= 4 ? 1 : 2)) k_qft_group(double2* __restrict__ psi, int64_t n_fibers, int B,
                                                    const __grid_constant__ QftGroupArgs ga) {
   const double r = 0.70710678118654752440;
   const int64_t lo_mask = (int64_t(1) << B) - 1;
+  constexpr bool kOne = G >= 5;
   for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < n_fibers;
-       f += (int64_t)gridDim.x * blockDim.x) {
+       f += kOne ? n_fibers : (int64_t)gridDim.x * blockDim.x) {
     int64_t lo = f & lo_mask, hi = f >> B;
     int64_t base = (hi << (B + G)) | lo;
+    // per-layer phases of the fixed low bits, before the amplitudes are live
+    double2 lofs[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      double sn, cs;
+      sincospi(static_cast<double>(lo) * ldexp(1.0, -(B + u)), &sn, &cs);
+      lofs[u] = make_double2(cs, sn);
+    }
     double2 x[1 << G];
 #pragma unroll
     for (int k = 0; k < (1 << G); ++k) x[k] = psi[base + (int64_t(k) << B)];
 #pragma unroll
     for (int u = G - 1; u >= 0; --u) {
-      double sn, cs;
-      sincospi(static_cast<double>(lo) * ldexp(1.0, -(B + u)), &sn, &cs);
-      const double2 lof = make_double2(cs, sn);
+      const double2 lof = lofs[u];
 #pragma unroll
       for (int k = 0; k < (1 << G); ++k) {
         if (k & (1 << u)) continue;
@@ -973,7 +983,7 @@ int qft_group_max() {
   static int v = [] {
     const char* e = std::getenv("QTNH_QFT_G");
     int g = e ? std::atoi(e) : 4;
-    return std::max(1, std::min(4, g));
+    return std::max(1, std::min(5, g));
   }();
   return v;
 }
@@ -1007,8 +1017,10 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
         ga.tab[(1 << u) + k] = make_double2(std::cos(ang), std::sin(ang));
       }
     int64_t n_f = int64_t(1) << (nb - g);
-    int grid = grid_for(n_f);
+    const int64_t one_grid = (n_f + 255) / 256;
+    int grid = g == 5 ? static_cast<int>(one_grid) : grid_for(n_f);
     switch (g) {
+      case 5: k_qft_group<5><<<grid, 256, 0, st>>>(p, n_f, B, ga); break;
       case 4: k_qft_group<4><<<grid, 256, 0, st>>>(p, n_f, B, ga); break;
       case 3: k_qft_group<3><<<grid, 256, 0, st>>>(p, n_f, B, ga); break;
       case 2: k_qft_group<2><<<grid, 256, 0, st>>>(p, n_f, B, ga); break;
