@@ -486,6 +486,9 @@ namespace {
 //  * k_bitrev2: the final SWAP network reverses the bit order -- one in-place pass
 //    that exchanges 32 x 32 tiles (a, m, b) <-> (rev b, rev m, rev a).
 constexpr int kQftLowMax = 11;
+#ifndef QTNH_LOW4_MINB
+#define QTNH_LOW4_MINB 1  // 4 (<= 128 registers) spills 20 bytes and is 1 % slower
+#endif
 
 __device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -500,6 +503,35 @@ __device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
 __constant__ double2 kQftSmallTw[15] = {{1.0, 0.0}, {1.0, 0.0}, {6.123233995736766e-17, 1.0}, {1.0, 0.0}, {0.7071067811865476, 0.7071067811865475}, {6.123233995736766e-17, 1.0}, {-0.7071067811865475, 0.7071067811865476}, {1.0, 0.0}, {0.9238795325112867, 0.3826834323650898}, {0.7071067811865476, 0.7071067811865475}, {0.38268343236508984, 0.9238795325112867}, {6.123233995736766e-17, 1.0}, {-0.3826834323650897, 0.9238795325112867}, {-0.7071067811865475, 0.7071067811865476}, {-0.9238795325112867, 0.3826834323650899}};  // e^{i pi k / 2^u}, index 2^u - 1 + k
 
 __device__ __forceinline__ int swz8(int i) { return i ^ ((i >> 3) & 7); }  // conflict-free 16-B rows
+
+// Compact twiddles of the low pass: the rounds run top-down in groups of up to 4
+// bits; a round with bits B..B+g-1 only needs e^{i pi lo / 2^(B+u)} for lo < 2^B,
+// u < g, stored at its round offset as [u][lo]. For L = 11 that is 547 entries
+// (8.75 KB) instead of a 2^L-entry table (32 KB), so more CTAs fit on an SM.
+__host__ __device__ constexpr int qft_low_g(int T) { return T + 1 >= 4 ? 4 : T + 1; }
+__host__ __device__ inline int qft_low_tw_count(int L) {
+  int n = 0;
+  for (int T = L - 1; T >= 0;) {
+    const int g = qft_low_g(T), B = T - g + 1;
+    n += g << B;
+    T = B - 1;
+  }
+  return n;
+}
+__device__ void qft_low_tw_build(double2* tw, int L) {
+  int off = 0;
+  for (int T = L - 1; T >= 0;) {
+    const int g = qft_low_g(T), B = T - g + 1;
+    for (int e = threadIdx.x; e < (g << B); e += blockDim.x) {
+      const int u = e >> B, lo = e & ((1 << B) - 1);
+      double sn, cs;
+      sincospi(static_cast<double>(lo) * ldexp(1.0, -(B + u)), &sn, &cs);
+      tw[off + e] = make_double2(cs, sn);
+    }
+    off += g << B;
+    T = B - 1;
+  }
+}
 
 // The butterflies are unnormalised (y0 = a0 + a1, y1 = (a0 - a1) w): the L
 // factors of 1/sqrt2 are applied once when the chunk is written back, which
@@ -517,7 +549,7 @@ __device__ __forceinline__ void qft_low_round(double2* __restrict__ data, const 
     // phase of layer t = B + u for in-fiber index k: e^{i pi klow / 2^u} * e^{i pi lo / 2^t}
     double2 lof[G];
 #pragma unroll
-    for (int u = 0; u < G; ++u) lof[u] = (B + u) > 0 ? tw[(1 << (B + u)) + lo] : make_double2(1.0, 0.0);
+    for (int u = 0; u < G; ++u) lof[u] = tw[(u << B) + lo];
 #pragma unroll
     for (int u = G - 1; u >= 0; --u) {
 #pragma unroll
@@ -558,14 +590,7 @@ __global__ void __launch_bounds__(128) k_qft_low3(double2* __restrict__ psi, int
   double2* buf0 = smq3;
   double2* buf1 = smq3 + C;
   double2* tw = smq3 + 2 * C;
-  for (int e = threadIdx.x; e < (1 << L); e += blockDim.x) {
-    if (e == 0) continue;
-    int t = 31 - __clz(e);
-    int v = e - (1 << t);
-    double sn, cs;
-    sincospi(static_cast<double>(v) * ldexp(1.0, -t), &sn, &cs);
-    tw[e] = make_double2(cs, sn);
-  }
+  qft_low_tw_build(tw, L);
   int64_t ch = blockIdx.x;
   if (ch < n_chunks)
     for (int e = threadIdx.x; e < C; e += blockDim.x) cp_async16(buf0 + swz8(e), psi + ch * C + e);
@@ -580,16 +605,17 @@ __global__ void __launch_bounds__(128) k_qft_low3(double2* __restrict__ psi, int
     cp_async_commit();
     cp_async_wait1();  // this chunk has landed (the next one may still be in flight)
     __syncthreads();
-    for (int T = L - 1; T >= 0;) {
-      int gg = T + 1 >= 4 ? 4 : T + 1;
+    for (int T = L - 1, off = 0; T >= 0;) {
+      int gg = qft_low_g(T);
       int B = T - gg + 1;
       switch (gg) {
-        case 4: qft_low_round<4>(data, tw, S, B); break;
-        case 3: qft_low_round<3>(data, tw, S, B); break;
-        case 2: qft_low_round<2>(data, tw, S, B); break;
-        default: qft_low_round<1>(data, tw, S, B); break;
+        case 4: qft_low_round<4>(data, tw + off, S, B); break;
+        case 3: qft_low_round<3>(data, tw + off, S, B); break;
+        case 2: qft_low_round<2>(data, tw + off, S, B); break;
+        default: qft_low_round<1>(data, tw + off, S, B); break;
       }
       __syncthreads();
+      off += gg << B;
       T = B - 1;
     }
     double2* g = psi + ch * C;
@@ -619,7 +645,7 @@ __device__ __forceinline__ void qft_low_round_from_global(const double2* __restr
     for (int k = 0; k < (1 << G); ++k) x[k] = g[base + (k << B)];
     double2 lof[G];
 #pragma unroll
-    for (int u = 0; u < G; ++u) lof[u] = (B + u) > 0 ? tw[(1 << (B + u)) + lo] : make_double2(1.0, 0.0);
+    for (int u = 0; u < G; ++u) lof[u] = tw[(u << B) + lo];
 #pragma unroll
     for (int u = G - 1; u >= 0; --u) {
 #pragma unroll
@@ -639,44 +665,39 @@ __device__ __forceinline__ void qft_low_round_from_global(const double2* __restr
   }
 }
 
-__global__ void __launch_bounds__(128) k_qft_low4(double2* __restrict__ psi, int64_t n_chunks, int S, int L) {
+__global__ void __launch_bounds__(128, QTNH_LOW4_MINB) k_qft_low4(double2* __restrict__ psi, int64_t n_chunks, int S, int L) {
   extern __shared__ double2 smq4[];
   const int C = 1 << S;
   double2* data = smq4;
   double2* tw = smq4 + C;
-  for (int e = threadIdx.x; e < (1 << L); e += blockDim.x) {
-    if (e == 0) continue;
-    int t = 31 - __clz(e);
-    int v = e - (1 << t);
-    double sn, cs;
-    sincospi(static_cast<double>(v) * ldexp(1.0, -t), &sn, &cs);
-    tw[e] = make_double2(cs, sn);
-  }
+  qft_low_tw_build(tw, L);
   __syncthreads();
   const double sc = ldexp(1.0, -(L / 2)) * (L & 1 ? 0.70710678118654752440 : 1.0);  // (1/sqrt2)^L
   for (int64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
     double2* g = psi + ch * C;
-    int T = L - 1;
+    int T = L - 1, off = 0;
     {
-      const int gg = T + 1 >= 4 ? 4 : T + 1, B = T - gg + 1;
+      const int gg = qft_low_g(T), B = T - gg + 1;
       switch (gg) {
         case 4: qft_low_round_from_global<4>(g, data, tw, S, B); break;
         case 3: qft_low_round_from_global<3>(g, data, tw, S, B); break;
         case 2: qft_low_round_from_global<2>(g, data, tw, S, B); break;
         default: qft_low_round_from_global<1>(g, data, tw, S, B); break;
       }
+      off += gg << B;
       T = B - 1;
     }
     __syncthreads();
     while (T >= 0) {
-      const int gg = T + 1 >= 4 ? 4 : T + 1, B = T - gg + 1;
+      const int gg = qft_low_g(T), B = T - gg + 1;
       switch (gg) {
-        case 4: qft_low_round<4>(data, tw, S, B); break;
-        case 3: qft_low_round<3>(data, tw, S, B); break;
-        case 2: qft_low_round<2>(data, tw, S, B); break;
-        default: qft_low_round<1>(data, tw, S, B); break;
+        case 4: qft_low_round<4>(data, tw + off, S, B); break;
+        case 3: qft_low_round<3>(data, tw + off, S, B); break;
+        case 2: qft_low_round<2>(data, tw + off, S, B); break;
+        default: qft_low_round<1>(data, tw + off, S, B); break;
       }
       __syncthreads();
+      off += gg << B;
       T = B - 1;
     }
     for (int e = threadIdx.x; e < C; e += blockDim.x) {
@@ -1034,7 +1055,8 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
     int Lc = top + 1;
     const int S = std::max(Lc, std::min(nb, kQftLowMax));
     const int64_t n_chunks = int64_t(1) << (nb - S);
-    size_t smem = ((static_cast<size_t>(2) << S) + (size_t(1) << Lc)) * sizeof(double2);  // 2 buffers + twiddles
+    const size_t n_tw = static_cast<size_t>(qft_low_tw_count(Lc));
+    size_t smem = ((static_cast<size_t>(2) << S) + n_tw) * sizeof(double2);  // 2 buffers + twiddles
     static bool attr = [] {
       cudaFuncSetAttribute(k_qft_low3, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 16 << kQftLowMax);
       return true;
@@ -1050,7 +1072,7 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
       return !(e && e[0] == '3');
     }();
     if (v4) {
-      const size_t smem4 = ((size_t(1) << S) + (size_t(1) << Lc)) * sizeof(double2);
+      const size_t smem4 = ((size_t(1) << S) + n_tw) * sizeof(double2);
       static bool attr4 = [] {
         cudaFuncSetAttribute(k_qft_low4, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16 << kQftLowMax);
         return true;
