@@ -89,11 +89,17 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 
 // ---- block-size templated kernels (B rows per block, pair of 2B rows) ------------------
 // Dynamic shared memory: the pair's Gram matrix G and eigenvectors V (2B x 2B+1).
+// Cross mode (dblk != nullptr): part holds only the pair's cross block
+// X_bi X_bj^H (B x B per split); the diagonal blocks X_b X_b^H come from dblk
+// (refreshed from X at the start of every sweep, then carried from round to round
+// as the rotated diagonal blocks of W^H G W, which this kernel writes back).
 template <int B>
 __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__ part, double2* __restrict__ wh,
                                                      int* __restrict__ flags, double* __restrict__ off_max,
                                                      int npairs, int splits, double tol, int inner_sweeps,
-                                                     const double* __restrict__ floor_abs) {
+                                                     const double* __restrict__ floor_abs,
+                                                     double2* __restrict__ dblk, const int* __restrict__ tab,
+                                                     int round, int nblk2) {
   constexpr int P2 = 2 * B, LD = P2 + 1;
   const int pair = blockIdx.x, mat = blockIdx.y, tid = threadIdx.x;
   const double fl = floor_abs[mat];
@@ -104,17 +110,47 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
   __shared__ double2 rot_ph[B];
   __shared__ int rp_[B], rq_[B];
   __shared__ double red[256];
-  const double2* P = part + (static_cast<int64_t>(mat) * npairs + pair) * splits * P2 * P2;
-  for (int e = tid; e < P2 * P2; e += 256) {
-    int i = e / P2, j = e % P2;
-    double2 sm = make_double2(0.0, 0.0);
-    for (int sp = 0; sp < splits; ++sp) {
-      double2 v = P[static_cast<int64_t>(sp) * P2 * P2 + e];
-      sm.x += v.x;
-      sm.y += v.y;
+  const bool cross = dblk != nullptr;
+  double2* Di = nullptr;
+  double2* Dj = nullptr;
+  if (cross) {
+    const int* pr = tab + (static_cast<int64_t>(round) * npairs + pair) * 2;
+    Di = dblk + (static_cast<int64_t>(mat) * nblk2 + pr[0]) * B * B;
+    Dj = dblk + (static_cast<int64_t>(mat) * nblk2 + pr[1]) * B * B;
+    const double2* P = part + (static_cast<int64_t>(mat) * npairs + pair) * splits * B * B;
+    for (int e = tid; e < P2 * P2; e += 256) {
+      const int i = e / P2, j = e % P2;
+      double2 v;
+      if (i < B && j < B) {
+        v = Di[i * B + j];
+      } else if (i >= B && j >= B) {
+        v = Dj[(i - B) * B + (j - B)];
+      } else {
+        const int r = i < B ? i : j, c = i < B ? j - B : i - B;  // cross element (r, c) of X_bi X_bj^H
+        double2 sm = make_double2(0.0, 0.0);
+        for (int sp = 0; sp < splits; ++sp) {
+          const double2 w = P[static_cast<int64_t>(sp) * B * B + r * B + c];
+          sm.x += w.x;
+          sm.y += w.y;
+        }
+        v = i < B ? sm : cconj(sm);
+      }
+      G[i * LD + j] = v;
+      V[i * LD + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
     }
-    G[i * LD + j] = sm;
-    V[i * LD + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+  } else {
+    const double2* P = part + (static_cast<int64_t>(mat) * npairs + pair) * splits * P2 * P2;
+    for (int e = tid; e < P2 * P2; e += 256) {
+      int i = e / P2, j = e % P2;
+      double2 sm = make_double2(0.0, 0.0);
+      for (int sp = 0; sp < splits; ++sp) {
+        double2 v = P[static_cast<int64_t>(sp) * P2 * P2 + e];
+        sm.x += v.x;
+        sm.y += v.y;
+      }
+      G[i * LD + j] = sm;
+      V[i * LD + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+    }
   }
   __syncthreads();
   auto measure = [&]() {
@@ -218,15 +254,48 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
     int i = e / P2, j = e % P2;
     out[e] = cconj(V[j * LD + i]);  // W^H
   }
+  if (cross) {  // G now holds W^H G W: its diagonal blocks are the updated rows' Grams
+    for (int e = tid; e < B * B; e += 256) {
+      const int i = e / B, j = e % B;
+      Di[e] = G[i * LD + j];
+      Dj[e] = G[(i + B) * LD + (j + B)];
+    }
+  }
   if (tid == 0) flags[fidx] = 1;
 }
 
-// Gram of a row-block pair on DMMA: P2/8 warps, warp w owns rows [8w, 8w+8) x P2.
+// Diagonal-block refresh of the cross mode: the full Gram of pairs (2k, 2k + 1)
+// (the extra tournament round) summed over splits; its diagonal blocks go to dblk.
 template <int B>
-__global__ void __launch_bounds__(B * 8) k_svd_gram_mma_t(const double2* __restrict__ wk, double2* __restrict__ part,
-                                                          const int* __restrict__ tab, int round, int npairs,
-                                                          int splits, int64_t rp, int64_t L, int64_t qw) {
-  constexpr int P2 = 2 * B, NT = P2 / 8, T = B * 8, GK = B >= 32 ? 32 : 64, PX = GK + 4;
+__global__ void k_svd_diag_store(const double2* __restrict__ part, double2* __restrict__ dblk, int npairs, int splits,
+                                 int nblk2) {
+  constexpr int P2 = 2 * B;
+  const int pair = blockIdx.x, mat = blockIdx.y;
+  const double2* P = part + (static_cast<int64_t>(mat) * npairs + pair) * splits * P2 * P2;
+  for (int e = threadIdx.x; e < 2 * B * B; e += blockDim.x) {
+    const int h = e / (B * B), i = (e % (B * B)) / B, j = e % B;
+    const int src = (h * B + i) * P2 + (h * B + j);
+    double2 sm = make_double2(0.0, 0.0);
+    for (int sp = 0; sp < splits; ++sp) {
+      const double2 v = P[static_cast<int64_t>(sp) * P2 * P2 + src];
+      sm.x += v.x;
+      sm.y += v.y;
+    }
+    dblk[(static_cast<int64_t>(mat) * nblk2 + 2 * pair + h) * B * B + i * B + j] = sm;
+  }
+}
+
+// Gram of a row-block pair on DMMA: P2/8 warps, warp w owns rows [8w, 8w+8) x P2.
+// CROSS: only the cross block X_bi X_bj^H (B x B): B/8 warps own rows of block bi,
+// the column tiles are the rows of block bj -- a quarter of the DMMAs.
+template <int B, bool CROSS = false>
+__global__ void __launch_bounds__(CROSS ? B * 4 : B * 8) k_svd_gram_mma_t(const double2* __restrict__ wk,
+                                                                           double2* __restrict__ part,
+                                                                           const int* __restrict__ tab, int round,
+                                                                           int npairs, int splits, int64_t rp,
+                                                                           int64_t L, int64_t qw) {
+  constexpr int P2 = 2 * B, NT = CROSS ? B / 8 : P2 / 8, T = CROSS ? B * 4 : B * 8, GK = B >= 32 ? 32 : 64,
+                PX = GK + 4, OC = CROSS ? B : P2, C0 = CROSS ? B : 0;
   const int pair = blockIdx.x, split = blockIdx.y, mat = blockIdx.z;
   const int64_t W = L + qw;
   const int* pr = tab + (static_cast<int64_t>(round) * npairs + pair) * 2;
@@ -270,7 +339,7 @@ __global__ void __launch_bounds__(B * 8) k_svd_gram_mma_t(const double2* __restr
       const double as = av.x + av.y;
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
-        double2 bv = xs[(j * 8 + fr) * PX + k4 + fk];
+        double2 bv = xs[(C0 + j * 8 + fr) * PX + k4 + fk];
         dmma(acc_re[j], av.x, bv.x);
         dmma(acc_im[j], av.y, bv.y);
         dmma(acc_s[j], as, bv.x - bv.y);
@@ -278,12 +347,12 @@ __global__ void __launch_bounds__(B * 8) k_svd_gram_mma_t(const double2* __restr
     }
     __syncthreads();  // buffer it & 1 is refilled two chunks on
   }
-  double2* out = part + ((static_cast<int64_t>(mat) * npairs + pair) * splits + split) * P2 * P2;
+  double2* out = part + ((static_cast<int64_t>(mat) * npairs + pair) * splits + split) * OC * OC;
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
     int row = warp * 8 + fr, col = j * 8 + 2 * fk;
-    out[row * P2 + col] = make_double2(acc_re[j][0] + acc_im[j][0], acc_s[j][0] - acc_re[j][0] + acc_im[j][0]);
-    out[row * P2 + col + 1] =
+    out[row * OC + col] = make_double2(acc_re[j][0] + acc_im[j][0], acc_s[j][0] - acc_re[j][0] + acc_im[j][0]);
+    out[row * OC + col + 1] =
         make_double2(acc_re[j][1] + acc_im[j][1], acc_s[j][1] - acc_re[j][1] + acc_im[j][1]);
   }
 }
@@ -563,8 +632,20 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   const bool acc_q = transpose || accumulate_q();
   const Dim qw = acc_q ? rp : 0;
   const Dim W = L + qw;
-  // tournament table (circle method, block nblk2-1 fixed)
-  std::vector<int> tab(static_cast<size_t>(rounds) * npairs * 2);
+  // Cross mode (default): each round computes only the pairs' cross Gram blocks
+  // and carries the diagonal blocks in dblk (a quarter of the Gram DMMAs); the
+  // diagonal blocks are recomputed from X at the start of every sweep.
+  static const bool cross = [] {
+    const char* e = std::getenv("QTNH_SVD_CROSS");
+    return !(e && e[0] == '0');
+  }();
+  // tournament table (circle method, block nblk2-1 fixed); one extra round of the
+  // pairs (2k, 2k+1) drives the cross mode's diagonal-block refresh
+  std::vector<int> tab(static_cast<size_t>(rounds + 1) * npairs * 2);
+  for (int k = 0; k < npairs; ++k) {
+    tab[(static_cast<size_t>(rounds) * npairs + k) * 2] = 2 * k;
+    tab[(static_cast<size_t>(rounds) * npairs + k) * 2 + 1] = 2 * k + 1;
+  }
   for (int rd = 0; rd < rounds; ++rd)
     for (int k = 0; k < npairs; ++k) {
       int p, q;
@@ -587,6 +668,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   DevBuf whb(static_cast<size_t>(batch * npairs) * P2 * P2 * 16, r);
   DevBuf flags(static_cast<size_t>(batch * npairs) * sizeof(int), r);
   DevBuf offm(static_cast<size_t>(batch) * sizeof(double), r);
+  DevBuf dblk(cross ? static_cast<size_t>(batch * nblk2) * B * B * 16 : 16, r);
   QTNH_CUDA(cudaMemcpyAsync(d_tab.ptr, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice, st));
   {
     dim3 g(static_cast<unsigned>(std::min<Dim>((rp * W + 255) / 256, 4096)), static_cast<unsigned>(batch));
@@ -613,6 +695,8 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_gram_mma_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem));
+  QTNH_CUDA(cudaFuncSetAttribute(k_svd_gram_mma_t<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)gram_smem));
   // The batch runs as two independent halves on two streams when it has >= 2
   // matrices: the latency-bound eigen step of one half overlaps the other half's
   // Gram / update DMMA work, and a half that converges stops early.
@@ -659,6 +743,20 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
     for (; sweep < max_sweeps; ++sweep) {
       for (auto& G : grp)
         if (!G.done) QTNH_CUDA(cudaMemsetAsync(static_cast<double*>(offm.ptr) + G.base, 0, G.cnt * 8, G.s));
+      if (cross)
+        for (auto& G : grp) {
+          if (G.done) continue;
+          const unsigned cnt = static_cast<unsigned>(G.cnt);
+          double2* wkg = static_cast<double2*>(wk.ptr) + G.base * rp * W;
+          double2* partg = static_cast<double2*>(part.ptr) + G.base * npairs * splits * P2 * P2;
+          k_svd_gram_mma_t<B><<<dim3(npairs, splits, cnt), B * 8, gram_smem, G.s>>>(
+              wkg, partg, static_cast<const int*>(d_tab.ptr), rounds, npairs, splits, rp, L, qw);
+          QTNH_LAUNCH_CHECK();
+          k_svd_diag_store<B><<<dim3(npairs, cnt), 256, 0, G.s>>>(
+              partg, static_cast<double2*>(dblk.ptr) + G.base * nblk2 * B * B, npairs, splits,
+              static_cast<int>(nblk2));
+          QTNH_LAUNCH_CHECK();
+        }
       for (int rd = 0; rd < rounds; ++rd)
         for (auto& G : grp) {
           if (G.done) continue;
@@ -667,12 +765,18 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
           double2* partg = static_cast<double2*>(part.ptr) + G.base * npairs * splits * P2 * P2;
           double2* whg = static_cast<double2*>(whb.ptr) + G.base * npairs * P2 * P2;
           int* flg = static_cast<int*>(flags.ptr) + G.base * npairs;
-          k_svd_gram_mma_t<B><<<dim3(npairs, splits, cnt), B * 8, gram_smem, G.s>>>(
-              wkg, partg, static_cast<const int*>(d_tab.ptr), rd, npairs, splits, rp, L, qw);
+          if (cross)
+            k_svd_gram_mma_t<B, true><<<dim3(npairs, splits, cnt), B * 4, gram_smem, G.s>>>(
+                wkg, partg, static_cast<const int*>(d_tab.ptr), rd, npairs, splits, rp, L, qw);
+          else
+            k_svd_gram_mma_t<B><<<dim3(npairs, splits, cnt), B * 8, gram_smem, G.s>>>(
+                wkg, partg, static_cast<const int*>(d_tab.ptr), rd, npairs, splits, rp, L, qw);
           QTNH_LAUNCH_CHECK();
           k_svd_eigen_t<B><<<dim3(npairs, cnt), 256, eig_smem, G.s>>>(
               partg, whg, flg, static_cast<double*>(offm.ptr) + G.base, npairs, splits, tol, inner_sweeps(),
-              static_cast<const double*>(floor_abs.ptr) + G.base);
+              static_cast<const double*>(floor_abs.ptr) + G.base,
+              cross ? static_cast<double2*>(dblk.ptr) + G.base * nblk2 * B * B : nullptr,
+              static_cast<const int*>(d_tab.ptr), rd, static_cast<int>(nblk2));
           QTNH_LAUNCH_CHECK();
           if (uc == 32)
             k_svd_update_mma_t<B, 32><<<dim3(ctiles, npairs, cnt), B * 8, upd_smem, G.s>>>(
