@@ -635,9 +635,17 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   // Cross mode (default): each round computes only the pairs' cross Gram blocks
   // and carries the diagonal blocks in dblk (a quarter of the Gram DMMAs); the
   // diagonal blocks are recomputed from X at the start of every sweep.
+  // Carried diagonal blocks do not see the rounding the updates leave on rows much
+  // smaller than their pair partners, so on graded spectra (MPS thetas) the cross
+  // mode converges only linearly once the off-norm is small: a group switches to
+  // full Grams after a sweep whose max off-norm fell below QTNH_SVD_CROSS_UNTIL.
   static const bool cross = [] {
     const char* e = std::getenv("QTNH_SVD_CROSS");
     return !(e && e[0] == '0');
+  }();
+  static const double cross_until = [] {
+    const char* e = std::getenv("QTNH_SVD_CROSS_UNTIL");
+    return e ? std::atof(e) : 1e-3;
   }();
   // tournament table (circle method, block nblk2-1 fixed); one extra round of the
   // pairs (2k, 2k+1) drives the cross mode's diagonal-block refresh
@@ -705,6 +713,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
     Dim base = 0, cnt = 0;
     cudaStream_t s = nullptr;
     bool done = false;
+    bool cross = false;  // this sweep uses cross Grams
     int sweeps = 0;
   };
   std::vector<Group> grp(ngroups);
@@ -714,6 +723,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   for (int g = 0; g < ngroups; ++g) {
     grp[g].base = g * batch / ngroups;
     grp[g].cnt = (g + 1) * batch / ngroups - grp[g].base;
+    grp[g].cross = cross;
     if (ngroups == 1) {
       grp[g].s = st;
     } else {
@@ -722,7 +732,9 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
     }
   }
   std::vector<double> off_h(batch);
-  const int max_sweeps = 40;
+  // Strongly graded spectra converge slowly (a 320 x 320 matrix with singular
+  // values over 12 decades takes ~45 sweeps; random and MPS-theta inputs 16-20).
+  const int max_sweeps = 64;
   const Dim gmax = (batch + ngroups - 1) / ngroups;
   const unsigned ctiles = static_cast<unsigned>(
       std::min<Dim>((W + uc - 1) / uc, std::max<Dim>(1, (B == 16 ? 8 : 4) * sms() / (npairs * gmax))));
@@ -743,9 +755,8 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
     for (; sweep < max_sweeps; ++sweep) {
       for (auto& G : grp)
         if (!G.done) QTNH_CUDA(cudaMemsetAsync(static_cast<double*>(offm.ptr) + G.base, 0, G.cnt * 8, G.s));
-      if (cross)
-        for (auto& G : grp) {
-          if (G.done) continue;
+      for (auto& G : grp) {
+          if (G.done || !G.cross) continue;
           const unsigned cnt = static_cast<unsigned>(G.cnt);
           double2* wkg = static_cast<double2*>(wk.ptr) + G.base * rp * W;
           double2* partg = static_cast<double2*>(part.ptr) + G.base * npairs * splits * P2 * P2;
@@ -765,7 +776,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
           double2* partg = static_cast<double2*>(part.ptr) + G.base * npairs * splits * P2 * P2;
           double2* whg = static_cast<double2*>(whb.ptr) + G.base * npairs * P2 * P2;
           int* flg = static_cast<int*>(flags.ptr) + G.base * npairs;
-          if (cross)
+          if (G.cross)
             k_svd_gram_mma_t<B, true><<<dim3(npairs, splits, cnt), B * 4, gram_smem, G.s>>>(
                 wkg, partg, static_cast<const int*>(d_tab.ptr), rd, npairs, splits, rp, L, qw);
           else
@@ -775,7 +786,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
           k_svd_eigen_t<B><<<dim3(npairs, cnt), 256, eig_smem, G.s>>>(
               partg, whg, flg, static_cast<double*>(offm.ptr) + G.base, npairs, splits, tol, inner_sweeps(),
               static_cast<const double*>(floor_abs.ptr) + G.base,
-              cross ? static_cast<double2*>(dblk.ptr) + G.base * nblk2 * B * B : nullptr,
+              G.cross ? static_cast<double2*>(dblk.ptr) + G.base * nblk2 * B * B : nullptr,
               static_cast<const int*>(d_tab.ptr), rd, static_cast<int>(nblk2));
           QTNH_LAUNCH_CHECK();
           if (uc == 32)
@@ -805,6 +816,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
           G.sweeps = sweep + 1;
         } else {
           all = false;
+          if (mx < cross_until) G.cross = false;
         }
       }
       if (all) break;

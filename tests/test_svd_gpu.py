@@ -92,6 +92,33 @@ def test_rank_deficient_and_zero():
     assert np.all(s == 0) and np.all((u * s) @ vh == 0)
 
 
+@pytest.mark.parametrize("cross", ["1", "0"])
+def test_svd_graded_spectrum(cross, monkeypatch):
+    """Singular values spanning 12 decades (an MPS theta's graded spectrum): the
+    cross-Gram sweeps must hand over to full Grams and still converge to the
+    truncated reconstruction within the north-star tolerance."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "from test_svd_gpu import gpu_svd; from conftest import rel_l2;"
+        "rng = np.random.default_rng(7); n = 320;"
+        "q1, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)));"
+        "q2, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)));"
+        "sv = np.logspace(0, -12, n); a = (q1 * sv) @ q2.conj().T;"
+        "u, s, vh = gpu_svd(a, chi=160);"
+        "U, S, VH = np.linalg.svd(a, full_matrices=False);"
+        "assert np.allclose(s, S[:160], rtol=1e-9, atol=1e-15), 'singular values';"
+        "assert rel_l2((u * s) @ vh, (U[:, :160] * S[:160]) @ VH[:160]) < 1e-10, 'reconstruction';"
+        "print('ok')"
+    )
+    import os
+    env = dict(os.environ, QTNH_SVD_CROSS=cross)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
 def test_svd_vs_reference_theta_like():
     """MPS two-site theta (chi_l, d, d, chi_r) -> (chi_l d) x (d chi_r), truncated."""
     if not oracle.ref_available():
