@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--chi", type=int, default=1024)
     ap.add_argument("--seed", type=int, default=2025)
     ap.add_argument("--bitstrings", type=int, default=1024)
+    ap.add_argument("--amps-out", default="", help="save the bitstring amplitudes (.npy) for run-to-run comparison")
     ap.add_argument("--sequential", action="store_true", help="one SVD per update instead of batched layers")
     ap.add_argument("--world", type=int, default=1,
                     help="ranks (thread per rank, round-robin over the visible GPUs); > 1 shards the sites "
@@ -71,6 +72,8 @@ def main():
         bits = rng.integers(0, 2, size=(args.bitstrings, args.n))
         ta = time.perf_counter()
         amps = m.amplitudes(bits)
+        if args.amps_out:
+            np.save(args.amps_out, np.asarray(amps))
         out.update(total_s=total, per_layer_s=per_layer, updates=upd, bond_dims=m.bond_dims(),
                    fidelity=float(np.exp(m.log_fidelity)), amp_time_s=time.perf_counter() - ta,
                    amp_norm2_sum=float(np.sum(np.abs(amps) ** 2)), amp_first=[str(a) for a in amps[:4]])
