@@ -99,7 +99,8 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
                                                      int npairs, int splits, double tol, int inner_sweeps,
                                                      const double* __restrict__ floor_abs,
                                                      double2* __restrict__ dblk, const int* __restrict__ tab,
-                                                     int round, int nblk2, int sort_pair) {
+                                                     int round, int nblk2, int sort_pair,
+                                                     const double* __restrict__ rot_thr) {
   constexpr int P2 = 2 * B, LD = P2 + 1;
   const int pair = blockIdx.x, mat = blockIdx.y, tid = threadIdx.x;
   const double fl = floor_abs[mat];
@@ -110,6 +111,15 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
   __shared__ double2 rot_ph[B];
   __shared__ int rp_[B], rq_[B];
   __shared__ double red[256];
+  // Rotation threshold (classical threshold Jacobi): pairs with |G_pq| below
+  // thr sqrt(G_pp G_qq) are not rotated (rot_thr, set per matrix by the host:
+  // adapt x the previous sweep's max off-norm once that falls only linearly). Inside a cluster of (nearly) equal singular
+  // values every rotation is ~45 degrees however small |G_pq| is, so rotating
+  // already-orthogonal pairs only churns the cluster: the C4 thetas (128-fold
+  // degenerate spectra) fell linearly (x0.4 per sweep). NumPy model of the block
+  // method (tools/svd_block_model.py): theta 28 -> 12 sweeps, random 11 -> 12.
+  const double thr = rot_thr[mat];
+  const double rot_thr2 = fmax(1e-34, thr * thr);
   const bool cross = dblk != nullptr;
   double2* Di = nullptr;
   double2* Dj = nullptr;
@@ -206,7 +216,7 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
         const double r2 = fma(x.x, x.x, x.y * x.y);
         double c = 1.0, sn = 0.0;
         double2 ph = make_double2(1.0, 0.0);
-        if (r2 > 1e-600 && !(r2 <= 1e-34 * fabs(a * b))) {
+        if (r2 > 1e-600 && !(r2 <= rot_thr2 * fabs(a * b))) {
           const double inv_ax = rsqrt(r2);
           ph = make_double2(x.x * inv_ax, -x.y * inv_ax);
           const double tau = 0.5 * (b - a) * inv_ax;
@@ -728,6 +738,12 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   DevBuf whb(static_cast<size_t>(batch * npairs) * P2 * P2 * 16, r);
   DevBuf flags(static_cast<size_t>(batch * npairs) * sizeof(int), r);
   DevBuf offm(static_cast<size_t>(batch) * sizeof(double), r);
+  DevBuf offp(static_cast<size_t>(batch) * sizeof(double), r);  // per-matrix rotation threshold
+  static const double adapt = [] {
+    const char* e = std::getenv("QTNH_SVD_ADAPT");
+    return e ? std::atof(e) : 1e-3;
+  }();
+  QTNH_CUDA(cudaMemsetAsync(offp.ptr, 0, batch * sizeof(double), st));
   DevBuf dblk(cross ? static_cast<size_t>(batch * nblk2) * B * B * 16 : 16, r);
   QTNH_CUDA(cudaMemcpyAsync(d_tab.ptr, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice, st));
   {
@@ -784,6 +800,8 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
     }
   }
   std::vector<double> off_h(batch);
+  std::vector<double> off_hist(2 * batch, 1.0), thr_h(batch, 0.0);  // per matrix: last two sweeps' max off
+  std::vector<char> thr_on(batch, 0);
   // Strongly graded spectra converge slowly (a 320 x 320 matrix with singular
   // values over 12 decades takes ~45 sweeps; random and MPS-theta inputs 16-20).
   const int max_sweeps = 64;
@@ -837,7 +855,21 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
         std::swap(wkp, wkq);
       }
       for (auto& G : grp)
-        if (!G.done) QTNH_CUDA(cudaMemsetAsync(static_cast<double*>(offm.ptr) + G.base, 0, G.cnt * 8, G.s));
+        if (!G.done) {
+          // The threshold engages (and stays on) once a matrix's off-norm falls only
+          // linearly (below 0.05, by less than x4 per sweep): clustered spectra. In the
+          // quadratic regime of well-separated spectra it would cut the convergence
+          // short (a 2048^2 random matrix whose early plateau dipped below 0.1 took
+          // 25 instead of 17 sweeps with it on).
+          for (Dim b = G.base; b < G.base + G.cnt; ++b) {
+            const double o1 = off_hist[b * 2], o2 = off_hist[b * 2 + 1];
+            if (sweep >= 2 && o1 < 0.05 && o1 < o2 && o1 > 0.25 * o2) thr_on[b] = 1;
+            thr_h[b] = thr_on[b] ? adapt * o1 : 0.0;
+          }
+          QTNH_CUDA(cudaMemcpyAsync(static_cast<double*>(offp.ptr) + G.base, thr_h.data() + G.base, G.cnt * 8,
+                                    cudaMemcpyHostToDevice, G.s));
+          QTNH_CUDA(cudaMemsetAsync(static_cast<double*>(offm.ptr) + G.base, 0, G.cnt * 8, G.s));
+        }
       for (auto& G : grp) {
           if (G.done || !G.cross) continue;
           const unsigned cnt = static_cast<unsigned>(G.cnt);
@@ -870,7 +902,8 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
               partg, whg, flg, static_cast<double*>(offm.ptr) + G.base, npairs, splits, tol, inner_sweeps(),
               static_cast<const double*>(floor_abs.ptr) + G.base,
               G.cross ? static_cast<double2*>(dblk.ptr) + G.base * nblk2 * B * B : nullptr,
-              static_cast<const int*>(d_tab.ptr), rd, static_cast<int>(nblk2), sort_pair ? 1 : 0);
+              static_cast<const int*>(d_tab.ptr), rd, static_cast<int>(nblk2), sort_pair ? 1 : 0,
+              static_cast<const double*>(offp.ptr) + G.base);
           QTNH_LAUNCH_CHECK();
           if (uc == 32)
             k_svd_update_mma_t<B, 32><<<dim3(ctiles, npairs, cnt), B * 8, upd_smem, G.s>>>(
@@ -891,6 +924,10 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
       for (auto& G : grp) {
         if (G.done) continue;
         QTNH_CUDA(cudaStreamSynchronize(G.s));
+        for (Dim b = G.base; b < G.base + G.cnt; ++b) {
+          off_hist[b * 2 + 1] = off_hist[b * 2];
+          off_hist[b * 2] = off_h[b];
+        }
         const double mx = *std::max_element(off_h.begin() + G.base, off_h.begin() + G.base + G.cnt);
         if (std::getenv("QTNH_SVD_DEBUG")) std::fprintf(stderr, "svd sweep %d group %d max_off %.3e\n", sweep,
                                                        static_cast<int>(&G - grp.data()), mx);

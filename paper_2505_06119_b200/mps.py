@@ -12,6 +12,7 @@ plus zeros, so amplitudes and fidelities are identical.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import List, Sequence, Tuple
 
 import numpy as np
@@ -111,6 +112,9 @@ class MPS:
             for i, (q, th) in enumerate(items):
                 src = torch.as_tensor(_DevView(th.device_ptr(), m * n), device=dev)
                 a[i].view(-1).copy_(src)
+            dump = os.environ.get("QTNH_MPS_DUMP")  # debugging aid: save one saturated theta
+            if dump and m == n == 2 * self.chi and not os.path.exists(dump):
+                np.save(dump, a[0].cpu().numpy())
             u = torch.empty((bsz, m, k), dtype=torch.complex128, device=dev)
             s = torch.empty((bsz, k), dtype=torch.float64, device=dev)
             vh = torch.empty((bsz, k, n), dtype=torch.complex128, device=dev)

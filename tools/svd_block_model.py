@@ -3,14 +3,14 @@ tournament over 16-row blocks, one parallel inner sweep on each pair's 32 x 32
 Gram, W^H applied to the pair's rows), used to tell algorithmic sweep counts from
 kernel effects (item 1). Slow (pure Python loops): n <= 256.
 
-  python tools/svd_block_model.py [n] [graded_decades] [--pair-sort]
+  python tools/svd_block_model.py [n] [graded_decades] [--pair-sort] [--adapt]
 """
 import sys
 
 import numpy as np
 
 
-def inner_sweep(G, B):
+def inner_sweep(G, B, thr=0.0):
     """One parallel cyclic Jacobi sweep on the Hermitian 2B x 2B G; returns V."""
     P2 = 2 * B
     G = G.copy()
@@ -27,7 +27,7 @@ def inner_sweep(G, B):
             a, b, x = G[p, p].real, G[q, q].real, G[p, q]
             r2 = abs(x) ** 2
             c, s, ph = 1.0, 0.0, 1.0
-            if r2 > 0 and not (r2 <= 1e-34 * abs(a * b)):
+            if r2 > 0 and not (r2 <= max(1e-34, thr * thr) * abs(a * b)):
                 inv = 1 / np.sqrt(r2)
                 ph = np.conj(x) * inv
                 tau = 0.5 * (b - a) * inv
@@ -48,7 +48,7 @@ def off(X):
     return R.max()
 
 
-def run(A, B=16, max_sweeps=60, tol=1e-13, pair_sort=False):
+def run(A, B=16, max_sweeps=60, tol=1e-13, pair_sort=False, adapt=None):
     X = A.copy()
     nblk2 = X.shape[0] // B
     npairs, rounds = nblk2 // 2, nblk2 - 1
@@ -63,7 +63,7 @@ def run(A, B=16, max_sweeps=60, tol=1e-13, pair_sort=False):
                 idx = np.r_[p * B:(p + 1) * B, q * B:(q + 1) * B]
                 Xp = X[idx]
                 G = Xp @ Xp.conj().T
-                V = inner_sweep(G, B)
+                V = inner_sweep(G, B, adapt(hist[-1]) if (adapt and sw > 0) else 0.0)
                 if pair_sort:
                     d = np.real(np.diag(V.conj().T @ G @ V))
                     order = np.argsort(-d) if p < q else np.argsort(d)
@@ -83,5 +83,7 @@ if __name__ == "__main__":
         A = (q1 * np.logspace(0, -dec, n)) @ q2.conj().T
     else:
         A = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
-    sw, hist = run(A, pair_sort="--pair-sort" in sys.argv)
+    # rotation threshold from the previous off-norm: skip |G_pq| < thr sqrt(G_pp G_qq)
+    adapt = (lambda o: 0.1 * o * o) if "--adapt" in sys.argv else None
+    sw, hist = run(A, pair_sort="--pair-sort" in sys.argv, adapt=adapt)
     print("sweeps", sw, " ".join("%.1e" % h for h in hist))
