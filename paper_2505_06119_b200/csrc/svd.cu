@@ -105,8 +105,9 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
   const int pair = blockIdx.x, mat = blockIdx.y, tid = threadIdx.x;
   const double fl = floor_abs[mat];
   extern __shared__ double2 esm[];
-  double2* G = esm;            // [P2][LD]
-  double2* V = esm + P2 * LD;  // [P2][LD]
+  double2* G = esm;                // [P2][LD], current Gram (ping-pong with G2 in the sweeps)
+  double2* V = esm + P2 * LD;      // [P2][LD]
+  double2* G2 = esm + 2 * P2 * LD;  // [P2][LD]
   __shared__ double rot_c[B], rot_s[B];
   __shared__ double2 rot_ph[B];
   __shared__ int rp_[B], rq_[B];
@@ -193,72 +194,163 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
     if (tid == 0) flags[fidx] = 0;
     return;
   }
-  for (int sw = 0; sw < inner_sweeps; ++sw) {
-    for (int step = 0; step < P2 - 1; ++step) {
-      if (tid < B) {
-        int p, q;
-        if (tid == 0) {
-          p = step;
-          q = P2 - 1;
-        } else {
-          p = (step + tid) % (P2 - 1);
-          q = (step - tid + (P2 - 1)) % (P2 - 1);
-        }
-        if (p > q) {
-          int tt = p;
-          p = q;
-          q = tt;
-        }
-        // one reciprocal square root instead of hypot and three divisions: these
-        // 16 threads are the critical path of every step (the rest wait at the barrier)
-        double a = G[p * LD + p].x, b = G[q * LD + q].x;
-        double2 x = G[p * LD + q];
-        const double r2 = fma(x.x, x.x, x.y * x.y);
-        double c = 1.0, sn = 0.0;
-        double2 ph = make_double2(1.0, 0.0);
-        if (r2 > 1e-600 && !(r2 <= rot_thr2 * fabs(a * b))) {
-          const double inv_ax = rsqrt(r2);
-          ph = make_double2(x.x * inv_ax, -x.y * inv_ax);
-          const double tau = 0.5 * (b - a) * inv_ax;
-          const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
-          c = rsqrt(fma(t, t, 1.0));
-          sn = t * c;
-        }
-        rot_c[tid] = c;
-        rot_s[tid] = sn;
-        rot_ph[tid] = ph;
-        rp_[tid] = p;
-        rq_[tid] = q;
+  if constexpr (B == 16) {
+    // One barrier per step: G is double-buffered (read Gc, write Gn), and every warp
+    // computes the step's 16 rotations itself (lane r & 15 -> rotation r & 15) and
+    // hands each thread the parameters it needs by shuffles, so the step no longer
+    // waits for 16 threads to publish them behind a second barrier.
+    double2* Gc = G;
+    double2* Gn = G2;
+    const int lane = tid & 31;
+    auto pair_of = [&](int step, int r, int& p, int& q) {
+      if (r == 0) {
+        p = step;
+        q = P2 - 1;
+      } else {
+        p = (step + r) % (P2 - 1);
+        q = (step - r + (P2 - 1)) % (P2 - 1);
       }
-      __syncthreads();
-      for (int task = tid; task < B * B; task += 256) {
-        const int k = task / B, l = task % B;
-        const int pk = rp_[k], qk = rq_[k], pl = rp_[l], ql = rq_[l];
-        const double ck = rot_c[k], sk = rot_s[k], cl = rot_c[l], sl = rot_s[l];
-        const double2 ek = cconj(rot_ph[k]), el = rot_ph[l];
-        double2 a = G[pk * LD + pl], b = G[pk * LD + ql], c = G[qk * LD + pl], d = G[qk * LD + ql];
-        double2 bq = cmul(b, el), dq = cmul(d, el);
-        double2 a1 = make_double2(cl * a.x - sl * bq.x, cl * a.y - sl * bq.y);
-        double2 b1 = make_double2(sl * a.x + cl * bq.x, sl * a.y + cl * bq.y);
-        double2 c1 = make_double2(cl * c.x - sl * dq.x, cl * c.y - sl * dq.y);
-        double2 d1 = make_double2(sl * c.x + cl * dq.x, sl * c.y + cl * dq.y);
-        double2 c2 = cmul(c1, ek), d2 = cmul(d1, ek);
-        G[pk * LD + pl] = make_double2(ck * a1.x - sk * c2.x, ck * a1.y - sk * c2.y);
-        G[pk * LD + ql] = make_double2(ck * b1.x - sk * d2.x, ck * b1.y - sk * d2.y);
-        G[qk * LD + pl] = make_double2(sk * a1.x + ck * c2.x, sk * a1.y + ck * c2.y);
-        G[qk * LD + ql] = make_double2(sk * b1.x + ck * d2.x, sk * b1.y + ck * d2.y);
+      if (p > q) {
+        const int tt = p;
+        p = q;
+        q = tt;
       }
-      for (int task = tid; task < P2 * B; task += 256) {
-        const int i = task % P2, kk = task / P2;
-        const int p = rp_[kk], q = rq_[kk];
-        const double cc = rot_c[kk], ss = rot_s[kk];
-        double2 vp = V[i * LD + p], vq = cmul(V[i * LD + q], rot_ph[kk]);
-        V[i * LD + p] = make_double2(cc * vp.x - ss * vq.x, cc * vp.y - ss * vq.y);
-        V[i * LD + q] = make_double2(ss * vp.x + cc * vq.x, ss * vp.y + cc * vq.y);
+    };
+    for (int sw = 0; sw < inner_sweeps; ++sw) {
+      for (int step = 0; step < P2 - 1; ++step) {
+        double c = 1.0, sn = 0.0, phx = 1.0, phy = 0.0;
+        {
+          int p, q;
+          pair_of(step, lane & 15, p, q);
+          const double a = Gc[p * LD + p].x, b = Gc[q * LD + q].x;
+          const double2 x = Gc[p * LD + q];
+          const double r2 = fma(x.x, x.x, x.y * x.y);
+          if (r2 > 1e-600 && !(r2 <= rot_thr2 * fabs(a * b))) {
+            const double inv_ax = rsqrt(r2);
+            phx = x.x * inv_ax;
+            phy = -x.y * inv_ax;
+            const double tau = 0.5 * (b - a) * inv_ax;
+            const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
+            c = rsqrt(fma(t, t, 1.0));
+            sn = t * c;
+          }
+        }
+        auto rot = [&](int r, double& rc, double& rs, double2& rph) {
+          rc = __shfl_sync(0xffffffffu, c, r);
+          rs = __shfl_sync(0xffffffffu, sn, r);
+          rph = make_double2(__shfl_sync(0xffffffffu, phx, r), __shfl_sync(0xffffffffu, phy, r));
+        };
+        {  // G task (k, l): the 2 x 2 blocks of rows (pk, qk) x columns (pl, ql), Gc -> Gn
+          const int k = tid / B, l = tid % B;
+          int pk, qk, pl, ql;
+          pair_of(step, k, pk, qk);
+          pair_of(step, l, pl, ql);
+          double ck, sk, cl, sl;
+          double2 phk, phl;
+          rot(k, ck, sk, phk);
+          rot(l, cl, sl, phl);
+          const double2 ek = cconj(phk), el = phl;
+          double2 a = Gc[pk * LD + pl], b = Gc[pk * LD + ql], cc = Gc[qk * LD + pl], d = Gc[qk * LD + ql];
+          double2 bq = cmul(b, el), dq = cmul(d, el);
+          double2 a1 = make_double2(cl * a.x - sl * bq.x, cl * a.y - sl * bq.y);
+          double2 b1 = make_double2(sl * a.x + cl * bq.x, sl * a.y + cl * bq.y);
+          double2 c1 = make_double2(cl * cc.x - sl * dq.x, cl * cc.y - sl * dq.y);
+          double2 d1 = make_double2(sl * cc.x + cl * dq.x, sl * cc.y + cl * dq.y);
+          double2 c2 = cmul(c1, ek), d2 = cmul(d1, ek);
+          Gn[pk * LD + pl] = make_double2(ck * a1.x - sk * c2.x, ck * a1.y - sk * c2.y);
+          Gn[pk * LD + ql] = make_double2(ck * b1.x - sk * d2.x, ck * b1.y - sk * d2.y);
+          Gn[qk * LD + pl] = make_double2(sk * a1.x + ck * c2.x, sk * a1.y + ck * c2.y);
+          Gn[qk * LD + ql] = make_double2(sk * b1.x + ck * d2.x, sk * b1.y + ck * d2.y);
+        }
+  #pragma unroll
+        for (int h = 0; h < 2; ++h) {  // V tasks (i, kk): columns p, q of rotation kk, in place
+          const int task = tid + h * 256, i = task % P2, kk = task / P2;
+          int p, q;
+          pair_of(step, kk, p, q);
+          double cc, ss;
+          double2 ph;
+          rot(kk, cc, ss, ph);
+          double2 vp = V[i * LD + p], vq = cmul(V[i * LD + q], ph);
+          V[i * LD + p] = make_double2(cc * vp.x - ss * vq.x, cc * vp.y - ss * vq.y);
+          V[i * LD + q] = make_double2(ss * vp.x + cc * vq.x, ss * vp.y + cc * vq.y);
+        }
+        __syncthreads();
+        double2* t = Gc;
+        Gc = Gn;
+        Gn = t;
       }
-      __syncthreads();
+      G = Gc;
+      if (sw + 1 < inner_sweeps && measure() < tol * 1e-2) break;
     }
-    if (sw + 1 < inner_sweeps && measure() < tol * 1e-2) break;
+    G = Gc;
+  } else {  // 32-row blocks (QTNH_SVD_B=32): two barriers per step, parameters in shared memory
+    for (int sw = 0; sw < inner_sweeps; ++sw) {
+      for (int step = 0; step < P2 - 1; ++step) {
+        if (tid < B) {
+          int p, q;
+          if (tid == 0) {
+            p = step;
+            q = P2 - 1;
+          } else {
+            p = (step + tid) % (P2 - 1);
+            q = (step - tid + (P2 - 1)) % (P2 - 1);
+          }
+          if (p > q) {
+            int tt = p;
+            p = q;
+            q = tt;
+          }
+          // one reciprocal square root instead of hypot and three divisions: these
+          // 16 threads are the critical path of every step (the rest wait at the barrier)
+          double a = G[p * LD + p].x, b = G[q * LD + q].x;
+          double2 x = G[p * LD + q];
+          const double r2 = fma(x.x, x.x, x.y * x.y);
+          double c = 1.0, sn = 0.0;
+          double2 ph = make_double2(1.0, 0.0);
+          if (r2 > 1e-600 && !(r2 <= rot_thr2 * fabs(a * b))) {
+            const double inv_ax = rsqrt(r2);
+            ph = make_double2(x.x * inv_ax, -x.y * inv_ax);
+            const double tau = 0.5 * (b - a) * inv_ax;
+            const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
+            c = rsqrt(fma(t, t, 1.0));
+            sn = t * c;
+          }
+          rot_c[tid] = c;
+          rot_s[tid] = sn;
+          rot_ph[tid] = ph;
+          rp_[tid] = p;
+          rq_[tid] = q;
+        }
+        __syncthreads();
+        for (int task = tid; task < B * B; task += 256) {
+          const int k = task / B, l = task % B;
+          const int pk = rp_[k], qk = rq_[k], pl = rp_[l], ql = rq_[l];
+          const double ck = rot_c[k], sk = rot_s[k], cl = rot_c[l], sl = rot_s[l];
+          const double2 ek = cconj(rot_ph[k]), el = rot_ph[l];
+          double2 a = G[pk * LD + pl], b = G[pk * LD + ql], c = G[qk * LD + pl], d = G[qk * LD + ql];
+          double2 bq = cmul(b, el), dq = cmul(d, el);
+          double2 a1 = make_double2(cl * a.x - sl * bq.x, cl * a.y - sl * bq.y);
+          double2 b1 = make_double2(sl * a.x + cl * bq.x, sl * a.y + cl * bq.y);
+          double2 c1 = make_double2(cl * c.x - sl * dq.x, cl * c.y - sl * dq.y);
+          double2 d1 = make_double2(sl * c.x + cl * dq.x, sl * c.y + cl * dq.y);
+          double2 c2 = cmul(c1, ek), d2 = cmul(d1, ek);
+          G[pk * LD + pl] = make_double2(ck * a1.x - sk * c2.x, ck * a1.y - sk * c2.y);
+          G[pk * LD + ql] = make_double2(ck * b1.x - sk * d2.x, ck * b1.y - sk * d2.y);
+          G[qk * LD + pl] = make_double2(sk * a1.x + ck * c2.x, sk * a1.y + ck * c2.y);
+          G[qk * LD + ql] = make_double2(sk * b1.x + ck * d2.x, sk * b1.y + ck * d2.y);
+        }
+        for (int task = tid; task < P2 * B; task += 256) {
+          const int i = task % P2, kk = task / P2;
+          const int p = rp_[kk], q = rq_[kk];
+          const double cc = rot_c[kk], ss = rot_s[kk];
+          double2 vp = V[i * LD + p], vq = cmul(V[i * LD + q], rot_ph[kk]);
+          V[i * LD + p] = make_double2(cc * vp.x - ss * vq.x, cc * vp.y - ss * vq.y);
+          V[i * LD + q] = make_double2(ss * vp.x + cc * vq.x, ss * vp.y + cc * vq.y);
+        }
+        __syncthreads();
+      }
+      if (sw + 1 < inner_sweeps && measure() < tol * 1e-2) break;
+    }
   }
   // Order the pair's new rows by norm (the diagonal of W^H G W), the larger half to
   // the lower-numbered block: big rows drift to the front blocks sweep by sweep
@@ -758,7 +850,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   k_svd_fro<<<dim3(64, static_cast<unsigned>(batch)), 256, 0, st>>>(static_cast<const double2*>(a), m * n,
                                                                    static_cast<double*>(floor_abs.ptr), floor_rel());
   QTNH_LAUNCH_CHECK();
-  const size_t eig_smem = static_cast<size_t>(2) * P2 * (P2 + 1) * 16;
+  const size_t eig_smem = static_cast<size_t>(3) * P2 * (P2 + 1) * 16;
   static const int uc = [] {
     const char* e = std::getenv("QTNH_SVD_UC");
     int v = e ? std::atoi(e) : 64;  // 64: steadiest batched timings (48 / 32 varied by 15-25 % run to run)
