@@ -16,6 +16,9 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <mutex>
+#include <vector>
+
 #include "ops.h"
 
 namespace qtnhb {
@@ -756,6 +759,101 @@ __global__ void __launch_bounds__(256, (G >= 4 ? 1 : 2)) k_qft_group(double2* __
   }
 }
 
+// ---- shared-memory group pass: G1 + G2 consecutive layers on strided bits ---------------
+// Bits B .. B+G1+G2-1 (B >= 4) in one pass: a CTA owns a tile of 2^(G1+G2) group
+// values x W = 16 consecutive low elements (256-byte rows, 64 KB at 8 bits), staged
+// in shared memory; the upper G1 layers run in registers with the lower G2 group
+// bits fixed per thread, then the lower G2 layers with the upper ones fixed. The
+// phase of layer t = B + u splits into e^{i pi x / 2^u} (x = the group bits below
+// u, table kQftMidTw) times e^{i pi lo / 2^(B+u)} (lo = the fixed low bits, one
+// sincospi per (u, column) per tile). 8 layers per pass instead of 4: QFT-33 takes
+// 3 + low + bit reversal = 5 passes over the state instead of 8.
+constexpr int kMidW = 16;
+__constant__ double2 kQftMidTw[256];  // e^{i pi x / 2^u} at index 2^u - 1 + x, u < 8
+
+template <int G1, int G2>
+__global__ void __launch_bounds__(256, 2) k_qft_mid(double2* __restrict__ psi, int64_t n_tiles, int B) {
+  constexpr int GB = G1 + G2, NG = 1 << GB, NE = NG * kMidW;
+  static_assert((1 << G1) * kMidW == 256 || (1 << G2) * kMidW <= 256, "fibers per round fit the block");
+  extern __shared__ double2 smid[];
+  double2* data = smid;              // [NG][kMidW]
+  double2* lofs = smid + NE;         // [GB][kMidW]
+  const int tid = threadIdx.x;
+  const double r = 0.70710678118654752440;
+  const int64_t lo_blocks = (int64_t(1) << B) / kMidW;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t hi = tile / lo_blocks, lo0 = (tile % lo_blocks) * kMidW;
+    double2* g0 = psi + (hi << (B + GB)) + lo0;
+    for (int e = tid; e < NE; e += 256) {
+      const int g = e / kMidW, w = e % kMidW;
+      cp_async16(data + e, g0 + (int64_t(g) << B) + w);
+    }
+    cp_async_commit();
+    for (int e = tid; e < GB * kMidW; e += 256) {
+      const int u = e / kMidW, w = e % kMidW;
+      double sn, cs;
+      sincospi(static_cast<double>(lo0 + w) * ldexp(1.0, -(B + u)), &sn, &cs);
+      lofs[e] = make_double2(cs, sn);
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    // round 1: upper G1 group bits (layers u = GB-1 .. G2), lower G2 bits fixed
+    for (int f = tid; f < (1 << G2) * kMidW; f += 256) {
+      const int w = f % kMidW, j = f / kMidW;
+      double2 x[1 << G1];
+#pragma unroll
+      for (int k = 0; k < (1 << G1); ++k) x[k] = data[((k << G2) | j) * kMidW + w];
+#pragma unroll
+      for (int s = G1 - 1; s >= 0; --s) {
+        const int u = G2 + s;
+        const double2 lf = lofs[u * kMidW + w];
+#pragma unroll
+        for (int k = 0; k < (1 << G1); ++k) {
+          if (k & (1 << s)) continue;
+          const int k1 = k | (1 << s);
+          const double2 a0 = x[k], a1 = x[k1];
+          x[k] = make_double2(r * a0.x + r * a1.x, r * a0.y + r * a1.y);
+          const double2 d = make_double2(r * a0.x - r * a1.x, r * a0.y - r * a1.y);
+          const int xg = ((k & ((1 << s) - 1)) << G2) | j;  // group bits below u
+          x[k1] = cmul2(d, cmul2(kQftMidTw[(1 << u) - 1 + xg], lf));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < (1 << G1); ++k) data[((k << G2) | j) * kMidW + w] = x[k];
+    }
+    __syncthreads();
+    // round 2: lower G2 group bits (layers u = G2-1 .. 0), upper G1 bits fixed
+    for (int f = tid; f < (1 << G1) * kMidW; f += 256) {
+      const int w = f % kMidW, i = f / kMidW;
+      double2 x[1 << G2];
+#pragma unroll
+      for (int k = 0; k < (1 << G2); ++k) x[k] = data[((i << G2) | k) * kMidW + w];
+#pragma unroll
+      for (int u = G2 - 1; u >= 0; --u) {
+        const double2 lf = lofs[u * kMidW + w];
+#pragma unroll
+        for (int k = 0; k < (1 << G2); ++k) {
+          if (k & (1 << u)) continue;
+          const int k1 = k | (1 << u);
+          const double2 a0 = x[k], a1 = x[k1];
+          x[k] = make_double2(r * a0.x + r * a1.x, r * a0.y + r * a1.y);
+          const double2 d = make_double2(r * a0.x - r * a1.x, r * a0.y - r * a1.y);
+          const int xg = k & ((1 << u) - 1);
+          x[k1] = cmul2(d, u > 0 ? cmul2(kQftMidTw[(1 << u) - 1 + xg], lf) : lf);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < (1 << G2); ++k) data[((i << G2) | k) * kMidW + w] = x[k];
+    }
+    __syncthreads();
+    for (int e = tid; e < NE; e += 256) {
+      const int g = e / kMidW, w = e % kMidW;
+      g0[(int64_t(g) << B) + w] = data[e];
+    }
+    __syncthreads();  // the tile buffer is reused by the next tile
+  }
+}
+
 __device__ __forceinline__ unsigned rev_bits(unsigned x, int bits) { return __brev(x) >> (32 - bits); }
 __device__ __forceinline__ uint64_t rev_bits64(uint64_t x, int bits) { return __brevll(x) >> (64 - bits); }
 
@@ -1022,13 +1120,65 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
   // a 2-round low pass, instead of L = 11 -> 4 + 1 passes and 3 rounds).
   int top = first_layer_bit;
   const int layers = top + 1, gmax = qft_group_max();
+  static const bool mid_on = [] {
+    const char* e = std::getenv("QTNH_QFT_MID");
+    return !(e && e[0] == '0');
+  }();
+  // passes over the state for R upper layers: shared-memory 6-8-layer passes
+  // while at least 6 remain (their lowest bit must be >= 4), register groups after
+  auto upper_passes = [&](int l) {
+    int R = layers - l, n = 0;
+    while (R > 0) {
+      R -= (mid_on && R >= 6 && l >= 4) ? std::min(R, 8) : std::min(R, gmax);
+      ++n;
+    }
+    return n;
+  };
   int L = std::min(layers, lmax);
   {
-    auto key = [&](int l) { return std::make_pair((layers - l + gmax - 1) / gmax, (l + 3) / 4); };
+    auto key = [&](int l) { return std::make_pair(upper_passes(l), (l + 3) / 4); };
     for (int l = std::min(layers, lmax); l >= 1; --l)
       if (key(l) < key(L)) L = l;
   }
+  if (mid_on && layers - L >= 6) {
+    int dev = 0;
+    QTNH_CUDA(cudaGetDevice(&dev));
+    static std::mutex mu;
+    static std::vector<char> ready(64, 0);
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 64 && !ready[dev]) {
+      double2 tw[256] = {};
+      for (int u = 0; u < 8; ++u)
+        for (int x = 0; x < (1 << u); ++x) {
+          const double ang = M_PI * x / std::ldexp(1.0, u);
+          tw[(1 << u) - 1 + x] = make_double2(std::cos(ang), std::sin(ang));
+        }
+      QTNH_CUDA(cudaMemcpyToSymbol(kQftMidTw, tw, sizeof(tw)));
+      ready[dev] = 1;
+    }
+  }
   while (top >= L) {
+    const int R = top - L + 1;
+    if (mid_on && R >= 6 && L >= 4) {
+      const int gb = std::min(R, 8), B = top - gb + 1;
+      const int64_t n_tiles = int64_t(1) << (nb - gb - 4);
+      const size_t smem = ((size_t(1) << gb) * kMidW + size_t(gb) * kMidW) * sizeof(double2);
+      static bool attr = [] {
+        const int mx = (256 * kMidW + 8 * kMidW) * 16;
+        cudaFuncSetAttribute(k_qft_mid<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_qft_mid<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_qft_mid<3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        return true;
+      }();
+      (void)attr;
+      const int grid = static_cast<int>(std::min<int64_t>(n_tiles, int64_t(148) * 2));
+      if (gb == 8) k_qft_mid<4, 4><<<grid, 256, smem, st>>>(p, n_tiles, B);
+      else if (gb == 7) k_qft_mid<4, 3><<<grid, 256, smem, st>>>(p, n_tiles, B);
+      else k_qft_mid<3, 3><<<grid, 256, smem, st>>>(p, n_tiles, B);
+      QTNH_LAUNCH_CHECK();
+      top = B - 1;
+      continue;
+    }
     int g = std::min(qft_group_max(), top - L + 1);  // 5 spills at 255 registers
     int B = top - g + 1;
     QftGroupArgs ga{};
