@@ -551,6 +551,95 @@ __global__ void __launch_bounds__(B * 8) k_svd_update_mma_t(double2* __restrict_
   }
 }
 
+// Update, v2 (16-row blocks): the pair's W^H fragments are loaded once into
+// registers (Gauss planes re, im, re + im for the 8 k4 steps of K = 32), and
+// 32-column tiles of X stream through a 3-stage cp.async ring (48 KB of shared
+// memory instead of 86 KB: 4 CTAs per SM instead of 2). The v1 kernel ran at
+// ~50 % of both the DMMA and the HBM bound in the batched C4 SVDs.
+template <int B>
+__global__ void __launch_bounds__(B * 8, 4) k_svd_update_v2(double2* __restrict__ wk, const double2* __restrict__ wh,
+                                                           const int* __restrict__ flags,
+                                                           const int* __restrict__ tab, int round, int npairs,
+                                                           int64_t rp, int64_t L, int64_t qw) {
+  static_assert(B == 16, "v2 update: 16-row blocks");
+  constexpr int P2 = 2 * B, T = B * 8, UC = 32, NT = UC / 8, PX = UC + 2, ST = 3, KS = P2 / 4;
+  const int pair = blockIdx.y, mat = blockIdx.z, tid = threadIdx.x;
+  const int64_t fidx = static_cast<int64_t>(mat) * npairs + pair;
+  if (!flags[fidx]) return;
+  const int64_t W = L + qw;
+  const int* pr = tab + (static_cast<int64_t>(round) * npairs + pair) * 2;
+  const int bi = pr[0], bj = pr[1];
+  double2* K = wk + static_cast<int64_t>(mat) * rp * W;
+  extern __shared__ double2 usm2[];  // [ST][P2][PX]
+  const int lane = tid & 31, warp = tid >> 5, fr = lane >> 2, fk = lane & 3;
+  // W^H rows warp*8 + fr, columns k4 + fk: the A fragments of all k4 steps
+  const double2* Wh = wh + fidx * P2 * P2 + (warp * 8 + fr) * P2 + fk;
+  double a_re[KS], a_im[KS], a_s[KS];
+#pragma unroll
+  for (int q = 0; q < KS; ++q) {
+    const double2 v = Wh[q * 4];
+    a_re[q] = v.x;
+    a_im[q] = v.y;
+    a_s[q] = v.x + v.y;
+  }
+  const int64_t step = static_cast<int64_t>(gridDim.x) * UC;
+  auto issue = [&](int buf, int64_t cb) {
+    double2* xs = usm2 + buf * P2 * PX;
+#pragma unroll
+    for (int e = tid; e < P2 * UC; e += T) {
+      const int r = e / UC, c = e % UC;
+      const int64_t row = r < B ? bi * B + r : bj * B + (r - B);
+      const int64_t col = cb + c;
+      const bool ok = col < W;
+      cp_async16z(xs + r * PX + c, ok ? K + row * W + col : K, ok);
+    }
+  };
+  const int64_t cb0 = static_cast<int64_t>(blockIdx.x) * UC;
+#pragma unroll
+  for (int s = 0; s < ST - 1; ++s) {
+    if (cb0 + s * step < W) issue(s, cb0 + s * step);
+    cp_async_commit_();
+  }
+  int buf = 0;
+  for (int64_t cb = cb0; cb < W; cb += step) {
+    {
+      const int64_t nb = cb + (ST - 1) * step;
+      if (nb < W) issue((buf + ST - 1) % ST, nb);
+      cp_async_commit_();
+    }
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(ST - 1));
+    __syncthreads();
+    const double2* xs = usm2 + buf * P2 * PX;
+    double acc_re[NT][2], acc_im[NT][2], acc_s[NT][2];
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+      acc_re[j][0] = acc_re[j][1] = acc_im[j][0] = acc_im[j][1] = acc_s[j][0] = acc_s[j][1] = 0.0;
+#pragma unroll
+    for (int q = 0; q < KS; ++q) {
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const double2 bv = xs[(q * 4 + fk) * PX + j * 8 + fr];
+        dmma(acc_re[j], a_re[q], bv.x);
+        dmma(acc_im[j], a_im[q], bv.y);
+        dmma(acc_s[j], a_s[q], bv.x + bv.y);
+      }
+    }
+    const int r = warp * 8 + fr;
+    const int64_t row = r < B ? bi * B + r : bj * B + (r - B);
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int64_t col = cb + j * 8 + 2 * fk;
+      if (col < W)
+        K[row * W + col] = make_double2(acc_re[j][0] - acc_im[j][0], acc_s[j][0] - acc_re[j][0] - acc_im[j][0]);
+      if (col + 1 < W)
+        K[row * W + col + 1] =
+            make_double2(acc_re[j][1] - acc_im[j][1], acc_s[j][1] - acc_re[j][1] - acc_im[j][1]);
+    }
+    __syncthreads();  // this slot is refilled ST - 1 tiles on
+    buf = (buf + 1) % ST;
+  }
+}
+
 // ---- ||A||_F^2 per matrix -> the absolute convergence floor ------------------------------
 __global__ void k_svd_fro(const double2* __restrict__ a, int64_t count, double* __restrict__ out, double rel) {
   const int64_t mat = blockIdx.y;
@@ -857,6 +946,13 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
     return v == 32 || v == 48 ? v : 64;
   }();
   const size_t upd_smem = static_cast<size_t>(P2) * ((P2 + 4) + 2 * (uc + 2)) * 16;
+  static const bool upd2 = [] {
+    const char* e = std::getenv("QTNH_SVD_UPD2");
+    return !(e && e[0] == '0');
+  }();
+  const size_t upd2_smem = static_cast<size_t>(3) * P2 * (32 + 2) * 16;
+  if constexpr (B == 16)
+    QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_v2<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd2_smem));
   const size_t gram_smem = static_cast<size_t>(2) * P2 * ((B >= 32 ? 32 : 64) + 4) * 16;
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_eigen_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_smem));
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
@@ -900,6 +996,8 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   const Dim gmax = (batch + ngroups - 1) / ngroups;
   const unsigned ctiles = static_cast<unsigned>(
       std::min<Dim>((W + uc - 1) / uc, std::max<Dim>(1, (B == 16 ? 8 : 4) * sms() / (npairs * gmax))));
+  const unsigned ctiles2 =
+      static_cast<unsigned>(std::min<Dim>((W + 31) / 32, std::max<Dim>(1, 8 * sms() / (npairs * gmax))));
   auto cleanup = [&] {
     for (int g = 0; g < ngroups; ++g) {
       if (ngroups > 1) {
@@ -997,6 +1095,14 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
               static_cast<const int*>(d_tab.ptr), rd, static_cast<int>(nblk2), sort_pair ? 1 : 0,
               static_cast<const double*>(offp.ptr) + G.base);
           QTNH_LAUNCH_CHECK();
+          if constexpr (B == 16) {
+            if (upd2) {
+              k_svd_update_v2<B><<<dim3(ctiles2, npairs, cnt), B * 8, upd2_smem, G.s>>>(
+                  wkg, whg, flg, static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
+              QTNH_LAUNCH_CHECK();
+              continue;
+            }
+          }
           if (uc == 32)
             k_svd_update_mma_t<B, 32><<<dim3(ctiles, npairs, cnt), B * 8, upd_smem, G.s>>>(
                 wkg, whg, flg, static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
