@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(CROSS ? B * 4 : B * 8) k_svd_gram_mma_t(const 
                                                                            const int* __restrict__ tab, int round,
                                                                            int npairs, int splits, int64_t rp,
                                                                            int64_t L, int64_t qw) {
-  constexpr int P2 = 2 * B, NT = CROSS ? B / 8 : P2 / 8, T = CROSS ? B * 4 : B * 8, GK = B >= 32 ? 32 : 64,
+  constexpr int P2 = 2 * B, NT = CROSS ? B / 8 : P2 / 8, T = CROSS ? B * 4 : B * 8, GK = (B >= 32 || CROSS) ? 32 : 64,
                 PX = GK + 4, OC = CROSS ? B : P2, C0 = CROSS ? B : 0;
   const int pair = blockIdx.x, split = blockIdx.y, mat = blockIdx.z;
   const int64_t W = L + qw;
@@ -959,8 +959,11 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_gram_mma_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem));
+  // cross Grams: 32-column chunks (37 KB, 6 CTAs/SM instead of 3 -- the kernel is
+  // HBM-bound: a quarter of the DMMAs of the full Gram for the same bytes)
+  const size_t gramx_smem = static_cast<size_t>(2) * P2 * (32 + 4) * 16;
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_gram_mma_t<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)gram_smem));
+                                 (int)gramx_smem));
   // The batch runs as two independent halves on two streams when it has >= 2
   // matrices: the latency-bound eigen step of one half overlaps the other half's
   // Gram / update DMMA work, and a half that converges stops early.
@@ -1082,7 +1085,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
           double2* whg = static_cast<double2*>(whb.ptr) + G.base * npairs * P2 * P2;
           int* flg = static_cast<int*>(flags.ptr) + G.base * npairs;
           if (G.cross)
-            k_svd_gram_mma_t<B, true><<<dim3(npairs, splits, cnt), B * 4, gram_smem, G.s>>>(
+            k_svd_gram_mma_t<B, true><<<dim3(npairs, splits, cnt), B * 4, gramx_smem, G.s>>>(
                 wkg, partg, static_cast<const int*>(d_tab.ptr), rd, npairs, splits, rp, L, qw);
           else
             k_svd_gram_mma_t<B><<<dim3(npairs, splits, cnt), B * 8, gram_smem, G.s>>>(
