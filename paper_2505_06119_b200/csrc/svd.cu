@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(CROSS ? B * 4 : B * 8) k_svd_gram_mma_t(const 
                                                                            const int* __restrict__ tab, int round,
                                                                            int npairs, int splits, int64_t rp,
                                                                            int64_t L, int64_t qw) {
-  constexpr int P2 = 2 * B, NT = CROSS ? B / 8 : P2 / 8, T = CROSS ? B * 4 : B * 8, GK = (B >= 32 || CROSS) ? 32 : 64,
+  constexpr int P2 = 2 * B, NT = CROSS ? B / 8 : P2 / 8, T = CROSS ? B * 4 : B * 8, GK = 32,
                 PX = GK + 4, OC = CROSS ? B : P2, C0 = CROSS ? B : 0;
   const int pair = blockIdx.x, split = blockIdx.y, mat = blockIdx.z;
   const int64_t W = L + qw;
@@ -953,7 +953,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   const size_t upd2_smem = static_cast<size_t>(3) * P2 * (32 + 2) * 16;
   if constexpr (B == 16)
     QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_v2<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd2_smem));
-  const size_t gram_smem = static_cast<size_t>(2) * P2 * ((B >= 32 ? 32 : 64) + 4) * 16;
+  const size_t gram_smem = static_cast<size_t>(2) * P2 * (32 + 4) * 16;
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_eigen_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_smem));
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
