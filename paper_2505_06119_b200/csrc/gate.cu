@@ -17,6 +17,7 @@
 #include <cstring>
 
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "ops.h"
@@ -1126,17 +1127,25 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
   }();
   // passes over the state for R upper layers: shared-memory 6-8-layer passes
   // while at least 6 remain (their lowest bit must be >= 4), register groups after
+  // (passes, shared-memory passes narrower than 8 layers): a 6- or 7-layer tile is
+  // smaller and less efficient (QFT-33: 8 + 8 + 8 over a 9-layer low pass 0.256 s,
+  // 8 + 8 + 6 over an 11-layer one 0.275 s)
   auto upper_passes = [&](int l) {
-    int R = layers - l, n = 0;
+    int R = layers - l, n = 0, narrow = 0;
     while (R > 0) {
-      R -= (mid_on && R >= 6 && l >= 4) ? std::min(R, 8) : std::min(R, gmax);
+      if (mid_on && R >= 6 && l >= 4) {
+        narrow += R < 8 ? 1 : 0;
+        R -= std::min(R, 8);
+      } else {
+        R -= std::min(R, gmax);
+      }
       ++n;
     }
-    return n;
+    return std::make_pair(n, narrow);
   };
   int L = std::min(layers, lmax);
   {
-    auto key = [&](int l) { return std::make_pair(upper_passes(l), (l + 3) / 4); };
+    auto key = [&](int l) { return std::make_tuple(upper_passes(l).first, upper_passes(l).second, (l + 3) / 4); };
     for (int l = std::min(layers, lmax); l >= 1; --l)
       if (key(l) < key(L)) L = l;
   }
