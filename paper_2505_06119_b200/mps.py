@@ -115,18 +115,22 @@ class MPS:
             dump = os.environ.get("QTNH_MPS_DUMP")  # debugging aid: save one saturated theta
             if dump and m == n == 2 * self.chi and not os.path.exists(dump):
                 np.save(dump, a[0].cpu().numpy())
-            u = torch.empty((bsz, m, k), dtype=torch.complex128, device=dev)
-            s = torch.empty((bsz, k), dtype=torch.float64, device=dev)
-            vh = torch.empty((bsz, k, n), dtype=torch.complex128, device=dev)
-            qtnh.check(qtnh.lib.qtnh_svd_device(self.rank._h, bsz, m, n, C.c_void_p(a.data_ptr()), k, ABSORB_LEFT,
+            # Only the kept triplets are formed (the U S = A Vh^H output GEMM and the
+            # output kernels shrink to chi columns); the discarded weight comes from
+            # ||theta||_F^2 = sum of all s^2 (linalg.hpp:476-505 keeps the chi largest).
+            u = torch.empty((bsz, m, keep), dtype=torch.complex128, device=dev)
+            s = torch.empty((bsz, keep), dtype=torch.float64, device=dev)
+            vh = torch.empty((bsz, keep, n), dtype=torch.complex128, device=dev)
+            tot_h = (a.real.square() + a.imag.square()).sum(dim=(1, 2)).cpu().numpy() if keep < k else None
+            qtnh.check(qtnh.lib.qtnh_svd_device(self.rank._h, bsz, m, n, C.c_void_p(a.data_ptr()), keep, ABSORB_LEFT,
                                                 C.c_void_p(u.data_ptr()), C.c_void_p(s.data_ptr()),
                                                 C.c_void_p(vh.data_ptr())))
             s_h = s.cpu().numpy()
             for i, (q, th) in enumerate(items):
                 frac = 1.0
                 if keep < k:
-                    tot = float(np.sum(s_h[i] ** 2))
-                    frac = float(np.sum(s_h[i][:keep] ** 2)) / tot if tot > 0 else 1.0
+                    tot = float(tot_h[i])
+                    frac = float(np.sum(s_h[i] ** 2)) / tot if tot > 0 else 1.0
                     self.log_fidelity += np.log(frac)
                 ui = u[i, :, :keep].contiguous()
                 vi = vh[i, :keep, :].contiguous()
