@@ -232,7 +232,23 @@ def measure_extras(rk, stream, torch):
     ms = e0.elapsed_time(e1)
     ex["svd_2048_chi1024"] = {"ms": ms, "sweeps": int(qtnh.lib.qtnh_last_error_info()),
                               "conv_TFLOPs": 88.0 * nn**3 / (ms * 1e-3) / 1e12,
-                              "flop_convention": "88 n^3 (BASELINE.md section 4)"}
+                              "flop_convention": "88 n^3 (BASELINE.md section 4)",
+                              "note": "one matrix: 64 block pairs per round, the latency-bound eigen step uses 64 SMs"}
+    del a, u, s, vh
+    # the same SVD batched as config 4 runs it (one layer's thetas at once)
+    bt = 8
+    a = torch.from_numpy(rng.standard_normal((bt, nn, nn)) + 1j * rng.standard_normal((bt, nn, nn))).cuda()
+    u = torch.empty((bt, nn, chi), dtype=torch.complex128, device="cuda")
+    s = torch.empty((bt, chi), dtype=torch.float64, device="cuda")
+    vh = torch.empty((bt, chi, nn), dtype=torch.complex128, device="cuda")
+    e0.record(stream)
+    qtnh.check(qtnh.lib.qtnh_svd_device(rk._h, bt, nn, nn, C.c_void_p(a.data_ptr()), chi, 1, C.c_void_p(u.data_ptr()),
+                                        C.c_void_p(s.data_ptr()), C.c_void_p(vh.data_ptr())))
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    ex["svd_2048_chi1024_batch8"] = {"ms_per_svd": ms / bt, "sweeps": int(qtnh.lib.qtnh_last_error_info()),
+                                     "conv_TFLOPs": bt * 88.0 * nn**3 / (ms * 1e-3) / 1e12}
     del a, u, s, vh
     return ex
 
