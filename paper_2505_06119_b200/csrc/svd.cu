@@ -924,7 +924,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   DevBuf offp(static_cast<size_t>(batch) * sizeof(double), r);  // per-matrix rotation threshold
   static const double adapt = [] {
     const char* e = std::getenv("QTNH_SVD_ADAPT");
-    return e ? std::atof(e) : 0.0;
+    return e ? std::atof(e) : 1e-3;
   }();
   QTNH_CUDA(cudaMemsetAsync(offp.ptr, 0, batch * sizeof(double), st));
   DevBuf dblk(cross ? static_cast<size_t>(batch * nblk2) * B * B * 16 : 16, r);
