@@ -210,7 +210,7 @@ def test_swap_indices_bit_exact(dims, split, a, b, world):
     assert np.array_equal(bits(got), bits(P.permute(dims, g, perm)))
 
 
-@pytest.mark.parametrize("n,split,world", [(8, 0, 1), (11, 0, 1), (16, 0, 1), (21, 0, 1), (14, 2, 4), (13, 3, 8),
+@pytest.mark.parametrize("n,split,world", [(8, 0, 1), (11, 0, 1), (16, 0, 1), (20, 0, 1), (21, 0, 1), (14, 2, 4), (13, 3, 8),
                                           (6, 3, 8), (7, 3, 8), (8, 3, 8), (9, 1, 2), (20, 3, 8), (19, 2, 4)])
 def test_blocked_qft(n, split, world, peer_mode):
     """Cache-blocked whole-QFT kernel path (qtnh_qft) against the oracle QFT."""
