@@ -477,6 +477,14 @@ void launch_mode(const double2* a, const int64_t* ro, const int64_t* co, const d
   QTNH_LAUNCH_CHECK();
 }
 
+bool narrow_gauss() {
+  static const bool on = [] {
+    const char* e = std::getenv("QTNH_ZGEMM_NARROW_GAUSS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool even_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("QTNH_ZGEMM_EVEN");
@@ -570,6 +578,10 @@ using G8 = Cfg<64, 64, 2, 2, 8, 4, 2, 32, 32, true>;
 // needs less lead; C1 41.6 vs 41.3 TFLOP/s with 4 stages). A pre-summed B plane
 // (4 instead of 8 DADDs per warp k4 step) spilled at 255 registers and lost 11 %.
 using G9 = Cfg<32, 64, 1, 2, 8, 3, 4, 32, 32, true>;
+// Narrow N (17..32): Gauss tile-aligned 64 x 32 tiles (two 32 x 32 warp tiles along
+// M). The 4M V4 kernel ran C3's big narrow contractions (M = 2^19, N = 32, K = 2^11,
+// at the ridge: 16 flop/B) at 2 TB/s.
+using G10 = Cfg<64, 32, 2, 1, 8, 3, 4, 32, 32, true>;
 
 int variant() {
   static int v = [] {
@@ -629,6 +641,9 @@ void zgemm_gather_a(const void* a, const int64_t* rowoff, const int64_t* coloff,
   } else if (n > 32) {
     if (rows_fastest) launch_mode<G6, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
     else launch_mode<G6, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
+  } else if (n > 16 && even_shape<G10>(m, n, k) && narrow_gauss()) {
+    if (rows_fastest) launch_even<G10, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
+    else launch_even<G10, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
   } else {
     if (rows_fastest) launch_mode<V4, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
     else launch_mode<V4, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
@@ -654,7 +669,8 @@ void zgemm(const void* a, const void* b, void* c, Dim m, Dim n, Dim k, cudaStrea
     default: break;
   }
   const Dim tiles = ((m + 31) / 32) * ((n + 63) / 64);
-  if (n <= 32) launch<V4>(A, B, Cp, m, n, k, st);
+  if (n <= 32 && n > 16 && narrow_gauss() && even_shape<G10>(m, n, k)) launch<G10>(A, B, Cp, m, n, k, st);
+  else if (n <= 32) launch<V4>(A, B, Cp, m, n, k, st);
   else if (tiles < 8192) launch<G22>(A, B, Cp, m, n, k, st);
   else launch<G6>(A, B, Cp, m, n, k, st);
 }
