@@ -891,7 +891,16 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
       tab[(rd * npairs + k) * 2] = p;
       tab[(rd * npairs + k) * 2 + 1] = q;
     }
-  const Dim per_group = batch >= 2 ? (batch + 1) / 2 : batch;  // see the two-stream split below
+  // streams the batch is split over (QTNH_SVD_GROUPS): each group's latency-bound
+  // eigen step overlaps the others' DMMA work; C4 (layer batches of 9-10): 2 groups
+  // 14.9 s, 3 groups 14.4 s, 4 groups 14.4-14.9 s
+  static const int want_groups = [] {
+    const char* e = std::getenv("QTNH_SVD_GROUPS");
+    const int g = e ? std::atoi(e) : 3;
+    return std::max(1, std::min(8, g));
+  }();
+  const int ngroups = static_cast<int>(std::max<Dim>(1, std::min<Dim>(batch, want_groups)));
+  const Dim per_group = (batch + ngroups - 1) / ngroups;  // see the multi-stream split below
   int splits = static_cast<int>(std::max<Dim>(1, std::min<Dim>((2 * sms() + npairs * per_group - 1) / (npairs * per_group),
                                                                 (L + kGramCols - 1) / kGramCols)));
   // de Rijk ordering (QTNH_SVD_SORT=1): rows sorted by descending norm before every
@@ -969,7 +978,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   // The batch runs as two independent halves on two streams when it has >= 2
   // matrices: the latency-bound eigen step of one half overlaps the other half's
   // Gram / update DMMA work, and a half that converges stops early.
-  const int ngroups = batch >= 2 ? 2 : 1;
+
   struct Group {
     Dim base = 0, cnt = 0;
     cudaStream_t s = nullptr;
