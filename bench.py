@@ -98,39 +98,125 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ---- reference / CPU arm ---------------------------------------------------------------------
-def cpu_reference_sample(budget_s: float = 15.0, rank_a: int = 22):
-    """The unmodified reference (oracle/_ref) on a bounded sample of the same
-    workload: a rank-22 A (same rank-14 B, 7 shared seeded positions), World(1),
-    OpenBLAS with all host threads. Returns (TFLOP/s, cores, sample description)."""
+# ---- C1 workload description shared by both arms ----------------------------------------------
+def fisher_yates(hash_fn, seed: int, tag: int, r: int):
+    """Seeded Fisher-Yates on hash_counter(seed, tag, i) (test_ops.cpp:124-129)."""
+    p = list(range(r))
+    for i in range(r - 1, 0, -1):
+        j = hash_fn(seed, tag, i) % (i + 1)
+        p[i], p[j] = p[j], p[i]
+    return p
+
+
+def c1_positions(hash_fn, rank_a: int = RANK_A):
+    """The 7 contracted positions of A and of B, paired in sorted order."""
+    ap = sorted(fisher_yates(hash_fn, SEED, 8, rank_a)[:K_SHARED])
+    bp = sorted(fisher_yates(hash_fn, SEED + 1, 8, RANK_B)[:K_SHARED])
+    return ap, bp
+
+
+class C1Sample:
+    """A bounded sample of the SAME rank-28 contraction for the CPU arms: fixing the
+    first FIXED open indices of A to a block value b cuts A into 2^FIXED rank-22
+    slices; contracting slice b with B (7 shared indices, the same positions) gives
+    exactly rows [b*2^22, (b+1)*2^22) of the rank-28 result (those indices lead the
+    SPEC.md:408 result order). The slice values are the rank-28 A's own elements
+    (the counter-based generator evaluated at their global indices), so the
+    reference's output for a slice is also a parity check of the GPU's rank-28
+    result on those rows."""
+
+    FIXED = 6
+
+    def __init__(self, port, shard: int = 0):
+        import numpy as np
+
+        self.np, self.P, self.shard = np, port, shard
+        self.ap, self.bp = c1_positions(port.hash_counter)
+        open_a = [i for i in range(RANK_A) if i not in self.ap]
+        self.fixed = open_a[: self.FIXED]
+        self.rest = [i for i in range(RANK_A) if i not in self.fixed]
+        self.rank_s = RANK_A - self.FIXED
+        self.ap_s = [self.rest.index(p) for p in self.ap]
+        j = np.arange(2**self.rank_s, dtype=np.int64)
+        base = np.zeros_like(j)
+        for t, pos in enumerate(self.rest):
+            base |= ((j >> (self.rank_s - 1 - t)) & 1) << (RANK_A - 1 - pos)
+        self.base = base + shard * 2**RANK_A
+        self.b = port.counter_normals(SEED + 1, 0, 2**RANK_B)
+
+    def a_slice(self, block: int):
+        off = 0
+        for t, pos in enumerate(self.fixed):
+            off |= ((block >> (self.FIXED - 1 - t)) & 1) << (RANK_A - 1 - pos)
+        return self.P.counter_normals_at(SEED, self.base + off)
+
+    @staticmethod
+    def rows(block: int):
+        n = 2 ** (RANK_A - C1Sample.FIXED)
+        return slice(block * n, (block + 1) * n)
+
+    def flops(self) -> float:
+        return flops_for(RANK_A) / 2**self.FIXED
+
+
+def c1_brute_force(port, outputs, shard: int = 0):
+    """Host brute force of selected rank-28 result elements straight from the
+    definition C[o] = sum_k A[a(o, k)] B[b(o, k)], with A and B
+    evaluated by the oracle port's counter-based generator at the needed indices."""
     import numpy as np
 
+    ap, bp = c1_positions(port.hash_counter)
+    open_a = [i for i in range(RANK_A) if i not in ap]
+    open_b = [i for i in range(RANK_B) if i not in bp]
+    o = np.asarray(outputs, dtype=np.int64)[:, None]
+    k = np.arange(2**K_SHARED, dtype=np.int64)[None, :]
+    ia = np.zeros((o.shape[0], k.shape[1]), np.int64)
+    ib = np.zeros_like(ia)
+    n_out = len(open_a) + len(open_b)
+    for t, pos in enumerate(open_a):
+        ia |= ((o >> (n_out - 1 - t)) & 1) << (RANK_A - 1 - pos)
+    for t, pos in enumerate(open_b):
+        ib |= ((o >> (n_out - 1 - len(open_a) - t)) & 1) << (RANK_B - 1 - pos)
+    for t in range(K_SHARED):
+        bit = (k >> (K_SHARED - 1 - t)) & 1
+        ia |= bit << (RANK_A - 1 - ap[t])
+        ib |= bit << (RANK_B - 1 - bp[t])
+    av = port.counter_normals_at(SEED, (ia + shard * 2**RANK_A).reshape(-1)).reshape(ia.shape)
+    bv = port.counter_normals_at(SEED + 1, ib.reshape(-1)).reshape(ib.shape)
+    return (av * bv).sum(axis=1)
+
+
+def cpu_reference_c1(budget_s: float = 15.0, blocks=None, keep_outputs: bool = False):
+    """The unmodified reference (oracle/_ref: t2m -> SUMMA cblas_zgemm -> m2t,
+    linalg.hpp:208-400, OpenBLAS on all host threads, World(1)) on 1/64 slices of the
+    rank-28 contraction (C1Sample), best of the calls made within the budget.
+    Returns (TFLOP/s, cores, sample, kind, {block: result rows})."""
     import oracle
-    from paper_2505_06119_b200 import circuits
 
     cores = os.cpu_count() or 1
-    R = oracle.ref() if oracle.ref_available() else None
-    a = circuits.counter_state(SEED, 2**rank_a)
-    b = circuits.counter_state(SEED + 1, 2**RANK_B)
-    ap, bp = circuits.contraction_positions(SEED, rank_a, RANK_B, K_SHARED)
-    if R is None:
-        P = oracle.port()
-        t0 = time.perf_counter()
-        P.contract([2] * rank_a, a, [2] * RANK_B, b, ap, bp)
-        dt = time.perf_counter() - t0
-        return flops_for(rank_a) / dt / 1e12, 1, f"C port brute force, rank-{rank_a} A, 1 call", "port"
+    P = oracle.port()
+    smp = C1Sample(P)
+    if not oracle.ref_available():
+        raise RuntimeError("oracle/_ref/libqtnh_ref.so missing (built by __graft_entry__.build())")
+    R = oracle.ref()
     R.set_threads(cores)
-    times = []
+    blocks = list(blocks) if blocks is not None else list(range(2**C1Sample.FIXED))
+    times, outs = [], {}
     t_start = time.perf_counter()
-    while True:
-        _, _, _, t = R.contract(1, [2] * rank_a, 0, (1, 1, 0), a, [2] * RANK_B, 0, (1, 1, 0), b, ap, bp, timing=True)
+    for i, blk in enumerate(blocks):
+        a = smp.a_slice(blk)
+        c, _, _, t = R.contract(1, [2] * smp.rank_s, 0, (1, 1, 0), a, [2] * RANK_B, 0, (1, 1, 0), smp.b,
+                                smp.ap_s, smp.bp, timing=True)
         times.append(t[3] / 1e3)
-        if time.perf_counter() - t_start > budget_s or len(times) >= 20:
+        if keep_outputs:
+            outs[blk] = c
+        if time.perf_counter() - t_start > budget_s:
             break
     best = min(times)
-    return (flops_for(rank_a) / best / 1e12, cores,
-            f"reference t2m->pgemm->m2t, rank-{rank_a} A x rank-14 B, {len(times)} calls, best of",
-            "reference")
+    sample = (f"{len(times)} of the 64 rank-22 slices of the rank-28 A (first 6 open indices of A fixed; "
+              f"each slice x the full B = 1/64 of the C1 contraction, rows of its result), through the "
+              f"reference's t2m->pgemm->m2t; best call {best:.3f} s")
+    return smp.flops() / best / 1e12, cores, sample, "reference", outs
 
 
 def c1_config(world_size: int) -> dict:
@@ -146,27 +232,46 @@ def c1_config(world_size: int) -> dict:
 
 
 def run_reference_arm(args):
+    """--impl reference: the reference's own CPU path (oracle/_ref = the unmodified
+    headers + OpenBLAS) on this host's cores. Each step is one 1/64 slice of the
+    rank-28 contraction (C1Sample; step i takes slice i mod 64), so the workload,
+    metric and unit are the GPU arm's. Nothing from paper_2505_06119_b200 is loaded."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    steps = []
-    value, cores, sample, kind = None, None, None, None
-    for _ in range(args.warmup):
-        cpu_reference_sample(budget_s=2.0)
-    for _ in range(args.steps):
-        value, cores, sample, kind = cpu_reference_sample(budget_s=2.0)
-        steps.append(value)
-    v = statistics.median(steps)
+    import oracle
+
+    if not oracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libqtnh_ref.so was not built"}))
+        return
+    P = oracle.port()
+    smp = C1Sample(P)
+    R = oracle.ref()
+    cores = os.cpu_count() or 1
+    R.set_threads(cores)
+
+    def step(i):
+        a = smp.a_slice(i % 2**C1Sample.FIXED)
+        _, _, _, t = R.contract(1, [2] * smp.rank_s, 0, (1, 1, 0), a, [2] * RANK_B, 0, (1, 1, 0), smp.b,
+                                smp.ap_s, smp.bp, timing=True)
+        return t[3] / 1e3
+
+    for i in range(args.warmup):
+        step(i)
+    times = [step(args.warmup + i) for i in range(args.steps)]
+    sec = sum(times)
+    v = smp.flops() * len(times) / sec / 1e12
+    sample = (f"each step = one of the 64 rank-22 slices of the rank-28 A (first 6 open indices of A fixed) "
+              f"contracted with the full B through the reference's t2m->pgemm->m2t (linalg.hpp:208-400), i.e. "
+              f"1/64 of the C1 contraction; {cores} OpenBLAS threads, World(1)")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (seeded counter-based normals)",
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
+            "data": "synthetic (seeded counter-based normals: the rank-28 A's own elements)",
             "config": c1_config(args.gpus),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
-                             "sample": sample + "; each step is this bounded sample of the config's workload "
-                                                "(same seeded generator, positions and B)"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-
 
 
 def hbm_peak():
@@ -275,19 +380,16 @@ def run_gpu_arm(args):
     flops_rank = flops_for(RANK_A)
 
     world_note = None
-    if world_size > 1 and world_size > torch.cuda.device_count():
-        world_note = (f"{world_size} ranks on {torch.cuda.device_count()} visible GPU(s): each rank contracts its "
-                      "own A shard in a 1-rank world (NCCL needs one GPU per rank)")
-        world = World(1, [local])
-    elif world_size > 1:
-        try:
-            world = World.from_env()
-        except Exception as e:  # C1 has no data-path collective: independent shards still measure it
-            world_note = f"NCCL world unavailable ({e}); each rank contracts its own A shard in a 1-rank world"
-            world = World(1, [local])
+    if world_size > 1:
+        # One node, one process per GPU. Default: the CUDA-IPC world (collectives are
+        # peer-memory kernels over NVLink; it also runs several ranks on one GPU);
+        # QTNH_BENCH_WORLD=nccl selects the NCCL world. A failure is fatal: no fallback.
+        kind = os.environ.get("QTNH_BENCH_WORLD", "ipc")
+        world = World.from_env() if kind == "nccl" else World.from_env_ipc()
+        world_note = f"{kind} world, {world_size} processes on {torch.cuda.device_count()} visible GPU(s)"
     else:
         world = World(1, [local])
-    nccl_world = world_size > 1 and world_note is None
+    nccl_world = world_size > 1
     stream = torch.cuda.Stream()
     lib = qtnh.lib
     result = {}
@@ -300,7 +402,7 @@ def run_gpu_arm(args):
     c_host = torch.empty(2**RANK_A, dtype=torch.complex128).pin_memory()
     ap_local, bp = circuits.contraction_positions(SEED, RANK_A, RANK_B, K_SHARED)
     # the distributed leading indices are open (a 1-rank fallback world holds the shard alone)
-    ap = [p + s for p in ap_local] if (nccl_world or world_size == 1) else list(ap_local)
+    ap = [p + s for p in ap_local]
 
     def barrier():
         if world_size > 1:
@@ -309,12 +411,8 @@ def run_gpu_arm(args):
     def body(rk):
         rk.set_stream(stream.cuda_stream)
         with torch.cuda.stream(stream):
-            if nccl_world or world_size == 1:
-                ta = Tensor.dense(rk, IndexTuple([2] * rank_a_global, s), DistParams(1, 1, 0), None)
-                tb = Tensor.dense(rk, IndexTuple([2] * RANK_B, 0), DistParams(world_size, 1, 0), None)
-            else:
-                ta = Tensor.dense(rk, IndexTuple([2] * RANK_A, 0), DistParams(1, 1, 0), None)
-                tb = Tensor.dense(rk, IndexTuple([2] * RANK_B, 0), DistParams(1, 1, 0), None)
+            ta = Tensor.dense(rk, IndexTuple([2] * rank_a_global, s), DistParams(1, 1, 0), None)
+            tb = Tensor.dense(rk, IndexTuple([2] * RANK_B, 0), DistParams(world_size, 1, 0), None)
             qtnh.check(lib.qtnh_tensor_upload_local(ta._h, C.c_void_p(a_host.data_ptr())))
             qtnh.check(lib.qtnh_tensor_upload_local(tb._h, C.c_void_p(b_host.data_ptr())))
             rk.synchronize()
@@ -346,6 +444,23 @@ def run_gpu_arm(args):
             ms = e0.elapsed_time(e1) / args.steps
             result.update(ms=ms, launches=launches, clocks=clk.summary())
 
+            # ---- parity of the TIMED contraction at its full size (outside the timed region) ------
+            # The result block of this rank (2^28 elements, SPEC.md:408 order) is checked
+            # (a) element-wise against a host brute-force sum from the oracle port at 1024
+            # seeded positions, and (b) on rank 0 of a 1-GPU run against the reference's
+            # own output for the slices the cpu_baseline leg contracts (below).
+            c = step()
+            qtnh.check(lib.qtnh_tensor_download_local(c._h, C.c_void_p(c_host.data_ptr())))
+            c.free()
+            import oracle
+
+            rng = np.random.default_rng(SEED)
+            outs = np.concatenate([[0, 2**RANK_A - 1], rng.integers(0, 2**RANK_A, size=1022)])
+            want = c1_brute_force(oracle.port(), outs, shard=rank)
+            got = c_host.numpy()[outs]
+            result["parity_bf"] = float(np.linalg.norm(got - want) / np.linalg.norm(want))
+            result["parity_bf_n"] = int(outs.size)
+
             # ---- dominant kernel: zgemm alone on the permuted operands ---------------------------
             M, N, K = 2 ** (RANK_A - K_SHARED), 2 ** (RANK_B - K_SHARED), 2**K_SHARED
             ga = torch.empty((M, K), dtype=torch.complex128, device="cuda")
@@ -365,11 +480,6 @@ def run_gpu_arm(args):
             z1.record(stream)
             z1.synchronize()
             result["zgemm_ms"] = z0.elapsed_time(z1) / reps
-            # numerics spot check of the timed GEMM against a host product of one row block
-            rows = 64
-            want = a_np[: rows * K].reshape(rows, K) @ b_host.numpy().reshape(K, N)
-            got = gc[:rows].cpu().numpy()
-            result["zgemm_spot_rel_err"] = float(np.linalg.norm(got - want) / np.linalg.norm(want))
             del ga, gb, gc
             # permute kernel share (A layout permutation)
             perm_a = [i for i in range(RANK_A) if i not in ap_local] + ap_local
@@ -414,7 +524,7 @@ def run_gpu_arm(args):
             barrier()
             torch.cuda.synchronize()
             f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e2e_steps = max(3, min(args.steps, 5))
+            e2e_steps = args.steps
             f0.record(stream)
             for _ in range(e2e_steps):
                 e2e_step().free()
@@ -452,12 +562,24 @@ def run_gpu_arm(args):
     achieved = 0.75 * flops_rank / (ms * 1e-3) / 1e12
     peak = result["fp64_peak"]
     cpu = None
+    parity = {"brute_force_rel_l2": rmax(result["parity_bf"]), "brute_force_elements": result["parity_bf_n"],
+              "tolerance": 1e-10}
     if rank == 0 and world_size == 1 and not args.no_cpu_baseline:
         try:
-            v, cores, sample, kind = cpu_reference_sample(budget_s=args.cpu_budget)
+            v, cores, sample, kind, outs = cpu_reference_c1(budget_s=args.cpu_budget, keep_outputs=True)
             cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+            # the reference's own rows of the rank-28 result vs the GPU's timed contraction
+            num = den = 0.0
+            for blk, ref_rows in outs.items():
+                got = c_host.numpy()[C1Sample.rows(blk)]
+                num += float(np.linalg.norm(got - ref_rows) ** 2)
+                den += float(np.linalg.norm(ref_rows) ** 2)
+            parity["reference_rows_rel_l2"] = (num / den) ** 0.5
+            parity["reference_rows"] = len(outs) * 2 ** (RANK_A - C1Sample.FIXED)
         except Exception as e:  # reported, never fatal for the GPU number
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+    parity["rel_l2"] = max(parity["brute_force_rel_l2"], parity.get("reference_rows_rel_l2", 0.0))
+    parity["ok"] = parity["rel_l2"] <= 1e-10
     traffic, kname = None, "k_zgemm (DMMA m8n8k4, 4M complex, fused A gather)"
     tpath = os.path.join(ROOT, "profiles", "zgemm_traffic.json")
     if os.path.exists(tpath):  # committed ncu --set full capture of the step's GEMM
@@ -482,9 +604,9 @@ def run_gpu_arm(args):
                          "traffic": traffic, "kernel_ms": ms,
                          "zgemm_dense_ms": zg, "zgemm_dense_tflops_8mnk": flops_rank / (zg * 1e-3) / 1e12,
                          "permute_ms": result["permute_ms"],
-                         "permute_GBps": 2 * 16 * 2**RANK_A / (result["permute_ms"] * 1e-3) / 1e9,
-                         "zgemm_spot_rel_err": result["zgemm_spot_rel_err"]},
+                         "permute_GBps": 2 * 16 * 2**RANK_A / (result["permute_ms"] * 1e-3) / 1e9},
             "cpu_baseline": cpu,
+            "parity_rel_l2": parity["rel_l2"], "parity": parity,
             "e2e": {"value": total_flops / (e2e_ms * 1e-3) / 1e12, "unit": UNIT,
                     "h2d_bytes_per_step": result["h2d"], "d2h_bytes_per_step": result["d2h"],
                     "ms_per_step": e2e_ms},

@@ -200,6 +200,7 @@ class _Port:
         L.qo_u64_to_unit.argtypes = [u64]
         L.qo_rng_complex_normals.argtypes = [u64, i64, vp]
         L.qo_counter_normals.argtypes = [u64, i64, i64, vp]
+        L.qo_counter_normals_at.argtypes = [u64, vp, i64, vp]
         P64, P32 = C.POINTER(C.c_int64), C.POINTER(C.c_int)
         L.qo_permute.argtypes = [i32, P64, vp, P32, vp]
         L.qo_contract.argtypes = [i32, P64, vp, i32, P64, vp, i32, P32, P32, vp]
@@ -217,6 +218,12 @@ class _Port:
     def counter_normals(self, seed: int, start: int, count: int) -> np.ndarray:
         out = np.empty(count, np.complex128)
         self.lib.qo_counter_normals(seed, start, count, out.ctypes.data)
+        return out
+
+    def counter_normals_at(self, seed: int, idx) -> np.ndarray:
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        out = np.empty(idx.size, np.complex128)
+        self.lib.qo_counter_normals_at(seed, idx.ctypes.data, idx.size, out.ctypes.data)
         return out
 
     def permute(self, dims, data, perm) -> np.ndarray:

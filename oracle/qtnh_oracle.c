@@ -77,6 +77,12 @@ void qo_counter_normals(uint64_t seed, int64_t start, int64_t count, double* out
   }
 }
 
+/* The same generator at arbitrary global element indices (a strided slice of a
+ * sharded input, e.g. bench.py's reference sample of the C1 operand A). */
+void qo_counter_normals_at(uint64_t seed, const int64_t* idx, int64_t count, double* out) {
+  for (int64_t i = 0; i < count; ++i) qo_counter_normals(seed, idx[i], 1, out + 2 * i);
+}
+
 /* ---- permutation: ops.hpp:27-49 via remap.hpp:56-161 ------------------------
  * result index p is source index perm[p]. Zero elements (both parts == 0.0,
  * either sign) are skipped by the reference's remap and the destination starts

@@ -60,36 +60,44 @@ struct TableKey {
     return std::tie(device, dims, strides) < std::tie(o.device, o.dims, o.strides);
   }
 };
-struct TableVal {
-  int64_t* ptr = nullptr;
-  size_t bytes = 0;
-};
+using Table = std::shared_ptr<const int64_t>;
 std::mutex g_tab_mu;
-std::map<TableKey, TableVal> g_tabs;
+std::map<TableKey, std::pair<Table, size_t>> g_tabs;
 size_t g_tab_bytes = 0;
 
-const int64_t* gather_table(RankCtx& r, const std::vector<Dim>& dims, const std::vector<Dim>& strides) {
+// Returns a reference-counted table: callers keep it alive until the GEMM that
+// reads it is enqueued, so evicting the cache (or another rank thread on the
+// same device evicting it) never frees a table a pending launch still names.
+// The last holder frees it after the device drains.
+Table gather_table(RankCtx& r, const std::vector<Dim>& dims, const std::vector<Dim>& strides) {
   TableKey key{r.device, dims, strides};
   std::lock_guard<std::mutex> lk(g_tab_mu);
   auto it = g_tabs.find(key);
-  if (it != g_tabs.end()) return it->second.ptr;
+  if (it != g_tabs.end()) return it->second.first;
   Dim count = 1;
   for (Dim d : dims) count *= d;
-  if (g_tab_bytes > (size_t(1) << 30)) {  // bounded: drop everything (tables are cheap to rebuild)
-    QTNH_CUDA(cudaStreamSynchronize(r.stream));
-    for (auto& kv : g_tabs) cudaFree(kv.second.ptr);
+  if (g_tab_bytes > (size_t(1) << 30)) {  // bounded: drop the cache's references (tables are cheap to rebuild)
     g_tabs.clear();
     g_tab_bytes = 0;
   }
-  TableVal v;
-  v.bytes = static_cast<size_t>(std::max<Dim>(1, count)) * 8;
-  QTNH_CUDA(cudaMalloc(&v.ptr, v.bytes));
-  index_offsets(v.ptr, count, dims, strides, r.stream);
+  const size_t bytes = static_cast<size_t>(std::max<Dim>(1, count)) * 8;
+  int64_t* ptr = nullptr;
+  QTNH_CUDA(cudaMalloc(&ptr, bytes));
+  const int dev = r.device;
+  Table t(ptr, [dev](const int64_t* p) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(dev);
+    cudaDeviceSynchronize();  // launches that named the table have been enqueued by now: let them finish
+    cudaFree(const_cast<int64_t*>(p));
+    cudaSetDevice(cur);
+  });
+  index_offsets(ptr, count, dims, strides, r.stream);
   // other ranks (streams) on this device may pick the table up right away
   QTNH_CUDA(cudaStreamSynchronize(r.stream));
-  g_tabs[key] = v;
-  g_tab_bytes += v.bytes;
-  return v.ptr;
+  g_tabs[key] = {t, bytes};
+  g_tab_bytes += bytes;
+  return t;
 }
 
 }  // namespace
@@ -231,8 +239,7 @@ TP op_contract(const TP& a_in, const TP& b_in, const std::vector<int>& apos, con
       Dim min_r = min_stride(rd, rs), min_c = min_stride(cd, cs);
       // Row offsets: for a long M two small tables, rowoff(m) = hi[m >> sh] +
       // lo[m & (2^sh - 1)], instead of an M-entry table (16 MB at C1).
-      const int64_t* ro = nullptr;
-      const int64_t* rohi = nullptr;
+      Table ro, rohi;
       int ro_sh = 0;
       static const bool row_split = [] {
         const char* e = std::getenv("QTNH_ROW_SPLIT");
@@ -263,8 +270,7 @@ TP op_contract(const TP& a_in, const TP& b_in, const std::vector<int>& apos, con
       if (!ro) ro = gather_table(r, rd, rs);
       // A long K keeps its column offsets in shared memory as two small tables:
       // coloff(k) = hi[k >> sh] + lo[k & (2^sh - 1)] (inner digits -> lo).
-      const int64_t* co = nullptr;
-      const int64_t* cohi = nullptr;
+      Table co, cohi;
       int co_sh = 0;
       if (K > 512) {
         for (size_t sp = 1; sp < cd.size() && !cohi; ++sp) {
@@ -278,8 +284,8 @@ TP op_contract(const TP& a_in, const TP& b_in, const std::vector<int>& apos, con
         }
       }
       if (!co) co = gather_table(r, cd, cs);
-      zgemm_gather_a(a->data(), ro, co, min_r <= min_c, B, c2->data(), M, N, K, r.stream, cohi, co_sh, rohi,
-                     ro_sh);
+      zgemm_gather_a(a->data(), ro.get(), co.get(), min_r <= min_c, B, c2->data(), M, N, K, r.stream, cohi.get(),
+                     co_sh, rohi.get(), ro_sh);
     }
   }
   // 4. Restore the SPEC order / split when a was reshuffled.

@@ -161,3 +161,69 @@ def test_contract_host_pipeline(da, db, ap, bp):
     got = run_collect(World(1), body)
     want = P.contract(da, a.reshape(-1), db, b.reshape(-1), ap, bp)
     assert rel_l2(got.reshape(-1), want) < TOL
+
+
+@pytest.mark.slow
+def test_c1_full_size_rank28_vs_reference():
+    """The bench's own contraction at its full size (BASELINE.json configs[1]: A
+    rank-28 = 4 GiB, B rank-14, 7 shared seeded positions, seed 2025) on the GPU,
+    against the UNMODIFIED reference's t2m -> pgemm -> m2t over the same 2^28
+    elements (~44 GB of host RSS; OpenBLAS on every host core), and against the
+    definition-level brute force of 4096 result elements (oracle port)."""
+    import os
+
+    import bench
+
+    if not oracle.ref_available():
+        pytest.skip("reference build absent")
+    ra, rb, k, seed = bench.RANK_A, bench.RANK_B, bench.K_SHARED, bench.SEED
+    a = circuits.counter_state(seed, 2**ra)
+    b = circuits.counter_state(seed + 1, 2**rb)
+    ap, bp = circuits.contraction_positions(seed, ra, rb, k)
+    assert (ap, bp) == bench.c1_positions(P.hash_counter)
+
+    def body(rk):
+        ta = Tensor.dense(rk, IndexTuple([2] * ra, 0), None, a)
+        tb = Tensor.dense(rk, IndexTuple([2] * rb, 0), None, b)
+        c = contract(ta, tb, ap, bp)
+        out = c.local_data().copy()
+        for t in (ta, tb, c):
+            t.free()
+        return out
+
+    got = run_collect(World(1), body)
+    rng = np.random.default_rng(7)
+    outs = np.concatenate([[0, 2**ra - 1], rng.integers(0, 2**ra, size=4094)])
+    assert rel_l2(got[outs], bench.c1_brute_force(P, outs)) < TOL
+    R = oracle.ref()
+    R.set_threads(os.cpu_count() or 1)
+    want, wd, ws = R.contract(1, [2] * ra, 0, (1, 1, 0), a, [2] * rb, 0, (1, 1, 0), b, ap, bp)
+    del a
+    assert wd == [2] * ra and ws == 0
+    assert rel_l2(got, want) < TOL
+
+
+@pytest.mark.parametrize("scale", [1e3, 1e8])
+def test_gauss_3m_ill_scaled_operands(scale):
+    """The GEMM forms the complex product with Gauss's three real products
+    (Im = P3 - P1 - P2). With |Re| >> |Im| the imaginary part is a difference of
+    O(|Re|^2) terms: its own relative error grows like eps * |Re| / |Im|, while the
+    north-star metric (relative L2 of the complex result) stays at rounding level.
+    Both are pinned here against a numpy complex128 product, contraction-shaped
+    (gathered A) and dense."""
+    rng = np.random.default_rng(int(scale))
+    da, db, ap, bp = [2] * 16, [2] * 12, [1, 4, 7, 9, 12, 14], [0, 2, 3, 5, 8, 11]
+    a = rng.standard_normal(2**16) * scale + 1j * rng.standard_normal(2**16)
+    b = rng.standard_normal(2**12) * scale + 1j * rng.standard_normal(2**12)
+
+    def body(rk):
+        ta = Tensor.from_global(rk, IndexTuple(da, 0), None, a)
+        tb = Tensor.from_global(rk, IndexTuple(db, 0), None, b)
+        return contract(ta, tb, ap, bp).to_global_vector()
+
+    got = run_collect(World(1), body)
+    want = P.contract(da, a, db, b, ap, bp)
+    assert rel_l2(got, want) < 1e-14
+    # per component: Re at rounding level, Im within eps * scale (the documented 3M bound)
+    assert rel_l2(got.real, want.real) < 1e-14
+    assert rel_l2(got.imag, want.imag) < 1e-14 * scale

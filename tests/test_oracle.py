@@ -131,3 +131,20 @@ def test_resource_error_on_small_world():
     with pytest.raises(oracle.OracleError) as e:
         R.permute(2, [2, 2, 4, 2], 1, (1, 1, 0), g, [2, 0, 1, 3], 1)
     assert e.value.code == 2 and e.value.info == 4
+
+
+def test_bench_c1_sample_is_a_slice_of_the_rank28_contraction():
+    """bench.py's CPU arms time 1/64 slices of the C1 contraction (first six open
+    indices of the rank-28 A fixed). The reference's output for a slice must equal
+    the definition-level brute force of those rows of the rank-28 result."""
+    import bench
+
+    if not oracle.ref_available():
+        pytest.skip("reference build absent")
+    P = oracle.port()
+    _, _, _, _, outs = bench.cpu_reference_c1(budget_s=0.0, blocks=[37], keep_outputs=True)
+    rows = bench.C1Sample.rows(37)
+    idx = np.arange(rows.start, rows.stop)[::997]
+    bf = bench.c1_brute_force(P, idx)
+    ref = outs[37][idx - rows.start]
+    assert np.linalg.norm(bf - ref) <= 1e-13 * np.linalg.norm(ref)
