@@ -539,6 +539,12 @@ def run_gpu_arm(args):
             torch.cuda.synchronize()
             if not args.skip_extras:
                 result["extras"] = measure_extras(rk, stream, torch)
+            if not args.skip_configs and world_size == 1:
+                import bench_legs
+
+                with torch.cuda.stream(stream):
+                    result["configs"] = bench_legs.run_all(rk, stream, torch,
+                                                           log=lambda m: print(m, file=sys.stderr, flush=True))
 
     world.run(body)
 
@@ -612,6 +618,7 @@ def run_gpu_arm(args):
                     "ms_per_step": e2e_ms},
             "gpu_launches": result["launches"],
             "extras": result.get("extras"),
+            "configs": result.get("configs"),
             "clocks": result["clocks"],
         }
         print(json.dumps(line), flush=True)
@@ -630,6 +637,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-extras", action="store_true")
+    ap.add_argument("--skip-configs", action="store_true",
+                    help="skip the C0/C2/C3/C4 legs (GPU + same-run CPU reference + parity)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

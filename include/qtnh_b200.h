@@ -132,6 +132,19 @@ int qtnh_barrier(qtnh_rank_t r);
 int qtnh_all_to_all_v(qtnh_rank_t r, int n_members, const int* members, const void* send_buf,
                       const int64_t* send_counts, const int64_t* send_displs, void* recv_buf,
                       const int64_t* recv_counts, const int64_t* recv_displs);
+/* Group::all_to_all_v on HOST data (runtime.hpp:448-475; the building block of the
+ * C++ layer's Group broadcast / gather / scatter / all_reduce_sum / barrier):
+ * members in group order; send_lists[i] holds send_counts[i] elements of
+ * elem_size bytes for member i. Receive counts are exchanged first; with
+ * expected_counts (may be NULL) a mismatch raises QTNH_E_PROTOCOL "all_to_all_v
+ * count mismatch for pair (src -> dst): got G, expected E" on every member.
+ * *recv_data = one malloc'ed buffer (release with qtnh_free_host) holding what
+ * each member sent here, concatenated in member order; recv_counts[i] = its
+ * element count. */
+int qtnh_group_all_to_all_v_host(qtnh_rank_t r, int n_members, const int* members, size_t elem_size,
+                                 const void* const* send_lists, const int64_t* send_counts,
+                                 const int64_t* expected_counts, void** recv_data, int64_t* recv_counts);
+void qtnh_free_host(void* p);
 
 /* ---- tensors ------------------------------------------------------------- */
 /* Dense tensor; `local` holds local_size complex numbers of this rank's block
@@ -200,6 +213,21 @@ int qtnh_gather_index(qtnh_tensor_t t, int pos, qtnh_tensor_t* out);
 int qtnh_slice_local_dims(qtnh_tensor_t t, const int64_t* new_local_dims, qtnh_tensor_t* out);
 int qtnh_pad_local_dims(qtnh_tensor_t t, const int64_t* new_local_dims, qtnh_tensor_t* out);
 int qtnh_conj(qtnh_tensor_t t, qtnh_tensor_t* out);
+/* Real factor factors[c] on every element whose coordinate at index `pos` is c
+ * (replaces absorb_singular_left / _right(..., power), linalg.hpp:508-523, on the
+ * tensor form of U / Vh: factors = s^power). `factors` has dims[pos] entries. */
+int qtnh_scale_index(qtnh_tensor_t t, int pos, const double* factors, qtnh_tensor_t* out);
+/* A new handle on the same immutable value (tensor.hpp:41-43 value semantics:
+ * copies share storage until one is mutated, see qtnh_tensor_make_mutable). */
+int qtnh_tensor_clone(qtnh_tensor_t t, qtnh_tensor_t* out);
+/* Copy-on-write for Tensor::mutable_local_data (tensor.hpp:177-178): after this
+ * call the handle's local block is not shared with any other handle, so
+ * qtnh_tensor_upload_local writes only this value. */
+int qtnh_tensor_make_mutable(qtnh_tensor_t t);
+/* Same local row-major block under new dims (no distributed indices before or
+ * after; equal element count); shares the value. Used to regroup matrix digits
+ * in matrix_to_tensor / pgemm when the row or column factorisation changes. */
+int qtnh_tensor_reshape(qtnh_tensor_t t, int n_idx, const int64_t* dims, qtnh_tensor_t* out);
 int qtnh_scale(qtnh_tensor_t t, double re, double im, qtnh_tensor_t* out);
 
 /* Contraction order of a labelled network (SPEC network::contract_order,
@@ -295,10 +323,28 @@ int qtnh_remap_plan_json(int n_idx, const int64_t* dims, int split, const int64_
 /* Tensor-level split (SPEC network::decompose / linalg psvd + truncate_svd +
  * absorb_singular_*): rows = indices row_pos (in order), cols = col_pos. Outputs
  * u with dims [row dims..., chi], vh with dims [chi, col dims...] (same DistParams
- * as t; t must have no distributed indices), s_host (chi doubles, descending,
- * zero-padded; may be NULL). qtnh_last_error_info() afterwards = Jacobi sweeps. */
+ * as t), s_host (chi doubles, descending, zero-padded; may be NULL).
+ * A t with distributed indices is first gathered onto its root copy (linalg::psvd
+ * gathers to the group root, linalg.hpp:441-462): u and vh live there, and S is
+ * sent back to every rank of t's span (:464). qtnh_last_error_info() afterwards
+ * = Jacobi sweeps (on the ranks that ran the SVD). */
 int qtnh_svd(qtnh_tensor_t t, int n_row, const int* row_pos, int n_col, const int* col_pos, int64_t chi,
              int absorb, qtnh_tensor_t* u, qtnh_tensor_t* vh, double* s_host);
+
+/* One brickwork layer of MPS two-site updates (config 4; SPEC apply_raw_gate,
+ * SPEC.md:371-379 / :475-483, composed in the reference from contract ->
+ * gate -> psvd -> truncate_svd -> absorb_singular_left, linalg.hpp:208-523).
+ * Pair i: left[i] (l, d, c) and right[i] (c, d, r), both held by the calling
+ * rank without distributed indices; gate = 4 x 4 complex128 (interleaved re/im,
+ * row-major (out1 out2, in1 in2)). Thetas of equal shape are factorised by one
+ * batched SVD; U S and Vh are written straight into the new site tensors
+ * new_left[i] (l, d, keep), new_right[i] (keep, d, r), keep = min(chi, l d, d r).
+ * s_out[i * chi ...] = the kept singular values (descending, zero-padded to chi;
+ * may be NULL), keep_out[i] = keep, norm2_out[i] = ||theta_i||_F^2 (the kept
+ * weight is sum(s^2) / norm2). The inputs are not consumed. */
+int qtnh_mps_apply_layer(int n_pairs, const qtnh_tensor_t* left, const qtnh_tensor_t* right, const double* gate,
+                         int64_t chi, qtnh_tensor_t* new_left, qtnh_tensor_t* new_right, double* s_out,
+                         int64_t* keep_out, double* norm2_out);
 
 /* ---- raw kernels on device buffers (bench / integration) ------------------ */
 /* out = a(M x K) * b(K x N), row-major complex128 on the rank's stream. */

@@ -274,3 +274,30 @@ def port() -> _Port:
 
 def ref_available() -> bool:
     return os.path.exists(REF_SO)
+
+
+# ---- network replay (numpy) -----------------------------------------------------------
+def network_contract(items, order, big_first: bool = True):
+    """Replay a pairwise contraction order on the host: `items` = [(array, labels)]
+    (tensor i = items[i]), `order` = [(a, b)] with the result of step s getting id
+    len(items) + s. Each step is SPEC network::contract (SPEC.md:361-369): sum over
+    the shared labels, result indices open(first) then open(second),
+    written with numpy.tensordot (OpenBLAS zgemm on all host cores) -- the same
+    contraction the reference composes from t2m -> pgemm -> m2t (linalg.hpp:208-400),
+    without its 24-byte-per-element redistribution, so 2^30-element intermediates
+    fit in host memory and minutes. Returns (array, labels) of the last result."""
+    import math
+
+    T = {i: (np.ascontiguousarray(a, dtype=np.complex128), list(l)) for i, (a, l) in enumerate(items)}
+    n = len(items)
+    last = None
+    for s, (a, b) in enumerate(order):
+        (ta, la), (tb, lb) = T.pop(a), T.pop(b)
+        if big_first and sum(math.log2(d) for d in tb.shape) > sum(math.log2(d) for d in ta.shape):
+            (ta, la), (tb, lb) = (tb, lb), (ta, la)
+        sh = [x for x in la if x in lb]
+        c = np.tensordot(ta, tb, axes=([la.index(x) for x in sh], [lb.index(x) for x in sh]))
+        del ta, tb
+        last = n + s
+        T[last] = (np.ascontiguousarray(c), [x for x in la if x not in sh] + [x for x in lb if x not in sh])
+    return T[last]

@@ -92,6 +92,14 @@ _SIGS = {
     "qtnh_qft_layer": (i32, [vp, i32]),
     "qtnh_qft": (i32, [vp, i32]),
     "qtnh_svd_device": (i32, [vp, i64, i64, i64, vp, i64, i32, vp, vp, vp]),
+    "qtnh_scale_index": (i32, [vp, i32, vp, C.POINTER(vp)]),
+    "qtnh_tensor_clone": (i32, [vp, C.POINTER(vp)]),
+    "qtnh_tensor_make_mutable": (i32, [vp]),
+    "qtnh_tensor_reshape": (i32, [vp, i32, P_i64, C.POINTER(vp)]),
+    "qtnh_group_all_to_all_v_host": (i32, [vp, i32, P_i32, sz, C.POINTER(vp), P_i64, vp, C.POINTER(vp), P_i64]),
+    "qtnh_free_host": (None, [vp]),
+    "qtnh_mps_apply_layer": (i32, [i32, C.POINTER(vp), C.POINTER(vp), vp, i64, C.POINTER(vp), C.POINTER(vp), vp, vp,
+                                   vp]),
     "qtnh_svd": (i32, [vp, i32, P_i32, i32, P_i32, i64, i32, C.POINTER(vp), C.POINTER(vp), vp]),
     "qtnh_zgemm_device": (i32, [vp, i64, i64, i64, vp, vp, vp]),
     "qtnh_permute_device": (i32, [vp, i32, P_i64, P_i32, vp, vp]),

@@ -705,6 +705,37 @@ int qtnh_scale(qtnh_tensor_t t, double re, double im, qtnh_tensor_t* out) {
   });
 }
 
+int qtnh_scale_index(qtnh_tensor_t t, int pos, const double* factors, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    need(factors, "factors");
+    TP& p = impl_of(t);
+    if (pos < 0 || pos >= p->shape.n_idx()) throw_invalid("scale_index position out of range");
+    std::vector<double> f(factors, factors + p->shape.dims[pos]);
+    *out = wrap(op_scale_index(p, pos, f));
+  });
+}
+
+int qtnh_tensor_clone(qtnh_tensor_t t, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    *out = wrap(impl_of(t));
+  });
+}
+
+int qtnh_tensor_reshape(qtnh_tensor_t t, int n, const int64_t* dims, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    TP& p = impl_of(t);
+    Shape ns = shape_from(n, dims, 0);
+    if (p->shape.split != 0) throw_invalid("reshape needs a tensor without distributed indices");
+    if (ns.total_size() != p->shape.total_size()) throw_invalid("reshape must keep the element count");
+    auto q = std::make_shared<TensorImpl>(*p);  // same value (row-major block), new index tuple
+    q->shape = ns;
+    *out = wrap(q);
+  });
+}
+
 int qtnh_contract_chain(int n_inputs, const qtnh_tensor_t* inputs, int n_steps, const int* step_ab,
                         const int* step_npairs, const int* a_pos, const int* b_pos, qtnh_tensor_t* out) {
   return guard([&] {
@@ -783,6 +814,120 @@ void make_exclusive(TP& p) {
   }
 }
 }  // namespace
+
+int qtnh_tensor_make_mutable(qtnh_tensor_t t) {
+  return guard([&] {
+    TP& p = impl_of(t);
+    make_exclusive(p);
+    QTNH_CUDA(cudaStreamSynchronize(p->rank->stream));
+  });
+}
+
+// Host-data all-to-all among `members` in group order (the Group collectives of
+// runtime.hpp:122-163): receive sizes travel first, so a count mismatch against
+// expected_counts is seen -- and raised as ProtocolError naming the first
+// "(src -> dst)" pair in member order -- by EVERY member (runtime.hpp:464-471
+// poisons the shared slot); then the payload moves through device staging with
+// the world's exchange (NVLink / NCCL / IPC).
+int qtnh_group_all_to_all_v_host(qtnh_rank_t r, int n_members, const int* members, size_t elem_size,
+                                 const void* const* send_lists, const int64_t* send_counts,
+                                 const int64_t* expected_counts, void** recv_data, int64_t* recv_counts) {
+  return guard([&] {
+    RankCtx& x = ctx_of(r);
+    need(recv_data, "recv_data");
+    need(recv_counts, "recv_counts");
+    if (n_members < 1) throw_invalid("group members must be non-empty");
+    if (elem_size < 1) throw_invalid("element size must be positive");
+    need(members, "members");
+    std::vector<int> mem(members, members + n_members), sorted = mem;
+    std::sort(sorted.begin(), sorted.end());
+    if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end()) throw_invalid("duplicate group member");
+    for (int m : mem)
+      if (m < 0 || m >= x.world->size) throw_invalid("group member " + std::to_string(m) + " out of range");
+    const int me = static_cast<int>(std::find(mem.begin(), mem.end(), x.rank) - mem.begin());
+    if (me >= n_members)
+      throw_invalid("rank " + std::to_string(x.rank) + " cannot open a group it is not a member of");
+    const Dim n = n_members;
+    // phase 1: counts (one 16-byte element per member pair)
+    std::vector<int64_t> cnt_out(2 * n, 0), cnt_in(2 * n, 0);
+    for (Dim i = 0; i < n; ++i) cnt_out[2 * i] = send_counts ? send_counts[i] : 0;
+    DevBuf cs(16 * n, x), cr(16 * n, x);
+    std::vector<Xfer> s1, r1;
+    for (Dim i = 0; i < n; ++i) {
+      s1.push_back({mem[i], i, 1});
+      r1.push_back({mem[i], i, 1});
+    }
+    QTNH_CUDA(cudaMemcpyAsync(cs.ptr, cnt_out.data(), 16 * n, cudaMemcpyHostToDevice, x.stream));
+    exchange(x, sorted, cs.ptr, s1, cr.ptr, r1);
+    QTNH_CUDA(cudaMemcpyAsync(cnt_in.data(), cr.ptr, 16 * n, cudaMemcpyDeviceToHost, x.stream));
+    QTNH_CUDA(cudaStreamSynchronize(x.stream));
+    // phase 2: every member learns the first mismatch (src member, got, expected)
+    int64_t bad[4] = {-1, 0, 0, 0};
+    if (expected_counts)
+      for (Dim i = 0; i < n; ++i)
+        if (cnt_in[2 * i] != expected_counts[i]) {
+          bad[0] = i;
+          bad[1] = cnt_in[2 * i];
+          bad[2] = expected_counts[i];
+          break;
+        }
+    std::vector<int64_t> flags_out(4 * n), flags_in(4 * n);
+    for (Dim i = 0; i < n; ++i) std::copy(bad, bad + 4, flags_out.begin() + 4 * i);
+    DevBuf fs(32 * n, x), fr(32 * n, x);
+    std::vector<Xfer> s2, r2;
+    for (Dim i = 0; i < n; ++i) {
+      s2.push_back({mem[i], 2 * i, 2});
+      r2.push_back({mem[i], 2 * i, 2});
+    }
+    QTNH_CUDA(cudaMemcpyAsync(fs.ptr, flags_out.data(), 32 * n, cudaMemcpyHostToDevice, x.stream));
+    exchange(x, sorted, fs.ptr, s2, fr.ptr, r2);
+    QTNH_CUDA(cudaMemcpyAsync(flags_in.data(), fr.ptr, 32 * n, cudaMemcpyDeviceToHost, x.stream));
+    QTNH_CUDA(cudaStreamSynchronize(x.stream));
+    for (Dim j = 0; j < n; ++j)
+      if (flags_in[4 * j] >= 0)
+        throw Status(QTNH_E_PROTOCOL, "all_to_all_v count mismatch for pair (" +
+                                          std::to_string(mem[flags_in[4 * j]]) + " -> " + std::to_string(mem[j]) +
+                                          "): got " + std::to_string(flags_in[4 * j + 1]) + ", expected " +
+                                          std::to_string(flags_in[4 * j + 2]));
+    // phase 3: payload in 16-byte units
+    auto units = [&](int64_t c) { return static_cast<Dim>((c * static_cast<int64_t>(elem_size) + 15) / 16); };
+    Dim so = 0, ro = 0;
+    std::vector<Xfer> s3, r3;
+    std::vector<Dim> soff(n), roff(n);
+    for (Dim i = 0; i < n; ++i) {
+      soff[i] = so;
+      roff[i] = ro;
+      if (cnt_out[2 * i]) s3.push_back({mem[i], so, units(cnt_out[2 * i])});
+      if (cnt_in[2 * i]) r3.push_back({mem[i], ro, units(cnt_in[2 * i])});
+      so += units(cnt_out[2 * i]);
+      ro += units(cnt_in[2 * i]);
+    }
+    std::vector<char> sh(static_cast<size_t>(so) * 16, 0), rh(static_cast<size_t>(ro) * 16);
+    for (Dim i = 0; i < n; ++i)
+      if (cnt_out[2 * i]) {
+        if (!send_lists || !send_lists[i]) throw_invalid("null send list");
+        std::memcpy(sh.data() + soff[i] * 16, send_lists[i], cnt_out[2 * i] * elem_size);
+      }
+    DevBuf ds(16 * std::max<Dim>(so, 1), x), dr(16 * std::max<Dim>(ro, 1), x);
+    if (so) QTNH_CUDA(cudaMemcpyAsync(ds.ptr, sh.data(), so * 16, cudaMemcpyHostToDevice, x.stream));
+    exchange(x, sorted, ds.ptr, s3, dr.ptr, r3);
+    if (ro) QTNH_CUDA(cudaMemcpyAsync(rh.data(), dr.ptr, ro * 16, cudaMemcpyDeviceToHost, x.stream));
+    QTNH_CUDA(cudaStreamSynchronize(x.stream));
+    int64_t total = 0;
+    for (Dim i = 0; i < n; ++i) total += cnt_in[2 * i];
+    char* out = static_cast<char*>(std::malloc(std::max<size_t>(1, total * elem_size)));
+    if (!out) throw std::bad_alloc();
+    size_t at = 0;
+    for (Dim i = 0; i < n; ++i) {
+      std::memcpy(out + at, rh.data() + roff[i] * 16, cnt_in[2 * i] * elem_size);
+      at += cnt_in[2 * i] * elem_size;
+      recv_counts[i] = cnt_in[2 * i];
+    }
+    *recv_data = out;
+  });
+}
+
+void qtnh_free_host(void* p) { std::free(p); }
 
 int qtnh_contract_host(qtnh_rank_t r, int na, const int64_t* dims_a, const double* a, int nb,
                        const int64_t* dims_b, const double* b, int n_pairs, const int* a_pos, const int* b_pos,
@@ -883,14 +1028,47 @@ int qtnh_svd_device(qtnh_rank_t r, int64_t batch, int64_t m, int64_t n, const vo
   });
 }
 
+int qtnh_mps_apply_layer(int n_pairs, const qtnh_tensor_t* left, const qtnh_tensor_t* right, const double* gate,
+                         int64_t chi, qtnh_tensor_t* new_left, qtnh_tensor_t* new_right, double* s_out,
+                         int64_t* keep_out, double* norm2_out) {
+  return guard([&] {
+    if (n_pairs < 0) throw_invalid("negative pair count");
+    if (n_pairs == 0) return;
+    need(left, "left");
+    need(right, "right");
+    need(gate, "gate");
+    need(new_left, "new_left");
+    need(new_right, "new_right");
+    std::vector<TP> l(n_pairs), r(n_pairs), nl, nr;
+    for (int i = 0; i < n_pairs; ++i) {
+      l[i] = impl_of(left[i]);
+      r[i] = impl_of(right[i]);
+    }
+    mps_apply_layer(l, r, gate, chi, nl, nr, s_out, keep_out, norm2_out);
+    for (int i = 0; i < n_pairs; ++i) {
+      new_left[i] = wrap(nl[i]);
+      new_right[i] = wrap(nr[i]);
+    }
+  });
+}
+
 int qtnh_svd(qtnh_tensor_t t, int n_row, const int* row_pos, int n_col, const int* col_pos, int64_t chi,
              int absorb, qtnh_tensor_t* u_out, qtnh_tensor_t* vh_out, double* s_host) {
   return guard([&] {
     need(u_out, "u");
     need(vh_out, "vh");
-    TP& p = impl_of(t);
+    TP p = impl_of(t);
+    // A distributed theta is gathered onto its root copy first (linalg::psvd gathers
+    // the block-cyclic matrix onto the group root, linalg.hpp:441-462); S then goes
+    // back to every rank of the original span (:464).
+    std::vector<int> span_members;
+    if (p->shape.split != 0) {
+      span_members = span_ranks(*p);
+      std::vector<int> id(p->shape.n_idx());
+      std::iota(id.begin(), id.end(), 0);
+      p = op_permute(p, id, 0);
+    }
     const Shape& sh = p->shape;
-    if (sh.split != 0) throw_invalid("svd needs a tensor without distributed indices (gather it first)");
     if (n_row + n_col != sh.n_idx()) throw_invalid("row/col index sets must partition the tensor indices");
     std::vector<int> perm, seen(sh.n_idx(), 0);
     for (int i = 0; i < n_row; ++i) perm.push_back(row_pos[i]);
@@ -917,15 +1095,29 @@ int qtnh_svd(qtnh_tensor_t t, int n_row, const int* row_pos, int n_col, const in
     TP mat = op_permute(p, perm, 0);
     TP u = make_tensor(r, Shape(udims, 0), p->dist, true);
     TP vh = make_tensor(r, Shape(vdims, 0), p->dist, true);
+    const Dim s_units = (chi + 1) / 2;  // S as 16-byte elements for the broadcast
+    DevBuf s(static_cast<size_t>(s_units) * 16, r);
     if (p->in_span) {
-      DevBuf s(static_cast<size_t>(chi) * sizeof(double), r);
       int sweeps = 0;
       svd_batched(r, 1, m, n, mat->data(), chi, absorb, u->data(), s.ptr, vh->data(), &sweeps);
+      t_info = sweeps;
+    }
+    if (!span_members.empty() &&
+        std::find(span_members.begin(), span_members.end(), r.rank) != span_members.end()) {
+      const int root = static_cast<int>(p->dist.canonical(0));
+      std::vector<Xfer> sends, recvs;
+      if (r.rank == root)
+        for (int mbr : span_members) sends.push_back({mbr, 0, s_units});
+      DevBuf got(static_cast<size_t>(s_units) * 16, r);
+      recvs.push_back({root, 0, s_units});
+      exchange(r, span_members, s.ptr, sends, got.ptr, recvs);
       if (s_host) {
-        QTNH_CUDA(cudaMemcpyAsync(s_host, s.ptr, chi * sizeof(double), cudaMemcpyDeviceToHost, r.stream));
+        QTNH_CUDA(cudaMemcpyAsync(s_host, got.ptr, chi * sizeof(double), cudaMemcpyDeviceToHost, r.stream));
         QTNH_CUDA(cudaStreamSynchronize(r.stream));
       }
-      t_info = sweeps;
+    } else if (p->in_span && s_host) {
+      QTNH_CUDA(cudaMemcpyAsync(s_host, s.ptr, chi * sizeof(double), cudaMemcpyDeviceToHost, r.stream));
+      QTNH_CUDA(cudaStreamSynchronize(r.stream));
     }
     *u_out = wrap(u);
     *vh_out = wrap(vh);

@@ -47,6 +47,9 @@ TP op_gather_index(const TP& t, int pos);                                  // op
 TP op_slice_local(const TP& t, const std::vector<Dim>& nl);                // ops.hpp:166
 TP op_pad_local(const TP& t, const std::vector<Dim>& nl);                  // ops.hpp:201
 TP op_scale(const TP& t, double re, double im, bool conj);                 // ops.hpp:147-161
+// Real factor f[c] on every element whose coordinate at index pos is c
+// (absorb_singular_left/right(..., power), linalg.hpp:508-523).
+TP op_scale_index(const TP& t, int pos, const std::vector<double>& f);
 void op_to_global(const TensorImpl& t, double* host);                      // tensor.hpp:341
 // Contraction order of a labelled network (plan.cpp); ids of results continue
 // after the n input tensors in step order.
@@ -91,6 +94,17 @@ void index_offsets(int64_t* out, Dim count, const std::vector<Dim>& dims, const 
 // singular values absorbed per QTNH_ABSORB_*; device row-major in/out.
 void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* u, void* s,
                  void* vh, int* sweeps_out);
+// The same with one output pointer per matrix (U: m x chi, Vh: chi x n each).
+void svd_batched_ptrs(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* const* u_ptrs,
+                      void* s, void* const* vh_ptrs, int* sweeps_out);
+// One layer of MPS two-site updates (mps.cu): pair i = (left[i], right[i]),
+// sites (l, d, c) and (c, d, r) held by this rank; gate = 4x4 complex row-major
+// (out1 out2, in1 in2). New sites U S (l, d, keep) and Vh (keep, d, r), keep =
+// min(chi, l d, d r); s_out[i*chi ..] = kept singular values (zero-padded),
+// keep_out[i], norm2_out[i] = ||theta_i||_F^2.
+void mps_apply_layer(const std::vector<TP>& left, const std::vector<TP>& right, const double* gate, Dim chi,
+                     std::vector<TP>& new_left, std::vector<TP>& new_right, double* s_out, int64_t* keep_out,
+                     double* norm2_out);
 // Fused QFT layer on a local qubit block (all dims 2): H on bit t + the layer's
 // controlled phases; phase-only variant for a distributed target with x_j = 1.
 void qft_layer_local(void* data, int local_bits, int t, cudaStream_t st);

@@ -347,6 +347,28 @@ TP op_scale(const TP& t, double re, double im, bool conj) {
   return out;
 }
 
+TP op_scale_index(const TP& t, int pos, const std::vector<double>& f) {
+  const Shape& sh = t->shape;
+  if (pos < 0 || pos >= sh.n_idx()) throw_invalid("scale_index position out of range");
+  if (static_cast<Dim>(f.size()) != sh.dims[pos]) throw_invalid("scale_index needs one factor per coordinate");
+  TP out = make_tensor(*t->rank, sh, t->dist, true);
+  if (!out->in_span) return out;
+  RankCtx& r = *t->rank;
+  const Dim nl = sh.local_size();
+  if (pos < sh.split) {  // a distributed index: this rank's block has one coordinate
+    const Dim c = unflat(t->block, sh.dist_dims())[pos];
+    scale_conj(t->data(), out->data(), nl, f[c], 0.0, false, r.stream);
+    return out;
+  }
+  Dim inner = 1;
+  for (int i = pos + 1; i < sh.n_idx(); ++i) inner *= sh.dims[i];
+  DevBuf fd(f.size() * sizeof(double), r);
+  QTNH_CUDA(cudaMemcpyAsync(fd.ptr, f.data(), f.size() * sizeof(double), cudaMemcpyHostToDevice, r.stream));
+  scale_index(t->data(), out->data(), nl, inner, sh.dims[pos], static_cast<const double*>(fd.ptr), r.stream);
+  QTNH_CUDA(cudaStreamSynchronize(r.stream));  // the host factors are the caller's
+  return out;
+}
+
 void op_to_global(const TensorImpl& t, double* host) {
   if (!t.in_span) return;
   RankCtx& r = *t.rank;

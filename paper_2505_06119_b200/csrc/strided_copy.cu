@@ -158,6 +158,18 @@ __global__ void k_scale_conj(const double2* __restrict__ in, double2* __restrict
   }
 }
 
+// out[i] = in[i] * f[(i / inner) % dim]: a real factor per coordinate of one index
+// (absorb_singular_* with an arbitrary power, linalg.hpp:508-523)
+__global__ void k_scale_index(const double2* __restrict__ in, double2* __restrict__ out, int64_t n, int64_t inner,
+                              int64_t dim, const double* __restrict__ f) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = f[(i / inner) % dim];
+    const double2 v = in[i];
+    out[i] = make_double2(v.x * x, v.y * x);
+  }
+}
+
 __global__ void k_fill_zero(double2* __restrict__ out, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -479,6 +491,16 @@ void scale_conj(const void* in, void* out, Dim n, double re, double im, bool con
   QTNH_CUDA(cudaGetDevice(&dev));
   int grid = static_cast<int>(std::min<Dim>((n + 255) / 256, (Dim)sm_count(dev) * 8));
   k_scale_conj<<<grid, 256, 0, st>>>(static_cast<const double2*>(in), static_cast<double2*>(out), n, re, im, conj);
+  QTNH_LAUNCH_CHECK();
+}
+
+void scale_index(const void* in, void* out, Dim n, Dim inner, Dim dim, const double* f_dev, cudaStream_t st) {
+  if (n <= 0) return;
+  int dev = 0;
+  QTNH_CUDA(cudaGetDevice(&dev));
+  int grid = static_cast<int>(std::min<Dim>((n + 255) / 256, (Dim)sm_count(dev) * 8));
+  k_scale_index<<<grid, 256, 0, st>>>(static_cast<const double2*>(in), static_cast<double2*>(out), n, inner, dim,
+                                      f_dev);
   QTNH_LAUNCH_CHECK();
 }
 

@@ -28,6 +28,8 @@ CopyBox permute_box(const std::vector<Dim>& dims, const std::vector<int>& perm);
 
 // Elementwise y = alpha * conj?(x) over n complex numbers.
 void scale_conj(const void* in, void* out, Dim n, double re, double im, bool conj, cudaStream_t st);
+// out[i] = in[i] * f_dev[(i / inner) % dim] (real factors, device array of dim)
+void scale_index(const void* in, void* out, Dim n, Dim inner, Dim dim, const double* f_dev, cudaStream_t st);
 void fill_zero(void* out, Dim n, cudaStream_t st);
 // Dense materialisation of an identity / swap tensor's local block (1 where every
 // pairing eq_in[k] == eq_out[k] holds on the global coordinates).

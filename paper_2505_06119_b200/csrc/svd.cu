@@ -687,16 +687,16 @@ __global__ void k_svd_norms(const double2* __restrict__ wk, double* __restrict__
 // not transposed (rows = m): U[:, c] = conj(Q[perm c, :])^T, Vh[c, :] = X[perm c, :] / s
 // transposed (rows = n):     U[:, c] = conj(X[perm c, :])^T / s, Vh[c, :] = Q[perm c, :]
 __global__ void k_svd_output(const double2* __restrict__ wk, const double* __restrict__ sig,
-                             const int* __restrict__ perm, double2* __restrict__ u, double* __restrict__ s,
-                             double2* __restrict__ vh, int64_t m, int64_t n, int64_t rows, int64_t rp, int64_t L, int64_t qw,
+                             const int* __restrict__ perm, double2* const* __restrict__ uptr, double* __restrict__ s,
+                             double2* const* __restrict__ vhptr, int64_t m, int64_t n, int64_t rows, int64_t rp, int64_t L, int64_t qw,
                              int64_t chi, int transpose, int absorb) {
   const int64_t W = L + qw;
   const int64_t mat = blockIdx.y;
   const double2* K = wk + mat * rp * W;
   const double* sg = sig + mat * rp;
   const int* pm = perm + mat * rp;
-  double2* U = u + mat * m * chi;
-  double2* VH = vh + mat * chi * n;
+  double2* U = uptr[mat];
+  double2* VH = vhptr[mat];
   const int64_t nu = m * chi, nv = chi * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nu + nv + chi;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -734,7 +734,7 @@ __global__ void k_svd_output(const double2* __restrict__ wk, const double* __res
 
 // no-Q output: s, Vh (absorbed for right/split), and B[b][x][c] = conj(unit vh_c[x])
 __global__ void k_svd_output_vh(const double2* __restrict__ wk, const double* __restrict__ sig,
-                                const int* __restrict__ perm, double* __restrict__ s, double2* __restrict__ vh,
+                                const int* __restrict__ perm, double* __restrict__ s, double2* const* __restrict__ vhptr,
                                 double2* __restrict__ bt, int64_t n, int64_t rows, int64_t rp, int64_t L, int64_t qw,
                                 int64_t chi, int absorb) {
   const int64_t W = L + qw;
@@ -742,7 +742,7 @@ __global__ void k_svd_output_vh(const double2* __restrict__ wk, const double* __
   const double2* K = wk + mat * rp * W;
   const double* sg = sig + mat * rp;
   const int* pm = perm + mat * rp;
-  double2* VH = vh + mat * chi * n;
+  double2* VH = vhptr[mat];
   double2* BT = bt + mat * n * chi;
   const int64_t nv = chi * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nv + chi;
@@ -769,10 +769,10 @@ __global__ void k_svd_output_vh(const double2* __restrict__ wk, const double* __
 }
 
 // U = (A Vh^H) / sigma^p per column: p = 1 (none, right), 1/2 (split); 0 for sigma = 0
-__global__ void k_svd_scale_u(double2* __restrict__ u, const double* __restrict__ s, int64_t m, int64_t chi,
+__global__ void k_svd_scale_u(double2* const* __restrict__ uptr, const double* __restrict__ s, int64_t m, int64_t chi,
                               int absorb) {
   const int64_t mat = blockIdx.y;
-  double2* U = u + mat * m * chi;
+  double2* U = uptr[mat];
   const double* S = s + mat * chi;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * chi; e += (int64_t)gridDim.x * blockDim.x) {
     double sv = S[e % chi];
@@ -834,9 +834,23 @@ int block_rows() {
   return v;
 }
 
+// Per-matrix streams of the batch split (QTNH_SVD_GROUPS), created once per host
+// thread and device (rank threads are long-lived) instead of on every call.
+cudaStream_t group_stream(int device, int g) {
+  thread_local std::vector<std::vector<cudaStream_t>> cache;
+  if (static_cast<int>(cache.size()) <= device) cache.resize(device + 1);
+  auto& v = cache[device];
+  while (static_cast<int>(v.size()) <= g) {
+    cudaStream_t st;
+    QTNH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    v.push_back(st);
+  }
+  return v[g];
+}
+
 template <int B>
-void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* u, void* s, void* vh,
-              int* sweeps_out) {
+void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* const* u_ptrs, void* s,
+              void* const* vh_ptrs, int* sweeps_out) {
   constexpr int P2 = 2 * B;
   cudaStream_t st = r.stream;
   if (std::getenv("QTNH_SVD_DEBUG"))
@@ -975,9 +989,9 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   const size_t gramx_smem = static_cast<size_t>(2) * P2 * (32 + 4) * 16;
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_gram_mma_t<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)gramx_smem));
-  // The batch runs as two independent halves on two streams when it has >= 2
-  // matrices: the latency-bound eigen step of one half overlaps the other half's
-  // Gram / update DMMA work, and a half that converges stops early.
+  // The batch runs as ngroups independent parts on as many streams when it has
+  // >= 2 matrices: the latency-bound eigen step of one part overlaps the others'
+  // Gram / update DMMA work, and a part that converges stops early.
 
   struct Group {
     Dim base = 0, cnt = 0;
@@ -997,7 +1011,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
     if (ngroups == 1) {
       grp[g].s = st;
     } else {
-      QTNH_CUDA(cudaStreamCreateWithFlags(&grp[g].s, cudaStreamNonBlocking));
+      grp[g].s = group_stream(r.device, g);
       QTNH_CUDA(cudaStreamWaitEvent(grp[g].s, evs[ngroups], 0));
     }
   }
@@ -1020,8 +1034,6 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
       }
     }
     cudaStreamSynchronize(st);
-    for (int g = 0; g < ngroups; ++g)
-      if (ngroups > 1) cudaStreamDestroy(grp[g].s);
     for (auto& e : evs) cudaEventDestroy(e);
   };
   int sweep = 0;
@@ -1183,12 +1195,22 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   }
   DevBuf d_perm(perm.size() * sizeof(int), r);
   QTNH_CUDA(cudaMemcpyAsync(d_perm.ptr, perm.data(), perm.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  // per-matrix output pointers (the batch's outputs may be separate tensors)
+  std::vector<void*> optr(2 * batch);
+  for (Dim b = 0; b < batch; ++b) {
+    optr[b] = u_ptrs[b];
+    optr[batch + b] = vh_ptrs[b];
+  }
+  DevBuf d_optr(optr.size() * sizeof(void*), r);
+  QTNH_CUDA(cudaMemcpyAsync(d_optr.ptr, optr.data(), optr.size() * sizeof(void*), cudaMemcpyHostToDevice, st));
+  double2* const* d_u = static_cast<double2* const*>(d_optr.ptr);
+  double2* const* d_vh = d_u + batch;
   if (acc_q) {
     Dim total = m * chi + chi * n + chi;
     dim3 g(static_cast<unsigned>(std::min<Dim>((total + 255) / 256, 8192)), static_cast<unsigned>(batch));
     k_svd_output<<<g, 256, 0, st>>>(wkp, static_cast<const double*>(sig.ptr),
-                                    static_cast<const int*>(d_perm.ptr), static_cast<double2*>(u),
-                                    static_cast<double*>(s), static_cast<double2*>(vh), m, n, rows, rp, L, qw, chi,
+                                    static_cast<const int*>(d_perm.ptr), d_u,
+                                    static_cast<double*>(s), d_vh, m, n, rows, rp, L, qw, chi,
                                     transpose, absorb);
     QTNH_LAUNCH_CHECK();
   } else {
@@ -1197,15 +1219,15 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
     dim3 g(static_cast<unsigned>(std::min<Dim>((total + 255) / 256, 8192)), static_cast<unsigned>(batch));
     k_svd_output_vh<<<g, 256, 0, st>>>(wkp, static_cast<const double*>(sig.ptr),
                                        static_cast<const int*>(d_perm.ptr), static_cast<double*>(s),
-                                       static_cast<double2*>(vh), static_cast<double2*>(bt.ptr), n, rows, rp, L, qw,
+                                       d_vh, static_cast<double2*>(bt.ptr), n, rows, rp, L, qw,
                                        chi, absorb);
     QTNH_LAUNCH_CHECK();
     for (Dim b = 0; b < batch; ++b)
       zgemm(static_cast<const double2*>(a) + b * m * n, static_cast<const double2*>(bt.ptr) + b * n * chi,
-            static_cast<double2*>(u) + b * m * chi, m, chi, n, st);
+            u_ptrs[b], m, chi, n, st);
     if (absorb != QTNH_ABSORB_LEFT) {
       dim3 g2(static_cast<unsigned>(std::min<Dim>((m * chi + 255) / 256, 8192)), static_cast<unsigned>(batch));
-      k_svd_scale_u<<<g2, 256, 0, st>>>(static_cast<double2*>(u), static_cast<const double*>(s), m, chi, absorb);
+      k_svd_scale_u<<<g2, 256, 0, st>>>(d_u, static_cast<const double*>(s), m, chi, absorb);
       QTNH_LAUNCH_CHECK();
     }
   }
@@ -1214,13 +1236,26 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
 
 }  // namespace
 
-void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* u, void* s,
-                 void* vh, int* sweeps_out) {
+void svd_batched_ptrs(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* const* u_ptrs,
+                      void* s, void* const* vh_ptrs, int* sweeps_out) {
   if (batch < 1 || m < 1 || n < 1) throw_invalid("svd needs positive batch and matrix dimensions");
   if (absorb < 0 || absorb > 3) throw_invalid("invalid absorb mode");
   // Small problems keep 16-row blocks (more pairs per round); large ones can use 32.
-  if (block_rows() == 32 && std::min(m, n) >= 256) svd_impl<32>(r, batch, m, n, a, chi, absorb, u, s, vh, sweeps_out);
-  else svd_impl<16>(r, batch, m, n, a, chi, absorb, u, s, vh, sweeps_out);
+  if (block_rows() == 32 && std::min(m, n) >= 256)
+    svd_impl<32>(r, batch, m, n, a, chi, absorb, u_ptrs, s, vh_ptrs, sweeps_out);
+  else
+    svd_impl<16>(r, batch, m, n, a, chi, absorb, u_ptrs, s, vh_ptrs, sweeps_out);
+}
+
+void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* u, void* s,
+                 void* vh, int* sweeps_out) {
+  const Dim c = chi > 0 ? chi : std::min(m, n);
+  std::vector<void*> up(std::max<Dim>(batch, 1)), vp(std::max<Dim>(batch, 1));
+  for (Dim b = 0; b < batch; ++b) {
+    up[b] = static_cast<char*>(u) + static_cast<size_t>(b * m * c) * 16;
+    vp[b] = static_cast<char*>(vh) + static_cast<size_t>(b * c * n) * 16;
+  }
+  svd_batched_ptrs(r, batch, m, n, a, chi, absorb, up.data(), s, vp.data(), sweeps_out);
 }
 
 }  // namespace qtnhb

@@ -88,61 +88,38 @@ class MPS:
         return s, frac
 
     def apply_layer(self, pairs: Sequence[Tuple[int, int]], g: np.ndarray) -> List[Tuple[np.ndarray, float]]:
-        """Two-site updates of disjoint pairs, with every group of equal-shape thetas
-        factorised by ONE batched Jacobi SVD launch sequence (qtnh_svd_device)."""
-        import torch
-
-        thetas = []
-        for (q, _) in pairs:
-            th = qtnh.contract(self.sites[q], self.sites[q + 1], [2], [0])
-            qtnh.apply_gate(th, [1, 2], g)
-            thetas.append((q, th, th.shape().dims))
-        groups: dict = {}
-        for q, th, sh in thetas:
-            groups.setdefault(tuple(sh), []).append((q, th))
-        results = {}
-        dev = torch.device("cuda")
-        for sh, items in groups.items():
-            l, d1, d2, r = sh
-            m, n = l * d1, d2 * r
-            k = min(m, n)
-            keep = min(self.chi, k)
-            bsz = len(items)
-            a = torch.empty((bsz, m, n), dtype=torch.complex128, device=dev)
-            for i, (q, th) in enumerate(items):
-                src = torch.as_tensor(_DevView(th.device_ptr(), m * n), device=dev)
-                a[i].view(-1).copy_(src)
-            dump = os.environ.get("QTNH_MPS_DUMP")  # debugging aid: save one saturated theta
-            if dump and m == n == 2 * self.chi and not os.path.exists(dump):
-                np.save(dump, a[0].cpu().numpy())
-            # Only the kept triplets are formed (the U S = A Vh^H output GEMM and the
-            # output kernels shrink to chi columns); the discarded weight comes from
-            # ||theta||_F^2 = sum of all s^2 (linalg.hpp:476-505 keeps the chi largest).
-            u = torch.empty((bsz, m, keep), dtype=torch.complex128, device=dev)
-            s = torch.empty((bsz, keep), dtype=torch.float64, device=dev)
-            vh = torch.empty((bsz, keep, n), dtype=torch.complex128, device=dev)
-            tot_h = (a.real.square() + a.imag.square()).sum(dim=(1, 2)).cpu().numpy() if keep < k else None
-            qtnh.check(qtnh.lib.qtnh_svd_device(self.rank._h, bsz, m, n, C.c_void_p(a.data_ptr()), keep, ABSORB_LEFT,
-                                                C.c_void_p(u.data_ptr()), C.c_void_p(s.data_ptr()),
-                                                C.c_void_p(vh.data_ptr())))
-            s_h = s.cpu().numpy()
-            for i, (q, th) in enumerate(items):
-                frac = 1.0
-                if keep < k:
-                    tot = float(tot_h[i])
-                    frac = float(np.sum(s_h[i] ** 2)) / tot if tot > 0 else 1.0
-                    self.log_fidelity += np.log(frac)
-                ui = u[i, :, :keep].contiguous()
-                vi = vh[i, :keep, :].contiguous()
-                nu = Tensor.from_device(self.rank, IndexTuple([l, d1, keep], 0), self.dist, ui.data_ptr())
-                nv = Tensor.from_device(self.rank, IndexTuple([keep, d2, r], 0), self.dist, vi.data_ptr())
-                self.rank.synchronize()  # the torch temporaries die at the end of the loop
-                self.sites[q].free()
-                self.sites[q + 1].free()
-                self.sites[q], self.sites[q + 1] = nu, nv
-                th.free()
-                results[q] = (s_h[i][:keep], frac)
-        return [results[q] for (q, _) in pairs]
+        """Two-site updates of disjoint pairs in ONE native call (qtnh_mps_apply_layer,
+        csrc/mps.cu): thetas formed by zgemm straight into the batched-SVD buffer, the
+        gate in place, every group of equal-shape thetas factorised by one batched
+        Jacobi SVD whose outputs are the new site tensors; no torch, no per-update
+        synchronisation. Returns (kept singular values, kept weight fraction) per pair."""
+        n = len(pairs)
+        if n == 0:
+            return []
+        left = (C.c_void_p * n)(*[self.sites[q]._h for q, _ in pairs])
+        right = (C.c_void_p * n)(*[self.sites[q + 1]._h for q, _ in pairs])
+        nl, nr = (C.c_void_p * n)(), (C.c_void_p * n)()
+        gate = np.ascontiguousarray(g, dtype=np.complex128)
+        s = np.zeros((n, self.chi), dtype=np.float64)
+        keep = np.zeros(n, dtype=np.int64)
+        nrm = np.zeros(n, dtype=np.float64)
+        qtnh.check(qtnh.lib.qtnh_mps_apply_layer(n, left, right, gate.ctypes.data, self.chi, nl, nr, s.ctypes.data,
+                                                 keep.ctypes.data, nrm.ctypes.data))
+        out = []
+        for i, (q, _) in enumerate(pairs):
+            a, b = self.sites[q], self.sites[q + 1]
+            l, d1, _ = a.shape().dims
+            _, d2, r = b.shape().dims
+            si = s[i, : keep[i]].copy()
+            frac = 1.0
+            if keep[i] < min(l * d1, d2 * r):  # truncated: kept weight of this update
+                frac = float(np.sum(si**2)) / float(nrm[i]) if nrm[i] > 0 else 1.0
+                self.log_fidelity += np.log(frac)
+            a.free()
+            b.free()
+            self.sites[q], self.sites[q + 1] = Tensor(self.rank, C.c_void_p(nl[i])), Tensor(self.rank, C.c_void_p(nr[i]))
+            out.append((si, frac))
+        return out
 
     def bond_dims(self) -> List[int]:
         return [t.shape().dims[2] for t in self.sites[:-1]]
@@ -196,19 +173,38 @@ class MPS:
         if not 0 <= centre < self.n:
             raise qtnh.InvalidArgument("canonical centre outside the chain")
         for q in range(centre):
-            u, _, svh = qtnh.svd(self.sites[q], [0, 1], [2], absorb=ABSORB_RIGHT)
+            u, sv, svh = qtnh.svd(self.sites[q], [0, 1], [2], absorb=ABSORB_RIGHT)
+            u, svh = self._drop_null(u, svh, sv)
             nxt = qtnh.contract(svh, self.sites[q + 1], [1], [0])  # (k, d, r)
             svh.free()
             self._set(q, u)
             self._set(q + 1, nxt)
         for q in range(self.n - 1, centre, -1):
-            us, _, vh = qtnh.svd(self.sites[q], [0], [1, 2], absorb=ABSORB_LEFT)
+            us, sv, vh = qtnh.svd(self.sites[q], [0], [1, 2], absorb=ABSORB_LEFT)
+            us, vh = self._drop_null(us, vh, sv)
             prv = qtnh.contract(self.sites[q - 1], us, [2], [0])  # (l, d, k)
             us.free()
             self._set(q, vh)
             self._set(q - 1, prv)
         self.centre = centre
         return self
+
+    @staticmethod
+    def _drop_null(u: Tensor, vh: Tensor, sv: np.ndarray) -> Tuple[Tensor, Tensor]:
+        """Drop the singular triplets with sigma <= 1e-13 sigma_max from a split: the
+        Jacobi SVD returns zero vectors for a null space (no orthonormal completion),
+        so a rank-deficient site keeps its isometry (A A^H = I) only on
+        the bond's effective rank. The dropped directions carry no weight."""
+        k = sv.size
+        keep = max(1, int(np.sum(sv > 1e-13 * sv[0]))) if k and sv[0] > 0 else max(1, k)
+        if keep == k:
+            return u, vh
+        ud, vd = u.shape().dims, vh.shape().dims
+        u2 = qtnh.ops.slice_local_dims(u, ud[:-1] + [keep])
+        v2 = qtnh.ops.slice_local_dims(vh, [keep] + vd[1:])
+        u.free()
+        vh.free()
+        return u2, v2
 
     def overlap(self, other: "MPS") -> complex:
         """<other|self> by the transfer-matrix contraction left to right:
@@ -416,6 +412,19 @@ class MPS:
 
         B = bitstrings.shape[0]
         dev = torch.device("cuda")
+        # The sites were written on the rank's stream; torch works on its current
+        # stream. Drain the rank stream before torch reads, and launch the zgemms on
+        # torch's stream for the duration (restored afterwards).
+        self.rank.synchronize()
+        prev = self.rank.stream_ptr()
+        self.rank.set_stream(torch.cuda.current_stream().cuda_stream)
+        try:
+            return self._amplitudes_on_torch_stream(bitstrings, torch, dev, B)
+        finally:
+            torch.cuda.current_stream().synchronize()
+            self.rank.set_stream(prev)
+
+    def _amplitudes_on_torch_stream(self, bitstrings, torch, dev, B):
         env = torch.ones((B, 1), dtype=torch.complex128, device=dev)
         for q in range(self.n):
             t = self.sites[q]

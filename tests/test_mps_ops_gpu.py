@@ -302,3 +302,61 @@ def test_truncated_mpo_lowers_norm():
 
     n2, logf, bmax = run_collect(World(1), body)
     assert n2 < 1.0 and logf < 0.0 and bmax <= 4
+
+
+def test_canonicalize_rank_deficient_site_stays_isometric():
+    """|00> then CNOT-like entangling that leaves a zero Schmidt value: bond 2 of a
+    bitstring MPS after a gate has sigma = (1, 0). The canonical sites must still
+    be isometries -- zero-sigma directions are dropped from the bond."""
+    cnot = np.eye(4, dtype=complex)[[0, 1, 3, 2]]
+
+    def body(rk):
+        m = MPS.bitstring(rk, [0, 0, 0], chi=4)
+        m.apply_layer([(0, 1)], cnot)  # product state stays product: bond (0,1) sigma = (1, 0)
+        m.apply_1q(1, circuits.H)
+        m.apply_layer([(1, 2)], cnot)
+        before = m.to_statevector()
+        m.canonicalize(2)
+        after = m.to_statevector()
+        out = (before, after, site_arrays(m))
+        m.free()
+        return out
+
+    before, after, sites = run_collect(World(1), body)
+    assert rel_l2(after, before) < 1e-12
+    for q, a in enumerate(sites[:2]):
+        r = a.shape[2]
+        g = np.einsum("lsr,lsk->rk", a.conj(), a)
+        assert np.allclose(g, np.eye(r), atol=1e-10), (q, a.shape)
+
+
+def test_apply_layer_native_matches_dense_evolution():
+    """qtnh_mps_apply_layer (one native call per layer) against the dense statevector
+    with the same gates, no truncation (chi ample), and with truncation the kept
+    weights multiply to the reported fidelity."""
+    from paper_2505_06119_b200 import mps as M
+
+    n, depth = 8, 6
+    layers = M.rcs_1d_layers(n, depth, 5)
+
+    def body(rk):
+        m = MPS(rk, n, 64)
+        psi = np.zeros(2**n, complex)
+        psi[0] = 1
+        for singles, pairs in layers:
+            for q, g in enumerate(singles):
+                m.apply_1q(q, M.SINGLE_QUBIT[g])
+                psi = np.moveaxis(np.tensordot(M.SINGLE_QUBIT[g], np.moveaxis(psi.reshape([2] * n), q, 0),
+                                               axes=([1], [0])), 0, q).reshape(-1)
+            m.apply_layer(pairs, circuits.FSIM)
+            for q, _ in pairs:
+                t = np.moveaxis(psi.reshape([2] * n), [q, q + 1], [0, 1]).reshape(4, -1)
+                t = (circuits.FSIM @ t).reshape([2, 2] + [2] * (n - 2))
+                psi = np.moveaxis(t, [0, 1], [q, q + 1]).reshape(-1)
+        out = (m.to_statevector(), psi, m.log_fidelity)
+        m.free()
+        return out
+
+    got, want, logf = run_collect(World(1), body)
+    assert logf == 0.0
+    assert rel_l2(got, want) < 1e-12
