@@ -537,8 +537,13 @@ def run_gpu_arm(args):
             ta.free()
             tb.free()
             torch.cuda.synchronize()
-            if not args.skip_extras:
+            if not args.skip_extras and world_size == 1:
                 result["extras"] = measure_extras(rk, stream, torch)
+            if not args.skip_configs and world_size > 1:
+                import bench_legs
+
+                shared = world_size > torch.cuda.device_count()
+                result["c2_sharded"] = bench_legs.gpu_c2_sharded(rk, stream, torch, dist, world_size, rank, shared)
             if not args.skip_configs and world_size == 1:
                 import bench_legs
 
@@ -619,6 +624,7 @@ def run_gpu_arm(args):
             "gpu_launches": result["launches"],
             "extras": result.get("extras"),
             "configs": result.get("configs"),
+            "c2_sharded": result.get("c2_sharded"),
             "clocks": result["clocks"],
         }
         print(json.dumps(line), flush=True)

@@ -392,3 +392,91 @@ def run_all(rk, stream, torch, log=None):
             log(f"leg {name}")
         leg(name, fn)
     return out
+
+
+# ---- C2 sharded (bench.py --gpus N under torchrun) -----------------------------------------------
+def gpu_c2_sharded(rk, stream, torch, dist, world_size, rank, shared_gpu, swaps=5, spots=4):
+    """QFT on a state sharded over the world (split s = log2 N, the leading s
+    qubits select the GPU) and the local<->distributed index
+    swap it is built from, timed on the device and reduced as the max over ranks:
+      * swap: qubit 0 (distributed) <-> qubit n-1 (local), in place; every GPU
+        sends and receives half its shard: 16 * 2^(n-s-1) B per direction;
+      * the whole QFT (distributed layers fused over peer memory, local layers
+        cache-blocked, bit reversal) with norm and DFT spot-amplitude checks.
+    n = 34 when every rank has its own GPU (BASELINE.json configs[2]); with
+    ranks sharing a GPU n = 30 + s (16 GiB per rank) and the bytes stay in HBM."""
+    from paper_2505_06119_b200 import qtnh
+    from paper_2505_06119_b200.mps import _DevView
+    from paper_2505_06119_b200.qtnh import DistParams, IndexTuple, Tensor
+
+    s = (world_size - 1).bit_length()
+    n = 30 + s if shared_gpu else 34
+    nl = n - s
+    N, NL = 2**n, 2**nl
+    t = Tensor.dense(rk, IndexTuple([2] * n, s), DistParams(1, 1, 0), None)
+    psi = torch.as_tensor(_DevView(t.device_ptr(), NL), device="cuda")
+    chunk = min(NL, 2**27)
+
+    def allsum(x):
+        v = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(v)
+        return float(v.item())
+
+    def allmax(x):
+        v = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        return float(v.item())
+
+    with torch.cuda.stream(stream):
+        qtnh.check(qtnh.lib.qtnh_counter_complex_normals_device(C.c_void_p(stream.cuda_stream), SEED, rank * NL, NL,
+                                                                C.c_void_p(t.device_ptr())))
+        nrm2 = allsum(sum(float(psi[c:c + chunk].abs().pow(2).sum()) for c in range(0, NL, chunk)))
+        psi.mul_(1.0 / math.sqrt(nrm2))
+        rng = np.random.default_rng(SEED)
+        ks = [0, 1, N - 1] + [int(x) for x in rng.integers(2, N - 1, size=max(0, spots - 3))]
+        want = {}
+        for k in ks:  # partial DFT sums over this shard, summed over ranks
+            acc = torch.zeros((), dtype=torch.complex128, device="cuda")
+            for c in range(0, NL, chunk):
+                j = torch.arange(rank * NL + c, rank * NL + c + chunk, dtype=torch.int64, device="cuda")
+                ph = torch.remainder(j * k, N).to(torch.float64) * (2 * math.pi / N)
+                acc += (psi[c:c + chunk] * torch.polar(torch.ones_like(ph), ph)).sum()
+            z = complex(acc.item())
+            want[k] = complex(allsum(z.real), allsum(z.imag)) / math.sqrt(N)
+        stream.synchronize()
+        e0, e1 = _events(torch, stream)
+        for _ in range(2):  # warm-up (an even count restores the state)
+            qtnh.swap_indices(t, 0, n - 1)
+        rk.synchronize()
+        dist.barrier()
+        e0.record(stream)
+        for _ in range(2 * swaps):
+            qtnh.swap_indices(t, 0, n - 1)
+        e1.record(stream)
+        e1.synchronize()
+        swap_ms = allmax(e0.elapsed_time(e1) / (2 * swaps))
+        dist.barrier()
+        e0.record(stream)
+        qtnh.qft(t, swaps=True)
+        e1.record(stream)
+        e1.synchronize()
+        qft_ms = allmax(e0.elapsed_time(e1))
+        nrm = math.sqrt(allsum(sum(float(psi[c:c + chunk].abs().pow(2).sum()) for c in range(0, NL, chunk))))
+        errs = []
+        for k, w in want.items():
+            owner = k >> nl
+            v = complex(psi[k - owner * NL].item()) if owner == rank else 0j
+            v = complex(allsum(v.real), allsum(v.imag))
+            errs.append(abs(v - w) / abs(w))
+    t.free()
+    bytes_dir = 16.0 * 2 ** (nl - 1)
+    gbs = bytes_dir / (swap_ms * 1e-3) / 1e9
+    gates = n + n * (n - 1) // 2 + n // 2
+    return {"n": n, "split": s, "ranks": world_size, "shard_GiB": 16.0 * NL / 2**30,
+            "swap_dist_local_ms": swap_ms, "swap_bytes_per_gpu_per_direction": bytes_dir,
+            "swap_GBps_per_direction": gbs, "swap_frac_of_900GBps_nvlink": gbs / 900.0,
+            "qft_ms": qft_ms, "qft_gates": gates,
+            "qft_effective_GBps_per_gpu_32B_per_gate": gates * 32.0 * NL / (qft_ms * 1e-3) / 1e9,
+            "norm_after": nrm, "dft_spot_max_rel_err": max(errs),
+            "note": ("ranks share one GPU: the swap moves bytes inside HBM, not over NVLink" if shared_gpu
+                     else "one GPU per rank: the swap moves bytes over NVLink (peer stores / NCCL)")}

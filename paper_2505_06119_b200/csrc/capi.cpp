@@ -4,6 +4,8 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
+#include <chrono>
 
 #include "nccl_loader.h"
 #include "ops.h"
@@ -94,7 +96,12 @@ int qtnh_world_create_local(int n, const int* devices, qtnh_world_t* out) {
     w->size = n;
     w->timeout_ms = env_timeout();
     for (int i = 0; i < n; ++i) w->devices.push_back(devices ? devices[i] : 0);
-    for (int d : w->devices) keep_pool(d);
+    {  // one keep per distinct device (qtnh_world_destroy trims each distinct device once)
+      std::vector<int> uniq = w->devices;
+      std::sort(uniq.begin(), uniq.end());
+      uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+      for (int d : uniq) keep_pool(d);
+    }
     // Peer access between distinct devices (NVLink) for the exchange copies and
     // the peer-memory kernels (remap push, in-place swaps).
     w->peer_ok = true;
@@ -151,8 +158,36 @@ int qtnh_world_create_nccl(int rank, int size, int device, const void* uid128, q
     keep_pool(device);
     ncclUniqueId id;
     std::memcpy(&id, uid128, sizeof(id));
-    ncclComm_t comm;
-    nccl_check(nccl().CommInitRank(&comm, size, id, rank), "comm init");
+    ncclComm_t comm = nullptr;
+    const Nccl& N = nccl();
+    if (N.CommInitRankConfig) {
+      // Non-blocking initialisation polled against the collective timeout: a
+      // missing peer aborts the communicator and raises ProtocolError instead of
+      // blocking forever (runtime.hpp:335-345). Blocking mode is restored after
+      // init so every later NCCL call completes its enqueue before returning.
+      ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      cfg.blocking = 0;
+      ncclResult_t rc = N.CommInitRankConfig(&comm, size, id, rank, &cfg);
+      if (rc != ncclSuccess && rc != ncclInProgress) nccl_check(rc, "comm init");
+      auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(w->timeout_ms > 0 ? w->timeout_ms : 1L << 40);
+      ncclResult_t st = ncclInProgress;
+      while (true) {
+        N.CommGetAsyncError(comm, &st);
+        if (st != ncclInProgress) break;
+        if (std::chrono::steady_clock::now() > deadline) {
+          N.CommAbort(comm);
+          throw Status(QTNH_E_PROTOCOL, "NCCL communicator initialisation timed out (rank " + std::to_string(rank) +
+                                            " of " + std::to_string(size) + "; missing peers?)");
+        }
+        std::this_thread::sleep_for(std::chrono::milliseconds(1));
+      }
+      if (st != ncclSuccess) {
+        N.CommAbort(comm);
+        nccl_check(st, "comm init");
+      }
+    } else {
+      nccl_check(N.CommInitRank(&comm, size, id, rank), "comm init");
+    }
     w->nccl_comm = comm;
     auto rc = std::make_unique<RankCtx>();
     rc->world = w.get();
@@ -204,10 +239,10 @@ int qtnh_world_destroy(qtnh_world_t w) {
       delete w;
       return;
     }
-    if (w->w->kind == World::kNccl && w->w->nccl_comm) {
+    if (w->w->kind == World::kNccl) {
       cudaSetDevice(w->w->proc_rank->device);
       cudaStreamSynchronize(w->w->proc_rank->stream);
-      nccl().CommDestroy(static_cast<ncclComm_t>(w->w->nccl_comm));
+      if (w->w->nccl_comm) nccl().CommDestroy(static_cast<ncclComm_t>(w->w->nccl_comm));
       cudaStreamDestroy(w->w->proc_rank->own_stream);
     }
     std::vector<int> devs = w->w->kind == World::kNccl ? std::vector<int>{w->w->proc_rank->device} : w->w->devices;
@@ -223,6 +258,10 @@ int qtnh_world_size(qtnh_world_t w) { return w ? w->w->size : 0; }
 int qtnh_world_abort(qtnh_world_t w) {
   return guard([&] {
     need(w, "world");
+    if (w->w->kind == World::kNccl) {  // ncclCommAbort: peers blocked in NCCL fail instead of hanging
+      nccl_abort(*w->w);
+      return;
+    }
     std::lock_guard<std::mutex> lk(w->w->mu);
     w->w->aborted = true;
     w->w->cv.notify_all();

@@ -32,6 +32,9 @@ const Nccl& nccl() {
   g_nccl.CommInitRank = reinterpret_cast<decltype(g_nccl.CommInitRank)>(sym(h, "ncclCommInitRank"));
   g_nccl.CommDestroy = reinterpret_cast<decltype(g_nccl.CommDestroy)>(sym(h, "ncclCommDestroy"));
   g_nccl.CommAbort = reinterpret_cast<decltype(g_nccl.CommAbort)>(sym(h, "ncclCommAbort"));
+  g_nccl.CommGetAsyncError =
+      reinterpret_cast<decltype(g_nccl.CommGetAsyncError)>(sym(h, "ncclCommGetAsyncError"));
+  g_nccl.CommInitRankConfig = reinterpret_cast<decltype(g_nccl.CommInitRankConfig)>(dlsym(h, "ncclCommInitRankConfig"));
   g_nccl.Send = reinterpret_cast<decltype(g_nccl.Send)>(sym(h, "ncclSend"));
   g_nccl.Recv = reinterpret_cast<decltype(g_nccl.Recv)>(sym(h, "ncclRecv"));
   g_nccl.GroupStart = reinterpret_cast<decltype(g_nccl.GroupStart)>(sym(h, "ncclGroupStart"));

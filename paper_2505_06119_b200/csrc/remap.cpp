@@ -468,44 +468,94 @@ void op_swap_dist_local_inplace(TP& t, int a, int b, Dim chunk_bytes) {
     peer_pointers(r, members, nullptr);
     return;
   }
-  // canonicalise the region that stays (b = my_i) in place
+  // Exchange form (NCCL world, or peer_direct off): a three-stage pipeline over
+  // two staging pairs -- pack chunk c+1 (side stream 0) and unpack chunk c-1
+  // (side stream 1) overlap the exchange of chunk c on the rank stream. Events
+  // keep each staging buffer free until its previous user is done. Counts are
+  // identical for every chunk, so the NCCL form verifies them once and waits for
+  // completion once, at the end.
   canon_region(static_cast<char*>(t->data()) + my_i * ls[lb] * 16, rdims, rstr, r.stream);
-  for (Dim ch = 0; ch < n_chunks; ++ch) {
-    auto oc = unflat(ch, odims);
-    Dim obase = 0;
-    for (size_t k = 0; k < oc.size(); ++k) obase += oc[k] * ostr[k];
-    std::vector<Xfer> sends, recvs;
-    int slot = 0;
-    for (Dim j = 0; j < d; ++j) {
-      if (j == my_i) continue;
-      // my region b = j (offset j * stride_b) -> staging slot
-      CopyBox pk;
-      pk.dims = idims;
-      pk.in_stride = istr;
-      pk.out_stride = irow;
-      const char* src = static_cast<const char*>(t->data()) + (obase + j * ls[lb]) * 16;
-      strided_copy(src, static_cast<char*>(sbuf.ptr) + slot * per_chunk * 16, pk, true, r.stream);
-      auto pc = cd;
-      pc[a] = j;
-      Dim pblock = flat(pc, ddims);
-      int peer = t->dist.home(pblock, nd, t->cycle, t->slot);
-      sends.push_back({peer, slot * per_chunk, per_chunk});
-      recvs.push_back({peer, slot * per_chunk, per_chunk});
-      ++slot;
-    }
-    exchange(r, members, sbuf.ptr, sends, rbuf.ptr, recvs);
-    slot = 0;
-    for (Dim j = 0; j < d; ++j) {
-      if (j == my_i) continue;
-      CopyBox up;
-      up.dims = idims;
-      up.in_stride = irow;
-      up.out_stride = istr;
-      char* dst = static_cast<char*>(t->data()) + (obase + j * ls[lb]) * 16;
-      strided_copy(static_cast<char*>(rbuf.ptr) + slot * per_chunk * 16, dst, up, false, r.stream);
-      ++slot;
-    }
+  DevBuf sbuf2(static_cast<size_t>(per_chunk * std::max(1, partners)) * 16, r);
+  DevBuf rbuf2(static_cast<size_t>(per_chunk * std::max(1, partners)) * 16, r);
+  char* sb[2] = {static_cast<char*>(sbuf.ptr), static_cast<char*>(sbuf2.ptr)};
+  char* rb[2] = {static_cast<char*>(rbuf.ptr), static_cast<char*>(rbuf2.ptr)};
+  cudaStream_t pk_st = r.side_stream(0), up_st = r.side_stream(1);
+  cudaEvent_t start, packed[2], xfered[2], unpacked[2];
+  auto mk = [](cudaEvent_t& e) { QTNH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); };
+  mk(start);
+  for (int k = 0; k < 2; ++k) {
+    mk(packed[k]);
+    mk(xfered[k]);
+    mk(unpacked[k]);
   }
+  QTNH_CUDA(cudaEventRecord(start, r.stream));
+  QTNH_CUDA(cudaStreamWaitEvent(pk_st, start, 0));
+  QTNH_CUDA(cudaStreamWaitEvent(up_st, start, 0));
+  std::vector<Dim> peers;
+  for (Dim j = 0; j < d; ++j)
+    if (j != my_i) peers.push_back(j);
+  auto peer_of = [&](Dim j) {
+    auto pc = cd;
+    pc[a] = j;
+    return t->dist.home(flat(pc, ddims), nd, t->cycle, t->slot);
+  };
+  try {
+    for (Dim ch = 0; ch < n_chunks; ++ch) {
+      const int k = static_cast<int>(ch & 1);
+      auto oc = unflat(ch, odims);
+      Dim obase = 0;
+      for (size_t q = 0; q < oc.size(); ++q) obase += oc[q] * ostr[q];
+      // pack: sb[k] is free once the exchange of chunk ch-2 has read it
+      if (ch >= 2) QTNH_CUDA(cudaStreamWaitEvent(pk_st, xfered[k], 0));
+      std::vector<Xfer> sends, recvs;
+      for (size_t sl = 0; sl < peers.size(); ++sl) {
+        CopyBox pk;
+        pk.dims = idims;
+        pk.in_stride = istr;
+        pk.out_stride = irow;
+        const char* src = static_cast<const char*>(t->data()) + (obase + peers[sl] * ls[lb]) * 16;
+        strided_copy(src, sb[k] + sl * per_chunk * 16, pk, true, pk_st);
+        const int peer = peer_of(peers[sl]);
+        sends.push_back({peer, static_cast<Dim>(sl) * per_chunk, per_chunk});
+        recvs.push_back({peer, static_cast<Dim>(sl) * per_chunk, per_chunk});
+      }
+      QTNH_CUDA(cudaEventRecord(packed[k], pk_st));
+      // exchange on the rank stream: rb[k] is free once chunk ch-2 is unpacked
+      QTNH_CUDA(cudaStreamWaitEvent(r.stream, packed[k], 0));
+      if (ch >= 2) QTNH_CUDA(cudaStreamWaitEvent(r.stream, unpacked[k], 0));
+      exchange(r, members, sb[k], sends, rb[k], recvs, /*checked=*/ch == 0, /*wait=*/false);
+      QTNH_CUDA(cudaEventRecord(xfered[k], r.stream));
+      // unpack
+      QTNH_CUDA(cudaStreamWaitEvent(up_st, xfered[k], 0));
+      for (size_t sl = 0; sl < peers.size(); ++sl) {
+        CopyBox up;
+        up.dims = idims;
+        up.in_stride = irow;
+        up.out_stride = istr;
+        char* dst = static_cast<char*>(t->data()) + (obase + peers[sl] * ls[lb]) * 16;
+        strided_copy(rb[k] + sl * per_chunk * 16, dst, up, false, up_st);
+      }
+      QTNH_CUDA(cudaEventRecord(unpacked[k], up_st));
+    }
+  } catch (...) {
+    QTNH_CUDA(cudaEventRecord(unpacked[0], up_st));
+    cudaStreamWaitEvent(r.stream, unpacked[0], 0);
+    cudaStreamWaitEvent(r.stream, packed[0], 0);
+    throw;
+  }
+  // the rank stream continues after the last unpack (and the staging buffers,
+  // freed stream-ordered on it, outlive every side-stream use)
+  QTNH_CUDA(cudaEventRecord(unpacked[0], up_st));
+  QTNH_CUDA(cudaEventRecord(packed[0], pk_st));
+  QTNH_CUDA(cudaStreamWaitEvent(r.stream, unpacked[0], 0));
+  QTNH_CUDA(cudaStreamWaitEvent(r.stream, packed[0], 0));
+  cudaEventDestroy(start);
+  for (int k = 0; k < 2; ++k) {
+    cudaEventDestroy(packed[k]);
+    cudaEventDestroy(xfered[k]);
+    cudaEventDestroy(unpacked[k]);
+  }
+  nccl_wait(r);
 }
 
 }  // namespace qtnhb

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <thread>
 #include <cstdlib>
 
 #include "nccl_loader.h"
@@ -12,6 +13,16 @@ namespace qtnhb {
 std::atomic<int64_t> g_kernel_launches{0};
 
 void RankCtx::activate() const { QTNH_CUDA(cudaSetDevice(device)); }
+
+cudaStream_t RankCtx::side_stream(int i) {
+  if (!side[i]) QTNH_CUDA(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
+  return side[i];
+}
+
+RankCtx::~RankCtx() {
+  for (auto& st : side)
+    if (st) cudaStreamDestroy(st);
+}
 
 // Tensors come from the device's stream-ordered pool. The default release
 // threshold (0) hands freed pages back to the driver at every synchronisation,
@@ -245,10 +256,106 @@ void local_exchange(RankCtx& r, const std::vector<int>& members, const void* sen
 }
 
 // ---- NCCL backend --------------------------------------------------------------
-void nccl_exchange(RankCtx& r, const void* send_buf, const std::vector<Xfer>& sends,
-                   void* recv_buf, const std::vector<Xfer>& recvs) {
+// Failure semantics of the simulated runtime carried over to NCCL:
+//  * counts: every member pair swaps (elements I send you, elements I expect from
+//    you) before the payload, so a mismatch is seen on BOTH sides of the pair and
+//    raised as ProtocolError "(src -> dst)" (runtime.hpp:464-471) instead of a hang;
+//  * timeout: completion is awaited by polling the stream and
+//    ncclCommGetAsyncError; past QTNH_COLLECTIVE_TIMEOUT_MS the communicator is
+//    aborted (ncclCommAbort) and ProtocolError "collective timed out" raised
+//    (runtime.hpp:335-345);
+//  * abort: qtnh_world_abort aborts the communicator; later calls raise
+//    AbortedError (runtime.hpp:276-298).
+void nccl_abort_comm(World& w) {
+  std::lock_guard<std::mutex> lk(w.mu);
+  if (w.nccl_comm && !w.aborted) nccl().CommAbort(static_cast<ncclComm_t>(w.nccl_comm));
+  if (w.nccl_comm) w.nccl_comm = nullptr;
+  w.aborted = true;
+  w.cv.notify_all();
+}
+
+void nccl_wait_impl(RankCtx& r) {
+  World& w = *r.world;
   const Nccl& N = nccl();
-  auto comm = static_cast<ncclComm_t>(r.world->nccl_comm);
+  cudaEvent_t ev;
+  QTNH_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  QTNH_CUDA(cudaEventRecord(ev, r.stream));
+  auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(w.timeout_ms > 0 ? w.timeout_ms : 1L << 40);
+  for (int spin = 0;; ++spin) {
+    cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) {
+      cudaEventDestroy(ev);
+      QTNH_CUDA(q);
+    }
+    if (w.aborted) {
+      cudaEventDestroy(ev);
+      throw Status(QTNH_E_ABORTED, "world aborted");
+    }
+    ncclResult_t ae = ncclSuccess;
+    if (w.nccl_comm) N.CommGetAsyncError(static_cast<ncclComm_t>(w.nccl_comm), &ae);
+    if (ae != ncclSuccess && ae != ncclInProgress) {
+      cudaEventDestroy(ev);
+      nccl_abort_comm(w);
+      throw Status(QTNH_E_RUNTIME, std::string("NCCL asynchronous error: ") + N.GetErrorString(ae));
+    }
+    if (std::chrono::steady_clock::now() > deadline) {
+      cudaEventDestroy(ev);
+      nccl_abort_comm(w);
+      throw Status(QTNH_E_PROTOCOL, "collective timed out (possible deadlock)");
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  cudaEventDestroy(ev);
+}
+
+ncclComm_t nccl_comm_of(RankCtx& r) {
+  if (r.world->aborted || !r.world->nccl_comm) throw Status(QTNH_E_ABORTED, "world aborted");
+  return static_cast<ncclComm_t>(r.world->nccl_comm);
+}
+
+void nccl_check_counts(RankCtx& r, const std::vector<int>& members, const std::vector<Xfer>& sends,
+                       const std::vector<Xfer>& recvs) {
+  const Nccl& N = nccl();
+  ncclComm_t comm = nccl_comm_of(r);
+  const int n = static_cast<int>(members.size());
+  std::vector<int64_t> out(2 * n, 0), in(2 * n, 0);
+  for (int i = 0; i < n; ++i) {
+    for (const Xfer& x : sends)
+      if (x.peer == members[i]) out[2 * i] += x.count;
+    for (const Xfer& x : recvs)
+      if (x.peer == members[i]) out[2 * i + 1] += x.count;
+  }
+  DevBuf ob(16 * n, r), ib(16 * n, r);
+  QTNH_CUDA(cudaMemcpyAsync(ob.ptr, out.data(), 16 * n, cudaMemcpyHostToDevice, r.stream));
+  nccl_check(N.GroupStart(), "group start");
+  for (int i = 0; i < n; ++i) {
+    if (members[i] == r.rank) continue;
+    nccl_check(N.Send(static_cast<char*>(ob.ptr) + 16 * i, 16, ncclUint8, members[i], comm, r.stream), "send");
+    nccl_check(N.Recv(static_cast<char*>(ib.ptr) + 16 * i, 16, ncclUint8, members[i], comm, r.stream), "recv");
+  }
+  nccl_check(N.GroupEnd(), "group end");
+  QTNH_CUDA(cudaMemcpyAsync(in.data(), ib.ptr, 16 * n, cudaMemcpyDeviceToHost, r.stream));
+  nccl_wait_impl(r);
+  for (int i = 0; i < n; ++i) {
+    if (members[i] == r.rank) continue;
+    // in[2i] = what member i sends me; in[2i+1] = what member i expects from me
+    if (in[2 * i] != out[2 * i + 1])
+      throw Status(QTNH_E_PROTOCOL, "exchange count mismatch for pair (" + std::to_string(members[i]) + " -> " +
+                                        std::to_string(r.rank) + "): got " + std::to_string(in[2 * i]) +
+                                        ", expected " + std::to_string(out[2 * i + 1]));
+    if (in[2 * i + 1] != out[2 * i])
+      throw Status(QTNH_E_PROTOCOL, "exchange count mismatch for pair (" + std::to_string(r.rank) + " -> " +
+                                        std::to_string(members[i]) + "): got " + std::to_string(out[2 * i]) +
+                                        ", expected " + std::to_string(in[2 * i + 1]));
+  }
+}
+
+void nccl_exchange(RankCtx& r, const std::vector<int>& members, const void* send_buf, const std::vector<Xfer>& sends,
+                   void* recv_buf, const std::vector<Xfer>& recvs, bool checked, bool wait) {
+  const Nccl& N = nccl();
+  ncclComm_t comm = nccl_comm_of(r);
+  if (checked && members.size() > 1) nccl_check_counts(r, members, sends, recvs);
   // Self chunks: direct device copies, matched in order.
   std::vector<const Xfer*> self_s, self_r;
   for (const Xfer& s : sends)
@@ -279,6 +386,7 @@ void nccl_exchange(RankCtx& r, const void* send_buf, const std::vector<Xfer>& se
                         v.peer, comm, r.stream),
                  "recv");
   nccl_check(N.GroupEnd(), "group end");
+  if (wait) nccl_wait_impl(r);
 }
 
 }  // namespace
@@ -338,15 +446,22 @@ std::vector<void*> peer_pointers(RankCtx& r, const std::vector<int>& members, vo
 }
 
 void exchange(RankCtx& r, const std::vector<int>& members, const void* send_buf,
-              const std::vector<Xfer>& sends, void* recv_buf, const std::vector<Xfer>& recvs) {
+              const std::vector<Xfer>& sends, void* recv_buf, const std::vector<Xfer>& recvs, bool checked,
+              bool wait) {
   if (r.world->kind == World::kLocal) {
     local_exchange(r, members, send_buf, sends, recv_buf, recvs);
   } else if (r.world->kind == World::kIpc) {
     ipc_exchange(r, members, send_buf, sends, recv_buf, recvs);
   } else {
-    nccl_exchange(r, send_buf, sends, recv_buf, recvs);
+    nccl_exchange(r, members, send_buf, sends, recv_buf, recvs, checked, wait);
   }
 }
+
+void nccl_wait(RankCtx& r) {
+  if (r.world->kind == World::kNccl) nccl_wait_impl(r);
+}
+
+void nccl_abort(World& w) { nccl_abort_comm(w); }
 
 void barrier(RankCtx& r, const std::vector<int>& members) {
   if (members.size() <= 1) return;
@@ -368,8 +483,7 @@ void barrier(RankCtx& r, const std::vector<int>& members) {
     v.push_back({members[i], static_cast<Dim>(i), 1});
   }
   QTNH_CUDA(cudaMemsetAsync(sb.ptr, 0, sb.bytes, r.stream));
-  nccl_exchange(r, sb.ptr, s, rb.ptr, v);
-  QTNH_CUDA(cudaStreamSynchronize(r.stream));
+  nccl_exchange(r, members, sb.ptr, s, rb.ptr, v, false, true);
 }
 
 }  // namespace qtnhb

@@ -32,7 +32,10 @@ struct RankCtx {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;  // current launch stream
   std::map<std::vector<int>, uint64_t> seq;  // per member-set collective sequence
+  cudaStream_t side[2] = {nullptr, nullptr}; // pipeline streams (pack / unpack), created on first use
   void activate() const;                     // cudaSetDevice(device)
+  cudaStream_t side_stream(int i);
+  ~RankCtx();
 };
 
 // One transfer of `count` complex elements at element `offset` of a buffer,
@@ -92,8 +95,18 @@ struct World {
 // are allowed. Stream-ordered on every member's stream; returns when all copies
 // are enqueued. Count mismatches raise ProtocolError naming "(src -> dst)"
 // (runtime.hpp:464-471).
+// NCCL world: `checked` = exchange the pairwise counts first (a mismatch raises
+// ProtocolError on both sides of the pair); `wait` = block until the transfer
+// completes, with the collective timeout (ncclCommAbort + ProtocolError) --
+// a pipelined caller verifies once and waits once (nccl_wait) at the end.
 void exchange(RankCtx& r, const std::vector<int>& members, const void* send_buf,
-              const std::vector<Xfer>& sends, void* recv_buf, const std::vector<Xfer>& recvs);
+              const std::vector<Xfer>& sends, void* recv_buf, const std::vector<Xfer>& recvs, bool checked = true,
+              bool wait = true);
+// NCCL world: wait for the rank stream with the collective timeout and async-error
+// polling; no-op for the other backends.
+void nccl_wait(RankCtx& r);
+// Abort the NCCL communicator of a process-per-GPU world (qtnh_world_abort).
+void nccl_abort(World& w);
 void barrier(RankCtx& r, const std::vector<int>& members);
 
 // Peer-memory collectives (local world with peer_ok): kernels read and write
