@@ -83,7 +83,9 @@ __global__ void __launch_bounds__(256) k_gate_dense(double2* __restrict__ psi, i
 #pragma unroll
     for (int u = 0; u < F; ++u) {
       if (base[u] < 0) continue;
-#pragma unroll
+      // D = 16: one output row per iteration keeps the 256 gate words out of
+      // registers (fully unrolled, ptxas hoisted them and spilled 88 B)
+#pragma unroll(D >= 16 ? 1 : D)
       for (int i = 0; i < D; ++i) {
         double re = 0.0, im = 0.0;
 #pragma unroll
@@ -160,7 +162,9 @@ __global__ void __launch_bounds__(256) k_gate_dense_v2(double2* __restrict__ psi
 #pragma unroll
     for (int u = 0; u < F; ++u) {
       if (base[u] < 0) continue;
-#pragma unroll
+      // D = 16: one output row per iteration keeps the 256 gate words out of
+      // registers (fully unrolled, ptxas hoisted them and spilled 88 B)
+#pragma unroll(D >= 16 ? 1 : D)
       for (int i = 0; i < D; ++i) {
         double r0 = 0.0, i0 = 0.0, r1 = 0.0, i1 = 0.0;
 #pragma unroll

@@ -2,6 +2,7 @@
 
 #include <dlfcn.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -24,7 +25,11 @@ void* sym(void* h, const char* name) {
 const Nccl& nccl() {
   std::lock_guard<std::mutex> lk(g_mu);
   if (g_loaded) return g_nccl;
-  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  // QTNH_NCCL_LIB names a specific build; otherwise the libnccl.so.2 already in
+  // the process (torch's) is reused, and only then one is loaded by soname.
+  void* h = nullptr;
+  if (const char* lib = std::getenv("QTNH_NCCL_LIB")) h = dlopen(lib, RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
   if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
   if (!h) throw_runtime("cannot load libnccl.so.2");

@@ -5,6 +5,7 @@ import ctypes as C
 
 import numpy as np
 import pytest
+import torch  # noqa: F401  (first: torch's bundled libnccl must be the process's libnccl.so.2)
 
 import oracle
 from conftest import bits, rel_l2
@@ -77,7 +78,6 @@ def test_nccl_world_of_one_count_check_and_abort():
     """The NCCL exchange's count bookkeeping (self chunks must match) raises the
     reference's ProtocolError "(src -> dst)"; qtnh_world_abort aborts the
     communicator and later collectives raise AbortedError (runtime.hpp:276-298)."""
-    import torch
 
     uid = (C.c_char * 128)()
     qtnh.check(lib.qtnh_nccl_unique_id(uid))
