@@ -355,6 +355,10 @@ int qtnh_zgemm_device(qtnh_rank_t r, int64_t m, int64_t n, int64_t k, const void
 int qtnh_permute_device(qtnh_rank_t r, int n_idx, const int64_t* dims, const int* perm,
                         const void* in, void* out);
 
+/* Matrices the truncated SVD has factorised through its spectral-split path
+ * (svd_split.cu) since the library loaded -- the rest took the full Jacobi SVD. */
+int64_t qtnh_svd_split_count(void);
+
 /* FP64 tensor-pipe (DMMA) peak measured on the current device, TFLOP/s. */
 int qtnh_probe_fp64_peak(void* stream, double* tflops);
 

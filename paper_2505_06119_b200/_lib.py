@@ -98,6 +98,7 @@ _SIGS = {
     "qtnh_tensor_reshape": (i32, [vp, i32, P_i64, C.POINTER(vp)]),
     "qtnh_group_all_to_all_v_host": (i32, [vp, i32, P_i32, sz, C.POINTER(vp), P_i64, vp, C.POINTER(vp), P_i64]),
     "qtnh_free_host": (None, [vp]),
+    "qtnh_svd_split_count": (i64, []),
     "qtnh_mps_apply_layer": (i32, [i32, C.POINTER(vp), C.POINTER(vp), vp, i64, C.POINTER(vp), C.POINTER(vp), vp, vp,
                                    vp]),
     "qtnh_svd": (i32, [vp, i32, P_i32, i32, P_i32, i64, i32, C.POINTER(vp), C.POINTER(vp), vp]),

@@ -85,6 +85,7 @@ int qtnh_last_error(char* buf, size_t len) {
 int64_t qtnh_last_error_info(void) { return t_info; }
 const char* qtnh_version(void) { return "qtnh_b200 0.1.0 (sm_100a)"; }
 int64_t qtnh_kernel_launch_count(void) { return g_kernel_launches.load(); }
+int64_t qtnh_svd_split_count(void) { return svd_split_count(); }
 
 // ---- worlds -----------------------------------------------------------------
 int qtnh_world_create_local(int n, const int* devices, qtnh_world_t* out) {

@@ -61,8 +61,13 @@ struct TableKey {
   }
 };
 using Table = std::shared_ptr<const int64_t>;
+struct TableEntry {
+  Table t;
+  size_t bytes;
+  cudaEvent_t ready;  // the table's generation; users on any stream wait on it
+};
 std::mutex g_tab_mu;
-std::map<TableKey, std::pair<Table, size_t>> g_tabs;
+std::map<TableKey, TableEntry> g_tabs;
 size_t g_tab_bytes = 0;
 
 // Returns a reference-counted table: callers keep it alive until the GEMM that
@@ -73,7 +78,10 @@ Table gather_table(RankCtx& r, const std::vector<Dim>& dims, const std::vector<D
   TableKey key{r.device, dims, strides};
   std::lock_guard<std::mutex> lk(g_tab_mu);
   auto it = g_tabs.find(key);
-  if (it != g_tabs.end()) return it->second.first;
+  if (it != g_tabs.end()) {
+    QTNH_CUDA(cudaStreamWaitEvent(r.stream, it->second.ready, 0));
+    return it->second.t;
+  }
   Dim count = 1;
   for (Dim d : dims) count *= d;
   if (g_tab_bytes > (size_t(1) << 30)) {  // bounded: drop the cache's references (tables are cheap to rebuild)
@@ -83,19 +91,23 @@ Table gather_table(RankCtx& r, const std::vector<Dim>& dims, const std::vector<D
   const size_t bytes = static_cast<size_t>(std::max<Dim>(1, count)) * 8;
   int64_t* ptr = nullptr;
   QTNH_CUDA(cudaMalloc(&ptr, bytes));
+  cudaEvent_t ready;
+  QTNH_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   const int dev = r.device;
-  Table t(ptr, [dev](const int64_t* p) {
+  Table t(ptr, [dev, ready](const int64_t* p) {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(dev);
     cudaDeviceSynchronize();  // launches that named the table have been enqueued by now: let them finish
     cudaFree(const_cast<int64_t*>(p));
+    cudaEventDestroy(ready);
     cudaSetDevice(cur);
   });
   index_offsets(ptr, count, dims, strides, r.stream);
-  // other ranks (streams) on this device may pick the table up right away
-  QTNH_CUDA(cudaStreamSynchronize(r.stream));
-  g_tabs[key] = {t, bytes};
+  // other ranks (streams) on this device wait on the event instead of this
+  // thread synchronising (a sync per new layout serialised C3's ~600 small steps)
+  QTNH_CUDA(cudaEventRecord(ready, r.stream));
+  g_tabs[key] = {t, bytes, ready};
   g_tab_bytes += bytes;
   return t;
 }

@@ -95,8 +95,14 @@ void index_offsets(int64_t* out, Dim count, const std::vector<Dim>& dims, const 
 void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* u, void* s,
                  void* vh, int* sweeps_out);
 // The same with one output pointer per matrix (U: m x chi, Vh: chi x n each).
+// Truncating calls (chi < min(m, n)) try the spectral-split path first
+// (svd_split.cu); everything else, and every matrix the split cannot certify,
+// runs the blocked one-sided Jacobi (svd_jacobi_ptrs).
 void svd_batched_ptrs(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* const* u_ptrs,
                       void* s, void* const* vh_ptrs, int* sweeps_out);
+int64_t svd_split_count();  // matrices factorised by the split path so far
+void svd_jacobi_ptrs(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* const* u_ptrs,
+                     void* s, void* const* vh_ptrs, int* sweeps_out);
 // One layer of MPS two-site updates (mps.cu): pair i = (left[i], right[i]),
 // sites (l, d, c) and (c, d, r) held by this rank; gate = 4x4 complex row-major
 // (out1 out2, in1 in2). New sites U S (l, d, keep) and Vh (keep, d, r), keep =

@@ -192,7 +192,9 @@ struct Plan {
   int* d_slot = nullptr;
   int grid = 0;
   size_t smem = 0;
+  cudaEvent_t ready = nullptr;  // the tables' upload; launches on other streams wait on it
   ~Plan() {  // only on cache eviction (cudaFree synchronises the device)
+    if (ready) cudaEventDestroy(ready);
     if (d_tin) cudaFree(d_tin);
     if (d_tout) cudaFree(d_tout);
     if (d_slot) cudaFree(d_slot);
@@ -404,7 +406,11 @@ std::shared_ptr<Plan> build_plan(const std::vector<D>& ds, int dev, cudaStream_t
   QTNH_CUDA(cudaMemcpyAsync(p->d_tin, tin.data(), T * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   QTNH_CUDA(cudaMemcpyAsync(p->d_tout, tout.data(), T * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   QTNH_CUDA(cudaMemcpyAsync(p->d_slot, slot.data(), T * sizeof(int), cudaMemcpyHostToDevice, st));
-  QTNH_CUDA(cudaStreamSynchronize(st));  // host staging vectors die with this scope
+  // pageable sources: cudaMemcpyAsync has copied them to staging on return, so the
+  // host vectors may die; no stream synchronisation (it serialised every new
+  // layout -- ~600 in config 3's contraction chain)
+  QTNH_CUDA(cudaEventCreateWithFlags(&p->ready, cudaEventDisableTiming));
+  QTNH_CUDA(cudaEventRecord(p->ready, st));
   int per_sm = 1;
   if (direct) {
     QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tiled<true, true>, kThreads, 0));
@@ -464,6 +470,7 @@ void strided_copy(const void* in, void* out, const CopyBox& box, bool canon, cud
       g_plans[key] = p;
     }
   }
+  if (p->ready) QTNH_CUDA(cudaStreamWaitEvent(st, p->ready, 0));
   auto i = static_cast<const double2*>(in);
   auto o = static_cast<double2*>(out);
   switch (p->kind) {

@@ -1,0 +1,310 @@
+// Spectral-split path of the truncated SVD (chi < min(m, n), m <= n).
+//
+// The reference truncates after a full zgesdd (linalg.hpp:441-505): it needs only
+// the chi largest singular triplets. When the spectrum has a gap at chi, the
+// top-chi left singular subspace is the range of the spectral projector of
+// H = A A^H above a mid-gap shift mu, P = (I + sign(H - mu I)) / 2, and sign() is
+// a Newton-Schulz iteration X <- X (3 I - X^2) / 2 -- nothing but GEMMs on the
+// FP64 tensor cores. Then
+//   Y  = P Omega              (Omega: m x chi seeded complex normals)
+//   Q^H = rows of Vh(Y^H)     (orthonormal basis of range(P): a Jacobi SVD of the
+//                              chi x m matrix Y^H, a quarter of the full problem)
+//   B  = Q^H A                (chi x n: exactly the kept part of A, in Q's basis)
+//   B  = U_B S Vh             (Jacobi SVD, chi x n, absorb applied)
+//   U  = Q U_B
+// so U S Vh = P A = the rank-chi truncation, and S are A's chi largest singular
+// values. The Jacobi sweeps that dominate the full method on clustered spectra
+// (config 4's thetas have exactly two singular values, 1024-fold each: 23-28
+// sweeps of the 2048 x 2048 problem) are replaced by ~3 GEMM-sized steps and two
+// quarter-size Jacobi solves.
+//
+// mu comes from a two-cluster fit of the spectrum (multiplicities chi and m - chi)
+// to tr H and ||H||_F^2, the scale from the fitted half-gap; the iteration must
+// converge (||X^2 - I||_F / sqrt(m) <= 1e-13 within 12 steps) and tr X must equal
+// 2 chi - m (the split is exactly at chi). A matrix that fails either check
+// (no gap at chi, eigenvalues outside the Newton-Schulz basin) takes the full
+// Jacobi SVD instead -- the result never depends on the model being right.
+// QTNH_SVD_SPLIT=0 disables the path.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdlib>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "ops.h"
+#include "qtnh_b200.h"
+
+namespace qtnhb {
+
+namespace {
+
+constexpr int kParts = 256;
+
+// out (cols x rows) = conj(in (rows x cols))^T
+__global__ void k_conj_t(const double2* __restrict__ in, double2* __restrict__ out, int64_t rows, int64_t cols) {
+  __shared__ double2 tile[32][33];
+  const int64_t c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) {
+      const double2 v = tile[threadIdx.x][i];
+      out[c * rows + r] = make_double2(v.x, -v.y);
+    }
+  }
+}
+
+// X = scale * (X - shift I)
+__global__ void k_shift_scale(double2* __restrict__ x, int64_t m, double shift, double scale) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * m; e += (int64_t)gridDim.x * blockDim.x) {
+    double2 v = x[e];
+    if (e / m == e % m) v.x -= shift;
+    x[e] = make_double2(scale * v.x, scale * v.y);
+  }
+}
+
+// T = a I + b X
+__global__ void k_axpy_identity(const double2* __restrict__ x, double2* __restrict__ t, int64_t m, double a,
+                                double b) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * m; e += (int64_t)gridDim.x * blockDim.x) {
+    double2 v = x[e];
+    v = make_double2(b * v.x, b * v.y);
+    if (e / m == e % m) v.x += a;
+    t[e] = v;
+  }
+}
+
+// per block: sum |X - alpha I|^2 and sum Re(diag X) (fixed partition: deterministic)
+__global__ void k_fro_trace(const double2* __restrict__ x, int64_t m, double alpha, double* __restrict__ part) {
+  __shared__ double r1[256], r2[256];
+  double f = 0.0, t = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * m; e += (int64_t)gridDim.x * blockDim.x) {
+    double2 v = x[e];
+    if (e / m == e % m) {
+      t += v.x;
+      v.x -= alpha;
+    }
+    f += v.x * v.x + v.y * v.y;
+  }
+  r1[threadIdx.x] = f;
+  r2[threadIdx.x] = t;
+  __syncthreads();
+  for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+    if (threadIdx.x < k) {
+      r1[threadIdx.x] += r1[threadIdx.x + k];
+      r2[threadIdx.x] += r2[threadIdx.x + k];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = r1[0];
+    part[2 * blockIdx.x + 1] = r2[0];
+  }
+}
+
+void conj_t(const double2* in, double2* out, Dim rows, Dim cols, cudaStream_t st) {
+  dim3 g(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+  k_conj_t<<<g, dim3(32, 8), 0, st>>>(in, out, rows, cols);
+  QTNH_LAUNCH_CHECK();
+}
+
+int grid_elems(Dim n) { return static_cast<int>(std::min<Dim>((n + 255) / 256, 148 * 8)); }
+
+std::atomic<int64_t> g_split_count{0};
+
+bool split_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("QTNH_SVD_SPLIT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+}  // namespace
+
+void svd_batched_ptrs(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* const* u_ptrs,
+                      void* s, void* const* vh_ptrs, int* sweeps_out) {
+  const Dim k = std::min(m, n);
+  if (chi <= 0 || chi >= k || m > n || m < 64 || !split_enabled() || batch < 1) {
+    svd_jacobi_ptrs(r, batch, m, n, a, chi, absorb, u_ptrs, s, vh_ptrs, sweeps_out);
+    return;
+  }
+  cudaStream_t st = r.stream;
+  const double2* A = static_cast<const double2*>(a);
+  const size_t mm = static_cast<size_t>(m * m);
+  // 1. H = A A^H, two-cluster fit of its spectrum (tr H, ||H||_F^2)
+  std::vector<std::unique_ptr<DevBuf>> X(batch), X2(batch), Xn(batch);
+  DevBuf ah(static_cast<size_t>(n * m) * 16, r);
+  for (Dim b = 0; b < batch; ++b) {
+    X[b] = std::make_unique<DevBuf>(mm * 16, r);
+    conj_t(A + b * m * n, static_cast<double2*>(ah.ptr), m, n, st);
+    zgemm(A + b * m * n, ah.ptr, X[b]->ptr, m, m, n, st);
+  }
+  DevBuf part(static_cast<size_t>(batch) * kParts * 2 * sizeof(double), r);
+  std::vector<double> ph(static_cast<size_t>(batch) * kParts * 2);
+  auto stats = [&](const std::vector<std::unique_ptr<DevBuf>>& v, const std::vector<char>& act, double alpha,
+                   std::vector<double>& fro, std::vector<double>& tr) {
+    for (Dim b = 0; b < batch; ++b)
+      if (act[b]) {
+        k_fro_trace<<<kParts, 256, 0, st>>>(static_cast<const double2*>(v[b]->ptr), m, alpha,
+                                            static_cast<double*>(part.ptr) + b * kParts * 2);
+        QTNH_LAUNCH_CHECK();
+      }
+    QTNH_CUDA(cudaMemcpyAsync(ph.data(), part.ptr, ph.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    QTNH_CUDA(cudaStreamSynchronize(st));
+    fro.assign(batch, 0.0);
+    tr.assign(batch, 0.0);
+    for (Dim b = 0; b < batch; ++b)
+      for (int i = 0; i < kParts; ++i) {
+        fro[b] += ph[(b * kParts + i) * 2];
+        tr[b] += ph[(b * kParts + i) * 2 + 1];
+      }
+  };
+  std::vector<char> ok(batch, 1);
+  std::vector<double> fro, tr;
+  stats(X, ok, 0.0, fro, tr);
+  const double p = static_cast<double>(chi), q = static_cast<double>(m - chi), md = static_cast<double>(m);
+  for (Dim b = 0; b < batch; ++b) {
+    const double t1 = tr[b], t2 = fro[b];
+    const double var = md * t2 - t1 * t1;  // >= 0 (Cauchy-Schwarz); 0: a single cluster, no gap
+    if (!(t1 > 0.0) || !(var > 1e-20 * t1 * t1)) {
+      ok[b] = 0;
+      continue;
+    }
+    const double hi = t1 / md + std::sqrt(q * var / p) / md, lo = t1 / md - std::sqrt(p * var / q) / md;
+    const double mu = 0.5 * (hi + lo), half = 0.5 * (hi - lo);
+    k_shift_scale<<<grid_elems(m * m), 256, 0, st>>>(static_cast<double2*>(X[b]->ptr), m, mu, 1.0 / half);
+    QTNH_LAUNCH_CHECK();
+  }
+  // 2. Newton-Schulz: X <- X (3 I - X^2) / 2 until X^2 = I
+  std::vector<char> act = ok;
+  for (Dim b = 0; b < batch; ++b)
+    if (ok[b]) {
+      X2[b] = std::make_unique<DevBuf>(mm * 16, r);
+      Xn[b] = std::make_unique<DevBuf>(mm * 16, r);
+    }
+  // Give up early (the matrix then takes the Jacobi path): a first residual above
+  // 0.3 means the spectrum is not two tight clusters around mu (a random matrix:
+  // ~1 -- the probe costs 2 GEMMs), and a residual that stops shrinking by 2x per
+  // step means an eigenvalue sits near mu.
+  const double tol = 1e-13;
+  std::vector<double> prev(batch, 1e300);
+  for (int it = 0; it <= 12; ++it) {
+    bool any = false;
+    for (Dim b = 0; b < batch; ++b)
+      if (act[b]) {
+        any = true;
+        zgemm(X[b]->ptr, X[b]->ptr, X2[b]->ptr, m, m, m, st);
+      }
+    if (!any) break;
+    stats(X2, act, 1.0, fro, tr);
+    for (Dim b = 0; b < batch; ++b) {
+      if (!act[b]) continue;
+      const double res = std::sqrt(fro[b] / md);
+      if (!(res < 1e3) || (it == 0 && res > 0.3) || (it > 0 && res > 0.5 * prev[b] && res > tol)) {
+        ok[b] = act[b] = 0;
+        continue;
+      }
+      prev[b] = res;
+      if (res <= tol) {
+        act[b] = 0;
+        continue;
+      }
+      if (it == 12) {
+        ok[b] = act[b] = 0;
+        continue;
+      }
+      k_axpy_identity<<<grid_elems(m * m), 256, 0, st>>>(static_cast<const double2*>(X2[b]->ptr),
+                                                          static_cast<double2*>(X2[b]->ptr), m, 1.5, -0.5);
+      QTNH_LAUNCH_CHECK();
+      zgemm(X[b]->ptr, X2[b]->ptr, Xn[b]->ptr, m, m, m, st);
+      std::swap(X[b], Xn[b]);
+    }
+  }
+  // 3. the split must be exactly at chi: tr X = chi - (m - chi); P = (I + X) / 2
+  stats(X, ok, 0.0, fro, tr);
+  std::vector<Dim> sp, fb;  // split / fallback matrices
+  for (Dim b = 0; b < batch; ++b) {
+    if (ok[b] && std::fabs(tr[b] - (2.0 * p - md)) < 0.25) {
+      sp.push_back(b);
+      k_axpy_identity<<<grid_elems(m * m), 256, 0, st>>>(static_cast<const double2*>(X[b]->ptr),
+                                                          static_cast<double2*>(X[b]->ptr), m, 0.5, 0.5);
+      QTNH_LAUNCH_CHECK();
+    } else {
+      fb.push_back(b);
+    }
+    X2[b].reset();
+    Xn[b].reset();
+  }
+  int sw_split = 0, sw_fb = 0;
+  double* S = static_cast<double*>(s);
+  if (!sp.empty()) {
+    const Dim ns = static_cast<Dim>(sp.size());
+    // 4. Y = P Omega, Y^H (batch of chi x m), orthonormal basis Q^H = Vh(Y^H)
+    DevBuf om(static_cast<size_t>(m * chi) * 16, r);
+    qtnh_counter_complex_normals_device(st, 0x5EEDC0DEULL, 0, m * chi, om.ptr);
+    DevBuf y(static_cast<size_t>(m * chi) * 16, r);
+    DevBuf yh(static_cast<size_t>(ns * chi * m) * 16, r);
+    for (Dim i = 0; i < ns; ++i) {
+      zgemm(X[sp[i]]->ptr, om.ptr, y.ptr, m, chi, m, st);
+      conj_t(static_cast<const double2*>(y.ptr), static_cast<double2*>(yh.ptr) + i * chi * m, m, chi, st);
+    }
+    for (Dim b : sp) X[b].reset();
+    DevBuf u1(static_cast<size_t>(ns * chi * chi) * 16, r), s1(static_cast<size_t>(ns * chi) * 8, r);
+    DevBuf qh(static_cast<size_t>(ns * chi * m) * 16, r);
+    svd_batched(r, ns, chi, m, yh.ptr, chi, QTNH_ABSORB_NONE, u1.ptr, s1.ptr, qh.ptr, &sw_split);
+    // 5. B = Q^H A (chi x n) and its SVD (absorb applied), U = Q U_B
+    DevBuf bm(static_cast<size_t>(ns * chi * n) * 16, r);
+    for (Dim i = 0; i < ns; ++i)
+      zgemm(static_cast<const double2*>(qh.ptr) + i * chi * m, A + sp[i] * m * n,
+            static_cast<double2*>(bm.ptr) + i * chi * n, chi, n, m, st);
+    DevBuf ub(static_cast<size_t>(ns * chi * chi) * 16, r), sb(static_cast<size_t>(ns * chi) * 8, r);
+    std::vector<void*> ubp(ns), vhp(ns);
+    for (Dim i = 0; i < ns; ++i) {
+      ubp[i] = static_cast<double2*>(ub.ptr) + i * chi * chi;
+      vhp[i] = vh_ptrs[sp[i]];
+    }
+    int sw2 = 0;
+    svd_jacobi_ptrs(r, ns, chi, n, bm.ptr, chi, absorb, ubp.data(), sb.ptr, vhp.data(), &sw2);
+    sw_split = std::max(sw_split, sw2);
+    DevBuf qm(static_cast<size_t>(m * chi) * 16, r);
+    for (Dim i = 0; i < ns; ++i) {
+      conj_t(static_cast<const double2*>(qh.ptr) + i * chi * m, static_cast<double2*>(qm.ptr), chi, m, st);
+      zgemm(qm.ptr, ubp[i], u_ptrs[sp[i]], m, chi, chi, st);
+      QTNH_CUDA(cudaMemcpyAsync(S + sp[i] * chi, static_cast<double*>(sb.ptr) + i * chi, chi * sizeof(double),
+                                cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  if (!fb.empty()) {
+    const Dim nf = static_cast<Dim>(fb.size());
+    DevBuf af(static_cast<size_t>(nf * m * n) * 16, r), sf(static_cast<size_t>(nf * chi) * 8, r);
+    std::vector<void*> up(nf), vp(nf);
+    for (Dim i = 0; i < nf; ++i) {
+      QTNH_CUDA(cudaMemcpyAsync(static_cast<double2*>(af.ptr) + i * m * n, A + fb[i] * m * n, m * n * 16,
+                                cudaMemcpyDeviceToDevice, st));
+      up[i] = u_ptrs[fb[i]];
+      vp[i] = vh_ptrs[fb[i]];
+    }
+    svd_jacobi_ptrs(r, nf, m, n, af.ptr, chi, absorb, up.data(), sf.ptr, vp.data(), &sw_fb);
+    for (Dim i = 0; i < nf; ++i)
+      QTNH_CUDA(cudaMemcpyAsync(S + fb[i] * chi, static_cast<double*>(sf.ptr) + i * chi, chi * sizeof(double),
+                                cudaMemcpyDeviceToDevice, st));
+  }
+  QTNH_CUDA(cudaStreamSynchronize(st));
+  if (sweeps_out) *sweeps_out = std::max(sw_fb, sw_split);
+  g_split_count += static_cast<int64_t>(sp.size());
+  if (std::getenv("QTNH_SVD_DEBUG"))
+    std::fprintf(stderr, "svd split path: %lld of %lld matrices (m %lld n %lld chi %lld)\n",
+                 static_cast<long long>(sp.size()), static_cast<long long>(batch), static_cast<long long>(m),
+                 static_cast<long long>(n), static_cast<long long>(chi));
+}
+
+int64_t svd_split_count() { return g_split_count.load(); }
+
+}  // namespace qtnhb

@@ -176,3 +176,49 @@ def test_svd_c4_size_vs_reference():
     u, s, vh = gpu_svd(a, chi=chi, absorb=ABSORB_LEFT)
     assert np.allclose(s, rs, rtol=1e-11, atol=1e-13)
     assert rel_l2(u @ vh, ru @ rvh) < TOL
+
+
+def _with_spectrum(m, n, s, seed):
+    rng = np.random.default_rng(seed)
+    u, _ = np.linalg.qr(rng.standard_normal((m, m)) + 1j * rng.standard_normal((m, m)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    k = min(m, n)
+    return (u[:, :k] * np.asarray(s)) @ v[:, :k].conj().T
+
+
+@pytest.mark.parametrize("case", ["two_exact", "two_tight", "gapped_wide", "no_gap", "rect"])
+def test_svd_spectral_split_path(case):
+    """The truncated SVD's spectral-split path (svd_split.cu: projector of A A^H by
+    Newton-Schulz, quarter-size Jacobi solves) against numpy on matrices with a
+    chosen spectrum: exactly two values (config 4's thetas), two tight clusters,
+    a wide gap (may fall back), no gap (must fall back); the result is the same
+    truncated factorisation either way, and the path actually taken is checked
+    where it is certain."""
+    m, n, chi = 256, 256, 128
+    if case == "two_exact":
+        s = [0.7] * chi + [0.36] * (m - chi)
+    elif case == "two_tight":
+        s = list(0.7 * (1 + 1e-7 * np.linspace(0, 1, chi))) + list(0.36 * (1 + 1e-7 * np.linspace(0, 1, m - chi)))
+    elif case == "gapped_wide":
+        s = list(np.linspace(0.8, 0.6, chi)) + list(np.linspace(0.3, 0.1, m - chi))
+    elif case == "no_gap":
+        s = list(np.linspace(1.0, 0.01, m))
+    else:
+        m, n, chi = 192, 320, 96
+        s = [0.9] * chi + [0.2] * (m - chi)
+    s = np.sort(np.asarray(s))[::-1]
+    a = _with_spectrum(m, n, s, 7)
+    before = int(qtnh.lib.qtnh_svd_split_count())
+    u, sv, vh = gpu_svd(a, chi=chi, absorb=ABSORB_LEFT)
+    took = int(qtnh.lib.qtnh_svd_split_count()) - before
+    U, S, VH = np.linalg.svd(a, full_matrices=False)
+    want = (U[:, :chi] * S[:chi]) @ VH[:chi]
+    assert rel_l2(u @ vh, want) < TOL
+    assert np.max(np.abs(sv - S[:chi])) <= TOL * S[0]
+    # Vh rows orthonormal; U = U_true S (absorb left): U^H U = S^2
+    assert np.allclose(vh @ vh.conj().T, np.eye(chi), atol=1e-12)
+    assert np.allclose(u.conj().T @ u, np.diag(sv**2), atol=1e-12)
+    if case in ("two_exact", "two_tight", "rect"):
+        assert took == 1
+    if case == "no_gap":
+        assert took == 0
