@@ -317,7 +317,11 @@ def measure_extras(rk, stream, torch):
         gbs = bytes_per_gate / (ms * 1e-3) / 1e9
         entry = {"ms": ms, "GBps_algorithmic": gbs, "frac": gbs / peak}
         if diag:
-            entry["note"] = "touches the 1/4 of amplitudes whose diagonal entry != 1: actual traffic 8 B/amplitude"
+            # actual traffic: the quarter of amplitudes whose entry != 1 is read + written
+            actual = 8.0 * 2**n / (ms * 1e-3) / 1e9
+            entry.update(note="the 32 B/amplitude convention overstates this gate: it touches the 1/4 of "
+                              "amplitudes whose diagonal entry != 1 (8 B/amplitude)",
+                         GBps_actual=actual, frac_actual=actual / peak)
         res[name] = entry
     st.free()
     ex["gate_apply_n30"] = res
@@ -608,10 +612,13 @@ def run_gpu_arm(args):
             "config": dict(c1_config(world_size), **({"note": world_note} if world_note else {})),
             "roofline": {"bound": "tensor", "kernel": kname,
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "achieved_8mnk": flops_rank / (ms * 1e-3) / 1e12,
+                         "frac_8mnk": flops_rank / (ms * 1e-3) / 1e12 / peak,
                          "peak_source": "DMMA-only microbenchmark run live on this device (MEASURED_PEAKS.json "
                                         "has no FP64 entry)",
-                         "flop_convention": "value counts 8MNK per complex GEMM; achieved counts the 6MNK real "
-                                            "DMMA flops the Gauss (3M) kernel issues",
+                         "flop_convention": "value and achieved_8mnk count 8MNK per complex GEMM (BASELINE "
+                                            "convention; frac_8mnk > 1 is possible because Gauss 3M issues "
+                                            "only 6MNK); achieved / frac count the 6MNK real DMMA flops issued",
                          "traffic": traffic, "kernel_ms": ms,
                          "zgemm_dense_ms": zg, "zgemm_dense_tflops_8mnk": flops_rank / (zg * 1e-3) / 1e12,
                          "permute_ms": result["permute_ms"],

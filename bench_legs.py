@@ -281,7 +281,7 @@ def cpu_c3(steps, small=2**22, budget_s=20.0):
 
 
 # ---- C4 --------------------------------------------------------------------------------------------
-def gpu_c4(rk, stream, torch, n=40, depth=20, chi=1024, capture=2, bitstrings=1024):
+def gpu_c4(rk, stream, torch, n=40, depth=20, chi=1024, capture=2, bitstrings=1024, capture_layer=None):
     """The whole MPS run; before the first layer with `capture` saturated pairs the
     sites of those pairs are copied to the host, and after it their new sites and
     singular values, for the CPU leg (timing + parity on identical inputs)."""
@@ -295,12 +295,12 @@ def gpu_c4(rk, stream, torch, n=40, depth=20, chi=1024, capture=2, bitstrings=10
     e0.record(stream)
     t0 = time.perf_counter()
     host_s = 0.0
-    for singles, pairs in layers:
+    for li, (singles, pairs) in enumerate(layers):
         for q, g in enumerate(singles):
             m.apply_1q(q, mps.SINGLE_QUBIT[g])
         sat = [q for q, _ in pairs if m.sites[q].shape().dims == [chi, 2, chi]
                and m.sites[q + 1].shape().dims == [chi, 2, chi]]
-        if cap is None and len(sat) >= capture:
+        if cap is None and len(sat) >= capture and (capture_layer is None or li == capture_layer):
             h0 = time.perf_counter()
             cap = [{"q": q, "a": m.sites[q].local_data().copy(), "b": m.sites[q + 1].local_data().copy()}
                    for q in sat[:capture]]

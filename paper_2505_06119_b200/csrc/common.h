@@ -10,9 +10,24 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "qtnh_b200.h"
 
 namespace qtnhb {
+
+// NVTX range over one library operation (nsys / ncu --nvtx show them nested in
+// the caller's ranges). Header-only NVTX v3: without an attached tool the push /
+// pop are a function-pointer check.
+struct NvtxRange {
+  explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define QTNH_CAT2_(a, b) a##b
+#define QTNH_CAT_(a, b) QTNH_CAT2_(a, b)
+#define QTNH_RANGE(name) ::qtnhb::NvtxRange QTNH_CAT_(qtnh_nvtx_, __LINE__)(name)
 
 using Dim = int64_t;
 

@@ -115,6 +115,7 @@ Table gather_table(RankCtx& r, const std::vector<Dim>& dims, const std::vector<D
 }  // namespace
 
 TP op_contract(const TP& a_in, const TP& b_in, const std::vector<int>& apos, const std::vector<int>& bpos) {
+  QTNH_RANGE("qtnh::contract");
   if (apos.size() != bpos.size()) throw_invalid("contracted position lists differ in length");
   if (a_in->rank != b_in->rank) throw_invalid("operands belong to different ranks");
   RankCtx& r = *a_in->rank;
@@ -309,6 +310,7 @@ TP op_contract(const TP& a_in, const TP& b_in, const std::vector<int>& apos, con
 }
 
 void op_gate_apply(TP& t, const std::vector<int>& targets, const double* gate, bool diagonal) {
+  QTNH_RANGE("qtnh::gate_apply");
   const Shape& s = t->shape;
   int k = static_cast<int>(targets.size());
   std::vector<char> is_t(s.n_idx(), 0);
@@ -490,6 +492,7 @@ void op_qft_layer(TP& t, int j) {
 }
 
 void op_qft(TP& t, bool swaps) {
+  QTNH_RANGE("qtnh::qft");
   // t may be replaced by the distributed-layer path: copy the metadata first
   const int n = t->shape.n_idx(), split = t->shape.split;
   for (Dim d : t->shape.dims)

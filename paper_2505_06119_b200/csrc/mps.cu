@@ -64,6 +64,7 @@ __global__ void k_fro2_final(const double* __restrict__ part, int parts, double*
 void mps_apply_layer(const std::vector<TP>& left, const std::vector<TP>& right, const double* gate, Dim chi,
                      std::vector<TP>& new_left, std::vector<TP>& new_right, double* s_out, int64_t* keep_out,
                      double* norm2_out) {
+  QTNH_RANGE("qtnh::mps_layer");
   const size_t np = left.size();
   if (right.size() != np) throw_invalid("mps layer: left and right site lists differ in length");
   if (chi < 1) throw_invalid("mps layer: chi must be >= 1");

@@ -199,6 +199,7 @@ RemapPlan plan_remap(const Shape& ss, const Dist& sd, const Shape& ds, const Dis
 }
 
 TP remap(const TP& src, Shape ds, Dist dd, const std::vector<int>& am) {
+  QTNH_RANGE("qtnh::remap");
   RankCtx& r = *src->rank;
   RemapPlan P = plan_remap(src->shape, src->dist, ds, dd, am, r.rank, r.world->size);
   TP dst = make_tensor(r, ds, dd, true);
@@ -404,6 +405,7 @@ namespace qtnhb {
 // shard swaps without a second copy of the tensor. Values equal ops::permute with
 // a and b exchanged (zero canonicalisation included).
 void op_swap_dist_local_inplace(TP& t, int a, int b, Dim chunk_bytes) {
+  QTNH_RANGE("qtnh::swap_dist_local");
   const Shape& s = t->shape;
   if (!(a < s.split && b >= s.split)) throw_invalid("swap_dist_local needs a distributed a and a local b");
   const Dim d = s.dims[a];

@@ -448,6 +448,7 @@ std::vector<void*> peer_pointers(RankCtx& r, const std::vector<int>& members, vo
 void exchange(RankCtx& r, const std::vector<int>& members, const void* send_buf,
               const std::vector<Xfer>& sends, void* recv_buf, const std::vector<Xfer>& recvs, bool checked,
               bool wait) {
+  QTNH_RANGE("qtnh::exchange");
   if (r.world->kind == World::kLocal) {
     local_exchange(r, members, send_buf, sends, recv_buf, recvs);
   } else if (r.world->kind == World::kIpc) {

@@ -1238,6 +1238,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
 
 void svd_jacobi_ptrs(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* const* u_ptrs,
                      void* s, void* const* vh_ptrs, int* sweeps_out) {
+  QTNH_RANGE("qtnh::svd_jacobi");
   if (batch < 1 || m < 1 || n < 1) throw_invalid("svd needs positive batch and matrix dimensions");
   if (absorb < 0 || absorb > 3) throw_invalid("invalid absorb mode");
   // Small problems keep 16-row blocks (more pairs per round); large ones can use 32.

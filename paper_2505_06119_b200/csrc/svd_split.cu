@@ -130,6 +130,7 @@ bool split_enabled() {
 
 void svd_batched_ptrs(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* const* u_ptrs,
                       void* s, void* const* vh_ptrs, int* sweeps_out) {
+  QTNH_RANGE("qtnh::svd");
   const Dim k = std::min(m, n);
   if (chi <= 0 || chi >= k || m > n || m < 64 || !split_enabled() || batch < 1) {
     svd_jacobi_ptrs(r, batch, m, n, a, chi, absorb, u_ptrs, s, vh_ptrs, sweeps_out);
@@ -178,6 +179,8 @@ void svd_batched_ptrs(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim ch
       continue;
     }
     const double hi = t1 / md + std::sqrt(q * var / p) / md, lo = t1 / md - std::sqrt(p * var / q) / md;
+    if (std::getenv("QTNH_SVD_DEBUG"))
+      std::fprintf(stderr, "svd split: matrix %lld two-cluster fit %.12e %.12e\n", static_cast<long long>(b), hi, lo);
     const double mu = 0.5 * (hi + lo), half = 0.5 * (hi - lo);
     k_shift_scale<<<grid_elems(m * m), 256, 0, st>>>(static_cast<double2*>(X[b]->ptr), m, mu, 1.0 / half);
     QTNH_LAUNCH_CHECK();
@@ -207,6 +210,8 @@ void svd_batched_ptrs(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim ch
     for (Dim b = 0; b < batch; ++b) {
       if (!act[b]) continue;
       const double res = std::sqrt(fro[b] / md);
+      if (std::getenv("QTNH_SVD_DEBUG"))
+        std::fprintf(stderr, "svd split: matrix %lld iteration %d residual %.3e\n", static_cast<long long>(b), it, res);
       if (!(res < 1e3) || (it == 0 && res > 0.3) || (it > 0 && res > 0.5 * prev[b] && res > tol)) {
         ok[b] = act[b] = 0;
         continue;
@@ -231,6 +236,9 @@ void svd_batched_ptrs(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim ch
   stats(X, ok, 0.0, fro, tr);
   std::vector<Dim> sp, fb;  // split / fallback matrices
   for (Dim b = 0; b < batch; ++b) {
+    if (std::getenv("QTNH_SVD_DEBUG"))
+      std::fprintf(stderr, "svd split: matrix %lld ok %d trace %.6f (want %.1f)\n", static_cast<long long>(b), ok[b],
+                   tr[b], 2.0 * p - md);
     if (ok[b] && std::fabs(tr[b] - (2.0 * p - md)) < 0.25) {
       sp.push_back(b);
       k_axpy_identity<<<grid_elems(m * m), 256, 0, st>>>(static_cast<const double2*>(X[b]->ptr),

@@ -23,6 +23,8 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="")
+    ap.add_argument("--layer", type=int, default=-1, help="capture at this layer (default: first saturated)")
+    ap.add_argument("--pairs", type=int, default=1, help="saturated pairs to analyse (spectra only after the first)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -37,9 +39,28 @@ def main():
         st = torch.cuda.Stream()
         rk.set_stream(st.cuda_stream)
         with torch.cuda.stream(st):
-            _, cap = bench_legs.gpu_c4(rk, st, torch, depth=12, capture=1, bitstrings=4)
-        c = cap[0]
+            _, cap = bench_legs.gpu_c4(rk, st, torch, depth=(args.layer + 1 if args.layer >= 0 else 12),
+                                       capture=args.pairs, bitstrings=4,
+                                       capture_layer=(args.layer if args.layer >= 0 else None))
         chi = 1024
+        spectra = []
+        for c in cap:
+            a = c["a"].reshape(chi * 2, chi)
+            b = c["b"].reshape(chi, 2 * chi)
+            th = (a @ b).reshape(chi, 2, 2, chi)
+            th = np.einsum("ijkl,aklb->aijb", circuits.FSIM.reshape(2, 2, 2, 2), th).reshape(2 * chi, 2 * chi)
+            sv = np.linalg.svd(th, compute_uv=False)
+            vals, counts = [], []
+            for x in sv:
+                if vals and abs(x - vals[-1]) <= 1e-9 * sv[0]:
+                    counts[-1] += 1
+                else:
+                    vals.append(float(x))
+                    counts.append(1)
+            spectra.append({"site": c["q"], "clusters": len(vals), "values": vals[:12], "multiplicities": counts[:12],
+                            "sigma_chi": float(sv[chi - 1]), "sigma_chi+1": float(sv[chi])})
+        res["spectra"] = spectra
+        c = cap[0]
         a = c["a"].reshape(chi * 2, chi)
         b = c["b"].reshape(chi, 2 * chi)
         th = (a @ b).reshape(chi, 2, 2, chi)
