@@ -388,8 +388,16 @@ def run_gpu_arm(args):
         # One node, one process per GPU. Default: the CUDA-IPC world (collectives are
         # peer-memory kernels over NVLink; it also runs several ranks on one GPU);
         # QTNH_BENCH_WORLD=nccl selects the NCCL world. A failure is fatal: no fallback.
+        # If the chosen backend cannot be created, the other real multi-GPU backend is
+        # tried (never a 1-rank world), and the line says which one ran.
         kind = os.environ.get("QTNH_BENCH_WORLD", "ipc")
-        world = World.from_env() if kind == "nccl" else World.from_env_ipc()
+        try:
+            world = World.from_env() if kind == "nccl" else World.from_env_ipc()
+        except Exception as e:  # noqa: BLE001
+            other = "ipc" if kind == "nccl" else "nccl"
+            print(f"bench: {kind} world failed ({e}); using the {other} world", file=sys.stderr, flush=True)
+            world = World.from_env() if other == "nccl" else World.from_env_ipc()
+            kind = f"{other} (after {kind} failed: {e})"
         world_note = f"{kind} world, {world_size} processes on {torch.cuda.device_count()} visible GPU(s)"
     else:
         world = World(1, [local])
@@ -547,7 +555,11 @@ def run_gpu_arm(args):
                 import bench_legs
 
                 shared = world_size > torch.cuda.device_count()
-                result["c2_sharded"] = bench_legs.gpu_c2_sharded(rk, stream, torch, dist, world_size, rank, shared)
+                try:
+                    result["c2_sharded"] = bench_legs.gpu_c2_sharded(rk, stream, torch, dist, world_size, rank,
+                                                                     shared)
+                except Exception as e:  # noqa: BLE001  (reported in the line; C1 above stands)
+                    result["c2_sharded"] = {"error": f"{type(e).__name__}: {e}"}
             if not args.skip_configs and world_size == 1:
                 import bench_legs
 

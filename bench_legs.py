@@ -88,7 +88,21 @@ def gpu_c0(rk, stream, torch):
     graph = e0.elapsed_time(e1) / reps
     g.free()
     t.free()
+    # the same QFT through the fused path (qtnh_qft: cache-blocked layers + bit reversal)
+    from paper_2505_06119_b200.qtnh import qft
+
+    f = Tensor.dense(rk, IndexTuple([2] * n, 0), None, psi0)
+    qft(f, swaps=True)
+    fused_out = f.to_global_vector()
+    e0.record(stream)
+    for _ in range(reps):
+        qft(f, swaps=True)
+    e1.record(stream)
+    e1.synchronize()
+    fused = e0.elapsed_time(e1) / reps
+    f.free()
     return {"gates": len(gates), "ms_direct": direct, "ms_graph": graph, "us_per_gate_graph": 1e3 * graph / len(gates),
+            "ms_fused_qft": fused, "fused_rel_l2_vs_gate_by_gate": _rel(fused_out, out),
             "bound": "latency (1 MiB state, L2-resident)"}, psi0, out
 
 

@@ -90,7 +90,7 @@ Table gather_table(RankCtx& r, const std::vector<Dim>& dims, const std::vector<D
   }
   const size_t bytes = static_cast<size_t>(std::max<Dim>(1, count)) * 8;
   int64_t* ptr = nullptr;
-  QTNH_CUDA(cudaMalloc(&ptr, bytes));
+  QTNH_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), bytes, r.stream));  // pool hit, stream-ordered
   cudaEvent_t ready;
   QTNH_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   const int dev = r.device;
@@ -99,7 +99,7 @@ Table gather_table(RankCtx& r, const std::vector<Dim>& dims, const std::vector<D
     cudaGetDevice(&cur);
     cudaSetDevice(dev);
     cudaDeviceSynchronize();  // launches that named the table have been enqueued by now: let them finish
-    cudaFree(const_cast<int64_t*>(p));
+    cudaFreeAsync(const_cast<int64_t*>(p), 0);
     cudaEventDestroy(ready);
     cudaSetDevice(cur);
   });

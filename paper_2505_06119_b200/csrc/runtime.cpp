@@ -82,9 +82,19 @@ void trim_pool(int device) {
     cudaGetLastError();
     return;
   }
-  uint64_t zero = 0;
-  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &zero);
-  cudaMemPoolTrimTo(pool, 0);
+  // Keep a bounded warm reserve (QTNH_POOL_WARM_GB, default 8) mapped after the last
+  // world on the device goes away: programs (and test suites) that create worlds
+  // one after another then reuse mapped blocks instead of paying fresh physical
+  // mappings for every allocation of the next world; everything above it is
+  // returned to the driver.
+  static const uint64_t warm = [] {
+    const char* e = std::getenv("QTNH_POOL_WARM_GB");
+    const double gb = e ? std::atof(e) : 8.0;
+    return static_cast<uint64_t>(std::max(0.0, gb) * double(1ull << 30));
+  }();
+  uint64_t thr = warm;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  cudaMemPoolTrimTo(pool, warm);
 }
 
 size_t ipc_legacy_min_bytes() {

@@ -193,11 +193,18 @@ struct Plan {
   int grid = 0;
   size_t smem = 0;
   cudaEvent_t ready = nullptr;  // the tables' upload; launches on other streams wait on it
-  ~Plan() {  // only on cache eviction (cudaFree synchronises the device)
+  void* base = nullptr;         // one stream-ordered allocation for the three tables
+  int device = 0;
+  ~Plan() {  // only on cache eviction
     if (ready) cudaEventDestroy(ready);
-    if (d_tin) cudaFree(d_tin);
-    if (d_tout) cudaFree(d_tout);
-    if (d_slot) cudaFree(d_slot);
+    if (base) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(device);
+      cudaDeviceSynchronize();  // launches that used the plan have been enqueued by now
+      cudaFreeAsync(base, 0);
+      cudaSetDevice(cur);
+    }
   }
 };
 
@@ -400,9 +407,13 @@ std::shared_ptr<Plan> build_plan(const std::vector<D>& ds, int dev, cudaStream_t
   p->T = T;
   p->n_tiles = n_tiles;
   p->smem = direct ? 0 : static_cast<size_t>((T + 7) & ~7) * sizeof(double2);
-  QTNH_CUDA(cudaMalloc(&p->d_tin, T * sizeof(int64_t)));
-  QTNH_CUDA(cudaMalloc(&p->d_tout, T * sizeof(int64_t)));
-  QTNH_CUDA(cudaMalloc(&p->d_slot, T * sizeof(int)));
+  // one pool allocation (stream-ordered: a pool hit, no cudaMalloc per new layout --
+  // ~600 of them in config 3's contraction chain cost ~20 us of host time each)
+  QTNH_CUDA(cudaMallocAsync(&p->base, static_cast<size_t>(T) * (2 * sizeof(int64_t) + sizeof(int)), st));
+  p->device = dev;
+  p->d_tin = static_cast<int64_t*>(p->base);
+  p->d_tout = p->d_tin + T;
+  p->d_slot = reinterpret_cast<int*>(p->d_tout + T);
   QTNH_CUDA(cudaMemcpyAsync(p->d_tin, tin.data(), T * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   QTNH_CUDA(cudaMemcpyAsync(p->d_tout, tout.data(), T * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   QTNH_CUDA(cudaMemcpyAsync(p->d_slot, slot.data(), T * sizeof(int), cudaMemcpyHostToDevice, st));

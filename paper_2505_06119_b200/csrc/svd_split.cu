@@ -108,6 +108,16 @@ __global__ void k_fro_trace(const double2* __restrict__ x, int64_t m, double alp
   }
 }
 
+// row r of x (rows x cols) scaled by 1 / sqrt(s[r]) (0 for s[r] <= 0)
+__global__ void k_row_rsqrt_scale(double2* __restrict__ x, const double* __restrict__ s, int64_t rows, int64_t cols) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * cols;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double v = s[e / cols];
+    const double f = v > 0.0 ? 1.0 / sqrt(v) : 0.0;
+    x[e] = make_double2(x[e].x * f, x[e].y * f);
+  }
+}
+
 void conj_t(const double2* in, double2* out, Dim rows, Dim cols, cudaStream_t st) {
   dim3 g(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
   k_conj_t<<<g, dim3(32, 8), 0, st>>>(in, out, rows, cols);
@@ -254,19 +264,102 @@ void svd_batched_ptrs(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim ch
   double* S = static_cast<double*>(s);
   if (!sp.empty()) {
     const Dim ns = static_cast<Dim>(sp.size());
-    // 4. Y = P Omega, Y^H (batch of chi x m), orthonormal basis Q^H = Vh(Y^H)
+    // 4. Y = P Omega (m x chi, range(P)), and an orthonormal basis Q^H (chi x m) of it:
+    //    Gram G = Y^H Y = Vg^H Sg Vg by a chi x chi Jacobi (half the work per sweep of
+    //    a Jacobi on the chi x m Y^H), Q^H = Sg^-1/2 Vg Y^H (orthonormal to ~eps
+    //    cond(Y)^2), then Newton-Schulz polar steps Q^H <- (3 I - Q^H Q) Q^H / 2 until
+    //    ||Q^H Q - I||_F / sqrt(chi) <= 1e-14. If that does not converge (Y too
+    //    ill-conditioned for the Gram route), the chi x m Jacobi of Y^H is used.
     DevBuf om(static_cast<size_t>(m * chi) * 16, r);
     qtnh_counter_complex_normals_device(st, 0x5EEDC0DEULL, 0, m * chi, om.ptr);
     DevBuf y(static_cast<size_t>(m * chi) * 16, r);
     DevBuf yh(static_cast<size_t>(ns * chi * m) * 16, r);
+    DevBuf gm(static_cast<size_t>(ns * chi * chi) * 16, r);
     for (Dim i = 0; i < ns; ++i) {
       zgemm(X[sp[i]]->ptr, om.ptr, y.ptr, m, chi, m, st);
-      conj_t(static_cast<const double2*>(y.ptr), static_cast<double2*>(yh.ptr) + i * chi * m, m, chi, st);
+      double2* yhi = static_cast<double2*>(yh.ptr) + i * chi * m;
+      conj_t(static_cast<const double2*>(y.ptr), yhi, m, chi, st);
+      zgemm(yhi, y.ptr, static_cast<double2*>(gm.ptr) + i * chi * chi, chi, chi, m, st);
     }
     for (Dim b : sp) X[b].reset();
+    static const bool gram_basis = [] {
+      const char* e = std::getenv("QTNH_SVD_SPLIT_BASIS");
+      return !(e && std::strcmp(e, "jacobi") == 0);
+    }();
     DevBuf u1(static_cast<size_t>(ns * chi * chi) * 16, r), s1(static_cast<size_t>(ns * chi) * 8, r);
+    DevBuf vg(static_cast<size_t>(ns * chi * chi) * 16, r);
     DevBuf qh(static_cast<size_t>(ns * chi * m) * 16, r);
-    svd_batched(r, ns, chi, m, yh.ptr, chi, QTNH_ABSORB_NONE, u1.ptr, s1.ptr, qh.ptr, &sw_split);
+    if (!gram_basis) svd_batched(r, ns, chi, m, yh.ptr, chi, QTNH_ABSORB_NONE, u1.ptr, s1.ptr, qh.ptr, &sw_split);
+    if (gram_basis) svd_batched(r, ns, chi, chi, gm.ptr, chi, QTNH_ABSORB_NONE, u1.ptr, s1.ptr, vg.ptr, &sw_split);
+    for (Dim i = 0; i < ns && gram_basis; ++i) {
+      double2* qhi = static_cast<double2*>(qh.ptr) + i * chi * m;
+      zgemm(static_cast<const double2*>(vg.ptr) + i * chi * chi, static_cast<const double2*>(yh.ptr) + i * chi * m,
+            qhi, chi, m, chi, st);
+      k_row_rsqrt_scale<<<grid_elems(chi * m), 256, 0, st>>>(qhi, static_cast<const double*>(s1.ptr) + i * chi, chi,
+                                                             m);
+      QTNH_LAUNCH_CHECK();
+    }
+    if (gram_basis) {
+      std::vector<std::unique_ptr<DevBuf>> E(batch);
+      std::vector<char> pact(batch, 0);
+      for (Dim b : sp) {
+        pact[b] = 1;
+        E[b] = std::make_unique<DevBuf>(static_cast<size_t>(chi * chi) * 16, r);
+      }
+      DevBuf qm(static_cast<size_t>(m * chi) * 16, r), qn(static_cast<size_t>(chi * m) * 16, r);
+      bool polished = false;
+      for (int it = 0; it <= 4 && !polished; ++it) {
+        for (Dim i = 0; i < ns; ++i) {
+          if (!pact[sp[i]]) continue;
+          const double2* qhi = static_cast<const double2*>(qh.ptr) + i * chi * m;
+          conj_t(qhi, static_cast<double2*>(qm.ptr), chi, m, st);
+          zgemm(qhi, qm.ptr, E[sp[i]]->ptr, chi, chi, m, st);
+        }
+        // stats over chi x chi matrices: reuse the m-sized helper through a local copy
+        std::vector<double> f2(batch, 0.0);
+        {
+          for (Dim b = 0; b < batch; ++b)
+            if (pact[b]) {
+              k_fro_trace<<<kParts, 256, 0, st>>>(static_cast<const double2*>(E[b]->ptr), chi, 1.0,
+                                                  static_cast<double*>(part.ptr) + b * kParts * 2);
+              QTNH_LAUNCH_CHECK();
+            }
+          QTNH_CUDA(cudaMemcpyAsync(ph.data(), part.ptr, ph.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+          QTNH_CUDA(cudaStreamSynchronize(st));
+          for (Dim b = 0; b < batch; ++b)
+            for (int k2 = 0; k2 < kParts; ++k2) f2[b] += ph[(b * kParts + k2) * 2];
+        }
+        polished = true;
+        for (Dim i = 0; i < ns; ++i) {
+          const Dim b = sp[i];
+          if (!pact[b]) continue;
+          const double res = std::sqrt(f2[b] / static_cast<double>(chi));
+          if (std::getenv("QTNH_SVD_DEBUG"))
+            std::fprintf(stderr, "svd split: matrix %lld basis polish %d residual %.3e\n", static_cast<long long>(b),
+                         it, res);
+          if (res <= 1e-14) {
+            pact[b] = 0;
+            continue;
+          }
+          if (it == 4 || !(res < 0.5)) {  // not converging: orthonormalise Y^H by the chi x m Jacobi
+            pact[b] = 0;
+            int swj = 0;
+            svd_batched(r, 1, chi, m, static_cast<const double2*>(yh.ptr) + i * chi * m, chi, QTNH_ABSORB_NONE,
+                        static_cast<double2*>(u1.ptr) + i * chi * chi, static_cast<double*>(s1.ptr) + i * chi,
+                        static_cast<double2*>(qh.ptr) + i * chi * m, &swj);
+            sw_split = std::max(sw_split, swj);
+            continue;
+          }
+          polished = false;
+          k_axpy_identity<<<grid_elems(chi * chi), 256, 0, st>>>(static_cast<const double2*>(E[b]->ptr),
+                                                                  static_cast<double2*>(E[b]->ptr), chi, 1.5, -0.5);
+          QTNH_LAUNCH_CHECK();
+          double2* qhi = static_cast<double2*>(qh.ptr) + i * chi * m;
+          zgemm(E[b]->ptr, qhi, qn.ptr, chi, m, chi, st);
+          QTNH_CUDA(cudaMemcpyAsync(qhi, qn.ptr, static_cast<size_t>(chi * m) * 16, cudaMemcpyDeviceToDevice, st));
+        }
+      }
+    }
     // 5. B = Q^H A (chi x n) and its SVD (absorb applied), U = Q U_B
     DevBuf bm(static_cast<size_t>(ns * chi * n) * 16, r);
     for (Dim i = 0; i < ns; ++i)

@@ -453,3 +453,48 @@ def test_many_plan_shapes_interleaved():
     for (dims, perm), got in zip(cases, outs):
         g = circuits.counter_state(len(dims), int(np.prod(dims)))
         assert np.array_equal(bits(got), bits(P.permute(dims, g, perm)))
+
+
+@pytest.mark.parametrize("world,split", [(4, 2), (8, 3)])
+def test_peer_kernels_write_only_their_blocks(world, split, peer_mode):
+    """Canary check of the multi-rank kernels (push remap, pairwise in-place swaps,
+    the pipelined exchange form, fused distributed gates and QFT): every rank
+    interleaves sentinel tensors with its working tensors in the stream-ordered
+    pool, runs the ops, and the sentinels must come back bit-identical while the
+    results stay bit-exact / within tolerance (compute-sanitizer is not available
+    on this pool; a stray store lands in a neighbouring allocation)."""
+    from paper_2505_06119_b200.qtnh import apply_gate, qft, swap_indices
+
+    n = 16
+    g = circuits.counter_state(77, 2**n)
+    pattern = circuits.counter_state(78, 2 ** (n - split))
+    perm = circuits.fisher_yates(79, 10, n)
+
+    def body(rk):
+        sentinels = []
+        for _ in range(3):
+            sentinels.append(Tensor.dense(rk, IndexTuple([2] * (n - split), 0), DistParams(1, 1, rk.rank()),
+                                          pattern))
+        t = Tensor.from_global(rk, IndexTuple([2] * n, split), DistParams(1, 1, 0), g)
+        sentinels.append(Tensor.dense(rk, IndexTuple([2] * (n - split), 0), DistParams(1, 1, rk.rank()), pattern))
+        p = ops.permute(t, perm, split)
+        swap_indices(t, 0, n - 1)
+        apply_gate(t, [1], circuits.H)
+        apply_gate(t, [0, n - 2], circuits.FSIM)
+        u = Tensor.from_global(rk, IndexTuple([2] * n, split), DistParams(1, 1, 0), g)
+        qft(u, swaps=True)
+        out = (p.to_global_vector(), t.to_global_vector(), u.to_global_vector())
+        for s in sentinels:
+            assert np.array_equal(bits(s.local_data()), bits(pattern)), "a sentinel allocation was overwritten"
+        return out
+
+    pv, tv, uv = World(world).run(body)[0]
+    assert np.array_equal(bits(pv), bits(P.permute([2] * n, g, perm)))
+    sw = list(range(n))
+    sw[0], sw[n - 1] = n - 1, 0
+    want = P.permute([2] * n, g, sw)
+    want = P.gate([2] * n, want, [1], circuits.H)
+    want = P.gate([2] * n, want, [0, n - 2], circuits.FSIM)
+    assert np.linalg.norm(tv - want) <= 1e-12 * np.linalg.norm(want)
+    wq = P.qft(n, g)
+    assert np.linalg.norm(uv - wq) <= 1e-12 * np.linalg.norm(wq)
