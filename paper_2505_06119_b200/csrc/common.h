@@ -63,6 +63,10 @@ inline void note_launch(int64_t n = 1) { g_kernel_launches.fetch_add(n, std::mem
     QTNH_CUDA(cudaGetLastError());                 \
   } while (0)
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, size):
+// a driver call per launch cost ~1-2 us of host time on every small contraction.
+void ensure_max_dynamic_smem(const void* kernel, int bytes);
+
 // ---- sharded layout metadata (indexing.hpp:32-191 semantics) -----------------
 // dims with the first `split` indices distributed (they select the rank block,
 // row-major) and the rest local (row-major inside the rank's block).

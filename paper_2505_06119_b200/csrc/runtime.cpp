@@ -14,6 +14,18 @@ std::atomic<int64_t> g_kernel_launches{0};
 
 void RankCtx::activate() const { QTNH_CUDA(cudaSetDevice(device)); }
 
+void ensure_max_dynamic_smem(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> size set
+  int dev = 0;
+  QTNH_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = done[{kernel, dev}];
+  if (have >= bytes) return;
+  QTNH_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  have = bytes;
+}
+
 cudaStream_t RankCtx::side_stream(int i) {
   if (!side[i]) QTNH_CUDA(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
   return side[i];

@@ -468,8 +468,7 @@ void launch_mode(const double2* a, const int64_t* ro, const int64_t* co, const d
   else if (MODE != 0 && k <= kCoSmemMax) co_bytes = static_cast<size_t>(k) * 8;
   if (co_bytes > kCoSmemMax * 8) throw_invalid("column offset split exceeds its shared-memory budget");
   const size_t smem = G::SMEM + co_bytes;
-  QTNH_CUDA(cudaFuncSetAttribute(k_zgemm<G, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(G::SMEM + kCoSmemMax * 8)));
+  ensure_max_dynamic_smem(reinterpret_cast<const void*>(k_zgemm<G, MODE>), (int)(G::SMEM + kCoSmemMax * 8));
   Dim tiles = ((m + G::BM - 1) / G::BM) * ((n + G::BN - 1) / G::BN);
   if (tiles > 0x7fffffff) throw_invalid("zgemm problem too large for one launch");
   k_zgemm<G, MODE><<<static_cast<unsigned>(tiles), G::THREADS, smem, st>>>(a, ro, co, b, c, m, n, k, cohi, co_sh, rohi,
@@ -502,8 +501,7 @@ template <class G, int MODE, int CO>
 void launch_even_co(const double2* a, const int64_t* ro, const int64_t* co, const double2* b, double2* c, Dim m,
                     Dim n, Dim k, cudaStream_t st, const int64_t* cohi, int co_sh, const int64_t* rohi, int ro_sh,
                     size_t co_bytes) {
-  QTNH_CUDA(cudaFuncSetAttribute(k_zgemm_even<G, MODE, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(G::SMEM + kCoSmemMax * 8)));
+  ensure_max_dynamic_smem(reinterpret_cast<const void*>(k_zgemm_even<G, MODE, CO>), (int)(G::SMEM + kCoSmemMax * 8));
   const Dim tiles = (m / G::BM) * (n / G::BN);
   if (tiles > 0x7fffffff) throw_invalid("zgemm problem too large for one launch");
   k_zgemm_even<G, MODE, CO><<<static_cast<unsigned>(tiles), G::THREADS, G::SMEM + co_bytes, st>>>(
