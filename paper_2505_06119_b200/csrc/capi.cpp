@@ -1065,6 +1065,13 @@ int qtnh_svd_device(qtnh_rank_t r, int64_t batch, int64_t m, int64_t n, const vo
     int sweeps = 0;
     svd_batched(x, batch, m, n, a, chi, absorb, u, s, vh, &sweeps);
     t_info = sweeps;
+    const Dim c = chi > 0 ? chi : std::min(m, n);
+    std::vector<void*> up(batch), vp(batch);
+    for (int64_t b = 0; b < batch; ++b) {
+      up[b] = static_cast<char*>(u) + static_cast<size_t>(b * m * c) * 16;
+      vp[b] = static_cast<char*>(vh) + static_cast<size_t>(b * c * n) * 16;
+    }
+    svd_complete_null(x, batch, m, n, c, absorb, up.data(), s, vp.data());
   });
 }
 
@@ -1141,6 +1148,9 @@ int qtnh_svd(qtnh_tensor_t t, int n_row, const int* row_pos, int n_col, const in
       int sweeps = 0;
       svd_batched(r, 1, m, n, mat->data(), chi, absorb, u->data(), s.ptr, vh->data(), &sweeps);
       t_info = sweeps;
+      void* up = u->data();
+      void* vp = vh->data();
+      svd_complete_null(r, 1, m, n, chi, absorb, &up, s.ptr, &vp);
     }
     if (!span_members.empty() &&
         std::find(span_members.begin(), span_members.end(), r.rank) != span_members.end()) {

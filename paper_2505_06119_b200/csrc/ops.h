@@ -101,6 +101,13 @@ void svd_batched(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, in
 void svd_batched_ptrs(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* const* u_ptrs,
                       void* s, void* const* vh_ptrs, int* sweeps_out);
 int64_t svd_split_count();  // matrices factorised by the split path so far
+// Null singular directions (sigma <= max(m, n) eps sigma_0) of svd outputs
+// replaced by an orthonormal completion (svd_null.cu): U and Vh stay isometries
+// on their non-absorbed side like zgesdd's (linalg.hpp:441-471).
+void svd_complete_null(RankCtx& r, Dim batch, Dim m, Dim n, Dim chi, int absorb, void* const* u_ptrs, const void* s,
+                       void* const* vh_ptrs);
+// out (cols x rows) = conj(in (rows x cols))^T, complex128 row-major.
+void conj_transpose(const void* in, void* out, Dim rows, Dim cols, cudaStream_t st);
 void svd_jacobi_ptrs(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* const* u_ptrs,
                      void* s, void* const* vh_ptrs, int* sweeps_out);
 // One layer of MPS two-site updates (mps.cu): pair i = (left[i], right[i]),

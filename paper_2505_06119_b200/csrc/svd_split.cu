@@ -138,6 +138,10 @@ bool split_enabled() {
 
 }  // namespace
 
+void conj_transpose(const void* in, void* out, Dim rows, Dim cols, cudaStream_t st) {
+  conj_t(static_cast<const double2*>(in), static_cast<double2*>(out), rows, cols, st);
+}
+
 void svd_batched_ptrs(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int absorb, void* const* u_ptrs,
                       void* s, void* const* vh_ptrs, int* sweeps_out) {
   QTNH_RANGE("qtnh::svd");

@@ -222,3 +222,48 @@ def test_svd_spectral_split_path(case):
         assert took == 1
     if case == "no_gap":
         assert took == 0
+
+
+def _iso_cols(u):
+    return np.abs(u.conj().T @ u - np.eye(u.shape[1])).max()
+
+
+@pytest.mark.parametrize("m,n,rank", [(48, 40, 5), (40, 48, 5), (8, 6, 0), (64, 64, 1), (300, 260, 120)])
+def test_svd_null_directions_are_completed(m, n, rank):
+    """Rank-deficient input: the bases stay isometries on their non-absorbed side
+    (zgesdd's do, linalg.hpp:441-471) -- null singular directions get an
+    orthonormal completion instead of zero / noise vectors -- and U S Vh is
+    unchanged."""
+    rng = np.random.default_rng(m + n + rank)
+    x = rng.standard_normal((m, max(rank, 1))) + 1j * rng.standard_normal((m, max(rank, 1)))
+    y = rng.standard_normal((max(rank, 1), n)) + 1j * rng.standard_normal((max(rank, 1), n))
+    a = (x @ y) * (1.0 if rank else 0.0)
+    k = min(m, n)
+    for mode in (ABSORB_NONE, ABSORB_LEFT, ABSORB_RIGHT):
+        u, s, vh = gpu_svd(a, chi=0, absorb=mode)
+        assert s.shape == (k,)
+        assert np.all(s[rank:] <= 1e-12 * max(s[0], 1.0))
+        if rank:
+            assert np.allclose(s[:rank], np.linalg.svd(a, compute_uv=False)[:rank], rtol=1e-12)
+        uu = u if mode != ABSORB_LEFT else None
+        vv = vh if mode != ABSORB_RIGHT else None
+        if uu is not None:
+            assert _iso_cols(uu) < 1e-12, mode
+        if vv is not None:
+            assert _iso_cols(vv.conj().T) < 1e-12, mode
+        prod = (u * s) @ vh if mode == ABSORB_NONE else u @ vh
+        if rank:
+            assert rel_l2(prod, a) < TOL
+        else:
+            assert np.abs(prod).max() == 0.0
+
+
+def test_svd_null_cnot_bell_bond():
+    """SPEC example: |00> then CNOT gives a Bell pair; its 2 x 2 theta has sigma = (1/sqrt2,
+    1/sqrt2) but H alone on |00> gives rank 1: the second direction is null and
+    must still be a unit vector orthogonal to the first."""
+    a = np.array([[1.0, 0.0], [1.0, 0.0]], dtype=np.complex128) / np.sqrt(2)
+    u, s, vh = gpu_svd(a, chi=2, absorb=ABSORB_NONE)
+    assert np.allclose(s, [1.0, 0.0], atol=1e-15)
+    assert _iso_cols(u) < 1e-14 and _iso_cols(vh.conj().T) < 1e-14
+    assert rel_l2((u * s) @ vh, a) < 1e-14
