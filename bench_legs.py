@@ -209,6 +209,11 @@ def gpu_c3(rk, stream, torch, rows=5, cols=6, depth=14, n_open=6, trials=64):
     t0 = time.perf_counter()
     order = network.Network.plan(net.labels, net.dims, SEED, trials=trials)
     plan_s = time.perf_counter() - t0
+    # one untimed run of the same order first (the memory pool maps its blocks and
+    # the offset-table caches fill, as in any run after the first)
+    warm = net.contract_order_native(order)
+    net.tensors[warm].free()
+    net, open_labels, open_q, fixed = network.build_rcs_network(rk, rows, cols, depth, SEED, n_open)
     labels0 = {k: list(v) for k, v in net.labels.items()}
     fl, big, by = network.Network.cost(net.labels, net.dims, order)
     rk.synchronize()

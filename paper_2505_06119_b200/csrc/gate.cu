@@ -13,6 +13,7 @@
 // Diagonal gates touch only the fibers' elements whose diagonal entry is not 1.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -21,6 +22,7 @@
 #include <vector>
 
 #include "ops.h"
+#include "tma.h"
 
 namespace qtnhb {
 
@@ -867,6 +869,82 @@ __device__ __forceinline__ double2 canon2(double2 v) {
   return v;
 }
 
+// TMA form of the in-place bit reversal (default): the tiles arrive by
+// cp.async.bulk.tensor instead of 2048 per-thread 16-byte cp.async per tile pair.
+// The state is a 3-D FLOAT64 tensor [a: 32][m: 2^(n-10)][b: 64 doubles]; a box
+// is {16 doubles = 8 amplitudes of b, 1 m, 32 a}, 4 KB with the 128-byte
+// swizzle (16-byte chunk j of row a stored at j ^ (a & 7)), so the bit-reversed
+// column reads below hit 8 distinct 16-byte bank groups per 32 lanes. A stage
+// is one tile pair (2 x 4 boxes, 32 KB), S stages per CTA with one mbarrier
+// each; one thread re-arms a stage after the CTA barrier that ends its reads.
+// Stores are plain coalesced 512-byte warp rows (the tile order is final).
+template <int S>
+__global__ void __launch_bounds__(512) k_bitrev_tma(const __grid_constant__ CUtensorMap tm, double2* __restrict__ psi,
+                                                       int n, int64_t n_mid) {
+  extern __shared__ unsigned char smem_raw[];
+  double2* tiles = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[S];
+  const int mbits = n - 10;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  auto rev_m = [&](int64_t m) {
+    return mbits > 0 ? static_cast<int64_t>(rev_bits64(static_cast<uint64_t>(m), mbits)) : m;
+  };
+  auto next_valid = [&](int64_t m) {
+    while (m < n_mid && rev_m(m) < m) m += gridDim.x;  // a pair is handled by its smaller member
+    return m;
+  };
+  int64_t m_issue = 0;
+  auto issue = [&](int stage, int64_t m) {
+    const int64_t mr = rev_m(m);
+    double2* t1 = tiles + stage * 2048;
+    double2* t2 = t1 + 1024;
+    mbar_arrive_expect_tx(&full[stage], mr != m ? 32768u : 16384u);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      tma_load_3d(t1 + c * 256, &tm, c * 16, static_cast<int>(m), 0, &full[stage]);
+      if (mr != m) tma_load_3d(t2 + c * 256, &tm, c * 16, static_cast<int>(mr), 0, &full[stage]);
+    }
+  };
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tm);
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    m_issue = next_valid(blockIdx.x);
+    for (int s = 0; s < S && m_issue < n_mid; ++s) {
+      issue(s, m_issue);
+      m_issue = next_valid(m_issue + gridDim.x);
+    }
+  }
+  __syncthreads();
+  const int rb = rev_bits(lane, 5);
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t m = next_valid(blockIdx.x); m < n_mid; m = next_valid(m + gridDim.x)) {
+    mbar_wait(&full[stage], phase);
+    const int64_t mr = rev_m(m);
+    const double2* t1 = tiles + stage * 2048;
+    const double2* t2 = mr != m ? t1 + 1024 : t1;
+    for (int a = warp; a < 32; a += nwarps) {
+      const int ra = rev_bits(a, 5);
+      // source (row rb, amplitude ra): box ra >> 3, chunk (ra & 7) ^ (rb & 7)
+      const int src = (ra >> 3) * 256 + rb * 8 + ((ra & 7) ^ (rb & 7));
+      // new (a, m, b) = old (rev b, rev m, rev a)
+      psi[(int64_t(a) << (n - 5)) | (m << 5) | lane] = canon2(t2[src]);
+      if (mr != m) psi[(int64_t(a) << (n - 5)) | (mr << 5) | lane] = canon2(t1[src]);
+    }
+    __syncthreads();  // every read of this stage is done
+    if (threadIdx.x == 0 && m_issue < n_mid) {
+      fence_proxy_async_smem();
+      issue(stage, m_issue);
+      m_issue = next_valid(m_issue + gridDim.x);
+    }
+    if (++stage == S) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+}
+
 // n >= 10: x = (a: top 5 bits, m: middle n-10 bits, b: low 5 bits).
 
 // In-place bit reversal: the two 32 x 32 tiles of a pair are
@@ -1255,15 +1333,50 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
 void bitrev_local(void* data, int nb, cudaStream_t st) {
   if (nb < 10) throw_invalid("in-place bit reversal needs at least 10 local qubits");
   int64_t n_mid = int64_t(1) << (nb - 10);
+  int dev = 0, occ = 0, sms = 0;
+  QTNH_CUDA(cudaGetDevice(&dev));
+  QTNH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // QTNH_BITREV_TMA=1: the TMA form (read per call). Measured at n = 30 (ncu,
+  // cold): 6.35 ms for k_bitrev2 vs 6.41 ms for the best TMA configuration (2
+  // stages, 256 threads, 3 CTAs/SM) and 7.9 ms with 6 stages at 1 CTA/SM -- the
+  // pass is bound by the DRAM traffic pattern (64 pages per tile pair), not by
+  // load issue, so deeper TMA pipelines only add outstanding scattered requests.
+  const char* tma_env = std::getenv("QTNH_BITREV_TMA");
+  const bool use_tma = tma_env && tma_env[0] == '1';
+  if (use_tma && n_mid <= (int64_t(1) << 31)) {
+    // QTNH_BITREV_CFG = "stages,threads,ctas_per_sm" (stages 2, 3, 4 or 6)
+    static int cfg[3] = {2, 256, 3};
+    static bool parsed = [] {
+      if (const char* e = std::getenv("QTNH_BITREV_CFG")) std::sscanf(e, "%d,%d,%d", &cfg[0], &cfg[1], &cfg[2]);
+      return true;
+    }();
+    (void)parsed;
+    CUtensorMap tm;
+    const uint64_t dims[3] = {64, static_cast<uint64_t>(n_mid), 32};
+    const uint64_t strides[2] = {512, static_cast<uint64_t>(16) << (nb - 5)};
+    const uint32_t box[3] = {16, 1, 32};
+    make_tensor_map_f64(&tm, data, 3, dims, strides, box, true);
+    const int grid = static_cast<int>(std::min<int64_t>(n_mid, static_cast<int64_t>(sms) * cfg[2]));
+    auto launch = [&](auto kern, int S) {
+      const size_t smem = static_cast<size_t>(S) * 2048 * sizeof(double2) + 1024;
+      QTNH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      kern<<<grid, cfg[1], smem, st>>>(tm, static_cast<double2*>(data), nb, n_mid);
+    };
+    switch (cfg[0]) {
+      case 2: launch(k_bitrev_tma<2>, 2); break;
+      case 3: launch(k_bitrev_tma<3>, 3); break;
+      case 4: launch(k_bitrev_tma<4>, 4); break;
+      default: launch(k_bitrev_tma<6>, 6); break;
+    }
+    QTNH_LAUNCH_CHECK();
+    return;
+  }
   const size_t smem = 4 * 1024 * sizeof(double2);  // 2 stages x 2 tiles
   static bool attr = [] {
     cudaFuncSetAttribute(k_bitrev2, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     return true;
   }();
   (void)attr;
-  int dev = 0, occ = 0, sms = 0;
-  QTNH_CUDA(cudaGetDevice(&dev));
-  QTNH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bitrev2, 256, smem));
   int grid = static_cast<int>(std::min<int64_t>(n_mid, (int64_t)sms * std::max(1, occ)));
   k_bitrev2<<<grid, 256, smem, st>>>(static_cast<double2*>(data), nb, n_mid);

@@ -324,3 +324,32 @@ def test_cuda_graph_of_a_gate_sequence():
     assert rel_l2(direct, P.qft(n, st)) < TOL
     seq2 = P.qft(n, P.qft(n, st))
     assert rel_l2(twice, seq2) < 1e-10
+
+
+@pytest.mark.parametrize("tma", ["0", "1"])
+@pytest.mark.parametrize("n", [10, 11, 12, 15, 20, 23])
+def test_qft_bit_reversal_pass_bit_exact(n, tma, monkeypatch):
+    """The final SWAP network of the whole-QFT path is one in-place bit-reversal
+    pass (gate.cu k_bitrev2, or k_bitrev_tma with QTNH_BITREV_TMA=1): QFT with swaps
+    must equal QFT without swaps followed by a host bit reversal of the index, bit
+    for bit."""
+    from paper_2505_06119_b200.qtnh import qft
+    monkeypatch.setenv("QTNH_BITREV_TMA", tma)
+    st = circuits.counter_state(500 + n, 2**n)
+
+    def body(swaps):
+        def f(rk):
+            t = Tensor.from_global(rk, IndexTuple([2] * n, 0), None, st)
+            qft(t, swaps=swaps)
+            return t.to_global_vector()
+        return f
+
+    with_swaps = run_collect(World(1), body(True))
+    without = run_collect(World(1), body(False))
+    idx = np.arange(2**n)
+    rev = np.zeros_like(idx)
+    for b in range(n):
+        rev |= ((idx >> b) & 1) << (n - 1 - b)
+    want = without[rev]
+    want = np.where(want == 0, 0.0, want)  # signed zeros canonicalised by the pass
+    assert np.array_equal(with_swaps.view(np.uint64), np.ascontiguousarray(want).view(np.uint64))
