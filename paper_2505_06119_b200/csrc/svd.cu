@@ -24,6 +24,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <numeric>
 #include <vector>
 
@@ -93,8 +94,8 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 // X_bi X_bj^H (B x B per split); the diagonal blocks X_b X_b^H come from dblk
 // (refreshed from X at the start of every sweep, then carried from round to round
 // as the rotated diagonal blocks of W^H G W, which this kernel writes back).
-template <int B>
-__global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__ part, double2* __restrict__ wh,
+template <int B, int T = 256, bool V3 = false>
+__global__ void __launch_bounds__(T) k_svd_eigen_t(const double2* __restrict__ part, double2* __restrict__ wh,
                                                      int* __restrict__ flags, double* __restrict__ off_max,
                                                      int npairs, int splits, double tol, int inner_sweeps,
                                                      const double* __restrict__ floor_abs,
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
   __shared__ double rot_c[B], rot_s[B];
   __shared__ double2 rot_ph[B];
   __shared__ int rp_[B], rq_[B];
-  __shared__ double red[256];
+  __shared__ double red[T];
   // Rotation threshold (classical threshold Jacobi): pairs with |G_pq| below
   // thr sqrt(G_pp G_qq) are not rotated (rot_thr, set per matrix by the host:
   // adapt x the previous sweep's max off-norm once that falls only linearly). Inside a cluster of (nearly) equal singular
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
     Di = dblk + (static_cast<int64_t>(mat) * nblk2 + pr[0]) * B * B;
     Dj = dblk + (static_cast<int64_t>(mat) * nblk2 + pr[1]) * B * B;
     const double2* P = part + (static_cast<int64_t>(mat) * npairs + pair) * splits * B * B;
-    for (int e = tid; e < P2 * P2; e += 256) {
+    for (int e = tid; e < P2 * P2; e += T) {
       const int i = e / P2, j = e % P2;
       double2 v;
       if (i < B && j < B) {
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
     }
   } else {
     const double2* P = part + (static_cast<int64_t>(mat) * npairs + pair) * splits * P2 * P2;
-    for (int e = tid; e < P2 * P2; e += 256) {
+    for (int e = tid; e < P2 * P2; e += T) {
       int i = e / P2, j = e % P2;
       double2 sm = make_double2(0.0, 0.0);
       for (int sp = 0; sp < splits; ++sp) {
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
   __syncthreads();
   auto measure = [&]() {
     double mx = 0.0;
-    for (int e = tid; e < P2 * P2; e += 256) {
+    for (int e = tid; e < P2 * P2; e += T) {
       int i = e / P2, j = e % P2;
       if (i >= j) continue;
       double d = sqrt(fmax(G[i * LD + i].x * G[j * LD + j].x, 0.0));
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
     }
     red[tid] = mx;
     __syncthreads();
-    for (int st = 128; st > 0; st >>= 1) {
+    for (int st = T / 2; st > 0; st >>= 1) {
       if (tid < st) red[tid] = fmax(red[tid], red[tid + st]);
       __syncthreads();
     }
@@ -194,7 +195,83 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
     if (tid == 0) flags[fidx] = 0;
     return;
   }
-  if constexpr (B == 16) {
+  if constexpr (V3) {
+    // Two barriers per step, G and V updated in place: the step's B rotations are
+    // computed once (threads 0..B-1) into shared memory, then every thread applies
+    // them to its 2 x 2 blocks of G and its V column pairs; the tournament is a
+    // shared table. Against the one-barrier form below (every warp recomputing all
+    // rotations and handing them out by shuffles, the pairs recomputed with integer
+    // modulo per task) this issues ~4x fewer instructions per step, and G needs no
+    // second buffer (more pair solves per SM).
+    __shared__ unsigned char pq_s[P2 - 1][B][2];
+    for (int e = tid; e < (P2 - 1) * B; e += T) {
+      const int step = e / B, rr = e % B;
+      int p, q;
+      if (rr == 0) {
+        p = step;
+        q = P2 - 1;
+      } else {
+        p = (step + rr) % (P2 - 1);
+        q = (step - rr + (P2 - 1)) % (P2 - 1);
+      }
+      pq_s[step][rr][0] = static_cast<unsigned char>(p < q ? p : q);
+      pq_s[step][rr][1] = static_cast<unsigned char>(p < q ? q : p);
+    }
+    __syncthreads();
+    for (int sw = 0; sw < inner_sweeps; ++sw) {
+      for (int step = 0; step < P2 - 1; ++step) {
+        if (tid < B) {
+          const int p = pq_s[step][tid][0], q = pq_s[step][tid][1];
+          const double a = G[p * LD + p].x, b = G[q * LD + q].x;
+          const double2 x = G[p * LD + q];
+          const double r2 = fma(x.x, x.x, x.y * x.y);
+          double c = 1.0, sn = 0.0;
+          double2 ph = make_double2(1.0, 0.0);
+          if (r2 > 1e-600 && !(r2 <= rot_thr2 * fabs(a * b))) {
+            const double inv_ax = rsqrt(r2);
+            ph = make_double2(x.x * inv_ax, -x.y * inv_ax);
+            const double tau = 0.5 * (b - a) * inv_ax;
+            const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
+            c = rsqrt(fma(t, t, 1.0));
+            sn = t * c;
+          }
+          rot_c[tid] = c;
+          rot_s[tid] = sn;
+          rot_ph[tid] = ph;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int task = tid; task < B * B; task += T) {  // 2 x 2 block (pk, qk) x (pl, ql), in place
+          const int k = task / B, l = task % B;
+          const int pk = pq_s[step][k][0], qk = pq_s[step][k][1], pl = pq_s[step][l][0], ql = pq_s[step][l][1];
+          const double ck = rot_c[k], sk = rot_s[k], cl = rot_c[l], sl = rot_s[l];
+          const double2 ek = cconj(rot_ph[k]), el = rot_ph[l];
+          double2 a = G[pk * LD + pl], b = G[pk * LD + ql], cc = G[qk * LD + pl], d = G[qk * LD + ql];
+          double2 bq = cmul(b, el), dq = cmul(d, el);
+          double2 a1 = make_double2(cl * a.x - sl * bq.x, cl * a.y - sl * bq.y);
+          double2 b1 = make_double2(sl * a.x + cl * bq.x, sl * a.y + cl * bq.y);
+          double2 c1 = make_double2(cl * cc.x - sl * dq.x, cl * cc.y - sl * dq.y);
+          double2 d1 = make_double2(sl * cc.x + cl * dq.x, sl * cc.y + cl * dq.y);
+          double2 c2 = cmul(c1, ek), d2 = cmul(d1, ek);
+          G[pk * LD + pl] = make_double2(ck * a1.x - sk * c2.x, ck * a1.y - sk * c2.y);
+          G[pk * LD + ql] = make_double2(ck * b1.x - sk * d2.x, ck * b1.y - sk * d2.y);
+          G[qk * LD + pl] = make_double2(sk * a1.x + ck * c2.x, sk * a1.y + ck * c2.y);
+          G[qk * LD + ql] = make_double2(sk * b1.x + ck * d2.x, sk * b1.y + ck * d2.y);
+        }
+#pragma unroll
+        for (int task = tid; task < P2 * B; task += T) {  // V columns p, q of rotation kk, in place
+          const int i = task % P2, kk = task / P2;
+          const int p = pq_s[step][kk][0], q = pq_s[step][kk][1];
+          const double cc = rot_c[kk], ss = rot_s[kk];
+          double2 vp = V[i * LD + p], vq = cmul(V[i * LD + q], rot_ph[kk]);
+          V[i * LD + p] = make_double2(cc * vp.x - ss * vq.x, cc * vp.y - ss * vq.y);
+          V[i * LD + q] = make_double2(ss * vp.x + cc * vq.x, ss * vp.y + cc * vq.y);
+        }
+        __syncthreads();
+      }
+      if (sw + 1 < inner_sweeps && measure() < tol * 1e-2) break;
+    }
+  } else if constexpr (B == 16) {
     // One barrier per step: G is double-buffered (read Gc, write Gn), and every warp
     // computes the step's 16 rotations itself (lane r & 15 -> rotation r & 15) and
     // hands each thread the parameters it needs by shuffles, so the step no longer
@@ -240,8 +317,9 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
           rs = __shfl_sync(0xffffffffu, sn, r);
           rph = make_double2(__shfl_sync(0xffffffffu, phx, r), __shfl_sync(0xffffffffu, phy, r));
         };
-        {  // G task (k, l): the 2 x 2 blocks of rows (pk, qk) x columns (pl, ql), Gc -> Gn
-          const int k = tid / B, l = tid % B;
+#pragma unroll
+        for (int task = tid; task < B * B; task += T) {  // G task (k, l): 2 x 2 blocks (pk, qk) x (pl, ql), Gc -> Gn
+          const int k = task / B, l = task % B;
           int pk, qk, pl, ql;
           pair_of(step, k, pk, qk);
           pair_of(step, l, pl, ql);
@@ -263,8 +341,8 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
           Gn[qk * LD + ql] = make_double2(sk * b1.x + ck * d2.x, sk * b1.y + ck * d2.y);
         }
   #pragma unroll
-        for (int h = 0; h < 2; ++h) {  // V tasks (i, kk): columns p, q of rotation kk, in place
-          const int task = tid + h * 256, i = task % P2, kk = task / P2;
+        for (int h = 0; h < P2 * B / T; ++h) {  // V tasks (i, kk): columns p, q of rotation kk, in place
+          const int task = tid + h * T, i = task % P2, kk = task / P2;
           int p, q;
           pair_of(step, kk, p, q);
           double cc, ss;
@@ -322,7 +400,7 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
           rq_[tid] = q;
         }
         __syncthreads();
-        for (int task = tid; task < B * B; task += 256) {
+        for (int task = tid; task < B * B; task += T) {
           const int k = task / B, l = task % B;
           const int pk = rp_[k], qk = rq_[k], pl = rp_[l], ql = rq_[l];
           const double ck = rot_c[k], sk = rot_s[k], cl = rot_c[l], sl = rot_s[l];
@@ -339,7 +417,7 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
           G[qk * LD + pl] = make_double2(sk * a1.x + ck * c2.x, sk * a1.y + ck * c2.y);
           G[qk * LD + ql] = make_double2(sk * b1.x + ck * d2.x, sk * b1.y + ck * d2.y);
         }
-        for (int task = tid; task < P2 * B; task += 256) {
+        for (int task = tid; task < P2 * B; task += T) {
           const int i = task % P2, kk = task / P2;
           const int p = rp_[kk], q = rq_[kk];
           const double cc = rot_c[kk], ss = rot_s[kk];
@@ -371,12 +449,12 @@ __global__ void __launch_bounds__(256) k_svd_eigen_t(const double2* __restrict__
   }
   __syncthreads();
   double2* out = wh + fidx * P2 * P2;
-  for (int e = tid; e < P2 * P2; e += 256) {
+  for (int e = tid; e < P2 * P2; e += T) {
     int i = e / P2, j = e % P2;
     out[e] = cconj(V[j * LD + perm_s[i]]);  // rows of W^H, reordered
   }
   if (cross) {  // G now holds W^H G W: its diagonal blocks are the updated rows' Grams
-    for (int e = tid; e < B * B; e += 256) {
+    for (int e = tid; e < B * B; e += T) {
       const int i = e / B, j = e % B;
       Di[e] = G[perm_s[i] * LD + perm_s[j]];
       Dj[e] = G[perm_s[i + B] * LD + perm_s[j + B]];
@@ -892,7 +970,31 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
     tab[(static_cast<size_t>(rounds) * npairs + k) * 2] = 2 * k;
     tab[(static_cast<size_t>(rounds) * npairs + k) * 2 + 1] = 2 * k + 1;
   }
-  for (int rd = 0; rd < rounds; ++rd)
+  // QTNH_SVD_ORDER=xor (power-of-two block counts): round r pairs block i with
+  // i ^ s_r, s_r = gray(r + 1) -- the hypercube ordering. Measured against the
+  // circle method: 2048^2 random 16 vs 17 sweeps at the same time per SVD, C4
+  // 7.35 vs 7.20 s. Its quads {i, i^s, i^t, i^s^t} allowed fusing each round's
+  // update with the next round's cross Grams (no separate read of X per round):
+  // 390 us per batch-8 round against 255 + 104 us for the two kernels -- the
+  // update is DMMA-bound, so the Gram DMMAs it absorbed cost more than the HBM
+  // pass they saved; the fused kernel was dropped.
+  static const bool xor_order = [] {
+    const char* e = std::getenv("QTNH_SVD_ORDER");
+    return e && std::strcmp(e, "xor") == 0;
+  }();
+  const bool use_xor = xor_order && (nblk2 & (nblk2 - 1)) == 0;
+  for (int rd = 0; rd < rounds; ++rd) {
+    if (use_xor) {
+      const int g = (rd + 1) ^ ((rd + 1) >> 1);
+      int k = 0;
+      for (int i = 0; i < nblk2; ++i)
+        if (i < (i ^ g)) {
+          tab[(rd * npairs + k) * 2] = i;
+          tab[(rd * npairs + k) * 2 + 1] = i ^ g;
+          ++k;
+        }
+      continue;
+    }
     for (int k = 0; k < npairs; ++k) {
       int p, q;
       if (k == 0) {
@@ -905,6 +1007,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
       tab[(rd * npairs + k) * 2] = p;
       tab[(rd * npairs + k) * 2 + 1] = q;
     }
+  }
   // streams the batch is split over (QTNH_SVD_GROUPS): each group's latency-bound
   // eigen step overlaps the others' DMMA work; C4 (layer batches of 9-10): 2 groups
   // 14.9 s, 3 groups 14.4 s, 4 groups 14.4-14.9 s
@@ -915,8 +1018,14 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   }();
   const int ngroups = static_cast<int>(std::max<Dim>(1, std::min<Dim>(batch, want_groups)));
   const Dim per_group = (batch + ngroups - 1) / ngroups;  // see the multi-stream split below
-  int splits = static_cast<int>(std::max<Dim>(1, std::min<Dim>((2 * sms() + npairs * per_group - 1) / (npairs * per_group),
-                                                                (L + kGramCols - 1) / kGramCols)));
+  // column splits of the Gram pass (the eigen step sums the partials in a fixed
+  // order); QTNH_SVD_GRAM_CTAS = target CTAs per SM per launch
+  static const int gram_ctas = [] {
+    const char* e = std::getenv("QTNH_SVD_GRAM_CTAS");
+    return e ? std::max(1, std::atoi(e)) : 4;  // batch-8 2048^2: 2 -> 4 CTAs/SM, 101-109 -> 97.5-98 ms per SVD
+  }();
+  int splits = static_cast<int>(std::max<Dim>(
+      1, std::min<Dim>((gram_ctas * sms() + npairs * per_group - 1) / (npairs * per_group), (L + kGramCols - 1) / kGramCols)));
   // de Rijk ordering (QTNH_SVD_SORT=1): rows sorted by descending norm before every
   // sweep (one gather of WK per sweep). 2048^2 random: 17 -> 14 sweeps, 8-decade
   // graded 320^2: 33 -> 23; but the C4 MPS thetas: ~32 -> ~42, so it is off by default.
@@ -980,6 +1089,24 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
     QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_v2<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd2_smem));
   const size_t gram_smem = static_cast<size_t>(2) * P2 * (32 + 4) * 16;
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_eigen_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_smem));
+  QTNH_CUDA(cudaFuncSetAttribute(k_svd_eigen_t<B, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_smem));
+  QTNH_CUDA(cudaFuncSetAttribute(k_svd_eigen_t<B, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_smem));
+  // threads per pair solve: every warp computes the step's rotations itself (one
+  // barrier per step), so fewer warps per pair means fewer redundant instructions
+  static const int eig_t = [] {
+    const char* e = std::getenv("QTNH_SVD_EIG_T");
+    const int v = e ? std::atoi(e) : 256;
+    return v == 64 || v == 128 ? v : 256;
+  }();
+  // QTNH_SVD_EIG=3 (default): the two-barrier in-place pair solve (k_svd_eigen_t<16, T, true>)
+  static const int eig_v = [] {
+    const char* e = std::getenv("QTNH_SVD_EIG");
+    return e ? std::atoi(e) : 3;
+  }();
+  const bool eig3 = B == 16 && eig_v == 3;
+  const size_t eig3_smem = static_cast<size_t>(2) * P2 * (P2 + 1) * 16;
+  QTNH_CUDA(cudaFuncSetAttribute(k_svd_eigen_t<B, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig3_smem));
+  QTNH_CUDA(cudaFuncSetAttribute(k_svd_eigen_t<B, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig3_smem));
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_update_mma_t<B, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
@@ -1114,12 +1241,24 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
             k_svd_gram_mma_t<B><<<dim3(npairs, splits, cnt), B * 8, gram_smem, G.s>>>(
                 wkg, partg, static_cast<const int*>(d_tab.ptr), rd, npairs, splits, rp, L, qw);
           QTNH_LAUNCH_CHECK();
-          k_svd_eigen_t<B><<<dim3(npairs, cnt), 256, eig_smem, G.s>>>(
-              partg, whg, flg, static_cast<double*>(offm.ptr) + G.base, npairs, splits, tol, inner_sweeps(),
-              static_cast<const double*>(floor_abs.ptr) + G.base,
-              G.cross ? static_cast<double2*>(dblk.ptr) + G.base * nblk2 * B * B : nullptr,
-              static_cast<const int*>(d_tab.ptr), rd, static_cast<int>(nblk2), sort_pair ? 1 : 0,
-              static_cast<const double*>(offp.ptr) + G.base);
+          {
+            auto eig = k_svd_eigen_t<B, 256>;
+            if (B == 16 && eig_t == 64) eig = k_svd_eigen_t<B, 64>;
+            if (B == 16 && eig_t == 128) eig = k_svd_eigen_t<B, 128>;
+            int et = B == 16 ? eig_t : 256;
+            size_t esm = eig_smem;
+            if (eig3) {
+              eig = eig_t == 128 ? k_svd_eigen_t<B, 128, true> : k_svd_eigen_t<B, 256, true>;
+              et = eig_t == 128 ? 128 : 256;
+              esm = eig3_smem;
+            }
+            eig<<<dim3(npairs, cnt), et, esm, G.s>>>(
+                partg, whg, flg, static_cast<double*>(offm.ptr) + G.base, npairs, splits, tol, inner_sweeps(),
+                static_cast<const double*>(floor_abs.ptr) + G.base,
+                G.cross ? static_cast<double2*>(dblk.ptr) + G.base * nblk2 * B * B : nullptr,
+                static_cast<const int*>(d_tab.ptr), rd, static_cast<int>(nblk2), sort_pair ? 1 : 0,
+                static_cast<const double*>(offp.ptr) + G.base);
+          }
           QTNH_LAUNCH_CHECK();
           if constexpr (B == 16) {
             if (upd2) {
