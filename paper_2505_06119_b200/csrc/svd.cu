@@ -228,12 +228,16 @@ __global__ void __launch_bounds__(T) k_svd_eigen_t(const double2* __restrict__ p
           double c = 1.0, sn = 0.0;
           double2 ph = make_double2(1.0, 0.0);
           if (r2 > 1e-600 && !(r2 <= rot_thr2 * fabs(a * b))) {
+            // division-free form of t = sign(tau) / (|tau| + sqrt(tau^2 + 1)), tau = d / r:
+            // d = b - a, r = 2 |x|, den = |d| + sqrt(d^2 + r^2); c = den / sqrt(den^2 + r^2),
+            // s = sign(d) r / sqrt(den^2 + r^2) (same rotation, no cancellation)
             const double inv_ax = rsqrt(r2);
             ph = make_double2(x.x * inv_ax, -x.y * inv_ax);
-            const double tau = 0.5 * (b - a) * inv_ax;
-            const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
-            c = rsqrt(fma(t, t, 1.0));
-            sn = t * c;
+            const double rr = 2.0 * r2 * inv_ax, d = b - a;
+            const double den = fabs(d) + sqrt(fma(d, d, rr * rr));
+            const double q = rsqrt(fma(den, den, rr * rr));
+            c = den * q;
+            sn = copysign(rr * q, d);
           }
           rot_c[tid] = c;
           rot_s[tid] = sn;
