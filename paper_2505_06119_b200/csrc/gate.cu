@@ -548,7 +548,7 @@ __device__ void qft_low_tw_build(double2* tw, int L) {
 // takes a third of the FP64 work out of a pass that is FP64-issue bound.
 template <int G>
 __device__ __forceinline__ void qft_low_round(double2* __restrict__ data, const double2* __restrict__ tw, int L,
-                                              int B) {
+                                              int B, double scale = 1.0) {
   const int nf = 1 << (L - G);
   for (int f = threadIdx.x; f < nf; f += blockDim.x) {
     const int lo = f & ((1 << B) - 1), hi = f >> B;
@@ -573,6 +573,10 @@ __device__ __forceinline__ void qft_low_round(double2* __restrict__ data, const 
         double2 ph = kl ? cmul2(kQftSmallTw[(1 << u) - 1 + kl], lof[u]) : lof[u];
         x[k1] = (B + u) > 0 || kl ? cmul2(d, ph) : d;
       }
+    }
+    if (scale != 1.0) {
+#pragma unroll
+      for (int k = 0; k < (1 << G); ++k) x[k] = make_double2(x[k].x * scale, x[k].y * scale);
     }
 #pragma unroll
     for (int k = 0; k < (1 << G); ++k) data[swz8(base + (k << B))] = x[k];
@@ -716,6 +720,87 @@ __global__ void __launch_bounds__(128, QTNH_LOW4_MINB) k_qft_low4(double2* __res
     }
     __syncthreads();
   }
+}
+
+// TMA form of the low pass (default): a chunk of 2^S amplitudes is one 2-D box
+// of a FLOAT64 tensor map [2^(n-3) rows][16 doubles] with the 128-byte swizzle,
+// which puts amplitude i at shared index i ^ ((i >> 3) & 7) -- exactly the swz8
+// layout the shared-memory rounds use -- so the chunk lands by one bulk tensor
+// load (mbarrier, NB buffers, issued NB - 1 chunks ahead) and leaves by one bulk
+// tensor store straight from the rounds' output (the 1/sqrt2^L scale folded into
+// the last round). k_qft_low4 (single buffer, first round from global into
+// registers) kept its loads in flight only during its load phase: 4.8 TB/s at
+// n = 33; here every CTA always has the next chunk loading and the previous one
+// storing.
+template <int NB, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_qft_low_tma(const __grid_constant__ CUtensorMap tm, int64_t n_chunks, int S,
+                                                    int L) {
+  extern __shared__ unsigned char smq_raw[];
+  double2* bufs = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smq_raw) + 1023) & ~uintptr_t(1023));
+  const int C = 1 << S, rows = C >> 3;
+  double2* tw = bufs + NB * C;
+  __shared__ uint64_t full[NB];
+  const int tid = threadIdx.x;
+  qft_low_tw_build(tw, L);
+  const int64_t grid = gridDim.x;
+  if (tid == 0) {
+    prefetch_tmap(&tm);
+    for (int b = 0; b < NB; ++b) mbar_init(&full[b], 1);
+    fence_mbar_init();
+    for (int b = 0; b < NB - 1; ++b) {
+      const int64_t c = blockIdx.x + b * grid;
+      if (c < n_chunks) {
+        mbar_arrive_expect_tx(&full[b], static_cast<uint32_t>(C) * 16u);
+        tma_load_2d(bufs + b * C, &tm, 0, static_cast<int>(c * rows), &full[b]);
+      }
+    }
+  }
+  __syncthreads();
+  const double sc = ldexp(1.0, -(L / 2)) * (L & 1 ? 0.70710678118654752440 : 1.0);  // (1/sqrt2)^L
+  int64_t i = 0;
+  for (int64_t ch = blockIdx.x; ch < n_chunks; ch += grid, ++i) {
+    const int b = static_cast<int>(i % NB);
+    if (NB == 1 && tid == 0) {  // one buffer: it is free once the previous store has read it
+      bulk_wait_read<0>();
+      mbar_arrive_expect_tx(&full[0], static_cast<uint32_t>(C) * 16u);
+      tma_load_2d(bufs, &tm, 0, static_cast<int>(ch * rows), &full[0]);
+    }
+    mbar_wait(&full[b], static_cast<uint32_t>((i / NB) & 1));
+    double2* data = bufs + b * C;
+    int T = L - 1, off = 0;
+    bool first = true;
+    while (T >= 0) {
+      const int gg = qft_low_g(T), B = T - gg + 1;
+      const double s_here = B == 0 ? sc : 1.0;  // the last round writes the scaled output
+      switch (gg) {
+        case 4: qft_low_round<4>(data, tw + off, S, B, s_here); break;
+        case 3: qft_low_round<3>(data, tw + off, S, B, s_here); break;
+        case 2: qft_low_round<2>(data, tw + off, S, B, s_here); break;
+        default: qft_low_round<1>(data, tw + off, S, B, s_here); break;
+      }
+      off += gg << B;
+      T = B - 1;
+      if (NB > 1 && first && tid == 0) {
+        // next load into the buffer of chunk i - 1, whose store has had a round to read it
+        const int64_t nc = ch + (NB - 1) * grid;
+        if (nc < n_chunks) {
+          const int nbuf = static_cast<int>((i + NB - 1) % NB);
+          bulk_wait_read<0>();
+          mbar_arrive_expect_tx(&full[nbuf], static_cast<uint32_t>(C) * 16u);
+          tma_load_2d(bufs + nbuf * C, &tm, 0, static_cast<int>(nc * rows), &full[nbuf]);
+        }
+      }
+      first = false;
+      __syncthreads();
+    }
+    fence_proxy_async_smem();  // this thread's round writes, visible to the bulk store
+    __syncthreads();
+    if (tid == 0) {
+      tma_store_2d(&tm, 0, static_cast<int>(ch * rows), data);
+      bulk_commit();
+    }
+  }
+  if (tid == 0) bulk_wait_read<0>();
 }
 
 struct QftGroupArgs {
@@ -1308,11 +1393,30 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
     QTNH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qft_low3, 128, smem));
     int grid = static_cast<int>(std::min<int64_t>(n_chunks, (int64_t)sms * std::max(1, occ)));
-    static const bool v4 = [] {  // default; QTNH_QFT_LOW=3 selects the double-buffered staging form
+    static const int low_v = [] {  // QTNH_QFT_LOW: tma (default), 4 (registers-first form), 3 (cp.async staging)
       const char* e = std::getenv("QTNH_QFT_LOW");
-      return !(e && e[0] == '3');
+      return e ? (e[0] == '3' ? 3 : e[0] == '4' ? 4 : 5) : 5;
     }();
-    if (v4) {
+    const bool v4 = low_v == 4;
+    if (low_v == 5 && S >= 6 && (int64_t(1) << (nb - 3)) <= (int64_t(1) << 31)) {
+      static const int nbuf = [] {
+        const char* e = std::getenv("QTNH_QFT_LOW_NB");
+        const int v = e ? std::atoi(e) : 2;
+        return v == 1 || v == 3 ? v : 2;
+      }();
+      CUtensorMap tm;
+      const uint64_t dims[2] = {16, uint64_t(1) << (nb - 3)};
+      const uint64_t strides[1] = {128};
+      const uint32_t box[2] = {16, static_cast<uint32_t>(1u << (S - 3))};
+      make_tensor_map_f64(&tm, p, 2, dims, strides, box, true);
+      const size_t smt = ((static_cast<size_t>(nbuf) << S) + n_tw) * sizeof(double2) + 1024;
+      auto kern = nbuf == 3 ? k_qft_low_tma<3, 2> : nbuf == 1 ? k_qft_low_tma<1, 4> : k_qft_low_tma<2, 3>;
+      QTNH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt)));
+      int occt = 0;
+      QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occt, kern, 128, smt));
+      const int gridt = static_cast<int>(std::min<int64_t>(n_chunks, (int64_t)sms * std::max(1, occt)));
+      kern<<<gridt, 128, smt, st>>>(tm, n_chunks, S, Lc);
+    } else if (v4 || low_v == 5) {
       const size_t smem4 = ((size_t(1) << S) + n_tw) * sizeof(double2);
       static bool attr4 = [] {
         cudaFuncSetAttribute(k_qft_low4, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16 << kQftLowMax);
