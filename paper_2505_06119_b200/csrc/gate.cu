@@ -1379,7 +1379,11 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
   if (top >= 0) {
     // remaining layers: bits top..0 with top = L - 1 (all of the low chunk)
     int Lc = top + 1;
-    const int S = std::max(Lc, std::min(nb, kQftLowMax));
+    static const int s_cap = [] {  // QTNH_QFT_LOW_S: largest low-pass chunk (bits), default 11
+      const char* e = std::getenv("QTNH_QFT_LOW_S");
+      return e ? std::max(6, std::min(kQftLowMax, std::atoi(e))) : kQftLowMax;
+    }();
+    const int S = std::max(Lc, std::min(nb, s_cap));
     const int64_t n_chunks = int64_t(1) << (nb - S);
     const size_t n_tw = static_cast<size_t>(qft_low_tw_count(Lc));
     size_t smem = ((static_cast<size_t>(2) << S) + n_tw) * sizeof(double2);  // 2 buffers + twiddles
@@ -1410,7 +1414,14 @@ void qft_local_fused(void* data, int nb, int first_layer_bit, cudaStream_t st) {
       const uint32_t box[2] = {16, static_cast<uint32_t>(1u << (S - 3))};
       make_tensor_map_f64(&tm, p, 2, dims, strides, box, true);
       const size_t smt = ((static_cast<size_t>(nbuf) << S) + n_tw) * sizeof(double2) + 1024;
+      static const int minb = [] {  // CTAs per SM the register budget is cut for (3, 4 or 5)
+        const char* e = std::getenv("QTNH_QFT_LOW_MINB");
+        const int v = e ? std::atoi(e) : 3;
+        return v == 4 || v == 5 ? v : 3;
+      }();
       auto kern = nbuf == 3 ? k_qft_low_tma<3, 2> : nbuf == 1 ? k_qft_low_tma<1, 4> : k_qft_low_tma<2, 3>;
+      if (nbuf == 2 && minb == 4) kern = k_qft_low_tma<2, 4>;
+      if (nbuf == 2 && minb == 5) kern = k_qft_low_tma<2, 5>;
       QTNH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt)));
       int occt = 0;
       QTNH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occt, kern, 128, smt));

@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(T) k_svd_eigen_t(const double2* __restrict__ p
                                                      const double* __restrict__ floor_abs,
                                                      double2* __restrict__ dblk, const int* __restrict__ tab,
                                                      int round, int nblk2, int sort_pair,
-                                                     const double* __restrict__ rot_thr) {
+                                                     const double* __restrict__ rot_thr, int herm = 0) {
   constexpr int P2 = 2 * B, LD = P2 + 1;
   const int pair = blockIdx.x, mat = blockIdx.y, tid = threadIdx.x;
   const double fl = floor_abs[mat];
@@ -217,6 +217,18 @@ __global__ void __launch_bounds__(T) k_svd_eigen_t(const double2* __restrict__ p
       pq_s[step][rr][0] = static_cast<unsigned char>(p < q ? p : q);
       pq_s[step][rr][1] = static_cast<unsigned char>(p < q ? q : p);
     }
+    // herm: G is Hermitian, so only the 2 x 2 blocks (k, l) with k <= l are
+    // computed; block (l, k) is written as their conjugate transpose.
+    __shared__ unsigned char kl_s[B * (B + 1) / 2][2];
+    for (int e = tid; e < B * B; e += T) {
+      const int k = e / B, l = e % B;
+      if (k <= l) {
+        const int idx = k * B - k * (k - 1) / 2 + (l - k);
+        kl_s[idx][0] = static_cast<unsigned char>(k);
+        kl_s[idx][1] = static_cast<unsigned char>(l);
+      }
+    }
+    const int ntask = herm ? B * (B + 1) / 2 : B * B;
     __syncthreads();
     for (int sw = 0; sw < inner_sweeps; ++sw) {
       for (int step = 0; step < P2 - 1; ++step) {
@@ -245,8 +257,8 @@ __global__ void __launch_bounds__(T) k_svd_eigen_t(const double2* __restrict__ p
         }
         __syncthreads();
 #pragma unroll
-        for (int task = tid; task < B * B; task += T) {  // 2 x 2 block (pk, qk) x (pl, ql), in place
-          const int k = task / B, l = task % B;
+        for (int task = tid; task < ntask; task += T) {  // 2 x 2 block (pk, qk) x (pl, ql), in place
+          const int k = herm ? kl_s[task][0] : task / B, l = herm ? kl_s[task][1] : task % B;
           const int pk = pq_s[step][k][0], qk = pq_s[step][k][1], pl = pq_s[step][l][0], ql = pq_s[step][l][1];
           const double ck = rot_c[k], sk = rot_s[k], cl = rot_c[l], sl = rot_s[l];
           const double2 ek = cconj(rot_ph[k]), el = rot_ph[l];
@@ -257,10 +269,20 @@ __global__ void __launch_bounds__(T) k_svd_eigen_t(const double2* __restrict__ p
           double2 c1 = make_double2(cl * cc.x - sl * dq.x, cl * cc.y - sl * dq.y);
           double2 d1 = make_double2(sl * cc.x + cl * dq.x, sl * cc.y + cl * dq.y);
           double2 c2 = cmul(c1, ek), d2 = cmul(d1, ek);
-          G[pk * LD + pl] = make_double2(ck * a1.x - sk * c2.x, ck * a1.y - sk * c2.y);
-          G[pk * LD + ql] = make_double2(ck * b1.x - sk * d2.x, ck * b1.y - sk * d2.y);
-          G[qk * LD + pl] = make_double2(sk * a1.x + ck * c2.x, sk * a1.y + ck * c2.y);
-          G[qk * LD + ql] = make_double2(sk * b1.x + ck * d2.x, sk * b1.y + ck * d2.y);
+          const double2 na = make_double2(ck * a1.x - sk * c2.x, ck * a1.y - sk * c2.y);
+          const double2 nb = make_double2(ck * b1.x - sk * d2.x, ck * b1.y - sk * d2.y);
+          const double2 nc = make_double2(sk * a1.x + ck * c2.x, sk * a1.y + ck * c2.y);
+          const double2 nd = make_double2(sk * b1.x + ck * d2.x, sk * b1.y + ck * d2.y);
+          G[pk * LD + pl] = na;
+          G[pk * LD + ql] = nb;
+          G[qk * LD + pl] = nc;
+          G[qk * LD + ql] = nd;
+          if (herm && k != l) {
+            G[pl * LD + pk] = cconj(na);
+            G[ql * LD + pk] = cconj(nb);
+            G[pl * LD + qk] = cconj(nc);
+            G[ql * LD + qk] = cconj(nd);
+          }
         }
 #pragma unroll
         for (int task = tid; task < P2 * B; task += T) {  // V columns p, q of rotation kk, in place
@@ -1107,7 +1129,8 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
     const char* e = std::getenv("QTNH_SVD_EIG");
     return e ? std::atoi(e) : 3;
   }();
-  const bool eig3 = B == 16 && eig_v == 3;
+  const bool eig3 = B == 16 && eig_v >= 3;
+  const bool eig_herm = eig_v == 4;  // QTNH_SVD_EIG=4: the in-place form on the upper block triangle
   const size_t eig3_smem = static_cast<size_t>(2) * P2 * (P2 + 1) * 16;
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_eigen_t<B, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig3_smem));
   QTNH_CUDA(cudaFuncSetAttribute(k_svd_eigen_t<B, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig3_smem));
@@ -1261,7 +1284,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
                 static_cast<const double*>(floor_abs.ptr) + G.base,
                 G.cross ? static_cast<double2*>(dblk.ptr) + G.base * nblk2 * B * B : nullptr,
                 static_cast<const int*>(d_tab.ptr), rd, static_cast<int>(nblk2), sort_pair ? 1 : 0,
-                static_cast<const double*>(offp.ptr) + G.base);
+                static_cast<const double*>(offp.ptr) + G.base, eig3 && eig_herm ? 1 : 0);
           }
           QTNH_LAUNCH_CHECK();
           if constexpr (B == 16) {
