@@ -863,32 +863,13 @@ __global__ void __launch_bounds__(256, (G >= 4 ? 1 : 2)) k_qft_group(double2* __
 constexpr int kMidW = 16;
 __constant__ double2 kQftMidTw[256];  // e^{i pi x / 2^u} at index 2^u - 1 + x, u < 8
 
+// The two register rounds of a shared-memory group pass over one staged tile
+// data[NG][kMidW] (phases: kQftMidTw table x the per-column lofs[GB][kMidW]).
 template <int G1, int G2>
-__global__ void __launch_bounds__(256, 2) k_qft_mid(double2* __restrict__ psi, int64_t n_tiles, int B) {
-  constexpr int GB = G1 + G2, NG = 1 << GB, NE = NG * kMidW;
-  static_assert((1 << G1) * kMidW == 256 || (1 << G2) * kMidW <= 256, "fibers per round fit the block");
-  extern __shared__ double2 smid[];
-  double2* data = smid;              // [NG][kMidW]
-  double2* lofs = smid + NE;         // [GB][kMidW]
+__device__ __forceinline__ void qft_mid_rounds(double2* __restrict__ data, const double2* __restrict__ lofs) {
+  constexpr int GB = G1 + G2;
   const int tid = threadIdx.x;
   const double r = 0.70710678118654752440;
-  const int64_t lo_blocks = (int64_t(1) << B) / kMidW;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int64_t hi = tile / lo_blocks, lo0 = (tile % lo_blocks) * kMidW;
-    double2* g0 = psi + (hi << (B + GB)) + lo0;
-    for (int e = tid; e < NE; e += 256) {
-      const int g = e / kMidW, w = e % kMidW;
-      cp_async16(data + e, g0 + (int64_t(g) << B) + w);
-    }
-    cp_async_commit();
-    for (int e = tid; e < GB * kMidW; e += 256) {
-      const int u = e / kMidW, w = e % kMidW;
-      double sn, cs;
-      sincospi(static_cast<double>(lo0 + w) * ldexp(1.0, -(B + u)), &sn, &cs);
-      lofs[e] = make_double2(cs, sn);
-    }
-    asm volatile("cp.async.wait_group 0;\n" ::);
-    __syncthreads();
     // round 1: upper G1 group bits (layers u = GB-1 .. G2), lower G2 bits fixed
     for (int f = tid; f < (1 << G2) * kMidW; f += 256) {
       const int w = f % kMidW, j = f / kMidW;
@@ -913,7 +894,7 @@ __global__ void __launch_bounds__(256, 2) k_qft_mid(double2* __restrict__ psi, i
 #pragma unroll
       for (int k = 0; k < (1 << G1); ++k) data[((k << G2) | j) * kMidW + w] = x[k];
     }
-    __syncthreads();
+  __syncthreads();
     // round 2: lower G2 group bits (layers u = G2-1 .. 0), upper G1 bits fixed
     for (int f = tid; f < (1 << G1) * kMidW; f += 256) {
       const int w = f % kMidW, i = f / kMidW;
@@ -937,6 +918,34 @@ __global__ void __launch_bounds__(256, 2) k_qft_mid(double2* __restrict__ psi, i
 #pragma unroll
       for (int k = 0; k < (1 << G2); ++k) data[((i << G2) | k) * kMidW + w] = x[k];
     }
+}
+
+template <int G1, int G2>
+__global__ void __launch_bounds__(256, 2) k_qft_mid(double2* __restrict__ psi, int64_t n_tiles, int B) {
+  constexpr int GB = G1 + G2, NG = 1 << GB, NE = NG * kMidW;
+  static_assert((1 << G1) * kMidW == 256 || (1 << G2) * kMidW <= 256, "fibers per round fit the block");
+  extern __shared__ double2 smid[];
+  double2* data = smid;              // [NG][kMidW]
+  double2* lofs = smid + NE;         // [GB][kMidW]
+  const int tid = threadIdx.x;
+  const int64_t lo_blocks = (int64_t(1) << B) / kMidW;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t hi = tile / lo_blocks, lo0 = (tile % lo_blocks) * kMidW;
+    double2* g0 = psi + (hi << (B + GB)) + lo0;
+    for (int e = tid; e < NE; e += 256) {
+      const int g = e / kMidW, w = e % kMidW;
+      cp_async16(data + e, g0 + (int64_t(g) << B) + w);
+    }
+    cp_async_commit();
+    for (int e = tid; e < GB * kMidW; e += 256) {
+      const int u = e / kMidW, w = e % kMidW;
+      double sn, cs;
+      sincospi(static_cast<double>(lo0 + w) * ldexp(1.0, -(B + u)), &sn, &cs);
+      lofs[e] = make_double2(cs, sn);
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    qft_mid_rounds<G1, G2>(data, lofs);
     __syncthreads();
     for (int e = tid; e < NE; e += 256) {
       const int g = e / kMidW, w = e % kMidW;
@@ -945,6 +954,7 @@ __global__ void __launch_bounds__(256, 2) k_qft_mid(double2* __restrict__ psi, i
     __syncthreads();  // the tile buffer is reused by the next tile
   }
 }
+
 
 __device__ __forceinline__ unsigned rev_bits(unsigned x, int bits) { return __brev(x) >> (32 - bits); }
 __device__ __forceinline__ uint64_t rev_bits64(uint64_t x, int bits) { return __brevll(x) >> (64 - bits); }
@@ -1028,6 +1038,92 @@ __global__ void __launch_bounds__(512) k_bitrev_tma(const __grid_constant__ CUte
       phase ^= 1;
     }
   }
+}
+
+// Bit reversal with TMA both ways (QTNH_BITREV_TMA=2): tile pairs stream
+// through NB 32 KB stages (4 swizzled 32 x 8 boxes per tile, loaded D = NB - 2
+// pairs ahead); each thread reads its 4 + 4 bit-reversed source elements into
+// registers, the CTA overwrites the stage in place with the output tiles in the
+// same swizzled layout, and one thread stores them with 8 bulk tensor stores.
+template <int NB>
+__global__ void __launch_bounds__(256) k_bitrev_tma2(const __grid_constant__ CUtensorMap tm, int n, int64_t n_mid) {
+  static_assert(NB >= 3, "a stage loading, one exchanging, one storing");
+  constexpr int D = NB - 2;
+  extern __shared__ unsigned char smem_raw[];
+  double2* stages = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[NB];
+  const int mbits = n - 10, tid = threadIdx.x, lane = tid & 31, a0 = tid >> 5;
+  auto rev_m = [&](int64_t m) {
+    return mbits > 0 ? static_cast<int64_t>(rev_bits64(static_cast<uint64_t>(m), mbits)) : m;
+  };
+  auto next_valid = [&](int64_t m) {
+    while (m < n_mid && rev_m(m) < m) m += gridDim.x;
+    return m;
+  };
+  auto load = [&](int stage, int64_t m) {
+    const int64_t mr = rev_m(m);
+    double2* t1 = stages + stage * 2048;
+    mbar_arrive_expect_tx(&full[stage], mr != m ? 32768u : 16384u);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      tma_load_3d(t1 + c * 256, &tm, c * 16, static_cast<int>(m), 0, &full[stage]);
+      if (mr != m) tma_load_3d(t1 + 1024 + c * 256, &tm, c * 16, static_cast<int>(mr), 0, &full[stage]);
+    }
+  };
+  int64_t m_issue = 0;
+  if (tid == 0) {
+    prefetch_tmap(&tm);
+    for (int s = 0; s < NB; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    m_issue = next_valid(blockIdx.x);
+    for (int s = 0; s < D && m_issue < n_mid; ++s) {
+      load(s, m_issue);
+      m_issue = next_valid(m_issue + gridDim.x);
+    }
+  }
+  __syncthreads();
+  const int rb = rev_bits(lane, 5);
+  int64_t i = 0;
+  for (int64_t m = next_valid(blockIdx.x); m < n_mid; m = next_valid(m + gridDim.x), ++i) {
+    const int stage = static_cast<int>(i % NB);
+    if (tid == 0 && m_issue < n_mid) {
+      bulk_wait_read<1>();  // the stores of pair i - 2 have read their stage
+      load(static_cast<int>((i + D) % NB), m_issue);
+      m_issue = next_valid(m_issue + gridDim.x);
+    }
+    mbar_wait(&full[stage], static_cast<uint32_t>((i / NB) & 1));
+    const int64_t mr = rev_m(m);
+    double2* t1 = stages + stage * 2048;
+    double2* t2 = mr != m ? t1 + 1024 : t1;
+    double2 v1[4], v2[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int a = a0 + 8 * j, ra = rev_bits(a, 5);
+      // source (row rb, amplitude ra); new (a, m, b) = old (rev b, rev m, rev a)
+      const int src = (ra >> 3) * 256 + rb * 8 + ((ra & 7) ^ (rb & 7));
+      v1[j] = canon2(t2[src]);  // -> tile m
+      v2[j] = canon2(t1[src]);  // -> tile mr
+    }
+    __syncthreads();  // every source element is in registers
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int a = a0 + 8 * j;
+      const int dst = (lane >> 3) * 256 + a * 8 + ((lane & 7) ^ (a & 7));
+      t1[dst] = v1[j];
+      if (mr != m) t2[dst] = v2[j];
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        tma_store_3d(&tm, c * 16, static_cast<int>(m), 0, t1 + c * 256);
+        if (mr != m) tma_store_3d(&tm, c * 16, static_cast<int>(mr), 0, t2 + c * 256);
+      }
+      bulk_commit();
+    }
+  }
+  if (tid == 0) bulk_wait_read<0>();
 }
 
 // n >= 10: x = (a: top 5 bits, m: middle n-10 bits, b: low 5 bits).
@@ -1458,6 +1554,25 @@ void bitrev_local(void* data, int nb, cudaStream_t st) {
   // load issue, so deeper TMA pipelines only add outstanding scattered requests.
   const char* tma_env = std::getenv("QTNH_BITREV_TMA");
   const bool use_tma = tma_env && tma_env[0] == '1';
+  if (tma_env && tma_env[0] == '2' && n_mid <= (int64_t(1) << 31)) {
+    static const int cfg2[2] = {[] { const char* e = std::getenv("QTNH_BITREV_NB"); return e ? std::atoi(e) : 3; }(),
+                                [] { const char* e = std::getenv("QTNH_BITREV_CTAS"); return e ? std::atoi(e) : 2; }()};
+    CUtensorMap tm;
+    const uint64_t dims[3] = {64, static_cast<uint64_t>(n_mid), 32};
+    const uint64_t strides[2] = {512, static_cast<uint64_t>(16) << (nb - 5)};
+    const uint32_t box[3] = {16, 1, 32};
+    make_tensor_map_f64(&tm, data, 3, dims, strides, box, true);
+    const int grid = static_cast<int>(std::min<int64_t>(n_mid, static_cast<int64_t>(sms) * std::max(1, cfg2[1])));
+    auto launch = [&](auto kern, int S) {
+      const size_t smem = static_cast<size_t>(S) * 2048 * sizeof(double2) + 1024;
+      QTNH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      kern<<<grid, 256, smem, st>>>(tm, nb, n_mid);
+    };
+    if (cfg2[0] >= 4) launch(k_bitrev_tma2<4>, 4);
+    else launch(k_bitrev_tma2<3>, 3);
+    QTNH_LAUNCH_CHECK();
+    return;
+  }
   if (use_tma && n_mid <= (int64_t(1) << 31)) {
     // QTNH_BITREV_CFG = "stages,threads,ctas_per_sm" (stages 2, 3, 4 or 6)
     static int cfg[3] = {2, 256, 3};
