@@ -1040,92 +1040,6 @@ __global__ void __launch_bounds__(512) k_bitrev_tma(const __grid_constant__ CUte
   }
 }
 
-// Bit reversal with TMA both ways (QTNH_BITREV_TMA=2): tile pairs stream
-// through NB 32 KB stages (4 swizzled 32 x 8 boxes per tile, loaded D = NB - 2
-// pairs ahead); each thread reads its 4 + 4 bit-reversed source elements into
-// registers, the CTA overwrites the stage in place with the output tiles in the
-// same swizzled layout, and one thread stores them with 8 bulk tensor stores.
-template <int NB>
-__global__ void __launch_bounds__(256) k_bitrev_tma2(const __grid_constant__ CUtensorMap tm, int n, int64_t n_mid) {
-  static_assert(NB >= 3, "a stage loading, one exchanging, one storing");
-  constexpr int D = NB - 2;
-  extern __shared__ unsigned char smem_raw[];
-  double2* stages = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[NB];
-  const int mbits = n - 10, tid = threadIdx.x, lane = tid & 31, a0 = tid >> 5;
-  auto rev_m = [&](int64_t m) {
-    return mbits > 0 ? static_cast<int64_t>(rev_bits64(static_cast<uint64_t>(m), mbits)) : m;
-  };
-  auto next_valid = [&](int64_t m) {
-    while (m < n_mid && rev_m(m) < m) m += gridDim.x;
-    return m;
-  };
-  auto load = [&](int stage, int64_t m) {
-    const int64_t mr = rev_m(m);
-    double2* t1 = stages + stage * 2048;
-    mbar_arrive_expect_tx(&full[stage], mr != m ? 32768u : 16384u);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      tma_load_3d(t1 + c * 256, &tm, c * 16, static_cast<int>(m), 0, &full[stage]);
-      if (mr != m) tma_load_3d(t1 + 1024 + c * 256, &tm, c * 16, static_cast<int>(mr), 0, &full[stage]);
-    }
-  };
-  int64_t m_issue = 0;
-  if (tid == 0) {
-    prefetch_tmap(&tm);
-    for (int s = 0; s < NB; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-    m_issue = next_valid(blockIdx.x);
-    for (int s = 0; s < D && m_issue < n_mid; ++s) {
-      load(s, m_issue);
-      m_issue = next_valid(m_issue + gridDim.x);
-    }
-  }
-  __syncthreads();
-  const int rb = rev_bits(lane, 5);
-  int64_t i = 0;
-  for (int64_t m = next_valid(blockIdx.x); m < n_mid; m = next_valid(m + gridDim.x), ++i) {
-    const int stage = static_cast<int>(i % NB);
-    if (tid == 0 && m_issue < n_mid) {
-      bulk_wait_read<1>();  // the stores of pair i - 2 have read their stage
-      load(static_cast<int>((i + D) % NB), m_issue);
-      m_issue = next_valid(m_issue + gridDim.x);
-    }
-    mbar_wait(&full[stage], static_cast<uint32_t>((i / NB) & 1));
-    const int64_t mr = rev_m(m);
-    double2* t1 = stages + stage * 2048;
-    double2* t2 = mr != m ? t1 + 1024 : t1;
-    double2 v1[4], v2[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int a = a0 + 8 * j, ra = rev_bits(a, 5);
-      // source (row rb, amplitude ra); new (a, m, b) = old (rev b, rev m, rev a)
-      const int src = (ra >> 3) * 256 + rb * 8 + ((ra & 7) ^ (rb & 7));
-      v1[j] = canon2(t2[src]);  // -> tile m
-      v2[j] = canon2(t1[src]);  // -> tile mr
-    }
-    __syncthreads();  // every source element is in registers
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int a = a0 + 8 * j;
-      const int dst = (lane >> 3) * 256 + a * 8 + ((lane & 7) ^ (a & 7));
-      t1[dst] = v1[j];
-      if (mr != m) t2[dst] = v2[j];
-    }
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        tma_store_3d(&tm, c * 16, static_cast<int>(m), 0, t1 + c * 256);
-        if (mr != m) tma_store_3d(&tm, c * 16, static_cast<int>(mr), 0, t2 + c * 256);
-      }
-      bulk_commit();
-    }
-  }
-  if (tid == 0) bulk_wait_read<0>();
-}
-
 // n >= 10: x = (a: top 5 bits, m: middle n-10 bits, b: low 5 bits).
 
 // In-place bit reversal: the two 32 x 32 tiles of a pair are
@@ -1552,27 +1466,10 @@ void bitrev_local(void* data, int nb, cudaStream_t st) {
   // stages, 256 threads, 3 CTAs/SM) and 7.9 ms with 6 stages at 1 CTA/SM -- the
   // pass is bound by the DRAM traffic pattern (64 pages per tile pair), not by
   // load issue, so deeper TMA pipelines only add outstanding scattered requests.
+  // TMA stores as well (tile pairs exchanged in place in the stage, 8 bulk tensor
+  // stores per pair) measured 71-81 ms against 50.6 ms at n = 33: dropped.
   const char* tma_env = std::getenv("QTNH_BITREV_TMA");
   const bool use_tma = tma_env && tma_env[0] == '1';
-  if (tma_env && tma_env[0] == '2' && n_mid <= (int64_t(1) << 31)) {
-    static const int cfg2[2] = {[] { const char* e = std::getenv("QTNH_BITREV_NB"); return e ? std::atoi(e) : 3; }(),
-                                [] { const char* e = std::getenv("QTNH_BITREV_CTAS"); return e ? std::atoi(e) : 2; }()};
-    CUtensorMap tm;
-    const uint64_t dims[3] = {64, static_cast<uint64_t>(n_mid), 32};
-    const uint64_t strides[2] = {512, static_cast<uint64_t>(16) << (nb - 5)};
-    const uint32_t box[3] = {16, 1, 32};
-    make_tensor_map_f64(&tm, data, 3, dims, strides, box, true);
-    const int grid = static_cast<int>(std::min<int64_t>(n_mid, static_cast<int64_t>(sms) * std::max(1, cfg2[1])));
-    auto launch = [&](auto kern, int S) {
-      const size_t smem = static_cast<size_t>(S) * 2048 * sizeof(double2) + 1024;
-      QTNH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      kern<<<grid, 256, smem, st>>>(tm, nb, n_mid);
-    };
-    if (cfg2[0] >= 4) launch(k_bitrev_tma2<4>, 4);
-    else launch(k_bitrev_tma2<3>, 3);
-    QTNH_LAUNCH_CHECK();
-    return;
-  }
   if (use_tma && n_mid <= (int64_t(1) << 31)) {
     // QTNH_BITREV_CFG = "stages,threads,ctas_per_sm" (stages 2, 3, 4 or 6)
     static int cfg[3] = {2, 256, 3};
