@@ -296,7 +296,10 @@ enum { QTNH_ABSORB_NONE = 0, QTNH_ABSORB_LEFT = 1, QTNH_ABSORB_RIGHT = 2, QTNH_A
  * (linalg.hpp:476-505), singular values absorbed per `absorb` (linalg.hpp:508-523).
  * Outputs (device, row-major): u [batch][m][chi], s [batch][chi] (doubles,
  * descending), vh [batch][chi][n]. chi <= 0 means min(m, n). Runs on the rank's
- * stream. NumericalError if Jacobi sweeps fail to converge. */
+ * stream. NumericalError if Jacobi sweeps fail to converge. Like zgesdd's, the
+ * non-absorbed factors are isometries whatever the rank of a: null directions
+ * (sigma <= max(m, n) eps sigma_0) get an orthonormal completion; columns past
+ * min(m, n) stay zero (truncate_svd's padding). */
 int qtnh_svd_device(qtnh_rank_t r, int64_t batch, int64_t m, int64_t n, const void* a,
                     int64_t chi, int absorb, void* u, void* s, void* vh);
 
@@ -327,7 +330,8 @@ int qtnh_remap_plan_json(int n_idx, const int64_t* dims, int split, const int64_
  * A t with distributed indices is first gathered onto its root copy (linalg::psvd
  * gathers to the group root, linalg.hpp:441-462): u and vh live there, and S is
  * sent back to every rank of t's span (:464). qtnh_last_error_info() afterwards
- * = Jacobi sweeps (on the ranks that ran the SVD). */
+ * = Jacobi sweeps (on the ranks that ran the SVD). Null directions are completed
+ * to orthonormal vectors as in qtnh_svd_device. */
 int qtnh_svd(qtnh_tensor_t t, int n_row, const int* row_pos, int n_col, const int* col_pos, int64_t chi,
              int absorb, qtnh_tensor_t* u, qtnh_tensor_t* vh, double* s_host);
 
