@@ -26,6 +26,14 @@ def main(shapes):
             for batch, n, chi in shapes:
                 rng = np.random.default_rng(0)
                 a = torch.from_numpy(rng.standard_normal((batch, n, n)) + 1j * rng.standard_normal((batch, n, n))).cuda()
+                if os.environ.get("BENCH_SVD_SPECTRUM") == "two":
+                    # config 4's early saturated thetas: two singular values, chi-fold each
+                    # (input generation only: torch QR of the random matrices)
+                    q1 = torch.linalg.qr(a)[0]
+                    q2 = torch.linalg.qr(a.transpose(1, 2).conj().contiguous())[0]
+                    sv = torch.tensor([0.70719] * chi + [0.35957] * (n - chi), dtype=torch.float64, device="cuda")
+                    a = (q1 * sv) @ q2.transpose(1, 2).conj()
+                    a = a.contiguous()
                 u = torch.empty((batch, n, chi), dtype=torch.complex128, device="cuda")
                 s = torch.empty((batch, chi), dtype=torch.float64, device="cuda")
                 vh = torch.empty((batch, chi, n), dtype=torch.complex128, device="cuda")
