@@ -128,6 +128,341 @@ int grid_elems(Dim n) { return static_cast<int>(std::min<Dim>((n + 255) / 256, 1
 
 std::atomic<int64_t> g_split_count{0};
 
+// ---- orthonormal basis of range(P) by block-greedy pivoted Cholesky -----------------
+// P (m x m) is the certified spectral projector (P^2 = P, rank chi). For a
+// projector <P e_p, P e_q> = P_pq, so Gram-Schmidt of greedily pivoted columns of
+// P is a pivoted Cholesky P = L L^H whose chi columns are orthonormal. Blocks of
+// up to kPcBs columns: the kPcCand unselected indices of largest residual
+// d_i = P_ii - sum_j |L_ij|^2 are the candidates; their residual columns
+// R = P[:, cand] - L L[cand, :]^H come from one GEMM; a pivoted Cholesky of the
+// candidates' residual Gram R[cand, :] = Rc^H Rc (one CTA) picks the block, and
+// L_new = R[:, sel] Rc^-1. Replaces the ~15-sweep Jacobi SVD of the chi x m
+// matrix Y^H = (P Omega)^H that the split path used for this basis.
+// Batched: matrix index = blockIdx.y (blockIdx.x for the one-CTA kernels);
+// per-matrix arrays at fixed strides: R, T [m][kPcCand], L [m][chi], M
+// [chi][kPcCand], d [m].
+constexpr int kPcCand = 64, kPcBs = 32;
+constexpr double kPcAccept = 1e-6;  // residual norms^2 below this: rank exhausted
+
+struct PcState {  // per matrix, device
+  int nsel, k, ncand, pad;
+  int cand[kPcCand];
+  int sel[kPcBs];
+  double2 rc[kPcBs * kPcBs];  // upper triangular, selection order
+};
+
+__global__ void k_pc_diag(const double2* const* __restrict__ P, double* __restrict__ d_all, int m) {
+  const double2* Pm = P[blockIdx.y];
+  double* d = d_all + static_cast<int64_t>(blockIdx.y) * m;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    d[i] = Pm[static_cast<int64_t>(i) * m + i].x;
+}
+
+// the kPcCand unselected indices of largest residual (bitonic sort in shared memory)
+__global__ void __launch_bounds__(1024) k_pc_candidates(const double* __restrict__ d_all, PcState* __restrict__ st_all,
+                                                         int m, int np2, int chi) {
+  extern __shared__ double pcs[];
+  const int mat = blockIdx.x;
+  const double* d = d_all + static_cast<int64_t>(mat) * m;
+  PcState* S = st_all + mat;
+  double* key = pcs;
+  int* idx = reinterpret_cast<int*>(pcs + np2);
+  for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+    key[i] = i < m ? d[i] : -2.0;
+    idx[i] = i;
+  }
+  __syncthreads();
+  for (int size = 2; size <= np2; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool desc = (i & size) == 0;
+          const double ki = key[i], kj = key[j];
+          const bool swap = desc ? (ki < kj || (ki == kj && idx[i] > idx[j])) : (ki > kj || (ki == kj && idx[i] < idx[j]));
+          if (swap) {
+            key[i] = kj;
+            key[j] = ki;
+            const int ti = idx[i];
+            idx[i] = idx[j];
+            idx[j] = ti;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  if (threadIdx.x == 0) {
+    int c = 0;
+    if (S->nsel < chi)
+      for (; c < kPcCand && key[c] > kPcAccept; ++c) S->cand[c] = idx[c];
+    S->ncand = c;
+  }
+}
+
+// M (chi x kPcCand) = conj(L[cand, :])^T (zero past nsel and for missing candidates)
+__global__ void k_pc_gather_m(const double2* __restrict__ L_all, const PcState* __restrict__ st_all,
+                              double2* __restrict__ M_all, int m, int chi) {
+  const int mat = blockIdx.y;
+  const PcState* S = st_all + mat;
+  const double2* L = L_all + static_cast<int64_t>(mat) * m * chi;
+  double2* M = M_all + static_cast<int64_t>(mat) * chi * kPcCand;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < chi * kPcCand; e += gridDim.x * blockDim.x) {
+    const int j = e / kPcCand, t = e % kPcCand;
+    double2 v = make_double2(0.0, 0.0);
+    if (t < S->ncand && j < S->nsel) {
+      const double2 l = L[static_cast<int64_t>(S->cand[t]) * chi + j];
+      v = make_double2(l.x, -l.y);
+    }
+    M[e] = v;
+  }
+}
+
+// R = P[:, cand] - T   (T = L M, zero while nsel = 0)
+__global__ void k_pc_residual(const double2* const* __restrict__ P, const double2* __restrict__ T_all,
+                              const PcState* __restrict__ st_all, double2* __restrict__ R_all, int m) {
+  const int mat = blockIdx.y;
+  const PcState* S = st_all + mat;
+  const double2* Pm = P[mat];
+  const double2* T = T_all + static_cast<int64_t>(mat) * m * kPcCand;
+  double2* R = R_all + static_cast<int64_t>(mat) * m * kPcCand;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < static_cast<int64_t>(m) * kPcCand;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = static_cast<int>(e / kPcCand), t = static_cast<int>(e % kPcCand);
+    double2 v = make_double2(0.0, 0.0);
+    if (t < S->ncand) {
+      const double2 p = Pm[static_cast<int64_t>(i) * m + S->cand[t]];
+      const double2 q = S->nsel > 0 ? T[e] : make_double2(0.0, 0.0);
+      v = make_double2(p.x - q.x, p.y - q.y);
+    }
+    R[e] = v;
+  }
+}
+
+// pivoted Cholesky of the candidates' residual Gram G = R[cand, :]:
+// G[sel, sel] = Rc^H Rc, Rc upper triangular in selection order
+constexpr size_t kPcCholSmem = (static_cast<size_t>(kPcCand) * (kPcCand + 1) + static_cast<size_t>(kPcBs) * kPcCand) * 16;
+__global__ void __launch_bounds__(256) k_pc_block_chol(const double2* __restrict__ R_all, PcState* __restrict__ st_all,
+                                                       int m, int chi) {
+  extern __shared__ double2 pcg[];
+  constexpr int LDG = kPcCand + 1;
+  double2* G = pcg;                     // [kPcCand][LDG]
+  double2* Rf = pcg + kPcCand * LDG;    // [kPcBs][kPcCand]: Cholesky rows over candidate positions
+  __shared__ int used[kPcCand];
+  __shared__ int piv_s;
+  __shared__ double rkk_s;
+  const int mat = blockIdx.x, tid = threadIdx.x;
+  PcState* S = st_all + mat;
+  const double2* R = R_all + static_cast<int64_t>(mat) * m * kPcCand;
+  const int nc = S->ncand;
+  for (int e = tid; e < kPcCand * kPcCand; e += blockDim.x) {
+    const int t = e / kPcCand, u = e % kPcCand;
+    G[t * LDG + u] = (t < nc && u < nc) ? R[static_cast<int64_t>(S->cand[t]) * kPcCand + u] : make_double2(0.0, 0.0);
+  }
+  for (int t = tid; t < kPcCand; t += blockDim.x) used[t] = t < nc ? 0 : 1;
+  __syncthreads();
+  const int kmax = S->nsel < chi ? min(kPcBs, chi - S->nsel) : 0;
+  int k = 0;
+  for (; k < kmax; ++k) {
+    if (tid == 0) {
+      int p = -1;
+      double best = kPcAccept;
+      for (int t = 0; t < kPcCand; ++t)
+        if (!used[t] && G[t * LDG + t].x > best) {
+          best = G[t * LDG + t].x;
+          p = t;
+        }
+      piv_s = p;
+      rkk_s = p >= 0 ? sqrt(best) : 0.0;
+      if (p >= 0) used[p] = 1;
+    }
+    __syncthreads();
+    const int p = piv_s;
+    if (p < 0) break;
+    const double rkk = rkk_s;
+    for (int q = tid; q < kPcCand; q += blockDim.x) {
+      double2 v = make_double2(0.0, 0.0);
+      if (q == p) v = make_double2(rkk, 0.0);
+      else if (!used[q]) v = make_double2(G[p * LDG + q].x / rkk, G[p * LDG + q].y / rkk);
+      Rf[k * kPcCand + q] = v;
+    }
+    __syncthreads();
+    for (int e = tid; e < kPcCand * kPcCand; e += blockDim.x) {
+      const int a = e / kPcCand, b = e % kPcCand;
+      if (!used[a] && !used[b]) {  // G[a][b] -= conj(Rk[a]) Rk[b]
+        const double2 x = Rf[k * kPcCand + a], y = Rf[k * kPcCand + b];
+        G[a * LDG + b].x -= x.x * y.x + x.y * y.y;
+        G[a * LDG + b].y -= x.x * y.y - x.y * y.x;
+      }
+    }
+    if (tid == 0) S->sel[k] = p;
+    __syncthreads();
+  }
+  for (int e = tid; e < kPcBs * kPcBs; e += blockDim.x) {
+    const int j = e / kPcBs, jj = e % kPcBs;
+    S->rc[e] = (j < k && jj < k && jj >= j) ? Rf[j * kPcCand + S->sel[jj]] : make_double2(0.0, 0.0);
+  }
+  if (tid == 0) S->k = k;
+}
+
+// L[:, nsel + j] = (R[:, sel] Rc^-1)_j by forward substitution per row; d_i -= |new|^2
+__global__ void k_pc_append(const double2* __restrict__ R_all, const PcState* __restrict__ st_all,
+                            double2* __restrict__ L_all, double* __restrict__ d_all, int m, int chi) {
+  const int mat = blockIdx.y;
+  const PcState* S = st_all + mat;
+  const int k = S->k, nsel = S->nsel;
+  if (k == 0) return;
+  const double2* R = R_all + static_cast<int64_t>(mat) * m * kPcCand;
+  double2* L = L_all + static_cast<int64_t>(mat) * m * chi;
+  double* d = d_all + static_cast<int64_t>(mat) * m;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    double2 x[kPcBs];
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < kPcBs; ++j) {
+      if (j < k) {
+        double2 v = R[static_cast<int64_t>(i) * kPcCand + S->sel[j]];
+#pragma unroll
+        for (int l = 0; l < kPcBs; ++l) {
+          if (l < j) {  // v -= x_l Rc[l][j]
+            const double2 rl = S->rc[l * kPcBs + j];
+            v.x -= x[l].x * rl.x - x[l].y * rl.y;
+            v.y -= x[l].x * rl.y + x[l].y * rl.x;
+          }
+        }
+        const double inv = 1.0 / S->rc[j * kPcBs + j].x;
+        x[j] = make_double2(v.x * inv, v.y * inv);
+        L[static_cast<int64_t>(i) * chi + nsel + j] = x[j];
+        acc += x[j].x * x[j].x + x[j].y * x[j].y;
+      }
+    }
+    if (d[i] >= 0.0) d[i] -= acc;
+  }
+}
+
+// retire the block's pivots, nsel += k
+__global__ void k_pc_advance(PcState* __restrict__ st_all, double* __restrict__ d_all, int m) {
+  PcState* S = st_all + blockIdx.x;
+  double* d = d_all + static_cast<int64_t>(blockIdx.x) * m;
+  if (threadIdx.x < S->k) d[S->cand[S->sel[threadIdx.x]]] = -1.0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    S->nsel += S->k;
+    S->k = 0;
+  }
+}
+
+bool pchol_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("QTNH_SVD_SPLIT_BASIS");
+    return !(e && (std::strcmp(e, "jacobi") == 0 || std::strcmp(e, "gram") == 0));
+  }();
+  return on;
+}
+
+// Q^H (chi x m per matrix, into qh) from the projectors P[i]; true when every
+// matrix reached chi pivots and ||Q^H Q - I||_F / sqrt(chi) <= 1e-13 after at
+// most two Newton-Schulz polishes.
+bool pchol_basis(RankCtx& r, const std::vector<double2*>& P, Dim m, Dim chi, double2* qh) {
+  QTNH_RANGE("qtnh::svd_split_basis");
+  cudaStream_t st = r.stream;
+  const int ns = static_cast<int>(P.size());
+  const bool dbg = std::getenv("QTNH_SVD_DEBUG") != nullptr;
+  DevBuf Lb(static_cast<size_t>(ns) * m * chi * 16, r), d(static_cast<size_t>(ns) * m * 8, r),
+      T(static_cast<size_t>(ns) * m * kPcCand * 16, r), R(static_cast<size_t>(ns) * m * kPcCand * 16, r),
+      M(static_cast<size_t>(ns) * chi * kPcCand * 16, r), St(static_cast<size_t>(ns) * sizeof(PcState), r),
+      Pp(static_cast<size_t>(ns) * sizeof(void*), r);
+  auto* L = static_cast<double2*>(Lb.ptr);
+  auto* S = static_cast<PcState*>(St.ptr);
+  QTNH_CUDA(cudaMemsetAsync(Lb.ptr, 0, Lb.bytes, st));
+  QTNH_CUDA(cudaMemsetAsync(St.ptr, 0, St.bytes, st));
+  QTNH_CUDA(cudaMemcpyAsync(Pp.ptr, P.data(), ns * sizeof(void*), cudaMemcpyHostToDevice, st));
+  const auto* PP = static_cast<const double2* const*>(Pp.ptr);
+  const dim3 g2(static_cast<unsigned>(std::min<Dim>((m * kPcCand + 255) / 256, 1024)), static_cast<unsigned>(ns));
+  const dim3 gm(static_cast<unsigned>(std::min<Dim>((m + 255) / 256, 64)), static_cast<unsigned>(ns));
+  k_pc_diag<<<gm, 256, 0, st>>>(PP, static_cast<double*>(d.ptr), static_cast<int>(m));
+  QTNH_LAUNCH_CHECK();
+  int np2 = 1;
+  while (np2 < m) np2 <<= 1;
+  const size_t cand_smem = static_cast<size_t>(np2) * 12;
+  static bool attrs = [] {
+    cudaFuncSetAttribute(k_pc_candidates, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_pc_block_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPcCholSmem));
+    return true;
+  }();
+  (void)attrs;
+  if (cand_smem > 200 * 1024) return false;
+  std::vector<PcState> hs(ns);
+  const int max_blocks = static_cast<int>(2 * chi / kPcBs + 8);
+  int it = 0;
+  for (; it < max_blocks; ++it) {
+    k_pc_candidates<<<ns, 1024, cand_smem, st>>>(static_cast<const double*>(d.ptr), S, static_cast<int>(m), np2,
+                                                  static_cast<int>(chi));
+    QTNH_LAUNCH_CHECK();
+    if (it > 0) {
+      k_pc_gather_m<<<g2, 256, 0, st>>>(L, S, static_cast<double2*>(M.ptr), static_cast<int>(m), static_cast<int>(chi));
+      QTNH_LAUNCH_CHECK();
+      for (int i = 0; i < ns; ++i)
+        zgemm(L + static_cast<size_t>(i) * m * chi, static_cast<double2*>(M.ptr) + static_cast<size_t>(i) * chi * kPcCand,
+              static_cast<double2*>(T.ptr) + static_cast<size_t>(i) * m * kPcCand, m, kPcCand, chi, st);
+    }
+    k_pc_residual<<<g2, 256, 0, st>>>(PP, static_cast<const double2*>(T.ptr), S, static_cast<double2*>(R.ptr),
+                                      static_cast<int>(m));
+    QTNH_LAUNCH_CHECK();
+    k_pc_block_chol<<<ns, 256, kPcCholSmem, st>>>(static_cast<const double2*>(R.ptr), S, static_cast<int>(m),
+                                                  static_cast<int>(chi));
+    QTNH_LAUNCH_CHECK();
+    k_pc_append<<<gm, 256, 0, st>>>(static_cast<const double2*>(R.ptr), S, L, static_cast<double*>(d.ptr),
+                                    static_cast<int>(m), static_cast<int>(chi));
+    QTNH_LAUNCH_CHECK();
+    k_pc_advance<<<ns, 32, 0, st>>>(S, static_cast<double*>(d.ptr), static_cast<int>(m));
+    QTNH_LAUNCH_CHECK();
+    if (it + 1 >= chi / kPcBs && (it + 1 - chi / kPcBs) % 4 == 0) {
+      QTNH_CUDA(cudaMemcpyAsync(hs.data(), St.ptr, ns * sizeof(PcState), cudaMemcpyDeviceToHost, st));
+      QTNH_CUDA(cudaStreamSynchronize(st));
+      bool all = true;
+      for (const auto& x : hs) all = all && x.nsel >= chi;
+      if (all) break;
+    }
+  }
+  QTNH_CUDA(cudaMemcpyAsync(hs.data(), St.ptr, ns * sizeof(PcState), cudaMemcpyDeviceToHost, st));
+  QTNH_CUDA(cudaStreamSynchronize(st));
+  for (int i = 0; i < ns; ++i) {
+    if (dbg) std::fprintf(stderr, "svd split basis: matrix %d pivots %d of %lld in %d blocks\n", i, hs[i].nsel,
+                          static_cast<long long>(chi), it + 1);
+    if (hs[i].nsel != chi) return false;
+  }
+  // Q^H = L^H, then Newton-Schulz polish Q^H <- (1.5 I - 0.5 Q^H Q) Q^H
+  DevBuf E(static_cast<size_t>(chi * chi) * 16, r), qn(static_cast<size_t>(chi * m) * 16, r),
+      part(static_cast<size_t>(kParts) * 2 * sizeof(double), r);
+  std::vector<double> ph(kParts * 2);
+  for (int i = 0; i < ns; ++i) {
+    double2* q = qh + static_cast<size_t>(i) * chi * m;
+    double2* Li = L + static_cast<size_t>(i) * m * chi;
+    conj_t(Li, q, m, chi, st);
+    double res = 1.0;
+    for (int pol = 0; pol <= 2; ++pol) {
+      zgemm(q, Li, E.ptr, chi, chi, m, st);  // Q^H Q (Li = Q, refreshed below)
+      k_fro_trace<<<kParts, 256, 0, st>>>(static_cast<const double2*>(E.ptr), chi, 1.0, static_cast<double*>(part.ptr));
+      QTNH_LAUNCH_CHECK();
+      QTNH_CUDA(cudaMemcpyAsync(ph.data(), part.ptr, ph.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+      QTNH_CUDA(cudaStreamSynchronize(st));
+      double f = 0.0;
+      for (int k2 = 0; k2 < kParts; ++k2) f += ph[k2 * 2];
+      res = std::sqrt(f / static_cast<double>(chi));
+      if (dbg) std::fprintf(stderr, "svd split basis: matrix %d polish %d residual %.3e\n", i, pol, res);
+      if (res <= 1e-14 || pol == 2) break;
+      k_axpy_identity<<<grid_elems(chi * chi), 256, 0, st>>>(static_cast<const double2*>(E.ptr),
+                                                              static_cast<double2*>(E.ptr), chi, 1.5, -0.5);
+      QTNH_LAUNCH_CHECK();
+      zgemm(E.ptr, q, qn.ptr, chi, m, chi, st);
+      QTNH_CUDA(cudaMemcpyAsync(q, qn.ptr, static_cast<size_t>(chi * m) * 16, cudaMemcpyDeviceToDevice, st));
+      conj_t(q, Li, chi, m, st);
+    }
+    if (!(res <= 1e-13)) return false;
+  }
+  return true;
+}
+
 bool split_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("QTNH_SVD_SPLIT");
@@ -268,104 +603,116 @@ void svd_batched_ptrs(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim ch
   double* S = static_cast<double*>(s);
   if (!sp.empty()) {
     const Dim ns = static_cast<Dim>(sp.size());
-    // 4. Y = P Omega (m x chi, range(P)), and an orthonormal basis Q^H (chi x m) of it
-    //    (Gram route: G = Y^H Y = Vg^H Sg Vg by a chi x chi Jacobi, Q^H = Sg^-1/2 Vg
-    //    Y^H, Newton-Schulz polar steps Q^H <- (3 I - Q^H Q) Q^H / 2 until
-    //    ||Q^H Q - I||_F / sqrt(chi) <= 1e-14, the chi x m Jacobi if that stalls).
-    DevBuf om(static_cast<size_t>(m * chi) * 16, r);
-    qtnh_counter_complex_normals_device(st, 0x5EEDC0DEULL, 0, m * chi, om.ptr);
-    DevBuf y(static_cast<size_t>(m * chi) * 16, r);
-    DevBuf yh(static_cast<size_t>(ns * chi * m) * 16, r);
-    DevBuf gm(static_cast<size_t>(ns * chi * chi) * 16, r);
-    for (Dim i = 0; i < ns; ++i) {
-      zgemm(X[sp[i]]->ptr, om.ptr, y.ptr, m, chi, m, st);
-      double2* yhi = static_cast<double2*>(yh.ptr) + i * chi * m;
-      conj_t(static_cast<const double2*>(y.ptr), yhi, m, chi, st);
-      zgemm(yhi, y.ptr, static_cast<double2*>(gm.ptr) + i * chi * chi, chi, chi, m, st);
+    // 4. An orthonormal basis Q^H (chi x m) of range(P): block-greedy pivoted
+    //    Cholesky of P (default, pchol_basis), certified by ||Q^H Q - I||; any
+    //    matrix it cannot certify takes the previous route for the whole batch:
+    //    Y = P Omega and the chi x m Jacobi SVD of Y^H (or the Gram route below).
+    DevBuf qh(static_cast<size_t>(ns * chi * m) * 16, r);
+    bool basis_done = false;
+    if (pchol_enabled()) {
+      std::vector<double2*> pv(ns);
+      for (Dim i = 0; i < ns; ++i) pv[i] = static_cast<double2*>(X[sp[i]]->ptr);
+      basis_done = pchol_basis(r, pv, m, chi, static_cast<double2*>(qh.ptr));
+    }
+    if (!basis_done) {
+      // 4. Y = P Omega (m x chi, range(P)), and an orthonormal basis Q^H (chi x m) of it
+      //    (Gram route: G = Y^H Y = Vg^H Sg Vg by a chi x chi Jacobi, Q^H = Sg^-1/2 Vg
+      //    Y^H, Newton-Schulz polar steps Q^H <- (3 I - Q^H Q) Q^H / 2 until
+      //    ||Q^H Q - I||_F / sqrt(chi) <= 1e-14, the chi x m Jacobi if that stalls).
+      DevBuf om(static_cast<size_t>(m * chi) * 16, r);
+      qtnh_counter_complex_normals_device(st, 0x5EEDC0DEULL, 0, m * chi, om.ptr);
+      DevBuf y(static_cast<size_t>(m * chi) * 16, r);
+      DevBuf yh(static_cast<size_t>(ns * chi * m) * 16, r);
+      DevBuf gm(static_cast<size_t>(ns * chi * chi) * 16, r);
+      for (Dim i = 0; i < ns; ++i) {
+        zgemm(X[sp[i]]->ptr, om.ptr, y.ptr, m, chi, m, st);
+        double2* yhi = static_cast<double2*>(yh.ptr) + i * chi * m;
+        conj_t(static_cast<const double2*>(y.ptr), yhi, m, chi, st);
+        zgemm(yhi, y.ptr, static_cast<double2*>(gm.ptr) + i * chi * chi, chi, chi, m, st);
+      }
+      // Basis of range(Y): the chi x m Jacobi of Y^H (default), or the Gram route
+      // (QTNH_SVD_SPLIT_BASIS=gram: chi x chi Jacobi of Y^H Y + Newton-Schulz polish).
+      // Measured on a C4 theta (batch of 8): 45.6 vs 47.1 ms per SVD -- the Gram's
+      // squared condition number (cond(Y)^2 ~ 1e6) costs it 24 sweeps instead of 15.
+      static const bool gram_basis = [] {
+        const char* e = std::getenv("QTNH_SVD_SPLIT_BASIS");
+        return e && std::strcmp(e, "gram") == 0;
+      }();
+      DevBuf u1(static_cast<size_t>(ns * chi * chi) * 16, r), s1(static_cast<size_t>(ns * chi) * 8, r);
+      DevBuf vg(static_cast<size_t>(ns * chi * chi) * 16, r);
+      if (!gram_basis) svd_batched(r, ns, chi, m, yh.ptr, chi, QTNH_ABSORB_NONE, u1.ptr, s1.ptr, qh.ptr, &sw_split);
+      if (gram_basis) svd_batched(r, ns, chi, chi, gm.ptr, chi, QTNH_ABSORB_NONE, u1.ptr, s1.ptr, vg.ptr, &sw_split);
+      for (Dim i = 0; i < ns && gram_basis; ++i) {
+        double2* qhi = static_cast<double2*>(qh.ptr) + i * chi * m;
+        zgemm(static_cast<const double2*>(vg.ptr) + i * chi * chi, static_cast<const double2*>(yh.ptr) + i * chi * m,
+              qhi, chi, m, chi, st);
+        k_row_rsqrt_scale<<<grid_elems(chi * m), 256, 0, st>>>(qhi, static_cast<const double*>(s1.ptr) + i * chi, chi,
+                                                               m);
+        QTNH_LAUNCH_CHECK();
+      }
+      if (gram_basis) {
+        std::vector<std::unique_ptr<DevBuf>> E(batch);
+        std::vector<char> pact(batch, 0);
+        for (Dim b : sp) {
+          pact[b] = 1;
+          E[b] = std::make_unique<DevBuf>(static_cast<size_t>(chi * chi) * 16, r);
+        }
+        DevBuf qm(static_cast<size_t>(m * chi) * 16, r), qn(static_cast<size_t>(chi * m) * 16, r);
+        bool polished = false;
+        for (int it = 0; it <= 4 && !polished; ++it) {
+          for (Dim i = 0; i < ns; ++i) {
+            if (!pact[sp[i]]) continue;
+            const double2* qhi = static_cast<const double2*>(qh.ptr) + i * chi * m;
+            conj_t(qhi, static_cast<double2*>(qm.ptr), chi, m, st);
+            zgemm(qhi, qm.ptr, E[sp[i]]->ptr, chi, chi, m, st);
+          }
+          // stats over chi x chi matrices: reuse the m-sized helper through a local copy
+          std::vector<double> f2(batch, 0.0);
+          {
+            for (Dim b = 0; b < batch; ++b)
+              if (pact[b]) {
+                k_fro_trace<<<kParts, 256, 0, st>>>(static_cast<const double2*>(E[b]->ptr), chi, 1.0,
+                                                    static_cast<double*>(part.ptr) + b * kParts * 2);
+                QTNH_LAUNCH_CHECK();
+              }
+            QTNH_CUDA(cudaMemcpyAsync(ph.data(), part.ptr, ph.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+            QTNH_CUDA(cudaStreamSynchronize(st));
+            for (Dim b = 0; b < batch; ++b)
+              for (int k2 = 0; k2 < kParts; ++k2) f2[b] += ph[(b * kParts + k2) * 2];
+          }
+          polished = true;
+          for (Dim i = 0; i < ns; ++i) {
+            const Dim b = sp[i];
+            if (!pact[b]) continue;
+            const double res = std::sqrt(f2[b] / static_cast<double>(chi));
+            if (std::getenv("QTNH_SVD_DEBUG"))
+              std::fprintf(stderr, "svd split: matrix %lld basis polish %d residual %.3e\n", static_cast<long long>(b),
+                           it, res);
+            if (res <= 1e-14) {
+              pact[b] = 0;
+              continue;
+            }
+            if (it == 4 || !(res < 0.5)) {  // not converging: orthonormalise Y^H by the chi x m Jacobi
+              pact[b] = 0;
+              int swj = 0;
+              svd_batched(r, 1, chi, m, static_cast<const double2*>(yh.ptr) + i * chi * m, chi, QTNH_ABSORB_NONE,
+                          static_cast<double2*>(u1.ptr) + i * chi * chi, static_cast<double*>(s1.ptr) + i * chi,
+                          static_cast<double2*>(qh.ptr) + i * chi * m, &swj);
+              sw_split = std::max(sw_split, swj);
+              continue;
+            }
+            polished = false;
+            k_axpy_identity<<<grid_elems(chi * chi), 256, 0, st>>>(static_cast<const double2*>(E[b]->ptr),
+                                                                    static_cast<double2*>(E[b]->ptr), chi, 1.5, -0.5);
+            QTNH_LAUNCH_CHECK();
+            double2* qhi = static_cast<double2*>(qh.ptr) + i * chi * m;
+            zgemm(E[b]->ptr, qhi, qn.ptr, chi, m, chi, st);
+            QTNH_CUDA(cudaMemcpyAsync(qhi, qn.ptr, static_cast<size_t>(chi * m) * 16, cudaMemcpyDeviceToDevice, st));
+          }
+        }
+      }
     }
     for (Dim b : sp) X[b].reset();
-    // Basis of range(Y): the chi x m Jacobi of Y^H (default), or the Gram route
-    // (QTNH_SVD_SPLIT_BASIS=gram: chi x chi Jacobi of Y^H Y + Newton-Schulz polish).
-    // Measured on a C4 theta (batch of 8): 45.6 vs 47.1 ms per SVD -- the Gram's
-    // squared condition number (cond(Y)^2 ~ 1e6) costs it 24 sweeps instead of 15.
-    static const bool gram_basis = [] {
-      const char* e = std::getenv("QTNH_SVD_SPLIT_BASIS");
-      return e && std::strcmp(e, "gram") == 0;
-    }();
-    DevBuf u1(static_cast<size_t>(ns * chi * chi) * 16, r), s1(static_cast<size_t>(ns * chi) * 8, r);
-    DevBuf vg(static_cast<size_t>(ns * chi * chi) * 16, r);
-    DevBuf qh(static_cast<size_t>(ns * chi * m) * 16, r);
-    if (!gram_basis) svd_batched(r, ns, chi, m, yh.ptr, chi, QTNH_ABSORB_NONE, u1.ptr, s1.ptr, qh.ptr, &sw_split);
-    if (gram_basis) svd_batched(r, ns, chi, chi, gm.ptr, chi, QTNH_ABSORB_NONE, u1.ptr, s1.ptr, vg.ptr, &sw_split);
-    for (Dim i = 0; i < ns && gram_basis; ++i) {
-      double2* qhi = static_cast<double2*>(qh.ptr) + i * chi * m;
-      zgemm(static_cast<const double2*>(vg.ptr) + i * chi * chi, static_cast<const double2*>(yh.ptr) + i * chi * m,
-            qhi, chi, m, chi, st);
-      k_row_rsqrt_scale<<<grid_elems(chi * m), 256, 0, st>>>(qhi, static_cast<const double*>(s1.ptr) + i * chi, chi,
-                                                             m);
-      QTNH_LAUNCH_CHECK();
-    }
-    if (gram_basis) {
-      std::vector<std::unique_ptr<DevBuf>> E(batch);
-      std::vector<char> pact(batch, 0);
-      for (Dim b : sp) {
-        pact[b] = 1;
-        E[b] = std::make_unique<DevBuf>(static_cast<size_t>(chi * chi) * 16, r);
-      }
-      DevBuf qm(static_cast<size_t>(m * chi) * 16, r), qn(static_cast<size_t>(chi * m) * 16, r);
-      bool polished = false;
-      for (int it = 0; it <= 4 && !polished; ++it) {
-        for (Dim i = 0; i < ns; ++i) {
-          if (!pact[sp[i]]) continue;
-          const double2* qhi = static_cast<const double2*>(qh.ptr) + i * chi * m;
-          conj_t(qhi, static_cast<double2*>(qm.ptr), chi, m, st);
-          zgemm(qhi, qm.ptr, E[sp[i]]->ptr, chi, chi, m, st);
-        }
-        // stats over chi x chi matrices: reuse the m-sized helper through a local copy
-        std::vector<double> f2(batch, 0.0);
-        {
-          for (Dim b = 0; b < batch; ++b)
-            if (pact[b]) {
-              k_fro_trace<<<kParts, 256, 0, st>>>(static_cast<const double2*>(E[b]->ptr), chi, 1.0,
-                                                  static_cast<double*>(part.ptr) + b * kParts * 2);
-              QTNH_LAUNCH_CHECK();
-            }
-          QTNH_CUDA(cudaMemcpyAsync(ph.data(), part.ptr, ph.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
-          QTNH_CUDA(cudaStreamSynchronize(st));
-          for (Dim b = 0; b < batch; ++b)
-            for (int k2 = 0; k2 < kParts; ++k2) f2[b] += ph[(b * kParts + k2) * 2];
-        }
-        polished = true;
-        for (Dim i = 0; i < ns; ++i) {
-          const Dim b = sp[i];
-          if (!pact[b]) continue;
-          const double res = std::sqrt(f2[b] / static_cast<double>(chi));
-          if (std::getenv("QTNH_SVD_DEBUG"))
-            std::fprintf(stderr, "svd split: matrix %lld basis polish %d residual %.3e\n", static_cast<long long>(b),
-                         it, res);
-          if (res <= 1e-14) {
-            pact[b] = 0;
-            continue;
-          }
-          if (it == 4 || !(res < 0.5)) {  // not converging: orthonormalise Y^H by the chi x m Jacobi
-            pact[b] = 0;
-            int swj = 0;
-            svd_batched(r, 1, chi, m, static_cast<const double2*>(yh.ptr) + i * chi * m, chi, QTNH_ABSORB_NONE,
-                        static_cast<double2*>(u1.ptr) + i * chi * chi, static_cast<double*>(s1.ptr) + i * chi,
-                        static_cast<double2*>(qh.ptr) + i * chi * m, &swj);
-            sw_split = std::max(sw_split, swj);
-            continue;
-          }
-          polished = false;
-          k_axpy_identity<<<grid_elems(chi * chi), 256, 0, st>>>(static_cast<const double2*>(E[b]->ptr),
-                                                                  static_cast<double2*>(E[b]->ptr), chi, 1.5, -0.5);
-          QTNH_LAUNCH_CHECK();
-          double2* qhi = static_cast<double2*>(qh.ptr) + i * chi * m;
-          zgemm(E[b]->ptr, qhi, qn.ptr, chi, m, chi, st);
-          QTNH_CUDA(cudaMemcpyAsync(qhi, qn.ptr, static_cast<size_t>(chi * m) * 16, cudaMemcpyDeviceToDevice, st));
-        }
-      }
-    }
     // 5. B = Q^H A (chi x n) and its SVD (absorb applied), U = Q U_B
     DevBuf bm(static_cast<size_t>(ns * chi * n) * 16, r);
     for (Dim i = 0; i < ns; ++i)
