@@ -357,7 +357,26 @@ def measure_extras(rk, stream, torch):
     e1.synchronize()
     ms = e0.elapsed_time(e1)
     ex["svd_2048_chi1024_batch8"] = {"ms_per_svd": ms / bt, "sweeps": int(qtnh.lib.qtnh_last_error_info()),
-                                     "conv_TFLOPs": bt * 88.0 * nn**3 / (ms * 1e-3) / 1e12}
+                                     "conv_TFLOPs": bt * 88.0 * nn**3 / (ms * 1e-3) / 1e12,
+                                     "input": "i.i.d. complex normal (continuous spectrum: full Jacobi)"}
+    # config 4's first saturated thetas have exactly two singular values (chi-fold
+    # each): the spectral-split path (projector by Newton-Schulz, pivoted-Cholesky
+    # basis); inputs U diag(s) V^H built with torch QR outside the timed region
+    q1 = torch.linalg.qr(a)[0]
+    q2 = torch.linalg.qr(a.transpose(1, 2).conj().contiguous())[0]
+    sv = torch.tensor([0.70719] * chi + [0.35957] * (nn - chi), dtype=torch.float64, device="cuda")
+    a = ((q1 * sv) @ q2.transpose(1, 2).conj()).contiguous()
+    del q1, q2
+    torch.cuda.synchronize()
+    e0.record(stream)
+    qtnh.check(qtnh.lib.qtnh_svd_device(rk._h, bt, nn, nn, C.c_void_p(a.data_ptr()), chi, 1, C.c_void_p(u.data_ptr()),
+                                        C.c_void_p(s.data_ptr()), C.c_void_p(vh.data_ptr())))
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    ex["svd_2048_chi1024_batch8_two_valued"] = {
+        "ms_per_svd": ms / bt, "conv_TFLOPs": bt * 88.0 * nn**3 / (ms * 1e-3) / 1e12,
+        "input": "U diag(0.70719 x 1024, 0.35957 x 1024) V^H, Haar U, V (config 4's early saturated thetas)"}
     del a, u, s, vh
     return ex
 
