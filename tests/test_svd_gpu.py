@@ -267,3 +267,36 @@ def test_svd_null_cnot_bell_bond():
     assert np.allclose(s, [1.0, 0.0], atol=1e-15)
     assert _iso_cols(u) < 1e-14 and _iso_cols(vh.conj().T) < 1e-14
     assert rel_l2((u * s) @ vh, a) < 1e-14
+
+
+def test_svd_device_batch_null_completion():
+    """qtnh_svd_device: a batch mixing a full-rank and a rank-3 matrix; the
+    rank-deficient one gets orthonormal completions, the other is untouched."""
+    import torch
+
+    m, n, chi = 40, 56, 20
+    rng = np.random.default_rng(11)
+    full = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+    low = (rng.standard_normal((m, 3)) + 1j * rng.standard_normal((m, 3))) @ (
+        rng.standard_normal((3, n)) + 1j * rng.standard_normal((3, n)))
+    a = np.stack([full, low])
+    ta = torch.from_numpy(a).cuda()
+    tu = torch.empty((2, m, chi), dtype=torch.complex128, device="cuda")
+    ts = torch.empty((2, chi), dtype=torch.float64, device="cuda")
+    tv = torch.empty((2, chi, n), dtype=torch.complex128, device="cuda")
+
+    def body(rk):
+        rk.set_stream(torch.cuda.current_stream().cuda_stream)
+        qtnh.check(qtnh.lib.qtnh_svd_device(rk._h, 2, m, n, C.c_void_p(ta.data_ptr()), chi, ABSORB_NONE,
+                                            C.c_void_p(tu.data_ptr()), C.c_void_p(ts.data_ptr()),
+                                            C.c_void_p(tv.data_ptr())))
+        torch.cuda.synchronize()
+
+    World(1).run(body)
+    for i in range(2):
+        u, s, vh = tu[i].cpu().numpy(), ts[i].cpu().numpy(), tv[i].cpu().numpy()
+        assert _iso_cols(u) < 1e-12 and _iso_cols(vh.conj().T) < 1e-12
+        U, S, VH = np.linalg.svd(a[i], full_matrices=False)
+        keep = 3 if i else chi
+        assert np.allclose(s[:keep], S[:keep], rtol=1e-12)
+        assert rel_l2((u * s) @ vh, (U[:, :chi] * S[:chi]) @ VH[:chi]) < TOL
