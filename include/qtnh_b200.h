@@ -179,23 +179,52 @@ int qtnh_tensor_upload_local(qtnh_tensor_t t, const double* host);
 /* Span-collective gather of the full global vector into `host` (total_size complex)
  * on every span rank (tensor.hpp:341-371). */
 int qtnh_tensor_to_global(qtnh_tensor_t t, double* host);
-/* QTNHTEN1 files (tensor.hpp:373-446), byte-identical to the reference's. Save is
- * span-collective (Tensor::save(path), tensor.hpp:388-397): the first span rank
- * writes the header, every canonical holder writes its own block at its offset
- * straight from HBM (no gather). Load (Tensor::load(Rank&, path), tensor.hpp:
- * 399-446) reads only this rank's block; dense / symmetric variants (0, 1) --
- * others return QTNH_E_INVALID_ARGUMENT and are materialised by the host layer. */
+/* ---- storage variants (tensor.hpp:28: dense 0, symmetric 1, diagonal 2, identity 3,
+ * swap 4) ---------------------------------------------------------------------
+ * The compact variants keep the reference's storage contract in HBM: a diagonal
+ * tensor holds its block's slice of the diagonal (only on blocks whose input and
+ * output distributed coordinates agree), identity and swap hold nothing. rebcast,
+ * conj, scale, clone, save and load keep the variant (ops.hpp:54-161, tensor.hpp:
+ * 373-446); every other operation reads the tensor through its dense value
+ * (to_dense, materialised on the device on first use), as the reference's ops do. */
+enum { QTNH_DENSE = 0, QTNH_SYMMETRIC = 1, QTNH_DIAGONAL = 2, QTNH_IDENTITY = 3, QTNH_SWAP = 4 };
 /* Tensor::identity / Tensor::swap_tensor (tensor.hpp:144-164): element = 1 iff
  * coords[in_pos[k]] == coords[out_pos[k]] for every pair (crossed != 0: swap, the
- * two outputs exchanged; exactly two pairs), materialised densely on the device. */
+ * two outputs exchanged; exactly two pairs). No storage. */
 int qtnh_tensor_paired(qtnh_rank_t r, int n, const int64_t* dims, int split, const int64_t* dist, int n_pairs,
                        const int* in_pos, const int* out_pos, int crossed, qtnh_tensor_t* out);
 /* Tensor::diagonal (tensor.hpp:114-142) over the symmetric half-split layout
- * (in_dist, out_dist; in_local, out_local), materialised densely: only blocks with
- * equal input / output distributed coordinates carry their slice of the diagonal
- * (`count` complex values, row-major over the input coordinates). */
+ * (in_dist, out_dist; in_local, out_local): `count` complex values, the diagonal in
+ * row-major order of the input coordinates; each on-diagonal block keeps its slice.
+ * diag_global == NULL with count < 0: a zero diagonal (filled later by upload_local). */
 int qtnh_tensor_diagonal(qtnh_rank_t r, int n, const int64_t* dims, int split, const int64_t* dist,
                          const double* diag_global, int64_t count, qtnh_tensor_t* out);
+/* Tensor::symmetric / symmetric_from_global (tensor.hpp:97-112): dense storage, the
+ * half-split layout validated first; data = this rank's block (is_global == 0,
+ * `count` must equal the local size) or the global vector (is_global != 0);
+ * data == NULL: a zero block. */
+int qtnh_tensor_symmetric(qtnh_rank_t r, int n, const int64_t* dims, int split, const int64_t* dist,
+                          const double* data, int64_t count, int is_global, qtnh_tensor_t* out);
+int qtnh_tensor_variant(qtnh_tensor_t t);          /* Tensor::variant(), tensor.hpp:174 */
+int64_t qtnh_tensor_stored_size(qtnh_tensor_t t);  /* local_data().size(): complex elements this rank stores */
+/* equality_in() / equality_out() (tensor.hpp:193-194): the rank/2 pairs as constructed. */
+int qtnh_tensor_pairs(qtnh_tensor_t t, int* in_pos, int* out_pos);
+/* Tensor::to_dense (tensor.hpp:282-296): same shape, distribution and values. */
+int qtnh_tensor_to_dense(qtnh_tensor_t t, qtnh_tensor_t* out);
+/* Tensor::local_element (tensor.hpp:209-247): value at global coordinates from this
+ * rank's storage (computed for identity / swap, 0 off the diagonal of a diagonal
+ * tensor); QTNH_E_INVALID_ARGUMENT when the hosting block lives on another rank. */
+int qtnh_tensor_local_element(qtnh_tensor_t t, const int64_t* coords, double* out_re_im);
+/* ops::squeeze / unsqueeze (ops.hpp:234-262): remove / insert a size-1 index;
+ * metadata only, the result shares the block. */
+int qtnh_squeeze(qtnh_tensor_t t, int pos, qtnh_tensor_t* out);
+int qtnh_unsqueeze(qtnh_tensor_t t, int pos, int as_dist, qtnh_tensor_t* out);
+/* QTNHTEN1 files (tensor.hpp:373-446), byte-identical to the reference's, every
+ * variant (a diagonal tensor stores its diagonal, identity and swap their pair
+ * list). Save is span-collective (Tensor::save(path), tensor.hpp:388-397): the first
+ * span rank writes the header, every canonical holder writes its own block (or
+ * diagonal slice) at its offset straight from HBM (no gather). Load
+ * (Tensor::load(Rank&, path), tensor.hpp:399-446) reads only this rank's part. */
 int qtnh_tensor_save(qtnh_tensor_t t, const char* path);
 int qtnh_tensor_load(qtnh_rank_t r, const char* path, qtnh_tensor_t* out);
 
@@ -273,6 +302,12 @@ int qtnh_contract_host(qtnh_rank_t r, int na, const int64_t* dims_a, const doubl
  * if the state handle is shared, it is duplicated first. */
 int qtnh_gate_apply(qtnh_tensor_t state, int n_targets, const int* targets,
                     const double* gate, int diagonal);
+/* The same with the gate as a replicated tensor (outputs; inputs) of any variant
+ * (split 0, DistParams{1, P, 0}): a diagonal-variant gate runs the diagonal kernel
+ * from its stored diagonal and needs no exchange even on distributed targets
+ * (tensor.hpp:114-142), an identity does nothing, a two-target swap
+ * is an index exchange, dense / symmetric gates take the dense path. */
+int qtnh_gate_apply_tensor(qtnh_tensor_t state, int n_targets, const int* targets, qtnh_tensor_t gate);
 
 /* In-place exchange of two equal-size indices (values of ops::permute with the
  * two positions swapped -- a contraction with a swap tensor, tensor.hpp:157-164);

@@ -42,6 +42,7 @@ namespace qtnh_b200 {
 
 using Complex = std::complex<double>;
 using Dim = std::int64_t;
+using Coords = std::vector<Dim>;  // indexing.hpp:27
 
 struct Error : std::runtime_error {
   explicit Error(const std::string& m) : std::runtime_error(m) {}
@@ -105,16 +106,127 @@ struct IndexTuple {  // indexing.hpp:32-80
   Dim total_size() const { return dist_size() * local_size(); }
   std::vector<Dim> dist_dims() const { return {dims.begin(), dims.begin() + split}; }
   std::vector<Dim> local_dims() const { return {dims.begin() + split, dims.end()}; }
+  /// "(d0,d1;l0,l1)": distributed dims, ';', local dims (indexing.hpp:70-79).
+  std::string str() const {
+    std::string out = "(";
+    for (int i = 0; i < n_idx(); ++i) {
+      if (i == split) out += ";";
+      else if (i > 0) out += ",";
+      out += std::to_string(dims[i]);
+    }
+    if (split == n_idx()) out += ";";
+    return out + ")";
+  }
 };
 
 struct DistParams {  // indexing.hpp:84-101
   Dim stretch = 1, cycles = 1, offset = 0;
+  DistParams() = default;
+  DistParams(Dim s, Dim c, Dim o) : stretch(s), cycles(c), offset(o) {}
+  void validate() const {
+    if (stretch < 1 || cycles < 1 || offset < 0)
+      throw InvalidArgument("invalid broadcast parameters (str=" + std::to_string(stretch) +
+                            ", cyc=" + std::to_string(cycles) + ", off=" + std::to_string(offset) + ")");
+  }
   Dim span(Dim dist_size) const { return stretch * cycles * dist_size; }
   bool operator==(const DistParams& o) const {
     return stretch == o.stretch && cycles == o.cycles && offset == o.offset;
   }
   bool operator!=(const DistParams& o) const { return !(*this == o); }
 };
+
+// ---- layout arithmetic (indexing.hpp:103-219), host only ---------------------------
+namespace idx {
+/// Row-major strides (rightmost index fastest).
+inline std::vector<Dim> strides(const std::vector<Dim>& dims) {
+  std::vector<Dim> st(dims.size(), 1);
+  for (std::size_t i = dims.size(); i-- > 1;) st[i - 1] = st[i] * dims[i];
+  return st;
+}
+/// Row-major flat offset of `coords` over `dims`, bounds checked.
+inline Dim flat(const Coords& coords, const std::vector<Dim>& dims) {
+  if (coords.size() != dims.size()) throw InvalidArgument("coordinate count does not match dimension count");
+  Dim at = 0;
+  for (std::size_t i = 0; i < dims.size(); ++i) {
+    if (coords[i] < 0 || coords[i] >= dims[i])
+      throw InvalidArgument("coordinate " + std::to_string(coords[i]) + " out of bounds for dimension " +
+                            std::to_string(dims[i]));
+    at = at * dims[i] + coords[i];
+  }
+  return at;
+}
+inline Coords unflat(Dim at, const std::vector<Dim>& dims) {
+  Coords c(dims.size(), 0);
+  for (std::size_t i = dims.size(); i-- > 0;) {
+    c[i] = at % dims[i];
+    at /= dims[i];
+  }
+  return c;
+}
+}  // namespace idx
+
+/// Offset of local coordinates inside a rank's block (indexing.hpp:137-139).
+inline Dim flat_offset(const Coords& local_coords, const IndexTuple& shape) {
+  return idx::flat(local_coords, shape.local_dims());
+}
+/// Every rank holding block b: offset + c str N_d + b str + t over cycles c and slots t
+/// (indexing.hpp:141-168).
+inline std::vector<int> home_ranks_of_block(Dim b, Dim dist_size, const DistParams& dist) {
+  std::vector<int> homes;
+  for (Dim c = 0; c < dist.cycles; ++c)
+    for (Dim t = 0; t < dist.stretch; ++t)
+      homes.push_back(static_cast<int>(dist.offset + (c * dist_size + b) * dist.stretch + t));
+  return homes;
+}
+inline std::vector<int> home_ranks(const Coords& dist_coords, const IndexTuple& shape, const DistParams& dist) {
+  return home_ranks_of_block(idx::flat(dist_coords, shape.dist_dims()), shape.dist_size(), dist);
+}
+/// The cycle-0, slot-0 holder of block b (indexing.hpp:171-173).
+inline int canonical_rank_of_block(Dim b, const DistParams& dist) {
+  return static_cast<int>(dist.offset + b * dist.stretch);
+}
+struct BlockLocation {
+  Dim cycle, block, slot;
+};
+/// Which copy of which block `rank` holds; false outside the span (indexing.hpp:181-191).
+inline bool locate_rank(int rank, Dim dist_size, const DistParams& dist, BlockLocation* loc) {
+  const Dim rel = rank - dist.offset;
+  if (rel < 0 || rel >= dist.span(dist_size)) return false;
+  const Dim per_cycle = dist.stretch * dist_size;
+  loc->cycle = rel / per_cycle;
+  loc->block = (rel % per_cycle) / dist.stretch;
+  loc->slot = rel % dist.stretch;
+  return true;
+}
+/// Row-major coordinate counter (indexing.hpp:193-219); advance() returns the index
+/// that was incremented, -1 after the last tuple.
+class Odometer {
+ public:
+  explicit Odometer(std::vector<Dim> dims) : dims_(std::move(dims)), at_(dims_.size(), 0) {
+    for (Dim d : dims_) count_ *= d;
+  }
+  Dim count() const { return count_; }
+  const Coords& coords() const { return at_; }
+  int advance() {
+    for (std::size_t i = dims_.size(); i-- > 0;) {
+      if (++at_[i] < dims_[i]) return static_cast<int>(i);
+      at_[i] = 0;
+    }
+    return -1;
+  }
+
+ private:
+  std::vector<Dim> dims_;
+  Coords at_;
+  Dim count_ = 1;
+};
+
+/// tensor.hpp:28-39
+enum class Variant : std::uint32_t { dense = 0, symmetric = 1, diagonal = 2, identity = 3, swap = 4 };
+inline const char* variant_name(Variant v) {
+  static const char* names[] = {"dense", "symmetric", "diagonal", "identity", "swap"};
+  return static_cast<std::uint32_t>(v) < 5 ? names[static_cast<std::uint32_t>(v)] : "?";
+}
 
 class Rank;
 
@@ -368,9 +480,14 @@ class Tensor {  // tensor.hpp:53-695 (dense)
   static Tensor dense(Rank& r, const IndexTuple& s, DistParams d, const std::vector<Complex>& local) {
     qtnh_tensor_t h;
     int64_t dd[3] = {d.stretch, d.cycles, d.offset};
+    const bool fits = static_cast<Dim>(local.size()) == s.local_size();
     check(qtnh_tensor_dense(r.handle(), s.n_idx(), s.dims.data(), s.split, dd,
-                            local.empty() ? nullptr : reinterpret_cast<const double*>(local.data()), &h));
-    return wrap(h, &r);
+                            fits && !local.empty() ? reinterpret_cast<const double*>(local.data()) : nullptr, &h));
+    Tensor t = wrap(h, &r);
+    if (!fits && t.in_span())  // span ranks need exactly their block (tensor.hpp:64-69)
+      throw InvalidArgument("dense local data has " + std::to_string(local.size()) + " elements, expected " +
+                            std::to_string(s.local_size()));
+    return t;
   }
   static Tensor from_global(Rank& r, const IndexTuple& s, DistParams d, const std::vector<Complex>& global) {
     if (static_cast<Dim>(global.size()) != s.total_size()) throw InvalidArgument("global element count mismatch");
@@ -380,7 +497,72 @@ class Tensor {  // tensor.hpp:53-695 (dense)
                                   reinterpret_cast<const double*>(global.data()), &h));
     return wrap(h, &r);
   }
-  // Tensor::identity / swap_tensor (tensor.hpp:144-164), dense on the device
+  /// tensor.hpp:72-80: elements computed per global coordinate tuple on every span rank.
+  static Tensor dense_fn(Rank& r, const IndexTuple& s, DistParams d, const std::function<Complex(const Coords&)>& fn) {
+    d.validate();
+    BlockLocation loc{0, 0, 0};
+    std::vector<Complex> block;
+    if (d.offset + d.span(s.dist_size()) <= r.size() && locate_rank(r.rank(), s.dist_size(), d, &loc)) {
+      Coords full = idx::unflat(loc.block, s.dist_dims());
+      full.resize(s.n_idx(), 0);
+      Odometer od(s.local_dims());
+      block.reserve(static_cast<std::size_t>(od.count()));
+      for (Dim i = 0; i < od.count(); ++i) {
+        std::copy(od.coords().begin(), od.coords().end(), full.begin() + s.split);
+        block.push_back(fn(full));
+        od.advance();
+      }
+    }
+    return dense(r, s, d, block);
+  }
+  /// tensor.hpp:97-112: dense storage, half-split (in, out) layout validated.
+  static Tensor symmetric(Rank& r, const IndexTuple& s, DistParams d, const std::vector<Complex>& local) {
+    qtnh_tensor_t h;
+    int64_t dd[3] = {d.stretch, d.cycles, d.offset};
+    check(qtnh_tensor_symmetric(r.handle(), s.n_idx(), s.dims.data(), s.split, dd,
+                                reinterpret_cast<const double*>(local.data()), static_cast<int64_t>(local.size()), 0,
+                                &h));
+    return wrap(h, &r);
+  }
+  static Tensor symmetric_from_global(Rank& r, const IndexTuple& s, DistParams d, const std::vector<Complex>& global) {
+    qtnh_tensor_t h;
+    int64_t dd[3] = {d.stretch, d.cycles, d.offset};
+    check(qtnh_tensor_symmetric(r.handle(), s.n_idx(), s.dims.data(), s.split, dd,
+                                reinterpret_cast<const double*>(global.data()), static_cast<int64_t>(global.size()),
+                                1, &h));
+    return wrap(h, &r);
+  }
+  /// tensor.hpp:114-142: `diag_global` = the diagonal in row-major order of the input
+  /// coordinates; each on-diagonal block keeps its slice in HBM.
+  static Tensor diagonal(Rank& r, const IndexTuple& s, DistParams d, const std::vector<Complex>& diag_global) {
+    qtnh_tensor_t h;
+    int64_t dd[3] = {d.stretch, d.cycles, d.offset};
+    check(qtnh_tensor_diagonal(r.handle(), s.n_idx(), s.dims.data(), s.split, dd,
+                               reinterpret_cast<const double*>(diag_global.data()),
+                               static_cast<int64_t>(diag_global.size()), &h));
+    return wrap(h, &r);
+  }
+  /// tensor.hpp:450-455: the same value under given metadata; `local` is this rank's
+  /// stored data (the block, or the diagonal slice of a diagonal tensor).
+  static Tensor adopt(Rank& r, Variant var, const IndexTuple& s, DistParams d, const std::vector<Complex>& local) {
+    if (var == Variant::identity || var == Variant::swap)
+      throw InvalidArgument("identity / swap tensors are rebuilt from their index pairs");
+    qtnh_tensor_t h;
+    int64_t dd[3] = {d.stretch, d.cycles, d.offset};
+    if (var == Variant::diagonal)
+      check(qtnh_tensor_diagonal(r.handle(), s.n_idx(), s.dims.data(), s.split, dd, nullptr, -1, &h));
+    else if (var == Variant::symmetric)
+      check(qtnh_tensor_symmetric(r.handle(), s.n_idx(), s.dims.data(), s.split, dd, nullptr, 0, 0, &h));
+    else
+      check(qtnh_tensor_dense(r.handle(), s.n_idx(), s.dims.data(), s.split, dd, nullptr, &h));
+    Tensor t = wrap(h, &r);
+    if (static_cast<Dim>(local.size()) == qtnh_tensor_stored_size(h) && !local.empty()) {
+      check(qtnh_tensor_upload_local(h, reinterpret_cast<const double*>(local.data())));
+      check(qtnh_rank_synchronize(r.handle()));
+    }
+    return t;
+  }
+  // Tensor::identity / swap_tensor (tensor.hpp:144-164): no storage
   static Tensor identity(Rank& r, const IndexTuple& s, DistParams d, const std::vector<int>& in_pos,
                          const std::vector<int>& out_pos) {
     return paired(r, s, d, in_pos, out_pos, 0);
@@ -407,9 +589,41 @@ class Tensor {  // tensor.hpp:53-695 (dense)
     check(qtnh_tensor_dist(h(), d));
     return {d[0], d[1], d[2]};
   }
+  Variant variant() const { return static_cast<Variant>(qtnh_tensor_variant(h())); }
   Dim span() const { return qtnh_tensor_span(h()); }
   bool in_span() const { return qtnh_tensor_in_span(h()) != 0; }
   Dim my_block() const { return qtnh_tensor_my_block(h()); }
+  bool is_canonical_holder() const { return qtnh_tensor_is_canonical(h()) != 0; }
+  /// Index pairs of an identity / swap tensor as constructed (tensor.hpp:193-194).
+  std::vector<int> equality_in() const { return pairs(0); }
+  std::vector<int> equality_out() const { return pairs(1); }
+  /// Input halves of the (in, out) layout (symmetric and diagonal tensors, tensor.hpp:196-203).
+  std::vector<Dim> in_dist_dims() const {
+    IndexTuple s = shape();
+    return {s.dims.begin(), s.dims.begin() + s.split / 2};
+  }
+  std::vector<Dim> in_local_dims() const {
+    IndexTuple s = shape();
+    return {s.dims.begin() + s.split, s.dims.begin() + s.split + s.n_local() / 2};
+  }
+  /// tensor.hpp:209-247: value at global coordinates from this rank's storage.
+  Complex local_element(const Coords& coords) const {
+    if (static_cast<int>(coords.size()) != qtnh_tensor_rank(h()))
+      throw InvalidArgument("expected " + std::to_string(qtnh_tensor_rank(h())) + " coordinates");
+    double v[2];
+    check(qtnh_tensor_local_element(h(), coords.data(), v));
+    return {v[0], v[1]};
+  }
+  /// tensor.hpp:251-264: span-collective; the canonical holder's value on every span rank.
+  Complex element(const Coords& coords) const { return element_over(coords, false); }
+  /// tensor.hpp:268-277: world-collective.
+  Complex element_world(const Coords& coords) const { return element_over(coords, true); }
+  /// tensor.hpp:282-296: dense tensor with the same shape, distribution and values.
+  Tensor to_dense() const {
+    qtnh_tensor_t o;
+    check(qtnh_tensor_to_dense(h(), &o));
+    return wrap(o, ctx_);
+  }
   std::vector<int> span_ranks() const {
     auto d = dist();
     std::vector<int> out;
@@ -417,9 +631,10 @@ class Tensor {  // tensor.hpp:53-695 (dense)
     return out;
   }
 
-  /// This rank's block, downloaded (tensor.hpp:177).
+  /// This rank's stored elements, downloaded (tensor.hpp:177): the block, a diagonal
+  /// tensor's slice of the diagonal, nothing for identity / swap.
   std::vector<Complex> local_data() const {
-    std::vector<Complex> v(in_span() ? qtnh_tensor_local_size(h()) : 0);
+    std::vector<Complex> v(static_cast<std::size_t>(qtnh_tensor_stored_size(h())));
     if (!v.empty()) check(qtnh_tensor_download_local(h(), reinterpret_cast<double*>(v.data())));
     return v;
   }
@@ -478,6 +693,32 @@ class Tensor {  // tensor.hpp:53-695 (dense)
     bool dirty = false;
   };
   Tensor(qtnh_tensor_t h, Rank* ctx) : st_(std::make_shared<State>(h)), ctx_(ctx) {}
+  std::vector<int> pairs(int which) const {
+    Variant v = variant();
+    if (v != Variant::identity && v != Variant::swap) return {};
+    std::vector<int> in(qtnh_tensor_rank(h()) / 2), out(in.size());
+    check(qtnh_tensor_pairs(h(), in.data(), out.data()));
+    return which ? out : in;
+  }
+  Complex element_over(const Coords& coords, bool world) const {
+    IndexTuple s = shape();
+    if (static_cast<int>(coords.size()) != s.n_idx())
+      throw InvalidArgument("expected " + std::to_string(s.n_idx()) + " coordinates");
+    for (int i = 0; i < s.n_idx(); ++i)
+      if (coords[i] < 0 || coords[i] >= s.dims[i])
+        throw InvalidArgument("coordinate out of bounds at index " + std::to_string(i));
+    if (!world) {
+      if (!in_span()) return {0.0, 0.0};
+      if (span() == 1) return local_element(coords);
+    }
+    DistParams d = dist();
+    const int root = canonical_rank_of_block(idx::flat(Coords(coords.begin(), coords.begin() + s.split), s.dist_dims()), d);
+    Group g = world ? ctx().world_group() : ctx().group(span_ranks());
+    std::vector<Complex> one;
+    if (ctx().rank() == root) one.push_back(local_element(coords));
+    one = g.broadcast(one, world ? root : root - static_cast<int>(d.offset));
+    return one.at(0);
+  }
   std::shared_ptr<State> st_;
   Rank* ctx_ = nullptr;
   friend Tensor wrap(qtnh_tensor_t, Rank*);
@@ -487,6 +728,8 @@ inline Tensor wrap(qtnh_tensor_t h, Rank* ctx) { return Tensor(h, ctx); }
 
 namespace ops {  // ops.hpp
 inline Tensor permute(const Tensor& t, const std::vector<int>& perm, int new_split) {  // ops.hpp:27-49
+  if (static_cast<int>(perm.size()) != qtnh_tensor_rank(t.h()))
+    throw InvalidArgument("permutation size does not match tensor rank");
   qtnh_tensor_t o;
   check(qtnh_permute(t.h(), perm.data(), new_split, &o));
   return wrap(o, &t.ctx());
@@ -508,11 +751,16 @@ inline Tensor gather_index(const Tensor& t, int pos) {  // ops.hpp:133
   return wrap(o, &t.ctx());
 }
 // remap::tensor_to_tensor (remap.hpp:106): axis_map[src] = dst position
-inline Tensor tensor_to_tensor(const Tensor& t, const IndexTuple& dst, DistParams d, const std::vector<int>& axis_map) {
+inline Tensor tensor_to_tensor(const Tensor& t, const IndexTuple& dst, DistParams d, const std::vector<int>& axis_map,
+                               Variant dst_variant = Variant::dense) {
+  if (dst_variant != Variant::dense && dst_variant != Variant::symmetric)
+    throw InvalidArgument("remap destinations store every element (dense or symmetric)");
   qtnh_tensor_t o;
   int64_t dd[3] = {d.stretch, d.cycles, d.offset};
   check(qtnh_remap(t.h(), axis_map.data(), dst.n_idx(), dst.dims.data(), dst.split, dd, &o));
-  return wrap(o, &t.ctx());
+  Tensor out = wrap(o, &t.ctx());
+  if (dst_variant == Variant::dense) return out;
+  return Tensor::adopt(t.ctx(), Variant::symmetric, dst, d, out.local_data());  // tag kept, as remap.hpp:125
 }
 inline Tensor slice_local_dims(const Tensor& t, const std::vector<Dim>& new_local) {  // ops.hpp:166
   qtnh_tensor_t o;
@@ -522,6 +770,16 @@ inline Tensor slice_local_dims(const Tensor& t, const std::vector<Dim>& new_loca
 inline Tensor pad_local_dims(const Tensor& t, const std::vector<Dim>& new_local) {  // ops.hpp:201
   qtnh_tensor_t o;
   check(qtnh_pad_local_dims(t.h(), new_local.data(), &o));
+  return wrap(o, &t.ctx());
+}
+inline Tensor squeeze(const Tensor& t, int pos) {  // ops.hpp:234
+  qtnh_tensor_t o;
+  check(qtnh_squeeze(t.h(), pos, &o));
+  return wrap(o, &t.ctx());
+}
+inline Tensor unsqueeze(const Tensor& t, int pos, bool as_dist = false) {  // ops.hpp:248
+  qtnh_tensor_t o;
+  check(qtnh_unsqueeze(t.h(), pos, as_dist ? 1 : 0, &o));
   return wrap(o, &t.ctx());
 }
 inline Tensor conj(const Tensor& t) {  // ops.hpp:147
@@ -881,6 +1139,12 @@ inline void apply(Tensor& state, const std::vector<int>& targets, const std::vec
                   bool diagonal = false) {
   check(qtnh_gate_apply(state.h(), static_cast<int>(targets.size()), targets.data(),
                         reinterpret_cast<const double*>(gate.data()), diagonal ? 1 : 0));
+}
+/// The gate as a replicated tensor (outputs; inputs) of any variant: a diagonal gate
+/// runs the diagonal kernel from its stored diagonal (no exchange even on distributed
+/// targets), an identity does nothing, a swap exchanges the two targets.
+inline void apply(Tensor& state, const std::vector<int>& targets, const Tensor& gate) {
+  check(qtnh_gate_apply_tensor(state.h(), static_cast<int>(targets.size()), targets.data(), gate.h()));
 }
 inline void swap_indices(Tensor& state, int a, int b) { check(qtnh_swap_indices(state.h(), a, b)); }
 inline void qft(Tensor& state, bool swaps = true) { check(qtnh_qft(state.h(), swaps ? 1 : 0)); }

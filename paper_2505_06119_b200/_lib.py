@@ -72,6 +72,15 @@ _SIGS = {
     "qtnh_tensor_to_global": (i32, [vp, vp]),
     "qtnh_tensor_paired": (i32, [vp, i32, P_i64, i32, P_i64, i32, P_i32, P_i32, i32, C.POINTER(vp)]),
     "qtnh_tensor_diagonal": (i32, [vp, i32, P_i64, i32, P_i64, vp, i64, C.POINTER(vp)]),
+    "qtnh_tensor_symmetric": (i32, [vp, i32, P_i64, i32, P_i64, vp, i64, i32, C.POINTER(vp)]),
+    "qtnh_tensor_variant": (i32, [vp]),
+    "qtnh_tensor_stored_size": (i64, [vp]),
+    "qtnh_tensor_pairs": (i32, [vp, P_i32, P_i32]),
+    "qtnh_tensor_to_dense": (i32, [vp, C.POINTER(vp)]),
+    "qtnh_tensor_local_element": (i32, [vp, P_i64, vp]),
+    "qtnh_squeeze": (i32, [vp, i32, C.POINTER(vp)]),
+    "qtnh_unsqueeze": (i32, [vp, i32, i32, C.POINTER(vp)]),
+    "qtnh_gate_apply_tensor": (i32, [vp, i32, P_i32, vp]),
     "qtnh_tensor_save": (i32, [vp, C.c_char_p]),
     "qtnh_tensor_load": (i32, [vp, C.c_char_p, C.POINTER(vp)]),
     "qtnh_permute": (i32, [vp, P_i32, i32, C.POINTER(vp)]),

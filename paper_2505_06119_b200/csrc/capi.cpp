@@ -48,10 +48,35 @@ RankCtx& ctx_of(qtnh_rank_t r) {
   return *r->ctx;
 }
 
-TP& impl_of(qtnh_tensor_t t) {
+// The tensor as constructed (any storage variant).
+TP& raw_of(qtnh_tensor_t t) {
   need(t, "tensor");
   t->impl->rank->activate();
   return t->impl;
+}
+
+// The tensor as the structural ops, contraction and factorisation see it: dense.
+// The reference's ops call to_dense() on the other variants (ops.hpp:128, :143,
+// :178, ...; remap.hpp:75-95 visits their non-zeros); here the dense block is
+// materialised on the device on first use and kept with the handle.
+TP& impl_of(qtnh_tensor_t t) {
+  TP& p = raw_of(t);
+  if (p->variant == kDense) return p;
+  if (!t->dense) t->dense = variant_to_dense(p);
+  return t->dense;
+}
+
+// Before an in-place update: the handle becomes its dense value.
+TP& dense_in_place(qtnh_tensor_t t) {
+  TP& p = raw_of(t);
+  if (p->variant != kDense) {
+    TP d = t->dense ? t->dense : variant_to_dense(p);
+    t->dense.reset();
+    if (p->variant == kSymmetric) d = std::make_shared<TensorImpl>(*d);  // own tag, shared block
+    d->variant = kDense;
+    p = d;
+  }
+  return p;
 }
 
 qtnh_tensor_t wrap(TP p) {
@@ -64,6 +89,18 @@ Shape shape_from(int n, const int64_t* dims, int split) {
   if (n < 0) throw_invalid("negative tensor rank");
   if (n > 0) need(dims, "dims");
   return Shape(std::vector<Dim>(dims, dims + n), split);
+}
+
+// Copy-on-write before an in-place update: other handles must not see it.
+void make_exclusive(TP& p) {
+  if (p->in_span && (p.use_count() > 1 || (p->buf && p->buf.use_count() > 1))) {
+    TP c = make_tensor(*p->rank, p->shape, p->dist, true);
+    QTNH_CUDA(cudaMemcpyAsync(c->data(), p->data(), p->shape.local_size() * 16, cudaMemcpyDeviceToDevice,
+                              p->rank->stream));
+    p = c;
+  } else if (!p->in_span && p.use_count() > 1) {
+    p = make_tensor(*p->rank, p->shape, p->dist, false);
+  }
 }
 
 long env_timeout() {
@@ -468,7 +505,7 @@ int qtnh_tensor_rank(qtnh_tensor_t t) { return t ? t->impl->shape.n_idx() : -1; 
 int qtnh_tensor_dims(qtnh_tensor_t t, int64_t* dims) {
   return guard([&] {
     need(t, "tensor");
-    need(dims, "dims");
+    if (t->impl->shape.n_idx() > 0) need(dims, "dims");  // a rank-0 scalar has none
     for (int i = 0; i < t->impl->shape.n_idx(); ++i) dims[i] = t->impl->shape.dims[i];
   });
 }
@@ -491,32 +528,33 @@ void* qtnh_tensor_device_ptr(qtnh_tensor_t t) { return t ? t->impl->data() : nul
 
 int qtnh_tensor_download_local(qtnh_tensor_t t, double* host) {
   return guard([&] {
-    TP& p = impl_of(t);
-    if (!p->in_span) return;
+    TP& p = raw_of(t);
+    const Dim n = stored_count(*p);
+    if (n == 0) return;
     need(host, "host");
-    QTNH_CUDA(cudaMemcpyAsync(host, p->data(), p->shape.local_size() * 16, cudaMemcpyDeviceToHost,
-                              p->rank->stream));
+    QTNH_CUDA(cudaMemcpyAsync(host, p->data(), n * 16, cudaMemcpyDeviceToHost, p->rank->stream));
     QTNH_CUDA(cudaStreamSynchronize(p->rank->stream));
   });
 }
 
 int qtnh_tensor_download_local_async(qtnh_tensor_t t, double* host) {
   return guard([&] {
-    TP& p = impl_of(t);
-    if (!p->in_span) return;
+    TP& p = raw_of(t);
+    const Dim n = stored_count(*p);
+    if (n == 0) return;
     need(host, "host");
-    QTNH_CUDA(cudaMemcpyAsync(host, p->data(), p->shape.local_size() * 16, cudaMemcpyDeviceToHost,
-                              p->rank->stream));
+    QTNH_CUDA(cudaMemcpyAsync(host, p->data(), n * 16, cudaMemcpyDeviceToHost, p->rank->stream));
   });
 }
 
 int qtnh_tensor_upload_local(qtnh_tensor_t t, const double* host) {
   return guard([&] {
-    TP& p = impl_of(t);
-    if (!p->in_span) return;
+    TP& p = raw_of(t);
+    const Dim n = stored_count(*p);
+    if (n == 0) return;
     need(host, "host");
-    QTNH_CUDA(cudaMemcpyAsync(p->data(), host, p->shape.local_size() * 16, cudaMemcpyHostToDevice,
-                              p->rank->stream));
+    t->dense.reset();
+    QTNH_CUDA(cudaMemcpyAsync(p->data(), host, n * 16, cudaMemcpyHostToDevice, p->rank->stream));
   });
 }
 
@@ -538,36 +576,10 @@ int qtnh_tensor_paired(qtnh_rank_t r, int n, const int64_t* dims, int split, con
       need(in_pos, "in_pos");
       need(out_pos, "out_pos");
     }
-    if (crossed && n_pairs != 2) throw_invalid("swap pairs exactly two indices");
-    std::vector<int> in(in_pos, in_pos + n_pairs), outp(out_pos, out_pos + n_pairs);
-    std::vector<char> used(n, 0);
-    auto chk = [&](int p) {
-      if (p < 0 || p >= n || used[p]) throw_invalid("invalid index pairing");
-      used[p] = 1;
-    };
-    for (int p : in) chk(p);
-    for (int p : outp) chk(p);
-    if (2 * n_pairs != n) throw_invalid("every index must belong to exactly one pair");
-    std::vector<int> eq_out = outp;
-    if (crossed) std::swap(eq_out[0], eq_out[1]);
-    for (int k = 0; k < n_pairs; ++k)
-      if (s.dims[in[k]] != s.dims[eq_out[k]]) throw_invalid("paired indices must have equal dimensions");
-    TP t = make_tensor(x, s, dist ? dist_from(dist) : Dist{}, true);
-    if (t->in_span) fill_paired(t->data(), t->shape.local_size(), t->block, t->shape.dims, t->shape.split, in, eq_out, x.stream);
-    *out = wrap(t);
+    *out = wrap(make_paired(x, s, dist ? dist_from(dist) : Dist{}, std::vector<int>(in_pos, in_pos + n_pairs),
+                            std::vector<int>(out_pos, out_pos + n_pairs), crossed != 0));
   });
 }
-
-namespace {
-void check_symmetric_shape(const Shape& s) {  // tensor.hpp:479-489
-  const int split = s.split, nl = s.n_idx() - s.split;
-  if (split % 2 != 0 || nl % 2 != 0) throw_invalid("symmetric tensors split both index groups in half");
-  for (int i = 0; i < split / 2; ++i)
-    if (s.dims[i] != s.dims[split / 2 + i]) throw_invalid("symmetric distributed dimensions differ");
-  for (int i = 0; i < nl / 2; ++i)
-    if (s.dims[split + i] != s.dims[split + nl / 2 + i]) throw_invalid("symmetric local dimensions differ");
-}
-}  // namespace
 
 int qtnh_tensor_diagonal(qtnh_rank_t r, int n, const int64_t* dims, int split, const int64_t* dist,
                          const double* diag_global, int64_t count, qtnh_tensor_t* out) {
@@ -576,41 +588,109 @@ int qtnh_tensor_diagonal(qtnh_rank_t r, int n, const int64_t* dims, int split, c
     RankCtx& x = ctx_of(r);
     Shape s = shape_from(n, dims, split);
     check_symmetric_shape(s);
-    Dim nd_in = 1, nl_in = 1;
-    for (int i = 0; i < split / 2; ++i) nd_in *= s.dims[i];
-    const int nl = n - split;
-    for (int i = 0; i < nl / 2; ++i) nl_in *= s.dims[split + i];
-    if (count != nd_in * nl_in) throw_invalid("diagonal payload has wrong length");
-    if (count) need(diag_global, "diag_global");
-    TP t = make_tensor(x, s, dist ? dist_from(dist) : Dist{}, true);
+    if (count < 0 && !diag_global) {  // zero diagonal of the right length (Tensor::adopt)
+      count = diag_local_count(s);
+      for (int i = 0; i < s.split / 2; ++i) count *= s.dims[i];
+    }
+    *out = wrap(make_diagonal(x, s, dist ? dist_from(dist) : Dist{}, diag_global, count));
+  });
+}
+
+int qtnh_tensor_symmetric(qtnh_rank_t r, int n, const int64_t* dims, int split, const int64_t* dist,
+                          const double* data, int64_t count, int is_global, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    RankCtx& x = ctx_of(r);
+    Shape s = shape_from(n, dims, split);
+    check_symmetric_shape(s);  // tensor.hpp:99, :107: the layout is validated first
+    if (data && is_global && count != s.total_size()) throw_invalid("global element count mismatch");
+    TP t = make_tensor(x, s, dist_from(dist), true);
+    t->variant = kSymmetric;
     if (t->in_span) {
-      fill_zero(t->data(), t->shape.local_size(), x.stream);
-      auto dc = unflat(t->block, t->shape.dist_dims());
-      const int k = split / 2;
-      bool on_diag = true;
-      for (int i = 0; i < k; ++i) on_diag &= dc[i] == dc[k + i];
-      if (on_diag && nl_in > 0) {
-        Dim b_in = flat(std::vector<Dim>(dc.begin(), dc.begin() + k),
-                        std::vector<Dim>(s.dims.begin(), s.dims.begin() + k));
-        DevBuf tmp(static_cast<size_t>(nl_in) * 16, x);
-        QTNH_CUDA(cudaMemcpyAsync(tmp.ptr, diag_global + 2 * b_in * nl_in, nl_in * 16, cudaMemcpyHostToDevice,
-                                  x.stream));
-        CopyBox b;  // local block (in, out) row-major: diagonal at j * (nl_in + 1)
-        b.dims = {nl_in};
-        b.in_stride = {1};
-        b.out_stride = {nl_in + 1};
-        strided_copy(tmp.ptr, t->data(), b, false, x.stream);
-        QTNH_CUDA(cudaStreamSynchronize(x.stream));  // host payload and staging die here
+      const Dim nl = t->shape.local_size();
+      if (!data) {  // zero block (Tensor::adopt)
+        fill_zero(t->data(), nl, x.stream);
+      } else if (!is_global && count != nl) {
+        throw_invalid("dense local data has " + std::to_string(count) + " elements, expected " + std::to_string(nl));
+      } else if (nl > 0) {
+        QTNH_CUDA(cudaMemcpyAsync(t->data(), data + (is_global ? 2 * t->block * nl : 0), nl * 16,
+                                  cudaMemcpyHostToDevice, x.stream));
+        QTNH_CUDA(cudaStreamSynchronize(x.stream));
       }
     }
     *out = wrap(t);
   });
 }
 
+int qtnh_tensor_variant(qtnh_tensor_t t) { return t ? t->impl->variant : -1; }
+int64_t qtnh_tensor_stored_size(qtnh_tensor_t t) { return t ? stored_count(*t->impl) : -1; }
+
+int qtnh_tensor_pairs(qtnh_tensor_t t, int* in_pos, int* out_pos) {
+  return guard([&] {
+    TP& p = raw_of(t);
+    for (size_t i = 0; i < p->pair_in.size(); ++i) {
+      if (in_pos) in_pos[i] = p->pair_in[i];
+      if (out_pos) out_pos[i] = p->pair_out[i];
+    }
+  });
+}
+
+int qtnh_tensor_to_dense(qtnh_tensor_t t, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    TP d = impl_of(t);
+    if (d->variant != kDense) {  // never the case; keep the tag honest
+      d = std::make_shared<TensorImpl>(*d);
+      d->variant = kDense;
+    }
+    *out = wrap(d);
+  });
+}
+
+int qtnh_tensor_local_element(qtnh_tensor_t t, const int64_t* coords, double* out2) {
+  return guard([&] {
+    need(out2, "out");
+    TP& p = raw_of(t);
+    const int n = p->shape.n_idx();
+    if (n) need(coords, "coords");
+    variant_local_element(*p, std::vector<Dim>(coords, coords + n), out2);
+  });
+}
+
+int qtnh_squeeze(qtnh_tensor_t t, int pos, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    const Shape& rs = raw_of(t)->shape;
+    if (pos < 0 || pos >= rs.n_idx() || rs.dims[pos] != 1) throw_invalid("squeeze needs a size-1 index");
+    TP& p = impl_of(t);
+    std::vector<Dim> dims = p->shape.dims;
+    dims.erase(dims.begin() + pos);
+    auto q = std::make_shared<TensorImpl>(*p);  // flat layouts ignore unit dimensions (ops.hpp:234-244)
+    q->shape = Shape(dims, p->shape.split - (pos < p->shape.split ? 1 : 0));
+    *out = wrap(q);
+  });
+}
+
+int qtnh_unsqueeze(qtnh_tensor_t t, int pos, int as_dist, qtnh_tensor_t* out) {
+  return guard([&] {
+    need(out, "out");
+    const Shape& rs = raw_of(t)->shape;
+    if (pos < 0 || pos > rs.n_idx()) throw_invalid("unsqueeze position out of range");
+    if (as_dist && pos > rs.split) throw_invalid("distributed index must precede the split");
+    if (!as_dist && pos < rs.split) throw_invalid("local index must follow the split");
+    TP& p = impl_of(t);
+    std::vector<Dim> dims = p->shape.dims;
+    dims.insert(dims.begin() + pos, 1);
+    auto q = std::make_shared<TensorImpl>(*p);
+    q->shape = Shape(dims, p->shape.split + (as_dist ? 1 : 0));
+    *out = wrap(q);
+  });
+}
+
 int qtnh_tensor_save(qtnh_tensor_t t, const char* path) {
   return guard([&] {
     need(path, "path");
-    op_save(*impl_of(t), path);
+    op_save(*raw_of(t), path);
   });
 }
 
@@ -657,7 +737,7 @@ int qtnh_permute(qtnh_tensor_t t, const int* perm, int new_split, qtnh_tensor_t*
 int qtnh_rebcast(qtnh_tensor_t t, const int64_t* nd, qtnh_tensor_t* out) {
   return guard([&] {
     need(out, "out");
-    *out = wrap(op_rebcast(impl_of(t), dist_from(nd)));
+    *out = wrap(variant_rebcast(raw_of(t), dist_from(nd)));
   });
 }
 
@@ -734,14 +814,14 @@ int qtnh_pad_local_dims(qtnh_tensor_t t, const int64_t* nl, qtnh_tensor_t* out) 
 int qtnh_conj(qtnh_tensor_t t, qtnh_tensor_t* out) {
   return guard([&] {
     need(out, "out");
-    *out = wrap(op_scale(impl_of(t), 1.0, 0.0, true));
+    *out = wrap(variant_scale(raw_of(t), 1.0, 0.0, true));
   });
 }
 
 int qtnh_scale(qtnh_tensor_t t, double re, double im, qtnh_tensor_t* out) {
   return guard([&] {
     need(out, "out");
-    *out = wrap(op_scale(impl_of(t), re, im, false));
+    *out = wrap(variant_scale(raw_of(t), re, im, false));
   });
 }
 
@@ -759,7 +839,7 @@ int qtnh_scale_index(qtnh_tensor_t t, int pos, const double* factors, qtnh_tenso
 int qtnh_tensor_clone(qtnh_tensor_t t, qtnh_tensor_t* out) {
   return guard([&] {
     need(out, "out");
-    *out = wrap(impl_of(t));
+    *out = wrap(raw_of(t));
   });
 }
 
@@ -824,7 +904,7 @@ int qtnh_contract(qtnh_tensor_t a, qtnh_tensor_t b, int n_pairs, const int* a_po
 
 int qtnh_gate_apply(qtnh_tensor_t state, int n_targets, const int* targets, const double* gate, int diagonal) {
   return guard([&] {
-    TP& p = impl_of(state);
+    TP& p = dense_in_place(state);
     if (n_targets < 1) throw_invalid("gate needs at least one target");
     need(targets, "targets");
     need(gate, "gate");
@@ -841,24 +921,64 @@ int qtnh_gate_apply(qtnh_tensor_t state, int n_targets, const int* targets, cons
   });
 }
 
-namespace {
-// Copy-on-write before an in-place update: other handles must not see it.
-void make_exclusive(TP& p) {
-  if (p->in_span && (p.use_count() > 1 || (p->buf && p->buf.use_count() > 1))) {
-    TP c = make_tensor(*p->rank, p->shape, p->dist, true);
-    QTNH_CUDA(cudaMemcpyAsync(c->data(), p->data(), p->shape.local_size() * 16, cudaMemcpyDeviceToDevice,
-                              p->rank->stream));
-    p = c;
-  } else if (!p->in_span && p.use_count() > 1) {
-    p = make_tensor(*p->rank, p->shape, p->dist, false);
-  }
+int qtnh_gate_apply_tensor(qtnh_tensor_t state, int n_targets, const int* targets, qtnh_tensor_t gate) {
+  return guard([&] {
+    TP& g = raw_of(gate);
+    TP& st = raw_of(state);
+    if (n_targets < 1) throw_invalid("gate needs at least one target");
+    need(targets, "targets");
+    const Shape& gs = g->shape;
+    if (gs.split != 0 || g->dist.stretch * g->dist.cycles != st->rank->world->size || g->dist.offset != 0)
+      throw_invalid("gate tensors are replicated on every rank (split 0, DistParams{1, P, 0})");
+    if (gs.n_idx() != 2 * n_targets) throw_invalid("gate tensor needs one output and one input index per target");
+    Dim D = 1;
+    for (int i = 0; i < n_targets; ++i) {
+      if (targets[i] < 0 || targets[i] >= st->shape.n_idx()) throw_invalid("gate target out of range");
+      const Dim d = st->shape.dims[targets[i]];
+      if (gs.dims[i] != d || gs.dims[n_targets + i] != d) throw_invalid("gate dimensions do not match the targets");
+      D *= d;
+    }
+    if (g->variant == kIdentity || g->variant == kSwap) {
+      // element = 1 iff the paired coordinates agree: with (outputs; inputs) pairs the
+      // identity leaves the state alone and the swap exchanges the two targets.
+      bool plain = n_targets == static_cast<int>(g->pair_in.size());
+      for (int i = 0; plain && i < n_targets; ++i) {
+        const int a = std::min(g->pair_in[i], g->pair_out[i]), b = std::max(g->pair_in[i], g->pair_out[i]);
+        plain = a < n_targets && b == a + n_targets;
+      }
+      if (plain && g->variant == kIdentity) return;
+      if (plain && n_targets == 2) {
+        TP& p = dense_in_place(state);
+        make_exclusive(p);
+        op_swap_indices(p, targets[0], targets[1]);
+        return;
+      }
+    }
+    const bool diag = g->variant == kDiagonal;
+    const Dim n = diag ? D : D * D;
+    std::vector<double> host(static_cast<size_t>(2 * n));
+    TP& src = diag ? g : impl_of(gate);
+    QTNH_CUDA(cudaMemcpyAsync(host.data(), src->data(), n * 16, cudaMemcpyDeviceToHost, src->rank->stream));
+    QTNH_CUDA(cudaStreamSynchronize(src->rank->stream));
+    TP& p = dense_in_place(state);
+    make_exclusive(p);
+    op_gate_apply(p, std::vector<int>(targets, targets + n_targets), host.data(), diag);
+  });
 }
-}  // namespace
 
 int qtnh_tensor_make_mutable(qtnh_tensor_t t) {
   return guard([&] {
-    TP& p = impl_of(t);
-    make_exclusive(p);
+    TP& p = raw_of(t);  // the stored elements of any variant (tensor.hpp:178)
+    t->dense.reset();
+    if (p->variant == kDiagonal) {
+      if (p.use_count() > 1 || (p->buf && p->buf.use_count() > 1)) p = variant_scale(p, 1.0, 0.0, false);
+    } else if (p->variant == kIdentity || p->variant == kSwap) {
+      if (p.use_count() > 1) p = std::make_shared<TensorImpl>(*p);
+    } else {
+      const int var = p->variant;
+      make_exclusive(p);
+      p->variant = var;
+    }
     QTNH_CUDA(cudaStreamSynchronize(p->rank->stream));
   });
 }
@@ -997,7 +1117,7 @@ int qtnh_contract_host(qtnh_rank_t r, int na, const int64_t* dims_a, const doubl
 
 int qtnh_swap_indices(qtnh_tensor_t t, int a, int b) {
   return guard([&] {
-    TP& p = impl_of(t);
+    TP& p = dense_in_place(t);
     make_exclusive(p);
     op_swap_indices(p, a, b);
   });
@@ -1005,7 +1125,7 @@ int qtnh_swap_indices(qtnh_tensor_t t, int a, int b) {
 
 int qtnh_qft_layer(qtnh_tensor_t t, int j) {
   return guard([&] {
-    TP& p = impl_of(t);
+    TP& p = dense_in_place(t);
     make_exclusive(p);
     op_qft_layer(p, j);
   });
@@ -1048,7 +1168,7 @@ int qtnh_set_option(const char* name, double value) {
 
 int qtnh_qft(qtnh_tensor_t t, int swaps) {
   return guard([&] {
-    TP& p = impl_of(t);
+    TP& p = dense_in_place(t);
     make_exclusive(p);
     op_qft(p, swaps != 0);
   });

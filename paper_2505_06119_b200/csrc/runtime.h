@@ -153,6 +153,14 @@ struct TensorImpl {
   bool in_span = false;
   Dim block = 0, cycle = 0, slot = 0;
   std::shared_ptr<DevBuf> buf;
+  // tensor.hpp:28 storage variant: 0 dense, 1 symmetric (dense storage, half-split
+  // layout), 2 diagonal (buf = this block's slice of the diagonal, only on blocks
+  // whose input and output distributed coordinates agree), 3 identity / 4 swap
+  // (no storage; pair_in / pair_out as constructed). Everything outside
+  // variants.cpp and io.cpp sees dense tensors only (capi.cpp's impl_of
+  // materialises the compact ones on demand).
+  int variant = 0;
+  std::vector<int> pair_in, pair_out;
   bool canonical() const { return in_span && cycle == 0 && slot == 0; }
   Dim span() const { return dist.span(shape.dist_size()); }
   void* data() const { return buf ? buf->ptr : nullptr; }
@@ -163,6 +171,23 @@ struct TensorImpl {
 // `alloc` (uninitialised).
 std::shared_ptr<TensorImpl> make_tensor(RankCtx& r, Shape shape, Dist dist, bool alloc);
 std::vector<int> span_ranks(const TensorImpl& t);
+
+// ---- tensor variants (variants.cpp; tensor.hpp:95-164, :209-337, ops.hpp:54-161) ----
+enum { kDense = 0, kSymmetric = 1, kDiagonal = 2, kIdentity = 3, kSwap = 4 };
+void check_symmetric_shape(const Shape& s);                       // tensor.hpp:479-489
+Dim diag_local_count(const Shape& s);                             // elements of one block's diagonal slice
+bool diag_block_on_diagonal(const Shape& s, Dim block, Dim* in_block = nullptr);
+Dim stored_count(const TensorImpl& t);                            // elements buf holds (local_data().size())
+std::shared_ptr<TensorImpl> make_diagonal(RankCtx& r, Shape s, Dist d, const double* diag_global_host, Dim count);
+std::shared_ptr<TensorImpl> make_paired(RankCtx& r, Shape s, Dist d, const std::vector<int>& in_pos,
+                                        const std::vector<int>& out_pos, bool crossed);
+std::shared_ptr<TensorImpl> variant_to_dense(const std::shared_ptr<TensorImpl>& t);       // tensor.hpp:282-296
+std::shared_ptr<TensorImpl> variant_rebcast(const std::shared_ptr<TensorImpl>& t, Dist d); // ops.hpp:54-112
+std::shared_ptr<TensorImpl> variant_scale(const std::shared_ptr<TensorImpl>& t, double re, double im,
+                                          bool conj);                                      // ops.hpp:147-161
+// Tensor::local_element (tensor.hpp:209-247): value at global coordinates from this
+// rank's storage; InvalidArgument when a stored variant's block lives elsewhere.
+void variant_local_element(const TensorImpl& t, const std::vector<Dim>& coords, double* out2);
 std::vector<int> union_members(const std::vector<std::pair<Dim, Dim>>& spans);
 
 }  // namespace qtnhb
@@ -177,5 +202,6 @@ struct qtnh_rank_s {
 };
 struct qtnh_tensor_s {
   std::shared_ptr<qtnhb::TensorImpl> impl;
+  std::shared_ptr<qtnhb::TensorImpl> dense;  // dense view of a non-dense variant, built on first use
   std::atomic<int> refs{1};
 };

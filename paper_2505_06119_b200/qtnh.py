@@ -434,6 +434,10 @@ def _as_c128(v) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(v, dtype=np.complex128))
 
 
+# Tensor storage variants (tensor.hpp:28)
+DENSE, SYMMETRIC, DIAGONAL, IDENTITY, SWAP = 0, 1, 2, 3, 4
+
+
 class Tensor:
     """Dense distributed tensor value held in HBM (tensor.hpp:53-695)."""
 
@@ -480,7 +484,8 @@ class Tensor:
 
     @staticmethod
     def identity(rank: Rank, shape: IndexTuple, dist, in_pos: Sequence[int], out_pos: Sequence[int]) -> "Tensor":
-        """Tensor::identity (tensor.hpp:144-153), materialised densely on the device."""
+        """Tensor::identity (tensor.hpp:144-153): no storage, element = 1 iff the paired
+        coordinates agree; operations read it through its dense value (to_dense)."""
         h = C.c_void_p()
         check(lib.qtnh_tensor_paired(rank._h, shape.n_idx(), i64_array(shape.dims), shape.split,
                                      _dist(dist).as_array(), len(in_pos), i32_array(in_pos), i32_array(out_pos), 0,
@@ -498,11 +503,30 @@ class Tensor:
 
     @staticmethod
     def diagonal(rank: Rank, shape: IndexTuple, dist, diag_global) -> "Tensor":
-        """Tensor::diagonal (tensor.hpp:114-142), materialised densely on the device."""
+        """Tensor::diagonal (tensor.hpp:114-142): each on-diagonal block keeps its slice of
+        the diagonal in HBM; rebcast / conj / scale / save keep the variant."""
         d = _as_c128(diag_global)
         h = C.c_void_p()
         check(lib.qtnh_tensor_diagonal(rank._h, shape.n_idx(), i64_array(shape.dims), shape.split,
                                        _dist(dist).as_array(), d.ctypes.data, d.size, C.byref(h)))
+        return Tensor(rank, h)
+
+    @staticmethod
+    def symmetric(rank: Rank, shape: IndexTuple, dist, local_data) -> "Tensor":
+        """Tensor::symmetric (tensor.hpp:97-104): dense storage, half-split layout validated."""
+        d = _as_c128(local_data)
+        h = C.c_void_p()
+        check(lib.qtnh_tensor_symmetric(rank._h, shape.n_idx(), i64_array(shape.dims), shape.split,
+                                        _dist(dist).as_array(), d.ctypes.data, d.size, 0, C.byref(h)))
+        return Tensor(rank, h)
+
+    @staticmethod
+    def symmetric_from_global(rank: Rank, shape: IndexTuple, dist, global_data) -> "Tensor":
+        """Tensor::symmetric_from_global (tensor.hpp:106-112)."""
+        d = _as_c128(global_data)
+        h = C.c_void_p()
+        check(lib.qtnh_tensor_symmetric(rank._h, shape.n_idx(), i64_array(shape.dims), shape.split,
+                                        _dist(dist).as_array(), d.ctypes.data, d.size, 1, C.byref(h)))
         return Tensor(rank, h)
 
     @staticmethod
@@ -536,6 +560,29 @@ class Tensor:
     def local_size(self) -> int:
         return int(lib.qtnh_tensor_local_size(self._h))
 
+    def variant(self) -> int:
+        """Tensor::variant (tensor.hpp:174): DENSE, SYMMETRIC, DIAGONAL, IDENTITY or SWAP."""
+        return int(lib.qtnh_tensor_variant(self._h))
+
+    def equality_pairs(self):
+        """(equality_in(), equality_out()) of an identity / swap tensor (tensor.hpp:193-194)."""
+        n = self.shape().n_idx() // 2 if self.variant() in (IDENTITY, SWAP) else 0
+        a, b = i32_array([0] * n), i32_array([0] * n)
+        check(lib.qtnh_tensor_pairs(self._h, a, b))
+        return [a[i] for i in range(n)], [b[i] for i in range(n)]
+
+    def to_dense(self) -> "Tensor":
+        """Tensor::to_dense (tensor.hpp:282-296), materialised on the device."""
+        h = C.c_void_p()
+        check(lib.qtnh_tensor_to_dense(self._h, C.byref(h)))
+        return self._new(h)
+
+    def local_element(self, coords: Sequence[int]) -> complex:
+        """Tensor::local_element (tensor.hpp:209-247)."""
+        out = np.zeros(1, dtype=np.complex128)
+        check(lib.qtnh_tensor_local_element(self._h, i64_array(list(coords)), out.ctypes.data))
+        return complex(out[0])
+
     def device_ptr(self) -> int:
         return int(lib.qtnh_tensor_device_ptr(self._h) or 0)
 
@@ -544,7 +591,7 @@ class Tensor:
 
     # -- data ----------------------------------------------------------------------------
     def local_data(self) -> np.ndarray:
-        out = np.empty(self.local_size() if self.in_span() else 0, dtype=np.complex128)
+        out = np.empty(int(lib.qtnh_tensor_stored_size(self._h)), dtype=np.complex128)  # the stored elements
         if out.size:
             check(lib.qtnh_tensor_download_local(self._h, out.ctypes.data))
         return out
@@ -560,59 +607,22 @@ class Tensor:
     _MAGIC = b"QTNHTEN1"
 
     def save(self, path: str) -> None:
-        """Span-collective save in the reference's QTNHTEN1 format (dense variant):
+        """Span-collective save in the reference's QTNHTEN1 format, every variant:
         magic, u32 variant, u32 rank, u32 split, i64 stretch/cycles/offset, i64 dims,
-        u64 payload count, LE f64 (re, im) pairs in global row-major order. Every
-        canonical holder writes its block straight from HBM (qtnh_tensor_save)."""
+        then u64 payload count and LE f64 (re, im) pairs in global row-major order
+        (dense, symmetric), the diagonal in row-major order of the input coordinates
+        (diagonal), or u64 pair count and i64 (in, out) positions (identity, swap).
+        Every canonical holder writes its part straight from HBM (qtnh_tensor_save)."""
         check(lib.qtnh_tensor_save(self._h, os.fsencode(path)))
 
     @staticmethod
     def load(rank: "Rank", path: str) -> "Tensor":
-        """Read a QTNHTEN1 file (every rank reads it independently, tensor.hpp:399-440).
-        Dense and symmetric payloads go straight into HBM (qtnh_tensor_load);
-        diagonal, identity and swap variants are materialised densely on the device
-        by their constructors (tensor.hpp:282-296)."""
-        import struct
-
-        with open(path, "rb") as f:
-            head = f.read(12)
-        if head[:8] == Tensor._MAGIC and len(head) == 12 and struct.unpack_from("<I", head, 8)[0] in (0, 1):
-            # dense / symmetric payload: each rank reads only its block into HBM
-            h = C.c_void_p()
-            check(lib.qtnh_tensor_load(rank._h, os.fsencode(path), C.byref(h)))
-            return Tensor(rank, h)
-        with open(path, "rb") as f:
-            blob = f.read()
-        if blob[:8] != Tensor._MAGIC:
-            raise Error("not a qtnh tensor stream")
-        off = 8
-        try:
-            var, r, split = struct.unpack_from("<III", blob, off)
-            off += 12
-            st, cy, of = struct.unpack_from("<qqq", blob, off)
-            off += 24
-            dims = list(struct.unpack_from("<%dq" % r, blob, off))
-            off += 8 * r
-        except struct.error:
-            raise Error("truncated tensor stream")
-        shape = IndexTuple(dims, split)
-        dist = DistParams(st, cy, of)
-        if var in (3, 4):  # identity / swap: pairs (in, out) of positions, built on the device
-            (npairs,) = struct.unpack_from("<Q", blob, off)
-            off += 8
-            pr = struct.unpack_from("<%dq" % (2 * npairs), blob, off)
-            pin, pout = list(pr[0::2]), list(pr[1::2])
-            return (Tensor.swap_tensor if var == 4 else Tensor.identity)(rank, shape, dist, pin, pout)
-        (count,) = struct.unpack_from("<Q", blob, off)
-        off += 8
-        if len(blob) < off + 16 * count:
-            raise Error("truncated tensor stream")
-        payload = np.frombuffer(blob, dtype="<c16", count=count, offset=off).astype(np.complex128)
-        if var in (0, 1):
-            return Tensor.from_global(rank, shape, dist, payload)
-        if var == 2:  # diagonal over the half-split (in, out) layout, built on the device
-            return Tensor.diagonal(rank, shape, dist, payload)
-        raise Error("corrupt tensor stream")
+        """Read a QTNHTEN1 file (every rank reads it independently, tensor.hpp:399-440);
+        each rank reads only its block (or diagonal slice) into HBM and the variant is
+        restored."""
+        h = C.c_void_p()
+        check(lib.qtnh_tensor_load(rank._h, os.fsencode(path), C.byref(h)))
+        return Tensor(rank, h)
 
     def free(self) -> None:
         if self._h is not None:
@@ -635,6 +645,8 @@ class Tensor:
 class ops:  # namespace
     @staticmethod
     def permute(t: Tensor, perm: Sequence[int], new_split: int) -> Tensor:
+        if len(perm) != lib.qtnh_tensor_rank(t._h):
+            raise InvalidArgument("permutation size does not match tensor rank")
         h = C.c_void_p()
         check(lib.qtnh_permute(t._h, i32_array(perm), int(new_split), C.byref(h)))
         return t._new(h)
@@ -664,6 +676,20 @@ class ops:  # namespace
     def gather_index(t: Tensor, pos: int) -> Tensor:
         h = C.c_void_p()
         check(lib.qtnh_gather_index(t._h, int(pos), C.byref(h)))
+        return t._new(h)
+
+    @staticmethod
+    def squeeze(t: Tensor, pos: int) -> Tensor:
+        """ops::squeeze (ops.hpp:234-244): drop a size-1 index (metadata only)."""
+        h = C.c_void_p()
+        check(lib.qtnh_squeeze(t._h, int(pos), C.byref(h)))
+        return t._new(h)
+
+    @staticmethod
+    def unsqueeze(t: Tensor, pos: int, as_dist: bool = False) -> Tensor:
+        """ops::unsqueeze (ops.hpp:248-262): insert a size-1 index at pos."""
+        h = C.c_void_p()
+        check(lib.qtnh_unsqueeze(t._h, int(pos), int(bool(as_dist)), C.byref(h)))
         return t._new(h)
 
     @staticmethod
@@ -724,6 +750,14 @@ def apply_gate(state: Tensor, targets: Sequence[int], gate, diagonal: bool = Fal
     Values equal contract(state, gate) followed by a permute back."""
     g = _as_c128(gate)
     check(lib.qtnh_gate_apply(state._h, len(targets), i32_array(targets), g.ctypes.data, int(bool(diagonal))))
+    return state
+
+
+def apply_gate_tensor(state: Tensor, targets: Sequence[int], gate: Tensor) -> Tensor:
+    """In-place gate given as a replicated tensor (outputs; inputs) of any variant: a
+    DIAGONAL gate runs the diagonal kernel from its stored diagonal (no exchange even on
+    distributed targets), IDENTITY does nothing, a two-target SWAP exchanges the indices."""
+    check(lib.qtnh_gate_apply_tensor(state._h, len(targets), i32_array(targets), gate._h))
     return state
 
 
