@@ -52,3 +52,13 @@ def peer_mode(request):
     check(lib.qtnh_set_option(b"peer_direct", float(request.param)))
     yield request.param
     check(lib.qtnh_set_option(b"peer_direct", 1.0))
+
+
+@pytest.fixture(autouse=True)
+def _restore_process_wide_options():
+    """Options set through qtnh_set_option are process-wide; a test that leaves
+    "pool_reserve_gb" set makes every later world map (and trim) that much HBM."""
+    yield
+    mod = sys.modules.get("paper_2505_06119_b200.qtnh")
+    if mod is not None:
+        mod.lib.qtnh_set_option(b"pool_reserve_gb", 0.0)

@@ -41,8 +41,13 @@ def test_c3_full_network_vs_host_replay():
         net.tensors[last].free()
         return np.transpose(amp, [res_labels.index(x) for x in open_labels]).reshape(-1)
 
+    # Map the pool once for this network only: left set, every later world of the
+    # process would map 120 GB at creation and trim it at destruction (~2 s a world).
     qtnh.check(qtnh.lib.qtnh_set_option(b"pool_reserve_gb", 120.0))
-    got = World(1).run(body)[0]
+    try:
+        got = World(1).run(body)[0]
+    finally:
+        qtnh.check(qtnh.lib.qtnh_set_option(b"pool_reserve_gb", 0.0))
     want, wl = oracle.network_contract(items, order)
     want = np.transpose(want, [wl.index(x) for x in open_labels]).reshape(-1)
     assert rel_l2(got, want) < TOL

@@ -1,4 +1,6 @@
 """GPU parity of gate application and the QFT workloads (configs 0 and 2)."""
+import functools
+
 import numpy as np
 import pytest
 
@@ -210,6 +212,16 @@ def test_swap_indices_bit_exact(dims, split, a, b, world):
     assert np.array_equal(bits(got), bits(P.permute(dims, g, perm)))
 
 
+@functools.lru_cache(maxsize=None)
+def _oracle_qft_of_counter_state(n):
+    """The oracle's QFT of test_blocked_qft's seeded state: computed once per n (the
+    port takes ~10-20 s at n = 20-21 on the GPU box's host), shared by both
+    redistribution forms and every split."""
+    st = circuits.counter_state(23 + n, 2**n)
+    st /= np.linalg.norm(st)
+    return P.qft(n, st)
+
+
 @pytest.mark.parametrize("n,split,world", [(8, 0, 1), (11, 0, 1), (16, 0, 1), (20, 0, 1), (21, 0, 1), (14, 2, 4), (13, 3, 8),
                                           (6, 3, 8), (7, 3, 8), (8, 3, 8), (9, 1, 2), (20, 3, 8), (19, 2, 4)])
 def test_blocked_qft(n, split, world, peer_mode):
@@ -224,7 +236,7 @@ def test_blocked_qft(n, split, world, peer_mode):
         return t.to_global_vector()
 
     got = World(world).run(body)[0]
-    assert rel_l2(got, P.qft(n, st)) < TOL
+    assert rel_l2(got, _oracle_qft_of_counter_state(n)) < TOL
     if n <= 16:
         def body2(rk):
             t = Tensor.from_global(rk, IndexTuple([2] * n, split), DistParams(1, 1, 0), st)
