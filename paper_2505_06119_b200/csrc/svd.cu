@@ -1153,7 +1153,18 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
     bool done = false;
     bool cross = false;  // this sweep uses cross Grams
     int sweeps = 0;
+    cudaGraphExec_t exec[2] = {nullptr, nullptr};  // captured sweep: full / cross Gram form
   };
+  // QTNH_SVD_GRAPH (default 1): replay each group's sweep as a CUDA graph when it is
+  // long enough to pay for the capture (>= 31 rounds: 512 rows and up). A captured
+  // sweep never runs on the caller's stream (it may be the legacy default stream, which
+  // cannot be captured): a single group then takes a group stream too.
+  static const bool graph_env = [] {
+    const char* e = std::getenv("QTNH_SVD_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  const bool use_graph = graph_env && rounds >= 31 && !sort_rows;
+  const bool own_streams = ngroups > 1 || use_graph;
   std::vector<Group> grp(ngroups);
   std::vector<cudaEvent_t> evs(ngroups + 1);
   for (auto& e : evs) QTNH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1162,7 +1173,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
     grp[g].base = g * batch / ngroups;
     grp[g].cnt = (g + 1) * batch / ngroups - grp[g].base;
     grp[g].cross = cross;
-    if (ngroups == 1) {
+    if (!own_streams) {
       grp[g].s = st;
     } else {
       grp[g].s = group_stream(r.device, g);
@@ -1182,13 +1193,19 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
       static_cast<unsigned>(std::min<Dim>((W + 31) / 32, std::max<Dim>(1, 8 * sms() / (npairs * gmax))));
   auto cleanup = [&] {
     for (int g = 0; g < ngroups; ++g) {
-      if (ngroups > 1) {
+      if (own_streams) {
         cudaEventRecord(evs[g], grp[g].s);
         cudaStreamWaitEvent(st, evs[g], 0);
       }
     }
     cudaStreamSynchronize(st);
     for (auto& e : evs) cudaEventDestroy(e);
+    for (auto& G : grp)
+      for (auto& ex : G.exec)
+        if (ex) {
+          cudaGraphExecDestroy(ex);
+          ex = nullptr;
+        }
   };
   int sweep = 0;
   try {
@@ -1253,9 +1270,8 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
               static_cast<int>(nblk2));
           QTNH_LAUNCH_CHECK();
         }
-      for (int rd = 0; rd < rounds; ++rd)
-        for (auto& G : grp) {
-          if (G.done) continue;
+      // One round of one group: Gram (or cross Gram) -> pair solves -> W^H update.
+      auto launch_round = [&](Group& G, int rd) {
           const unsigned cnt = static_cast<unsigned>(G.cnt);
           double2* wkg = wkp + G.base * rp * W;
           double2* partg = static_cast<double2*>(part.ptr) + G.base * npairs * splits * P2 * P2;
@@ -1292,7 +1308,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
               k_svd_update_v2<B><<<dim3(ctiles2, npairs, cnt), B * 8, upd2_smem, G.s>>>(
                   wkg, whg, flg, static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
               QTNH_LAUNCH_CHECK();
-              continue;
+              return;
             }
           }
           if (uc == 32)
@@ -1305,7 +1321,36 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
             k_svd_update_mma_t<B, 48><<<dim3(ctiles, npairs, cnt), B * 8, upd_smem, G.s>>>(
                 wkg, whg, flg, static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
           QTNH_LAUNCH_CHECK();
+      };
+      if (!use_graph) {
+        for (int rd = 0; rd < rounds; ++rd)
+          for (auto& G : grp)
+            if (!G.done) launch_round(G, rd);
+      } else {
+        // A sweep of one group is the same 3 x rounds kernels every time (only the
+        // thresholds in device memory change): captured once per (group, cross form)
+        // and replayed, so the sweep does not depend on the host's launch rate.
+        for (auto& G : grp) {
+          if (G.done) continue;
+          cudaGraphExec_t& ex = G.exec[G.cross ? 1 : 0];
+          if (!ex) {
+            cudaGraph_t graph = nullptr;
+            QTNH_CUDA(cudaStreamBeginCapture(G.s, cudaStreamCaptureModeThreadLocal));
+            try {
+              for (int rd = 0; rd < rounds; ++rd) launch_round(G, rd);
+            } catch (...) {
+              cudaStreamEndCapture(G.s, &graph);
+              if (graph) cudaGraphDestroy(graph);
+              throw;
+            }
+            QTNH_CUDA(cudaStreamEndCapture(G.s, &graph));
+            cudaError_t ie = cudaGraphInstantiate(&ex, graph, 0);
+            cudaGraphDestroy(graph);
+            QTNH_CUDA(ie);
+          }
+          QTNH_CUDA(cudaGraphLaunch(ex, G.s));
         }
+      }
       for (auto& G : grp)
         if (!G.done)
           QTNH_CUDA(cudaMemcpyAsync(off_h.data() + G.base, static_cast<double*>(offm.ptr) + G.base, G.cnt * 8,
