@@ -333,9 +333,14 @@ def measure_extras(rk, stream, torch):
     s = torch.empty((chi,), dtype=torch.float64, device="cuda")
     vh = torch.empty((chi, nn), dtype=torch.complex128, device="cuda")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    def svd_call(bt_):
+        qtnh.check(qtnh.lib.qtnh_svd_device(rk._h, bt_, nn, nn, C.c_void_p(a.data_ptr()), chi, 1,
+                                            C.c_void_p(u.data_ptr()), C.c_void_p(s.data_ptr()),
+                                            C.c_void_p(vh.data_ptr())))
+
+    svd_call(1)  # untimed warm-up (workspace mapping, module load, graph instantiation)
     e0.record(stream)
-    qtnh.check(qtnh.lib.qtnh_svd_device(rk._h, 1, nn, nn, C.c_void_p(a.data_ptr()), chi, 1, C.c_void_p(u.data_ptr()),
-                                        C.c_void_p(s.data_ptr()), C.c_void_p(vh.data_ptr())))
+    svd_call(1)
     e1.record(stream)
     e1.synchronize()
     ms = e0.elapsed_time(e1)
@@ -350,9 +355,9 @@ def measure_extras(rk, stream, torch):
     u = torch.empty((bt, nn, chi), dtype=torch.complex128, device="cuda")
     s = torch.empty((bt, chi), dtype=torch.float64, device="cuda")
     vh = torch.empty((bt, chi, nn), dtype=torch.complex128, device="cuda")
+    svd_call(bt)  # untimed warm-up
     e0.record(stream)
-    qtnh.check(qtnh.lib.qtnh_svd_device(rk._h, bt, nn, nn, C.c_void_p(a.data_ptr()), chi, 1, C.c_void_p(u.data_ptr()),
-                                        C.c_void_p(s.data_ptr()), C.c_void_p(vh.data_ptr())))
+    svd_call(bt)
     e1.record(stream)
     e1.synchronize()
     ms = e0.elapsed_time(e1)
@@ -368,9 +373,9 @@ def measure_extras(rk, stream, torch):
     a = ((q1 * sv) @ q2.transpose(1, 2).conj()).contiguous()
     del q1, q2
     torch.cuda.synchronize()
+    svd_call(bt)  # untimed warm-up
     e0.record(stream)
-    qtnh.check(qtnh.lib.qtnh_svd_device(rk._h, bt, nn, nn, C.c_void_p(a.data_ptr()), chi, 1, C.c_void_p(u.data_ptr()),
-                                        C.c_void_p(s.data_ptr()), C.c_void_p(vh.data_ptr())))
+    svd_call(bt)
     e1.record(stream)
     e1.synchronize()
     ms = e0.elapsed_time(e1)

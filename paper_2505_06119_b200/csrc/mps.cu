@@ -21,6 +21,9 @@
 #include <map>
 #include <tuple>
 
+#include <exception>
+#include <thread>
+
 #include "ops.h"
 
 namespace qtnhb {
@@ -85,41 +88,49 @@ void mps_apply_layer(const std::vector<TP>& left, const std::vector<TP>& right, 
     if (a->shape.dims[2] != b->shape.dims[0]) throw_invalid("mps layer: bond dimensions of a pair differ");
     groups[Key{a->shape.dims[0], a->shape.dims[1], b->shape.dims[1], b->shape.dims[2]}].push_back(i);
   }
+  // Output sites first, on the caller's stream: the groups below may run on a second
+  // stream from a second host thread.
   for (auto& [key, idx] : groups) {
+    const auto [l, d1, d2, rr] = key;
+    const Dim keep = std::min(chi, std::min(l * d1, d2 * rr));
+    for (size_t i : idx) {
+      new_left[i] = make_tensor(r, Shape({l, d1, keep}, 0), left[i]->dist, true);
+      new_right[i] = make_tensor(r, Shape({keep, d2, rr}, 0), right[i]->dist, true);
+    }
+  }
+  auto run_group = [&](RankCtx& rc, const Key& key, const std::vector<size_t>& idx) {
     const auto [l, d1, d2, rr] = key;
     const Dim bsz = static_cast<Dim>(idx.size());
     const Dim m = l * d1, n = d2 * rr, k = std::min(m, n), keep = std::min(chi, k);
-    DevBuf theta(static_cast<size_t>(bsz * m * n) * 16, r);
+    DevBuf theta(static_cast<size_t>(bsz * m * n) * 16, rc);
     double2* th = static_cast<double2*>(theta.ptr);
     for (Dim j = 0; j < bsz; ++j) {
       const TP& a = left[idx[j]];
       const TP& b = right[idx[j]];
-      zgemm(a->data(), b->data(), th + j * m * n, m, n, a->shape.dims[2], r.stream);
+      zgemm(a->data(), b->data(), th + j * m * n, m, n, a->shape.dims[2], rc.stream);
     }
-    gate_local(th, {bsz * l, d1, d2, rr}, {1, 2}, gate, false, r.stream);
-    DevBuf part(static_cast<size_t>(bsz) * kFroParts * sizeof(double), r);
-    DevBuf nrm(static_cast<size_t>(bsz) * sizeof(double), r);
-    k_fro2_partial<<<dim3(kFroParts, static_cast<unsigned>(bsz)), 256, 0, r.stream>>>(th, m * n,
+    gate_local(th, {bsz * l, d1, d2, rr}, {1, 2}, gate, false, rc.stream);
+    DevBuf part(static_cast<size_t>(bsz) * kFroParts * sizeof(double), rc);
+    DevBuf nrm(static_cast<size_t>(bsz) * sizeof(double), rc);
+    k_fro2_partial<<<dim3(kFroParts, static_cast<unsigned>(bsz)), 256, 0, rc.stream>>>(th, m * n,
                                                                                      static_cast<double*>(part.ptr));
     QTNH_LAUNCH_CHECK();
-    k_fro2_final<<<static_cast<unsigned>(bsz), 256, 0, r.stream>>>(static_cast<const double*>(part.ptr), kFroParts,
+    k_fro2_final<<<static_cast<unsigned>(bsz), 256, 0, rc.stream>>>(static_cast<const double*>(part.ptr), kFroParts,
                                                                    static_cast<double*>(nrm.ptr));
     QTNH_LAUNCH_CHECK();
     std::vector<void*> up(bsz), vp(bsz);
     for (Dim j = 0; j < bsz; ++j) {
       const size_t i = idx[j];
-      new_left[i] = make_tensor(r, Shape({l, d1, keep}, 0), left[i]->dist, true);
-      new_right[i] = make_tensor(r, Shape({keep, d2, rr}, 0), right[i]->dist, true);
       up[j] = new_left[i]->data();
       vp[j] = new_right[i]->data();
     }
-    DevBuf s(static_cast<size_t>(bsz * keep) * sizeof(double), r);
+    DevBuf s(static_cast<size_t>(bsz * keep) * sizeof(double), rc);
     int sweeps = 0;
-    svd_batched_ptrs(r, bsz, m, n, th, keep, QTNH_ABSORB_LEFT, up.data(), s.ptr, vp.data(), &sweeps);
+    svd_batched_ptrs(rc, bsz, m, n, th, keep, QTNH_ABSORB_LEFT, up.data(), s.ptr, vp.data(), &sweeps);
     std::vector<double> sh(bsz * keep), nh(bsz);
-    QTNH_CUDA(cudaMemcpyAsync(sh.data(), s.ptr, sh.size() * sizeof(double), cudaMemcpyDeviceToHost, r.stream));
-    QTNH_CUDA(cudaMemcpyAsync(nh.data(), nrm.ptr, nh.size() * sizeof(double), cudaMemcpyDeviceToHost, r.stream));
-    QTNH_CUDA(cudaStreamSynchronize(r.stream));
+    QTNH_CUDA(cudaMemcpyAsync(sh.data(), s.ptr, sh.size() * sizeof(double), cudaMemcpyDeviceToHost, rc.stream));
+    QTNH_CUDA(cudaMemcpyAsync(nh.data(), nrm.ptr, nh.size() * sizeof(double), cudaMemcpyDeviceToHost, rc.stream));
+    QTNH_CUDA(cudaStreamSynchronize(rc.stream));
     for (Dim j = 0; j < bsz; ++j) {
       const size_t i = idx[j];
       if (s_out) {
@@ -129,7 +140,63 @@ void mps_apply_layer(const std::vector<TP>& left, const std::vector<TP>& right, 
       if (keep_out) keep_out[i] = keep;
       if (norm2_out) norm2_out[i] = nh[j];
     }
+  };
+  // The largest group (the saturated thetas: one batched SVD) runs here; the other
+  // shapes (the unsaturated pairs towards the chain's ends: single-matrix, latency-
+  // bound SVDs, ~20 % of a late config-4 layer when run one after the other) run
+  // concurrently on a side stream from a second host thread -- the pairs of a layer
+  // are disjoint, so the results do not depend on the interleaving
+  // (QTNH_MPS_OVERLAP=0: one after the other).
+  static const bool overlap = [] {
+    const char* e = std::getenv("QTNH_MPS_OVERLAP");
+    return !(e && e[0] == '0');
+  }();
+  const Key* big = nullptr;
+  double big_work = -1.0;
+  for (auto& [key, idx] : groups) {
+    const auto [l, d1, d2, rr] = key;
+    const double w = static_cast<double>(idx.size()) * double(l * d1) * double(d2 * rr) * double(std::min(l * d1, d2 * rr));
+    if (w > big_work) {
+      big_work = w;
+      big = &key;
+    }
   }
+  if (!overlap || groups.size() < 2 || big_work < 1e9) {
+    for (auto& [key, idx] : groups) run_group(r, key, idx);
+    return;
+  }
+  RankCtx side;  // same rank and device, its own launch stream; owns nothing
+  side.world = r.world;
+  side.rank = r.rank;
+  side.device = r.device;
+  side.stream = r.side_stream(0);
+  cudaEvent_t ev = nullptr;
+  QTNH_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  QTNH_CUDA(cudaEventRecord(ev, r.stream));
+  QTNH_CUDA(cudaStreamWaitEvent(side.stream, ev, 0));
+  std::exception_ptr side_err;
+  std::thread worker([&] {
+    try {
+      side.activate();
+      for (auto& [key, idx] : groups)
+        if (&key != big) run_group(side, key, idx);
+    } catch (...) {
+      side_err = std::current_exception();
+    }
+  });
+  std::exception_ptr main_err;
+  try {
+    run_group(r, *big, groups.at(*big));
+  } catch (...) {
+    main_err = std::current_exception();
+  }
+  worker.join();
+  cudaEventRecord(ev, side.stream);
+  cudaStreamWaitEvent(r.stream, ev, 0);
+  cudaEventDestroy(ev);
+  side.stream = nullptr;
+  if (main_err) std::rethrow_exception(main_err);
+  if (side_err) std::rethrow_exception(side_err);
 }
 
 }  // namespace qtnhb

@@ -940,8 +940,17 @@ int block_rows() {
 
 // Per-matrix streams of the batch split (QTNH_SVD_GROUPS), created once per host
 // thread and device (rank threads are long-lived) instead of on every call.
+struct GroupStreams {  // destroyed with the host thread (short-lived helper threads included)
+  std::vector<std::vector<cudaStream_t>> per_device;
+  ~GroupStreams() {
+    for (auto& d : per_device)
+      for (cudaStream_t st : d) cudaStreamDestroy(st);
+  }
+};
+
 cudaStream_t group_stream(int device, int g) {
-  thread_local std::vector<std::vector<cudaStream_t>> cache;
+  thread_local GroupStreams gs;
+  auto& cache = gs.per_device;
   if (static_cast<int>(cache.size()) <= device) cache.resize(device + 1);
   auto& v = cache[device];
   while (static_cast<int>(v.size()) <= g) {
