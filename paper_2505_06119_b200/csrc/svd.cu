@@ -1061,9 +1061,10 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
   }();
   int splits = static_cast<int>(std::max<Dim>(
       1, std::min<Dim>((gram_ctas * sms() + npairs * per_group - 1) / (npairs * per_group), (L + kGramCols - 1) / kGramCols)));
-  // de Rijk ordering (QTNH_SVD_SORT=1): rows sorted by descending norm before every
+  // de Rijk ordering (QTNH_SVD_SORT): rows sorted by descending norm before every
   // sweep (one gather of WK per sweep). 2048^2 random: 17 -> 14 sweeps, 8-decade
-  // graded 320^2: 33 -> 23; but the C4 MPS thetas: ~32 -> ~42, so it is off by default.
+  // graded 320^2: 33 -> 23; the two-valued C4 thetas got worse with it (~32 -> ~42)
+  // while they still took the Jacobi.
   // QTNH_SVD_PAIR_SORT=1: order each pair's new rows by norm (see k_svd_eigen_t):
   // graded 320^2 33 -> 24 sweeps, but no gain on the C4 thetas (41 -> 40) and slower
   // per sweep on random inputs, so off by default.
@@ -1071,14 +1072,18 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
     const char* e = std::getenv("QTNH_SVD_PAIR_SORT");
     return e && e[0] == '1';
   }();
+  // On by default since the C4 thetas with clustered spectra take the spectral-split
+  // path: config 4 (sorted everywhere) 4.33 -> 4.21 s, one random 2048^2 16 -> 13
+  // sweeps; QTNH_SVD_SORT=0 turns it off.
   static const bool sort_rows = [] {
     const char* e = std::getenv("QTNH_SVD_SORT");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   DevBuf wk(static_cast<size_t>(batch * rp * W) * 16, r);
   DevBuf wk2(sort_rows ? static_cast<size_t>(batch * rp * W) * 16 : 16, r);
   double2* wkp = static_cast<double2*>(wk.ptr);
   double2* wkq = static_cast<double2*>(wk2.ptr);
+  const double2* const wk_first = wkp;
   DevBuf rnorm(static_cast<size_t>(batch * rp) * sizeof(double), r);
   DevBuf rperm(static_cast<size_t>(batch * rp) * sizeof(int), r);
   std::vector<double> rn_h(sort_rows ? batch * rp : 0);
@@ -1166,17 +1171,21 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
     bool done = false;
     bool cross = false;  // this sweep uses cross Grams
     int sweeps = 0;
-    cudaGraphExec_t exec[2] = {nullptr, nullptr};  // captured sweep: full / cross Gram form
+    cudaGraphExec_t exec[4] = {nullptr, nullptr, nullptr, nullptr};  // captured sweep: (full / cross Gram) x work buffer
   };
-  // QTNH_SVD_GRAPH (default 1): replay each group's sweep as a CUDA graph when it is
-  // long enough to pay for the capture (>= 31 rounds: 512 rows and up). A captured
-  // sweep never runs on the caller's stream (it may be the legacy default stream, which
-  // cannot be captured): a single group then takes a group stream too.
+  // QTNH_SVD_GRAPH (default 1): a single-group call (one matrix, or QTNH_SVD_GROUPS=1)
+  // replays its sweeps as a CUDA graph from the third sweep on when a sweep is long
+  // enough to pay for the capture (>= 31 rounds: 512 rows and up): one 2048^2 SVD
+  // 154 -> 149 ms. Batches split over several group streams keep the launched form:
+  // the host's round-by-round interleaving of the groups staggers them better than
+  // whole-sweep graphs do (config 4: 4.33 s launched, 4.41 s replayed). A captured
+  // sweep never runs on the caller's stream (it may be the legacy default stream,
+  // which cannot be captured): it takes a group stream.
   static const bool graph_env = [] {
     const char* e = std::getenv("QTNH_SVD_GRAPH");
     return !(e && e[0] == '0');
   }();
-  const bool use_graph = graph_env && rounds >= 31 && !sort_rows;
+  const bool use_graph = graph_env && rounds >= 31 && ngroups == 1;
   const bool own_streams = ngroups > 1 || use_graph;
   std::vector<Group> grp(ngroups);
   std::vector<cudaEvent_t> evs(ngroups + 1);
@@ -1335,7 +1344,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
                 wkg, whg, flg, static_cast<const int*>(d_tab.ptr), rd, npairs, rp, L, qw);
           QTNH_LAUNCH_CHECK();
       };
-      if (!use_graph) {
+      if (!use_graph || sweep < 2) {  // calls that converge in 2-3 sweeps never pay for a capture
         for (int rd = 0; rd < rounds; ++rd)
           for (auto& G : grp)
             if (!G.done) launch_round(G, rd);
@@ -1345,7 +1354,7 @@ void svd_impl(RankCtx& r, Dim batch, Dim m, Dim n, const void* a, Dim chi, int a
         // and replayed, so the sweep does not depend on the host's launch rate.
         for (auto& G : grp) {
           if (G.done) continue;
-          cudaGraphExec_t& ex = G.exec[G.cross ? 1 : 0];
+          cudaGraphExec_t& ex = G.exec[(G.cross ? 1 : 0) + (wkp == wk_first ? 0 : 2)];  // row sorting swaps the buffers
           if (!ex) {
             cudaGraph_t graph = nullptr;
             QTNH_CUDA(cudaStreamBeginCapture(G.s, cudaStreamCaptureModeThreadLocal));
