@@ -300,3 +300,23 @@ def test_svd_device_batch_null_completion():
         keep = 3 if i else chi
         assert np.allclose(s[:keep], S[:keep], rtol=1e-12)
         assert rel_l2((u * s) @ vh, (U[:, :chi] * S[:chi]) @ VH[:chi]) < TOL
+
+
+@pytest.mark.parametrize("m,n,values", [(384, 384, (0.70719, 0.35957)), (256, 512, (1.0, 1.0)),
+                                        (320, 320, (0.9, 0.5, 0.5000001, 0.1))])
+def test_svd_clustered_spectrum_full_jacobi(m, n, values):
+    """Exactly (or nearly) equal singular values in large clusters, chi = min(m, n) so
+    the call takes the plain Jacobi: inside a cluster the sweeps end on the stagnation
+    rule (off-norm within 10x of the tolerance and no longer falling), which must
+    leave S, the isometries and the reconstruction at the parity tolerance."""
+    k = min(m, n)
+    rng = np.random.default_rng(m + n)
+    q1, _ = np.linalg.qr(rng.standard_normal((m, k)) + 1j * rng.standard_normal((m, k)))
+    q2, _ = np.linalg.qr(rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k)))
+    sv = np.sort(np.repeat(np.asarray(values), -(-k // len(values)))[:k])[::-1]
+    a = (q1 * sv) @ q2.conj().T
+    u, s, vh = gpu_svd(a)
+    assert np.max(np.abs(s - sv)) < TOL * sv[0]
+    assert rel_l2((u * s) @ vh, a) < TOL
+    assert np.max(np.abs(u.conj().T @ u - np.eye(k))) < TOL
+    assert np.max(np.abs(vh @ vh.conj().T - np.eye(k))) < TOL
