@@ -16,7 +16,9 @@
 //   * the batched Jacobi SVD writes U S and Vh straight into the new site tensors
 //     (per-matrix output pointers);
 //   * the only host synchronisation is the download of the kept singular values
-//     and norms, once per group.
+//     and norms, once per group;
+//   * the largest group (the saturated thetas) runs on the rank's stream, the other
+//     shapes concurrently on a side stream from a second host thread.
 #include <algorithm>
 #include <map>
 #include <tuple>
