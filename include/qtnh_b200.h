@@ -267,6 +267,11 @@ int qtnh_scale(qtnh_tensor_t t, double re, double im, qtnh_tensor_t* out);
  * pairs; the result of step s gets id n_tensors + s. */
 int qtnh_plan_order(int n_tensors, const int* label_offsets, const int* labels, int n_labels,
                     const double* label_log2, uint64_t seed, int trials, int* order_out);
+/* The same search under a memory budget: orders whose largest intermediate has at
+ * most 2^log2_cap elements compete on flops (then size) and beat every order that
+ * does not fit; log2_cap <= 0 is qtnh_plan_order. */
+int qtnh_plan_order_capped(int n_tensors, const int* label_offsets, const int* labels, int n_labels,
+                           const double* label_log2, uint64_t seed, int trials, double log2_cap, int* order_out);
 
 /* ---- contraction ----------------------------------------------------------- */
 /* Contract a[a_pos[i]] with b[b_pos[i]] for i < n_pairs. Result indices: open

@@ -93,6 +93,7 @@ _SIGS = {
     "qtnh_conj": (i32, [vp, C.POINTER(vp)]),
     "qtnh_scale": (i32, [vp, f64, f64, C.POINTER(vp)]),
     "qtnh_plan_order": (i32, [i32, P_i32, P_i32, i32, vp, C.c_uint64, i32, P_i32]),
+    "qtnh_plan_order_capped": (i32, [i32, P_i32, P_i32, i32, vp, C.c_uint64, i32, C.c_double, P_i32]),
     "qtnh_contract_chain": (i32, [i32, C.POINTER(vp), i32, P_i32, P_i32, P_i32, P_i32, C.POINTER(vp)]),
     "qtnh_contract": (i32, [vp, vp, i32, P_i32, P_i32, C.POINTER(vp)]),
     "qtnh_gate_apply": (i32, [vp, i32, P_i32, vp, i32]),

@@ -704,6 +704,11 @@ int qtnh_tensor_load(qtnh_rank_t r, const char* path, qtnh_tensor_t* out) {
 
 int qtnh_plan_order(int n_tensors, const int* label_offsets, const int* labels, int n_labels,
                     const double* label_log2, uint64_t seed, int trials, int* order_out) {
+  return qtnh_plan_order_capped(n_tensors, label_offsets, labels, n_labels, label_log2, seed, trials, 0.0, order_out);
+}
+
+int qtnh_plan_order_capped(int n_tensors, const int* label_offsets, const int* labels, int n_labels,
+                           const double* label_log2, uint64_t seed, int trials, double log2_cap, int* order_out) {
   return guard([&] {
     if (n_tensors < 1) throw_invalid("empty network");
     need(label_offsets, "label_offsets");
@@ -715,7 +720,7 @@ int qtnh_plan_order(int n_tensors, const int* label_offsets, const int* labels, 
         lab[t].push_back(labels[j]);
       }
     std::vector<double> lg(label_log2, label_log2 + n_labels);
-    auto order = plan_order(lab, lg, seed, trials);
+    auto order = plan_order(lab, lg, seed, trials, log2_cap);
     for (size_t i = 0; i < order.size(); ++i) {
       order_out[2 * i] = order[i].first;
       order_out[2 * i + 1] = order[i].second;

@@ -54,7 +54,7 @@ void op_to_global(const TensorImpl& t, double* host);                      // te
 // Contraction order of a labelled network (plan.cpp); ids of results continue
 // after the n input tensors in step order.
 std::vector<std::pair<int, int>> plan_order(const std::vector<std::vector<int>>& labels, const std::vector<double>& lg,
-                                            uint64_t seed, int trials);
+                                            uint64_t seed, int trials, double log2_cap = 0.0);
 void op_save(const TensorImpl& t, const std::string& path);                // tensor.hpp:388-397
 TP op_load(RankCtx& r, const std::string& path);                           // tensor.hpp:399-446 (dense)
 

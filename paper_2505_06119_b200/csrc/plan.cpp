@@ -141,7 +141,7 @@ Trial greedy(const std::vector<std::vector<int>>& labels0, const std::vector<dou
 }  // namespace
 
 std::vector<std::pair<int, int>> plan_order(const std::vector<std::vector<int>>& labels, const std::vector<double>& lg,
-                                            uint64_t seed, int trials) {
+                                            uint64_t seed, int trials, double log2_cap) {
   const int n = static_cast<int>(labels.size());
   const int nt = std::max(1, trials);
   // Trials are independent: run them on the host cores (trial t on worker
@@ -167,9 +167,20 @@ std::vector<std::pair<int, int>> plan_order(const std::vector<std::vector<int>>&
     run(0, W);
     for (auto& x : th) x.join();
   }
+  // Winner: without a memory budget (log2_cap <= 0) the smallest (peak, flops, t).
+  // With one, the orders whose largest intermediate fits 2^log2_cap elements compete
+  // on flops first (then peak, then t) and beat every order that does not fit: the
+  // 5x6 depth-14 network has orders of peak 2^30 from 1.1e13 down to 3.9e12 flops
+  // (8MNK), and one of peak 2^29 at 9.0e13 that "smallest peak first" would pick.
+  auto key = [&](int t) {
+    const bool fits = log2_cap > 0 && res[t].peak <= log2_cap + 1e-9;
+    return log2_cap > 0 ? std::make_tuple(fits ? 0 : 1, fits ? res[t].flops : res[t].peak,
+                                          fits ? res[t].peak : res[t].flops)
+                        : std::make_tuple(0, res[t].peak, res[t].flops);
+  };
   int best = 0;
   for (int t = 1; t < nt; ++t)
-    if (std::make_pair(res[t].peak, res[t].flops) < std::make_pair(res[best].peak, res[best].flops)) best = t;
+    if (key(t) < key(best)) best = t;
   return res[best].order;
 }
 

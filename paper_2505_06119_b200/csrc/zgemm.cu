@@ -585,6 +585,10 @@ using G9 = Cfg<32, 64, 1, 2, 8, 3, 4, 32, 32, true>;
 // M). The 4M V4 kernel ran C3's big narrow contractions (M = 2^19, N = 32, K = 2^11,
 // at the ridge: 16 flop/B) at 2 TB/s.
 using G10 = Cfg<64, 32, 2, 1, 8, 3, 4, 32, 32, true>;
+// Narrower still (N = 16, e.g. config 3's M = 2^24, N = 16, K = 64 step, HBM-bound at
+// 6.5 flop/B): 64 x 16 tiles, 32 x 16 warp tiles -- the 64 x 32 V4 tiles (4M) spent
+// half their DMMAs on columns that do not exist.
+using G11 = Cfg<64, 16, 2, 1, 8, 3, 4, 32, 16, true>;
 
 int variant() {
   static int v = [] {
@@ -647,6 +651,9 @@ void zgemm_gather_a(const void* a, const int64_t* rowoff, const int64_t* coloff,
   } else if (n > 16 && even_shape<G10>(m, n, k) && narrow_gauss()) {
     if (rows_fastest) launch_even<G10, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
     else launch_even<G10, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
+  } else if (n == 16 && even_shape<G11>(m, n, k) && narrow_gauss()) {
+    if (rows_fastest) launch_even<G11, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
+    else launch_even<G11, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
   } else {
     if (rows_fastest) launch_mode<V4, 1>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);
     else launch_mode<V4, 2>(A, rowoff, coloff, B, Cp, m, n, k, st, cohi, co_sh, rohi, ro_sh);

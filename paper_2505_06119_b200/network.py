@@ -81,11 +81,13 @@ class Network:
 
     @staticmethod
     def plan(labels: Dict[int, List[str]], dims: Dict[str, int], seed: int = 0, trials: int = 64,
-             keep_open: Sequence[str] = ()) -> List[Tuple[int, int]]:
+             keep_open: Sequence[str] = (), max_log2_size: float = 0.0) -> List[Tuple[int, int]]:
         """Seeded greedy contraction order, planned natively (csrc/plan.cpp via
         qtnh_plan_order): trial 0 is the plain smallest-result greedy (SURVEY.md
         8(d)), further trials seeded randomised greedy passes; the order with the
-        smallest largest intermediate, then fewest flops, wins. Deterministic per
+        smallest largest intermediate, then fewest flops, wins -- or, with a memory
+        budget `max_log2_size`, the fewest flops among the orders whose largest
+        intermediate has at most 2^max_log2_size elements. Deterministic per
         seed; tensor ids must be 0..n-1 and the result of step s gets id n + s."""
         import math
 
@@ -102,9 +104,10 @@ class Network:
             offs.append(len(flat))
         lg = np.array([math.log2(dims[x]) for x in names], dtype=np.float64)
         out = np.zeros(2 * max(1, len(ids) - 1), dtype=np.int32)
-        qtnh.check(qtnh.lib.qtnh_plan_order(len(ids), i32_array(offs), i32_array(flat or [0]), len(names),
-                                            lg.ctypes.data, int(seed) & (2**64 - 1), int(trials),
-                                            out.ctypes.data_as(qtnh.C.POINTER(qtnh.C.c_int))))
+        qtnh.check(qtnh.lib.qtnh_plan_order_capped(len(ids), i32_array(offs), i32_array(flat or [0]), len(names),
+                                                   lg.ctypes.data, int(seed) & (2**64 - 1), int(trials),
+                                                   float(max_log2_size),
+                                                   out.ctypes.data_as(qtnh.C.POINTER(qtnh.C.c_int))))
         return [(int(out[2 * s]), int(out[2 * s + 1])) for s in range(len(ids) - 1)]
 
     # ---- multi-rank placement ---------------------------------------------------------

@@ -30,7 +30,7 @@ def test_c3_full_network_vs_host_replay():
     dims = {}
     for a, l in items:
         dims.update(zip(l, a.shape))
-    order = network.Network.plan(labels, dims, SEED, trials=64)
+    order = network.Network.plan(labels, dims, SEED, trials=2048, max_log2_size=30.0)  # the bench leg's order
 
     def body(rk):
         net, ol, _, _ = network.build_rcs_network(rk, 5, 6, 14, SEED, 6)

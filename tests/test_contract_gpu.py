@@ -227,3 +227,24 @@ def test_gauss_3m_ill_scaled_operands(scale):
     # per component: Re at rounding level, Im within eps * scale (the documented 3M bound)
     assert rel_l2(got.real, want.real) < 1e-14
     assert rel_l2(got.imag, want.imag) < 1e-14 * scale
+
+
+@pytest.mark.parametrize("da,db,ap,bp", [
+    ([2] * 18, [2] * 10, [0, 3, 5, 8, 11, 14], [9, 0, 2, 4, 6, 7]),     # N = 16, K = 64, A's innermost index open
+    ([2] * 18, [2] * 10, [1, 4, 6, 9, 12, 17], [0, 1, 2, 3, 4, 5]),     # N = 16, innermost index contracted
+    ([2] * 18, [2] * 10, [0, 2, 7, 13, 17], [3, 8, 1, 0, 6]),           # N = 32, K = 32
+    ([2] * 17, [2] * 7, [2, 5, 9, 16], [0, 1, 2, 3]),                   # N = 8: the general narrow kernel
+])
+def test_narrow_n_gather_contractions(da, db, ap, bp):
+    """Narrow result matrices (N = 8, 16, 32 columns: config 3's large steps under the
+    flop-minimising order) through the 64 x 16 / 64 x 32 tile-aligned Gauss kernels and
+    the general narrow kernel."""
+    a = circuits.rng_normals(41, int(np.prod(da)))
+    b = circuits.rng_normals(42, int(np.prod(db)))
+
+    def body(rk):
+        ta = Tensor.from_global(rk, IndexTuple(da, 0), None, a)
+        tb = Tensor.from_global(rk, IndexTuple(db, 0), None, b)
+        return contract(ta, tb, ap, bp).to_global_vector()
+
+    assert rel_l2(run_collect(World(1), body), P.contract(da, a, db, b, ap, bp)) < TOL

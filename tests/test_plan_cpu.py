@@ -55,3 +55,31 @@ def test_plan_small_networks_and_disconnected():
     dims2 = {"a": 2, "b": 3, "c": 4, "x": 5, "y": 6}
     final2, _ = replay(labels2, dims2, network.Network.plan(labels2, dims2, 1))
     assert sorted(final2) == ["a", "c", "y"]
+
+
+def order_flops(labels, dims, order):
+    L = {k: list(v) for k, v in labels.items()}
+    nxt, fl = len(L), 0.0
+    for s, (a, b) in enumerate(order):
+        la, lb = L.pop(a), L.pop(b)
+        sh = [x for x in la if x in lb]
+        new = [x for x in la if x not in sh] + [x for x in lb if x not in sh]
+        fl += 8.0 * 2.0 ** (sum(math.log2(dims[x]) for x in new) + sum(math.log2(dims[x]) for x in sh))
+        L[nxt + s] = new
+    return fl
+
+
+def test_plan_under_a_memory_budget_minimises_flops():
+    """qtnh_plan_order_capped: among the orders whose largest intermediate fits the
+    budget the fewest flops win (config 3: the budget is 2^30 elements); without a
+    budget the smallest peak wins whatever it costs."""
+    labels, dims, open_labels = labels_dims(5, 6, 14, 2025, 6)
+    free = network.Network.plan(labels, dims, 2025, trials=96)
+    capped = network.Network.plan(labels, dims, 2025, trials=96, max_log2_size=30.0)
+    assert capped == network.Network.plan(labels, dims, 2025, trials=96, max_log2_size=30.0)
+    final, peak = replay(labels, dims, capped)
+    assert sorted(final) == sorted(open_labels) and peak <= 30
+    assert order_flops(labels, dims, capped) <= order_flops(labels, dims, free)
+    # a budget nothing fits falls back to the smallest peak
+    tight = network.Network.plan(labels, dims, 2025, trials=96, max_log2_size=8.0)
+    assert replay(labels, dims, tight)[1] == replay(labels, dims, free)[1]

@@ -26,7 +26,8 @@ def main():
         for rep in range(2):
             net, *_ = network.build_rcs_network(rk, rows, cols, depth, seed, n_open)
             if order is None:
-                order = network.Network.plan(net.labels, net.dims, seed, trials=64)
+                order = network.Network.plan(net.labels, net.dims, seed, trials=int(os.environ.get("TRIALS", "2048")),
+                                             max_log2_size=float(os.environ.get("CAP", "30")))
             nxt = max(net.tensors) + 1
             recs = []
             for s, (a, b) in enumerate(order):

@@ -22,7 +22,9 @@ def main():
     ap.add_argument("--open", type=int, default=6)
     ap.add_argument("--seed", type=int, default=2025)
     ap.add_argument("--no-statevector", action="store_true")
-    ap.add_argument("--trials", type=int, default=64)
+    ap.add_argument("--trials", type=int, default=2048)
+    ap.add_argument("--cap", type=float, default=30.0,
+                    help="memory budget of the order search: log2 of the largest intermediate (elements); 0 = smallest peak first")
     ap.add_argument("--world", type=int, default=1,
                     help="ranks (thread per rank over the visible GPUs): tensors replicated, contractions of "
                          ">= --shard-flops M-sharded")
@@ -53,7 +55,7 @@ def main():
         if rk.rank() == 0:  # the order is host-only and identical on every rank: plan once
             out["n_tensors"] = len(net.tensors)
             t0 = time.perf_counter()
-            shared["order"] = network.Network.plan(net.labels, net.dims, args.seed, trials=args.trials)
+            shared["order"] = network.Network.plan(net.labels, net.dims, args.seed, trials=args.trials, max_log2_size=args.cap)
             out["plan_s"] = time.perf_counter() - t0
             planned.set()
         planned.wait()
