@@ -298,6 +298,10 @@ def measure_extras(rk, stream, torch):
     ex = {"hbm_peak_gbs": peak, "hbm_peak_source": src}
     n = 30
     st = Tensor.dense(rk, IndexTuple([2] * n, 0), None, None)
+    # seeded random amplitudes rather than the zero fill (the arithmetic-heavy QFT passes
+    # run ~10 % faster on an all-zero state; these gate kernels measured the same on both)
+    qtnh.check(qtnh.lib.qtnh_counter_complex_normals_device(C.c_void_p(stream.cuda_stream), SEED + 7, 0, 2**n,
+                                                            C.c_void_p(st.device_ptr())))
     bytes_per_gate = 32.0 * 2**n
     cases = [("dense_1q_H_q15", [15], circuits.H, False), ("dense_1q_H_q29", [29], circuits.H, False),
              ("dense_2q_fsim_q3_q20", [3, 20], circuits.FSIM, False),
