@@ -679,6 +679,7 @@ void zgemm(const void* a, const void* b, void* c, Dim m, Dim n, Dim k, cudaStrea
   }
   const Dim tiles = ((m + 31) / 32) * ((n + 63) / 64);
   if (n <= 32 && n > 16 && narrow_gauss() && even_shape<G10>(m, n, k)) launch<G10>(A, B, Cp, m, n, k, st);
+  else if (n == 16 && narrow_gauss() && even_shape<G11>(m, n, k)) launch<G11>(A, B, Cp, m, n, k, st);
   else if (n <= 32) launch<V4>(A, B, Cp, m, n, k, st);
   else if (tiles < 8192) launch<G22>(A, B, Cp, m, n, k, st);
   else launch<G6>(A, B, Cp, m, n, k, st);

@@ -123,6 +123,7 @@ def test_long_k_gather_contractions(da, db, ap, bp):
 
 
 @pytest.mark.parametrize("m,n,k", [(1, 1, 1), (64, 128, 8), (2**14, 128, 128), (1000, 100, 37), (3, 300, 500),
+                                   (4096, 16, 64), (4096, 32, 32), (4100, 16, 64),
                                    (2048, 2048, 64)])
 def test_zgemm_device_against_numpy(m, n, k):
     import torch
