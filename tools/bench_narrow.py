@@ -7,6 +7,8 @@ from paper_2505_06119_b200 import qtnh
 from paper_2505_06119_b200.qtnh import IndexTuple, Tensor, World, contract
 
 SHAPES = [(25, 5, 5), (24, 4, 6), (23, 7, 5), (24, 6, 6), (23, 5, 5)]
+if os.environ.get("NARROW_SHAPES"):  # e.g. NARROW_SHAPES=24x4x6 for one ncu capture
+    SHAPES = [tuple(int(x) for x in t.split("x")) for t in os.environ["NARROW_SHAPES"].split(",")]
 
 def body(rk):
     st = torch.cuda.Stream(); rk.set_stream(st.cuda_stream)
