@@ -818,6 +818,85 @@ inline Tensor contract(const Tensor& a, const Tensor& b, const std::vector<int>&
   check(qtnh_contract(a.h(), b.h(), static_cast<int>(a_pos.size()), a_pos.data(), b_pos.data(), &o));
   return wrap(o, &a.ctx());
 }
+
+/// Contraction order of a labelled network (SPEC network::contract_order, SPEC.md:
+/// 391-399): labels[t] names the indices of tensor t in order, a label shared by two
+/// tensors is a bond, label_dim[l] its dimension. Seeded randomised greedy search on
+/// the host cores, best of `trials`: by (largest intermediate, flops), or -- with
+/// max_log2_size > 0 -- the fewest flops among the orders whose largest intermediate
+/// has at most 2^max_log2_size elements. Step s joins (first, second); its result
+/// gets id labels.size() + s.
+inline std::vector<std::pair<int, int>> plan_order(const std::vector<std::vector<int>>& labels,
+                                                   const std::vector<Dim>& label_dim, std::uint64_t seed = 0,
+                                                   int trials = 64, double max_log2_size = 0.0) {
+  const int n = static_cast<int>(labels.size());
+  std::vector<int> offs{0}, flat;
+  for (const auto& l : labels) {
+    flat.insert(flat.end(), l.begin(), l.end());
+    offs.push_back(static_cast<int>(flat.size()));
+  }
+  std::vector<double> lg(label_dim.size());
+  for (size_t i = 0; i < lg.size(); ++i) lg[i] = std::log2(static_cast<double>(label_dim[i]));
+  std::vector<int> out(2 * static_cast<size_t>(n > 1 ? n - 1 : 1));
+  if (flat.empty()) flat.push_back(0);
+  check(qtnh_plan_order_capped(n, offs.data(), flat.data(), static_cast<int>(lg.size()), lg.data(), seed, trials,
+                               max_log2_size, out.data()));
+  std::vector<std::pair<int, int>> order;
+  for (int s = 0; s + 1 < n; ++s) order.emplace_back(out[2 * s], out[2 * s + 1]);
+  return order;
+}
+
+/// The whole order in one call (qtnh_contract_chain): every step contracts the labels
+/// its two operands share, the result carries open(a) then open(b), and
+/// intermediates are released as soon as they are consumed. Returns the last result
+/// and, through `result_labels`, its index labels.
+inline Tensor contract_order(const std::vector<Tensor>& tensors, const std::vector<std::vector<int>>& labels,
+                             const std::vector<std::pair<int, int>>& order,
+                             std::vector<int>* result_labels = nullptr) {
+  if (tensors.empty() || tensors.size() != labels.size()) throw InvalidArgument("one label list per tensor");
+  if (order.empty()) {
+    if (result_labels) *result_labels = labels[0];
+    return tensors[0];
+  }
+  std::vector<std::vector<int>> lab = labels;
+  std::vector<qtnh_tensor_t> in;
+  for (const Tensor& t : tensors) in.push_back(t.h());
+  std::vector<int> ab, np, ap, bp;
+  for (const auto& st : order) {
+    if (st.first < 0 || st.second < 0 || st.first >= static_cast<int>(lab.size()) ||
+        st.second >= static_cast<int>(lab.size()))
+      throw InvalidArgument("order refers to a tensor that does not exist yet");
+    const auto& la = lab[st.first];
+    const auto& lb = lab[st.second];
+    std::vector<int> nl;
+    int pairs = 0;
+    for (size_t i = 0; i < la.size(); ++i) {
+      auto it = std::find(lb.begin(), lb.end(), la[i]);
+      if (it == lb.end()) {
+        nl.push_back(la[i]);
+      } else {
+        ap.push_back(static_cast<int>(i));
+        bp.push_back(static_cast<int>(it - lb.begin()));
+        ++pairs;
+      }
+    }
+    for (int x : lb)
+      if (std::find(la.begin(), la.end(), x) == la.end()) nl.push_back(x);
+    ab.push_back(st.first);
+    ab.push_back(st.second);
+    np.push_back(pairs);
+    lab.push_back(nl);
+  }
+  if (ap.empty()) {
+    ap.push_back(0);
+    bp.push_back(0);
+  }
+  qtnh_tensor_t o;
+  check(qtnh_contract_chain(static_cast<int>(in.size()), in.data(), static_cast<int>(order.size()), ab.data(),
+                            np.data(), ap.data(), bp.data(), &o));
+  if (result_labels) *result_labels = lab.back();
+  return wrap(o, &tensors[0].ctx());
+}
 }  // namespace network
 
 namespace linalg {  // linalg.hpp

@@ -96,6 +96,35 @@ int main() {
     EXPECT(err < 1e-12);
     EXPECT(same);
   }
+  // network::plan_order + contract_order: D[d] = sum A[a,b] B[b,c] C[c,d,a]
+  {
+    qtnh::World w(1);
+    std::vector<Complex> got;
+    std::vector<int> res_labels;
+    std::vector<Complex> A(2 * 3), B(3 * 4), Cc(4 * 2 * 2);
+    for (int i = 0; i < 6; ++i) A[i] = {0.3 * i - 1.0, 0.2 * i};
+    for (int i = 0; i < 12; ++i) B[i] = {std::cos(0.9 * i), 0.1 * i - 0.4};
+    for (int i = 0; i < 16; ++i) Cc[i] = {0.05 * i * i - 0.7, std::sin(1.1 * i)};
+    const std::vector<std::vector<int>> labels{{0, 1}, {1, 2}, {2, 3, 0}};  // a b c d = 0 1 2 3
+    const std::vector<qtnh::Dim> dims{2, 3, 4, 2};
+    auto order = qtnh::network::plan_order(labels, dims, 7, 8);
+    auto capped = qtnh::network::plan_order(labels, dims, 7, 8, 4.0);
+    EXPECT(order.size() == 2 && capped.size() == 2);
+    w.run([&](qtnh::Rank& rk) {
+      std::vector<qtnh::Tensor> ts{qtnh::Tensor::from_global(rk, {{2, 3}, 0}, {}, A),
+                                   qtnh::Tensor::from_global(rk, {{3, 4}, 0}, {}, B),
+                                   qtnh::Tensor::from_global(rk, {{4, 2, 2}, 0}, {}, Cc)};
+      got = qtnh::network::contract_order(ts, labels, capped, &res_labels).to_global_vector();
+    });
+    EXPECT((res_labels == std::vector<int>{3}) && got.size() == 2);
+    for (int d = 0; d < 2; ++d) {
+      Complex want = 0;
+      for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 3; ++b)
+          for (int c = 0; c < 4; ++c) want += A[a * 3 + b] * B[b * 4 + c] * Cc[(c * 2 + d) * 2 + a];
+      EXPECT(std::abs(got[d] - want) < 1e-12 * (1.0 + std::abs(want)));
+    }
+  }
   std::printf("cpp api ok\n");
   return 0;
 }
