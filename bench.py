@@ -578,7 +578,10 @@ def run_gpu_arm(args):
             tb.free()
             torch.cuda.synchronize()
             if not args.skip_extras and world_size == 1:
-                result["extras"] = measure_extras(rk, stream, torch)
+                try:  # secondary figures: a failure here is reported, never fatal for the C1 line
+                    result["extras"] = measure_extras(rk, stream, torch)
+                except Exception as e:  # noqa: BLE001
+                    result["extras"] = {"error": f"{type(e).__name__}: {e}"}
             if not args.skip_configs and world_size > 1:
                 import bench_legs
 
