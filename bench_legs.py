@@ -439,13 +439,17 @@ def gpu_c2_sharded(rk, stream, torch, dist, world_size, rank, shared_gpu, swaps=
       * the whole QFT (distributed layers fused over peer memory, local layers
         cache-blocked, bit reversal) with norm and DFT spot-amplitude checks.
     n = 34 when every rank has its own GPU (BASELINE.json configs[2]); with
-    ranks sharing a GPU n = 30 + s (16 GiB per rank) and the bytes stay in HBM."""
+    ranks sharing a GPU n = 30 + s (16 GiB per rank; 29 + s beyond 4 ranks per GPU) and
+    the bytes stay in HBM."""
     from paper_2505_06119_b200 import qtnh
     from paper_2505_06119_b200.mps import _DevView
     from paper_2505_06119_b200.qtnh import DistParams, IndexTuple, Tensor
 
     s = (world_size - 1).bit_length()
-    n = 30 + s if shared_gpu else 34
+    # ranks sharing one GPU: 16 GiB shards up to 4 ranks per GPU, 8 GiB beyond (8 x 16 GiB
+    # plus what the C1 leg left in the pool does not fit 180 GB)
+    per_gpu = -(-world_size // max(1, torch.cuda.device_count()))
+    n = (30 + s if per_gpu <= 4 else 29 + s) if shared_gpu else 34
     nl = n - s
     N, NL = 2**n, 2**nl
     t = Tensor.dense(rk, IndexTuple([2] * n, s), DistParams(1, 1, 0), None)
