@@ -404,7 +404,10 @@ def run_gpu_arm(args):
     torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
     local = local % max(1, torch.cuda.device_count())
     if world_size > 1:
-        dist.init_process_group("gloo", init_method="env://")
+        import datetime
+
+        # barriers of a run whose peer died fail in minutes, not gloo's default half hour
+        dist.init_process_group("gloo", init_method="env://", timeout=datetime.timedelta(seconds=600))
     s = (world_size - 1).bit_length() if world_size > 1 else 0
     if world_size > 1 and 2**s != world_size:
         raise SystemExit("--gpus must be a power of two")
